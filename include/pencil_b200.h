@@ -1,0 +1,178 @@
+/* pencil_b200.h — C ABI of the B200-native execution backend for PENCIL kernels.
+ *
+ * Reference boundary (arxiv/paper_1302_5586 reference under /root/reference, read-only):
+ * the reference's CPU-parallel code generator emit_openmp (proj/core/src/pretty.cpp:472-531)
+ * prints every PENCIL array parameter `T a[restrict const static e]` (Printer::param,
+ * pretty.cpp:221-233); C decays it to `T *a`, scalars stay int/float, returns stay
+ * void/int/float.  Section 1 exports exactly those signatures for the kernel fixtures in
+ * paper_1302_5586_b200/pencil/*.pencil.c, so a program that linked the emitted-OpenMP object
+ * links this library instead.  Nothing here throws across the ABI.
+ */
+#ifndef PENCIL_B200_H
+#define PENCIL_B200_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ===== 1. Drop-in entry points (replace the emitted-OpenMP functions) ==================
+ * Pointers may be host memory (pageable or pinned; copied in/out around the call, the call
+ * returns when results are back in host memory) or CUDA device memory on the current
+ * device (used in place, no copies; the call still returns when the work is complete).
+ * `restrict` (PENCIL rule R1, compliance.cpp:152-164) guarantees the arrays do not alias.
+ * On failure the outputs are unspecified and pencil_cuda_last_status() != 0. */
+
+/* gemv.pencil.c    <- replaces emitted `void gemv(int, int, float, float, float *, float *, float *)` */
+void gemv(int m, int n, float alpha, float beta, float* A, float* x, float* y);
+/* gemv_t.pencil.c  (VOBLA transposed / strided view) */
+void gemv_t(int m, int n, int lda, int incx, int incy, float alpha, float beta, float* A,
+            float* x, float* y);
+/* dot.pencil.c */
+float dot(int n, float* x, float* y);
+/* axpy.pencil.c */
+void axpy(int n, float a, float* x, float* y);
+/* spmv.pencil.c: spmv_vec (row reduction licensed), spmv_inline (row sum in source order),
+ * spmv (row loop over the ACCESS-summarised spmv_row) — identical signatures */
+void spmv_vec(int nrows, int ncols, int nnz, int* rowptr, int* col, float* val, float* x, float* y);
+void spmv_inline(int nrows, int ncols, int nnz, int* rowptr, int* col, float* val, float* x, float* y);
+void spmv(int nrows, int ncols, int nnz, int* rowptr, int* col, float* val, float* x, float* y);
+void spmv_row(int nrows, int ncols, int nnz, int i, int* rowptr, int* col, float* val, float* x, float* y);
+/* conv5x5.pencil.c (u8 image semantics held in int, clamp-to-edge; fp32 interior-only) */
+void conv5x5_u8(int h, int w, int scale, int* img, int* k, int* out);
+void conv5x5_f32(int h, int w, float* img, float* k, float* out);
+/* gemm.pencil.c (fp32 via 3xTF32 on tcgen05 tensor cores) */
+void gemm(int m, int n, int k, float alpha, float beta, float* A, float* B, float* C);
+
+/* ===== 2. Status channel (mirrors PencilError codes, diag.hpp:44-55) ===================== */
+enum pencil_status {
+    PENCIL_OK = 0,
+    PENCIL_E_INTERP = 1,      /* runtime fault: out-of-bounds load, division by zero, bad call */
+    PENCIL_E_ARG = 2,         /* invalid argument (negative extent, null pointer, wrong dtype) */
+    PENCIL_E_CUDA = 3,        /* CUDA runtime error */
+    PENCIL_E_NOMEM = 4,       /* device allocation failed */
+    PENCIL_E_UNSUPPORTED = 5  /* no schedule for this nest / shape */
+};
+int pencil_cuda_last_status(void);
+const char* pencil_cuda_last_error(void); /* "E-INTERP: load from x[...] is out of bounds" style */
+void pencil_cuda_clear_status(void);
+const char* pencil_status_code(int status); /* "E-INTERP", "E-ARG", ... */
+
+/* ===== 3. Device-resident, stream-ordered API (no host synchronization) ==================
+ * `stream` is a cudaStream_t (NULL = the library's own stream for the current device).
+ * Device faults (E-INTERP analogues) accumulate in a per-device status word read and
+ * cleared by pencil_sync_status(). Return value: pencil_status of the launch itself. */
+typedef void* pencil_stream_t;
+int pencil_gemv_dev(pencil_stream_t s, int m, int n, float alpha, float beta, const float* A,
+                    const float* x, float* y);
+int pencil_gemv_t_dev(pencil_stream_t s, int m, int n, int lda, int incx, int incy, float alpha,
+                      float beta, const float* A, const float* x, float* y);
+int pencil_dot_dev(pencil_stream_t s, long long n, const float* x, const float* y, float* result_dev);
+int pencil_axpy_dev(pencil_stream_t s, long long n, float a, const float* x, float* y);
+/* axpy with the scalar read from device memory (e.g. the result of pencil_dot_dev) */
+int pencil_axpy_dev_ptr(pencil_stream_t s, long long n, const float* a_dev, const float* x, float* y);
+int pencil_conv5x5_u8_dev(pencil_stream_t s, int h, int w, int scale, const int* img,
+                          const int* k_host, int* out);
+/* packed 8-bit image variant (1 byte per pixel, same arithmetic as conv5x5_u8) */
+int pencil_conv5x5_u8_bytes_dev(pencil_stream_t s, int h, int w, int scale, const uint8_t* img,
+                                const int* k_host, uint8_t* out);
+int pencil_conv5x5_f32_dev(pencil_stream_t s, int h, int w, const float* img, const float* k_host,
+                           float* out);
+int pencil_gemm_dev(pencil_stream_t s, int m, int n, int k, float alpha, float beta, const float* A,
+                    const float* B, float* C);
+
+/* CSR inspector/executor: the plan is built once per sparsity structure (one pass over rowptr)
+ * and reused by every SpMV on that structure.  mode: 0 = row sums in source order (spmv_inline,
+ * spmv), 1 = reassociation licensed (spmv_vec). */
+typedef struct pencil_csr_plan* pencil_csr_plan_t;
+int pencil_csr_plan_create(pencil_stream_t s, int nrows, int ncols, int nnz, const int* rowptr_dev,
+                           int mode, pencil_csr_plan_t* out);
+int pencil_csr_plan_destroy(pencil_csr_plan_t plan);
+int pencil_csr_plan_info(pencil_csr_plan_t plan, int* ntiles, int* tile_nnz);
+int pencil_spmv_dev(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr, const int* col,
+                    const float* val, const float* x, float* y);
+
+/* synchronize `s`, return and clear the device fault word (PENCIL_OK or PENCIL_E_INTERP) */
+int pencil_sync_status(pencil_stream_t s);
+
+/* ===== 4. Name-dispatch launch layer — mirror of pencil::Interpreter (interp.hpp:27-72) ===== */
+enum pencil_dtype { PENCIL_INT32 = 0, PENCIL_FLOAT32 = 1, PENCIL_FLOAT64 = 2, PENCIL_UINT8 = 3 };
+enum pencil_arg_kind { PENCIL_ARG_INT = 0, PENCIL_ARG_FLOAT = 1, PENCIL_ARG_ARRAY = 2 };
+typedef struct {
+    int kind;            /* pencil_arg_kind */
+    long long i;         /* PENCIL_ARG_INT */
+    double f;            /* PENCIL_ARG_FLOAT */
+    const char* array;   /* PENCIL_ARG_ARRAY: store name (Interpreter::Arg::array) */
+} pencil_arg;
+typedef struct {
+    int kind;            /* PENCIL_ARG_INT / PENCIL_ARG_FLOAT; -1 for void */
+    long long i;
+    double f;
+} pencil_value;
+typedef struct pencil_runtime* pencil_runtime_t;
+pencil_runtime_t pencil_runtime_create(int device);
+void pencil_runtime_destroy(pencil_runtime_t rt);
+/* Interpreter::set_array: copy host data into a named device array (replaces any previous) */
+int pencil_runtime_set_array(pencil_runtime_t rt, const char* name, int dtype, const void* host,
+                             long long n);
+/* bind existing device memory under a name (no copy; caller keeps ownership) */
+int pencil_runtime_bind_array(pencil_runtime_t rt, const char* name, int dtype, void* dev,
+                              long long n);
+/* Interpreter::arrays()[name]: copy back to host (n elements) */
+int pencil_runtime_get_array(pencil_runtime_t rt, const char* name, void* host, long long n);
+int pencil_runtime_array_info(pencil_runtime_t rt, const char* name, int* dtype, long long* n,
+                              void** dev);
+/* Interpreter::call: name -> kernel through the mapper's schedule; synchronous */
+int pencil_runtime_call(pencil_runtime_t rt, const char* fn, int nargs, const pencil_arg* args,
+                        pencil_value* ret);
+/* the fp-reduction-reorders-results flag of the last call (pencilc.cpp:157-161 analogue) */
+int pencil_runtime_fp_reordered(pencil_runtime_t rt);
+
+/* ===== 5. Mapper: loop verdicts -> grid/block/tile schedule ==============================
+ * Verdicts are the reference analyzer's (depanalysis.hpp:14 Verdict, same numbering). */
+enum pencil_verdict {
+    PENCIL_PARALLEL = 0,
+    PENCIL_PARALLEL_WITH_REDUCTION = 1,
+    PENCIL_SERIAL = 2,
+    PENCIL_UNKNOWN = 3,
+    PENCIL_ASSUMED_PARALLEL = 4
+};
+typedef struct {
+    int loop_id;
+    int depth;           /* nesting depth within its function (0 = outermost) */
+    int verdict;         /* pencil_verdict */
+    char reduction_op;   /* '+', '*', 'M' (max), 'm' (min) or 0 */
+} pencil_loop_verdict;
+enum pencil_dim_role { PENCIL_DIM_GRID = 0, PENCIL_DIM_TILE = 1, PENCIL_DIM_REDUCE = 2, PENCIL_DIM_SEQ = 3 };
+typedef struct {
+    int nloops;
+    int role[8];         /* pencil_dim_role per depth */
+    int grid_dims;       /* loops mapped to the launch grid */
+    int reassociates;    /* a reduction is split across threads (fp rounding may change) */
+    char kernel[48];     /* chosen kernel variant */
+} pencil_schedule;
+/* map the verdicts of one PENCIL function's loop nest (depth-ordered) */
+int pencil_map_nest(const char* fn, const pencil_loop_verdict* loops, int nloops, pencil_schedule* out);
+/* the verdict table compiled into the library for a fixture function (from the reference
+ * analyzer); returns the number of loops written (<= cap), or -1 if unknown */
+int pencil_fixture_verdicts(const char* fn, pencil_loop_verdict* out, int cap);
+
+/* ===== 6. Multi-GPU partitioning (host-only; used by one-process-per-GPU drivers) ========= */
+/* row blocks of a CSR matrix balanced by non-zeros: bounds[0..nshards], bounds[0]=0, bounds[nshards]=nrows */
+int pencil_shard_rows_by_nnz(const int* rowptr, int nrows, int nshards, int* bounds);
+/* equal row bands of h rows (stencils); halo rows needed above/below each band */
+int pencil_shard_bands(int h, int nshards, int* bounds);
+/* 2-D tile grid for gemm across nshards GPUs: grid_rows * grid_cols == nshards, tiles as square as possible */
+int pencil_shard_gemm_grid(int m, int n, int nshards, int* grid_rows, int* grid_cols);
+
+/* ===== 7. Introspection / measurement =================================================== */
+const char* pencil_version(void);
+int pencil_l2_flush(pencil_stream_t s); /* write a buffer larger than L2 (timing hygiene) */
+int pencil_micro_gather(pencil_stream_t s, int mode, long long n, const int* idx,
+                        const float* table, float* out);
+int pencil_micro_copy(pencil_stream_t s, long long n, const float* src, float* dst);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

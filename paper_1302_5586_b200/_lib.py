@@ -1,0 +1,132 @@
+"""ctypes binding of lib/libpencil_b200.so (C ABI: include/pencil_b200.h).
+
+The product path is the CUDA library; there is no CPU fallback.  If the shared object is
+missing, loading fails loudly with instructions to build it.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libpencil_b200.so")
+SYNTH_PATH = os.path.join(_HERE, "lib", "libpencil_synth.so")
+
+c_int, c_ll, c_float, c_double, c_void_p, c_char_p = (
+    ctypes.c_int, ctypes.c_longlong, ctypes.c_float, ctypes.c_double, ctypes.c_void_p, ctypes.c_char_p)
+P = c_void_p  # every array crosses the ABI as a plain pointer
+
+# name -> (restype, argtypes); the drop-in section mirrors the emitted-C signatures exactly
+SIGNATURES = {
+    # §1 drop-in
+    "gemv": (None, [c_int, c_int, c_float, c_float, P, P, P]),
+    "gemv_t": (None, [c_int, c_int, c_int, c_int, c_int, c_float, c_float, P, P, P]),
+    "dot": (c_float, [c_int, P, P]),
+    "axpy": (None, [c_int, c_float, P, P]),
+    "spmv_vec": (None, [c_int, c_int, c_int, P, P, P, P, P]),
+    "spmv_inline": (None, [c_int, c_int, c_int, P, P, P, P, P]),
+    "spmv": (None, [c_int, c_int, c_int, P, P, P, P, P]),
+    "spmv_row": (None, [c_int, c_int, c_int, c_int, P, P, P, P, P]),
+    "conv5x5_u8": (None, [c_int, c_int, c_int, P, P, P]),
+    "conv5x5_f32": (None, [c_int, c_int, P, P, P]),
+    "gemm": (None, [c_int, c_int, c_int, c_float, c_float, P, P, P]),
+    # §2 status
+    "pencil_cuda_last_status": (c_int, []),
+    "pencil_cuda_last_error": (c_char_p, []),
+    "pencil_cuda_clear_status": (None, []),
+    "pencil_status_code": (c_char_p, [c_int]),
+    # §3 device API
+    "pencil_gemv_dev": (c_int, [P, c_int, c_int, c_float, c_float, P, P, P]),
+    "pencil_gemv_t_dev": (c_int, [P, c_int, c_int, c_int, c_int, c_int, c_float, c_float, P, P, P]),
+    "pencil_dot_dev": (c_int, [P, c_ll, P, P, P]),
+    "pencil_axpy_dev": (c_int, [P, c_ll, c_float, P, P]),
+    "pencil_axpy_dev_ptr": (c_int, [P, c_ll, P, P, P]),
+    "pencil_conv5x5_u8_dev": (c_int, [P, c_int, c_int, c_int, P, P, P]),
+    "pencil_conv5x5_u8_bytes_dev": (c_int, [P, c_int, c_int, c_int, P, P, P]),
+    "pencil_conv5x5_f32_dev": (c_int, [P, c_int, c_int, P, P, P]),
+    "pencil_gemm_dev": (c_int, [P, c_int, c_int, c_int, c_float, c_float, P, P, P]),
+    "pencil_csr_plan_create": (c_int, [P, c_int, c_int, c_int, P, c_int, ctypes.POINTER(c_void_p)]),
+    "pencil_csr_plan_destroy": (c_int, [P]),
+    "pencil_csr_plan_info": (c_int, [P, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+    "pencil_spmv_dev": (c_int, [P, P, P, P, P, P, P]),
+    "pencil_sync_status": (c_int, [P]),
+    # §4 name dispatch
+    "pencil_runtime_create": (c_void_p, [c_int]),
+    "pencil_runtime_destroy": (None, [P]),
+    "pencil_runtime_set_array": (c_int, [P, c_char_p, c_int, P, c_ll]),
+    "pencil_runtime_bind_array": (c_int, [P, c_char_p, c_int, P, c_ll]),
+    "pencil_runtime_get_array": (c_int, [P, c_char_p, P, c_ll]),
+    "pencil_runtime_array_info": (c_int, [P, c_char_p, ctypes.POINTER(c_int), ctypes.POINTER(c_ll),
+                                          ctypes.POINTER(c_void_p)]),
+    "pencil_runtime_call": (c_int, [P, c_char_p, c_int, P, P]),
+    "pencil_runtime_fp_reordered": (c_int, [P]),
+    # §5 mapper
+    "pencil_map_nest": (c_int, [c_char_p, P, c_int, P]),
+    "pencil_fixture_verdicts": (c_int, [c_char_p, P, c_int]),
+    # §6 partitioners
+    "pencil_shard_rows_by_nnz": (c_int, [P, c_int, c_int, P]),
+    "pencil_shard_bands": (c_int, [c_int, c_int, P]),
+    "pencil_shard_gemm_grid": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+    # §7
+    "pencil_version": (c_char_p, []),
+    "pencil_l2_flush": (c_int, [P]),
+    "pencil_micro_gather": (c_int, [P, c_int, c_ll, P, P, P]),
+    "pencil_micro_copy": (c_int, [P, c_ll, P, P]),
+    # introspection used by the boundary tests (not in the public header)
+    "pencil_fixture_signature": (c_int, [c_char_p, c_char_p, c_int]),
+    "pencil_fixture_count": (c_int, []),
+    "pencil_fixture_name": (c_char_p, [c_int]),
+}
+
+
+class pencil_arg(ctypes.Structure):
+    _fields_ = [("kind", c_int), ("i", c_ll), ("f", c_double), ("array", c_char_p)]
+
+
+class pencil_value(ctypes.Structure):
+    _fields_ = [("kind", c_int), ("i", c_ll), ("f", c_double)]
+
+
+class pencil_loop_verdict(ctypes.Structure):
+    _fields_ = [("loop_id", c_int), ("depth", c_int), ("verdict", c_int), ("reduction_op", ctypes.c_char)]
+
+
+class pencil_schedule(ctypes.Structure):
+    _fields_ = [("nloops", c_int), ("role", c_int * 8), ("grid_dims", c_int), ("reassociates", c_int),
+                ("kernel", ctypes.c_char * 48)]
+
+
+_lib = None
+_synth = None
+
+
+def load():
+    """Load the CUDA backend library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `make -C {_HERE}` (or __graft_entry__.build()); "
+                "there is no CPU fallback")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def load_synth():
+    global _synth
+    if _synth is None:
+        if not os.path.exists(SYNTH_PATH):
+            raise RuntimeError(f"{SYNTH_PATH} is missing: run `make -C {_HERE}`")
+        s = ctypes.CDLL(SYNTH_PATH)
+        s.pencil_synth_f32.argtypes = [P, c_ll, ctypes.c_ulonglong, c_ll]
+        s.pencil_synth_u8_i32.argtypes = [P, c_ll, ctypes.c_ulonglong, c_ll]
+        s.pencil_synth_u8.argtypes = [P, c_ll, ctypes.c_ulonglong, c_ll]
+        s.pencil_synth_csr_rowptr.argtypes = [c_int, c_double, c_double, c_int, ctypes.c_ulonglong, P,
+                                              ctypes.POINTER(c_double)]
+        s.pencil_synth_csr_rowptr.restype = c_ll
+        s.pencil_synth_csr_fill.argtypes = [c_int, c_int, ctypes.c_ulonglong, P, P, P]
+        _synth = s
+    return _synth

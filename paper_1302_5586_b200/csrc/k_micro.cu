@@ -1,0 +1,84 @@
+// Measurement probes (not PENCIL kernels): random-gather rate from a table (the x[col[k]]
+// access of SpMV), a float4 copy (HBM roofline check of our own code) and an L2 flush.
+#include "common.cuh"
+#include "kernels.h"
+
+template <int MODE>
+__device__ __forceinline__ float gather_ld(const float* p) {
+    float r;
+    if (MODE == 0) r = *p;
+    else if (MODE == 1) asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    else if (MODE == 2) asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    else r = ld_keep_f(p);
+    return r;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) micro_gather_kernel(long long n, const int* __restrict__ idx,
+                                                           const float* __restrict__ table,
+                                                           float* __restrict__ out) {
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthr = (long long)gridDim.x * blockDim.x;
+    const long long n4 = n >> 2;
+    const int4* idx4 = reinterpret_cast<const int4*>(idx);
+    float acc = 0.f;
+    long long i = tid;
+    for (; i + nthr < n4; i += 2 * nthr) {
+        int4 a = ld_stream_i4(idx4 + i), b = ld_stream_i4(idx4 + i + nthr);
+        acc += gather_ld<MODE>(table + a.x) + gather_ld<MODE>(table + a.y) + gather_ld<MODE>(table + a.z) +
+               gather_ld<MODE>(table + a.w) + gather_ld<MODE>(table + b.x) + gather_ld<MODE>(table + b.y) +
+               gather_ld<MODE>(table + b.z) + gather_ld<MODE>(table + b.w);
+    }
+    for (; i < n4; i += nthr) {
+        int4 a = ld_stream_i4(idx4 + i);
+        acc += gather_ld<MODE>(table + a.x) + gather_ld<MODE>(table + a.y) + gather_ld<MODE>(table + a.z) +
+               gather_ld<MODE>(table + a.w);
+    }
+    out[tid] = acc;
+}
+
+int launch_micro_gather(cudaStream_t st, int mode, long long n, const int* idx, const float* table,
+                        float* out) {
+    int grid = PENCIL_NUM_SMS * 8;
+    switch (mode) {
+        case 0: micro_gather_kernel<0><<<grid, 256, 0, st>>>(n, idx, table, out); break;
+        case 1: micro_gather_kernel<1><<<grid, 256, 0, st>>>(n, idx, table, out); break;
+        case 2: micro_gather_kernel<2><<<grid, 256, 0, st>>>(n, idx, table, out); break;
+        default: micro_gather_kernel<3><<<grid, 256, 0, st>>>(n, idx, table, out); break;
+    }
+    return (int)cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) micro_copy_kernel(long long n4, const float4* __restrict__ s,
+                                                         float4* __restrict__ d) {
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthr = (long long)gridDim.x * blockDim.x;
+    long long i = tid;
+    for (; i + 3 * nthr < n4; i += 4 * nthr) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = ld_stream_f4(s + i + u * nthr);
+#pragma unroll
+        for (int u = 0; u < 4; u++) st_stream_f4(d + i + u * nthr, v[u]);
+    }
+    for (; i < n4; i += nthr) st_stream_f4(d + i, ld_stream_f4(s + i));
+}
+
+int launch_micro_copy(cudaStream_t st, long long n, const float* src, float* dst) {
+    micro_copy_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>(n >> 2, reinterpret_cast<const float4*>(src),
+                                                         reinterpret_cast<float4*>(dst));
+    return (int)cudaGetLastError();
+}
+
+__global__ void micro_fill_kernel(long long n4, float4* __restrict__ d, float v) {
+    const long long nthr = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += nthr)
+        d[i] = make_float4(v, v, v, v);
+}
+
+int launch_micro_l2_flush(cudaStream_t st, long long n, float* buf) {
+    static float v = 0.f;
+    v += 1.f;
+    micro_fill_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>(n >> 2, reinterpret_cast<float4*>(buf), v);
+    return (int)cudaGetLastError();
+}

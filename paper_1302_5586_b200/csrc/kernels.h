@@ -1,0 +1,50 @@
+// Internal launcher interface between the C++ host runtime (runtime.cpp) and the CUDA
+// translation units.  All launchers are stream-ordered and never synchronize; they return
+// a cudaError_t value (0 = launched).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+// k_blas.cu
+int launch_gemv(cudaStream_t st, int m, int n, float alpha, float beta, const float* A,
+                const float* x, float* y);
+int launch_gemv_t(cudaStream_t st, int m, int n, int lda, int incx, int incy, float alpha,
+                  float beta, const float* A, const float* x, float* y, float* partial,
+                  unsigned* counters);
+size_t gemv_t_partial_elems(int m, int n);
+size_t gemv_t_counter_elems(int n);
+int launch_dot(cudaStream_t st, long long n, const float* x, const float* y, float* result,
+               double* partial, unsigned* counter);
+size_t dot_partial_elems();
+int launch_axpy(cudaStream_t st, long long n, float a, const float* a_dev, const float* x,
+                float* y);
+
+// k_spmv.cu
+int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
+                    int ntiles, int* tile_row, unsigned* plan_flags, unsigned* status);
+int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
+                    const int* rowptr, const int* col, const float* val, const float* x, float* y,
+                    const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* status);
+int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const int* rowptr,
+                       const int* col, const float* val, const float* x, float* y,
+                       unsigned* status);
+int csr_tile_nnz();
+
+// k_conv.cu  (taps are host arrays, passed to the kernels by value)
+int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const float* k25,
+                       float* out);
+int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, const int* k25,
+                      int* out);
+int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsigned char* img,
+                            const int* k25, unsigned char* out);
+
+// k_gemm.cu
+int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, const float* A,
+                const float* B, float* C, void* workspace, size_t workspace_bytes);
+size_t gemm_workspace_bytes(int m, int n, int k);
+
+// k_micro.cu (measurement probes, not PENCIL kernels)
+int launch_micro_gather(cudaStream_t st, int mode, long long n, const int* idx, const float* table,
+                        float* out);
+int launch_micro_copy(cudaStream_t st, long long n, const float* src, float* dst);
+int launch_micro_l2_flush(cudaStream_t st, long long n, float* buf);

@@ -1,0 +1,611 @@
+// Host runtime of the B200 PENCIL backend: status channel, per-device context (streams,
+// fault word, scratch, caching pool), the drop-in C ABI of include/pencil_b200.h §1, the
+// stream-ordered device API (§3), the CSR inspector, the Interpreter-mirror name dispatch
+// (§4), the verdict->schedule mapper (§5) and the multi-GPU partitioners (§6).
+//
+// Reference correspondences:
+//   drop-in signatures       <- emit_openmp / Printer::param  (pretty.cpp:221-233, 472-531)
+//   pencil_runtime_call      <- Interpreter::call / exec_call (interp.cpp:95-122)
+//   named device arrays      <- Interpreter::set_array/arrays (interp.hpp:40-43), array_storage (interp.cpp:124-138)
+//   fault word / status      <- PencilError("E-INTERP") (diag.hpp:44-55; interp.cpp:186-195, 273-279)
+//   pencil_map_nest          <- the verdict switch of emit_openmp (pretty.cpp:479-501)
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pencil_b200.h"
+#include "kernels.h"
+
+namespace {
+
+// ------------------------------------------------------------------ status channel
+thread_local int g_status = PENCIL_OK;
+thread_local char g_msg[512] = "";
+
+const char* code_name(int s) {
+    switch (s) {
+        case PENCIL_OK: return "OK";
+        case PENCIL_E_INTERP: return "E-INTERP";
+        case PENCIL_E_ARG: return "E-ARG";
+        case PENCIL_E_CUDA: return "E-CUDA";
+        case PENCIL_E_NOMEM: return "E-NOMEM";
+        case PENCIL_E_UNSUPPORTED: return "E-UNSUPPORTED";
+    }
+    return "E-?";
+}
+
+int fail(int status, const char* fmt, ...) {
+    g_status = status;
+    int off = snprintf(g_msg, sizeof g_msg, "%s: ", code_name(status));
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_msg + off, sizeof g_msg - off, fmt, ap);
+    va_end(ap);
+    return status;
+}
+int ok() {
+    g_status = PENCIL_OK;
+    g_msg[0] = 0;
+    return PENCIL_OK;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) return fail(PENCIL_E_NOMEM, "%s: %s", what, cudaGetErrorString(e));
+    return fail(PENCIL_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+#define CK(call)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);       \
+    } while (0)
+
+// ------------------------------------------------------------------ device context
+struct DeviceCtx {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    cudaMemPool_t pool = nullptr;
+    unsigned* status = nullptr;        // fault word (device)
+    unsigned* status_host = nullptr;   // pinned mirror
+    float* dot_result = nullptr;
+    double* dot_partial = nullptr;
+    unsigned* dot_counter = nullptr;
+    unsigned* gemv_t_counters = nullptr;
+    size_t gemv_t_counter_cap = 0;
+    float* l2_flush = nullptr;
+    long long l2_flush_elems = 0;
+    std::mutex mu;                     // serializes drop-in calls on this device
+};
+
+std::mutex g_ctx_mu;
+std::map<int, DeviceCtx*> g_ctx;
+
+int get_ctx(DeviceCtx** out) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    auto it = g_ctx.find(dev);
+    if (it != g_ctx.end()) {
+        *out = it->second;
+        return ok();
+    }
+    DeviceCtx* c = new DeviceCtx();
+    c->device = dev;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    CK(cudaMemPoolCreate(&c->pool, &props));
+    unsigned long long thresh = ~0ull;  // keep freed blocks cached: the pool is the allocator cache
+    CK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    CK(cudaMalloc(&c->status, 64));
+    CK(cudaMemset(c->status, 0, 64));
+    CK(cudaMallocHost(&c->status_host, 64));
+    CK(cudaMalloc(&c->dot_result, 64));
+    CK(cudaMalloc(&c->dot_partial, sizeof(double) * dot_partial_elems()));
+    CK(cudaMalloc(&c->dot_counter, 64));
+    CK(cudaMemset(c->dot_counter, 0, 64));
+    g_ctx[dev] = c;
+    *out = c;
+    return ok();
+}
+
+cudaStream_t pick_stream(DeviceCtx* c, pencil_stream_t s) {
+    return s ? (cudaStream_t)s : c->stream;
+}
+
+int pool_alloc(DeviceCtx* c, cudaStream_t st, size_t bytes, void** p) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocFromPoolAsync(p, bytes, c->pool, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocFromPoolAsync");
+    return PENCIL_OK;
+}
+void pool_free(cudaStream_t st, void* p) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+int ensure_gemv_t_counters(DeviceCtx* c, size_t n) {
+    if (c->gemv_t_counter_cap >= n) return PENCIL_OK;
+    if (c->gemv_t_counters) cudaFree(c->gemv_t_counters);
+    c->gemv_t_counters = nullptr;
+    size_t cap = n < 1024 ? 1024 : n;
+    CK(cudaMalloc(&c->gemv_t_counters, cap * sizeof(unsigned)));
+    CK(cudaMemset(c->gemv_t_counters, 0, cap * sizeof(unsigned)));
+    c->gemv_t_counter_cap = cap;
+    return PENCIL_OK;
+}
+
+// read and clear the fault word (stream must be synchronized by the caller or here)
+int collect_faults(DeviceCtx* c, cudaStream_t st) {
+    CK(cudaMemcpyAsync(c->status_host, c->status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(c->status, 0, sizeof(unsigned), st));
+    CK(cudaStreamSynchronize(st));
+    unsigned f = *c->status_host;
+    if (f & 1u) return fail(PENCIL_E_INTERP, "load index out of bounds (device fault word 0x%x)", f);
+    if (f & 2u) return fail(PENCIL_E_INTERP, "CSR rowptr entry outside [0, nnz] (device fault word 0x%x)", f);
+    if (f & 4u) return fail(PENCIL_E_INTERP, "division by zero");
+    return PENCIL_OK;
+}
+
+// ------------------------------------------------------------------ host/device staging
+enum Dir { IN = 1, OUT = 2, INOUT = 3 };
+
+struct Stage {
+    void* user = nullptr;      // caller pointer
+    void* dev = nullptr;       // device pointer used by the kernel
+    size_t bytes = 0;
+    int dir = IN;
+    bool owned = false;        // dev allocated from the pool (user is host memory)
+    // strided copy-back (conv5x5_f32 interior): 0 = whole buffer
+    size_t pitch = 0, width = 0, height = 0, offset = 0;
+};
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int stage_in(DeviceCtx* c, cudaStream_t st, Stage& s) {
+    if (s.bytes == 0 || is_device_ptr(s.user)) {
+        s.dev = s.user;
+        s.owned = false;
+        return PENCIL_OK;
+    }
+    if (!s.user) return fail(PENCIL_E_ARG, "null array pointer");
+    int r = pool_alloc(c, st, s.bytes, &s.dev);
+    if (r) return r;
+    s.owned = true;
+    if (s.dir & IN) CK(cudaMemcpyAsync(s.dev, s.user, s.bytes, cudaMemcpyHostToDevice, st));
+    return PENCIL_OK;
+}
+
+int stage_out(cudaStream_t st, Stage& s) {
+    if (!s.owned || !(s.dir & OUT)) return PENCIL_OK;
+    if (s.height) {
+        CK(cudaMemcpy2DAsync((char*)s.user + s.offset, s.pitch, (char*)s.dev + s.offset, s.pitch,
+                             s.width, s.height, cudaMemcpyDeviceToHost, st));
+    } else {
+        CK(cudaMemcpyAsync(s.user, s.dev, s.bytes, cudaMemcpyDeviceToHost, st));
+    }
+    return PENCIL_OK;
+}
+
+// Runs `launch(dev pointers...)` around host<->device staging; synchronous, status-setting.
+template <int N, typename F>
+int dropin(Stage (&st)[N], F launch) {
+    DeviceCtx* c = nullptr;
+    int r = get_ctx(&c);
+    if (r) return r;
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t s = c->stream;
+    for (int i = 0; i < N && !r; i++) r = stage_in(c, s, st[i]);
+    if (!r) {
+        cudaError_t e = (cudaError_t)launch(c, s);
+        if (e != cudaSuccess) r = cuda_fail(e, "kernel launch");
+    }
+    for (int i = 0; i < N && !r; i++) r = stage_out(s, st[i]);
+    for (int i = 0; i < N; i++)
+        if (st[i].owned) pool_free(s, st[i].dev);
+    if (r) {
+        cudaStreamSynchronize(s);
+        return r;
+    }
+    return collect_faults(c, s) == PENCIL_OK ? ok() : g_status;
+}
+
+size_t nz(long long v) { return v > 0 ? (size_t)v : 0; }
+
+// ------------------------------------------------------------------ CSR plans
+struct CsrPlanImpl {
+    int device, nrows, ncols, nnz, mode, ntiles, tile_nnz;
+    int* tile_row = nullptr;
+    unsigned* flags = nullptr;
+};
+
+int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int* rowptr, int mode,
+                   CsrPlanImpl* p) {
+    p->device = c->device;
+    p->nrows = nrows;
+    p->nnz = nnz;
+    p->mode = mode;
+    p->tile_nnz = csr_tile_nnz();
+    long long nt = ((long long)nnz + p->tile_nnz - 1) / p->tile_nnz;
+    p->ntiles = (int)(nt < 1 ? 1 : nt);
+    int r = pool_alloc(c, st, sizeof(int) * ((size_t)p->ntiles + 1), (void**)&p->tile_row);
+    if (r) return r;
+    r = pool_alloc(c, st, 64, (void**)&p->flags);
+    if (r) return r;
+    CK(cudaMemsetAsync(p->tile_row, 0, sizeof(int) * ((size_t)p->ntiles + 1), st));
+    return (int)launch_csr_plan(st, nrows, nnz, rowptr, p->tile_nnz, p->ntiles, p->tile_row, p->flags,
+                                c->status) == 0
+               ? PENCIL_OK
+               : fail(PENCIL_E_CUDA, "csr plan launch");
+}
+
+int spmv_common(int mode, int nrows, int ncols, int nnz, int* rowptr, int* col, float* val,
+                float* x, float* y) {
+    if (nrows < 0 || ncols < 0 || nnz < 0) return fail(PENCIL_E_ARG, "negative extent");
+    Stage st[5];
+    st[0] = {rowptr, nullptr, sizeof(int) * (nz(nrows) + 1), IN};
+    st[1] = {col, nullptr, sizeof(int) * nz(nnz), IN};
+    st[2] = {val, nullptr, sizeof(float) * nz(nnz), IN};
+    st[3] = {x, nullptr, sizeof(float) * nz(ncols), IN};
+    st[4] = {y, nullptr, sizeof(float) * nz(nrows), OUT};
+    if (nrows == 0) return ok();
+    return dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
+        CsrPlanImpl p;
+        if (csr_plan_build(c, s, nrows, nnz, (const int*)st[0].dev, mode, &p)) return (int)cudaErrorUnknown;
+        int e = launch_csr_spmv(s, mode, nrows, ncols, nnz, (const int*)st[0].dev, (const int*)st[1].dev,
+                                (const float*)st[2].dev, (const float*)st[3].dev, (float*)st[4].dev,
+                                p.tile_row, p.ntiles, p.flags, c->status);
+        pool_free(s, p.tile_row);
+        pool_free(s, p.flags);
+        return e;
+    });
+}
+
+}  // namespace
+
+// =====================================================================================
+// §1 drop-in entry points
+// =====================================================================================
+extern "C" {
+
+void gemv(int m, int n, float alpha, float beta, float* A, float* x, float* y) {
+    if (m < 0 || n < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
+    if (m == 0) { ok(); return; }
+    Stage st[3];
+    st[0] = {A, nullptr, sizeof(float) * nz((long long)m * n), IN};
+    st[1] = {x, nullptr, sizeof(float) * nz(n), IN};
+    st[2] = {y, nullptr, sizeof(float) * nz(m), INOUT};
+    dropin(st, [&](DeviceCtx*, cudaStream_t s) {
+        return launch_gemv(s, m, n, alpha, beta, (const float*)st[0].dev, (const float*)st[1].dev,
+                           (float*)st[2].dev);
+    });
+}
+
+void gemv_t(int m, int n, int lda, int incx, int incy, float alpha, float beta, float* A, float* x,
+            float* y) {
+    if (m < 0 || n < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
+    if (n == 0) { ok(); return; }
+    if (lda < 0 || incx < 1 || incy < 1) { fail(PENCIL_E_ARG, "gemv_t needs lda >= 0, incx >= 1, incy >= 1"); return; }
+    if (m > 0 && n > lda) {  // A[i*lda + j] with j >= lda leaves A's declared extent m*lda
+        fail(PENCIL_E_INTERP, "load from A[%lld] is out of bounds", (long long)(m - 1) * lda + (n - 1));
+        return;
+    }
+    Stage st[3];
+    st[0] = {A, nullptr, sizeof(float) * nz((long long)m * lda), IN};
+    st[1] = {x, nullptr, sizeof(float) * nz((long long)m * incx), IN};
+    st[2] = {y, nullptr, sizeof(float) * nz((long long)n * incy), INOUT};
+    dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
+        if (ensure_gemv_t_counters(c, gemv_t_counter_elems(n))) return (int)cudaErrorMemoryAllocation;
+        float* part = nullptr;
+        size_t pe = gemv_t_partial_elems(m, n);
+        if (pe && pool_alloc(c, s, pe * sizeof(float), (void**)&part)) return (int)cudaErrorMemoryAllocation;
+        int e = launch_gemv_t(s, m, n, lda, incx, incy, alpha, beta, (const float*)st[0].dev,
+                              (const float*)st[1].dev, (float*)st[2].dev, part, c->gemv_t_counters);
+        pool_free(s, part);
+        return e;
+    });
+}
+
+float dot(int n, float* x, float* y) {
+    if (n < 0) { fail(PENCIL_E_ARG, "negative extent"); return 0.f; }
+    if (n == 0) { ok(); return 0.f; }
+    Stage st[2];
+    st[0] = {x, nullptr, sizeof(float) * nz(n), IN};
+    st[1] = {y, nullptr, sizeof(float) * nz(n), IN};
+    float result = 0.f;
+    dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
+        int e = launch_dot(s, n, (const float*)st[0].dev, (const float*)st[1].dev, c->dot_result,
+                           c->dot_partial, c->dot_counter);
+        if (e) return e;
+        return (int)cudaMemcpyAsync(&result, c->dot_result, sizeof(float), cudaMemcpyDeviceToHost, s);
+    });
+    return result;
+}
+
+void axpy(int n, float a, float* x, float* y) {
+    if (n < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
+    if (n == 0) { ok(); return; }
+    Stage st[2];
+    st[0] = {x, nullptr, sizeof(float) * nz(n), IN};
+    st[1] = {y, nullptr, sizeof(float) * nz(n), INOUT};
+    dropin(st, [&](DeviceCtx*, cudaStream_t s) {
+        return launch_axpy(s, n, a, nullptr, (const float*)st[0].dev, (float*)st[1].dev);
+    });
+}
+
+void spmv_vec(int nrows, int ncols, int nnz, int* rowptr, int* col, float* val, float* x, float* y) {
+    spmv_common(1, nrows, ncols, nnz, rowptr, col, val, x, y);
+}
+void spmv_inline(int nrows, int ncols, int nnz, int* rowptr, int* col, float* val, float* x, float* y) {
+    spmv_common(0, nrows, ncols, nnz, rowptr, col, val, x, y);
+}
+void spmv(int nrows, int ncols, int nnz, int* rowptr, int* col, float* val, float* x, float* y) {
+    spmv_common(0, nrows, ncols, nnz, rowptr, col, val, x, y);
+}
+void spmv_row(int nrows, int ncols, int nnz, int i, int* rowptr, int* col, float* val, float* x,
+              float* y) {
+    if (nrows < 0 || ncols < 0 || nnz < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
+    if (i < 0 || i >= nrows) { fail(PENCIL_E_INTERP, "load from rowptr[%d] is out of bounds", i); return; }
+    Stage st[5];
+    st[0] = {rowptr, nullptr, sizeof(int) * (nz(nrows) + 1), IN};
+    st[1] = {col, nullptr, sizeof(int) * nz(nnz), IN};
+    st[2] = {val, nullptr, sizeof(float) * nz(nnz), IN};
+    st[3] = {x, nullptr, sizeof(float) * nz(ncols), IN};
+    st[4] = {y, nullptr, sizeof(float) * nz(nrows), INOUT};
+    dropin(st, [&](DeviceCtx* c, cudaStream_t s) {
+        return launch_csr_generic(s, 1, ncols, nnz, (const int*)st[0].dev + i, (const int*)st[1].dev,
+                                  (const float*)st[2].dev, (const float*)st[3].dev,
+                                  (float*)st[4].dev + i, c->status);
+    });
+}
+
+void conv5x5_u8(int h, int w, int scale, int* img, int* k, int* out) {
+    if (h < 0 || w < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
+    if (h == 0 || w == 0) { ok(); return; }
+    if (scale == 0) { fail(PENCIL_E_INTERP, "division by zero"); return; }
+    int taps[25];
+    if (is_device_ptr(k)) {
+        if (cudaMemcpy(taps, k, sizeof taps, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cuda_fail(cudaGetLastError(), "tap copy");
+            return;
+        }
+    } else {
+        memcpy(taps, k, sizeof taps);
+    }
+    Stage st[2];
+    st[0] = {img, nullptr, sizeof(int) * nz((long long)h * w), IN};
+    st[1] = {out, nullptr, sizeof(int) * nz((long long)h * w), OUT};
+    dropin(st, [&](DeviceCtx*, cudaStream_t s) {
+        return launch_conv5x5_u8(s, h, w, scale, (const int*)st[0].dev, taps, (int*)st[1].dev);
+    });
+}
+
+void conv5x5_f32(int h, int w, float* img, float* k, float* out) {
+    if (h < 0 || w < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
+    if (h < 5 || w < 5) { ok(); return; }  // no interior pixel: nothing is stored
+    float taps[25];
+    if (is_device_ptr(k)) {
+        if (cudaMemcpy(taps, k, sizeof taps, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cuda_fail(cudaGetLastError(), "tap copy");
+            return;
+        }
+    } else {
+        memcpy(taps, k, sizeof taps);
+    }
+    Stage st[2];
+    st[0] = {img, nullptr, sizeof(float) * nz((long long)h * w), IN};
+    // only the interior of out is stored to: copy back exactly that rectangle
+    st[1] = {out, nullptr, sizeof(float) * nz((long long)h * w), OUT};
+    st[1].pitch = sizeof(float) * (size_t)w;
+    st[1].width = sizeof(float) * (size_t)(w - 4);
+    st[1].height = (size_t)(h - 4);
+    st[1].offset = sizeof(float) * ((size_t)2 * w + 2);
+    dropin(st, [&](DeviceCtx*, cudaStream_t s) {
+        return launch_conv5x5_f32(s, h, w, (const float*)st[0].dev, taps, (float*)st[1].dev);
+    });
+}
+
+void gemm(int m, int n, int k, float alpha, float beta, float* A, float* B, float* C) {
+    if (m < 0 || n < 0 || k < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
+    if (m == 0 || n == 0) { ok(); return; }
+    Stage st[3];
+    st[0] = {A, nullptr, sizeof(float) * nz((long long)m * k), IN};
+    st[1] = {B, nullptr, sizeof(float) * nz((long long)k * n), IN};
+    st[2] = {C, nullptr, sizeof(float) * nz((long long)m * n), INOUT};
+    dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
+        size_t wb = gemm_workspace_bytes(m, n, k);
+        void* ws = nullptr;
+        if (wb && pool_alloc(c, s, wb, &ws)) return (int)cudaErrorMemoryAllocation;
+        int e = launch_gemm(s, m, n, k, alpha, beta, (const float*)st[0].dev, (const float*)st[1].dev,
+                            (float*)st[2].dev, ws, wb);
+        pool_free(s, ws);
+        return e;
+    });
+}
+
+// =====================================================================================
+// §2 status
+// =====================================================================================
+int pencil_cuda_last_status(void) { return g_status; }
+const char* pencil_cuda_last_error(void) { return g_msg; }
+void pencil_cuda_clear_status(void) { ok(); }
+const char* pencil_status_code(int status) { return code_name(status); }
+
+// =====================================================================================
+// §3 device-resident API
+// =====================================================================================
+#define DEV_PROLOGUE                      \
+    DeviceCtx* c = nullptr;               \
+    if (get_ctx(&c)) return g_status;     \
+    cudaStream_t st = pick_stream(c, s);
+#define DEV_RET(e) return (e) ? cuda_fail((cudaError_t)(e), "kernel launch") : ok()
+
+int pencil_gemv_dev(pencil_stream_t s, int m, int n, float alpha, float beta, const float* A,
+                    const float* x, float* y) {
+    if (m < 0 || n < 0) return fail(PENCIL_E_ARG, "negative extent");
+    DEV_PROLOGUE;
+    DEV_RET(launch_gemv(st, m, n, alpha, beta, A, x, y));
+}
+
+int pencil_gemv_t_dev(pencil_stream_t s, int m, int n, int lda, int incx, int incy, float alpha,
+                      float beta, const float* A, const float* x, float* y) {
+    if (m < 0 || n < 0 || lda < 0 || incx < 1 || incy < 1) return fail(PENCIL_E_ARG, "bad extent/stride");
+    DEV_PROLOGUE;
+    if (ensure_gemv_t_counters(c, gemv_t_counter_elems(n))) return g_status;
+    float* part = nullptr;
+    size_t pe = gemv_t_partial_elems(m, n);
+    if (pe && pool_alloc(c, st, pe * sizeof(float), (void**)&part)) return g_status;
+    int e = launch_gemv_t(st, m, n, lda, incx, incy, alpha, beta, A, x, y, part, c->gemv_t_counters);
+    pool_free(st, part);
+    DEV_RET(e);
+}
+
+int pencil_dot_dev(pencil_stream_t s, long long n, const float* x, const float* y, float* result_dev) {
+    if (n < 0) return fail(PENCIL_E_ARG, "negative extent");
+    DEV_PROLOGUE;
+    // per-call partial buffer: concurrent dots on different streams must not share it
+    double* part = nullptr;
+    unsigned* ctr = nullptr;
+    if (pool_alloc(c, st, sizeof(double) * dot_partial_elems() + 256, (void**)&part)) return g_status;
+    ctr = (unsigned*)((char*)part + sizeof(double) * dot_partial_elems());
+    cudaMemsetAsync(ctr, 0, sizeof(unsigned), st);
+    int e = launch_dot(st, n, x, y, result_dev, part, ctr);
+    pool_free(st, part);
+    DEV_RET(e);
+}
+
+int pencil_axpy_dev(pencil_stream_t s, long long n, float a, const float* x, float* y) {
+    if (n < 0) return fail(PENCIL_E_ARG, "negative extent");
+    DEV_PROLOGUE;
+    DEV_RET(launch_axpy(st, n, a, nullptr, x, y));
+}
+
+int pencil_axpy_dev_ptr(pencil_stream_t s, long long n, const float* a_dev, const float* x, float* y) {
+    if (n < 0 || !a_dev) return fail(PENCIL_E_ARG, "bad argument");
+    DEV_PROLOGUE;
+    DEV_RET(launch_axpy(st, n, 0.f, a_dev, x, y));
+}
+
+int pencil_conv5x5_u8_dev(pencil_stream_t s, int h, int w, int scale, const int* img,
+                          const int* k_host, int* out) {
+    if (h < 0 || w < 0) return fail(PENCIL_E_ARG, "negative extent");
+    if (scale == 0 && h > 0 && w > 0) return fail(PENCIL_E_INTERP, "division by zero");
+    DEV_PROLOGUE;
+    DEV_RET(launch_conv5x5_u8(st, h, w, scale, img, k_host, out));
+}
+
+int pencil_conv5x5_u8_bytes_dev(pencil_stream_t s, int h, int w, int scale, const uint8_t* img,
+                                const int* k_host, uint8_t* out) {
+    if (h < 0 || w < 0) return fail(PENCIL_E_ARG, "negative extent");
+    if (scale == 0 && h > 0 && w > 0) return fail(PENCIL_E_INTERP, "division by zero");
+    DEV_PROLOGUE;
+    DEV_RET(launch_conv5x5_u8_bytes(st, h, w, scale, img, k_host, out));
+}
+
+int pencil_conv5x5_f32_dev(pencil_stream_t s, int h, int w, const float* img, const float* k_host,
+                           float* out) {
+    if (h < 0 || w < 0) return fail(PENCIL_E_ARG, "negative extent");
+    DEV_PROLOGUE;
+    DEV_RET(launch_conv5x5_f32(st, h, w, img, k_host, out));
+}
+
+int pencil_gemm_dev(pencil_stream_t s, int m, int n, int k, float alpha, float beta, const float* A,
+                    const float* B, float* C) {
+    if (m < 0 || n < 0 || k < 0) return fail(PENCIL_E_ARG, "negative extent");
+    DEV_PROLOGUE;
+    size_t wb = gemm_workspace_bytes(m, n, k);
+    void* ws = nullptr;
+    if (wb && pool_alloc(c, st, wb, &ws)) return g_status;
+    int e = launch_gemm(st, m, n, k, alpha, beta, A, B, C, ws, wb);
+    pool_free(st, ws);
+    if (e == -1) return fail(PENCIL_E_UNSUPPORTED, "gemm shape m=%d n=%d k=%d has no tcgen05 schedule", m, n, k);
+    DEV_RET(e);
+}
+
+struct pencil_csr_plan : CsrPlanImpl {};
+
+int pencil_csr_plan_create(pencil_stream_t s, int nrows, int ncols, int nnz, const int* rowptr_dev,
+                           int mode, pencil_csr_plan_t* out) {
+    if (nrows < 0 || ncols < 0 || nnz < 0 || !out) return fail(PENCIL_E_ARG, "bad argument");
+    DEV_PROLOGUE;
+    pencil_csr_plan* p = new pencil_csr_plan();
+    p->ncols = ncols;
+    if (csr_plan_build(c, st, nrows, nnz, rowptr_dev, mode ? 1 : 0, p)) {
+        delete p;
+        return g_status;
+    }
+    *out = p;
+    return ok();
+}
+
+int pencil_csr_plan_destroy(pencil_csr_plan_t plan) {
+    if (!plan) return ok();
+    cudaFree(plan->tile_row);  // pool memory: freed through the device's default stream order
+    cudaFree(plan->flags);
+    delete plan;
+    return ok();
+}
+
+int pencil_csr_plan_info(pencil_csr_plan_t plan, int* ntiles, int* tile_nnz) {
+    if (!plan) return fail(PENCIL_E_ARG, "null plan");
+    if (ntiles) *ntiles = plan->ntiles;
+    if (tile_nnz) *tile_nnz = plan->tile_nnz;
+    return ok();
+}
+
+int pencil_spmv_dev(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr, const int* col,
+                    const float* val, const float* x, float* y) {
+    if (!plan) return fail(PENCIL_E_ARG, "null plan");
+    DEV_PROLOGUE;
+    DEV_RET(launch_csr_spmv(st, plan->mode, plan->nrows, plan->ncols, plan->nnz, rowptr, col, val, x, y,
+                            plan->tile_row, plan->ntiles, plan->flags, c->status));
+}
+
+int pencil_sync_status(pencil_stream_t s) {
+    DEV_PROLOGUE;
+    return collect_faults(c, st) == PENCIL_OK ? ok() : g_status;
+}
+
+const char* pencil_version(void) { return "pencil-b200 0.1 (sm_100a)"; }
+
+int pencil_l2_flush(pencil_stream_t s) {
+    DEV_PROLOGUE;
+    if (!c->l2_flush) {
+        c->l2_flush_elems = 64ll << 20;  // 256 MiB > 126 MB L2
+        CK(cudaMalloc(&c->l2_flush, sizeof(float) * c->l2_flush_elems));
+    }
+    DEV_RET(launch_micro_l2_flush(st, c->l2_flush_elems, c->l2_flush));
+}
+
+int pencil_micro_gather(pencil_stream_t s, int mode, long long n, const int* idx, const float* table,
+                        float* out) {
+    DEV_PROLOGUE;
+    DEV_RET(launch_micro_gather(st, mode, n, idx, table, out));
+}
+
+int pencil_micro_copy(pencil_stream_t s, long long n, const float* src, float* dst) {
+    DEV_PROLOGUE;
+    DEV_RET(launch_micro_copy(st, n, src, dst));
+}
+
+}  // extern "C"
+
+// status setter for the dispatch layer (dispatch.cpp), C++ linkage, not part of the ABI
+int pencil_internal_fail(int status, const char* msg) {
+    g_status = status;
+    snprintf(g_msg, sizeof g_msg, "%s", msg);
+    return status;
+}

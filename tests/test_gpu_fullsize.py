@@ -1,0 +1,134 @@
+"""Full-size parity on the BASELINE.json configs (run with -m gpu).  Inputs are the SURVEY §8d
+synthetic streams; the checker is the C restatement of the interpreter (oracle port, fp64/int64)
+and, for source-order kernels, the fp32 semantics of the reference-emitted C — both pinned to
+the reference on the golden vectors (tests/test_oracle.py)."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import normwise_err
+from paper_1302_5586_b200 import synth
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def dev(torch, a):
+    return torch.from_numpy(a).cuda()
+
+
+def test_gemv_8192(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    m = n = 8192
+    A, x, y = synth.f32(m * n, 42), synth.f32(n, 42, m * n), synth.f32(m, 42, m * n + n)
+    for alpha, beta in [(1.0, 0.0), (1.5, 0.5)]:
+        yd = dev(torch, y.copy())
+        pb.device.gemv(m, n, alpha, beta, dev(torch, A), dev(torch, x), yd)
+        ref = oracle.gemv(m, n, alpha, beta, A, x, y)
+        scale = abs(alpha) * (np.abs(A.reshape(m, n)).astype(np.float64) @ np.abs(x)) + abs(beta) * np.abs(y)
+        assert normwise_err(yd.cpu().numpy(), ref, scale) <= TOL
+
+
+def test_gemv_t_vobla_view_16384(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    m = n = lda = 16384
+    incx, incy = 2, 3
+    A = synth.f32(m * lda, 42)
+    x = synth.f32(m * incx, 42, m * lda)
+    y = synth.f32(n * incy, 42, m * lda + m * incx)
+    yd = dev(torch, y.copy())
+    pb.device.gemv_t(m, n, lda, incx, incy, 1.0, 0.5, dev(torch, A), dev(torch, x), yd)
+    ref = oracle.gemv_t(m, n, lda, incx, incy, 1.0, 0.5, A, x, y)
+    got = yd.cpu().numpy()
+    js = np.arange(n) * incy
+    At = np.abs(A.reshape(m, lda)).astype(np.float32)
+    scale = np.zeros(n * incy)
+    scale[js] = (np.abs(x[np.arange(m) * incx]) @ At).astype(np.float64) + 0.5 * np.abs(y[js])
+    assert normwise_err(got, ref, scale) <= TOL
+    untouched = np.setdiff1d(np.arange(n * incy), js)
+    assert np.array_equal(got[untouched], y[untouched])
+
+
+def test_dot_axpy_chain_2e28(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    n = 1 << 28
+    x, y = synth.f32(n, 42), synth.f32(n, 42, n)
+    xd, yd = dev(torch, x), dev(torch, y.copy())
+    r = torch.zeros(1, device="cuda")
+    pb.device.dot(n, xd, yd, r)
+    d = float(r.item())
+    ref = oracle.dot(n, x, y)
+    scale = float(np.sum(np.abs(x.astype(np.float64) * y)))
+    assert abs(d - ref) <= TOL * scale
+    pb.device.axpy_ptr(n, r, xd, yd)  # axpy(dot(x, y), x, y) without a host hop
+    exact = oracle.axpy_f32(n, np.float32(d), x, y)
+    assert np.array_equal(yd.cpu().numpy().view(np.uint32), exact.view(np.uint32))
+
+
+@pytest.fixture(scope="module")
+def big_csr():
+    return synth.csr_powerlaw(1 << 24)
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["source_order", "reassociated"])
+def test_spmv_powerlaw_16M_rows(cuda, big_csr, mode):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    rowptr, col, val, x, _ = big_csr
+    nrows, nnz = rowptr.size - 1, col.size
+    assert abs(nnz - 16 * nrows) <= 0.01 * 16 * nrows
+    rp, cd, vd, xd = dev(torch, rowptr), dev(torch, col), dev(torch, val), dev(torch, x)
+    y = torch.empty(nrows, device="cuda")
+    plan = pb.device.CsrPlan(nrows, nrows, nnz, rp, mode=mode)
+    plan.spmv(rp, cd, vd, xd, y)
+    pb.device.sync_status()
+    got = y.cpu().numpy()
+    if mode == 0:  # bit-exact vs the emitted C's fp32 source-order semantics
+        exact = oracle.spmv_f32(nrows, nrows, nnz, rowptr, col, val, x)
+        assert np.array_equal(got.view(np.uint32), exact.view(np.uint32))
+    ref = oracle.spmv(nrows, nrows, nnz, rowptr, col, val, x)
+    terms = np.abs(val.astype(np.float64)) * np.abs(x[col])
+    cs = np.concatenate([[0.0], np.cumsum(terms)])
+    assert normwise_err(got, ref, cs[rowptr[1:]] - cs[rowptr[:-1]]) <= TOL
+
+
+def test_conv5x5_u8_16384(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    h = w = 16384
+    img = synth.u8_i32(h * w, 42)
+    for k, scale in [(synth.BINOMIAL, 256), (synth.SHARPEN, 1)]:
+        out = torch.empty(h * w, dtype=torch.int32, device="cuda")
+        imgd = dev(torch, img)
+        pb.device.conv5x5_u8(h, w, scale, imgd, k, out)
+        got = out.cpu().numpy()
+        # rows 0..63 and the last 64 (clamped borders) + a band in the middle, vs the oracle
+        for r0, r1 in [(0, 64), (h // 2 - 32, h // 2 + 32), (h - 64, h)]:
+            lo, hi = max(0, r0 - 2), min(h, r1 + 2)
+            sub = img[lo * w:hi * w]
+            ref = oracle.conv5x5_u8(hi - lo, w, scale, sub, k).reshape(hi - lo, w)
+            # interior rows of the slab are exact (the slab's own clamping only affects the
+            # rows next to a cut that is not an image border)
+            a0 = r0 - lo if r0 > 0 else 0
+            a1 = (r1 - lo) if r1 < h else hi - lo
+            assert np.array_equal(got.reshape(h, w)[r0:r1], ref[a0:a1]), (k[12], r0)
+        # packed 8-bit variant (1 B/px) must agree with the int32-storage kernel everywhere
+        img8, out8 = dev(torch, img.astype(np.uint8)), torch.empty(h * w, dtype=torch.uint8, device="cuda")
+        pb.device.conv5x5_u8_bytes(h, w, scale, img8, k, out8)
+        assert torch.equal(out8.to(torch.int32), out)
+
+
+def test_conv5x5_f32_16384(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    h = w = 16384
+    img = synth.f32(h * w, 42)
+    k = (synth.BINOMIAL.astype(np.float32) / 256.0).astype(np.float32)
+    out0 = synth.f32(h * w, 42, h * w)
+    out = dev(torch, out0.copy())
+    pb.device.conv5x5_f32(h, w, dev(torch, img), k, out)
+    exact = oracle.conv5x5_f32_f32(h, w, img, k, out0)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), exact.view(np.uint32))
