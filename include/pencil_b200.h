@@ -59,7 +59,7 @@ void pencil_cuda_clear_status(void);
 const char* pencil_status_code(int status); /* "E-INTERP", "E-ARG", ... */
 
 /* ===== 3. Device-resident, stream-ordered API (no host synchronization) ==================
- * `stream` is a cudaStream_t (NULL = the library's own stream for the current device).
+ * `stream` is a cudaStream_t of the current device (0 = the legacy default stream).
  * Device faults (E-INTERP analogues) accumulate in a per-device status word read and
  * cleared by pencil_sync_status(). Return value: pencil_status of the launch itself. */
 typedef void* pencil_stream_t;

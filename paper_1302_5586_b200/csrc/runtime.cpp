@@ -115,9 +115,10 @@ int get_ctx(DeviceCtx** out) {
     return ok();
 }
 
-cudaStream_t pick_stream(DeviceCtx* c, pencil_stream_t s) {
-    return s ? (cudaStream_t)s : c->stream;
-}
+// the device API takes the caller's stream literally (0 = the legacy default stream, the CUDA
+// convention, so launches order with the caller's other work); only the drop-in path uses the
+// library's own stream
+cudaStream_t pick_stream(DeviceCtx*, pencil_stream_t s) { return (cudaStream_t)s; }
 
 int pool_alloc(DeviceCtx* c, cudaStream_t st, size_t bytes, void** p) {
     if (bytes == 0) bytes = 16;

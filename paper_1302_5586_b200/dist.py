@@ -75,7 +75,10 @@ class RowShardedCsr:
         import torch.distributed as dist
         if out is None:
             out = torch.empty(self.ncols_padded, dtype=torch.float32, device=x_local_padded.device)
-        dist.all_gather_into_tensor(out, x_local_padded)
+        if dist.get_backend() == "nccl":
+            dist.all_gather_into_tensor(out, x_local_padded)
+        else:  # gloo (CPU tests): list form
+            dist.all_gather(list(out.view(self.world, self.max_rows).unbind(0)), x_local_padded)
         return out
 
 
