@@ -37,14 +37,28 @@ __global__ void __launch_bounds__(256) micro_gather_kernel(long long n, const in
     out[tid] = acc;
 }
 
+// mode bits 0-3: load flavour; 4-7: CTAs per SM (0 -> 8); bit 8: 150 KB dynamic smem per CTA
+// (one CTA per SM); bit 9: launch on half the SMs (74 CTAs) — separates per-SM (L1TEX) from
+// chip-wide (L2) gather limits.
 int launch_micro_gather(cudaStream_t st, int mode, long long n, const int* idx, const float* table,
                         float* out) {
-    int grid = PENCIL_NUM_SMS * 8;
-    switch (mode) {
-        case 0: micro_gather_kernel<0><<<grid, 256, 0, st>>>(n, idx, table, out); break;
-        case 1: micro_gather_kernel<1><<<grid, 256, 0, st>>>(n, idx, table, out); break;
-        case 2: micro_gather_kernel<2><<<grid, 256, 0, st>>>(n, idx, table, out); break;
-        default: micro_gather_kernel<3><<<grid, 256, 0, st>>>(n, idx, table, out); break;
+    int per_sm = (mode >> 4) & 15;
+    if (!per_sm) per_sm = 8;
+    int grid = ((mode >> 9) & 1) ? PENCIL_NUM_SMS / 2 : PENCIL_NUM_SMS * per_sm;
+    size_t smem = ((mode >> 8) & 1) ? 150 * 1024 : 0;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(micro_gather_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(micro_gather_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(micro_gather_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(micro_gather_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        attr = true;
+    }
+    switch (mode & 15) {
+        case 0: micro_gather_kernel<0><<<grid, 256, smem, st>>>(n, idx, table, out); break;
+        case 1: micro_gather_kernel<1><<<grid, 256, smem, st>>>(n, idx, table, out); break;
+        case 2: micro_gather_kernel<2><<<grid, 256, smem, st>>>(n, idx, table, out); break;
+        default: micro_gather_kernel<3><<<grid, 256, smem, st>>>(n, idx, table, out); break;
     }
     return (int)cudaGetLastError();
 }

@@ -5,10 +5,10 @@
 // Inspector (plan): the nnz stream is cut into windows of TILE_NNZ non-zeros; tile t owns
 // the rows whose first non-zero falls in window t (tile_row[t] = first row with
 // rowptr[row] - rowptr[0] >= t*TILE_NNZ).  Built once per matrix by one pass over rowptr
-// (csr_plan_kernel), it gives every CTA a contiguous row range holding ~TILE_NNZ
+// (csr_plan_kernel), it gives every warp a contiguous row range holding ~TILE_NNZ
 // non-zeros regardless of the power-law row-length distribution.
 //
-// Executor (csr_stream_kernel): per tile, per batch of 256 rows, the batch's non-zeros
+// Executor (csr_stream_kernel): per tile, per batch of 32 rows, the batch's non-zeros
 // are streamed with coalesced loads (col, val: evict-first) while x[col] is gathered
 // (evict-last, so the 64 MB vector stays L2-resident), staged in shared memory, then each
 // thread folds its own row in source order: s = s + val[k]*x[col[k]], product and sum each
@@ -24,7 +24,7 @@
 #include "kernels.h"
 
 #define SPMV_THREADS 256
-#define SPMV_CHUNK 2048
+#define SPMV_TILE_NNZ 512  // non-zeros per warp tile (plan window)
 
 __global__ void csr_plan_kernel(int nrows, int nnz_len, const int* __restrict__ rowptr,
                                 int tile_nnz, int ntiles, int* __restrict__ tile_row,
@@ -70,62 +70,108 @@ __device__ void spmv_generic(int nrows, int ncols, int nnz_len, const int* __res
     }
 }
 
+// Persistent warps, no CTA-wide barrier: the kernel is bound by the L1TEX rate of random
+// 4-byte gathers (~1 per SM clock, tools/microbench.py), so what matters is that every warp
+// keeps its gathers in flight independently of the others.  Each warp draws tiles from a
+// ticket counter (so a warp stuck on a 4096-long row never idles a whole CTA).  Per batch of
+// 32 rows (one row per lane) the warp streams the batch's non-zeros in chunks of WCHUNK:
+// coalesced col/val loads and x gathers, products staged in the warp's own smem slice, then
+// every lane folds its row's slice in source order.  With the reduction licensed (ASSOC),
+// slices longer than 16 are folded by the whole warp instead (strided partials + tree).
+#define WARPS_PER_CTA (SPMV_THREADS / 32)
+#define WCHUNK 128
+#define CTAS_PER_SM 8
+// Skewed staging index: lane i folds row i, whose slice starts near i*len; without the skew
+// rows of equal length 16 put 16 lanes on one bank (a 16-way conflict on every read).
+__device__ __forceinline__ int skew(int t) { return t + (t >> 5); }
+#define WCHUNK_SKEWED (WCHUNK + WCHUNK / 32)
+
 template <bool ASSOC>
-__global__ void __launch_bounds__(SPMV_THREADS) csr_stream_kernel(
+__global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_stream_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
-    const int* __restrict__ tile_row, int ntiles, const unsigned* __restrict__ plan_flags,
+    const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
     unsigned* __restrict__ status) {
-    __shared__ float s_prod[SPMV_CHUNK];
-    if (*plan_flags) {  // written by the plan kernel earlier on this stream
+    __shared__ float s_prod[WARPS_PER_CTA][WCHUNK_SKEWED];
+    if (plan[0]) {  // non-monotone rowptr, flagged by the plan kernel earlier on this stream
         spmv_generic(nrows, ncols, nnz_len, rowptr, col, val, x, y, status);
         return;
     }
-    const int tid = threadIdx.x;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int r0 = __ldg(tile_row + tile), r1 = __ldg(tile_row + tile + 1);
-        for (int rb = r0; rb < r1; rb += SPMV_THREADS) {
-            const int re = min(rb + SPMV_THREADS, r1);
-            const int row = rb + tid;
-            const bool active = row < re;
-            int my_s = 0, my_e = 0;
-            if (active) {
-                my_s = __ldg(rowptr + row);
-                my_e = __ldg(rowptr + row + 1);
-            }
-            const int q_begin = max(__ldg(rowptr + rb), 0);
-            const int q_end = min(__ldg(rowptr + re), nnz_len);
-            float s = 0.f;
-            for (int q = q_begin; q < q_end; q += SPMV_CHUNK) {
-                const int cnt = min(SPMV_CHUNK, q_end - q);
-                // stage: coalesced col/val stream + x gather; 8 independent loads per thread
-#pragma unroll 4
-                for (int t = tid; t < cnt; t += SPMV_THREADS) {
-                    const int p = q + t;
-                    const int c = ld_stream_i(col + p);
-                    float xv = 0.f;
-                    if ((unsigned)c < (unsigned)ncols) xv = ld_keep_f(x + c);
-                    else raise_fault(status, FAULT_OOB_LOAD);
-                    // the product rounds on its own, as in the emitted C compiled as written
-                    s_prod[t] = __fmul_rn(ld_stream_f(val + p), xv);
-                }
-                __syncthreads();
-                const int lo = max(my_s, q), hi = min(my_e, q + cnt);
-                if (!ASSOC) {
-                    for (int p = lo; p < hi; p++) s = __fadd_rn(s, s_prod[p - q]);
-                } else {
-                    for (int p = lo; p < hi; p++) s = __fadd_rn(s, s_prod[p - q]);
-                }
-                __syncthreads();
-            }
-            if (active) y[row] = s;
-        }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
+    float* sp = s_prod[warp];
+    for (;;) {
+    unsigned ticket = 0;
+    if (lane == 0) ticket = atomicAdd(&plan[1], 1u);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    if (ticket >= (unsigned)ntiles) {
+        // every warp draws exactly one failing ticket; the last one re-arms the counter
+        if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
+        return;
     }
+    const int tile = (int)ticket;
+    const int r0 = __ldg(tile_row + tile), r1 = __ldg(tile_row + tile + 1);
+    for (int rb = r0; rb < r1; rb += 32) {
+        const int re = min(rb + 32, r1);
+        const int row = rb + lane;
+        const bool active = row < re;
+        int my_s = 0, my_e = 0;
+        if (active) {
+            my_s = __ldg(rowptr + row);
+            my_e = __ldg(rowptr + row + 1);
+        }
+        const int q_begin = max(__shfl_sync(0xffffffffu, my_s, 0), 0);
+        const int q_end = min(__ldg(rowptr + re), nnz_len);
+        float s = 0.f;
+        for (int q = q_begin; q < q_end; q += WCHUNK) {
+            const int cnt = min(WCHUNK, q_end - q);
+            int c[WCHUNK / 32];
+            float v[WCHUNK / 32], xv[WCHUNK / 32];
+#pragma unroll
+            for (int u = 0; u < WCHUNK / 32; u++) {
+                const int t = u * 32 + lane;
+                c[u] = t < cnt ? ld_stream_i(col + q + t) : 0;
+                v[u] = t < cnt ? ld_stream_f(val + q + t) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < WCHUNK / 32; u++) {
+                xv[u] = 0.f;
+                if (u * 32 + lane < cnt) {
+                    if ((unsigned)c[u] < (unsigned)ncols) xv[u] = ld_keep_f(x + c[u]);
+                    else raise_fault(status, FAULT_OOB_LOAD);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < WCHUNK / 32; u++)  // the product rounds on its own (emitted C as written)
+                sp[skew(u * 32 + lane)] = __fmul_rn(v[u], xv[u]);
+            __syncwarp();
+            const int lo = max(my_s, q), hi = min(my_e, q + cnt);
+            if (ASSOC) {
+                unsigned big = __ballot_sync(0xffffffffu, hi - lo > 16);
+                if (hi - lo <= 16)
+                    for (int p = lo; p < hi; p++) s = __fadd_rn(s, sp[skew(p - q)]);
+                while (big) {
+                    const int o = __ffs(big) - 1;
+                    big &= big - 1;
+                    const int olo = __shfl_sync(0xffffffffu, lo, o), ohi = __shfl_sync(0xffffffffu, hi, o);
+                    float part = 0.f;
+                    for (int p = olo + lane; p < ohi; p += 32) part += sp[skew(p - q)];
+                    part = warp_sum<32>(part);
+                    if (lane == o) s += part;
+                }
+            } else {
+                for (int p = lo; p < hi; p++) s = __fadd_rn(s, sp[skew(p - q)]);
+            }
+            __syncwarp();
+        }
+        if (active) y[row] = s;
+    }
+    }  // tickets
 }
 
 int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
                     int ntiles, int* tile_row, unsigned* plan_flags, unsigned* status) {
-    cudaMemsetAsync(plan_flags, 0, sizeof(unsigned), st);
+    cudaMemsetAsync(plan_flags, 0, 64, st);  // [0] non-monotone flag, [1] tile ticket counter
     long long blocks = ((long long)nrows + 1 + 255) / 256;
     if (blocks > PENCIL_NUM_SMS * 16) blocks = PENCIL_NUM_SMS * 16;
     csr_plan_kernel<<<(int)blocks, 256, 0, st>>>(nrows, nnz_len, rowptr, tile_nnz, ntiles, tile_row,
@@ -135,16 +181,53 @@ int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, 
 
 int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                     const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                    const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* status) {
+                    const int* tile_row, int ntiles, unsigned* plan_flags, unsigned* status) {
     if (nrows <= 0) return 0;
-    int grid = ntiles;
+    int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;  // persistent: at most one wave
+    if (grid > PENCIL_NUM_SMS * CTAS_PER_SM) grid = PENCIL_NUM_SMS * CTAS_PER_SM;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(SPMV_THREADS);
+    cfg.stream = st;
+    // x is the only re-read operand (each entry ~nnz/ncols times): ask L2 to keep it resident
+    // against the 2 GB col/val stream (per-launch access-policy window; PENCIL_SPMV_PERSIST=0
+    // disables it).
+    cudaLaunchAttribute attr[1];
+    static int persist = -1;
+    static size_t persist_bytes = 0;
+    if (persist < 0) {
+        const char* e = getenv("PENCIL_SPMV_PERSIST");
+        persist = !(e && e[0] == '0');
+        int dev = 0, maxp = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        persist_bytes = (size_t)maxp;
+        if (persist && persist_bytes) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist_bytes);
+        cudaGetLastError();
+    }
+    size_t xbytes = (size_t)ncols * sizeof(float);
+    if (persist && persist_bytes && xbytes) {
+        int dev = 0, maxwin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        size_t win = xbytes < (size_t)maxwin ? xbytes : (size_t)maxwin;
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = (void*)x;
+        attr[0].val.accessPolicyWindow.num_bytes = win;
+        attr[0].val.accessPolicyWindow.hitRatio = win <= persist_bytes ? 1.0f : (float)persist_bytes / (float)win;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    cudaError_t e;
     if (assoc)
-        csr_stream_kernel<true><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val,
-                                                            x, y, tile_row, ntiles, plan_flags, status);
+        e = cudaLaunchKernelEx(&cfg, csr_stream_kernel<true>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                               tile_row, ntiles, plan_flags, status);
     else
-        csr_stream_kernel<false><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val,
-                                                             x, y, tile_row, ntiles, plan_flags, status);
-    return (int)cudaGetLastError();
+        e = cudaLaunchKernelEx(&cfg, csr_stream_kernel<false>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                               tile_row, ntiles, plan_flags, status);
+    return (int)e;
 }
 
 __global__ void csr_generic_kernel(int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr,
@@ -164,4 +247,4 @@ int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const
     return (int)cudaGetLastError();
 }
 
-int csr_tile_nnz() { return SPMV_CHUNK; }
+int csr_tile_nnz() { return SPMV_TILE_NNZ; }

@@ -24,7 +24,7 @@ int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, 
                     int ntiles, int* tile_row, unsigned* plan_flags, unsigned* status);
 int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                     const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                    const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* status);
+                    const int* tile_row, int ntiles, unsigned* plan_flags, unsigned* status);
 int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const int* rowptr,
                        const int* col, const float* val, const float* x, float* y,
                        unsigned* status);

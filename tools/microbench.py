@@ -39,6 +39,11 @@ def main():
     for mode, name in enumerate(["ld.global", "ld.global.nc", "ld.global.cg", "ld.nc.L2::evict_last"]):
         best, avg = time_ms(lambda: lib.pencil_micro_gather(st, mode, n, idx.data_ptr(), table.data_ptr(), res.data_ptr()))
         out[f"gather_{name}"] = {"ms": best, "Ggathers/s": n / best / 1e6, "idx_GB/s": 4 * n / best / 1e6}
+    # scaling: CTAs per SM (1,2,4) and one CTA per SM on all / half of the SMs
+    for label, mode in [("1cta_per_sm", 1 | (1 << 4)), ("2cta_per_sm", 1 | (2 << 4)), ("4cta_per_sm", 1 | (4 << 4)),
+                        ("1cta_bigsmem_148sm", 1 | (1 << 4) | (1 << 8)), ("1cta_bigsmem_74sm", 1 | (1 << 8) | (1 << 9))]:
+        best, _ = time_ms(lambda: lib.pencil_micro_gather(st, mode, n, idx.data_ptr(), table.data_ptr(), res.data_ptr()))
+        out[f"gather_scaling_{label}"] = {"ms": best, "Ggathers/s": n / best / 1e6}
     # sorted indices (perfect locality) for contrast
     idx_sorted, _ = torch.sort(idx)
     best, _ = time_ms(lambda: lib.pencil_micro_gather(st, 1, n, idx_sorted.data_ptr(), table.data_ptr(), res.data_ptr()))
