@@ -1,9 +1,329 @@
-// gemm.pencil.c — placeholder until the tcgen05 3xTF32 kernel lands (returns -1: no schedule).
+// gemm.pencil.c on the 5th-generation tensor cores: C = alpha * A B + beta * C in fp32 via
+// 3xTF32 (tcgen05.mma kind::tf32, accumulators in TMEM, operands staged by TMA).
+//
+// Schedule (mapper): i, j ASSUMED_PARALLEL -> 2-D grid of 128 x 256 output tiles; p
+// PARALLEL_WITH_REDUCTION(+) -> the K loop is split across tensor-core MMAs (reassociates).
+//
+// Precision: every fp32 operand is split once, by a prologue kernel, into tf32 hi = rna(x)
+// and lo = rna(x - hi); the kernel accumulates hi*hi + hi*lo + lo*hi in fp32 (TMEM) — the
+// dropped lo*lo term and the tf32 rounding of lo are ~2^-22 relative, well inside the 1e-5
+// normwise tolerance of the tests.  The prologue also writes B transposed (N x K, K-major)
+// and pads K to a multiple of 32 with zeros, so every operand tile is a K-major 128-byte
+// swizzled TMA box and ragged M/N edges are zero-filled by the TMA unit.
+//
+// Kernel anatomy (one output tile per CTA, 6 warps):
+//   warp 0  TMA producer: per K block of 32, four boxes (A_hi, A_lo 128x32; B_hi, B_lo 256x32)
+//           into a 2-stage smem ring (96 KB/stage), completion on the stage's `full` mbarrier
+//   warp 1  TMEM allocator + MMA issuer (one elected lane): 4 k-steps x 3 products
+//           tcgen05.mma.cta_group::1.kind::tf32 128x256x8 per stage, tcgen05.commit -> `empty`
+//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 (TMEM lane quarter = warp % 4) -> alpha, beta
+//           -> 128-bit global stores
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
-int launch_gemm(cudaStream_t, int, int, int, float, float, const float*, const float*, float*, void*,
-                size_t) {
-    return -1;
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 32;  // BK fp32 = 128 bytes = one swizzle-128B row
+constexpr int STAGES = 2;
+constexpr int A_TILE = BM * BK * 4;  // 16 KB
+constexpr int B_TILE = BN * BK * 4;  // 32 KB
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+constexpr int TMEM_COLS = 256;
+constexpr int GEMM_THREADS = 192;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int GROUP_M = 16;  // tile raster: groups of 16 M-tiles share B panels in L2
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
 }
-size_t gemm_workspace_bytes(int, int, int) { return 0; }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+// K-major, 128-byte-swizzled operand tile: 8-row x 128 B swizzle atoms stacked every 1024 B
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;            // leading byte offset (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset: next 8-row atom
+    d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+    return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+// idesc: D fp32, A/B tf32, both K-major, N>>3 at [17,23), M>>4 at [24,29)
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_3xtf32_kernel(
+    const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+    const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo, int M, int N,
+    int Kp, float alpha, float beta, float* __restrict__ C) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* accum = empty + STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // grouped raster over output tiles
+    const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+    const int tid = blockIdx.x;
+    const int group = tid / (GROUP_M * tiles_n);
+    const int first_m = group * GROUP_M;
+    const int gsize = min(tiles_m - first_m, GROUP_M);
+    const int tm = first_m + (tid % (GROUP_M * tiles_n)) % gsize;
+    const int tn = (tid % (GROUP_M * tiles_n)) / gsize;
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int nk = Kp / BK;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_ahi) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_alo) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_bhi) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_blo) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer
+            for (int kb = 0; kb < nk; kb++) {
+                const int s = kb % STAGES;
+                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                mbar_expect_tx(&full[s], STAGE_BYTES);
+                tma_load_2d(st, &tm_ahi, &full[s], kb * BK, m0);
+                tma_load_2d(st + A_TILE, &tm_alo, &full[s], kb * BK, m0);
+                tma_load_2d(st + 2 * A_TILE, &tm_bhi, &full[s], kb * BK, n0);
+                tma_load_2d(st + 2 * A_TILE + B_TILE, &tm_blo, &full[s], kb * BK, n0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            for (int kb = 0; kb < nk; kb++) {
+                const int s = kb % STAGES;
+                mbar_wait(&full[s], (kb / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
+                const uint64_t ahi = umma_desc_sw128(sa), alo = umma_desc_sw128(sa + A_TILE);
+                const uint64_t bhi = umma_desc_sw128(sa + 2 * A_TILE), blo = umma_desc_sw128(sa + 2 * A_TILE + B_TILE);
+#pragma unroll
+                for (int ks = 0; ks < BK / 8; ks++) {
+                    const uint64_t off = (uint64_t)(ks * 32) >> 4;  // 8 tf32 = 32 B along K inside the atom
+                    const uint32_t first = (kb | ks) != 0;
+                    mma_tf32(tmem, alo + off, bhi + off, IDESC, first);  // small terms first
+                    mma_tf32(tmem, ahi + off, blo + off, IDESC, 1);
+                    mma_tf32(tmem, ahi + off, bhi + off, IDESC, 1);
+                }
+                mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+            }
+            mma_commit(accum);
+        }
+    } else {
+        // epilogue: warps 2..5, TMEM lane quarter = warp % 4
+        const int q = warp & 3;
+        mbar_wait(accum, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int row = m0 + q * 32 + lane;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (row < M) {
+                float* crow = C + (long long)row * N + n0 + c0;
+                const int ncols = min(32, N - (n0 + c0));
+                if (ncols == 32 && ((uintptr_t)crow & 15) == 0) {
+#pragma unroll
+                    for (int v = 0; v < 8; v++) {
+                        float4 o;
+                        float4 old = beta != 0.f ? *reinterpret_cast<const float4*>(crow + 4 * v)
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+                        o.x = alpha * __uint_as_float(r[4 * v + 0]) + beta * old.x;
+                        o.y = alpha * __uint_as_float(r[4 * v + 1]) + beta * old.y;
+                        o.z = alpha * __uint_as_float(r[4 * v + 2]) + beta * old.z;
+                        o.w = alpha * __uint_as_float(r[4 * v + 3]) + beta * old.w;
+                        *reinterpret_cast<float4*>(crow + 4 * v) = o;
+                    }
+                } else {
+                    for (int v = 0; v < ncols; v++)
+                        crow[v] = alpha * __uint_as_float(r[v]) + (beta != 0.f ? beta * crow[v] : 0.f);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+// ---------------------------------------------------------------- prologue: tf32 split
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// A (rows x K, row-major) -> hi, lo (rows x Kp, zero-padded)
+__global__ void split_rows_kernel(const float* __restrict__ A, int rows, int K, int Kp,
+                                  float* __restrict__ hi, float* __restrict__ lo) {
+    const long long total = (long long)rows * Kp;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / Kp;
+        const int k = (int)(i - r * Kp);
+        float x = k < K ? A[r * K + k] : 0.f;
+        float h = tf32_rna(x);
+        hi[i] = h;
+        lo[i] = tf32_rna(x - h);
+    }
+}
+
+// B (K x N, row-major) -> Bt hi, lo (N x Kp, K-major), 32x32 smem transpose
+__global__ void split_transpose_kernel(const float* __restrict__ B, int K, int N, int Kp,
+                                       float* __restrict__ hi, float* __restrict__ lo) {
+    __shared__ float t[32][33];
+    const int k0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        int k = k0 + i, n = n0 + threadIdx.x;
+        t[i][threadIdx.x] = (k < K && n < N) ? B[(long long)k * N + n] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        int n = n0 + i, k = k0 + threadIdx.x;
+        if (n < N && k < Kp) {
+            float x = t[threadIdx.x][i];
+            float h = tf32_rna(x);
+            hi[(long long)n * Kp + k] = h;
+            lo[(long long)n * Kp + k] = tf32_rna(x - h);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const float* base, int rows, int Kp, int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)Kp * 4};
+    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t kpad(int k) { return ((size_t)(k > 0 ? k : 1) + BK - 1) / BK * BK; }
+
+}  // namespace
+
+size_t gemm_workspace_bytes(int m, int n, int k) {
+    return 2 * ((size_t)m + (size_t)n) * kpad(k) * sizeof(float) + 4096;
+}
+
+int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, const float* A,
+                const float* B, float* C, void* workspace, size_t workspace_bytes) {
+    if (m <= 0 || n <= 0) return 0;
+    const int Kp = (int)kpad(k);
+    if (workspace_bytes < gemm_workspace_bytes(m, n, k)) return (int)cudaErrorInvalidValue;
+    float* ahi = (float*)(((uintptr_t)workspace + 1023) & ~(uintptr_t)1023);
+    float* alo = ahi + (size_t)m * Kp;
+    float* bhi = alo + (size_t)m * Kp;
+    float* blo = bhi + (size_t)n * Kp;
+    {
+        long long total = (long long)m * Kp;
+        long long blocks = (total + 255) / 256;
+        split_rows_kernel<<<(int)(blocks < PENCIL_NUM_SMS * 16 ? blocks : PENCIL_NUM_SMS * 16), 256, 0, st>>>(
+            A, m, k, Kp, ahi, alo);
+        dim3 g((Kp + 31) / 32, (n + 31) / 32);
+        split_transpose_kernel<<<g, dim3(32, 8), 0, st>>>(B, k, n, Kp, bhi, blo);
+    }
+    CUtensorMap maps[4];
+    if (!make_map(&maps[0], ahi, m, Kp, BM) || !make_map(&maps[1], alo, m, Kp, BM) ||
+        !make_map(&maps[2], bhi, n, Kp, BN) || !make_map(&maps[3], blo, n, Kp, BN))
+        return (int)cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        attr = true;
+    }
+    const int tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+    gemm_3xtf32_kernel<<<tiles, GEMM_THREADS, SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], m, n, Kp,
+                                                               alpha, beta, C);
+    return (int)cudaGetLastError();
+}

@@ -121,6 +121,42 @@ def test_conv5x5_u8_16384(cuda):
         assert torch.equal(out8.to(torch.int32), out)
 
 
+def _gemm_scale(A, B, C, alpha, beta, m, n, k):
+    return abs(alpha) * (np.abs(A.reshape(m, k)).astype(np.float64) @ np.abs(B.reshape(k, n))) + \
+        abs(beta) * np.abs(C.reshape(m, n))
+
+
+@pytest.mark.parametrize("shape", [(2048, 2048, 2048, 1.0, 0.0), (1000, 777, 333, 1.25, 0.5), (128, 256, 32, 1.0, 0.0),
+                                   (129, 257, 33, -0.5, 2.0)])
+def test_gemm_3xtf32_vs_fp64(cuda, shape):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    m, n, k, alpha, beta = shape
+    A, B, C = synth.f32(m * k, 42), synth.f32(k * n, 43), synth.f32(m * n, 44)
+    Cd = dev(torch, C.copy())
+    pb.device.gemm(m, n, k, alpha, beta, dev(torch, A), dev(torch, B), Cd)
+    ref = alpha * (A.reshape(m, k).astype(np.float64) @ B.reshape(k, n).astype(np.float64)) + beta * C.reshape(m, n)
+    err = normwise_err(Cd.cpu().numpy().reshape(m, n), ref, _gemm_scale(A, B, C, alpha, beta, m, n, k))
+    assert err <= TOL, err
+
+
+def test_gemm_16384_sampled(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    m = n = k = 16384
+    A, B = synth.f32(m * k, 42), synth.f32(k * n, 43)
+    Cd = torch.zeros(m * n, device="cuda")
+    pb.device.gemm(m, n, k, 1.0, 0.0, dev(torch, A), dev(torch, B), Cd)
+    got = Cd.view(m, n)
+    rng = np.random.default_rng(0)
+    rows, cols = rng.integers(0, m, 64), rng.integers(0, n, 64)
+    A2, B2 = A.reshape(m, k), B.reshape(k, n)
+    sub = got[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu().numpy()
+    ref = A2[rows].astype(np.float64) @ B2[:, cols].astype(np.float64)
+    scale = np.abs(A2[rows]).astype(np.float64) @ np.abs(B2[:, cols]).astype(np.float64)
+    assert normwise_err(sub, ref, scale) <= TOL  # 4096 sampled entries of C
+
+
 def test_conv5x5_f32_16384(cuda):
     import paper_1302_5586_b200 as pb
     torch = cuda
