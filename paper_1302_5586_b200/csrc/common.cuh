@@ -66,6 +66,34 @@ __device__ __forceinline__ void st_stream_f4(float4* p, float4 v) {
                  "f"(v.y), "f"(v.z), "f"(v.w));
 }
 
+// mbarrier + 1-D bulk async copy (TMA engine, no tensor map): global -> shared, completion
+// counted in bytes on the mbarrier.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "BWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra BWAIT_%=;\n}" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+// dst, src 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
 template <int W>
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

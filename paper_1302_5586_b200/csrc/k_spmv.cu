@@ -20,6 +20,9 @@
 // Faults (E-INTERP analogues): col outside [0, ncols) or rowptr outside [0, nnz] set a bit
 // in the status word and contribute 0.  A non-monotone rowptr (legal in PENCIL: the row
 // is empty) switches the launch to a generic thread-per-row schedule.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -169,6 +172,155 @@ __global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_stream_kernel(
     }  // tickets
 }
 
+// TMA-fed variant (experimental, PENCIL_SPMV_KERNEL=tma).  The LSU path above spends the SM's
+// L1TEX miss-request bandwidth (the limiter, ~1 request per clock) on both the x gathers AND
+// the col/val stream.  Here the stream comes in through the TMA engine instead: each warp
+// ring-buffers 128-non-zero chunks of col and val with 1-D bulk copies (cp.async.bulk,
+// mbarrier completion), so L1TEX only carries the gathers.  Chunks are cut at 4-aligned
+// absolute positions over the tile's contiguous non-zero range; 32-row batches are merged
+// against the chunk stream.  Measured slower than the LSU path (see TNBUF): per-warp
+// 512-byte bulk copies are too small for the TMA engine.
+#define TCH 128
+#define TNBUF 2  // chunks in flight per warp (measured: 2 -> 1.87 ms, 4 -> 3.78 ms at 2^24 rows)
+#define TMA_CTAS_PER_SM 8
+struct __align__(16) TmaWarpBufs {
+    int col[TNBUF][TCH];
+    float val[TNBUF][TCH];
+    float prod[TCH + TCH / 32];
+    uint64_t bar[TNBUF];
+};
+
+template <bool ASSOC>
+__global__ void __launch_bounds__(SPMV_THREADS, TMA_CTAS_PER_SM) csr_tma_kernel(
+    int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
+    const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
+    const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
+    unsigned* __restrict__ status) {
+    __shared__ TmaWarpBufs wb[WARPS_PER_CTA];
+    if (plan[0]) {
+        spmv_generic(nrows, ncols, nnz_len, rowptr, col, val, x, y, status);
+        return;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
+    TmaWarpBufs& B = wb[warp];
+    if (lane == 0) {
+        for (int b = 0; b < TNBUF; b++) bar_init(&B.bar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    unsigned phases = 0;  // bit b = parity to wait for on buffer b
+    int bi = 0;           // buffer of the next chunk to consume (ring continues across tiles)
+    auto clampp = [&](int v) { return v < 0 ? 0 : (v > nnz_len ? nnz_len : v); };
+    for (;;) {
+        unsigned ticket = 0;
+        if (lane == 0) ticket = atomicAdd(&plan[1], 1u);
+        ticket = __shfl_sync(0xffffffffu, ticket, 0);
+        if (ticket >= (unsigned)ntiles) {
+            if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
+            return;
+        }
+        const int r0 = __ldg(tile_row + ticket), r1 = __ldg(tile_row + ticket + 1);
+        const int P0 = clampp(__ldg(rowptr + r0)), P1 = max(P0, clampp(__ldg(rowptr + r1)));
+        const int A0 = P0 & ~3;
+        const int nch = P1 > A0 ? (P1 - A0 + TCH - 1) / TCH : 0;
+        // chunk j = [A0 + j*TCH, min(A0 + (j+1)*TCH, P1)); bulk-copied when its 16-byte rounded
+        // extent stays inside the arrays, else read directly (only the array's last chunk)
+        auto chunk_tma_ok = [&](int j) {
+            const int c0 = A0 + j * TCH, cnt = min(TCH, P1 - c0);
+            return c0 + ((cnt + 3) & ~3) <= nnz_len;
+        };
+        auto issue = [&](int j, int b) {
+            const int c0 = A0 + j * TCH, cnt = min(TCH, P1 - c0);
+            const unsigned n4 = (unsigned)((cnt + 3) & ~3);
+            bar_expect_tx(&B.bar[b], n4 * 8u);
+            bulk_g2s(B.col[b], col + c0, n4 * 4u, &B.bar[b]);
+            bulk_g2s(B.val[b], val + c0, n4 * 4u, &B.bar[b]);
+        };
+        if (lane == 0)
+            for (int j = 0; j < TNBUF - 1 && j < nch; j++)
+                if (chunk_tma_ok(j)) issue(j, (bi + j) % TNBUF);
+
+        // 32-row batch state
+        int rb = r0, re = 0, row = 0, my_s = 0, my_e = 0, bend = 0;
+        bool active = false;
+        auto load_batch = [&]() {
+            re = min(rb + 32, r1);
+            row = rb + lane;
+            active = row < re;
+            my_s = active ? clampp(__ldg(rowptr + row)) : 0;
+            my_e = active ? max(my_s, clampp(__ldg(rowptr + row + 1))) : 0;
+            bend = clampp(__ldg(rowptr + re));
+        };
+        if (rb < r1) load_batch();
+        float s = 0.f;
+
+        for (int j = 0; j < nch; j++) {
+            const int c0 = A0 + j * TCH, cend = min(c0 + TCH, P1), cnt = cend - c0;
+            const bool tma = chunk_tma_ok(j);
+            if (j + TNBUF - 1 < nch && lane == 0 && chunk_tma_ok(j + TNBUF - 1))
+                issue(j + TNBUF - 1, (bi + TNBUF - 1) % TNBUF);
+            if (tma) {
+                bar_wait(&B.bar[bi], (phases >> bi) & 1u);
+                phases ^= 1u << bi;
+            }
+            int cc[TCH / 32];
+            float vv[TCH / 32], xv[TCH / 32];
+#pragma unroll
+            for (int u = 0; u < TCH / 32; u++) {
+                const int t = u * 32 + lane;
+                const bool in = t < cnt && c0 + t >= P0;
+                cc[u] = in ? (tma ? B.col[bi][t] : __ldg(col + c0 + t)) : 0;
+                vv[u] = in ? (tma ? B.val[bi][t] : __ldg(val + c0 + t)) : 0.f;
+                xv[u] = 0.f;
+                if (in) {
+                    if ((unsigned)cc[u] < (unsigned)ncols) xv[u] = ld_keep_f(x + cc[u]);
+                    else raise_fault(status, FAULT_OOB_LOAD);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < TCH / 32; u++) B.prod[skew(u * 32 + lane)] = __fmul_rn(vv[u], xv[u]);
+            __syncwarp();
+            for (;;) {  // fold every batch overlapping this chunk
+                const int lo = max(my_s, c0), hi = min(my_e, cend);
+                if (ASSOC) {
+                    unsigned big = __ballot_sync(0xffffffffu, hi - lo > 16);
+                    if (hi - lo <= 16)
+                        for (int p = lo; p < hi; p++) s = __fadd_rn(s, B.prod[skew(p - c0)]);
+                    while (big) {
+                        const int o = __ffs(big) - 1;
+                        big &= big - 1;
+                        const int olo = __shfl_sync(0xffffffffu, lo, o), ohi = __shfl_sync(0xffffffffu, hi, o);
+                        float part = 0.f;
+                        for (int p = olo + lane; p < ohi; p += 32) part += B.prod[skew(p - c0)];
+                        part = warp_sum<32>(part);
+                        if (lane == o) s += part;
+                    }
+                } else {
+                    for (int p = lo; p < hi; p++) s = __fadd_rn(s, B.prod[skew(p - c0)]);
+                }
+                if (rb < r1 && bend <= cend) {  // batch complete inside this chunk
+                    if (active) y[row] = s;
+                    rb += 32;
+                    s = 0.f;
+                    if (rb >= r1) break;
+                    load_batch();
+                    continue;
+                }
+                break;
+            }
+            __syncwarp();
+            bi = (bi + 1) % TNBUF;
+        }
+        while (rb < r1) {  // batches of empty rows past the last chunk (or tiles without non-zeros)
+            if (active) y[row] = s;
+            s = 0.f;
+            rb += 32;
+            if (rb < r1) load_batch();
+        }
+    }
+}
+
 int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
                     int ntiles, int* tile_row, unsigned* plan_flags, unsigned* status) {
     cudaMemsetAsync(plan_flags, 0, 64, st);  // [0] non-monotone flag, [1] tile ticket counter
@@ -220,13 +372,29 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     }
+    // executor: all-LSU (default; 1.44 ms at 2^24 rows) or the TMA-fed stream
+    // (PENCIL_SPMV_KERNEL=tma; 1.87 ms — 512-byte bulk copies cost more than they free)
+    static int use_tma = -1;
+    if (use_tma < 0) {
+        const char* e = getenv("PENCIL_SPMV_KERNEL");
+        use_tma = (e && !strcmp(e, "tma"));
+    }
     cudaError_t e;
-    if (assoc)
+    if (use_tma && grid > PENCIL_NUM_SMS * TMA_CTAS_PER_SM) cfg.gridDim = dim3(PENCIL_NUM_SMS * TMA_CTAS_PER_SM);
+    if (use_tma) {
+        if (assoc)
+            e = cudaLaunchKernelEx(&cfg, csr_tma_kernel<true>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                   tile_row, ntiles, plan_flags, status);
+        else
+            e = cudaLaunchKernelEx(&cfg, csr_tma_kernel<false>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                   tile_row, ntiles, plan_flags, status);
+    } else if (assoc) {
         e = cudaLaunchKernelEx(&cfg, csr_stream_kernel<true>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
                                tile_row, ntiles, plan_flags, status);
-    else
+    } else {
         e = cudaLaunchKernelEx(&cfg, csr_stream_kernel<false>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
                                tile_row, ntiles, plan_flags, status);
+    }
     return (int)e;
 }
 
