@@ -166,7 +166,7 @@ def bench_spmv(args, torch, pb, rank, world, dist):
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
            "config": {"workload": "CSR SpMV fp32 (spmv_vec), power-law rows 2^24 x 2^24, 16 nnz/row",
                       "nrows": nrows, "ncols": nrows, "nnz": nnz, "alpha": 1.5, "xm": round(xm, 4),
-                      "maxlen": 4096, "seed": 42, "schedule": "csr_stream_assoc (nnz-window tiles, 2048 nnz)",
+                      "maxlen": 4096, "seed": 42, "schedule": "csr_stream_assoc (persistent warps, 512-nnz window tiles)",
                       "l2": "256 MiB flush between steps, outside the per-step events; inputs 2.35 GB > L2"}}
     if rank == 0 and world == 1 and not args.no_e2e:
         res["e2e"] = e2e_spmv(args, torch, pb, rowptr, col, val, x)
@@ -319,6 +319,7 @@ def main():
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--suite-steps", type=int, default=10)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -334,15 +335,21 @@ def main():
 
     import torch
     import paper_1302_5586_b200 as pb
-    torch.cuda.set_device(local_rank)
+    # one process per GPU; with fewer GPUs than ranks (plumbing test: --dist-backend gloo) ranks
+    # share devices — their kernels never wait on one another, only host-side collectives do
+    dev = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            tdist.init_process_group(args.dist_backend)
         dist = tdist
     hbm, tf, peak_kind = peaks()
 
-    with Clocks(local_rank) as clk:
+    with Clocks(dev) as clk:
         res = bench_spmv(args, torch, pb, rank, world, dist)
     ms = res["ms"]
     if dist:

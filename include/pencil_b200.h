@@ -171,6 +171,9 @@ int pencil_l2_flush(pencil_stream_t s); /* write a buffer larger than L2 (timing
 int pencil_micro_gather(pencil_stream_t s, int mode, long long n, const int* idx,
                         const float* table, float* out);
 int pencil_micro_copy(pencil_stream_t s, long long n, const float* src, float* dst);
+/* SpMV data path without rows: stream idx + val, gather table[idx] (roofline probe) */
+int pencil_micro_gather_val(pencil_stream_t s, long long n, const int* idx, const float* val,
+                            const float* table, float* out);
 
 #ifdef __cplusplus
 }

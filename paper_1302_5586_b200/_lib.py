@@ -70,6 +70,7 @@ SIGNATURES = {
     "pencil_l2_flush": (c_int, [P]),
     "pencil_micro_gather": (c_int, [P, c_int, c_ll, P, P, P]),
     "pencil_micro_copy": (c_int, [P, c_ll, P, P]),
+    "pencil_micro_gather_val": (c_int, [P, c_ll, P, P, P, P]),
     # introspection used by the boundary tests (not in the public header)
     "pencil_fixture_signature": (c_int, [c_char_p, c_char_p, c_int]),
     "pencil_fixture_count": (c_int, []),

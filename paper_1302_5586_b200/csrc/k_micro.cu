@@ -13,6 +13,31 @@ __device__ __forceinline__ float gather_ld(const float* p) {
     return r;
 }
 
+// the SpMV data path without rows: stream idx + val (8 B/nnz, 128-bit loads), gather table[idx]
+// (evict-last), accumulate val * x — the practical ceiling of a CSR SpMV on this matrix
+__global__ void __launch_bounds__(256) micro_gather_val_kernel(long long n, const int* __restrict__ idx,
+                                                               const float* __restrict__ val,
+                                                               const float* __restrict__ table,
+                                                               float* __restrict__ out) {
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthr = (long long)gridDim.x * blockDim.x;
+    const long long n4 = n >> 2;
+    float acc = 0.f;
+    for (long long i = tid; i < n4; i += nthr) {
+        const int4 a = ld_stream_i4(reinterpret_cast<const int4*>(idx) + i);
+        const float4 v = ld_stream_f4(reinterpret_cast<const float4*>(val) + i);
+        acc += v.x * ld_keep_f(table + a.x) + v.y * ld_keep_f(table + a.y) + v.z * ld_keep_f(table + a.z) +
+               v.w * ld_keep_f(table + a.w);
+    }
+    out[tid] = acc;
+}
+
+int launch_micro_gather_val(cudaStream_t st, long long n, const int* idx, const float* val, const float* table,
+                            float* out) {
+    micro_gather_val_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>(n, idx, val, table, out);
+    return (int)cudaGetLastError();
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) micro_gather_kernel(long long n, const int* __restrict__ idx,
                                                            const float* __restrict__ table,

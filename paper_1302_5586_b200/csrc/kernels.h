@@ -47,4 +47,6 @@ size_t gemm_workspace_bytes(int m, int n, int k);
 int launch_micro_gather(cudaStream_t st, int mode, long long n, const int* idx, const float* table,
                         float* out);
 int launch_micro_copy(cudaStream_t st, long long n, const float* src, float* dst);
+int launch_micro_gather_val(cudaStream_t st, long long n, const int* idx, const float* val, const float* table,
+                            float* out);
 int launch_micro_l2_flush(cudaStream_t st, long long n, float* buf);

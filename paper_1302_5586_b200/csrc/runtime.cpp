@@ -597,6 +597,12 @@ int pencil_micro_gather(pencil_stream_t s, int mode, long long n, const int* idx
     DEV_RET(launch_micro_gather(st, mode, n, idx, table, out));
 }
 
+int pencil_micro_gather_val(pencil_stream_t s, long long n, const int* idx, const float* val,
+                            const float* table, float* out) {
+    DEV_PROLOGUE;
+    DEV_RET(launch_micro_gather_val(st, n, idx, val, table, out));
+}
+
 int pencil_micro_copy(pencil_stream_t s, long long n, const float* src, float* dst) {
     DEV_PROLOGUE;
     DEV_RET(launch_micro_copy(st, n, src, dst));

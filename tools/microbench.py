@@ -44,6 +44,11 @@ def main():
                         ("1cta_bigsmem_148sm", 1 | (1 << 4) | (1 << 8)), ("1cta_bigsmem_74sm", 1 | (1 << 8) | (1 << 9))]:
         best, _ = time_ms(lambda: lib.pencil_micro_gather(st, mode, n, idx.data_ptr(), table.data_ptr(), res.data_ptr()))
         out[f"gather_scaling_{label}"] = {"ms": best, "Ggathers/s": n / best / 1e6}
+    # the SpMV data path without rows: idx + val streams and the gather (practical SpMV ceiling)
+    val = torch.randn(n, device="cuda")
+    best, _ = time_ms(lambda: lib.pencil_micro_gather_val(st, n, idx.data_ptr(), val.data_ptr(), table.data_ptr(), res.data_ptr()))
+    out["gather_val_stream"] = {"ms": best, "Ggathers/s": n / best / 1e6, "spmv_algo_GB/s": (8 * n + 12 * ncols) / best / 1e6}
+    del val
     # sorted indices (perfect locality) for contrast
     idx_sorted, _ = torch.sort(idx)
     best, _ = time_ms(lambda: lib.pencil_micro_gather(st, 1, n, idx_sorted.data_ptr(), table.data_ptr(), res.data_ptr()))
