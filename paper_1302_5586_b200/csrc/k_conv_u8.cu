@@ -38,16 +38,18 @@ struct Div {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-__device__ __forceinline__ unsigned scale_sat(int acc, const Div& d) {
+__device__ __forceinline__ unsigned scale_sat(long long acc, const Div& d) {
     if (d.scale > 0) {
-        const long long nn = (long long)acc + (d.scale >> 1);
+        const long long nn = acc + (d.scale >> 1);
         if (nn < 0) return 0u;  // truncation toward zero gives <= 0 -> saturates at 0
         unsigned long long q;
         if (d.shift >= 0) q = (unsigned long long)nn >> d.shift;
-        else q = __umul64hi((unsigned long long)nn, d.magic);
+        else if (nn >= 256ll * d.scale) return 255u;  // saturates whatever the quotient
+        else if (nn < (1ll << 32)) q = __umul64hi((unsigned long long)nn, d.magic);  // n * scale < 2^64
+        else q = (unsigned long long)(nn / d.scale);
         return q > 255ull ? 255u : (unsigned)q;
     }
-    const int q = (int)(((long long)acc + d.scale / 2) / d.scale);  // negative scale: exact C semantics
+    const long long q = (acc + d.scale / 2) / d.scale;  // negative scale: exact C semantics
     return (unsigned)(q < 0 ? 0 : (q > 255 ? 255 : q));
 }
 
@@ -143,12 +145,13 @@ __device__ __forceinline__ bool finish_row(const Raw<I32>& rr, int lane, u64 (&E
 template <bool I32>
 __device__ __forceinline__ unsigned pixel_exact(const typename Pix<I32>::T* __restrict__ img, int h, int w, int i,
                                                 int j, const TapsU8& k, const Div& dv) {
-    int acc = 0;
+    long long acc = 0;  // int64 like the interpreter (interp.cpp:49-64): exact for any int input
 #pragma unroll 1
     for (int di = 0; di < 5; di++) {
         const typename Pix<I32>::T* row = img + (long long)clampi(i + di - 2, 0, h - 1) * w;
 #pragma unroll 1
-        for (int dj = 0; dj < 5; dj++) acc += k.ki[di * 5 + dj] * (int)row[clampi(j + dj - 2, 0, w - 1)];
+        for (int dj = 0; dj < 5; dj++)
+            acc += (long long)k.ki[di * 5 + dj] * (long long)row[clampi(j + dj - 2, 0, w - 1)];
     }
     return scale_sat(acc, dv);
 }

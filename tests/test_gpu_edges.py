@@ -1,0 +1,151 @@
+"""Edge cases of the CUDA path (run with -m gpu): schedules the golden shapes do not reach —
+non-monotone CSR rowptr (the generic per-row schedule), ragged widths that take the scalar
+stencil kernels, misaligned device pointers, views that leave their declared extent, faults."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import normwise_err
+from paper_1302_5586_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def test_spmv_non_monotone_rowptr_takes_generic_schedule(cuda):
+    import paper_1302_5586_b200 as pb
+    # row 1 has end < start: an empty row in PENCIL semantics (the k loop does not run)
+    rowptr = np.array([0, 3, 1, 4, 6], np.int32)
+    col = np.array([0, 2, 1, 3, 0, 1], np.int32)
+    val = synth.f32(6, seed=3)
+    x = synth.f32(4, seed=4)
+    for fn in (pb.dropin.spmv_inline, pb.dropin.spmv_vec):
+        y = np.zeros(4, np.float32)
+        fn(4, 4, 6, rowptr, col, val, x, y)
+        ref = oracle.spmv_f32(4, 4, 6, rowptr, col, val, x)
+        assert np.array_equal(y.view(np.uint32), ref.view(np.uint32))
+
+
+def test_spmv_out_of_range_column_faults_then_recovers(cuda):
+    import paper_1302_5586_b200 as pb
+    rowptr = np.array([0, 2, 3], np.int32)
+    col = np.array([0, 9, 1], np.int32)
+    with pytest.raises(pb.PencilError) as e:
+        pb.dropin.spmv_vec(2, 4, 3, rowptr, col, synth.f32(3), synth.f32(4), np.zeros(2, np.float32))
+    assert e.value.code == "E-INTERP"
+    # the fault word was collected and cleared: the next good call succeeds
+    y = np.zeros(2, np.float32)
+    pb.dropin.spmv_vec(2, 4, 3, rowptr, np.array([0, 3, 1], np.int32), synth.f32(3), synth.f32(4), y)
+
+
+def test_spmv_all_rows_empty_and_single_long_row(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    for lens in ([0] * 1000, [0] * 10 + [5000] + [0] * 10, [4096] * 3 + [1] * 5000):
+        rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        nnz, nrows = int(rowptr[-1]), len(lens)
+        col = (synth.u8_i32(max(nnz, 1), seed=7)[:nnz] * 3) % 977
+        val, x = synth.f32(max(nnz, 1), seed=8)[:nnz], synth.f32(977, seed=9)
+        for mode in (0, 1):
+            rp = torch.from_numpy(rowptr).cuda()
+            plan = pb.device.CsrPlan(nrows, 977, nnz, rp, mode=mode)
+            y = torch.full((nrows,), 7.0, device="cuda")
+            plan.spmv(rp, torch.from_numpy(col.astype(np.int32)).cuda(), torch.from_numpy(val).cuda(),
+                      torch.from_numpy(x).cuda(), y)
+            pb.device.sync_status()
+            got = y.cpu().numpy()
+            ref64 = oracle.spmv(nrows, 977, nnz, rowptr, col.astype(np.int32), val, x)
+            if mode == 0:
+                exact = oracle.spmv_f32(nrows, 977, nnz, rowptr, col.astype(np.int32), val, x)
+                assert np.array_equal(got.view(np.uint32), exact.view(np.uint32))
+            terms = np.abs(val.astype(np.float64)) * np.abs(x[col])
+            cs = np.concatenate([[0.0], np.cumsum(terms)])
+            assert normwise_err(got, ref64, cs[rowptr[1:]] - cs[rowptr[:-1]]) <= 1e-5
+
+
+@pytest.mark.parametrize("h,w", [(13, 37), (64, 130), (5, 5), (130, 6)])
+def test_stencils_ragged_widths(cuda, h, w):
+    import paper_1302_5586_b200 as pb
+    img = synth.u8_i32(h * w, seed=h * w)
+    for k, scale in ((synth.BINOMIAL, 256), (synth.SHARPEN, 1), (synth.BINOMIAL, 7)):
+        out = np.zeros(h * w, np.int32)
+        pb.dropin.conv5x5_u8(h, w, scale, img, k, out)
+        assert np.array_equal(out.astype(np.int64), oracle.conv5x5_u8(h, w, scale, img, k))
+    imgf, kf, o0 = synth.f32(h * w, seed=5), synth.f32(25, seed=6), synth.f32(h * w, seed=7)
+    outf = o0.copy()
+    pb.dropin.conv5x5_f32(h, w, imgf, kf, outf)
+    exact = oracle.conv5x5_f32_f32(h, w, imgf, kf, o0)
+    assert np.array_equal(outf.view(np.uint32), exact.view(np.uint32))
+
+
+def test_conv_u8_int32_storage_not_an_8bit_image(cuda):
+    """int32 storage may hold any int: the warp-rows with values outside [0, 255] take the exact
+    int32 path inside the fast kernel."""
+    import paper_1302_5586_b200 as pb
+    h, w = 70, 256
+    img = synth.u8_i32(h * w, seed=11)
+    img[5 * w + 17] = 100000
+    img[40 * w + 200] = -77
+    out = np.zeros(h * w, np.int32)
+    pb.dropin.conv5x5_u8(h, w, 256, img, synth.BINOMIAL, out)
+    assert np.array_equal(out.astype(np.int64), oracle.conv5x5_u8(h, w, 256, img, synth.BINOMIAL))
+    big = synth.BINOMIAL * 1000  # taps beyond the fp32-exact range -> exact int path
+    pb.dropin.conv5x5_u8(h, w, 7, img, big, out)
+    assert np.array_equal(out.astype(np.int64), oracle.conv5x5_u8(h, w, 7, img, big))
+
+
+def test_conv_u8_bytes_matches_int32_storage_ragged(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    for h, w in ((33, 512), (20, 1000), (9, 16)):
+        img = synth.u8_i32(h * w, seed=w)
+        for k, scale in ((synth.BINOMIAL, 256), (synth.SHARPEN, 1), (synth.BINOMIAL * 3, 5)):
+            out8 = torch.empty(h * w, dtype=torch.uint8, device="cuda")
+            pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img.astype(np.uint8)).cuda(), k, out8)
+            ref = oracle.conv5x5_u8(h, w, scale, img, k)
+            assert np.array_equal(out8.cpu().numpy().astype(np.int64), ref), (h, w, scale)
+
+
+def test_misaligned_device_pointers(cuda):
+    """views starting one element into a buffer are not 16-byte aligned: scalar paths"""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    m, n = 37, 101
+    A, x, y = synth.f32(m * n + 1), synth.f32(n + 1, 3), synth.f32(m + 1, 4)
+    Ad, xd, yd = (torch.from_numpy(a).cuda() for a in (A, x, y))
+    pb.device.gemv(m, n, 1.0, 0.5, Ad[1:], xd[1:], yd[1:])
+    ref = oracle.gemv(m, n, 1.0, 0.5, A[1:], x[1:], y[1:])
+    scale = np.abs(A[1:].reshape(m, n)).astype(np.float64) @ np.abs(x[1:]) + 0.5 * np.abs(y[1:])
+    assert normwise_err(yd[1:].cpu().numpy(), ref, scale) <= 1e-5
+    nv = 1001
+    a, b = synth.f32(nv + 1, 5), synth.f32(nv + 1, 6)
+    ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    r = torch.zeros(1, device="cuda")
+    pb.device.dot(nv, ad[1:], bd[1:], r)
+    assert abs(r.item() - oracle.dot(nv, a[1:], b[1:])) <= 1e-5 * float(np.sum(np.abs(a[1:].astype(np.float64) * b[1:])))
+
+
+def test_gemv_t_view_leaving_its_extent_faults(cuda):
+    import paper_1302_5586_b200 as pb
+    with pytest.raises(pb.PencilError) as e:
+        pb.dropin.gemv_t(4, 9, 8, 1, 1, 1.0, 0.0, synth.f32(32), synth.f32(4), np.zeros(9, np.float32))
+    assert e.value.code == "E-INTERP"
+
+
+def test_interpreter_mirror_errors(cuda):
+    import paper_1302_5586_b200 as pb
+    it = pb.CudaInterpreter(0)
+    it.set_array("A", synth.f32(6))
+    with pytest.raises(pb.PencilError, match="no function named"):
+        it.call("nope", [])
+    with pytest.raises(pb.PencilError, match="wrong argument count"):
+        it.call("dot", [pb.Arg.scalar(3)])
+    with pytest.raises(pb.PencilError, match="needs an array"):
+        it.call("dot", [pb.Arg.scalar(3), pb.Arg.scalar(1), pb.Arg.array("A")])
+    with pytest.raises(pb.PencilError, match="no array storage"):
+        it.call("dot", [pb.Arg.scalar(3), pb.Arg.array("A"), pb.Arg.array("B")])
+    # an array shorter than its C99 static extent: the interpreter would fault on the first
+    # load past its end
+    with pytest.raises(pb.PencilError) as e:
+        it.call("dot", [pb.Arg.scalar(7), pb.Arg.array("A"), pb.Arg.array("A")])
+    assert e.value.code == "E-INTERP"
+    assert it.call("dot", [pb.Arg.scalar(6), pb.Arg.array("A"), pb.Arg.array("A")]) > 0
