@@ -166,7 +166,7 @@ def bench_spmv(args, torch, pb, rank, world, dist):
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
            "config": {"workload": "CSR SpMV fp32 (spmv_vec), power-law rows 2^24 x 2^24, 16 nnz/row",
                       "nrows": nrows, "ncols": nrows, "nnz": nnz, "alpha": 1.5, "xm": round(xm, 4),
-                      "maxlen": 4096, "seed": 42, "schedule": "csr_stream_assoc (persistent warps, 512-nnz window tiles)",
+                      "maxlen": 4096, "seed": 42, "schedule": "csr_stream_assoc (persistent warps, 1024-nnz window tiles)",
                       "l2": "256 MiB flush between steps, outside the per-step events; inputs 2.35 GB > L2"}}
     if rank == 0 and world == 1 and not args.no_e2e:
         res["e2e"] = e2e_spmv(args, torch, pb, rowptr, col, val, x)

@@ -27,7 +27,9 @@
 #include "kernels.h"
 
 #define SPMV_THREADS 256
-#define SPMV_TILE_NNZ 512  // non-zeros per warp tile (plan window)
+// non-zeros per warp tile (plan window); swept over {256..2048} x WCHUNK {64,128,256} at
+// 2^24 rows (tools/spmv_sweep.sh): 1024 x 128 is fastest (1.28 ms; 512: 1.34; 256: 1.59)
+#define SPMV_TILE_NNZ 1024
 
 __global__ void csr_plan_kernel(int nrows, int nnz_len, const int* __restrict__ rowptr,
                                 int tile_nnz, int ntiles, int* __restrict__ tile_row,
@@ -87,15 +89,15 @@ __device__ void spmv_generic(int nrows, int ncols, int nnz_len, const int* __res
 // Skewed staging index: lane i folds row i, whose slice starts near i*len; without the skew
 // rows of equal length 16 put 16 lanes on one bank (a 16-way conflict on every read).
 __device__ __forceinline__ int skew(int t) { return t + (t >> 5); }
-#define WCHUNK_SKEWED (WCHUNK + WCHUNK / 32)
+#define WCHUNK_SKEWED (WCHUNK + WCH / 32)
 
-template <bool ASSOC>
-__global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_stream_kernel(
+template <bool ASSOC, int WCH>
+__global__ void __launch_bounds__(SPMV_THREADS, (WCH <= 128 ? CTAS_PER_SM : 6)) csr_stream_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
     const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
     unsigned* __restrict__ status) {
-    __shared__ float s_prod[WARPS_PER_CTA][WCHUNK_SKEWED];
+    __shared__ float s_prod[WARPS_PER_CTA][WCH + WCH / 32];
     if (plan[0]) {  // non-monotone rowptr, flagged by the plan kernel earlier on this stream
         spmv_generic(nrows, ncols, nnz_len, rowptr, col, val, x, y, status);
         return;
@@ -126,18 +128,18 @@ __global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_stream_kernel(
         const int q_begin = max(__shfl_sync(0xffffffffu, my_s, 0), 0);
         const int q_end = min(__ldg(rowptr + re), nnz_len);
         float s = 0.f;
-        for (int q = q_begin; q < q_end; q += WCHUNK) {
-            const int cnt = min(WCHUNK, q_end - q);
-            int c[WCHUNK / 32];
-            float v[WCHUNK / 32], xv[WCHUNK / 32];
+        for (int q = q_begin; q < q_end; q += WCH) {
+            const int cnt = min(WCH, q_end - q);
+            int c[WCH / 32];
+            float v[WCH / 32], xv[WCH / 32];
 #pragma unroll
-            for (int u = 0; u < WCHUNK / 32; u++) {
+            for (int u = 0; u < WCH / 32; u++) {
                 const int t = u * 32 + lane;
                 c[u] = t < cnt ? ld_stream_i(col + q + t) : 0;
                 v[u] = t < cnt ? ld_stream_f(val + q + t) : 0.f;
             }
 #pragma unroll
-            for (int u = 0; u < WCHUNK / 32; u++) {
+            for (int u = 0; u < WCH / 32; u++) {
                 xv[u] = 0.f;
                 if (u * 32 + lane < cnt) {
                     if ((unsigned)c[u] < (unsigned)ncols) xv[u] = ld_keep_f(x + c[u]);
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_stream_kernel(
                 }
             }
 #pragma unroll
-            for (int u = 0; u < WCHUNK / 32; u++)  // the product rounds on its own (emitted C as written)
+            for (int u = 0; u < WCH / 32; u++)  // the product rounds on its own (emitted C as written)
                 sp[skew(u * 32 + lane)] = __fmul_rn(v[u], xv[u]);
             __syncwarp();
             const int lo = max(my_s, q), hi = min(my_e, q + cnt);
@@ -392,12 +394,21 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
         else
             e = cudaLaunchKernelEx(&cfg, csr_tma_kernel<false>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
                                    tile_row, ntiles, plan_flags, status);
-    } else if (assoc) {
-        e = cudaLaunchKernelEx(&cfg, csr_stream_kernel<true>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                               tile_row, ntiles, plan_flags, status);
     } else {
-        e = cudaLaunchKernelEx(&cfg, csr_stream_kernel<false>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                               tile_row, ntiles, plan_flags, status);
+        // chunk of non-zeros per warp step (gathers in flight per lane = wch / 32);
+        // PENCIL_SPMV_WCHUNK = 64 | 128 | 256 (tuning knob, default 128)
+        static int wch = -1;
+        if (wch < 0) {
+            const char* w = getenv("PENCIL_SPMV_WCHUNK");
+            wch = w ? atoi(w) : 128;
+            if (wch != 64 && wch != 256) wch = 128;
+        }
+        if (wch == 256 && (int)cfg.gridDim.x > PENCIL_NUM_SMS * 6) cfg.gridDim = dim3(PENCIL_NUM_SMS * 6);
+#define CSR_LAUNCH(A, W) \
+    cudaLaunchKernelEx(&cfg, csr_stream_kernel<A, W>, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, status)
+        if (assoc) e = wch == 64 ? CSR_LAUNCH(true, 64) : (wch == 256 ? CSR_LAUNCH(true, 256) : CSR_LAUNCH(true, 128));
+        else e = wch == 64 ? CSR_LAUNCH(false, 64) : (wch == 256 ? CSR_LAUNCH(false, 256) : CSR_LAUNCH(false, 128));
+#undef CSR_LAUNCH
     }
     return (int)e;
 }
@@ -419,4 +430,12 @@ int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const
     return (int)cudaGetLastError();
 }
 
-int csr_tile_nnz() { return SPMV_TILE_NNZ; }
+int csr_tile_nnz() {  // PENCIL_SPMV_TILE overrides the plan window (tuning knob)
+    static int t = -1;
+    if (t < 0) {
+        const char* e = getenv("PENCIL_SPMV_TILE");
+        t = e ? atoi(e) : SPMV_TILE_NNZ;
+        if (t < 32) t = SPMV_TILE_NNZ;
+    }
+    return t;
+}
