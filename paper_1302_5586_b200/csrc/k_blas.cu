@@ -14,58 +14,89 @@
 #include "kernels.h"
 
 // ------------------------------------------------------------------ gemv
+// A warp owns two rows and streams them together (x loaded once for both): 8 x 16-byte A
+// loads in flight per lane.  CTA = 4 warps = 8 rows, <= 64 registers: at 8192 rows the whole
+// grid (1024 CTAs) is resident in ONE wave (7 CTAs/SM), so every SM streams ~55 rows to the end
+// instead of a second, mostly empty wave (the tail that capped the 1-row/warp kernel at 76%).
+#define GEMV_WARPS 4
+#define GEMV_ROWS_PER_WARP 2
 template <bool VEC>
-__global__ void __launch_bounds__(256) gemv_kernel(int m, int n, float alpha, float beta,
-                                                   const float* __restrict__ A,
-                                                   const float* __restrict__ x,
-                                                   float* __restrict__ y) {
+__global__ void __launch_bounds__(32 * GEMV_WARPS, 7) gemv_kernel(int m, int n, float alpha, float beta,
+                                                                  const float* __restrict__ A,
+                                                                  const float* __restrict__ x,
+                                                                  float* __restrict__ y) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long row = (long long)blockIdx.x * 8 + warp;
-    if (row >= m) return;
-    const float* a = A + row * (long long)n;
-    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+    const long long r0 = ((long long)blockIdx.x * GEMV_WARPS + warp) * GEMV_ROWS_PER_WARP;
+    if (r0 >= m) return;
+    const bool two = r0 + 1 < m;
+    const float* a0 = A + r0 * (long long)n;
+    const float* a1 = two ? a0 + n : a0;
+    float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f, q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
     if (VEC) {
-        const float4* a4 = reinterpret_cast<const float4*>(a);
         const float4* x4 = reinterpret_cast<const float4*>(x);
+        const float4* b0 = reinterpret_cast<const float4*>(a0);
+        const float4* b1 = reinterpret_cast<const float4*>(a1);
         const int n4 = n >> 2;
         int j = lane;
-        // 8 independent 16-byte loads in flight per lane
-        for (; j + 7 * 32 < n4; j += 8 * 32) {
-            float4 av[8], xv[8];
+        for (; j + 3 * 32 < n4; j += 4 * 32) {
+            float4 u0[4], u1[4], xv[4];
 #pragma unroll
-            for (int u = 0; u < 8; u++) av[u] = ld_stream_f4(a4 + j + u * 32);
+            for (int u = 0; u < 4; u++) u0[u] = ld_stream_f4(b0 + j + u * 32);
 #pragma unroll
-            for (int u = 0; u < 8; u++) xv[u] = __ldg(x4 + j + u * 32);
+            for (int u = 0; u < 4; u++) u1[u] = ld_stream_f4(b1 + j + u * 32);
 #pragma unroll
-            for (int u = 0; u < 8; u++) {
-                acc0 = fmaf(av[u].x, xv[u].x, acc0);
-                acc1 = fmaf(av[u].y, xv[u].y, acc1);
-                acc2 = fmaf(av[u].z, xv[u].z, acc2);
-                acc3 = fmaf(av[u].w, xv[u].w, acc3);
+            for (int u = 0; u < 4; u++) xv[u] = __ldg(x4 + j + u * 32);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                p0 = fmaf(u0[u].x, xv[u].x, p0);
+                p1 = fmaf(u0[u].y, xv[u].y, p1);
+                p2 = fmaf(u0[u].z, xv[u].z, p2);
+                p3 = fmaf(u0[u].w, xv[u].w, p3);
+                q0 = fmaf(u1[u].x, xv[u].x, q0);
+                q1 = fmaf(u1[u].y, xv[u].y, q1);
+                q2 = fmaf(u1[u].z, xv[u].z, q2);
+                q3 = fmaf(u1[u].w, xv[u].w, q3);
             }
         }
         for (; j < n4; j += 32) {
-            float4 av = ld_stream_f4(a4 + j), xv = __ldg(x4 + j);
-            acc0 = fmaf(av.x, xv.x, acc0);
-            acc1 = fmaf(av.y, xv.y, acc1);
-            acc2 = fmaf(av.z, xv.z, acc2);
-            acc3 = fmaf(av.w, xv.w, acc3);
+            const float4 v0 = ld_stream_f4(b0 + j), v1 = ld_stream_f4(b1 + j), xv = __ldg(x4 + j);
+            p0 = fmaf(v0.x, xv.x, p0);
+            p1 = fmaf(v0.y, xv.y, p1);
+            p2 = fmaf(v0.z, xv.z, p2);
+            p3 = fmaf(v0.w, xv.w, p3);
+            q0 = fmaf(v1.x, xv.x, q0);
+            q1 = fmaf(v1.y, xv.y, q1);
+            q2 = fmaf(v1.z, xv.z, q2);
+            q3 = fmaf(v1.w, xv.w, q3);
         }
-        for (int t = (n4 << 2) + lane; t < n; t += 32) acc0 = fmaf(a[t], __ldg(x + t), acc0);
+        for (int t = (n4 << 2) + lane; t < n; t += 32) {
+            const float xt = __ldg(x + t);
+            p0 = fmaf(a0[t], xt, p0);
+            q0 = fmaf(a1[t], xt, q0);
+        }
     } else {
-        for (int t = lane; t < n; t += 32) acc0 = fmaf(ld_stream_f(a + t), __ldg(x + t), acc0);
+        for (int t = lane; t < n; t += 32) {
+            const float xt = __ldg(x + t);
+            p0 = fmaf(ld_stream_f(a0 + t), xt, p0);
+            q0 = fmaf(ld_stream_f(a1 + t), xt, q0);
+        }
     }
-    float s = warp_sum<32>((acc0 + acc1) + (acc2 + acc3));
-    if (lane == 0) y[row] = alpha * s + beta * y[row];
+    const float s0 = warp_sum<32>((p0 + p1) + (p2 + p3));
+    const float s1 = warp_sum<32>((q0 + q1) + (q2 + q3));
+    if (lane == 0) {
+        y[r0] = alpha * s0 + beta * y[r0];
+        if (two) y[r0 + 1] = alpha * s1 + beta * y[r0 + 1];
+    }
 }
 
 int launch_gemv(cudaStream_t st, int m, int n, float alpha, float beta, const float* A,
                 const float* x, float* y) {
     if (m <= 0) return 0;
     bool vec = (n % 4 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)x % 16 == 0);
-    dim3 grid((m + 7) / 8);
-    if (vec) gemv_kernel<true><<<grid, 256, 0, st>>>(m, n, alpha, beta, A, x, y);
-    else gemv_kernel<false><<<grid, 256, 0, st>>>(m, n, alpha, beta, A, x, y);
+    const int rows_per_cta = GEMV_WARPS * GEMV_ROWS_PER_WARP;
+    dim3 grid((m + rows_per_cta - 1) / rows_per_cta);
+    if (vec) gemv_kernel<true><<<grid, 32 * GEMV_WARPS, 0, st>>>(m, n, alpha, beta, A, x, y);
+    else gemv_kernel<false><<<grid, 32 * GEMV_WARPS, 0, st>>>(m, n, alpha, beta, A, x, y);
     return (int)cudaGetLastError();
 }
 
