@@ -25,8 +25,13 @@
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 32;  // BK fp32 = 128 bytes = one swizzle-128B row
-constexpr int STAGES = 2;
+// BK fp32 per stage: 16 -> 64-byte operand rows (swizzle-64B), 4 stages of 48 KB in flight;
+// (BK 32 / swizzle-128B fits only 2 stages of 96 KB: measured 83% tensor-pipe activity)
+constexpr int BM = 128, BN = 256, BK = 16;
+constexpr int STAGES = 4;
+constexpr int ROW_BYTES = BK * 4;
+constexpr int ATOM_BYTES = 8 * ROW_BYTES;  // 8-row swizzle atom
+constexpr unsigned long long SW_LAYOUT = ROW_BYTES == 128 ? 2 : (ROW_BYTES == 64 ? 4 : 6);  // UMMA layout type
 constexpr int A_TILE = BM * BK * 4;  // 16 KB
 constexpr int B_TILE = BN * BK * 4;  // 32 KB
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
@@ -61,14 +66,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
-// K-major, 128-byte-swizzled operand tile: 8-row x 128 B swizzle atoms stacked every 1024 B
+// K-major, ROW_BYTES-swizzled operand tile: 8-row swizzle atoms stacked every ATOM_BYTES
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;            // leading byte offset (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset: next 8-row atom
-    d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+    d |= (uint64_t)1 << 16;                   // leading byte offset (unused for swizzled K-major)
+    d |= (uint64_t)(ATOM_BYTES >> 4) << 32;   // stride byte offset: next 8-row atom
+    d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+    d |= (uint64_t)SW_LAYOUT << 61;           // SWIZZLE_64B / 128B
     return d;
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -227,6 +232,21 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __global__ void split_rows_kernel(const float* __restrict__ A, int rows, int K, int Kp,
                                   float* __restrict__ hi, float* __restrict__ lo) {
     const long long total = (long long)rows * Kp;
+    if (K == Kp && ((uintptr_t)A & 15) == 0) {  // no padding: straight float4 stream
+        const long long t4 = total >> 2;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < t4;
+             i += (long long)gridDim.x * blockDim.x) {
+            const float4 x = ld_stream_f4(reinterpret_cast<const float4*>(A) + i);
+            float4 h, l;
+            h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+            h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+            h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+            h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+            reinterpret_cast<float4*>(hi)[i] = h;
+            reinterpret_cast<float4*>(lo)[i] = l;
+        }
+        return;
+    }
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const long long r = i / Kp;
@@ -284,7 +304,9 @@ bool make_map(CUtensorMap* m, const float* base, int rows, int Kp, int box_rows)
     cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE,
+               ROW_BYTES == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
