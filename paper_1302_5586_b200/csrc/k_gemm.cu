@@ -312,6 +312,191 @@ bool make_map(CUtensorMap* m, const float* base, int rows, int Kp, int box_rows)
 
 size_t kpad(int k) { return ((size_t)(k > 0 ? k : 1) + BK - 1) / BK * BK; }
 
+// ---------------------------------------------------------------- 2-SM (CTA pair) variant
+// A cluster of 2 CTAs owns a 256 x 256 output tile; tcgen05.mma.cta_group::2 (M = 256) issued
+// by the leader CTA reads A rows 0-127 / 128-255 and B columns 0-127 / 128-255 from the two
+// CTAs' shared memory at the same offsets, so each SM streams half of B: per MMA 8 KB of smem
+// operand reads per SM instead of 12 KB (the 1-SM kernel's tensor pipe idled ~17% on that).
+// Each CTA TMA-loads its own halves; completion is counted on the leader's `full` barrier (the
+// peer-bit-cleared address); the leader's tcgen05.commit multicasts to both CTAs' `empty` and
+// `accum` barriers.  Each CTA's epilogue drains its own TMEM (its 128 rows x 256 columns).
+constexpr int P_BN_HALF = 128;                        // B rows (N) per CTA
+constexpr int P_B_TILE = P_BN_HALF * BK * 4;
+constexpr int P_STAGE_BYTES = 2 * A_TILE + 2 * P_B_TILE;  // per CTA
+constexpr int P_STAGES = 6;
+#ifndef P_GROUP_M_DEF
+#define P_GROUP_M_DEF 2  // swept 2/4/8 at 16384^3: 36.6 / 36.8 / 39.2 ms (tools/gemm_group_probe.sh)
+#endif
+constexpr int P_GROUP_M = P_GROUP_M_DEF;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr uint32_t P_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar_leader, int c0,
+                                                int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mma_tf32_2sm(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                             uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1) gemm_3xtf32_2sm_kernel(
+    const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+    const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo, int M, int N,
+    int Kp, float alpha, float beta, float* __restrict__ C) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + P_STAGES * P_STAGE_BYTES);
+    uint64_t* empty = full + P_STAGES;
+    uint64_t* accum = empty + P_STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cta_rank();
+    const bool leader = rank == 0;
+    const int tiles_m = (M + 255) / 256, tiles_n = (N + BN - 1) / BN;
+    const int tid = blockIdx.x >> 1;  // cluster index
+    constexpr int G = P_GROUP_M;      // raster group in 256-row tiles
+    const int group = tid / (G * tiles_n);
+    const int first_m = group * G;
+    const int gsize = min(tiles_m - first_m, G);
+    const int tm = first_m + (tid % (G * tiles_n)) % gsize;
+    const int tn = (tid % (G * tiles_n)) / gsize;
+    const int m0 = tm * 256 + (int)rank * 128;          // this CTA's A rows / output rows
+    const int nb = tn * BN + (int)rank * P_BN_HALF;     // this CTA's B half
+    const int n0 = tn * BN;
+    const int nk = Kp / BK;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < P_STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_ahi) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_alo) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_bhi) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_blo) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer CTA
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer (both CTAs); bytes land on the leader's full barrier
+            for (int kb = 0; kb < nk; kb++) {
+                const int s = kb % P_STAGES;
+                mbar_wait(&empty[s], ((kb / P_STAGES) & 1) ^ 1);
+                uint8_t* st = smem + s * P_STAGE_BYTES;
+                const uint32_t bar = smem_u32(&full[s]) & 0xFEFFFFFFu;
+                if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);
+                tma_load_2d_2sm(st, &tm_ahi, bar, kb * BK, m0);
+                tma_load_2d_2sm(st + A_TILE, &tm_alo, bar, kb * BK, m0);
+                tma_load_2d_2sm(st + 2 * A_TILE, &tm_bhi, bar, kb * BK, nb);
+                tma_load_2d_2sm(st + 2 * A_TILE + P_B_TILE, &tm_blo, bar, kb * BK, nb);
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {  // MMA issuer (leader only)
+            for (int kb = 0; kb < nk; kb++) {
+                const int s = kb % P_STAGES;
+                mbar_wait(&full[s], (kb / P_STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sa = smem_u32(smem + s * P_STAGE_BYTES);
+                const uint64_t ahi = umma_desc_sw128(sa), alo = umma_desc_sw128(sa + A_TILE);
+                const uint64_t bhi = umma_desc_sw128(sa + 2 * A_TILE), blo = umma_desc_sw128(sa + 2 * A_TILE + P_B_TILE);
+#pragma unroll
+                for (int ks = 0; ks < BK / 8; ks++) {
+                    const uint64_t off = (uint64_t)(ks * 32) >> 4;
+                    const uint32_t first = (kb | ks) != 0;
+                    mma_tf32_2sm(tmem, alo + off, bhi + off, P_IDESC, first);
+                    mma_tf32_2sm(tmem, ahi + off, blo + off, P_IDESC, 1);
+                    mma_tf32_2sm(tmem, ahi + off, bhi + off, P_IDESC, 1);
+                }
+                mma_commit_2sm(&empty[s]);  // frees the stage in BOTH CTAs once read
+            }
+            mma_commit_2sm(accum);
+        }
+    } else {
+        const int q = warp & 3;
+        mbar_wait(accum, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int row = m0 + q * 32 + lane;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (row < M) {
+                float* crow = C + (long long)row * N + n0 + c0;
+                const int ncols = min(32, N - (n0 + c0));
+                if (ncols == 32 && ((uintptr_t)crow & 15) == 0) {
+#pragma unroll
+                    for (int v = 0; v < 8; v++) {
+                        float4 o;
+                        float4 old = beta != 0.f ? *reinterpret_cast<const float4*>(crow + 4 * v)
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+                        o.x = alpha * __uint_as_float(r[4 * v + 0]) + beta * old.x;
+                        o.y = alpha * __uint_as_float(r[4 * v + 1]) + beta * old.y;
+                        o.z = alpha * __uint_as_float(r[4 * v + 2]) + beta * old.z;
+                        o.w = alpha * __uint_as_float(r[4 * v + 3]) + beta * old.w;
+                        *reinterpret_cast<float4*>(crow + 4 * v) = o;
+                    }
+                } else {
+                    for (int v = 0; v < ncols; v++)
+                        crow[v] = alpha * __uint_as_float(r[v]) + (beta != 0.f ? beta * crow[v] : 0.f);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncwarp();        // producer / issuer lanes rejoin their warps before the aligned barrier
+    cluster_sync_all();  // both CTAs done with TMEM and with each other's barriers
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
 }  // namespace
 
 size_t gemm_workspace_bytes(int m, int n, int k) {
@@ -335,14 +520,28 @@ int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, c
         dim3 g((Kp + 31) / 32, (n + 31) / 32);
         split_transpose_kernel<<<g, dim3(32, 8), 0, st>>>(B, k, n, Kp, bhi, blo);
     }
+    // CTA-pair kernel by default (PENCIL_GEMM_2SM=0 selects the single-CTA kernel)
+    static int two_sm = -1;
+    if (two_sm < 0) {
+        const char* e = getenv("PENCIL_GEMM_2SM");
+        two_sm = !(e && e[0] == '0');
+    }
     CUtensorMap maps[4];
+    const int b_box = two_sm ? P_BN_HALF : BN;
     if (!make_map(&maps[0], ahi, m, Kp, BM) || !make_map(&maps[1], alo, m, Kp, BM) ||
-        !make_map(&maps[2], bhi, n, Kp, BN) || !make_map(&maps[3], blo, n, Kp, BN))
+        !make_map(&maps[2], bhi, n, Kp, b_box) || !make_map(&maps[3], blo, n, Kp, b_box))
         return (int)cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(gemm_3xtf32_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
         attr = true;
+    }
+    if (two_sm) {
+        const int clusters = ((m + 255) / 256) * ((n + BN - 1) / BN);
+        gemm_3xtf32_2sm_kernel<<<2 * clusters, GEMM_THREADS, P_SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3],
+                                                                               m, n, Kp, alpha, beta, C);
+        return (int)cudaGetLastError();
     }
     const int tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
     gemm_3xtf32_kernel<<<tiles, GEMM_THREADS, SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], m, n, Kp,
