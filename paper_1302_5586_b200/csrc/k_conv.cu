@@ -167,8 +167,9 @@ __global__ void conv5x5_f32_simple(int h, int w, const float* __restrict__ img,
     }
 }
 
-int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const float* k25,
-                       float* out) {
+// fallback for layouts the smem-ring kernel (k_stencil.cu) does not take
+int launch_conv5x5_f32_reg(cudaStream_t st, int h, int w, const float* img, const float* k25,
+                           float* out) {
     if (h < 5 || w < 5) return 0;
     TapsF k;
     for (int t = 0; t < 25; t++) k.k[t] = k25[t];

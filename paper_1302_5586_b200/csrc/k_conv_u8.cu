@@ -286,7 +286,8 @@ int launch_u8(cudaStream_t st, int h, int w, int scale, const typename Pix<I32>:
 
 }  // namespace
 
-int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, const int* k25, int* out) {
+// fallback for layouts the smem-ring kernel (k_stencil.cu) does not take
+int launch_conv5x5_u8_reg(cudaStream_t st, int h, int w, int scale, const int* img, const int* k25, int* out) {
     return launch_u8<true>(st, h, w, scale, img, k25, out);
 }
 
