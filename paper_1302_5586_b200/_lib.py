@@ -7,7 +7,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpencil_b200.so")
+# PENCIL_B200_LIB: load another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("PENCIL_B200_LIB") or os.path.join(_HERE, "lib", "libpencil_b200.so")
 SYNTH_PATH = os.path.join(_HERE, "lib", "libpencil_synth.so")
 
 c_int, c_ll, c_float, c_double, c_void_p, c_char_p = (

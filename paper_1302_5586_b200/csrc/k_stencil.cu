@@ -14,6 +14,7 @@
 //   U8   conv5x5_u8 on int32 storage: clamp-to-edge; integer sums on the fp32 pipe (exact for
 //        pixels in [0, 255] and |k| <= 657); a warp-row whose window holds a non-byte value (or
 //        a launch with larger taps) takes the exact int64 path from global memory.
+#include <cmath>
 #include <cstring>
 
 #include "common.cuh"
@@ -23,7 +24,10 @@ namespace {
 
 constexpr int S_WARPS = 4;
 constexpr int S_BAND = 64;
-constexpr int S_RING = 8;    // rows per warp ring
+#ifndef STENCIL_RING
+#define STENCIL_RING 8
+#endif
+constexpr int S_RING = STENCIL_RING;  // rows per warp ring
 constexpr int S_ROWE = 136;  // ring row: columns [c0 - 4, c0 + 132)
 typedef unsigned long long u64;
 
@@ -43,6 +47,11 @@ __device__ __forceinline__ u64 f2fma(u64 a, u64 b, u64 c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
+__device__ __forceinline__ u64 f2fma_rm(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
 __device__ __forceinline__ void cp16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
@@ -56,6 +65,8 @@ struct StencilArgs {
     float kf[25];              // taps as fp32 (exact small integers for U8)
     long long ki[25];          // int taps for the exact U8 path
     u64 negz, one;             // runtime (-0, -0) and (1, 1) for the F32 exact rounding
+    u64 negmag;                // runtime (-2^23, -2^23): U8 int -> float
+    u64 inv_scale, half_scaled, magic2;  // U8 pow2 scale: 2^-shift, (scale/2) * 2^-shift, 1.5 * 2^23
     int scale, shift;          // U8: scale, shift >= 0 when scale = 1 << shift
     unsigned long long magic;  // U8: ceil(2^64 / scale)
     int exact_only;            // U8: taps too large for the fp32 path
@@ -88,58 +99,81 @@ struct Pol<true> {
     typedef int T;
 };
 
-template <bool U8>
-__device__ __forceinline__ void ring_issue(const typename Pol<U8>::T* __restrict__ img, int h, int w, int r, int c0,
-                                           int lane, typename Pol<U8>::T* slot) {
-    const int rr = U8 ? clampi(r, 0, h - 1) : r;
-    const typename Pol<U8>::T* src = img + (long long)rr * w;
+// Per-lane copy plan, fixed for the whole sweep: lane l copies columns c..c+3 (c = c0 + 4l) of
+// a row to ring index 4 + 4l; lane 0 also copies the 4-column left halo (ring index 0) and lane
+// 31 the right halo (ring index 132) — one extra 16-byte copy at offset `hdir` * 4.
+struct RingLane {
+    bool body;  // c + 3 < w
+    bool halo;  // lane 0 with c0 >= 4, or lane 31 with c0 + 131 < w
+    int hdir;   // -1 (left halo) or +1 (right halo)
+};
+__device__ __forceinline__ RingLane ring_lane(int w, int c0, int lane) {
+    RingLane L;
     const int c = c0 + 4 * lane;
-    if (c + 3 < w) cp16(slot + 4 + 4 * lane, src + c);
-    if (lane == 0 && c0 >= 4) cp16(slot, src + c0 - 4);
-    if (lane == 31 && c0 + 131 < w) cp16(slot + 132, src + c0 + 128);
+    L.body = c + 3 < w;
+    L.halo = (lane == 0 && c0 >= 4) || (lane == 31 && c0 + 131 < w);
+    L.hdir = lane == 0 ? -1 : 1;
+    return L;
+}
+// src = &img[row][c0 + 4 * lane]
+template <typename T>
+__device__ __forceinline__ void ring_issue(const T* src, const RingLane& L, int lane, T* slot) {
+    T* dst = slot + 4 + 4 * lane;
+    if (L.body) cp16(dst, src);
+    if (L.halo) cp16(dst + 4 * L.hdir, src + 4 * L.hdir);
 }
 
-// window row entering the register window: pixel pairs E[m] = (e[m], e[m+2]), e[m] = column
-// c-2+m (clamped for U8); returns whether any value is outside [0, 255] (U8)
+// Window row entering the register window, as packed pixel-pair operands for FFMA2; e[m] =
+// column c-2+m (clamped for U8).
+//   F32: 7 pairs P[m] = (e[m], e[m+1]); the lane's pixel pair (c, c+1) takes tap dj from P[dj],
+//        pair (c+2, c+3) from P[dj+2].  The even pairs come straight from the 8-byte-aligned
+//        ring reads; the odd pairs (P[1], P[3], P[5]) share every value with an even pair, so
+//        they are produced by an FFMA2 (x * 1 + -0, exact) into registers of their own — a plain
+//        pack is rematerialised by ptxas at every use (~40 MOVs per output row).
+//   U8:  6 pairs P[m] = (e[m], e[m+2]) for pixel pairs (c, c+2) and (c+1, c+3) (taps P[dj],
+//        P[dj+1]); each pair is converted int -> float by its own LOP3s + one FFMA2, so it lands
+//        in fresh registers too.  `orv` collects every value read (non-byte check).
 template <bool U8>
-__device__ __forceinline__ bool ring_read(const typename Pol<U8>::T* slot, int w, int c0, int lane, u64 (&E)[6]) {
+__device__ __forceinline__ void ring_read(const typename Pol<U8>::T* slot, int w, int c0, int lane,
+                                          const StencilArgs& a, u64 (&P)[7], unsigned& orv) {
     const int c = c0 + 4 * lane;
     // columns c-2 .. c+5 sit at ring index 4*lane+2 .. 4*lane+9: 8 B + 16 B + 8 B aligned reads
-    typename Pol<U8>::T v[8];
     const typename Pol<U8>::T* p = slot + 4 * lane + 2;
+    u64 q[4];
+    q[0] = *reinterpret_cast<const u64*>(p);
     {
-        const uint2 l = *reinterpret_cast<const uint2*>(p);
-        const uint4 mid = *reinterpret_cast<const uint4*>(p + 2);
-        const uint2 r = *reinterpret_cast<const uint2*>(p + 6);
-        const unsigned u[8] = {l.x, l.y, mid.x, mid.y, mid.z, mid.w, r.x, r.y};
-#pragma unroll
-        for (int m = 0; m < 8; m++) memcpy(&v[m], &u[m], 4);
+        const ulonglong2 mid = *reinterpret_cast<const ulonglong2*>(p + 2);
+        q[1] = mid.x;
+        q[2] = mid.y;
     }
-    if (U8 && (c0 == 0 || c0 + 132 > w)) {  // image-edge strips: clamp-to-edge columns
-#pragma unroll
-        for (int m = 0; m < 8; m++) {
-            const int col = c - 2 + m;
-            if (col < 0 || col > w - 1) v[m] = slot[clampi(col, 0, w - 1) - (c0 - 4)];
-        }
-    }
-    float f[8];
-    bool bad = false;
+    q[3] = *reinterpret_cast<const u64*>(p + 6);
     if (U8) {
-        int orv = 0;
+        unsigned v[8];
 #pragma unroll
-        for (int m = 0; m < 8; m++) {
-            const int iv = (int)v[m];
-            orv |= iv;
-            f[m] = __int_as_float((iv & 255) | 0x4B000000) - 8388608.f;  // exact int -> float
+        for (int m = 0; m < 4; m++) {
+            v[2 * m] = (unsigned)q[m];
+            v[2 * m + 1] = (unsigned)(q[m] >> 32);
         }
-        bad = (orv & ~255) != 0;
+        if (c0 == 0 || c0 + 132 > w) {  // image-edge strips: clamp-to-edge columns
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const int col = c - 2 + m;
+                if (col < 0 || col > w - 1) v[m] = (unsigned)slot[clampi(col, 0, w - 1) - (c0 - 4)];
+            }
+        }
+        orv |= (v[0] | v[1] | v[2]) | (v[3] | v[4] | v[5]) | (v[6] | v[7]);
+        // exact int -> float: bits (v & 255) | 0x4B000000 are 2^23 + v; the FFMA2 subtracts 2^23
+#pragma unroll
+        for (int m = 0; m < 6; m++) {
+            const u64 bits = ((u64)((v[m + 2] & 255u) | 0x4B000000u) << 32) | ((v[m] & 255u) | 0x4B000000u);
+            P[m] = f2fma(bits, a.one, a.negmag);
+        }
     } else {
 #pragma unroll
-        for (int m = 0; m < 8; m++) f[m] = (float)v[m];
-    }
+        for (int m = 0; m < 4; m++) P[2 * m] = q[m];
 #pragma unroll
-    for (int m = 0; m < 6; m++) E[m] = f2pk(f[m], f[m + 2]);
-    return bad;
+        for (int m = 0; m < 3; m++) P[2 * m + 1] = f2fma((q[m] >> 32) | (q[m + 1] << 32), a.one, a.negz);
+    }
 }
 
 template <bool U8>
@@ -155,119 +189,145 @@ __device__ __forceinline__ unsigned pixel_exact(const int* __restrict__ img, int
     return sat_div(acc, a);
 }
 
+// Sweep state advanced by one row per step: `src` points at the lane's columns of the next row
+// to enter the ring (rows past the image bottom clamp to `src_last` for U8), `dst` at the
+// lane's columns of the output row.
+template <typename T>
+struct Sweep {
+    const T* src;
+    const T* src_last;
+    T* dst;
+    long long w;
+};
+
 template <bool U8, int S, bool POW2>
-__device__ __forceinline__ void stencil_step(const typename Pol<U8>::T* __restrict__ img,
-                                             typename Pol<U8>::T* __restrict__ out, int h, int w, int i, int c0,
-                                             int lane, int r_end, typename Pol<U8>::T (*ring)[S_ROWE], u64 (&W)[5][6],
-                                             unsigned& badmask, const StencilArgs& a) {
+__device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int r_end, const RingLane& L,
+                                             typename Pol<U8>::T (*ring)[S_ROWE], u64 (&W)[5][7],
+                                             Sweep<typename Pol<U8>::T>& sw, unsigned& orv,
+                                             const StencilArgs& a) {
+    typedef typename Pol<U8>::T T;
     // the ring holds rows i+2 .. i+2+S_RING-1 in flight; the oldest (row i+2) must have landed
     cp_wait<S_RING - 1>();
     __syncwarp();
-    typename Pol<U8>::T* slot = ring[(i + 2) % S_RING];
-    const bool b = ring_read<U8>(slot, w, c0, lane, W[S]);
-    if (U8) badmask = (badmask & ~(1u << S)) | ((unsigned)b << S);
+    T* slot = ring[(i + 2) % S_RING];
+    ring_read<U8>(slot, w, c - 4 * lane, lane, a, W[S], orv);
     __syncwarp();
-    if (i + 2 + S_RING < r_end) ring_issue<U8>(img, h, w, i + 2 + S_RING, c0, lane, slot);
+    if (i + 2 + S_RING < r_end) {
+        const T* src = sw.src;
+        if (U8 && src > sw.src_last) src = sw.src_last;  // clamp-to-edge rows below the image
+        ring_issue<T>(src, L, lane, slot);
+    }
     cp_commit();
+    sw.src += sw.w;
 
-    const int c = c0 + 4 * lane;
-    float o[4];
-    // a non-byte pixel in the window: flag the launch for the exact repair pass (u8_repair_kernel)
-    // and keep going — keeping the exact path out of this loop keeps it at 80 registers
-    if (U8 && __any_sync(0xffffffffu, badmask != 0) && lane == 0) atomicOr(a.repair_flag, 1u);
-    const bool exact = false;
-    if (!exact) {
-        u64 a02 = 0ull, a13 = 0ull;
+    u64 a01 = 0ull, a23 = 0ull;  // pixel pairs (c, c+1) and (c+2, c+3)
 #pragma unroll
-        for (int di = 0; di < 5; di++) {
-            const int sl = (S + 1 + di) % 5;
+    for (int di = 0; di < 5; di++) {
+        const int sl = (S + 1 + di) % 5;
 #pragma unroll
-            for (int dj = 0; dj < 5; dj++) {
-                const u64 kk = f2pk(a.kf[di * 5 + dj], a.kf[di * 5 + dj]);
-                if (U8) {  // exact integer sums: fused is fine
-                    a02 = f2fma(kk, W[sl][dj], a02);
-                    a13 = f2fma(kk, W[sl][dj + 1], a13);
-                } else {   // product and sum rounded separately, as written
-                    a02 = f2fma(f2fma(kk, W[sl][dj], a.negz), a.one, a02);
-                    a13 = f2fma(f2fma(kk, W[sl][dj + 1], a.negz), a.one, a13);
-                }
+        for (int dj = 0; dj < 5; dj++) {
+            const u64 kk = f2pk(a.kf[di * 5 + dj], a.kf[di * 5 + dj]);
+            if (U8) {  // exact integer sums: fused is fine
+                a01 = f2fma(kk, W[sl][dj], a01);      // pixels (c, c+2)
+                a23 = f2fma(kk, W[sl][dj + 1], a23);  // pixels (c+1, c+3)
+            } else {   // product and sum rounded separately, as written
+                a01 = f2fma(f2fma(kk, W[sl][dj], a.negz), a.one, a01);
+                a23 = f2fma(f2fma(kk, W[sl][dj + 2], a.negz), a.one, a23);
             }
         }
-        const float2 p02 = f2unpk(a02), p13 = f2unpk(a13);
-        o[0] = p02.x; o[1] = p13.x; o[2] = p02.y; o[3] = p13.y;
     }
-    typename Pol<U8>::T* orow = out + (long long)i * w;
+    T* orow = sw.dst;
+    sw.dst += sw.w;
     if (U8) {
         int v[4];
-        if (!exact) {
+        if (POW2) {
+            // (acc + scale/2) >> shift on the pair: t = (acc + scale/2) * 2^-shift is exact, and
+            // t + 1.5 * 2^23 rounded toward -inf holds floor(t) in its low mantissa bits
+            const float2 f02 = f2unpk(f2fma_rm(f2fma(a01, a.inv_scale, a.half_scaled), a.one, a.magic2));
+            const float2 f13 = f2unpk(f2fma_rm(f2fma(a23, a.inv_scale, a.half_scaled), a.one, a.magic2));
+            const float f[4] = {f02.x, f13.x, f02.y, f13.y};
+#pragma unroll
+            for (int t = 0; t < 4; t++) v[t] = __vimin_s32_relu(__float_as_int(f[t]) - 0x4B400000, 255);
+        } else {
+            const float2 p02 = f2unpk(a01), p13 = f2unpk(a23);
+            const float o[4] = {p02.x, p13.x, p02.y, p13.y};
 #pragma unroll
             for (int t = 0; t < 4; t++) {
                 const int acc = __float_as_int(__fadd_rn(o[t], 12582912.f)) - 0x4B400000;  // exact, |acc| < 2^22
-                if (POW2) {
-                    const int n = acc + (a.scale >> 1);
-                    v[t] = n < 0 ? 0 : min(n >> a.shift, 255);
-                } else {
-                    v[t] = (int)sat_div(acc, a);
-                }
+                v[t] = (int)sat_div(acc, a);
             }
         }
-        if (c + 3 < w) *reinterpret_cast<int4*>((int*)orow + c) = make_int4(v[0], v[1], v[2], v[3]);
-        else
-            for (int t = 0; t < 4; t++)
-                if (c + t < w) ((int*)orow)[c + t] = v[t];
+        if (L.body) *reinterpret_cast<int4*>((int*)orow) = make_int4(v[0], v[1], v[2], v[3]);
     } else {
+        const float2 p01 = f2unpk(a01), p23 = f2unpk(a23);
+        const float o[4] = {p01.x, p01.y, p23.x, p23.y};
         if (c >= 2 && c + 3 < w - 2) {
-            st_stream_f4(reinterpret_cast<float4*>((float*)orow + c), make_float4(o[0], o[1], o[2], o[3]));
+            st_stream_f4(reinterpret_cast<float4*>((float*)orow), make_float4(o[0], o[1], o[2], o[3]));
         } else {
 #pragma unroll
             for (int t = 0; t < 4; t++)
-                if (c + t >= 2 && c + t < w - 2) ((float*)orow)[c + t] = o[t];
+                if (c + t >= 2 && c + t < w - 2) ((float*)orow)[t] = o[t];
         }
     }
 }
 
+#ifndef STENCIL_F32_MINB
+#define STENCIL_F32_MINB 4
+#endif
+#ifndef STENCIL_U8_MINB
+#define STENCIL_U8_MINB 4
+#endif
 template <bool U8, bool POW2>
-__global__ void __launch_bounds__(32 * S_WARPS, U8 ? 5 : 6) stencil_ring_kernel(int h, int w,
-                                                                       const typename Pol<U8>::T* __restrict__ img,
-                                                                       typename Pol<U8>::T* __restrict__ out,
-                                                                       StencilArgs a) {
-    __shared__ __align__(16) typename Pol<U8>::T ring_all[S_WARPS][S_RING][S_ROWE];
+__global__ void __launch_bounds__(32 * S_WARPS, U8 ? STENCIL_U8_MINB : STENCIL_F32_MINB) stencil_ring_kernel(
+    int h, int w, const typename Pol<U8>::T* __restrict__ img, typename Pol<U8>::T* __restrict__ out, StencilArgs a) {
+    typedef typename Pol<U8>::T T;
+    __shared__ __align__(16) T ring_all[S_WARPS][S_RING][S_ROWE];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int strip = blockIdx.x * S_WARPS + warp;
     const int c0 = strip * 128;
     if (c0 >= w) return;
+    const int c = c0 + 4 * lane;
     // output rows [i0, i1); input rows [i0 - 2, i1 + 2)
     const int i0 = (U8 ? 0 : 2) + blockIdx.y * S_BAND;
     const int i1 = min(U8 ? h : h - 2, i0 + S_BAND);
     if (i0 >= i1) return;
     const int r_end = i1 + 2;
-    typename Pol<U8>::T(*ring)[S_ROWE] = ring_all[warp];
+    const RingLane L = ring_lane(w, c0, lane);
+    T(*ring)[S_ROWE] = ring_all[warp];
+    auto row_src = [&](int r) { return img + (long long)(U8 ? clampi(r, 0, h - 1) : r) * w + c; };
 #pragma unroll
     for (int d = 0; d < S_RING; d++) {  // prologue: rows i0-2 .. i0+5 in flight
-        if (i0 - 2 + d < r_end) ring_issue<U8>(img, h, w, i0 - 2 + d, c0, lane, ring[(i0 - 2 + d + S_RING) % S_RING]);
+        if (i0 - 2 + d < r_end) ring_issue<T>(row_src(i0 - 2 + d), L, lane, ring[(i0 - 2 + d + S_RING) % S_RING]);
         cp_commit();
     }
-    u64 W[5][6];
-    unsigned badmask = 0;
+    u64 W[5][7];
+    unsigned orv = 0;
 #pragma unroll
     for (int d = 0; d < 4; d++) {  // rows i0-2 .. i0+1 into the window, slots refilled
         cp_wait<S_RING - 1>();
         __syncwarp();
-        typename Pol<U8>::T* slot = ring[(i0 - 2 + d + S_RING) % S_RING];
-        const bool b = ring_read<U8>(slot, w, c0, lane, W[d]);
-        if (U8) badmask |= (unsigned)b << d;
+        T* slot = ring[(i0 - 2 + d + S_RING) % S_RING];
+        ring_read<U8>(slot, w, c0, lane, a, W[d], orv);
         __syncwarp();
-        if (i0 - 2 + d + S_RING < r_end) ring_issue<U8>(img, h, w, i0 - 2 + d + S_RING, c0, lane, slot);
+        if (i0 - 2 + d + S_RING < r_end) ring_issue<T>(row_src(i0 - 2 + d + S_RING), L, lane, slot);
         cp_commit();
     }
+    Sweep<T> sw;
+    sw.w = w;
+    sw.src_last = img + (long long)(h - 1) * w + c;
+    sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;  // next row to enter the ring: i0 + 2 + S_RING
+    sw.dst = out + (long long)i0 * w + c;
     for (int i = i0; i < i1; i += 5) {
-        stencil_step<U8, 4, POW2>(img, out, h, w, i, c0, lane, r_end, ring, W, badmask, a);
-        if (i + 1 < i1) stencil_step<U8, 0, POW2>(img, out, h, w, i + 1, c0, lane, r_end, ring, W, badmask, a);
-        if (i + 2 < i1) stencil_step<U8, 1, POW2>(img, out, h, w, i + 2, c0, lane, r_end, ring, W, badmask, a);
-        if (i + 3 < i1) stencil_step<U8, 2, POW2>(img, out, h, w, i + 3, c0, lane, r_end, ring, W, badmask, a);
-        if (i + 4 < i1) stencil_step<U8, 3, POW2>(img, out, h, w, i + 4, c0, lane, r_end, ring, W, badmask, a);
+        stencil_step<U8, 4, POW2>(w, i, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 1 < i1) stencil_step<U8, 0, POW2>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 2 < i1) stencil_step<U8, 1, POW2>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 3 < i1) stencil_step<U8, 2, POW2>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 4 < i1) stencil_step<U8, 3, POW2>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a);
     }
     cp_wait<0>();
+    // a non-byte pixel anywhere in the sweep: flag the launch for the exact repair pass
+    // (u8_repair_kernel), which recomputes the whole image in int64
+    if (U8 && __any_sync(0xffffffffu, (orv & ~255u) != 0) && lane == 0) atomicOr(a.repair_flag, 1u);
 }
 
 // exact int64 repair pass for conv5x5_u8 on int32 storage: runs after the fast kernel and
@@ -306,6 +366,7 @@ int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const fl
     for (int t = 0; t < 25; t++) a.kf[t] = k25[t];
     a.negz = pack2(-0.0f);
     a.one = pack2(1.0f);
+    a.negmag = pack2(-8388608.0f);
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h - 4 + S_BAND - 1) / S_BAND);
     stencil_ring_kernel<false, false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     return (int)cudaGetLastError();
@@ -322,11 +383,17 @@ int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, 
         small &= (k25[t] >= -657 && k25[t] <= 657);  // |acc| <= 25 * 255 * 657 < 2^22
     }
     a.exact_only = small ? 0 : 1;
+    a.negz = pack2(-0.0f);
+    a.one = pack2(1.0f);
+    a.negmag = pack2(-8388608.0f);
     a.scale = scale;
     a.shift = -1;
     if (scale > 0 && (scale & (scale - 1)) == 0) {
         a.shift = 0;
         while ((1 << a.shift) != scale) a.shift++;
+        a.inv_scale = pack2(ldexpf(1.0f, -a.shift));
+        a.half_scaled = pack2((float)(scale >> 1) * ldexpf(1.0f, -a.shift));
+        a.magic2 = pack2(12582912.0f);
     } else if (scale >= 2) {
         a.magic = ~0ull / (unsigned long long)scale + 1;
     }
