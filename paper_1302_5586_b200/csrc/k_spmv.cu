@@ -379,7 +379,9 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     // executor: all-LSU (default; 1.34 ms at 2^24 rows) or the TMA-fed stream
     // (PENCIL_SPMV_KERNEL=tma; 1.87 ms — 512-byte bulk copies cost more than they free).
     // Also measured and dropped: a 3-stage software-pipelined LSU variant (1.41 ms — more
-    // gathers in flight, but the chunk/batch merge doubled the instruction count).
+    // gathers in flight, but the chunk/batch merge doubled the instruction count), and a
+    // cp.async double-buffered col/val prefetch (2.43 ms: MIO-throttled, 16-B LDGSTS per lane
+    // plus the smem re-read of col/val saturate the MIO queue the gathers also need).
     static int use_tma = -1;
     if (use_tma < 0) {
         const char* e = getenv("PENCIL_SPMV_KERNEL");
