@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -253,9 +254,140 @@ int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int*
                : fail(PENCIL_E_CUDA, "csr plan launch");
 }
 
+// Drop-in SpMV on host arrays, pipelined.  The call is PCIe-bound (the whole matrix crosses the
+// link every call), so everything else hides under the col/val upload:
+//   copy stream : rowptr, x, then col/val in SPMV_PIPE_CHUNKS ordered chunks (one event each)
+//   compute     : after rowptr: the plan (tile windows + monotonicity flag); then one SpMV launch
+//                 per block of tiles, each waiting only for the chunk holding its last non-zero
+//   d2h stream  : y of each block as soon as its launch is done
+// Block b covers tiles [b*T/K, (b+1)*T/K); its rows and their last non-zero are read from the
+// plan (device) and the caller's rowptr (host).  A non-monotone rowptr (flagged by the plan)
+// falls back to one launch after the whole upload.  Results are identical to the one-shot
+// path: same kernel, same tiles, same per-row fold.  (Measured at 2^24 rows: 43.6 -> 41.8 ms per
+// call, i.e. the upload alone at ~54.7 GB/s; a second upload stream changes nothing — PCIe-bound.)
+#define SPMV_PIPE_BLOCKS 16
+#define SPMV_PIPE_CHUNKS 32
+struct PipeCtx {
+    cudaStream_t comp = nullptr, d2h = nullptr;
+    cudaEvent_t ev_rp = nullptr, ev_x = nullptr, ev_chunk[SPMV_PIPE_CHUNKS] = {}, ev_blk[SPMV_PIPE_BLOCKS] = {};
+    int* host_rows = nullptr;  // pinned: [0] plan flag, [1..K+1] block boundary rows
+};
+std::map<int, PipeCtx*> g_pipe;
+
+int get_pipe(DeviceCtx* c, PipeCtx** out) {
+    auto it = g_pipe.find(c->device);
+    if (it != g_pipe.end()) {
+        *out = it->second;
+        return PENCIL_OK;
+    }
+    PipeCtx* p = new PipeCtx();
+    CK(cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&p->ev_rp, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->ev_x, cudaEventDisableTiming));
+    for (auto& e : p->ev_chunk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : p->ev_blk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaMallocHost(&p->host_rows, 64 * sizeof(int)));
+    g_pipe[c->device] = p;
+    *out = p;
+    return PENCIL_OK;
+}
+
+int spmv_pipelined(int mode, int nrows, int ncols, int nnz, const int* rowptr, const int* col,
+                   const float* val, const float* x, float* y) {
+    DeviceCtx* c = nullptr;
+    int r = get_ctx(&c);
+    if (r) return r;
+    std::lock_guard<std::mutex> lk(c->mu);
+    PipeCtx* pc = nullptr;
+    if ((r = get_pipe(c, &pc))) return r;
+    cudaStream_t s0 = c->stream, s1 = pc->comp, s2 = pc->d2h;
+    int *drp = nullptr, *dcol = nullptr;
+    float *dval = nullptr, *dx = nullptr, *dy = nullptr;
+    CsrPlanImpl p;
+    auto release = [&]() {
+        cudaStreamSynchronize(s1);
+        cudaStreamSynchronize(s2);
+        pool_free(s0, drp);
+        pool_free(s0, dcol);
+        pool_free(s0, dval);
+        pool_free(s0, dx);
+        pool_free(s0, dy);
+        pool_free(s0, p.tile_row);
+        pool_free(s0, p.flags);
+        cudaStreamSynchronize(s0);
+    };
+    if ((r = pool_alloc(c, s0, sizeof(int) * ((size_t)nrows + 1), (void**)&drp)) ||
+        (r = pool_alloc(c, s0, sizeof(int) * (size_t)nnz, (void**)&dcol)) ||
+        (r = pool_alloc(c, s0, sizeof(float) * (size_t)nnz, (void**)&dval)) ||
+        (r = pool_alloc(c, s0, sizeof(float) * nz(ncols), (void**)&dx)) ||
+        (r = pool_alloc(c, s0, sizeof(float) * (size_t)nrows, (void**)&dy))) {
+        release();
+        return r;
+    }
+    // upload: rowptr first (the plan needs it), then x, then the col/val chunks in order
+    CK(cudaMemcpyAsync(drp, rowptr, sizeof(int) * ((size_t)nrows + 1), cudaMemcpyHostToDevice, s0));
+    CK(cudaEventRecord(pc->ev_rp, s0));
+    if (ncols) CK(cudaMemcpyAsync(dx, x, sizeof(float) * (size_t)ncols, cudaMemcpyHostToDevice, s0));
+    CK(cudaEventRecord(pc->ev_x, s0));
+    const long long chunk = ((long long)nnz + SPMV_PIPE_CHUNKS - 1) / SPMV_PIPE_CHUNKS;
+    for (int k = 0; k < SPMV_PIPE_CHUNKS; k++) {
+        const long long lo = k * chunk, hi = lo + chunk < nnz ? lo + chunk : nnz;
+        if (hi > lo) {
+            CK(cudaMemcpyAsync(dcol + lo, col + lo, sizeof(int) * (hi - lo), cudaMemcpyHostToDevice, s0));
+            CK(cudaMemcpyAsync(dval + lo, val + lo, sizeof(float) * (hi - lo), cudaMemcpyHostToDevice, s0));
+        }
+        CK(cudaEventRecord(pc->ev_chunk[k], s0));
+    }
+    // plan on the compute stream as soon as rowptr has landed; fetch the block boundaries
+    CK(cudaStreamWaitEvent(s1, pc->ev_rp, 0));
+    if (csr_plan_build(c, s1, nrows, nnz, drp, mode, &p)) {
+        release();
+        return g_status;
+    }
+    const int K = p.ntiles < SPMV_PIPE_BLOCKS ? p.ntiles : SPMV_PIPE_BLOCKS;
+    int* hb = pc->host_rows;
+    CK(cudaMemcpyAsync(hb, p.flags, sizeof(int), cudaMemcpyDeviceToHost, s1));
+    for (int b = 0; b <= K; b++) {
+        const long long t = (long long)b * p.ntiles / K;
+        CK(cudaMemcpyAsync(hb + 1 + b, p.tile_row + t, sizeof(int), cudaMemcpyDeviceToHost, s1));
+    }
+    CK(cudaStreamSynchronize(s1));
+    CK(cudaStreamWaitEvent(s1, pc->ev_x, 0));
+    auto launch = [&](long long t0, long long t1) {
+        return launch_csr_spmv(s1, mode, nrows, ncols, nnz, drp, dcol, dval, dx, dy, p.tile_row + t0,
+                               (int)(t1 - t0), p.flags, c->status);
+    };
+    if (hb[0] != 0) {  // non-monotone rowptr: generic schedule after the whole upload
+        CK(cudaStreamWaitEvent(s1, pc->ev_chunk[SPMV_PIPE_CHUNKS - 1], 0));
+        if (launch(0, p.ntiles)) return cuda_fail(cudaGetLastError(), "spmv launch");
+        CK(cudaMemcpyAsync(y, dy, sizeof(float) * (size_t)nrows, cudaMemcpyDeviceToHost, s1));
+    } else {
+        for (int b = 0; b < K; b++) {
+            const int rlo = hb[1 + b], rhi = hb[2 + b];
+            if (rhi <= rlo) continue;
+            // last non-zero the block reads: rowptr[rhi] - 1 (monotone, clamped to the array)
+            long long need = (long long)rowptr[rhi];
+            need = need < 1 ? 1 : (need > nnz ? nnz : need);
+            const int k = (int)((need - 1) / chunk);
+            CK(cudaStreamWaitEvent(s1, pc->ev_chunk[k < SPMV_PIPE_CHUNKS ? k : SPMV_PIPE_CHUNKS - 1], 0));
+            if (launch((long long)b * p.ntiles / K, (long long)(b + 1) * p.ntiles / K))
+                return cuda_fail(cudaGetLastError(), "spmv launch");
+            CK(cudaEventRecord(pc->ev_blk[b], s1));
+            CK(cudaStreamWaitEvent(s2, pc->ev_blk[b], 0));
+            CK(cudaMemcpyAsync(y + rlo, dy + rlo, sizeof(float) * (size_t)(rhi - rlo), cudaMemcpyDeviceToHost, s2));
+        }
+    }
+    release();
+    return collect_faults(c, s0) == PENCIL_OK ? ok() : g_status;
+}
+
 int spmv_common(int mode, int nrows, int ncols, int nnz, int* rowptr, int* col, float* val,
                 float* x, float* y) {
     if (nrows < 0 || ncols < 0 || nnz < 0) return fail(PENCIL_E_ARG, "negative extent");
+    if (nrows > 0 && nnz >= (1 << 22) && rowptr && col && val && y && (x || !ncols) && !is_device_ptr(rowptr) &&
+        !is_device_ptr(col) && !is_device_ptr(val) && !is_device_ptr(x) && !is_device_ptr(y))
+        return spmv_pipelined(mode, nrows, ncols, nnz, rowptr, col, val, x, y);
     Stage st[5];
     st[0] = {rowptr, nullptr, sizeof(int) * (nz(nrows) + 1), IN};
     st[1] = {col, nullptr, sizeof(int) * nz(nnz), IN};

@@ -95,6 +95,46 @@ def test_spmv_powerlaw_16M_rows(cuda, big_csr, mode):
     assert normwise_err(got, ref, cs[rowptr[1:]] - cs[rowptr[:-1]]) <= TOL
 
 
+@pytest.mark.parametrize("mode", [0, 1], ids=["source_order", "reassociated"])
+def test_spmv_dropin_host_arrays_pipelined(cuda, big_csr, mode):
+    """Host arrays at full size take the pipelined drop-in (chunked upload, one launch per block of
+    tiles, per-block y download): results are bit-identical to the device-resident path."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    rowptr, col, val, x, _ = big_csr
+    nrows, nnz = rowptr.size - 1, col.size
+    rp = dev(torch, rowptr)
+    yd = torch.empty(nrows, device="cuda")
+    plan = pb.device.CsrPlan(nrows, nrows, nnz, rp, mode=mode)
+    plan.spmv(rp, dev(torch, col), dev(torch, val), dev(torch, x), yd)
+    pb.device.sync_status()
+    y = np.full(nrows, np.nan, np.float32)
+    (pb.dropin.spmv_vec if mode else pb.dropin.spmv_inline)(nrows, nrows, nnz, rowptr, col, val, x, y)
+    assert np.array_equal(y.view(np.uint32), yd.cpu().numpy().view(np.uint32))
+
+
+def test_spmv_dropin_pipelined_non_monotone_and_fault(cuda):
+    import paper_1302_5586_b200 as pb
+    nrows = 1 << 18
+    lens = np.full(nrows, 17, np.int64)
+    rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    nnz = int(rowptr[-1])
+    assert nnz >= 1 << 22
+    col = (synth.u8_i32(nnz, seed=5).astype(np.int64) * 4099 % nrows).astype(np.int32)
+    val, x = synth.f32(nnz, seed=6), synth.f32(nrows, seed=7)
+    bad = rowptr.copy()
+    bad[nrows // 2] = bad[nrows // 2 + 1] + 5  # row nrows/2 - 1 reads past, row nrows/2 is empty
+    y = np.zeros(nrows, np.float32)
+    pb.dropin.spmv_inline(nrows, nrows, nnz, bad, col, val, x, y)
+    exact = oracle.spmv_f32(nrows, nrows, nnz, bad, col, val, x)
+    assert np.array_equal(y.view(np.uint32), exact.view(np.uint32))
+    col_bad = col.copy()
+    col_bad[nnz - 3] = nrows + 11
+    with pytest.raises(pb.PencilError) as e:
+        pb.dropin.spmv_vec(nrows, nrows, nnz, rowptr, col_bad, val, x, y)
+    assert e.value.code == "E-INTERP"
+
+
 def test_conv5x5_u8_16384(cuda):
     import paper_1302_5586_b200 as pb
     torch = cuda
