@@ -8,6 +8,10 @@
     per step.
   * 5x5 stencils — equal row bands; each rank exchanges 2 halo rows with each neighbour
     (send/recv) and runs the stencil on its band extended by the halos.
+  * gemv — row blocks, x replicated (all-gathered from its shards when it starts sharded);
+    gemv_t — column blocks of the strided view, no collective; dot — ranges + one all-reduce of
+    fp64 partials; axpy — ranges, no collective; gemm — the R x C tile grid of
+    pencil_shard_gemm_grid on replicated inputs, C tiles all-gathered on request.
 
 The local compute is a callable so the same plumbing is exercised on CPU (gloo + the oracle)
 and on GPUs (NCCL + the CUDA kernels).
@@ -116,3 +120,112 @@ class BandShardedImage:
         if self.rank < self.world - 1:
             ext[own1:own1 + H] = bot
         return ext
+
+
+# ---------------------------------------------------------------- dense BLAS
+def shard_range(n, world, rank, align=4):
+    """Contiguous [lo, hi) of n elements for `rank`, interior boundaries multiples of `align`
+    (keeps every shard's base 16-byte aligned for the float4 kernels)."""
+    units = (n + align - 1) // align
+    lo = min(n, (units * rank // world) * align)
+    hi = min(n, (units * (rank + 1) // world) * align) if rank < world - 1 else n
+    return lo, hi
+
+
+def allgather_vector(local, n, world, rank, align=4):
+    """Replicate a vector whose rank shards are shard_range(n, world, r, align): one all-gather of
+    rank-padded pieces, then the padding is dropped.  Returns the full length-n tensor."""
+    import torch
+    import torch.distributed as dist
+    bounds = [shard_range(n, world, r, align) for r in range(world)]
+    width = max(hi - lo for lo, hi in bounds)
+    pad = torch.zeros(width, dtype=local.dtype, device=local.device)
+    pad[: local.numel()] = local
+    out = torch.empty(width * world, dtype=local.dtype, device=local.device)
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out, pad)
+    else:
+        dist.all_gather(list(out.view(world, width).unbind(0)), pad)
+    parts = out.view(world, width)
+    return torch.cat([parts[r, : hi - lo] for r, (lo, hi) in enumerate(bounds)])
+
+
+class RowShardedGemv:
+    """gemv (i PARALLEL over rows): rank owns rows [r0, r1) of A and of y; x is replicated (or
+    all-gathered from its shards with `allgather_vector`).  No collective on y: each rank's
+    rows are final; `gather_y` assembles them when a caller wants the whole vector."""
+
+    def __init__(self, m, n, rank, world):
+        self.m, self.n, self.rank, self.world = m, n, rank, world
+        self.r0, self.r1 = shard_range(m, world, rank, align=1)
+
+    def step(self, local_gemv, alpha, beta, A_rows, x, y_rows):
+        """local_gemv(m, n, alpha, beta, A, x, y): the CUDA kernel (pb.device.gemv) or a checker."""
+        return local_gemv(self.r1 - self.r0, self.n, alpha, beta, A_rows, x, y_rows)
+
+    def gather_y(self, y_rows):
+        return allgather_vector(y_rows, self.m, self.world, self.rank, align=1)
+
+
+class ColShardedGemvT:
+    """gemv_t (VOBLA transposed view, j PARALLEL over columns): rank owns columns [j0, j1); every
+    rank reads all m rows of its column block (A at offset j0, same lda) and the replicated x,
+    and writes y[j*incy] for its j only.  No collective."""
+
+    def __init__(self, m, n, rank, world):
+        self.m, self.n, self.rank, self.world = m, n, rank, world
+        self.j0, self.j1 = shard_range(n, world, rank, align=4)
+
+    def views(self, A_flat, y_flat, incy):
+        """(A view, y view) of this rank's column block inside the caller's flat arrays."""
+        return A_flat[self.j0:], y_flat[self.j0 * incy:]
+
+
+def dot_sharded(local_dot, x_local, y_local):
+    """dot (i PARALLEL_WITH_REDUCTION): local partial on this rank's range, then one all-reduce.
+    The partials are summed in fp64 (rank order fixed by the collective) and rounded once."""
+    import torch
+    import torch.distributed as dist
+    part = torch.tensor([float(local_dot(x_local, y_local))], dtype=torch.float64, device=x_local.device)
+    dist.all_reduce(part)
+    return float(part.item())
+
+
+class GemmTileGrid:
+    """gemm (i, j independent; p reduction kept local): the R x C process grid of
+    pencil_shard_gemm_grid; rank (ri, ci) computes the C tile rows [m0, m1) x cols [n0, n1) from
+    A's row panel and B's column panel (inputs replicated: no data-path collective; `gather_c`
+    assembles C on every rank when asked)."""
+
+    def __init__(self, m, n, k, rank, world):
+        self.m, self.n, self.k, self.rank, self.world = m, n, k, rank, world
+        self.R, self.C = shard_gemm_grid(m, n, world)
+        self.ri, self.ci = divmod(rank, self.C)
+        self.m0, self.m1 = shard_range(m, self.R, self.ri, align=1)
+        self.n0, self.n1 = shard_range(n, self.C, self.ci, align=4)
+
+    def panels(self, A, B):
+        """(A row panel, B column panel made contiguous) for this rank's tile."""
+        Ap = A.reshape(self.m, self.k)[self.m0:self.m1].reshape(-1)
+        Bp = B.reshape(self.k, self.n)[:, self.n0:self.n1]
+        Bp = Bp.contiguous().reshape(-1) if hasattr(Bp, "contiguous") else Bp.copy().reshape(-1)
+        return Ap, Bp
+
+    def step(self, local_gemm, alpha, beta, Ap, Bp, C_tile):
+        return local_gemm(self.m1 - self.m0, self.n1 - self.n0, self.k, alpha, beta, Ap, Bp, C_tile)
+
+    def gather_c(self, c_tile):
+        """All-gather every rank's tile (padded to the largest) and assemble the m x n matrix."""
+        import torch
+        import torch.distributed as dist
+        tiles = [(shard_range(self.m, self.R, r // self.C, 1), shard_range(self.n, self.C, r % self.C, 4))
+                 for r in range(self.world)]
+        width = max((a1 - a0) * (b1 - b0) for (a0, a1), (b0, b1) in tiles)
+        pad = torch.zeros(width, dtype=c_tile.dtype, device=c_tile.device)
+        pad[: c_tile.numel()] = c_tile.reshape(-1)
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(parts, pad)
+        out = torch.empty(self.m, self.n, dtype=c_tile.dtype, device=c_tile.device)
+        for r, ((a0, a1), (b0, b1)) in enumerate(tiles):
+            out[a0:a1, b0:b1] = parts[r][: (a1 - a0) * (b1 - b0)].view(a1 - a0, b1 - b0)
+        return out

@@ -1,7 +1,10 @@
 """Multi-process (world_size 2, gloo on CPU) coverage of the N>1 data path of bench.py: row
 shards balanced by nnz with an x all-gather for SpMV, and row bands with a 2-row halo exchange
-for the 5x5 stencils.  The local compute is the oracle (the CUDA kernels replace it on GPUs);
-the assembled result must equal the single-process result bit for bit."""
+for the 5x5 stencils, plus the dense rows of SURVEY §8e: gemv row blocks (x replicated by an
+all-gather of its shards), gemv_t column blocks (no collective), dot ranges + one all-reduce,
+axpy ranges, and gemm on the R x C tile grid.  The local compute is the oracle (the CUDA kernels
+replace it on GPUs); the assembled result must equal the single-process result bit for bit
+(dot: the fp64 partials re-associate, checked to 1e-12 relative)."""
 import os
 import socket
 
@@ -75,6 +78,65 @@ def _conv_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _dense_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    from paper_1302_5586_b200 import synth
+    from paper_1302_5586_b200 import dist as pd
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    try:
+        # gemv: row blocks, x all-gathered from its shards, y gathered
+        m, n = 203, 77
+        A, x, y = synth.f32(m * n, 1), synth.f32(n, 2), synth.f32(m, 3)
+        g = pd.RowShardedGemv(m, n, rank, world)
+        lo, hi = pd.shard_range(n, world, rank, align=1)
+        xr = pd.allgather_vector(torch.from_numpy(x[lo:hi].copy()), n, world, rank, align=1).numpy()
+        yl = g.step(lambda mm, nn, a, b, AA, xx, yy: oracle.gemv(mm, nn, a, b, AA, xx, yy).astype(np.float32),
+                    1.5, 0.5, A[g.r0 * n:g.r1 * n], xr, y[g.r0:g.r1])
+        full = g.gather_y(torch.from_numpy(yl)).numpy()
+        ref = oracle.gemv(m, n, 1.5, 0.5, A, x, y).astype(np.float32)
+        res["gemv"] = bool(np.array_equal(full.view(np.uint32), ref.view(np.uint32)))
+        # gemv_t: column blocks of the strided view, no collective
+        m, n, lda, incx, incy = 41, 90, 96, 2, 3
+        A, x, y = synth.f32(m * lda, 4), synth.f32(m * incx, 5), synth.f32(n * incy, 6)
+        gt = pd.ColShardedGemvT(m, n, rank, world)
+        Av, yv = gt.views(A, y, incy)
+        mine = oracle.gemv_t(m, gt.j1 - gt.j0, lda, incx, incy, 1.0, 0.25, Av.copy(), x, yv.copy())
+        ref = oracle.gemv_t(m, n, lda, incx, incy, 1.0, 0.25, A, x, y)
+        js = np.arange(gt.j1 - gt.j0) * incy
+        res["gemv_t"] = bool(np.array_equal(mine[js], ref[gt.j0 * incy + js]))
+        # dot / axpy: contiguous ranges; dot adds one all-reduce
+        n = 10007
+        x, y = synth.f32(n, 7), synth.f32(n, 8)
+        lo, hi = pd.shard_range(n, world, rank)
+        d = pd.dot_sharded(lambda a, b: oracle.dot(a.numel(), a.numpy(), b.numpy()),
+                           torch.from_numpy(x[lo:hi].copy()), torch.from_numpy(y[lo:hi].copy()))
+        dref = oracle.dot(n, x, y)
+        res["dot"] = abs(d - dref) <= 1e-12 * float(np.sum(np.abs(x.astype(np.float64) * y)))
+        ya = oracle.axpy_f32(hi - lo, np.float32(0.75), x[lo:hi].copy(), y[lo:hi].copy())
+        res["axpy"] = bool(np.array_equal(ya, oracle.axpy_f32(n, np.float32(0.75), x, y)[lo:hi]))
+        # gemm: R x C tile grid, C assembled on every rank
+        m, n, k = 37, 45, 19
+        A, B, C = synth.f32(m * k, 9), synth.f32(k * n, 10), synth.f32(m * n, 11)
+        tg = pd.GemmTileGrid(m, n, k, rank, world)
+        Ap, Bp = tg.panels(A, B)
+        Ct = C.reshape(m, n)[tg.m0:tg.m1, tg.n0:tg.n1].copy().reshape(-1)
+        tile = tg.step(lambda mm, nn, kk, a, b, AA, BB, CC: oracle.gemm(mm, nn, kk, a, b, AA, BB, CC),
+                       1.0, 0.5, Ap.copy(), Bp, Ct)
+        full = tg.gather_c(torch.from_numpy(tile)).numpy()
+        res["gemm"] = bool(np.array_equal(full.reshape(-1), oracle.gemm(m, n, k, 1.0, 0.5, A, B, C)))
+        res["grid"] = (tg.R, tg.C)
+        flags = torch.tensor([int(all(v for kk, v in res.items() if kk != "grid"))])
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            q.put((bool(flags.item()), res))
+    finally:
+        dist.destroy_process_group()
+
+
 def _run(worker, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
@@ -90,3 +152,10 @@ def test_row_sharded_spmv_allgather_gloo():
 
 def test_band_sharded_stencil_halo_exchange_gloo():
     assert _run(_conv_worker)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dense_shards_gemv_gemvt_dot_axpy_gemm_gloo(world):
+    ok, res = _run(_dense_worker, world)
+    assert ok, res
+    assert res["grid"][0] * res["grid"][1] == world
