@@ -158,8 +158,10 @@ static unsigned pack_s8(int a, int b, int c, int d) {
 
 }  // namespace
 
-int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsigned char* img,
-                            const int* k25, unsigned char* out) {
+// the packed-u8 ring kernel (k_stencil.cu) is the default; this is its fallback for taps
+// with |k| > 657 and layouts it does not take
+int launch_conv5x5_u8_bytes_dp4a(cudaStream_t st, int h, int w, int scale, const unsigned char* img,
+                                 const int* k25, unsigned char* out) {
     if (h <= 0 || w <= 0) return 0;
     Divider dv = make_divider(scale);
     bool s8 = true;

@@ -343,6 +343,152 @@ __global__ void u8_repair_kernel(int h, int w, const int* __restrict__ img, int*
 }
 __global__ void u8_rearm_kernel(unsigned* flag) { *flag = 0u; }
 
+// ---------------------------------------------------------------- packed 8-bit images
+// conv5x5_u8 semantics on 1-byte pixels (pencil_conv5x5_u8_bytes_dev): the same sweep with a
+// byte ring (136 bytes per row: columns [c0 - 4, c0 + 132)), filled by 4-byte cp.async per
+// lane.  A lane owns 4 pixels; its 8 window bytes come from 3 ring words, each pixel pair is
+// built by two PRMTs (byte | 0x4B000000 = 2^23 + v) and one FFMA2 (- 2^23), then the same
+// 25 fused FFMA2 per pair and pairwise requantisation as the int32-storage kernel; the 4 output
+// bytes leave as one 32-bit store.  Taps are limited to |k| <= 657 (exact fp32 sums); larger
+// taps take the dp4a / scalar kernels of k_conv_u8b.cu.
+constexpr int SB_ROWE = 136;
+
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ u64 byte_pair(unsigned wlo, int blo, unsigned whi, int bhi, const StencilArgs& a) {
+    const unsigned lo = __byte_perm(wlo, 0x4B000000u, 0x7540u + blo);
+    const unsigned hi = __byte_perm(whi, 0x4B000000u, 0x7540u + bhi);
+    return f2fma(((u64)hi << 32) | lo, a.one, a.negmag);
+}
+
+// window row of the lane (columns c-2 .. c+5) as pairs P[m] = (e[m], e[m+2]), m = 0..5
+__device__ __forceinline__ void bytes_read(const unsigned char* slot, int w, int c0, int lane, const StencilArgs& a,
+                                           u64 (&P)[7]) {
+    const unsigned* wp = reinterpret_cast<const unsigned*>(slot) + lane;  // ring words lane .. lane+2
+    unsigned W0 = wp[0], W1 = wp[1], W2 = wp[2];  // columns c-4..c-1 | c..c+3 | c+4..c+7
+    const int c = c0 + 4 * lane;
+    if (c0 == 0 || c0 + 132 > w) {  // image-edge strips: clamp-to-edge columns
+        unsigned char v[8];
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            const int col = c - 2 + m;
+            v[m] = slot[clampi(col, 0, w - 1) - (c0 - 4)];
+        }
+        W0 = ((unsigned)v[0] << 16) | ((unsigned)v[1] << 24);
+        W1 = v[2] | ((unsigned)v[3] << 8) | ((unsigned)v[4] << 16) | ((unsigned)v[5] << 24);
+        W2 = v[6] | ((unsigned)v[7] << 8);
+    }
+    // e[m] = byte (m + 2) of the 12-byte run W0 W1 W2
+    P[0] = byte_pair(W0, 2, W1, 0, a);
+    P[1] = byte_pair(W0, 3, W1, 1, a);
+    P[2] = byte_pair(W1, 0, W1, 2, a);
+    P[3] = byte_pair(W1, 1, W1, 3, a);
+    P[4] = byte_pair(W1, 2, W2, 0, a);
+    P[5] = byte_pair(W1, 3, W2, 1, a);
+}
+
+template <int S, bool POW2>
+__device__ __forceinline__ void bytes_step(int w, int i, int c, int lane, int r_end, const RingLane& L,
+                                           unsigned char (*ring)[SB_ROWE], u64 (&W)[5][7],
+                                           Sweep<unsigned char>& sw, const StencilArgs& a) {
+    cp_wait<S_RING - 1>();
+    __syncwarp();
+    unsigned char* slot = ring[(i + 2) % S_RING];
+    bytes_read(slot, w, c - 4 * lane, lane, a, W[S]);
+    __syncwarp();
+    if (i + 2 + S_RING < r_end) {
+        const unsigned char* src = sw.src > sw.src_last ? sw.src_last : sw.src;
+        unsigned char* dst = slot + 4 + 4 * lane;
+        if (L.body) cp4(dst, src);
+        if (L.halo) cp4(dst + 4 * L.hdir, src + 4 * L.hdir);
+    }
+    cp_commit();
+    sw.src += sw.w;
+    u64 a02 = 0ull, a13 = 0ull;
+#pragma unroll
+    for (int di = 0; di < 5; di++) {
+        const int sl = (S + 1 + di) % 5;
+#pragma unroll
+        for (int dj = 0; dj < 5; dj++) {
+            const u64 kk = f2pk(a.kf[di * 5 + dj], a.kf[di * 5 + dj]);
+            a02 = f2fma(kk, W[sl][dj], a02);
+            a13 = f2fma(kk, W[sl][dj + 1], a13);
+        }
+    }
+    unsigned char* orow = sw.dst;
+    sw.dst += sw.w;
+    int v[4];
+    if (POW2) {
+        const float2 f02 = f2unpk(f2fma_rm(f2fma(a02, a.inv_scale, a.half_scaled), a.one, a.magic2));
+        const float2 f13 = f2unpk(f2fma_rm(f2fma(a13, a.inv_scale, a.half_scaled), a.one, a.magic2));
+        const float f[4] = {f02.x, f13.x, f02.y, f13.y};
+#pragma unroll
+        for (int t = 0; t < 4; t++) v[t] = __vimin_s32_relu(__float_as_int(f[t]) - 0x4B400000, 255);
+    } else {
+        const float2 p02 = f2unpk(a02), p13 = f2unpk(a13);
+        const float o[4] = {p02.x, p13.x, p02.y, p13.y};
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+            v[t] = (int)sat_div(__float_as_int(__fadd_rn(o[t], 12582912.f)) - 0x4B400000, a);
+    }
+    if (L.body)
+        *reinterpret_cast<unsigned*>(orow) =
+            (unsigned)v[0] | ((unsigned)v[1] << 8) | ((unsigned)v[2] << 16) | ((unsigned)v[3] << 24);
+}
+
+template <bool POW2>
+__global__ void __launch_bounds__(32 * S_WARPS, STENCIL_U8_MINB) stencil_bytes_kernel(int h, int w,
+                                                                                 const unsigned char* __restrict__ img,
+                                                                                 unsigned char* __restrict__ out,
+                                                                                 StencilArgs a) {
+    __shared__ __align__(16) unsigned char ring_all[S_WARPS][S_RING][SB_ROWE];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = (blockIdx.x * S_WARPS + warp) * 128;
+    if (c0 >= w) return;
+    const int c = c0 + 4 * lane;
+    const int i0 = blockIdx.y * S_BAND, i1 = min(h, i0 + S_BAND);
+    if (i0 >= i1) return;
+    const int r_end = i1 + 2;
+    const RingLane L = ring_lane(w, c0, lane);
+    unsigned char(*ring)[SB_ROWE] = ring_all[warp];
+    auto issue = [&](int r, unsigned char* slot) {
+        const unsigned char* src = img + (long long)clampi(r, 0, h - 1) * w + c;
+        unsigned char* dst = slot + 4 + 4 * lane;
+        if (L.body) cp4(dst, src);
+        if (L.halo) cp4(dst + 4 * L.hdir, src + 4 * L.hdir);
+    };
+#pragma unroll
+    for (int d = 0; d < S_RING; d++) {
+        if (i0 - 2 + d < r_end) issue(i0 - 2 + d, ring[(i0 - 2 + d + S_RING) % S_RING]);
+        cp_commit();
+    }
+    u64 W[5][7];
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        cp_wait<S_RING - 1>();
+        __syncwarp();
+        unsigned char* slot = ring[(i0 - 2 + d + S_RING) % S_RING];
+        bytes_read(slot, w, c0, lane, a, W[d]);
+        __syncwarp();
+        if (i0 - 2 + d + S_RING < r_end) issue(i0 - 2 + d + S_RING, slot);
+        cp_commit();
+    }
+    Sweep<unsigned char> sw;
+    sw.w = w;
+    sw.src_last = img + (long long)(h - 1) * w + c;
+    sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;
+    sw.dst = out + (long long)i0 * w + c;
+    for (int i = i0; i < i1; i += 5) {
+        bytes_step<4, POW2>(w, i, c, lane, r_end, L, ring, W, sw, a);
+        if (i + 1 < i1) bytes_step<0, POW2>(w, i + 1, c, lane, r_end, L, ring, W, sw, a);
+        if (i + 2 < i1) bytes_step<1, POW2>(w, i + 2, c, lane, r_end, L, ring, W, sw, a);
+        if (i + 3 < i1) bytes_step<2, POW2>(w, i + 3, c, lane, r_end, L, ring, W, sw, a);
+        if (i + 4 < i1) bytes_step<3, POW2>(w, i + 4, c, lane, r_end, L, ring, W, sw, a);
+    }
+    cp_wait<0>();
+}
+
 u64 pack2(float v) {
     unsigned u;
     memcpy(&u, &v, 4);
@@ -414,5 +560,40 @@ int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, 
     const long long n = (long long)h * w, blocks = (n + 255) / 256;
     u8_repair_kernel<<<(int)(blocks < PENCIL_NUM_SMS * 8 ? blocks : PENCIL_NUM_SMS * 8), 256, 0, st>>>(h, w, img, out, a);
     u8_rearm_kernel<<<1, 1, 0, st>>>(a.repair_flag);
+    return (int)cudaGetLastError();
+}
+
+int launch_conv5x5_u8_bytes_dp4a(cudaStream_t st, int h, int w, int scale, const unsigned char* img,
+                                 const int* k25, unsigned char* out);
+
+int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsigned char* img, const int* k25,
+                            unsigned char* out) {
+    if (h <= 0 || w <= 0) return 0;
+    bool small = true;
+    for (int t = 0; t < 25; t++) small &= (k25[t] >= -657 && k25[t] <= 657);
+    if (!small || w % 4 != 0 || (uintptr_t)img % 4 != 0 || (uintptr_t)out % 4 != 0)
+        return launch_conv5x5_u8_bytes_dp4a(st, h, w, scale, img, k25, out);
+    StencilArgs a = {};
+    for (int t = 0; t < 25; t++) {
+        a.kf[t] = (float)k25[t];
+        a.ki[t] = k25[t];
+    }
+    a.negz = pack2(-0.0f);
+    a.one = pack2(1.0f);
+    a.negmag = pack2(-8388608.0f);
+    a.scale = scale;
+    a.shift = -1;
+    if (scale > 0 && (scale & (scale - 1)) == 0) {
+        a.shift = 0;
+        while ((1 << a.shift) != scale) a.shift++;
+        a.inv_scale = pack2(ldexpf(1.0f, -a.shift));
+        a.half_scaled = pack2((float)(scale >> 1) * ldexpf(1.0f, -a.shift));
+        a.magic2 = pack2(12582912.0f);
+    } else if (scale >= 2) {
+        a.magic = ~0ull / (unsigned long long)scale + 1;
+    }
+    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
+    if (a.shift >= 0) stencil_bytes_kernel<true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+    else stencil_bytes_kernel<false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     return (int)cudaGetLastError();
 }

@@ -96,9 +96,12 @@ def test_conv_u8_int32_storage_not_an_8bit_image(cuda):
 def test_conv_u8_bytes_matches_int32_storage_ragged(cuda):
     import paper_1302_5586_b200 as pb
     torch = cuda
-    for h, w in ((33, 512), (20, 1000), (9, 16)):
+    # ring kernel (w % 4 == 0, |k| <= 657) incl. strips narrower than a warp; w % 4 != 0 and
+    # taps beyond 657 take the dp4a / scalar kernels
+    for h, w in ((33, 512), (20, 1000), (9, 16), (70, 132), (11, 1002), (5, 4)):
         img = synth.u8_i32(h * w, seed=w)
-        for k, scale in ((synth.BINOMIAL, 256), (synth.SHARPEN, 1), (synth.BINOMIAL * 3, 5)):
+        for k, scale in ((synth.BINOMIAL, 256), (synth.SHARPEN, 1), (synth.BINOMIAL * 3, 5),
+                         (synth.SHARPEN * 82, 3), (synth.BINOMIAL * 18, 1000), (synth.BINOMIAL * 20, 1000)):
             out8 = torch.empty(h * w, dtype=torch.uint8, device="cuda")
             pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img.astype(np.uint8)).cuda(), k, out8)
             ref = oracle.conv5x5_u8(h, w, scale, img, k)
