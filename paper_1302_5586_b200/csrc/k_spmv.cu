@@ -381,7 +381,10 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     // Also measured and dropped: a 3-stage software-pipelined LSU variant (1.41 ms — more
     // gathers in flight, but the chunk/batch merge doubled the instruction count), and a
     // cp.async double-buffered col/val prefetch (2.43 ms: MIO-throttled, 16-B LDGSTS per lane
-    // plus the smem re-read of col/val saturate the MIO queue the gathers also need).
+    // plus the smem re-read of col/val saturate the MIO queue the gathers also need), and a
+    // register prefetch of the next chunk's column indices (1.34 ms at 8 CTAs/SM, 1.39 at 7:
+    // the ~38% of stall samples on first use of col[] are the request path being full, not
+    // latency that more loads in flight could hide).
     static int use_tma = -1;
     if (use_tma < 0) {
         const char* e = getenv("PENCIL_SPMV_KERNEL");
