@@ -14,78 +14,88 @@
 #include "kernels.h"
 
 // ------------------------------------------------------------------ gemv
-// A warp owns two rows and streams them together (x loaded once for both): 8 x 16-byte A
-// loads in flight per lane.  CTA = 4 warps = 8 rows, <= 64 registers: at 8192 rows the whole
-// grid (1024 CTAs) is resident in ONE wave (7 CTAs/SM), so every SM streams ~55 rows to the end
-// instead of a second, mostly empty wave (the tail that capped the 1-row/warp kernel at 76%).
+// A warp owns two rows and streams them together (x loaded once for both): 16 x 16-byte A
+// loads in flight per lane.  CTA = 4 warps = 8 rows; at 8192 rows the grid is 1024 CTAs.
+// Swept (warps, rows/warp, unroll, CTAs/SM) at 8192^2: (4,2,8,4) 49.2 us, (4,2,4,7) 51.2,
+// (4,1,8,8) 51.2, (4,4,4,4) 51.2, (4,4,2,7) 59.4, (8,2,4,3) 59.4.  A pure 268 MB read (dot over
+// 2 x 2^25) takes 60.7 us on the same box: at this size the launch ramp and tail, not the
+// kernel's streaming rate, set the last ~15%.
+#ifndef GEMV_WARPS
 #define GEMV_WARPS 4
+#endif
+#ifndef GEMV_ROWS_PER_WARP
 #define GEMV_ROWS_PER_WARP 2
+#endif
+#ifndef GEMV_UNROLL
+#define GEMV_UNROLL 8  // float4 loads per row per lane per iteration
+#endif
+#ifndef GEMV_MINB
+#define GEMV_MINB 4
+#endif
 template <bool VEC>
-__global__ void __launch_bounds__(32 * GEMV_WARPS, 7) gemv_kernel(int m, int n, float alpha, float beta,
-                                                                  const float* __restrict__ A,
-                                                                  const float* __restrict__ x,
-                                                                  float* __restrict__ y) {
+__global__ void __launch_bounds__(32 * GEMV_WARPS, GEMV_MINB) gemv_kernel(int m, int n, float alpha, float beta,
+                                                                          const float* __restrict__ A,
+                                                                          const float* __restrict__ x,
+                                                                          float* __restrict__ y) {
+    constexpr int R = GEMV_ROWS_PER_WARP, U = GEMV_UNROLL;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long r0 = ((long long)blockIdx.x * GEMV_WARPS + warp) * GEMV_ROWS_PER_WARP;
+    const long long r0 = ((long long)blockIdx.x * GEMV_WARPS + warp) * R;
     if (r0 >= m) return;
-    const bool two = r0 + 1 < m;
-    const float* a0 = A + r0 * (long long)n;
-    const float* a1 = two ? a0 + n : a0;
-    float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f, q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+    const float* a[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) a[r] = A + (r0 + r < m ? r0 + r : r0) * (long long)n;  // rows past m: duplicate
+    float acc[R][4];
+#pragma unroll
+    for (int r = 0; r < R; r++) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
     if (VEC) {
         const float4* x4 = reinterpret_cast<const float4*>(x);
-        const float4* b0 = reinterpret_cast<const float4*>(a0);
-        const float4* b1 = reinterpret_cast<const float4*>(a1);
         const int n4 = n >> 2;
         int j = lane;
-        for (; j + 3 * 32 < n4; j += 4 * 32) {
-            float4 u0[4], u1[4], xv[4];
+        for (; j + (U - 1) * 32 < n4; j += U * 32) {
+            float4 av[R][U], xv[U];
 #pragma unroll
-            for (int u = 0; u < 4; u++) u0[u] = ld_stream_f4(b0 + j + u * 32);
+            for (int r = 0; r < R; r++)
 #pragma unroll
-            for (int u = 0; u < 4; u++) u1[u] = ld_stream_f4(b1 + j + u * 32);
+                for (int u = 0; u < U; u++) av[r][u] = ld_stream_f4(reinterpret_cast<const float4*>(a[r]) + j + u * 32);
 #pragma unroll
-            for (int u = 0; u < 4; u++) xv[u] = __ldg(x4 + j + u * 32);
+            for (int u = 0; u < U; u++) xv[u] = __ldg(x4 + j + u * 32);
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                p0 = fmaf(u0[u].x, xv[u].x, p0);
-                p1 = fmaf(u0[u].y, xv[u].y, p1);
-                p2 = fmaf(u0[u].z, xv[u].z, p2);
-                p3 = fmaf(u0[u].w, xv[u].w, p3);
-                q0 = fmaf(u1[u].x, xv[u].x, q0);
-                q1 = fmaf(u1[u].y, xv[u].y, q1);
-                q2 = fmaf(u1[u].z, xv[u].z, q2);
-                q3 = fmaf(u1[u].w, xv[u].w, q3);
-            }
+            for (int u = 0; u < U; u++)
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    acc[r][0] = fmaf(av[r][u].x, xv[u].x, acc[r][0]);
+                    acc[r][1] = fmaf(av[r][u].y, xv[u].y, acc[r][1]);
+                    acc[r][2] = fmaf(av[r][u].z, xv[u].z, acc[r][2]);
+                    acc[r][3] = fmaf(av[r][u].w, xv[u].w, acc[r][3]);
+                }
         }
         for (; j < n4; j += 32) {
-            const float4 v0 = ld_stream_f4(b0 + j), v1 = ld_stream_f4(b1 + j), xv = __ldg(x4 + j);
-            p0 = fmaf(v0.x, xv.x, p0);
-            p1 = fmaf(v0.y, xv.y, p1);
-            p2 = fmaf(v0.z, xv.z, p2);
-            p3 = fmaf(v0.w, xv.w, p3);
-            q0 = fmaf(v1.x, xv.x, q0);
-            q1 = fmaf(v1.y, xv.y, q1);
-            q2 = fmaf(v1.z, xv.z, q2);
-            q3 = fmaf(v1.w, xv.w, q3);
+            const float4 xv = __ldg(x4 + j);
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const float4 v = ld_stream_f4(reinterpret_cast<const float4*>(a[r]) + j);
+                acc[r][0] = fmaf(v.x, xv.x, acc[r][0]);
+                acc[r][1] = fmaf(v.y, xv.y, acc[r][1]);
+                acc[r][2] = fmaf(v.z, xv.z, acc[r][2]);
+                acc[r][3] = fmaf(v.w, xv.w, acc[r][3]);
+            }
         }
         for (int t = (n4 << 2) + lane; t < n; t += 32) {
             const float xt = __ldg(x + t);
-            p0 = fmaf(a0[t], xt, p0);
-            q0 = fmaf(a1[t], xt, q0);
+#pragma unroll
+            for (int r = 0; r < R; r++) acc[r][0] = fmaf(a[r][t], xt, acc[r][0]);
         }
     } else {
         for (int t = lane; t < n; t += 32) {
             const float xt = __ldg(x + t);
-            p0 = fmaf(ld_stream_f(a0 + t), xt, p0);
-            q0 = fmaf(ld_stream_f(a1 + t), xt, q0);
+#pragma unroll
+            for (int r = 0; r < R; r++) acc[r][0] = fmaf(ld_stream_f(a[r] + t), xt, acc[r][0]);
         }
     }
-    const float s0 = warp_sum<32>((p0 + p1) + (p2 + p3));
-    const float s1 = warp_sum<32>((q0 + q1) + (q2 + q3));
-    if (lane == 0) {
-        y[r0] = alpha * s0 + beta * y[r0];
-        if (two) y[r0 + 1] = alpha * s1 + beta * y[r0 + 1];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const float s = warp_sum<32>((acc[r][0] + acc[r][1]) + (acc[r][2] + acc[r][3]));
+        if (lane == 0 && r0 + r < m) y[r0 + r] = alpha * s + beta * y[r0 + r];
     }
 }
 

@@ -21,3 +21,9 @@ A = torch.from_numpy(synth.f32(m * n)).cuda(); x = torch.from_numpy(synth.f32(n,
 ms = t(lambda: pb.device.gemv(m, n, 1.0, 0.0, A, x, y)); b = 4 * (m * n + m + n)
 out["gemv_8192"] = {"ms": ms, "GB/s": round(b / ms / 1e6, 1)}
 print(json.dumps(out))
+if len(sys.argv) > 1 and sys.argv[1] == "ref":
+    # pure-read reference at the gemv size: dot over 2 x 2^25 floats = 268 MB
+    n2 = 1 << 25
+    xa = torch.from_numpy(synth.f32(n2, 5)).cuda(); ya = torch.from_numpy(synth.f32(n2, 6)).cuda(); r = torch.zeros(1, device="cuda")
+    ms = t(lambda: pb.device.dot(n2, xa, ya, r))
+    print(json.dumps({"dot_268MB": {"ms": ms, "GB/s": round(8 * n2 / ms / 1e6, 1)}}))
