@@ -8,6 +8,9 @@
 // into the 5-row register window (packed pixel pairs for FFMA2) when it enters it, and its ring
 // slot is refilled at once.  Window slots rotate at compile time (unroll by 5).
 //
+// Measured and dropped: two output rows per step (6-row window, four FFMA2 add chains per warp
+// instead of two): 0.485 ms vs 0.475 — the f32 kernel's `wait` stalls are not chain latency.
+//
 // Policies (same arithmetic as the fallbacks, so the parity claims carry over unchanged):
 //   F32  conv5x5_f32: interior only; acc = acc + k*img per tap in source order with the product
 //        and the sum each rounded (FFMA2 against runtime -0 / 1): bit-exact vs the emitted C.
