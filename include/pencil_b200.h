@@ -51,7 +51,12 @@ enum pencil_status {
     PENCIL_E_ARG = 2,         /* invalid argument (negative extent, null pointer, wrong dtype) */
     PENCIL_E_CUDA = 3,        /* CUDA runtime error */
     PENCIL_E_NOMEM = 4,       /* device allocation failed */
-    PENCIL_E_UNSUPPORTED = 5  /* no schedule for this nest / shape */
+    PENCIL_E_UNSUPPORTED = 5, /* no schedule for this nest / shape */
+    /* OP2 mesh-model codes (op2.hpp:79-81, op2.cpp:14-17, 205, 226, 233) */
+    PENCIL_E_OP2_SHAPE = 6,   /* malformed document, wrong table/data lengths, unknown names */
+    PENCIL_E_OP2_RANGE = 7,   /* map entry or arg offset out of range */
+    PENCIL_E_OP2_KERNEL = 8,  /* kernel missing, unparsable, or signature != 2m+n */
+    PENCIL_E_OP2_CONFLICT = 9 /* a dat both incremented and written in one par_loop */
 };
 int pencil_cuda_last_status(void);
 const char* pencil_cuda_last_error(void); /* "E-INTERP: load from x[...] is out of bounds" style */
@@ -174,6 +179,31 @@ int pencil_micro_copy(pencil_stream_t s, long long n, const float* src, float* d
 /* SpMV data path without rows: stream idx + val, gather table[idx] (roofline probe) */
 int pencil_micro_gather_val(pencil_stream_t s, long long n, const int* idx, const float* val,
                             const float* table, float* out);
+
+/* ===== 8. OP2 mesh loops on the GPU ======================================
+ * The reference's mesh model (core/include/pencil/op2.hpp; JSON format of docs/op2-input.md)
+ * executed on the device with the sequential semantics of interpret_op2_reference
+ * (core/src/op2.cpp:388-429).  Kernels are compiled from their PENCIL source (NVRTC, sm_100a);
+ * dats stay device-resident between runs. */
+typedef struct pencil_op2_model* pencil_op2_t;
+/* load_op2_model (op2.hpp:79) + kernel parse/signature/conflict checks of lower_op2_model;
+ * NULL on error (status E-OP2-SHAPE / -RANGE / -KERNEL / -CONFLICT / E-UNSUPPORTED) */
+pencil_op2_t pencil_op2_load(const char* json_text);
+void pencil_op2_free(pencil_op2_t m);
+int pencil_op2_num_loops(pencil_op2_t m);
+/* schedule of par_loop `loop`: 0 parallel (OP_INC as atomic adds), 1 iteration levels,
+ * 2 serial; levels = launches for strategy 1 (known after pencil_op2_prepare) */
+int pencil_op2_loop_info(pencil_op2_t m, int loop, int* strategy, int* levels);
+int pencil_op2_prepare(pencil_op2_t m);        /* compile + upload (also done by the first run) */
+int pencil_op2_run(pencil_op2_t m);            /* every par_loop in order; synchronous, faults -> E-INTERP */
+int pencil_op2_run_loop_async(pencil_op2_t m, int loop); /* enqueue one par_loop on the model's stream */
+int pencil_op2_sync(pencil_op2_t m);           /* wait for the model's stream, report faults */
+long long pencil_op2_dat_size(pencil_op2_t m, const char* dat); /* values (set size x dim), -1 if unknown */
+int pencil_op2_get_dat(pencil_op2_t m, const char* dat, long long* out, long long n);
+int pencil_op2_set_dat(pencil_op2_t m, const char* dat, const long long* in, long long n);
+const char* pencil_op2_cuda_source(pencil_op2_t m); /* generated CUDA (inspection) */
+const char* pencil_op2_lowered(pencil_op2_t m);     /* the model lowered to PENCIL drivers (append_driver) */
+void* pencil_op2_stream(pencil_op2_t m);            /* cudaStream_t the model runs on */
 
 #ifdef __cplusplus
 }

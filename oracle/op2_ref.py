@@ -1,0 +1,97 @@
+"""TEST INFRASTRUCTURE ONLY — the OP2 oracle: the reference Interpreter run on a mesh model.
+
+The reference's own OP2 module (core/src/op2.cpp) needs nlohmann/json, absent here, so it is not
+built.  Its semantics are `interpret_op2_reference` (op2.cpp:388-429): every par_loop in order,
+the kernel called per iteration with (sizes of the distinct dats, the dats, one index per arg:
+`i` or `map[arity*i + offset]`).  This module restates the documented lowering (append_driver,
+op2.cpp:253-345; docs/op2-input.md "Lowering produces one driver per par_loop") in Python, adds
+one `op2_main` that calls the drivers in order, and runs that unit through the REFERENCE
+Interpreter (oracle/_ref/ref_driver `run`), so the outputs are the reference's own.
+
+`mesh_increment_numpy` is the numpy restatement of the increment kernel used at full size
+(beyond the interpreter's 100 M-step budget, interp.hpp:71).
+"""
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+
+from . import REF_DRIVER, OracleFault
+
+
+def _distinct(seq):
+    out = []
+    for s in seq:
+        if s not in out:
+            out.append(s)
+    return out
+
+
+def lower_unit(doc):
+    """PENCIL text: the model's kernels, one `<kernel>_loop` driver per par_loop, and `op2_main`."""
+    maps = {m["name"]: m for m in doc.get("maps", [])}
+    dats = {d["name"]: d for d in doc.get("dats", [])}
+    sets = {s["name"]: s for s in doc.get("sets", [])}
+    parts = [k["source"] for k in doc.get("kernels", [])]
+    calls = []
+    for li, L in enumerate(doc.get("par_loops", [])):
+        ds = _distinct(a["dat"] for a in L["args"])
+        ms = _distinct(a["map"] for a in L["args"] if a.get("map"))
+        fn = f"{L['kernel']}_loop{li}"
+        params = ["int n_iter"] + [f"int n_{d}" for d in ds] + [f"int n_{m}" for m in ms]
+        params += [f"int {d}[restrict const static n_{d}]" for d in ds]
+        params += [f"int {m}[restrict const static n_{m}]" for m in ms]
+        idx = []
+        for a in L["args"]:
+            if a.get("map"):
+                idx.append(f"{a['map']}[{maps[a['map']]['arity']} * i + {a['offset']}]")
+            else:
+                idx.append("i")
+        kargs = [f"n_{d}" for d in ds] + ds + idx
+        parts.append(f"void {fn}({', '.join(params)})\n{{\n  int i;\n  for (i = 0; i < n_iter; i++) {{\n"
+                     f"    {L['kernel']}({', '.join(kargs)});\n  }}\n}}\n")
+        cargs = [str(sets[L["set"]]["size"])] + [str(len(dats[d]["data"])) for d in ds] + \
+            [str(len(maps[m]["table"])) for m in ms] + ds + ms
+        calls.append(f"  {fn}({', '.join(cargs)});")
+    arrays = [d["name"] for d in doc.get("dats", [])] + [m["name"] for m in doc.get("maps", [])]
+    sizes = [len(d["data"]) for d in doc.get("dats", [])] + [len(m["table"]) for m in doc.get("maps", [])]
+    mparams = [f"int n_{a}" for a in arrays] + [f"int {a}[restrict const static n_{a}]" for a in arrays]
+    parts.append(f"void op2_main({', '.join(mparams)})\n{{\n" + "\n".join(calls) + "\n}\n")
+    return "\n".join(parts), arrays, sizes
+
+
+def reference_run(doc):
+    """Final dat contents after interpreting every par_loop (dict name -> int64 array)."""
+    if not os.path.exists(REF_DRIVER):
+        raise FileNotFoundError(REF_DRIVER)
+    src, arrays, sizes = lower_unit(doc)
+    content = {d["name"]: d["data"] for d in doc.get("dats", [])}
+    content.update({m["name"]: m["table"] for m in doc.get("maps", [])})
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "model.pencil.c")
+        with open(path, "w") as f:
+            f.write(src)
+        lines = [f"scalar int {n}" for n in sizes]
+        for a in arrays:
+            p = os.path.join(td, a + ".bin")
+            np.asarray(content[a], dtype=np.int32).tofile(p)
+            lines.append(f"array i32 {p}")
+        r = subprocess.run([REF_DRIVER, "run", path, "op2_main"], input="\n".join(lines) + "\n",
+                           capture_output=True, text=True)
+        if r.returncode == 3:
+            raise OracleFault(r.stdout.strip())
+        if r.returncode != 0:
+            raise RuntimeError(f"ref_driver failed: {r.stderr}{r.stdout}")
+        return {d["name"]: np.fromfile(os.path.join(td, d["name"] + ".bin.out"), dtype=np.int64)
+                for d in doc.get("dats", [])}
+
+
+def mesh_increment_numpy(cells0, edges_val, table):
+    """dcells[map[2e]] += dedges[e]; dcells[map[2e+1]] += dedges[e] for every edge e (int64)."""
+    out = np.asarray(cells0, dtype=np.int64).copy()
+    t = np.asarray(table, dtype=np.int64).reshape(-1, 2)
+    v = np.asarray(edges_val, dtype=np.int64)
+    np.add.at(out, t[:, 1], v)
+    np.add.at(out, t[:, 0], v)
+    return out

@@ -72,6 +72,21 @@ SIGNATURES = {
     "pencil_micro_gather": (c_int, [P, c_int, c_ll, P, P, P]),
     "pencil_micro_copy": (c_int, [P, c_ll, P, P]),
     "pencil_micro_gather_val": (c_int, [P, c_ll, P, P, P, P]),
+    # §8 OP2 mesh loops
+    "pencil_op2_load": (c_void_p, [c_char_p]),
+    "pencil_op2_free": (None, [P]),
+    "pencil_op2_num_loops": (c_int, [P]),
+    "pencil_op2_loop_info": (c_int, [P, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+    "pencil_op2_prepare": (c_int, [P]),
+    "pencil_op2_run": (c_int, [P]),
+    "pencil_op2_run_loop_async": (c_int, [P, c_int]),
+    "pencil_op2_sync": (c_int, [P]),
+    "pencil_op2_dat_size": (c_ll, [P, c_char_p]),
+    "pencil_op2_get_dat": (c_int, [P, c_char_p, P, c_ll]),
+    "pencil_op2_set_dat": (c_int, [P, c_char_p, P, c_ll]),
+    "pencil_op2_cuda_source": (c_char_p, [P]),
+    "pencil_op2_lowered": (c_char_p, [P]),
+    "pencil_op2_stream": (c_void_p, [P]),
     # introspection used by the boundary tests (not in the public header)
     "pencil_fixture_signature": (c_int, [c_char_p, c_char_p, c_int]),
     "pencil_fixture_count": (c_int, []),

@@ -37,6 +37,10 @@ const char* code_name(int s) {
         case PENCIL_E_CUDA: return "E-CUDA";
         case PENCIL_E_NOMEM: return "E-NOMEM";
         case PENCIL_E_UNSUPPORTED: return "E-UNSUPPORTED";
+        case PENCIL_E_OP2_SHAPE: return "E-OP2-SHAPE";
+        case PENCIL_E_OP2_RANGE: return "E-OP2-RANGE";
+        case PENCIL_E_OP2_KERNEL: return "E-OP2-KERNEL";
+        case PENCIL_E_OP2_CONFLICT: return "E-OP2-CONFLICT";
     }
     return "E-?";
 }
@@ -742,9 +746,10 @@ int pencil_micro_copy(pencil_stream_t s, long long n, const float* src, float* d
 
 }  // extern "C"
 
-// status setter for the dispatch layer (dispatch.cpp), C++ linkage, not part of the ABI
+// status setters for the dispatch and OP2 layers (dispatch.cpp, op2.cpp), C++ linkage, not part of the ABI
 int pencil_internal_fail(int status, const char* msg) {
     g_status = status;
     snprintf(g_msg, sizeof g_msg, "%s", msg);
     return status;
 }
+int pencil_internal_ok() { return ok(); }

@@ -1,0 +1,106 @@
+"""OP2 mesh models on the GPU (include/pencil_b200.h §8; reference core/include/pencil/op2.hpp).
+
+``Op2Model(doc)`` takes the reference's mesh-model document (docs/op2-input.md: sets, maps, dats,
+kernels, par_loops; a dict or JSON text) and mirrors the reference's entry points:
+
+  * construction = ``load_op2_model`` (op2.hpp:79) plus the kernel checks of ``lower_op2_model``
+    (E-OP2-SHAPE / E-OP2-RANGE / E-OP2-KERNEL / E-OP2-CONFLICT raise ``PencilError``);
+  * ``run()`` = ``interpret_op2_reference`` (op2.hpp:114): every par_loop in declaration order,
+    on the device; ``dats()`` returns the final contents (int64), like its result map;
+  * ``lowered`` = the PENCIL text of ``lower_op2_model`` (one driver per par_loop).
+"""
+import ctypes
+import json
+
+import numpy as np
+
+from . import _lib
+from .interp import check_status
+
+STRATEGIES = {0: "parallel", 1: "levels", 2: "serial"}
+
+
+class Op2Model:
+    def __init__(self, doc):
+        lib = _lib.load()
+        text = doc if isinstance(doc, str) else json.dumps(doc)
+        self._lib = lib
+        self._h = lib.pencil_op2_load(text.encode())
+        if not self._h:
+            check_status()
+            raise RuntimeError("pencil_op2_load failed without a status")
+        self._doc = json.loads(text)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.pencil_op2_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- execution ---------------------------------------------------------------------------
+    def prepare(self):
+        self._lib.pencil_op2_prepare(self._h)
+        check_status()
+
+    def run(self):
+        """All par_loops in order (synchronous); device faults raise PencilError('E-INTERP')."""
+        self._lib.pencil_op2_run(self._h)
+        check_status()
+        return self
+
+    def run_loop_async(self, i):
+        self._lib.pencil_op2_run_loop_async(self._h, i)
+        check_status()
+
+    def sync(self):
+        self._lib.pencil_op2_sync(self._h)
+        check_status()
+
+    @property
+    def stream(self):
+        return self._lib.pencil_op2_stream(self._h)
+
+    # -- data --------------------------------------------------------------------------------
+    def dat(self, name):
+        n = self._lib.pencil_op2_dat_size(self._h, name.encode())
+        if n < 0:
+            raise KeyError(name)
+        out = np.empty(n, np.int64)
+        self._lib.pencil_op2_get_dat(self._h, name.encode(), out.ctypes.data, n)
+        check_status()
+        return out
+
+    def set_dat(self, name, values):
+        v = np.ascontiguousarray(values, dtype=np.int64)
+        self._lib.pencil_op2_set_dat(self._h, name.encode(), v.ctypes.data, v.size)
+        check_status()
+
+    def dats(self):
+        return {d["name"]: self.dat(d["name"]) for d in self._doc.get("dats", [])}
+
+    # -- introspection -----------------------------------------------------------------------
+    def loop_info(self, i):
+        s, lv = ctypes.c_int(), ctypes.c_int()
+        self._lib.pencil_op2_loop_info(self._h, i, ctypes.byref(s), ctypes.byref(lv))
+        check_status()
+        return STRATEGIES[s.value], lv.value
+
+    @property
+    def num_loops(self):
+        return self._lib.pencil_op2_num_loops(self._h)
+
+    @property
+    def cuda_source(self):
+        return self._lib.pencil_op2_cuda_source(self._h).decode()
+
+    @property
+    def lowered(self):
+        return self._lib.pencil_op2_lowered(self._h).decode()
