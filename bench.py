@@ -258,6 +258,12 @@ def suite(args, torch, pb, hbm):
     out["conv5x5_f32_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm}
     del imgf, outf
 
+    # OP2 mesh loop: the reference's edge->cell increment kernel on a random mesh
+    try:
+        out["op2_mesh_inc_4M_cells_8M_edges"] = op2_line(args, torch, pb, k, w)
+    except Exception as e:  # noqa: BLE001 — a suite line must not take the headline down
+        out["op2_mesh_inc_4M_cells_8M_edges"] = {"unavailable": str(e)[:200]}
+
     # gemm 16384^3 via 3xTF32
     try:
         m = n = kk = 16384
@@ -267,6 +273,41 @@ def suite(args, torch, pb, hbm):
     except pb.PencilError as e:
         out["gemm_16384_3xtf32"] = {"unavailable": str(e)}
     return out
+
+
+def op2_line(args, torch, pb, k, w):
+    import json as _json
+    import tempfile
+    import ctypes
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import op2_probe
+    from paper_1302_5586_b200.op2 import Op2Model
+    nc, ne = 1 << 22, 1 << 23
+    doc = op2_probe.mesh_doc(nc, ne)
+    m = Op2Model(_json.dumps(doc))
+    m.prepare()
+    st = torch.cuda.ExternalStream(m.stream)
+    with torch.cuda.stream(st):
+        ms = statistics.mean(run_steps(torch, lambda: m.run_loop_async(0), k, w, lambda: pb.device.l2_flush()))
+    m.sync()
+    res = {"ms": ms, "Gedges/s": ne / ms / 1e6, "GB/s": (ne * 32 + nc * 16) / ms / 1e6,
+           "schedule": m.loop_info(0)[0], "data": "random edge->cell map (arity 2), int64 dats"}
+    if not args.no_cpu_baseline:
+        # CPU beside it: the model's lowering compiled as C (serial: the emitted reduction on an array
+        # parameter is not valid OpenMP), one par_loop over the same mesh
+        from oracle import op2_ref
+        with tempfile.TemporaryDirectory() as td:
+            lib, arrays, sizes = op2_ref.compile_lowered_c(doc, td)
+            content = {d["name"]: np.asarray(d["data"], np.int32) for d in doc["dats"]}
+            content.update({mm["name"]: np.asarray(mm["table"], np.int32) for mm in doc["maps"]})
+            cargs = [ctypes.c_int(n) for n in sizes] + [ctypes.c_void_p(content[a].ctypes.data) for a in arrays]
+            t0 = time.perf_counter()
+            lib.op2_main(*cargs)
+            cpu_s = time.perf_counter() - t0
+        res["cpu_baseline"] = {"ms": cpu_s * 1e3, "Gedges/s": ne / cpu_s / 1e9, "cores": 1, "kind": "port",
+                               "sample": "the model's lowered driver + kernel as C, gcc -O3, serial"}
+    m.close()
+    return res
 
 
 # ------------------------------------------------------------------ reference arm (CPU)

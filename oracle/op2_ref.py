@@ -95,3 +95,22 @@ def mesh_increment_numpy(cells0, edges_val, table):
     np.add.at(out, t[:, 1], v)
     np.add.at(out, t[:, 0], v)
     return out
+
+
+def compile_lowered_c(doc, outdir):
+    """The model's lowering (kernels + drivers, as above) compiled as plain C with gcc -O3: the
+    reference's CPU path for a mesh model.  emit_openmp would attach `reduction(+: dcells)` to
+    the driver loop, which is not valid OpenMP for an array parameter ([P10]), so
+    the C runs serially.  C `int` is 32-bit (the interpreter's values are int64): use inputs
+    whose sums stay in range.  Returns a ctypes handle exposing `op2_main`."""
+    import ctypes
+    src, arrays, sizes = lower_unit(doc)
+    path = os.path.join(outdir, "model.c")
+    with open(path, "w") as f:
+        f.write(src)
+    so = os.path.join(outdir, "model.so")
+    subprocess.run(["gcc", "-O3", "-march=x86-64-v3", "-std=gnu11", "-fPIC", "-shared", "-DACCESS(x)=",
+                    "-DDEF(x)=(void)0", "-DUSE(x)=(void)0", "-DMAY_DEF(x)=(void)0", "-o", so, path], check=True)
+    lib = ctypes.CDLL(so)
+    lib.op2_main.restype = None
+    return lib, arrays, sizes

@@ -98,6 +98,20 @@ struct Reader {
         return true;
     }
     bool num(Value& v) {
+        {  // fast path: a plain integer of <= 18 digits
+            size_t q = p;
+            bool neg = q < t.size() && t[q] == '-';
+            if (neg) q++;
+            size_t d0 = q;
+            long long x = 0;
+            while (q < t.size() && t[q] >= '0' && t[q] <= '9' && q - d0 < 18) x = x * 10 + (t[q++] - '0');
+            if (q > d0 && (q >= t.size() || (t[q] != '.' && t[q] != 'e' && t[q] != 'E' && !(t[q] >= '0' && t[q] <= '9')))) {
+                p = q;
+                v.kind = Value::Int;
+                v.i = neg ? -x : x;
+                return true;
+            }
+        }
         size_t s = p;
         if (t[p] == '-') p++;
         while (p < t.size() && t[p] >= '0' && t[p] <= '9') p++;
@@ -172,10 +186,40 @@ struct Reader {
                 p++;
                 return true;
             }
+            bool all_int = true;
             for (;;) {
-                Value e;
-                if (!val(e, depth + 1)) return false;
-                v.arr.push_back(std::move(e));
+                ws();
+                if (all_int && p < t.size() && (t[p] == '-' || (t[p] >= '0' && t[p] <= '9'))) {
+                    Value e;
+                    if (!num(e)) return false;
+                    if (e.kind == Value::Int) {
+                        v.ints.push_back(e.i);
+                    } else {  // first non-integer: move the integers into generic values
+                        all_int = false;
+                        for (long long x : v.ints) {
+                            Value iv;
+                            iv.kind = Value::Int;
+                            iv.i = x;
+                            v.arr.push_back(std::move(iv));
+                        }
+                        v.ints.clear();
+                        v.arr.push_back(std::move(e));
+                    }
+                } else {
+                    if (all_int) {
+                        all_int = false;
+                        for (long long x : v.ints) {
+                            Value iv;
+                            iv.kind = Value::Int;
+                            iv.i = x;
+                            v.arr.push_back(std::move(iv));
+                        }
+                        v.ints.clear();
+                    }
+                    Value e;
+                    if (!val(e, depth + 1)) return false;
+                    v.arr.push_back(std::move(e));
+                }
                 ws();
                 if (p < t.size() && t[p] == ',') {
                     p++;

@@ -18,10 +18,12 @@ struct Value {
     double f = 0.0;
     std::string s;
     std::vector<Value> arr;
+    std::vector<long long> ints;  // Array whose elements are all integers (kept compact; arr empty)
     std::vector<std::pair<std::string, Value>> obj;  // document order kept
 
     bool is_object() const { return kind == Object; }
     bool is_array() const { return kind == Array; }
+    size_t size() const { return arr.empty() ? ints.size() : arr.size(); }
     bool is_string() const { return kind == String; }
     bool is_int() const { return kind == Int; }
     bool is_null() const { return kind == Null; }

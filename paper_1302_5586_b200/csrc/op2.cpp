@@ -132,6 +132,7 @@ std::string req_str(const mjson::Value& v, const char* what) {
 }
 std::vector<long long> req_ints(const mjson::Value& v, const char* what) {
     if (!v.is_array()) shape(std::string(what) + " must be a list");
+    if (v.arr.empty()) return v.ints;  // all-integer list (parsed compactly)
     std::vector<long long> out;
     out.reserve(v.arr.size());
     for (const auto& e : v.arr) out.push_back(req_int(e, what));
@@ -993,6 +994,12 @@ void build_levels(const Model& m, const Loop& L, std::vector<long long>& order, 
     for (long long i = 0; i < n; i++) order[pos[lvl[i]]++] = i;
 }
 
+bool map_fits_i32(const Map& mp) {
+    for (long long e : mp.table)
+        if (e > 2147483647ll) return false;
+    return true;
+}
+
 std::string driver_source(const Model& m, const Loop& L, int li, const pf::Func& kf) {
     (void)kf;
     auto dats = distinct_dats(L);
@@ -1000,7 +1007,8 @@ std::string driver_source(const Model& m, const Loop& L, int li, const pf::Func&
     std::ostringstream o;
     o << "extern \"C\" __global__ void op2_loop_" << li << "(Ctx cx, ll n_iter, const ll* __restrict__ iters";
     for (size_t j = 0; j < dats.size(); j++) o << ", ll* d" << j << ", ll n" << j << ", int inc" << j;
-    for (size_t j = 0; j < maps.size(); j++) o << ", const ll* __restrict__ m" << j;
+    for (size_t j = 0; j < maps.size(); j++)  // maps into sets below 2^31 elements are stored as int32
+        o << ", const " << (map_fits_i32(*m.map(maps[j])) ? "int" : "ll") << "* __restrict__ m" << j;
     o << ") {\n  const ll stride = (ll)gridDim.x * blockDim.x;\n";
     o << "  for (ll t = (ll)blockIdx.x * blockDim.x + threadIdx.x; t < n_iter; t += stride) {\n";
     o << "    const ll i = iters ? iters[t] : t;\n";
@@ -1049,8 +1057,14 @@ int device_setup(pencil_op2_model* M) {
     M->d_map.assign(M->m.maps.size(), nullptr);
     for (size_t j = 0; j < M->m.maps.size(); j++) {
         const auto& t = M->m.maps[j].table;
-        OCK(cudaMalloc(&M->d_map[j], std::max<size_t>(8, t.size() * 8)));
-        if (!t.empty()) OCK(cudaMemcpy(M->d_map[j], t.data(), t.size() * 8, cudaMemcpyHostToDevice));
+        if (map_fits_i32(M->m.maps[j])) {
+            std::vector<int> t32(t.begin(), t.end());
+            OCK(cudaMalloc(&M->d_map[j], std::max<size_t>(8, t.size() * 4)));
+            if (!t.empty()) OCK(cudaMemcpy(M->d_map[j], t32.data(), t.size() * 4, cudaMemcpyHostToDevice));
+        } else {
+            OCK(cudaMalloc(&M->d_map[j], std::max<size_t>(8, t.size() * 8)));
+            if (!t.empty()) OCK(cudaMemcpy(M->d_map[j], t.data(), t.size() * 8, cudaMemcpyHostToDevice));
+        }
     }
     M->d_iters.assign(M->m.loops.size(), nullptr);
     M->lvl_off.assign(M->m.loops.size(), {});

@@ -29,7 +29,8 @@ class Op2Model:
         if not self._h:
             check_status()
             raise RuntimeError("pencil_op2_load failed without a status")
-        self._doc = json.loads(text)
+        self._doc = doc if isinstance(doc, dict) else None  # parsed lazily (large meshes)
+        self._text = None if isinstance(doc, dict) else text
 
     def close(self):
         if getattr(self, "_h", None):
@@ -84,6 +85,8 @@ class Op2Model:
         check_status()
 
     def dats(self):
+        if self._doc is None:
+            self._doc = json.loads(self._text)
         return {d["name"]: self.dat(d["name"]) for d in self._doc.get("dats", [])}
 
     # -- introspection -----------------------------------------------------------------------
