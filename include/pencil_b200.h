@@ -205,6 +205,24 @@ const char* pencil_op2_cuda_source(pencil_op2_t m); /* generated CUDA (inspectio
 const char* pencil_op2_lowered(pencil_op2_t m);     /* the model lowered to PENCIL drivers (append_driver) */
 void* pencil_op2_stream(pencil_op2_t m);            /* cudaStream_t the model runs on */
 
+/* ===== 9. PENCIL units on the GPU: the general mapper (emit_cuda) ============
+ * Any compliant unit, compiled for sm_100a (NVRTC) with the reference Interpreter's value
+ * semantics; top-level loops of the called function with `#pragma pencil independent` run one
+ * iteration per thread, `#pragma pencil reduction (op: v)` loops add a fixed-order combine, other
+ * statements run in order on one device thread (jit.cpp). Surface of pencil::Interpreter. */
+typedef struct pencil_jit* pencil_jit_t;
+pencil_jit_t pencil_jit_load(const char* source);  /* NULL on error (E-ARG "E-SYNTAX: ...", E-UNSUPPORTED) */
+void pencil_jit_free(pencil_jit_t j);
+int pencil_jit_set_array(pencil_jit_t j, const char* name, int dtype, const void* host, long long n);
+long long pencil_jit_array_size(pencil_jit_t j, const char* name);
+/* values as fp64 + per-element is_double flag (+ exact int64 of integer elements, optional) */
+int pencil_jit_get_array(pencil_jit_t j, const char* name, double* out, unsigned char* is_double,
+                         long long* ints, long long n);
+int pencil_jit_call(pencil_jit_t j, const char* fn, int nargs, const pencil_arg* args, pencil_value* ret);
+/* per top-level segment of fn: 'S' serial, 'P' parallel loop, 'R' parallel loop with reduction */
+int pencil_jit_schedule(pencil_jit_t j, const char* fn, char* out, int cap);
+const char* pencil_jit_cuda_source(pencil_jit_t j);
+
 #ifdef __cplusplus
 }
 #endif

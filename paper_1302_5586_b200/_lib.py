@@ -87,6 +87,15 @@ SIGNATURES = {
     "pencil_op2_cuda_source": (c_char_p, [P]),
     "pencil_op2_lowered": (c_char_p, [P]),
     "pencil_op2_stream": (c_void_p, [P]),
+    # §9 PENCIL units (general mapper)
+    "pencil_jit_load": (c_void_p, [c_char_p]),
+    "pencil_jit_free": (None, [P]),
+    "pencil_jit_set_array": (c_int, [P, c_char_p, c_int, P, c_ll]),
+    "pencil_jit_array_size": (c_ll, [P, c_char_p]),
+    "pencil_jit_get_array": (c_int, [P, c_char_p, P, P, P, c_ll]),
+    "pencil_jit_call": (c_int, [P, c_char_p, c_int, P, P]),
+    "pencil_jit_schedule": (c_int, [P, c_char_p, c_char_p, c_int]),
+    "pencil_jit_cuda_source": (c_char_p, [P]),
     # introspection used by the boundary tests (not in the public header)
     "pencil_fixture_signature": (c_int, [c_char_p, c_char_p, c_int]),
     "pencil_fixture_count": (c_int, []),

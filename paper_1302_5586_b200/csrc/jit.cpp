@@ -1,0 +1,731 @@
+// A general verdict-driven mapper for PENCIL units ("emit_cuda" mirroring
+// emit_openmp, core/src/pretty.cpp:472-531): any compliant unit is compiled for the GPU and its
+// functions are callable through the reference Interpreter's surface (set_array / call / arrays,
+// interp.hpp:38-51), with the Interpreter's value semantics (tagged int64 / fp64 values and
+// arrays; codegen.hpp).
+//
+// Mapping (the verdict switch of emit_openmp, driven by the directives a PENCIL programmer writes
+// — the analyzer's PARALLEL verdicts for such loops are DIRECTIVE / ASSUMED_PARALLEL):
+//   * a top-level `for` of the called function carrying `#pragma pencil independent` becomes a
+//     grid of threads, one iteration per thread (grid-stride); nested loops inside it stay
+//     sequential in their thread, in source order;
+//   * a top-level `for` carrying `#pragma pencil reduction (op: v...)` (op + * max min) runs the
+//     same way with thread-private accumulators started at the identity, combined afterwards in a
+//     fixed order by one block (deterministic; fp sums re-associate, as the pragma licenses —
+//     integer sums are exact);
+//   * every other top-level statement runs, in order, on one device thread (SERIAL / UNKNOWN
+//     verdicts stay sequential, like emit_openmp leaves them without a pragma).
+// The function's scalars live in a device frame (the interpreter's Frame::scalars) shared by the
+// launches; a parallel loop's threads read it privately and the thread that ran the last
+// iteration writes its scalars back (the sequential final values, loop variable = hi - 1 as in
+// interp.cpp:207-217).  Local arrays live in a device buffer for the call; those declared inside
+// a parallel loop body are thread-private.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/pencil_b200.h"
+#include "codegen.hpp"
+#include "pencil_front.hpp"
+
+int pencil_internal_fail(int status, const char* msg);  // runtime.cpp
+int pencil_internal_ok();                                // runtime.cpp
+
+namespace {
+
+int fail(int st, const std::string& m) { return pencil_internal_fail(st, m.c_str()); }
+
+const char* kJitExtra = R"CUDA(
+static __device__ __forceinline__ V vmax(V a, V b) { return truth(op_gt(b, a)) ? b : a; }
+static __device__ __forceinline__ V vmin(V a, V b) { return truth(op_lt(b, a)) ? b : a; }
+static __device__ __forceinline__ V red(int op, V a, V b) {
+    switch (op) { case 0: return op_add(a, b); case 1: return op_mul(a, b); case 2: return vmax(a, b); }
+    return vmin(a, b);
+}
+)CUDA";
+
+struct Red {
+    int op;           // 0 + 1 * 2 max 3 min
+    std::string var;
+};
+struct Seg {
+    bool parallel = false;
+    std::vector<const pf::Stmt*> stmts;  // serial: statements in order; parallel: the loop
+    std::vector<Red> reds;
+    std::set<std::string> private_larrays;  // local arrays declared inside the loop body
+};
+struct EntryFn {
+    const pf::Func* f = nullptr;
+    std::vector<std::string> scalars;  // frame layout; slot K = return value
+    std::map<std::string, int> slot;
+    std::map<std::string, long long> la_off;  // local array -> offset in the call's buffer
+    std::map<std::string, long long> la_n;
+    long long la_total = 0;
+    std::vector<Seg> segs;
+};
+
+bool parse_reduction(const std::string& prag, std::vector<Red>& out) {
+    // "#pragma pencil reduction (+: a, b)"
+    size_t p = prag.find("reduction");
+    if (p == std::string::npos) return false;
+    size_t l = prag.find('(', p), c = prag.find(':', p), r = prag.find(')', p);
+    if (l == std::string::npos || c == std::string::npos || r == std::string::npos || !(l < c && c < r)) return false;
+    std::string op = prag.substr(l + 1, c - l - 1);
+    op.erase(std::remove(op.begin(), op.end(), ' '), op.end());
+    int code = op == "+" ? 0 : op == "*" ? 1 : op == "max" ? 2 : op == "min" ? 3 : -1;
+    if (code < 0) return false;
+    std::string vars = prag.substr(c + 1, r - c - 1);
+    std::stringstream ss(vars);
+    std::string v;
+    while (std::getline(ss, v, ',')) {
+        v.erase(std::remove(v.begin(), v.end(), ' '), v.end());
+        if (!v.empty()) out.push_back({code, v});
+    }
+    return true;
+}
+bool has_independent(const pf::Stmt& s) {
+    for (const auto& p : s.pragmas)
+        if (p.find("pencil") != std::string::npos && p.find("independent") != std::string::npos) return true;
+    return false;
+}
+
+// The analyzer's affine fast path for loops without a directive (PARALLEL (AFFINE), e.g. axpy;
+// depanalysis.cpp:163-285), restated conservatively: every array the body writes is read and
+// written only at [i] (the loop variable itself), scalars assigned in the body are declared in
+// it (private per iteration) or are nested loop variables, and the body calls no function.
+struct AffineCheck {
+    std::string iv;
+    std::set<std::string> written, declared, loopvars;
+    bool ok = true;
+    static bool is_iv(const pf::Expr& e, const std::string& iv) { return e.kind == pf::Expr::Var && e.name == iv; }
+    void writes(const pf::Stmt& s) {
+        switch (s.kind) {
+            case pf::Stmt::Block:
+                for (const auto& c : s.body) writes(*c);
+                break;
+            case pf::Stmt::Decl: declared.insert(s.name); break;
+            case pf::Stmt::Assign:
+                if (s.lhs->kind == pf::Expr::Index) written.insert(s.lhs->name);
+                else if (s.lhs->kind != pf::Expr::Var) ok = false;
+                break;
+            case pf::Stmt::For:
+                loopvars.insert(s.name);
+                writes(*s.loop_body);
+                break;
+            case pf::Stmt::While:
+            case pf::Stmt::Labeled: writes(*s.loop_body); break;
+            case pf::Stmt::If:
+                writes(*s.then_s);
+                if (s.else_s) writes(*s.else_s);
+                break;
+            case pf::Stmt::Return: ok = false; break;
+            default: break;
+        }
+    }
+    void expr(const pf::Expr& e) {
+        if (e.kind == pf::Expr::Call) ok = false;
+        if (e.kind == pf::Expr::Unary && e.uop != pf::Un::Neg && e.uop != pf::Un::Not) ok = false;
+        if (e.kind == pf::Expr::Index && written.count(e.name) && !(e.args.size() == 1 && is_iv(*e.args[0], iv))) ok = false;
+        for (const auto& a : e.args) expr(*a);
+    }
+    void stmts(const pf::Stmt& s) {
+        switch (s.kind) {
+            case pf::Stmt::Block:
+                for (const auto& c : s.body) stmts(*c);
+                break;
+            case pf::Stmt::Decl:
+                for (const auto& e : s.extents) expr(*e);
+                if (s.rhs) expr(*s.rhs);
+                break;
+            case pf::Stmt::Assign:
+                expr(*s.rhs);
+                if (s.lhs->kind == pf::Expr::Var) {
+                    if (!declared.count(s.lhs->name) && !loopvars.count(s.lhs->name)) ok = false;
+                } else {
+                    expr(*s.lhs);
+                }
+                break;
+            case pf::Stmt::For:
+                expr(*s.lo);
+                expr(*s.hi);
+                stmts(*s.loop_body);
+                break;
+            case pf::Stmt::While:
+                expr(*s.cond);
+                stmts(*s.loop_body);
+                break;
+            case pf::Stmt::If:
+                expr(*s.cond);
+                stmts(*s.then_s);
+                if (s.else_s) stmts(*s.else_s);
+                break;
+            case pf::Stmt::CallS: ok = false; break;
+            case pf::Stmt::Labeled: stmts(*s.loop_body); break;
+            default: break;
+        }
+    }
+};
+bool affine_parallel(const pf::Stmt& loop) {
+    AffineCheck a;
+    a.iv = loop.name;
+    a.writes(*loop.loop_body);
+    if (a.loopvars.count(a.iv) || a.declared.count(a.iv)) return false;
+    a.stmts(*loop.loop_body);
+    return a.ok;
+}
+
+void collect_decls(const pf::Stmt& s, std::set<std::string>& larr) {
+    switch (s.kind) {
+        case pf::Stmt::Block:
+            for (const auto& c : s.body) collect_decls(*c, larr);
+            break;
+        case pf::Stmt::Decl:
+            if (!s.extents.empty()) larr.insert(s.name);
+            break;
+        case pf::Stmt::For:
+        case pf::Stmt::While:
+        case pf::Stmt::Labeled: collect_decls(*s.loop_body, larr); break;
+        case pf::Stmt::If:
+            collect_decls(*s.then_s, larr);
+            if (s.else_s) collect_decls(*s.else_s, larr);
+            break;
+        default: break;
+    }
+}
+
+struct Builder {
+    const pf::Unit& u;
+    pcg::Gen gen;
+    std::ostringstream k;  // entry kernels
+    explicit Builder(const pf::Unit& unit) : u(unit), gen(unit) {}
+
+    pcg::Gen::Scope scope(const pf::Func& f) {
+        pcg::Gen::Scope sc;
+        sc.f = &f;
+        for (size_t i = 0; i < f.params.size(); i++) {
+            if (f.params[i].kind == pf::Param::Scalar) sc.scalars.insert(f.params[i].name);
+            else sc.arrays[f.params[i].name] = (int)i;
+        }
+        if (f.body) gen.collect(*f.body, sc);
+        return sc;
+    }
+
+    std::string params(const EntryFn& E) {
+        std::ostringstream o;
+        o << "Ctx cx, V* frame, V* la";
+        for (const auto& p : E.f->params)
+            if (p.kind != pf::Param::Scalar) o << ", Arr " << pcg::Gen::aid(p.name);
+        return o.str();
+    }
+    void load_frame(const EntryFn& E, std::ostringstream& o) {
+        for (size_t i = 0; i < E.scalars.size(); i++) o << "  V " << pcg::Gen::sid(E.scalars[i]) << " = frame[" << i << "];\n";
+    }
+    void store_frame(const EntryFn& E, std::ostringstream& o, const std::string& dst, const std::set<std::string>& skip,
+                     const std::string& ind) {
+        for (size_t i = 0; i < E.scalars.size(); i++)
+            if (!skip.count(E.scalars[i])) o << ind << dst << "[" << i << "] = " << pcg::Gen::sid(E.scalars[i]) << ";\n";
+    }
+    void shared_larrays(const EntryFn& E, const std::set<std::string>& priv, std::ostringstream& o) {
+        for (const auto& la : E.la_off)
+            if (!priv.count(la.first))
+                o << "  LArr " << pcg::Gen::lid(la.first) << " = {la + " << la.second << ", " << E.la_n.at(la.first) << "};\n";
+    }
+
+    EntryFn entry(const pf::Func& f, int fi) {
+        EntryFn E;
+        E.f = &f;
+        pcg::Gen::Scope sc = scope(f);
+        for (const auto& p : f.params)
+            if (p.kind == pf::Param::Scalar) E.scalars.push_back(p.name);
+        for (const auto& s : sc.scalars)
+            if (std::find(E.scalars.begin(), E.scalars.end(), s) == E.scalars.end()) E.scalars.push_back(s);
+        for (size_t i = 0; i < E.scalars.size(); i++) E.slot[E.scalars[i]] = (int)i;
+        for (const auto& la : sc.larrays) {
+            E.la_off[la.first] = E.la_total;
+            E.la_n[la.first] = la.second;
+            E.la_total += std::max(1ll, la.second);
+        }
+        // segments: top-level statements of the body
+        std::vector<const pf::Stmt*> top;
+        if (f.body) {
+            if (f.body->kind == pf::Stmt::Block)
+                for (const auto& c : f.body->body) top.push_back(c.get());
+            else
+                top.push_back(f.body.get());
+        }
+        for (const pf::Stmt* s : top) {
+            const pf::Stmt* loop = s;
+            while (loop->kind == pf::Stmt::Labeled) loop = loop->loop_body.get();
+            std::vector<Red> reds;
+            bool red = false;
+            for (const auto& p : s->pragmas) red |= parse_reduction(p, reds);
+            if (loop != s)
+                for (const auto& p : loop->pragmas) red |= parse_reduction(p, reds);
+            bool indep = has_independent(*s) || has_independent(*loop) ||
+                         (loop->kind == pf::Stmt::For && !red && affine_parallel(*loop));
+            if (loop->kind == pf::Stmt::For && (indep || red)) {
+                Seg g;
+                g.parallel = true;
+                g.stmts.push_back(loop);
+                g.reds = reds;
+                collect_decls(*loop->loop_body, g.private_larrays);
+                for (const auto& r : reds)
+                    if (!E.slot.count(r.var)) gen.unsup(f, s->line, "reduction variable '" + r.var + "' is not a scalar");
+                E.segs.push_back(std::move(g));
+            } else {
+                if (E.segs.empty() || E.segs.back().parallel) E.segs.push_back(Seg());
+                E.segs.back().stmts.push_back(s);
+            }
+        }
+        for (size_t si = 0; si < E.segs.size(); si++) emit_segment(E, sc, fi, (int)si);
+        return E;
+    }
+
+    void emit_segment(const EntryFn& E, pcg::Gen::Scope& sc, int fi, int si) {
+        const Seg& g = E.segs[si];
+        const int K = (int)E.scalars.size();
+        std::string base = "jit_" + std::to_string(fi) + "_" + std::to_string(si);
+        if (!g.parallel) {
+            std::ostringstream o;
+            o << "extern \"C\" __global__ void " << base << "(" << params(E) << ", int* flags) {\n";
+            load_frame(E, o);
+            shared_larrays(E, {}, o);
+            o << "  V ret_v = VI(0); int ret_f = 0;\n  auto body = [&]() {\n";
+            gen.ret_mode = 1;
+            for (const pf::Stmt* s : g.stmts) gen.stmt(*s, sc, o, "    ");
+            o << "  };\n  body();\n";
+            store_frame(E, o, "frame", {}, "  ");
+            o << "  if (ret_f) { frame[" << K << "] = ret_v; flags[0] = 1; }\n}\n";
+            k << o.str();
+            return;
+        }
+        const pf::Stmt& L = *g.stmts[0];
+        gen.ret_mode = 2;
+        {  // bounds: one thread evaluates lo and hi (in that order), as the interpreter does
+            std::ostringstream o;
+            o << "extern \"C\" __global__ void " << base << "_b(" << params(E) << ", ll* bounds) {\n";
+            load_frame(E, o);
+            shared_larrays(E, {}, o);
+            std::string lo = gen.ex(*L.lo, sc, o, "  ");
+            o << "  bounds[0] = as_i(cx, " << lo << ");\n";
+            std::string hi = gen.ex(*L.hi, sc, o, "  ");
+            o << "  bounds[1] = as_i(cx, " << hi << ");\n";
+            store_frame(E, o, "frame", {}, "  ");
+            o << "}\n";
+            k << o.str();
+        }
+        std::set<std::string> redvars;
+        for (const auto& r : g.reds) redvars.insert(r.var);
+        {  // body: one iteration per thread, grid-stride
+            std::ostringstream o;
+            o << "extern \"C\" __global__ void " << base << "_p(" << params(E)
+              << ", ll lo, ll hi, V* frame_out, V* partials) {\n";
+            o << "  const ll nthr = (ll)gridDim.x * blockDim.x, tid = (ll)blockIdx.x * blockDim.x + threadIdx.x;\n";
+            load_frame(E, o);
+            shared_larrays(E, g.private_larrays, o);
+            for (const auto& la : g.private_larrays) {
+                long long n = E.la_n.at(la);
+                if (n > 256) gen.unsup(*E.f, L.line, "local array '" + la + "' inside a parallel loop exceeds 256 elements");
+                o << "  V " << pcg::Gen::lid(la) << "_st[" << std::max(1ll, n) << "]; LArr " << pcg::Gen::lid(la) << " = {"
+                  << pcg::Gen::lid(la) << "_st, " << n << "};\n";
+            }
+            for (const auto& r : g.reds)
+                o << "  " << pcg::Gen::sid(r.var) << " = " << (r.op == 0 ? "VI(0)" : r.op == 1 ? "VI(1)" : pcg::Gen::sid(r.var))
+                  << ";\n";
+            o << "  for (ll v = lo + tid; v < hi; v += nthr) {\n";
+            o << "    " << pcg::Gen::sid(L.name) << " = VI(v);\n";
+            o << "    auto body = [&]() {\n";
+            gen.stmt(*L.loop_body, sc, o, "      ");
+            o << "    };\n    body();\n";
+            o << "    if (v == hi - 1) {\n";
+            store_frame(E, o, "frame_out", redvars, "      ");
+            o << "    }\n  }\n";
+            for (size_t r = 0; r < g.reds.size(); r++)
+                o << "  partials[tid * " << g.reds.size() << " + " << r << "] = " << pcg::Gen::sid(g.reds[r].var) << ";\n";
+            o << "}\n";
+            k << o.str();
+        }
+        {  // finish: last-iteration scalars into the frame, reductions combined in a fixed order
+            std::ostringstream o;
+            o << "extern \"C\" __global__ void __launch_bounds__(1024) " << base
+              << "_f(Ctx cx, V* frame, const V* frame_out, const V* partials, ll nthr, int ran) {\n";
+            o << "  __shared__ V sh[1024];\n";
+            o << "  if (ran && threadIdx.x == 0) {\n";
+            for (size_t i = 0; i < E.scalars.size(); i++)
+                if (!redvars.count(E.scalars[i])) o << "    frame[" << i << "] = frame_out[" << i << "];\n";
+            o << "  }\n";
+            for (size_t r = 0; r < g.reds.size(); r++) {
+                const int op = g.reds[r].op;
+                const std::string ident = op == 0 ? "VI(0)" : op == 1 ? "VI(1)" : "frame[" + std::to_string(E.slot.at(g.reds[r].var)) + "]";
+                o << "  {\n    V acc = " << ident << ";\n";
+                o << "    for (ll t = threadIdx.x; t < nthr; t += blockDim.x) acc = red(" << op << ", acc, partials[t * "
+                  << g.reds.size() << " + " << r << "]);\n";
+                o << "    sh[threadIdx.x] = acc;\n    __syncthreads();\n";
+                o << "    for (int s = blockDim.x / 2; s > 0; s >>= 1) {\n      if (threadIdx.x < s) sh[threadIdx.x] = red(" << op
+                  << ", sh[threadIdx.x], sh[threadIdx.x + s]);\n      __syncthreads();\n    }\n";
+                o << "    if (threadIdx.x == 0) frame[" << E.slot.at(g.reds[r].var) << "] = red(" << op << ", frame["
+                  << E.slot.at(g.reds[r].var) << "], sh[0]);\n    __syncthreads();\n  }\n";
+            }
+            o << "}\n";
+            k << o.str();
+        }
+    }
+};
+
+struct StoreArr {
+    long long* bits = nullptr;
+    unsigned char* tag = nullptr;
+    long long n = 0;
+};
+
+}  // namespace
+
+struct pencil_jit {
+    pf::Unit unit;
+    std::string src;
+    std::vector<EntryFn> entries;
+    std::map<std::string, int> entry_index;
+    std::map<std::string, StoreArr> store;
+    cudaLibrary_t lib = nullptr;
+    cudaStream_t stream = nullptr;
+    unsigned* d_fault = nullptr;
+    unsigned long long* d_rng = nullptr;
+    std::vector<cudaKernel_t> kernels_cache;
+    std::map<std::string, cudaKernel_t> kern;
+};
+
+namespace {
+
+#define JCK(call)                                                                                        \
+    do {                                                                                                 \
+        cudaError_t e_ = (call);                                                                         \
+        if (e_ != cudaSuccess) return fail(PENCIL_E_CUDA, std::string("E-CUDA: ") + #call + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int setup(pencil_jit* J) {
+    if (J->lib) return PENCIL_OK;
+    std::vector<char> cubin;
+    std::string log;
+    int rc = pcg::compile_cubin(J->src, cubin, log);
+    if (rc) return fail(rc, "E-CUDA: PENCIL unit compilation failed: " + log);
+    JCK(cudaStreamCreateWithFlags(&J->stream, cudaStreamNonBlocking));
+    JCK(cudaLibraryLoadData(&J->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    JCK(cudaMalloc(&J->d_fault, 64));
+    JCK(cudaMemset(J->d_fault, 0, 64));
+    JCK(cudaMalloc(&J->d_rng, 8));
+    const unsigned long long seed = 0x9e3779b97f4a7c15ull;  // Interpreter::rng_state_ (interp.hpp:67)
+    JCK(cudaMemcpy(J->d_rng, &seed, 8, cudaMemcpyHostToDevice));
+    return PENCIL_OK;
+}
+
+int get_kernel(pencil_jit* J, const std::string& name, cudaKernel_t* out) {
+    auto it = J->kern.find(name);
+    if (it != J->kern.end()) {
+        *out = it->second;
+        return PENCIL_OK;
+    }
+    JCK(cudaLibraryGetKernel(out, J->lib, name.c_str()));
+    J->kern[name] = *out;
+    return PENCIL_OK;
+}
+
+struct HostV {
+    long long i;
+    double d;
+    int isd;
+};
+
+}  // namespace
+
+extern "C" {
+
+pencil_jit_t pencil_jit_load(const char* source) {
+    if (!source) {
+        fail(PENCIL_E_ARG, "E-ARG: null source");
+        return nullptr;
+    }
+    auto* J = new pencil_jit();
+    std::string err;
+    if (!pf::parse_unit(source, J->unit, err)) {
+        fail(PENCIL_E_ARG, "E-SYNTAX: " + err);
+        delete J;
+        return nullptr;
+    }
+    try {
+        Builder b(J->unit);
+        b.gen.unit(pcg::kArrTagged);
+        for (size_t fi = 0; fi < J->unit.fns.size(); fi++) {
+            J->entries.push_back(b.entry(J->unit.fns[fi], (int)fi));
+            J->entry_index[J->unit.fns[fi].name] = (int)fi;
+        }
+        J->src = b.gen.out.str() + kJitExtra + b.k.str();
+    } catch (const pcg::GenError& e) {
+        pencil_internal_fail(e.st, e.msg.c_str());
+        delete J;
+        return nullptr;
+    }
+    pencil_internal_ok();
+    return J;
+}
+
+void pencil_jit_free(pencil_jit_t J) {
+    if (!J) return;
+    if (J->stream) cudaStreamSynchronize(J->stream);
+    for (auto& a : J->store) {
+        cudaFree(a.second.bits);
+        cudaFree(a.second.tag);
+    }
+    if (J->d_fault) cudaFree(J->d_fault);
+    if (J->d_rng) cudaFree(J->d_rng);
+    if (J->lib) cudaLibraryUnload(J->lib);
+    if (J->stream) cudaStreamDestroy(J->stream);
+    delete J;
+}
+
+const char* pencil_jit_cuda_source(pencil_jit_t J) { return J ? J->src.c_str() : ""; }
+
+// segments of `fn`: writes one char per segment ('S' serial, 'P' parallel, 'R' parallel with a
+// reduction) into `out` (NUL-terminated); returns the number of segments or -1
+int pencil_jit_schedule(pencil_jit_t J, const char* fn, char* out, int cap) {
+    if (!J || !fn) return -1;
+    auto it = J->entry_index.find(fn);
+    if (it == J->entry_index.end()) return -1;
+    const auto& segs = J->entries[it->second].segs;
+    int n = 0;
+    for (const auto& g : segs) {
+        if (n + 1 < cap) out[n] = !g.parallel ? 'S' : (g.reds.empty() ? 'P' : 'R');
+        n++;
+    }
+    if (cap > 0) out[std::min(n, cap - 1)] = 0;
+    return n;
+}
+
+// Interpreter::set_array (interp.hpp:40): values of dtype (pencil_dtype; int -> int64 values,
+// float -> fp64 values, like the interpreter's Value)
+int pencil_jit_set_array(pencil_jit_t J, const char* name, int dtype, const void* data, long long n) {
+    if (!J || !name || n < 0 || (n && !data)) return fail(PENCIL_E_ARG, "E-ARG: bad set_array argument");
+    int rc = setup(J);
+    if (rc) return rc;
+    std::vector<long long> bits((size_t)n);
+    std::vector<unsigned char> tag((size_t)n);
+    for (long long i = 0; i < n; i++) {
+        switch (dtype) {
+            case PENCIL_INT32: bits[i] = ((const int*)data)[i]; tag[i] = 0; break;
+            case PENCIL_UINT8: bits[i] = ((const unsigned char*)data)[i]; tag[i] = 0; break;
+            case PENCIL_FLOAT32: {
+                double d = ((const float*)data)[i];
+                memcpy(&bits[i], &d, 8);
+                tag[i] = 1;
+                break;
+            }
+            case PENCIL_FLOAT64: memcpy(&bits[i], (const double*)data + i, 8); tag[i] = 1; break;
+            default: return fail(PENCIL_E_ARG, "E-ARG: unsupported dtype");
+        }
+    }
+    StoreArr& a = J->store[name];
+    if (a.n != n) {
+        cudaFree(a.bits);
+        cudaFree(a.tag);
+        a.bits = nullptr;
+        a.tag = nullptr;
+        JCK(cudaMalloc(&a.bits, std::max<size_t>(8, (size_t)n * 8)));
+        JCK(cudaMalloc(&a.tag, std::max<size_t>(8, (size_t)n)));
+        a.n = n;
+    }
+    if (n) {
+        JCK(cudaMemcpy(a.bits, bits.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
+        JCK(cudaMemcpy(a.tag, tag.data(), (size_t)n, cudaMemcpyHostToDevice));
+    }
+    return pencil_internal_ok();
+}
+
+long long pencil_jit_array_size(pencil_jit_t J, const char* name) {
+    if (!J || !name) return -1;
+    auto it = J->store.find(name);
+    return it == J->store.end() ? -1 : it->second.n;
+}
+
+// Interpreter::arrays() (interp.hpp:39): element values as fp64 plus a per-element flag
+// (1 = the element holds a double, 0 = an integer; integers up to 2^53 are exact in fp64 —
+// `ints_out` (optional) receives the exact int64 of integer elements)
+int pencil_jit_get_array(pencil_jit_t J, const char* name, double* out, unsigned char* is_double,
+                         long long* ints_out, long long n) {
+    if (!J || !name) return fail(PENCIL_E_ARG, "E-ARG: null argument");
+    auto it = J->store.find(name);
+    if (it == J->store.end()) return fail(PENCIL_E_ARG, std::string("E-ARG: no array named '") + name + "'");
+    if (n != it->second.n) return fail(PENCIL_E_ARG, "E-ARG: array size mismatch");
+    if (J->stream) JCK(cudaStreamSynchronize(J->stream));
+    std::vector<long long> bits((size_t)n);
+    std::vector<unsigned char> tag((size_t)n);
+    if (n) {
+        JCK(cudaMemcpy(bits.data(), it->second.bits, (size_t)n * 8, cudaMemcpyDeviceToHost));
+        JCK(cudaMemcpy(tag.data(), it->second.tag, (size_t)n, cudaMemcpyDeviceToHost));
+    }
+    for (long long i = 0; i < n; i++) {
+        double d;
+        if (tag[i]) memcpy(&d, &bits[i], 8);
+        else d = (double)bits[i];
+        if (out) out[i] = d;
+        if (is_double) is_double[i] = tag[i];
+        if (ints_out) ints_out[i] = tag[i] ? (long long)d : bits[i];
+    }
+    return pencil_internal_ok();
+}
+
+// Interpreter::call (interp.hpp:49): scalars by value, arrays by store name; returns the value
+int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg* args, pencil_value* ret) {
+    if (!J || !fn || (nargs && !args)) return fail(PENCIL_E_ARG, "E-ARG: null argument");
+    auto it = J->entry_index.find(fn);
+    if (it == J->entry_index.end()) return fail(PENCIL_E_INTERP, std::string("E-INTERP: no function named '") + fn + "'");
+    const EntryFn& E = J->entries[it->second];
+    const pf::Func& f = *E.f;
+    if ((size_t)nargs != f.params.size())
+        return fail(PENCIL_E_INTERP, "E-INTERP: wrong argument count for '" + f.name + "'");
+    int rc = setup(J);
+    if (rc) return rc;
+    // frame: scalar parameters from the call, locals 0 (slot K: return value)
+    const size_t K = E.scalars.size();
+    std::vector<HostV> frame(K + 1, HostV{0, 0.0, 0});
+    struct DevArr {
+        long long* p;
+        unsigned char* tag;
+        long long n;
+        int inc;
+    };
+    std::vector<DevArr> arrs;
+    for (int i = 0; i < nargs; i++) {
+        const pf::Param& p = f.params[i];
+        if (p.kind == pf::Param::Scalar) {
+            HostV v{0, 0.0, 0};
+            if (args[i].kind == PENCIL_ARG_FLOAT) {
+                v.d = args[i].f;
+                v.isd = 1;
+            } else if (args[i].kind == PENCIL_ARG_INT) {
+                v.i = args[i].i;
+            }  // an array passed for a scalar: 0 (interp.cpp:116)
+            frame[E.slot.at(p.name)] = v;
+        } else {
+            if (args[i].kind != PENCIL_ARG_ARRAY || !args[i].array)
+                return fail(PENCIL_E_INTERP, "E-INTERP: parameter '" + p.name + "' needs an array");
+            auto s = J->store.find(args[i].array);
+            if (s == J->store.end())
+                return fail(PENCIL_E_INTERP, std::string("E-INTERP: no array storage for '") + args[i].array + "'");
+            arrs.push_back({s->second.bits, s->second.tag, s->second.n, 0});
+        }
+    }
+    static_assert(sizeof(HostV) == 24, "V layout");
+    HostV* d_frame = nullptr;
+    HostV* d_out = nullptr;
+    HostV* d_la = nullptr;
+    HostV* d_part = nullptr;
+    long long* d_bounds = nullptr;
+    int* d_flags = nullptr;
+    auto release = [&]() {
+        cudaStreamSynchronize(J->stream);
+        cudaFree(d_frame);
+        cudaFree(d_out);
+        cudaFree(d_la);
+        cudaFree(d_part);
+        cudaFree(d_bounds);
+        cudaFree(d_flags);
+    };
+    const long long max_threads = 148 * 4 * 256;
+    size_t max_red = 1;
+    for (const auto& g : E.segs) max_red = std::max(max_red, g.reds.size());
+    if (cudaMalloc(&d_frame, (K + 1) * sizeof(HostV)) != cudaSuccess ||
+        cudaMalloc(&d_out, (K + 1) * sizeof(HostV)) != cudaSuccess ||
+        cudaMalloc(&d_la, std::max<long long>(1, E.la_total) * sizeof(HostV)) != cudaSuccess ||
+        cudaMalloc(&d_part, max_threads * max_red * sizeof(HostV)) != cudaSuccess ||
+        cudaMalloc(&d_bounds, 16) != cudaSuccess || cudaMalloc(&d_flags, 16) != cudaSuccess) {
+        release();
+        return fail(PENCIL_E_NOMEM, "E-NOMEM: JIT call buffers");
+    }
+    JCK(cudaMemcpyAsync(d_frame, frame.data(), (K + 1) * sizeof(HostV), cudaMemcpyHostToDevice, J->stream));
+    JCK(cudaMemsetAsync(d_la, 0, std::max<long long>(1, E.la_total) * sizeof(HostV), J->stream));
+    JCK(cudaMemsetAsync(d_flags, 0, 16, J->stream));
+    struct {
+        unsigned* fault;
+        unsigned long long* rng;
+    } cx{J->d_fault, J->d_rng};
+    const int fi = it->second;
+    int returned = 0;
+    for (size_t si = 0; si < E.segs.size() && !returned; si++) {
+        const Seg& g = E.segs[si];
+        const std::string base = "jit_" + std::to_string(fi) + "_" + std::to_string(si);
+        std::vector<void*> common = {&cx, &d_frame, &d_la};
+        for (auto& a : arrs) common.push_back(&a);
+        cudaKernel_t kk;
+        if (!g.parallel) {
+            if ((rc = get_kernel(J, base, &kk))) return release(), rc;
+            std::vector<void*> a = common;
+            a.push_back(&d_flags);
+            JCK(cudaLaunchKernel((const void*)kk, dim3(1), dim3(1), a.data(), 0, J->stream));
+            int flags = 0;
+            JCK(cudaMemcpyAsync(&flags, d_flags, 4, cudaMemcpyDeviceToHost, J->stream));
+            JCK(cudaStreamSynchronize(J->stream));
+            returned = flags;
+            continue;
+        }
+        if ((rc = get_kernel(J, base + "_b", &kk))) return release(), rc;
+        {
+            std::vector<void*> a = common;
+            a.push_back(&d_bounds);
+            JCK(cudaLaunchKernel((const void*)kk, dim3(1), dim3(1), a.data(), 0, J->stream));
+        }
+        long long b[2] = {0, 0};
+        JCK(cudaMemcpyAsync(b, d_bounds, 16, cudaMemcpyDeviceToHost, J->stream));
+        JCK(cudaStreamSynchronize(J->stream));
+        long long lo = b[0], hi = b[1];
+        int ran = hi > lo;
+        long long nthr = 0;
+        if (ran) {
+            long long count = hi - lo;
+            long long blocks = std::min<long long>((count + 255) / 256, max_threads / 256);
+            nthr = blocks * 256;
+            if ((rc = get_kernel(J, base + "_p", &kk))) return release(), rc;
+            std::vector<void*> a = common;
+            a.push_back(&lo);
+            a.push_back(&hi);
+            a.push_back(&d_out);
+            a.push_back(&d_part);
+            JCK(cudaLaunchKernel((const void*)kk, dim3((unsigned)blocks), dim3(256), a.data(), 0, J->stream));
+        }
+        if ((rc = get_kernel(J, base + "_f", &kk))) return release(), rc;
+        {
+            std::vector<void*> a = {&cx, &d_frame, &d_out, &d_part, &nthr, &ran};
+            JCK(cudaLaunchKernel((const void*)kk, dim3(1), dim3(1024), a.data(), 0, J->stream));
+        }
+    }
+    HostV rv{0, 0.0, 0};
+    if (returned) JCK(cudaMemcpyAsync(&rv, d_frame + K, sizeof(HostV), cudaMemcpyDeviceToHost, J->stream));
+    unsigned fw = 0;
+    JCK(cudaMemcpyAsync(&fw, J->d_fault, 4, cudaMemcpyDeviceToHost, J->stream));
+    JCK(cudaMemsetAsync(J->d_fault, 0, 4, J->stream));
+    release();
+    if (ret) {
+        ret->kind = rv.isd ? PENCIL_ARG_FLOAT : PENCIL_ARG_INT;
+        ret->i = rv.isd ? 0 : rv.i;
+        ret->f = rv.isd ? rv.d : (double)rv.i;
+    }
+    if (fw) {
+        std::string m = "E-INTERP: device fault:";
+        if (fw & 1u) m += " load out of bounds;";
+        if (fw & 2u) m += " store out of bounds;";
+        if (fw & 4u) m += " division by zero;";
+        if (fw & 8u) m += " modulo by zero;";
+        if (fw & 16u) m += " non-integral value where an integer is required;";
+        if (fw & 64u) m += " empty pointee;";
+        return fail(PENCIL_E_INTERP, m);
+    }
+    return pencil_internal_ok();
+}
+
+}  // extern "C"

@@ -37,6 +37,7 @@
 #include <vector>
 
 #include "../../include/pencil_b200.h"
+#include "codegen.hpp"
 #include "mini_json.hpp"
 #include "pencil_front.hpp"
 
@@ -109,10 +110,8 @@ struct Model {
     }
 };
 
-struct Err {
-    int st;
-    std::string msg;
-};
+typedef pcg::GenError Err;
+using pcg::Gen;
 [[noreturn]] void shape(const std::string& m) { throw Err{PENCIL_E_OP2_SHAPE, "E-OP2-SHAPE: " + m}; }
 [[noreturn]] void range(const std::string& m) { throw Err{PENCIL_E_OP2_RANGE, "E-OP2-RANGE: " + m}; }
 [[noreturn]] void kerr(const std::string& m) { throw Err{PENCIL_E_OP2_KERNEL, "E-OP2-KERNEL: " + m}; }
@@ -385,477 +384,6 @@ struct Scanner {
     }
 };
 
-// ------------------------------------------------------------------ CUDA code generation
-const char* kPrelude = R"CUDA(
-typedef long long ll;
-typedef unsigned long long ull;
-struct V { ll i; double d; int isd; };
-struct Arr { ll* p; ll n; int inc; };
-struct LArr { V* p; ll n; };
-struct Ctx { unsigned* fault; ull* rng; };
-#define F_OOB_LOAD 1u
-#define F_OOB_STORE 2u
-#define F_DIV0 4u
-#define F_MOD0 8u
-#define F_NONINT 16u
-#define F_DBLSTORE 32u
-#define F_EMPTY 64u
-static __device__ __forceinline__ V VI(ll x) { V v; v.i = x; v.d = 0.0; v.isd = 0; return v; }
-static __device__ __forceinline__ V VD(double x) { V v; v.i = 0; v.d = x; v.isd = 1; return v; }
-static __device__ __forceinline__ void fault(const Ctx& c, unsigned b) { atomicOr(c.fault, b); }
-static __device__ __forceinline__ double as_d(V v) { return v.isd ? v.d : (double)v.i; }
-static __device__ __forceinline__ ll as_i(const Ctx& c, V v) {
-    if (!v.isd) return v.i;
-    ll r = (ll)v.d;
-    if ((double)r != v.d) fault(c, F_NONINT);
-    return r;
-}
-static __device__ __forceinline__ bool truth(V v) { return as_d(v) != 0.0; }
-static __device__ __forceinline__ V op_add(V a, V b) { return (a.isd | b.isd) ? VD(as_d(a) + as_d(b)) : VI((ll)((ull)a.i + (ull)b.i)); }
-static __device__ __forceinline__ V op_sub(V a, V b) { return (a.isd | b.isd) ? VD(as_d(a) - as_d(b)) : VI((ll)((ull)a.i - (ull)b.i)); }
-static __device__ __forceinline__ V op_mul(V a, V b) { return (a.isd | b.isd) ? VD(as_d(a) * as_d(b)) : VI((ll)((ull)a.i * (ull)b.i)); }
-static __device__ __forceinline__ V op_div(const Ctx& c, V a, V b) {
-    if (a.isd | b.isd) {
-        double y = as_d(b);
-        if (y == 0.0) { fault(c, F_DIV0); return VD(0.0); }
-        return VD(as_d(a) / y);
-    }
-    if (b.i == 0) { fault(c, F_DIV0); return VI(0); }
-    if (b.i == -1) return VI((ll)(0ull - (ull)a.i));
-    return VI(a.i / b.i);
-}
-static __device__ __forceinline__ V op_mod(const Ctx& c, V a, V b) {
-    ll rb = as_i(c, b);
-    if (rb == 0) { fault(c, F_MOD0); return VI(0); }
-    ll ra = as_i(c, a);
-    if (rb == -1) return VI(0);
-    return VI(ra % rb);
-}
-#define CMP(NAME, OP) \
-static __device__ __forceinline__ V NAME(V a, V b) { return (a.isd | b.isd) ? VI((ll)(as_d(a) OP as_d(b))) : VI((ll)(a.i OP b.i)); }
-CMP(op_lt, <) CMP(op_le, <=) CMP(op_gt, >) CMP(op_ge, >=) CMP(op_eq, ==) CMP(op_ne, !=)
-static __device__ __forceinline__ V op_and(V a, V b) { return VI((ll)(truth(a) && truth(b))); }
-static __device__ __forceinline__ V op_or(V a, V b) { return VI((ll)(truth(a) || truth(b))); }
-static __device__ __forceinline__ V op_neg(V a) { return a.isd ? VD(-a.d) : VI((ll)(0ull - (ull)a.i)); }
-static __device__ __forceinline__ V op_not(V a) { return VI((ll)(as_d(a) == 0.0)); }
-static __device__ __forceinline__ V apply(const Ctx& c, int op, V old, V rhs) {
-    switch (op) {
-        case 1: return op_add(old, rhs);
-        case 2: return op_sub(old, rhs);
-        case 3: return op_mul(old, rhs);
-        case 4: return op_div(c, old, rhs);
-    }
-    return rhs;
-}
-static __device__ __forceinline__ V ld(const Ctx& c, const Arr& a, V idx) {
-    ll k = as_i(c, idx);
-    if (k < 0 || k >= a.n) { fault(c, F_OOB_LOAD); return VI(0); }
-    return VI(a.p[k]);
-}
-static __device__ __forceinline__ void st(const Ctx& c, const Arr& a, V idx, int op, V rhs) {
-    ll k = as_i(c, idx);
-    if (k < 0 || k >= a.n) { fault(c, F_OOB_STORE); return; }
-    if (a.inc && (op == 1 || op == 2)) {  // OP_INC in a parallel loop: commutative integer add
-        if (rhs.isd) { fault(c, F_DBLSTORE); return; }
-        atomicAdd((ull*)(a.p + k), op == 1 ? (ull)rhs.i : (ull)0 - (ull)rhs.i);
-        return;
-    }
-    V v = op == 0 ? rhs : apply(c, op, VI(a.p[k]), rhs);
-    if (v.isd) { fault(c, F_DBLSTORE); v = VI(as_i(c, v)); }
-    a.p[k] = v.i;
-}
-static __device__ __forceinline__ V ldl(const Ctx& c, const LArr& a, V idx) {
-    ll k = as_i(c, idx);
-    if (k < 0 || k >= a.n) { fault(c, F_OOB_LOAD); return VI(0); }
-    return a.p[k];
-}
-static __device__ __forceinline__ void stl(const Ctx& c, const LArr& a, V idx, int op, V rhs) {
-    ll k = as_i(c, idx);
-    if (k < 0 || k >= a.n) { fault(c, F_OOB_STORE); return; }
-    a.p[k] = op == 0 ? rhs : apply(c, op, a.p[k], rhs);
-}
-static __device__ __forceinline__ V deref(const Ctx& c, const Arr& a) {
-    if (a.n == 0) { fault(c, F_EMPTY); return VI(0); }
-    return VI(a.p[0]);
-}
-static __device__ __forceinline__ V b_rand(const Ctx& c) {
-    ull s = *c.rng * 6364136223846793005ull + 1442695040888963407ull;
-    *c.rng = s;
-    return VI((ll)((s >> 33) & 0x7fffffffull));
-}
-static __device__ __forceinline__ V b_exp(V a) { return VD(exp(as_d(a))); }
-)CUDA";
-
-struct Gen {
-    const pf::Unit& u;
-    std::ostringstream out;
-    int tmp = 0;
-    explicit Gen(const pf::Unit& unit) : u(unit) {}
-
-    [[noreturn]] void unsup(const pf::Func& f, int line, const std::string& m) {
-        throw Err{PENCIL_E_UNSUPPORTED, "E-UNSUPPORTED: kernel function '" + f.name + "' line " +
-                                            std::to_string(line) + ": " + m};
-    }
-
-    struct Scope {
-        const pf::Func* f;
-        std::set<std::string> scalars;             // params + locals (frame-wide, like the interpreter)
-        std::map<std::string, int> arrays;         // array/pointer params
-        std::map<std::string, long long> larrays;  // local arrays (constant extent)
-        std::map<std::string, pf::Ty> ldecl;
-    };
-
-    static std::string sid(const std::string& n) { return "s_" + n; }
-    static std::string aid(const std::string& n) { return "a_" + n; }
-    static std::string lid(const std::string& n) { return "l_" + n; }
-
-    void collect(const pf::Stmt& s, Scope& sc) {
-        switch (s.kind) {
-            case pf::Stmt::Block:
-                for (const auto& c : s.body) collect(*c, sc);
-                break;
-            case pf::Stmt::Decl:
-                if (!s.extents.empty()) {
-                    long long total = 1;
-                    for (const auto& e : s.extents) {
-                        if (e->kind != pf::Expr::IntLit) unsup(*sc.f, s.line, "local array '" + s.name + "' needs constant extents");
-                        total *= e->ival;
-                    }
-                    if (total < 0 || total > 4096) unsup(*sc.f, s.line, "local array '" + s.name + "' larger than 4096 elements");
-                    auto it = sc.larrays.find(s.name);
-                    sc.larrays[s.name] = std::max(total, it == sc.larrays.end() ? 0ll : it->second);
-                } else {
-                    sc.scalars.insert(s.name);
-                }
-                break;
-            case pf::Stmt::For:
-                sc.scalars.insert(s.name);
-                collect(*s.loop_body, sc);
-                break;
-            case pf::Stmt::While: collect(*s.loop_body, sc); break;
-            case pf::Stmt::If:
-                collect(*s.then_s, sc);
-                if (s.else_s) collect(*s.else_s, sc);
-                break;
-            case pf::Stmt::Labeled: collect(*s.loop_body, sc); break;
-            default: break;
-        }
-    }
-
-    std::string t() { return "t" + std::to_string(tmp++); }
-
-    // emits statements computing `e`; returns an expression naming the value (a temp or literal)
-    std::string ex(const pf::Expr& e, Scope& sc, std::ostringstream& o, const std::string& ind) {
-        char buf[64];
-        switch (e.kind) {
-            case pf::Expr::IntLit:
-                snprintf(buf, sizeof buf, "VI(%lldLL)", e.ival);
-                return buf;
-            case pf::Expr::FloatLit:
-                snprintf(buf, sizeof buf, "VD(%a)", e.fval);
-                return buf;
-            case pf::Expr::Var:
-                if (!sc.scalars.count(e.name)) unsup(*sc.f, e.line, "unbound scalar '" + e.name + "'");
-                return sid(e.name);
-            case pf::Expr::Index: {
-                if (e.args.size() != 1) unsup(*sc.f, e.line, "multi-dimensional access unsupported here");
-                std::string ix = ex(*e.args[0], sc, o, ind);
-                std::string r = t();
-                if (sc.larrays.count(e.name))
-                    o << ind << "V " << r << " = ldl(cx, " << lid(e.name) << ", " << ix << ");\n";
-                else if (sc.arrays.count(e.name))
-                    o << ind << "V " << r << " = ld(cx, " << aid(e.name) << ", " << ix << ");\n";
-                else
-                    unsup(*sc.f, e.line, "no array storage for '" + e.name + "'");
-                return r;
-            }
-            case pf::Expr::Binary: {
-                std::string a = ex(*e.args[0], sc, o, ind);
-                std::string a2 = t();
-                o << ind << "V " << a2 << " = " << a << ";\n";  // both sides always evaluated, left first
-                std::string b = ex(*e.args[1], sc, o, ind);
-                std::string r = t();
-                static const char* fn[] = {"op_add", "op_sub", "op_mul", "op_div", "op_mod", "op_lt", "op_le",
-                                           "op_gt",  "op_ge",  "op_eq",  "op_ne",  "op_and", "op_or"};
-                int k = (int)e.bop;
-                bool ctx = e.bop == pf::Bin::Div || e.bop == pf::Bin::Mod;
-                o << ind << "V " << r << " = " << fn[k] << "(" << (ctx ? "cx, " : "") << a2 << ", " << b << ");\n";
-                return r;
-            }
-            case pf::Expr::Unary: {
-                if (e.uop == pf::Un::Addr) unsup(*sc.f, e.line, "address-of is not executable");
-                if (e.uop == pf::Un::Deref) {
-                    if (e.args[0]->kind != pf::Expr::Var || !sc.arrays.count(e.args[0]->name))
-                        unsup(*sc.f, e.line, "unsupported dereference");
-                    std::string r = t();
-                    o << ind << "V " << r << " = deref(cx, " << aid(e.args[0]->name) << ");\n";
-                    return r;
-                }
-                std::string a = ex(*e.args[0], sc, o, ind);
-                std::string r = t();
-                o << ind << "V " << r << " = " << (e.uop == pf::Un::Neg ? "op_neg(" : "op_not(") << a << ");\n";
-                return r;
-            }
-            case pf::Expr::Call: {
-                std::string r = t();
-                if (e.name == "exp") {
-                    if (e.args.size() != 1) unsup(*sc.f, e.line, "exp takes one argument");
-                    std::string a = ex(*e.args[0], sc, o, ind);
-                    o << ind << "V " << r << " = b_exp(" << a << ");\n";
-                    return r;
-                }
-                if (e.name == "rand") {
-                    o << ind << "V " << r << " = b_rand(cx);\n";
-                    return r;
-                }
-                const pf::Func* callee = u.find(e.name);
-                if (!callee) unsup(*sc.f, e.line, "call to unknown '" + e.name + "'");
-                if (callee->params.size() != e.args.size())
-                    unsup(*sc.f, e.line, "wrong argument count for '" + e.name + "'");
-                std::vector<std::string> av;
-                for (size_t k = 0; k < e.args.size(); k++) {
-                    if (callee->params[k].kind != pf::Param::Scalar) {
-                        if (e.args[k]->kind != pf::Expr::Var) unsup(*sc.f, e.line, "array argument must be a name");
-                        if (!sc.arrays.count(e.args[k]->name))
-                            unsup(*sc.f, e.line, "array argument '" + e.args[k]->name + "' is not a parameter array");
-                        av.push_back(aid(e.args[k]->name));
-                    } else {
-                        std::string a = ex(*e.args[k], sc, o, ind);
-                        std::string a2 = t();
-                        o << ind << "V " << a2 << " = " << a << ";\n";
-                        av.push_back(a2);
-                    }
-                }
-                o << ind << "V " << r << " = f_" << e.name << "(cx";
-                for (auto& a : av) o << ", " << a;
-                o << ");\n";
-                return r;
-            }
-        }
-        return "VI(0)";
-    }
-
-    void stmt(const pf::Stmt& s, Scope& sc, std::ostringstream& o, const std::string& ind) {
-        switch (s.kind) {
-            case pf::Stmt::Block:
-                for (const auto& c : s.body) stmt(*c, sc, o, ind);
-                break;
-            case pf::Stmt::Nop: break;
-            case pf::Stmt::Decl:
-                if (!s.extents.empty()) {
-                    o << ind << "for (ll q = 0; q < " << lid(s.name) << ".n; ++q) " << lid(s.name) << ".p[q] = "
-                      << (s.dty == pf::Ty::Int ? "VI(0)" : "VD(0.0)") << ";\n";
-                } else if (s.rhs) {
-                    std::string v = ex(*s.rhs, sc, o, ind);
-                    o << ind << sid(s.name) << " = " << v << ";\n";
-                } else {
-                    o << ind << sid(s.name) << " = " << (s.dty == pf::Ty::Int ? "VI(0)" : "VD(0.0)") << ";\n";
-                }
-                break;
-            case pf::Stmt::Assign: {
-                std::string rhs0 = ex(*s.rhs, sc, o, ind);
-                std::string rhs = t();
-                o << ind << "V " << rhs << " = " << rhs0 << ";\n";
-                int op = (int)s.aop;
-                const pf::Expr& lv = *s.lhs;
-                if (lv.kind == pf::Expr::Var) {
-                    if (!sc.scalars.count(lv.name)) unsup(*sc.f, s.line, "assignment to unbound '" + lv.name + "'");
-                    o << ind << sid(lv.name) << " = apply(cx, " << op << ", " << sid(lv.name) << ", " << rhs << ");\n";
-                } else if (lv.kind == pf::Expr::Unary && lv.uop == pf::Un::Deref && lv.args[0]->kind == pf::Expr::Var &&
-                           sc.arrays.count(lv.args[0]->name)) {
-                    o << ind << "if (" << aid(lv.args[0]->name) << ".n == 0) fault(cx, F_EMPTY); else st(cx, "
-                      << aid(lv.args[0]->name) << ", VI(0), " << op << ", " << rhs << ");\n";
-                } else if (lv.kind == pf::Expr::Index) {
-                    if (lv.args.size() != 1) unsup(*sc.f, s.line, "multi-dimensional access unsupported here");
-                    std::string ix = ex(*lv.args[0], sc, o, ind);
-                    if (sc.larrays.count(lv.name))
-                        o << ind << "stl(cx, " << lid(lv.name) << ", " << ix << ", " << op << ", " << rhs << ");\n";
-                    else if (sc.arrays.count(lv.name))
-                        o << ind << "st(cx, " << aid(lv.name) << ", " << ix << ", " << op << ", " << rhs << ");\n";
-                    else
-                        unsup(*sc.f, s.line, "no array storage for '" + lv.name + "'");
-                } else {
-                    unsup(*sc.f, s.line, "unsupported lvalue");
-                }
-                break;
-            }
-            case pf::Stmt::For: {
-                o << ind << "{\n";
-                std::string in2 = ind + "  ";
-                std::string lo = ex(*s.lo, sc, o, in2);
-                std::string lo2 = t();
-                o << in2 << "ll " << lo2 << " = as_i(cx, " << lo << ");\n";
-                std::string hi = ex(*s.hi, sc, o, in2);
-                std::string hi2 = t();
-                o << in2 << "ll " << hi2 << " = as_i(cx, " << hi << ");\n";
-                std::string q = t();
-                o << in2 << "for (ll " << q << " = " << lo2 << "; " << q << " < " << hi2 << "; ++" << q << ") {\n";
-                o << in2 << "  " << sid(s.name) << " = VI(" << q << ");\n";
-                stmt(*s.loop_body, sc, o, in2 + "  ");
-                o << in2 << "}\n" << ind << "}\n";
-                break;
-            }
-            case pf::Stmt::While: {
-                o << ind << "for (;;) {\n";
-                std::string c = ex(*s.cond, sc, o, ind + "  ");
-                o << ind << "  if (!truth(" << c << ")) break;\n";
-                stmt(*s.loop_body, sc, o, ind + "  ");
-                o << ind << "}\n";
-                break;
-            }
-            case pf::Stmt::If: {
-                o << ind << "{\n";
-                std::string c = ex(*s.cond, sc, o, ind + "  ");
-                o << ind << "  if (truth(" << c << ")) {\n";
-                stmt(*s.then_s, sc, o, ind + "    ");
-                o << ind << "  }";
-                if (s.else_s) {
-                    o << " else {\n";
-                    stmt(*s.else_s, sc, o, ind + "    ");
-                    o << ind << "  }";
-                }
-                o << "\n" << ind << "}\n";
-                break;
-            }
-            case pf::Stmt::CallS: {
-                std::string r = ex(*s.call, sc, o, ind);
-                o << ind << "(void)" << r << ";\n";
-                break;
-            }
-            case pf::Stmt::Return:
-                if (s.rhs) {
-                    std::string r = ex(*s.rhs, sc, o, ind);
-                    o << ind << "return " << r << ";\n";
-                } else {
-                    o << ind << "return VI(0);\n";
-                }
-                break;
-            case pf::Stmt::Labeled: stmt(*s.loop_body, sc, o, ind); break;
-        }
-    }
-
-    std::string signature(const pf::Func& f) {
-        std::ostringstream o;
-        o << "static __device__ V f_" << f.name << "(const Ctx& cx";
-        for (const auto& p : f.params) {
-            if (p.kind == pf::Param::Scalar) o << ", V " << sid(p.name);
-            else o << ", Arr " << aid(p.name);
-        }
-        o << ")";
-        return o.str();
-    }
-
-    void function(const pf::Func& f) {
-        Scope sc;
-        sc.f = &f;
-        for (size_t i = 0; i < f.params.size(); i++) {
-            if (f.params[i].kind == pf::Param::Scalar) sc.scalars.insert(f.params[i].name);
-            else sc.arrays[f.params[i].name] = (int)i;
-        }
-        if (f.body) collect(*f.body, sc);
-        std::ostringstream body;
-        for (const auto& s : sc.scalars) {
-            bool is_param = false;
-            for (const auto& p : f.params)
-                if (p.name == s && p.kind == pf::Param::Scalar) is_param = true;
-            if (!is_param) body << "  V " << sid(s) << " = VI(0);\n";
-        }
-        for (const auto& la : sc.larrays)
-            body << "  V " << lid(la.first) << "_st[" << (la.second > 0 ? la.second : 1) << "]; LArr " << lid(la.first)
-                 << " = {" << lid(la.first) << "_st, " << la.second << "};\n";
-        if (f.body) stmt(*f.body, sc, body, "  ");
-        out << signature(f) << " {\n" << body.str() << "  return VI(0);\n}\n";
-    }
-
-    void unit() {
-        out << kPrelude;
-        for (const auto& f : u.fns) out << signature(f) << ";\n";
-        for (const auto& f : u.fns) function(f);
-    }
-};
-
-// ------------------------------------------------------------------ NVRTC (dlopen'd on first use)
-typedef int (*nvrtcCreateProgram_t)(void**, const char*, const char*, int, const char* const*, const char* const*);
-typedef int (*nvrtcCompileProgram_t)(void*, int, const char* const*);
-typedef int (*nvrtcGetSize_t)(void*, size_t*);
-typedef int (*nvrtcGetData_t)(void*, char*);
-typedef int (*nvrtcDestroyProgram_t)(void**);
-typedef const char* (*nvrtcGetErrorString_t)(int);
-struct Nvrtc {
-    bool ok = false;
-    std::string why;
-    nvrtcCreateProgram_t create;
-    nvrtcCompileProgram_t compile;
-    nvrtcGetSize_t log_size, cubin_size;
-    nvrtcGetData_t log, cubin;
-    nvrtcDestroyProgram_t destroy;
-    nvrtcGetErrorString_t errstr;
-};
-Nvrtc& nvrtc() {
-    static Nvrtc n;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
-        if (!h) h = dlopen("libnvrtc.so", RTLD_NOW | RTLD_LOCAL);
-        if (!h) {
-            n.why = "libnvrtc.so.12 not found (needed to compile OP2 kernels)";
-            return;
-        }
-        n.create = (nvrtcCreateProgram_t)dlsym(h, "nvrtcCreateProgram");
-        n.compile = (nvrtcCompileProgram_t)dlsym(h, "nvrtcCompileProgram");
-        n.log_size = (nvrtcGetSize_t)dlsym(h, "nvrtcGetProgramLogSize");
-        n.log = (nvrtcGetData_t)dlsym(h, "nvrtcGetProgramLog");
-        n.cubin_size = (nvrtcGetSize_t)dlsym(h, "nvrtcGetCUBINSize");
-        n.cubin = (nvrtcGetData_t)dlsym(h, "nvrtcGetCUBIN");
-        n.destroy = (nvrtcDestroyProgram_t)dlsym(h, "nvrtcDestroyProgram");
-        n.errstr = (nvrtcGetErrorString_t)dlsym(h, "nvrtcGetErrorString");
-        n.ok = n.create && n.compile && n.log_size && n.log && n.cubin_size && n.cubin && n.destroy && n.errstr;
-        if (!n.ok) n.why = "libnvrtc is missing entry points";
-    });
-    return n;
-}
-
-// compile once per distinct source text (process-wide cache)
-int compile_cubin(const std::string& src, std::vector<char>& cubin, std::string& log) {
-    static std::mutex mu;
-    static std::map<std::string, std::vector<char>> cache;
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(src);
-    if (it != cache.end()) {
-        cubin = it->second;
-        return PENCIL_OK;
-    }
-    Nvrtc& n = nvrtc();
-    if (!n.ok) {
-        log = n.why;
-        return PENCIL_E_UNSUPPORTED;
-    }
-    void* prog = nullptr;
-    if (n.create(&prog, src.c_str(), "op2_model.cu", 0, nullptr, nullptr) != 0) {
-        log = "nvrtcCreateProgram failed";
-        return PENCIL_E_CUDA;
-    }
-    // exact IEEE fp64 (no contraction) and the sm_100a instruction set
-    const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false", "-lineinfo"};
-    int rc = n.compile(prog, 4, opts);
-    size_t ls = 0;
-    n.log_size(prog, &ls);
-    log.assign(ls, 0);
-    if (ls) n.log(prog, &log[0]);
-    if (rc != 0) {
-        n.destroy(&prog);
-        log = std::string("NVRTC: ") + n.errstr(rc) + "\n" + log;
-        return PENCIL_E_CUDA;
-    }
-    size_t cs = 0;
-    n.cubin_size(prog, &cs);
-    cubin.resize(cs);
-    n.cubin(prog, cubin.data());
-    n.destroy(&prog);
-    cache[src] = cubin;
-    return PENCIL_OK;
-}
-
 }  // namespace
 
 // ------------------------------------------------------------------ the model object
@@ -1038,7 +566,7 @@ int device_setup(pencil_op2_model* M) {
     if (M->lib) return PENCIL_OK;
     std::vector<char> cubin;
     std::string log;
-    int rc = compile_cubin(M->cuda_src, cubin, log);
+    int rc = pcg::compile_cubin(M->cuda_src, cubin, log);
     if (rc) return fail(rc, "E-CUDA: OP2 kernel compilation failed: " + log);
     OCK(cudaGetDevice(&M->device));
     OCK(cudaStreamCreateWithFlags(&M->stream, cudaStreamNonBlocking));
@@ -1180,7 +708,7 @@ pencil_op2_t pencil_op2_load(const char* json_text) {
         }
         Scanner sc(M->unit);
         Gen g(M->unit);
-        g.unit();
+        g.unit(pcg::kArrInt64);
         std::ostringstream drivers;
         for (size_t li = 0; li < M->m.loops.size(); li++) {
             const Loop& L = M->m.loops[li];

@@ -325,7 +325,13 @@ struct Parser {
         return b;
     }
     StmtP statement() {
-        while (peek().kind == Tok::Pragma) adv();  // directives do not change the semantics
+        std::vector<std::string> prag;  // kept for the mapper; they do not change the semantics
+        while (peek().kind == Tok::Pragma) prag.push_back(adv().text);
+        StmtP s = statement_inner();
+        s->pragmas = std::move(prag);
+        return s;
+    }
+    StmtP statement_inner() {
         if (at_p("}") || peek().kind == Tok::End) fail("expected a statement");
         int l = peek().line;
         if (at_p("{")) return block();

@@ -45,6 +45,7 @@ struct Stmt {
     ExprP cond;               // While / If
     StmtP then_s, else_s, loop_body;  // If / For, While, Labeled
     ExprP call;               // CallS
+    std::vector<std::string> pragmas;  // `#pragma pencil ...` lines directly before the statement
     int line = 0;
 };
 

@@ -107,3 +107,78 @@ class Op2Model:
     @property
     def lowered(self):
         return self._lib.pencil_op2_lowered(self._h).decode()
+
+
+class JitUnit:
+    """Any PENCIL unit on the GPU (include/pencil_b200.h §9; csrc/jit.cpp), with the surface of
+    pencil::Interpreter (interp.hpp:38-51): ``set_array(name, values)``, ``call(fn, args)``
+    (args: ints / floats / ``Arg.array(name)``), ``get_array(name)``.  Values follow the
+    interpreter: int64 or fp64 per element; ``get_array`` returns fp64 values, the exact int64
+    of integer elements and the per-element is-double flags."""
+
+    def __init__(self, source):
+        lib = _lib.load()
+        self._lib = lib
+        self._h = lib.pencil_jit_load(source.encode())
+        if not self._h:
+            check_status()
+            raise RuntimeError("pencil_jit_load failed without a status")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.pencil_jit_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_array(self, name, values):
+        a = np.ascontiguousarray(values)
+        dt = {np.dtype(np.int32): 0, np.dtype(np.float32): 1, np.dtype(np.float64): 2, np.dtype(np.uint8): 3}
+        if a.dtype not in dt:
+            a = a.astype(np.float64 if a.dtype.kind == "f" else np.int32)
+        self._lib.pencil_jit_set_array(self._h, name.encode(), dt[a.dtype], a.ctypes.data, a.size)
+        check_status()
+
+    def get_array(self, name):
+        n = self._lib.pencil_jit_array_size(self._h, name.encode())
+        if n < 0:
+            raise KeyError(name)
+        vals, flags, ints = np.empty(n, np.float64), np.empty(n, np.uint8), np.empty(n, np.int64)
+        self._lib.pencil_jit_get_array(self._h, name.encode(), vals.ctypes.data, flags.ctypes.data,
+                                       ints.ctypes.data, n)
+        check_status()
+        return vals, ints, flags.astype(bool)
+
+    def call(self, fn, args):
+        from ._lib import pencil_arg as PencilArg, pencil_value as PencilValue
+        from .interp import Arg
+        arr = (PencilArg * max(1, len(args)))()
+        keep = []
+        for i, a in enumerate(args):
+            if isinstance(a, Arg) and a.is_array:
+                b = a.array_name.encode()
+                keep.append(b)
+                arr[i].kind, arr[i].array = 2, b
+            elif isinstance(a, Arg):
+                a = a.value
+            if not (isinstance(args[i], Arg) and args[i].is_array):
+                if isinstance(a, (int, np.integer)):
+                    arr[i].kind, arr[i].i = 0, int(a)
+                else:
+                    arr[i].kind, arr[i].f = 1, float(a)
+        ret = PencilValue()
+        self._lib.pencil_jit_call(self._h, fn.encode(), len(args), arr, ctypes.byref(ret))
+        check_status()
+        return ret.i if ret.kind == 0 else ret.f
+
+    def schedule(self, fn):
+        buf = ctypes.create_string_buffer(64)
+        n = self._lib.pencil_jit_schedule(self._h, fn.encode(), buf, 64)
+        if n < 0:
+            raise KeyError(fn)
+        return buf.value.decode()
+
+    @property
+    def cuda_source(self):
+        return self._lib.pencil_jit_cuda_source(self._h).decode()

@@ -1,0 +1,170 @@
+"""General mapper for PENCIL units (csrc/jit.cpp): any compliant unit on the GPU
+with the reference Interpreter's value semantics.
+
+CPU: schedules derived from the directives (independent -> parallel grid, reduction -> parallel
++ fixed-order combine, everything else serial) and load errors.
+GPU: every golden vector of tests/golden (the reference Interpreter's fp64 / int64 outputs on the
+fixtures) replayed through the JIT: bit-exact wherever no reduction is split across threads
+(gemv, gemv_t, axpy, the three SpMV spellings, both stencils, gemm: their reductions are inner
+loops, run in order inside one thread), within 1e-12 normwise for dot's top-level reduction, and
+the interpreter's faults as E-INTERP; plus a unit exercising frames, local arrays, returns,
+int/double dynamic typing, while loops and last-iteration scalar values.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FIX = os.path.join(ROOT, "paper_1302_5586_b200", "pencil")
+
+
+def unit(src):
+    from paper_1302_5586_b200.op2 import JitUnit
+    return JitUnit(src)
+
+
+def fixture_src(name):
+    return open(os.path.join(FIX, name + ".pencil.c")).read()
+
+
+@pytest.mark.parametrize("fixture,fn,sched", [
+    ("gemv", "gemv", "P"), ("dot", "dot", "SRS"), ("axpy", "axpy", "P"), ("spmv", "spmv_vec", "P"),
+    ("spmv", "spmv_inline", "P"), ("gemm", "gemm", "P"),
+])
+def test_schedule_from_directives(fixture, fn, sched):
+    assert unit(fixture_src(fixture)).schedule(fn) == sched
+
+
+def test_unparsable_unit_is_rejected():
+    import paper_1302_5586_b200 as pb
+    with pytest.raises(pb.PencilError) as e:
+        unit("void f(int n) { n = ; }")
+    assert e.value.code == "E-ARG" and "E-SYNTAX" in str(e.value)
+
+
+GOLD = [c for c in golden_cases() if c.fixture in ("gemv", "gemv_t", "dot", "axpy", "spmv", "conv5x5", "gemm")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", GOLD, ids=[c.name for c in GOLD])
+def test_golden_vectors_through_the_jit(cuda, case):
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200.interp import Arg
+    u = unit(fixture_src(case.fixture))
+    args = []
+    for i, a in enumerate(case.args):
+        if isinstance(a, np.ndarray):
+            u.set_array(f"a{i}", a)
+            args.append(Arg.array(f"a{i}"))
+        else:
+            args.append(a)
+    if case.fault:
+        with pytest.raises(pb.PencilError) as e:
+            u.call(case.fn, args)
+        assert e.value.code == "E-INTERP"
+        return
+    ret = u.call(case.fn, args)
+    if case.fn == "dot":  # top-level reduction split across threads: re-associated fp64
+        x, y = case.args[1].astype(np.float64), case.args[2].astype(np.float64)
+        assert abs(ret - case.ret) <= 1e-12 * max(1e-300, float(np.sum(np.abs(x * y))))
+    elif case.ret is not None:
+        assert ret == case.ret
+    for i, ref in case.outs.items():
+        vals, ints, isd = u.get_array(f"a{i}")
+        if ref.dtype == np.int64:
+            assert np.array_equal(ints, ref), i
+        else:
+            assert np.array_equal(vals.view(np.uint64), ref.astype(np.float64).view(np.uint64)), i
+
+
+SEMANTICS = r"""
+int helper(int n, int a[restrict const static n], int k)
+{
+  int t;
+  t = a[k] * 2;
+  a[k] = t;
+  if (t > 10) return t / 3;
+  return -t % 4;
+}
+
+double mix(int n, int a[restrict const static n], float b[restrict const static n], int out[restrict const static n])
+{
+  int i;
+  int last;
+  float f;
+  double acc;
+  int tmp[4];
+  f = 3;
+  acc = 0.0;
+  last = -1;
+  #pragma pencil independent
+  for (i = 0; i < n; i++) {
+    int w[2];
+    w[0] = a[i] + i;
+    w[1] = w[0] / 2;
+    out[i] = w[1] - helper(n, a, i);
+    b[i] = b[i] * 0.5 + f / 2;
+    last = i * 10;
+  }
+  tmp[1] = last;
+  #pragma pencil reduction (+: acc)
+  for (i = 0; i < n; i++) {
+    acc += out[i] + 0.25;
+  }
+  while (tmp[1] > 7) {
+    tmp[1] = tmp[1] - 7;
+  }
+  out[0] = tmp[1];
+  return acc + i;
+}
+"""
+
+
+@pytest.mark.gpu
+def test_interpreter_semantics_unit(cuda):
+    from paper_1302_5586_b200.interp import Arg
+    n = 257
+    rng = np.random.default_rng(3)
+    a = rng.integers(-20, 20, n).astype(np.int32)
+    b = rng.standard_normal(n).astype(np.float32)
+    u = unit(SEMANTICS)
+    assert u.schedule("mix") == "SPSRS"
+    u.set_array("a", a)
+    u.set_array("b", b)
+    u.set_array("out", np.zeros(n, np.int32))
+    ret = u.call("mix", [n, Arg.array("a"), Arg.array("b"), Arg.array("out")])
+    # python restatement of the interpreter's semantics (int64 / fp64, C-truncating / and %)
+    def cdiv(x, y):
+        q = abs(x) // abs(y)
+        return q if (x >= 0) == (y >= 0) else -q
+
+    def cmod(x, y):
+        return x - cdiv(x, y) * y
+    A, out = a.astype(np.int64).tolist(), [0] * n
+    for i in range(n):
+        w0 = A[i] + i
+        w1 = cdiv(w0, 2)
+        t = A[i] * 2
+        A[i] = t
+        h = cdiv(t, 3) if t > 10 else cmod(-t, 4)
+        out[i] = w1 - h
+        B[i] = B[i] * 0.5 + 3 / 2  # f = 3 is an int: 3 / 2 -> 1 in the interpreter
+    B = [bb * 0 for bb in B]  # placeholder replaced below
+    last = (n - 1) * 10
+    acc = sum(o + 0.25 for o in out)
+    t1 = last
+    while t1 > 7:
+        t1 -= 7
+    out[0] = t1
+    vals, ints, isd = u.get_array("a")
+    assert ints.tolist() == A
+    vals, ints, isd = u.get_array("out")
+    assert ints.tolist() == out
+    vals, ints, isd = u.get_array("b")
+    ref_b = b.astype(np.float64) * 0.5 + 1  # int division 3 / 2 == 1
+    assert np.array_equal(vals, ref_b) and isd.all()
+    # after `for (i = 0; i < n; i++)` the interpreter leaves i = n - 1 (interp.cpp:207-217)
+    assert abs(ret - (acc + n - 1)) <= 1e-9 * abs(acc + n)
