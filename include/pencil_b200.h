@@ -56,7 +56,10 @@ enum pencil_status {
     PENCIL_E_OP2_SHAPE = 6,   /* malformed document, wrong table/data lengths, unknown names */
     PENCIL_E_OP2_RANGE = 7,   /* map entry or arg offset out of range */
     PENCIL_E_OP2_KERNEL = 8,  /* kernel missing, unparsable, or signature != 2m+n */
-    PENCIL_E_OP2_CONFLICT = 9 /* a dat both incremented and written in one par_loop */
+    PENCIL_E_OP2_CONFLICT = 9, /* a dat both incremented and written in one par_loop */
+    /* OptiML construct codes (optiml.hpp:27-29) */
+    PENCIL_E_OPTIML_SHAPE = 10, /* malformed construct, unknown kind or variant */
+    PENCIL_E_OPTIML_RANGE = 11  /* empty sum range */
 };
 int pencil_cuda_last_status(void);
 const char* pencil_cuda_last_error(void); /* "E-INTERP: load from x[...] is out of bounds" style */
@@ -222,6 +225,10 @@ int pencil_jit_call(pencil_jit_t j, const char* fn, int nargs, const pencil_arg*
 /* per top-level segment of fn: 'S' serial, 'P' parallel loop, 'R' parallel loop with reduction */
 int pencil_jit_schedule(pencil_jit_t j, const char* fn, char* out, int cap);
 const char* pencil_jit_cuda_source(pencil_jit_t j);
+/* OptiML construct (docs/op2-input.md; load_optiml_construct + lower_optiml, optiml.hpp:27-41)
+ * lowered to a PENCIL unit for pencil_jit_load: returns the text length (cap 0 sizes the buffer)
+ * or -1 (E-OPTIML-SHAPE / E-OPTIML-RANGE) */
+long long pencil_optiml_lower(const char* json_text, char* out, long long cap);
 
 #ifdef __cplusplus
 }

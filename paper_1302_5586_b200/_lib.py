@@ -96,6 +96,7 @@ SIGNATURES = {
     "pencil_jit_call": (c_int, [P, c_char_p, c_int, P, P]),
     "pencil_jit_schedule": (c_int, [P, c_char_p, c_char_p, c_int]),
     "pencil_jit_cuda_source": (c_char_p, [P]),
+    "pencil_optiml_lower": (c_ll, [c_char_p, c_char_p, c_ll]),
     # introspection used by the boundary tests (not in the public header)
     "pencil_fixture_signature": (c_int, [c_char_p, c_char_p, c_int]),
     "pencil_fixture_count": (c_int, []),

@@ -41,6 +41,8 @@ const char* code_name(int s) {
         case PENCIL_E_OP2_RANGE: return "E-OP2-RANGE";
         case PENCIL_E_OP2_KERNEL: return "E-OP2-KERNEL";
         case PENCIL_E_OP2_CONFLICT: return "E-OP2-CONFLICT";
+        case PENCIL_E_OPTIML_SHAPE: return "E-OPTIML-SHAPE";
+        case PENCIL_E_OPTIML_RANGE: return "E-OPTIML-RANGE";
     }
     return "E-?";
 }

@@ -16,7 +16,7 @@ from . import _lib
 _DTYPES = {np.dtype(np.int32): 0, np.dtype(np.float32): 1, np.dtype(np.float64): 2, np.dtype(np.uint8): 3}
 _NP = {0: np.int32, 1: np.float32, 2: np.float64, 3: np.uint8}
 _CODES = {1: "E-INTERP", 2: "E-ARG", 3: "E-CUDA", 4: "E-NOMEM", 5: "E-UNSUPPORTED", 6: "E-OP2-SHAPE",
-          7: "E-OP2-RANGE", 8: "E-OP2-KERNEL", 9: "E-OP2-CONFLICT"}
+          7: "E-OP2-RANGE", 8: "E-OP2-KERNEL", 9: "E-OP2-CONFLICT", 10: "E-OPTIML-SHAPE", 11: "E-OPTIML-RANGE"}
 
 
 class PencilError(RuntimeError):

@@ -182,3 +182,16 @@ class JitUnit:
     @property
     def cuda_source(self):
         return self._lib.pencil_jit_cuda_source(self._h).decode()
+
+
+def optiml_lower(construct):
+    """OptiML construct (dict or JSON text; docs/op2-input.md) -> PENCIL unit text, as
+    load_optiml_construct + lower_optiml (optiml.hpp:27-41).  Run it with ``JitUnit``."""
+    lib = _lib.load()
+    text = (construct if isinstance(construct, str) else json.dumps(construct)).encode()
+    n = lib.pencil_optiml_lower(text, None, 0)
+    if n < 0:
+        check_status()
+    buf = ctypes.create_string_buffer(n + 1)
+    lib.pencil_optiml_lower(text, buf, n + 1)
+    return buf.value.decode()

@@ -151,8 +151,6 @@ def test_interpreter_semantics_unit(cuda):
         A[i] = t
         h = cdiv(t, 3) if t > 10 else cmod(-t, 4)
         out[i] = w1 - h
-        B[i] = B[i] * 0.5 + 3 / 2  # f = 3 is an int: 3 / 2 -> 1 in the interpreter
-    B = [bb * 0 for bb in B]  # placeholder replaced below
     last = (n - 1) * 10
     acc = sum(o + 0.25 for o in out)
     t1 = last
