@@ -225,6 +225,14 @@ int pencil_jit_call(pencil_jit_t j, const char* fn, int nargs, const pencil_arg*
 /* per top-level segment of fn: 'S' serial, 'P' parallel loop, 'R' parallel loop with reduction */
 int pencil_jit_schedule(pencil_jit_t j, const char* fn, char* out, int cap);
 const char* pencil_jit_cuda_source(pencil_jit_t j);
+/* access summary of fn's array parameters: "name=r|w|rw|-[!]" comma separated,
+ * "!" = written in full before any read; returns the length or -1 */
+int pencil_jit_access(pencil_jit_t j, const char* fn, char* out, int cap);
+/* call on HOST arrays (args[i] of kind PENCIL_ARG_ARRAY use host[i], dtypes[i], counts[i]) with
+ * uploads / downloads planned from the access summary; bytes moved: pencil_jit_last_traffic */
+int pencil_jit_call_host(pencil_jit_t j, const char* fn, int nargs, const pencil_arg* args, void* const* host,
+                         const int* dtypes, const long long* counts, pencil_value* ret);
+int pencil_jit_last_traffic(pencil_jit_t j, long long* h2d, long long* d2h);
 /* OptiML construct (docs/op2-input.md; load_optiml_construct + lower_optiml, optiml.hpp:27-41)
  * lowered to a PENCIL unit for pencil_jit_load: returns the text length (cap 0 sizes the buffer)
  * or -1 (E-OPTIML-SHAPE / E-OPTIML-RANGE) */

@@ -97,6 +97,9 @@ SIGNATURES = {
     "pencil_jit_schedule": (c_int, [P, c_char_p, c_char_p, c_int]),
     "pencil_jit_cuda_source": (c_char_p, [P]),
     "pencil_optiml_lower": (c_ll, [c_char_p, c_char_p, c_ll]),
+    "pencil_jit_access": (c_int, [P, c_char_p, c_char_p, c_int]),
+    "pencil_jit_call_host": (c_int, [P, c_char_p, c_int, P, P, P, P, P]),
+    "pencil_jit_last_traffic": (c_int, [P, ctypes.POINTER(c_ll), ctypes.POINTER(c_ll)]),
     # introspection used by the boundary tests (not in the public header)
     "pencil_fixture_signature": (c_int, [c_char_p, c_char_p, c_int]),
     "pencil_fixture_count": (c_int, []),

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <set>
@@ -386,6 +387,221 @@ struct StoreArr {
     long long n = 0;
 };
 
+// ---- access summaries -> data movement (the reference's read / must / may sets,
+// access.hpp:39-53, summaries.cpp:635-663).  Per array parameter of a function: loaded anywhere
+// (through calls that pass it by name, too), stored anywhere, and must-written in full — a
+// top-level `for (i = 0; i < E; i++)` whose body unconditionally stores p[i] with E the
+// parameter's declared extent, and p never loaded.  Reads need the upload, stores need the
+// download, a must-written never-read array needs no upload.
+struct Access {
+    bool load = false, store = false, must_all = false;
+    int must_at = -1;  // scalar parameter k: the function unconditionally writes arr[k]
+};
+
+std::string expr_str(const pf::Expr& e) {
+    std::ostringstream o;
+    switch (e.kind) {
+        case pf::Expr::IntLit: o << e.ival; break;
+        case pf::Expr::FloatLit: o << e.fval; break;
+        case pf::Expr::Var: o << e.name; break;
+        default:
+            o << "(" << (int)e.kind << ":" << e.name << ":" << (int)e.bop << ":" << (int)e.uop;
+            for (const auto& a : e.args) o << "," << expr_str(*a);
+            o << ")";
+    }
+    return o.str();
+}
+
+struct Summarizer {
+    const pf::Unit& u;
+    std::map<std::string, std::vector<Access>> memo;
+    std::set<std::string> busy;
+    explicit Summarizer(const pf::Unit& unit) : u(unit) {}
+
+    const std::vector<Access>& of(const pf::Func& f) {
+        auto it = memo.find(f.name);
+        if (it != memo.end()) return it->second;
+        std::vector<Access> acc(f.params.size());
+        if (busy.count(f.name)) {  // recursion: everything may happen
+            for (auto& a : acc) a.load = a.store = true;
+            return memo[f.name] = acc;
+        }
+        busy.insert(f.name);
+        std::map<std::string, int> pos;
+        for (size_t i = 0; i < f.params.size(); i++)
+            if (f.params[i].kind != pf::Param::Scalar) pos[f.params[i].name] = (int)i;
+        std::function<void(const pf::Expr&)> ex = [&](const pf::Expr& e) {
+            if (e.kind == pf::Expr::Index || (e.kind == pf::Expr::Unary && e.uop == pf::Un::Deref && !e.args.empty() &&
+                                               e.args[0]->kind == pf::Expr::Var)) {
+                auto p = pos.find(e.kind == pf::Expr::Index ? e.name : e.args[0]->name);
+                if (p != pos.end()) acc[p->second].load = true;
+            }
+            if (e.kind == pf::Expr::Call) {
+                const pf::Func* c = u.find(e.name);
+                if (c) {
+                    const auto ca = of(*c);
+                    for (size_t k = 0; k < e.args.size() && k < c->params.size(); k++) {
+                        if (c->params[k].kind == pf::Param::Scalar || e.args[k]->kind != pf::Expr::Var) continue;
+                        auto p = pos.find(e.args[k]->name);
+                        if (p == pos.end()) continue;
+                        acc[p->second].load |= ca[k].load;
+                        acc[p->second].store |= ca[k].store;
+                    }
+                }
+            }
+            for (const auto& a : e.args)
+                if (!(e.kind == pf::Expr::Call && a->kind == pf::Expr::Var)) ex(*a);
+        };
+        std::function<void(const pf::Stmt&)> st = [&](const pf::Stmt& s) {
+            switch (s.kind) {
+                case pf::Stmt::Block:
+                    for (const auto& c : s.body) st(*c);
+                    break;
+                case pf::Stmt::Decl:
+                    for (const auto& e : s.extents) ex(*e);
+                    if (s.rhs) ex(*s.rhs);
+                    break;
+                case pf::Stmt::Assign: {
+                    ex(*s.rhs);
+                    const pf::Expr& lv = *s.lhs;
+                    std::string n;
+                    if (lv.kind == pf::Expr::Index) {
+                        n = lv.name;
+                        for (const auto& a : lv.args) ex(*a);
+                    } else if (lv.kind == pf::Expr::Unary && lv.uop == pf::Un::Deref) {
+                        n = lv.args[0]->name;
+                    }
+                    auto p = pos.find(n);
+                    if (p != pos.end()) {
+                        acc[p->second].store = true;
+                        if (s.aop != pf::AOp::Set) acc[p->second].load = true;  // compound: reads the old value
+                    }
+                    break;
+                }
+                case pf::Stmt::For:
+                    ex(*s.lo);
+                    ex(*s.hi);
+                    st(*s.loop_body);
+                    break;
+                case pf::Stmt::While:
+                    ex(*s.cond);
+                    st(*s.loop_body);
+                    break;
+                case pf::Stmt::If:
+                    ex(*s.cond);
+                    st(*s.then_s);
+                    if (s.else_s) st(*s.else_s);
+                    break;
+                case pf::Stmt::CallS: ex(*s.call); break;
+                case pf::Stmt::Return:
+                    if (s.rhs) ex(*s.rhs);
+                    break;
+                case pf::Stmt::Labeled: st(*s.loop_body); break;
+                case pf::Stmt::Nop: break;
+            }
+        };
+        if (f.body) st(*f.body);
+        // ACCESS-summarised function (summaries.cpp:635-648): its summary function's DEF / USE /
+        // MAY_DEF statements, mapped through the binding's arguments, declare what it touches
+        if (!f.access_fn.empty()) {
+            const pf::Func* g = u.find(f.access_fn);
+            if (g && g->body) {
+                std::map<std::string, std::string> to_f;  // summary param -> f's param name
+                for (size_t j = 0; j < g->params.size() && j < f.access_args.size(); j++)
+                    if (f.access_args[j]->kind == pf::Expr::Var) to_f[g->params[j].name] = f.access_args[j]->name;
+                std::map<std::string, int> fscalar;
+                for (size_t i = 0; i < f.params.size(); i++)
+                    if (f.params[i].kind == pf::Param::Scalar) fscalar[f.params[i].name] = (int)i;
+                std::function<void(const pf::Stmt&, bool)> sm = [&](const pf::Stmt& s, bool top) {
+                    if (s.kind == pf::Stmt::Block) {
+                        for (const auto& c : s.body) sm(*c, top);
+                        return;
+                    }
+                    if (s.kind == pf::Stmt::For || s.kind == pf::Stmt::While || s.kind == pf::Stmt::Labeled) {
+                        sm(*s.loop_body, false);
+                        return;
+                    }
+                    if (s.kind == pf::Stmt::If) {
+                        sm(*s.then_s, false);
+                        if (s.else_s) sm(*s.else_s, false);
+                        return;
+                    }
+                    if (s.kind != pf::Stmt::Nop || s.summary < 0 || !s.lhs) return;
+                    const std::string base = s.lhs->kind == pf::Expr::Index ? s.lhs->name : s.lhs->name;
+                    auto m = to_f.find(base);
+                    if (m == to_f.end()) return;
+                    auto p = pos.find(m->second);
+                    if (p == pos.end()) return;
+                    if (s.summary == 1) acc[p->second].load = true;
+                    else acc[p->second].store = true;
+                    if (s.summary == 0 && top && s.lhs->kind == pf::Expr::Index && s.lhs->args.size() == 1 &&
+                        s.lhs->args[0]->kind == pf::Expr::Var) {
+                        auto k = to_f.find(s.lhs->args[0]->name);
+                        if (k != to_f.end() && fscalar.count(k->second)) acc[p->second].must_at = fscalar[k->second];
+                    }
+                };
+                sm(*g->body, true);
+            }
+        }
+        // an unconditional top-level `p[k] = ...` with k a scalar parameter
+        if (f.body && f.body->kind == pf::Stmt::Block) {
+            for (const auto& top : f.body->body) {
+                const pf::Stmt& s0 = *top;
+                if (s0.kind != pf::Stmt::Assign || s0.aop != pf::AOp::Set || s0.lhs->kind != pf::Expr::Index ||
+                    s0.lhs->args.size() != 1 || s0.lhs->args[0]->kind != pf::Expr::Var)
+                    continue;
+                auto p = pos.find(s0.lhs->name);
+                if (p == pos.end()) continue;
+                for (size_t i = 0; i < f.params.size(); i++)
+                    if (f.params[i].kind == pf::Param::Scalar && f.params[i].name == s0.lhs->args[0]->name)
+                        acc[p->second].must_at = (int)i;
+            }
+        }
+        // must-write-all: a top-level 0..extent loop storing p[i] unconditionally, directly or
+        // through a call whose summary must-writes the element at the loop variable
+        if (f.body && f.body->kind == pf::Stmt::Block) {
+            for (const auto& top : f.body->body) {
+                const pf::Stmt* L = top.get();
+                while (L->kind == pf::Stmt::Labeled) L = L->loop_body.get();
+                if (L->kind != pf::Stmt::For || L->lo->kind != pf::Expr::IntLit || L->lo->ival != 0) continue;
+                std::vector<const pf::Stmt*> body;
+                if (L->loop_body->kind == pf::Stmt::Block)
+                    for (const auto& c : L->loop_body->body) body.push_back(c.get());
+                else
+                    body.push_back(L->loop_body.get());
+                auto mark = [&](const std::string& arr) {
+                    auto p = pos.find(arr);
+                    if (p == pos.end() || !f.params[p->second].extent) return;
+                    if (expr_str(*f.params[p->second].extent) == expr_str(*L->hi)) acc[p->second].must_all = true;
+                };
+                for (const pf::Stmt* s : body) {
+                    if (s->kind == pf::Stmt::Assign && s->aop == pf::AOp::Set && s->lhs->kind == pf::Expr::Index &&
+                        s->lhs->args.size() == 1 && s->lhs->args[0]->kind == pf::Expr::Var &&
+                        s->lhs->args[0]->name == L->name)
+                        mark(s->lhs->name);
+                    if (s->kind == pf::Stmt::CallS) {
+                        const pf::Expr& c = *s->call;
+                        const pf::Func* g = u.find(c.name);
+                        if (!g) continue;
+                        const auto ga = of(*g);
+                        for (size_t k = 0; k < c.args.size() && k < g->params.size(); k++) {
+                            if (g->params[k].kind == pf::Param::Scalar || c.args[k]->kind != pf::Expr::Var) continue;
+                            const int at = ga[k].must_at;
+                            if (at >= 0 && at < (int)c.args.size() && c.args[at]->kind == pf::Expr::Var &&
+                                c.args[at]->name == L->name)
+                                mark(c.args[k]->name);
+                        }
+                    }
+                }
+            }
+        }
+        for (auto& a : acc)
+            if (a.load) a.must_all = false;
+        busy.erase(f.name);
+        return memo[f.name] = acc;
+    }
+};
+
 }  // namespace
 
 struct pencil_jit {
@@ -400,6 +616,7 @@ struct pencil_jit {
     unsigned long long* d_rng = nullptr;
     std::vector<cudaKernel_t> kernels_cache;
     std::map<std::string, cudaKernel_t> kern;
+    long long h2d = 0, d2h = 0;  // bytes moved by the last pencil_jit_call_host
 };
 
 namespace {
@@ -725,6 +942,102 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
         if (fw & 64u) m += " empty pointee;";
         return fail(PENCIL_E_INTERP, m);
     }
+    return pencil_internal_ok();
+}
+
+
+// per array parameter of fn: "name=r|w|rw|-" (+ "!" when must-written in full), comma separated
+int pencil_jit_access(pencil_jit_t J, const char* fn, char* out, int cap) {
+    if (!J || !fn) return -1;
+    const pf::Func* f = J->unit.find(fn);
+    if (!f) return -1;
+    Summarizer S(J->unit);
+    const auto& acc = S.of(*f);
+    std::string r;
+    for (size_t i = 0; i < f->params.size(); i++) {
+        if (f->params[i].kind == pf::Param::Scalar) continue;
+        const Access& a = acc[i];
+        if (!r.empty()) r += ",";
+        r += f->params[i].name + "=" + (a.load && a.store ? "rw" : a.load ? "r" : a.store ? "w" : "-");
+        if (a.must_all) r += "!";
+    }
+    if (out && cap > 0) {
+        size_t n = std::min<size_t>(r.size(), (size_t)cap - 1);
+        r.copy(out, n);
+        out[n] = 0;
+    }
+    return (int)r.size();
+}
+
+// Interpreter::call on HOST arrays with the data movement planned from the access summary:
+// args[i] of kind PENCIL_ARG_ARRAY take host[i] (dtype dtypes[i], counts[i] elements); an array
+// is uploaded when it is read or only partly written, downloaded (converted back to its dtype)
+// when it is written; a must-written, never-read array is not uploaded.  The bytes moved are
+// reported by pencil_jit_last_traffic.
+int pencil_jit_call_host(pencil_jit_t J, const char* fn, int nargs, const pencil_arg* args, void* const* host,
+                         const int* dtypes, const long long* counts, pencil_value* ret) {
+    if (!J || !fn || (nargs && (!args || !host || !dtypes || !counts))) return fail(PENCIL_E_ARG, "E-ARG: null argument");
+    const pf::Func* f = J->unit.find(fn);
+    if (!f) return fail(PENCIL_E_INTERP, std::string("E-INTERP: no function named '") + fn + "'");
+    if ((size_t)nargs != f->params.size())
+        return fail(PENCIL_E_INTERP, "E-INTERP: wrong argument count for '" + f->name + "'");
+    int rc = setup(J);
+    if (rc) return rc;
+    Summarizer S(J->unit);
+    const auto acc = S.of(*f);
+    static const int esize[] = {4, 4, 8, 1};
+    std::vector<pencil_arg> a(args, args + nargs);
+    std::vector<std::string> names((size_t)nargs);
+    J->h2d = J->d2h = 0;
+    for (int i = 0; i < nargs; i++) {
+        if (f->params[i].kind == pf::Param::Scalar) continue;
+        if (!host[i] && counts[i]) return fail(PENCIL_E_ARG, "E-ARG: null host array");
+        if (dtypes[i] < 0 || dtypes[i] > 3) return fail(PENCIL_E_ARG, "E-ARG: unsupported dtype");
+        names[i] = "__host_arg_" + std::to_string(i);
+        const bool upload = acc[i].load || !acc[i].must_all;
+        if (upload) {
+            if ((rc = pencil_jit_set_array(J, names[i].c_str(), dtypes[i], host[i], counts[i]))) return rc;
+            J->h2d += counts[i] * esize[dtypes[i]];
+        } else {  // fully overwritten before any read: allocate only
+            StoreArr& s = J->store[names[i]];
+            if (s.n != counts[i]) {
+                cudaFree(s.bits);
+                cudaFree(s.tag);
+                s.bits = nullptr;
+                s.tag = nullptr;
+                JCK(cudaMalloc(&s.bits, std::max<size_t>(8, (size_t)counts[i] * 8)));
+                JCK(cudaMalloc(&s.tag, std::max<size_t>(8, (size_t)counts[i])));
+                s.n = counts[i];
+            }
+        }
+        a[i].kind = PENCIL_ARG_ARRAY;
+        a[i].array = names[i].c_str();
+    }
+    rc = pencil_jit_call(J, fn, nargs, a.data(), ret);
+    if (rc) return rc;
+    for (int i = 0; i < nargs; i++) {
+        if (f->params[i].kind == pf::Param::Scalar || !acc[i].store) continue;
+        const long long n = counts[i];
+        std::vector<double> v((size_t)n);
+        std::vector<long long> iv((size_t)n);
+        if ((rc = pencil_jit_get_array(J, names[i].c_str(), v.data(), nullptr, iv.data(), n))) return rc;
+        for (long long k = 0; k < n; k++) {
+            switch (dtypes[i]) {
+                case PENCIL_INT32: ((int*)host[i])[k] = (int)iv[k]; break;
+                case PENCIL_UINT8: ((unsigned char*)host[i])[k] = (unsigned char)iv[k]; break;
+                case PENCIL_FLOAT32: ((float*)host[i])[k] = (float)v[k]; break;
+                case PENCIL_FLOAT64: ((double*)host[i])[k] = v[k]; break;
+            }
+        }
+        J->d2h += n * esize[dtypes[i]];
+    }
+    return pencil_internal_ok();
+}
+
+int pencil_jit_last_traffic(pencil_jit_t J, long long* h2d, long long* d2h) {
+    if (!J) return fail(PENCIL_E_ARG, "E-ARG: null unit");
+    if (h2d) *h2d = J->h2d;
+    if (d2h) *d2h = J->d2h;
     return pencil_internal_ok();
 }
 

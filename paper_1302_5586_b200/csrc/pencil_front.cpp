@@ -391,13 +391,15 @@ struct Parser {
         if (peek().kind == Tok::Ident) {
             const std::string w = peek().text;
             if ((w == "DEF" || w == "USE" || w == "MAY_DEF") && peek(1).kind == Tok::Punct && peek(1).text == "(") {
-                // summary statement: no runtime effect
+                // summary statement: no runtime effect; kept for the data-movement planner
                 adv();
                 expect("(");
-                expr();
+                auto s = mks(Stmt::Nop, l);
+                s->summary = w == "DEF" ? 0 : w == "USE" ? 1 : 2;
+                s->lhs = expr();
                 expect(")");
                 expect(";");
-                return mks(Stmt::Nop, l);
+                return s;
             }
             if (peek(1).kind == Tok::Punct && peek(1).text == ":") {
                 auto s = mks(Stmt::Labeled, l);
@@ -534,13 +536,17 @@ struct Parser {
         if (peek().kind == Tok::Ident && peek().text == "ACCESS") {  // summary binding: no runtime effect
             adv();
             expect("(");
-            int depth = 1;
-            while (depth > 0) {
-                if (peek().kind == Tok::End) fail("unterminated ACCESS clause");
-                if (at_p("(")) depth++;
-                if (at_p(")")) depth--;
-                adv();
+            f.access_fn = ident("summary function name");
+            expect("(");
+            if (!at_p(")")) {
+                f.access_args.push_back(expr());
+                while (at_p(",")) {
+                    adv();
+                    f.access_args.push_back(expr());
+                }
             }
+            expect(")");
+            expect(")");
         }
         f.body = block();
         return f;

@@ -46,6 +46,7 @@ struct Stmt {
     StmtP then_s, else_s, loop_body;  // If / For, While, Labeled
     ExprP call;               // CallS
     std::vector<std::string> pragmas;  // `#pragma pencil ...` lines directly before the statement
+    int summary = -1;         // Nop from DEF (0) / USE (1) / MAY_DEF (2): target in lhs
     int line = 0;
 };
 
@@ -61,6 +62,8 @@ struct Func {
     std::string name;
     std::vector<Param> params;
     StmtP body;
+    std::string access_fn;             // ACCESS(summary_fn(args...)) binding, if any
+    std::vector<ExprP> access_args;
 };
 
 struct Unit {

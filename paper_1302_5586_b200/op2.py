@@ -195,3 +195,48 @@ def optiml_lower(construct):
     buf = ctypes.create_string_buffer(n + 1)
     lib.pencil_optiml_lower(text, buf, n + 1)
     return buf.value.decode()
+
+
+def _jit_access(self, fn):
+    """Access summary of fn's array parameters: {name: ("r"|"w"|"rw"|"-", must_write_all)}."""
+    buf = ctypes.create_string_buffer(4096)
+    n = self._lib.pencil_jit_access(self._h, fn.encode(), buf, 4096)
+    if n < 0:
+        raise KeyError(fn)
+    out = {}
+    for item in filter(None, buf.value.decode().split(",")):
+        name, mode = item.split("=")
+        out[name] = (mode.rstrip("!"), mode.endswith("!"))
+    return out
+
+
+def _jit_call_host(self, fn, args):
+    """Call on host numpy arrays; uploads/downloads planned from the access summary (written
+    arrays are updated in place).  Returns (value, (h2d_bytes, d2h_bytes))."""
+    from ._lib import pencil_arg as PencilArg, pencil_value as PencilValue
+    n = len(args)
+    arr = (PencilArg * max(1, n))()
+    host = (ctypes.c_void_p * max(1, n))()
+    dts = (ctypes.c_int * max(1, n))()
+    cnt = (ctypes.c_longlong * max(1, n))()
+    code = {np.dtype(np.int32): 0, np.dtype(np.float32): 1, np.dtype(np.float64): 2, np.dtype(np.uint8): 3}
+    for i, a in enumerate(args):
+        if isinstance(a, np.ndarray):
+            if a.dtype not in code or not a.flags.c_contiguous:
+                raise TypeError("host arrays must be contiguous int32/float32/float64/uint8")
+            arr[i].kind = 2
+            host[i], dts[i], cnt[i] = a.ctypes.data, code[a.dtype], a.size
+        elif isinstance(a, (int, np.integer)):
+            arr[i].kind, arr[i].i = 0, int(a)
+        else:
+            arr[i].kind, arr[i].f = 1, float(a)
+    ret = PencilValue()
+    self._lib.pencil_jit_call_host(self._h, fn.encode(), n, arr, host, dts, cnt, ctypes.byref(ret))
+    check_status()
+    h2d, d2h = ctypes.c_longlong(), ctypes.c_longlong()
+    self._lib.pencil_jit_last_traffic(self._h, ctypes.byref(h2d), ctypes.byref(d2h))
+    return (ret.i if ret.kind == 0 else ret.f), (h2d.value, d2h.value)
+
+
+JitUnit.access = _jit_access
+JitUnit.call_host = _jit_call_host
