@@ -174,6 +174,116 @@ __global__ void __launch_bounds__(SPMV_THREADS, (WCH <= 128 ? CTAS_PER_SM : 6)) 
     }  // tickets
 }
 
+// 128-bit variant (PENCIL_SPMV_KERNEL=vec): the same tiles, batches and fold, but each lane
+// streams 4 CONSECUTIVE non-zeros with one 16-byte load per array (chunks are 4-aligned windows
+// [qa, qa + 128); lanes whose 4 positions miss the batch's range do not load) and stores its 4
+// products with one 16-byte shared store: 2 + 1 instructions where the scalar kernel issues
+// 8 + 4.  The staging pad moves to 4 floats per 32 (aligned for the vector store; still
+// conflict-free for rows of equal length).  Needs 16-byte-aligned col / val.
+__device__ __forceinline__ int skew4(int t) { return t + 4 * (t >> 5); }
+template <bool ASSOC, int VU>
+__global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_vec_kernel(
+    int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
+    const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
+    const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
+    unsigned* __restrict__ status) {
+    __shared__ __align__(16) float s_prod[WARPS_PER_CTA][128 * VU + 16 * VU];
+    if (plan[0]) {
+        spmv_generic(nrows, ncols, nnz_len, rowptr, col, val, x, y, status);
+        return;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
+    float* sp = s_prod[warp];
+    for (;;) {
+        unsigned ticket = 0;
+        if (lane == 0) ticket = atomicAdd(&plan[1], 1u);
+        ticket = __shfl_sync(0xffffffffu, ticket, 0);
+        if (ticket >= (unsigned)ntiles) {
+            if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
+            return;
+        }
+        const int r0 = __ldg(tile_row + ticket), r1 = __ldg(tile_row + ticket + 1);
+        for (int rb = r0; rb < r1; rb += 32) {
+            const int re = min(rb + 32, r1);
+            const int row = rb + lane;
+            const bool active = row < re;
+            int my_s = 0, my_e = 0;
+            if (active) {
+                my_s = __ldg(rowptr + row);
+                my_e = __ldg(rowptr + row + 1);
+            }
+            const int q_begin = max(__shfl_sync(0xffffffffu, my_s, 0), 0);
+            const int q_end = min(__ldg(rowptr + re), nnz_len);
+            float s = 0.f;
+            for (int qa = q_begin & ~3; qa < q_end; qa += 128 * VU) {
+                float pr[VU][4];
+                int c[VU][4];
+                float v[VU][4];
+#pragma unroll
+                for (int u = 0; u < VU; u++) {
+                    const int p = qa + 128 * u + 4 * lane;
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        pr[u][k] = 0.f;
+                        c[u][k] = -1;
+                        v[u][k] = 0.f;
+                    }
+                    if (p + 3 >= q_begin && p < q_end) {
+                        if (p + 3 < nnz_len) {
+                            const int4 c4 = ld_stream_i4(reinterpret_cast<const int4*>(col + p));
+                            const float4 v4 = ld_stream_f4(reinterpret_cast<const float4*>(val + p));
+                            c[u][0] = c4.x; c[u][1] = c4.y; c[u][2] = c4.z; c[u][3] = c4.w;
+                            v[u][0] = v4.x; v[u][1] = v4.y; v[u][2] = v4.z; v[u][3] = v4.w;
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 4; k++) {
+                                c[u][k] = p + k < nnz_len ? __ldg(col + p + k) : 0;
+                                v[u][k] = p + k < nnz_len ? __ldg(val + p + k) : 0.f;
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < VU; u++) {
+                    const int p = qa + 128 * u + 4 * lane;
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        if (p + k >= q_begin && p + k < q_end) {
+                            float xv = 0.f;
+                            if ((unsigned)c[u][k] < (unsigned)ncols) xv = ld_keep_f(x + c[u][k]);
+                            else raise_fault(status, FAULT_OOB_LOAD);
+                            pr[u][k] = __fmul_rn(v[u][k], xv);  // the product rounds on its own
+                        }
+                    }
+                    *reinterpret_cast<float4*>(sp + skew4(128 * u + 4 * lane)) =
+                        make_float4(pr[u][0], pr[u][1], pr[u][2], pr[u][3]);
+                }
+                __syncwarp();
+                const int lo = max(my_s, qa), hi = min(my_e, qa + 128 * VU);
+                if (ASSOC) {
+                    unsigned big = __ballot_sync(0xffffffffu, hi - lo > 16);
+                    if (hi - lo <= 16)
+                        for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[skew4(t - qa)]);
+                    while (big) {
+                        const int o = __ffs(big) - 1;
+                        big &= big - 1;
+                        const int olo = __shfl_sync(0xffffffffu, lo, o), ohi = __shfl_sync(0xffffffffu, hi, o);
+                        float part = 0.f;
+                        for (int t = olo + lane; t < ohi; t += 32) part += sp[skew4(t - qa)];
+                        part = warp_sum<32>(part);
+                        if (lane == o) s += part;
+                    }
+                } else {
+                    for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[skew4(t - qa)]);
+                }
+                __syncwarp();
+            }
+            if (active) y[row] = s;
+        }
+    }
+}
+
 // TMA-fed variant (experimental, PENCIL_SPMV_KERNEL=tma).  The LSU path above spends the SM's
 // L1TEX miss-request bandwidth (the limiter, ~1 request per clock) on both the x gathers AND
 // the col/val stream.  Here the stream comes in through the TMA engine instead: each warp
@@ -385,12 +495,35 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     // register prefetch of the next chunk's column indices (1.34 ms at 8 CTAs/SM, 1.39 at 7:
     // the ~38% of stall samples on first use of col[] are the request path being full, not
     // latency that more loads in flight could hide).
-    static int use_tma = -1;
+    static int use_tma = -1, use_vec = -1;
     if (use_tma < 0) {
         const char* e = getenv("PENCIL_SPMV_KERNEL");
         use_tma = (e && !strcmp(e, "tma"));
+        // default: the 128-bit kernel (1.263 ms at 2^24 rows vs 1.288 for the scalar-load one,
+        // PENCIL_SPMV_KERNEL=lsu; PENCIL_SPMV_VU=2, 8 non-zeros per lane: 1.355)
+        use_vec = !(e && (!strcmp(e, "lsu") || !strcmp(e, "tma")));
     }
     cudaError_t e;
+    if (use_vec && (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
+        static int vu = -1;
+        if (vu < 0) {
+            const char* w = getenv("PENCIL_SPMV_VU");
+            vu = (w && w[0] == '2') ? 2 : 1;
+        }
+        if (vu == 2) {
+            if ((int)cfg.gridDim.x > PENCIL_NUM_SMS * 6) cfg.gridDim = dim3(PENCIL_NUM_SMS * 6);
+            if (assoc)
+                return (int)cudaLaunchKernelEx(&cfg, csr_vec_kernel<true, 2>, nrows, ncols, nnz_len, rowptr, col, val,
+                                               x, y, tile_row, ntiles, plan_flags, status);
+            return (int)cudaLaunchKernelEx(&cfg, csr_vec_kernel<false, 2>, nrows, ncols, nnz_len, rowptr, col, val, x,
+                                           y, tile_row, ntiles, plan_flags, status);
+        }
+        if (assoc)
+            return (int)cudaLaunchKernelEx(&cfg, csr_vec_kernel<true, 1>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                           tile_row, ntiles, plan_flags, status);
+        return (int)cudaLaunchKernelEx(&cfg, csr_vec_kernel<false, 1>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                       tile_row, ntiles, plan_flags, status);
+    }
     if (use_tma && grid > PENCIL_NUM_SMS * TMA_CTAS_PER_SM) cfg.gridDim = dim3(PENCIL_NUM_SMS * TMA_CTAS_PER_SM);
     if (use_tma) {
         if (assoc)
