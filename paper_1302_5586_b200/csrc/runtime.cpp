@@ -279,8 +279,10 @@ struct PipeCtx {
     int* host_rows = nullptr;  // pinned: [0] plan flag, [1..K+1] block boundary rows
 };
 std::map<int, PipeCtx*> g_pipe;
+std::mutex g_pipe_mu;  // the map is shared by all devices (each PipeCtx is used under its DeviceCtx::mu)
 
 int get_pipe(DeviceCtx* c, PipeCtx** out) {
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
     auto it = g_pipe.find(c->device);
     if (it != g_pipe.end()) {
         *out = it->second;
