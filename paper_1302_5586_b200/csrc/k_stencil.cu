@@ -26,7 +26,10 @@
 namespace {
 
 constexpr int S_WARPS = 4;
-constexpr int S_BAND = 64;
+#ifndef STENCIL_BAND
+#define STENCIL_BAND 64
+#endif
+constexpr int S_BAND = STENCIL_BAND;  // output rows per warp sweep (swept 32/64/128/256: 64 ~ 128 best, within 1%)
 #ifndef STENCIL_RING
 #define STENCIL_RING 8
 #endif
