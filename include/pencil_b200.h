@@ -175,6 +175,8 @@ int pencil_shard_gemm_grid(int m, int n, int nshards, int* grid_rows, int* grid_
 
 /* ===== 7. Introspection / measurement =================================================== */
 const char* pencil_version(void);
+/* bytes the last drop-in call on this thread moved host->device and device->host */
+int pencil_last_transfer_bytes(long long* h2d, long long* d2h);
 int pencil_l2_flush(pencil_stream_t s); /* write a buffer larger than L2 (timing hygiene) */
 int pencil_micro_gather(pencil_stream_t s, int mode, long long n, const int* idx,
                         const float* table, float* out);

@@ -68,6 +68,7 @@ SIGNATURES = {
     "pencil_shard_gemm_grid": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     # §7
     "pencil_version": (c_char_p, []),
+    "pencil_last_transfer_bytes": (c_int, [ctypes.POINTER(c_ll), ctypes.POINTER(c_ll)]),
     "pencil_l2_flush": (c_int, [P]),
     "pencil_micro_gather": (c_int, [P, c_int, c_ll, P, P, P]),
     "pencil_micro_copy": (c_int, [P, c_ll, P, P]),

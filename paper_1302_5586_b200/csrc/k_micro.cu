@@ -121,3 +121,4 @@ int launch_micro_l2_flush(cudaStream_t st, long long n, float* buf) {
     micro_fill_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>(n >> 2, reinterpret_cast<float4*>(buf), v);
     return (int)cudaGetLastError();
 }
+
