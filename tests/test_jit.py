@@ -166,3 +166,91 @@ def test_interpreter_semantics_unit(cuda):
     assert np.array_equal(vals, ref_b) and isd.all()
     # after `for (i = 0; i < n; i++)` the interpreter leaves i = n - 1 (interp.cpp:207-217)
     assert abs(ret - (acc + n - 1)) <= 1e-9 * abs(acc + n)
+
+
+REDUCTIONS = r"""
+double red4(int n, int a[restrict const static n], float b[restrict const static n], int out[restrict const static 4])
+{
+  int i;
+  int s;
+  int p;
+  int mx;
+  double mn;
+  s = 0;
+  p = 1;
+  mx = -1000000;
+  mn = 1000000.0;
+  #pragma pencil reduction (+: s)
+  for (i = 0; i < n; i++) {
+    s += a[i] * 3 - i % 7;
+  }
+  #pragma pencil reduction (*: p)
+  for (i = 0; i < n; i++) {
+    if (a[i] % 5 == 0) p *= -1;
+  }
+  #pragma pencil reduction (max: mx)
+  for (i = 0; i < n; i++) {
+    if (a[i] > mx) mx = a[i];
+  }
+  #pragma pencil reduction (min: mn)
+  for (i = 0; i < n; i++) {
+    if (b[i] < mn) mn = b[i];
+  }
+  out[0] = s;
+  out[1] = p;
+  out[2] = mx;
+  return mn;
+}
+
+void oob(int n, int a[restrict const static n])
+{
+  int i;
+  #pragma pencil independent
+  for (i = 0; i < n; i++) {
+    a[i + 1] = i;
+  }
+}
+
+int divz(int n, int a[restrict const static n])
+{
+  int i;
+  int t;
+  t = 0;
+  for (i = 0; i < n; i++) {
+    t = t + 100 / (a[i] - 3);
+  }
+  return t;
+}
+"""
+
+
+@pytest.mark.gpu
+def test_reductions_and_faults(cuda):
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200.interp import Arg
+    n = 100003
+    rng = np.random.default_rng(9)
+    a = rng.integers(-10000, 10000, n).astype(np.int32)
+    b = rng.standard_normal(n).astype(np.float32)
+    u = unit(REDUCTIONS)
+    assert u.schedule("red4") == "SRRRRS"
+    u.set_array("a", a)
+    u.set_array("b", b)
+    u.set_array("out", np.zeros(4, np.int32))
+    mn = u.call("red4", [n, Arg.array("a"), Arg.array("b"), Arg.array("out")])
+    _, ints, _ = u.get_array("out")
+    i = np.arange(n)
+    a64 = a.astype(np.int64)
+    s_ref = int(np.sum(a64 * 3 - (i % 7)))
+    p_ref = (-1) ** int(np.sum(np.fmod(a64, 5) == 0))
+    assert ints[:3].tolist() == [s_ref, p_ref, int(a.max())]
+    assert mn == float(b.astype(np.float64).min())  # min is exact whatever the order
+    # a store past the end inside a parallel loop, and a division by zero: E-INTERP like the interpreter
+    u.set_array("z", np.zeros(16, np.int32))
+    with pytest.raises(pb.PencilError) as e:
+        u.call("oob", [16, Arg.array("z")])
+    assert e.value.code == "E-INTERP" and "store out of bounds" in str(e.value)
+    u.set_array("d", np.array([1, 2, 3, 4], np.int32))
+    with pytest.raises(pb.PencilError) as e:
+        u.call("divz", [4, Arg.array("d")])
+    assert e.value.code == "E-INTERP" and "division by zero" in str(e.value)
