@@ -166,7 +166,7 @@ def bench_spmv(args, torch, pb, rank, world, dist):
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
            "config": {"workload": "CSR SpMV fp32 (spmv_vec), power-law rows 2^24 x 2^24, 16 nnz/row",
                       "nrows": nrows, "ncols": nrows, "nnz": nnz, "alpha": 1.5, "xm": round(xm, 4),
-                      "maxlen": 4096, "seed": 42, "schedule": "csr_vec_kernel, reassociated (persistent warps, 1024-nnz window tiles, 128-bit col/val streams)",
+                      "maxlen": 4096, "seed": 42, "schedule": "csr_flow_kernel, reassociated (persistent warps, 1024-nnz window tiles, continuous 128-bit col/val streams)",
                       "l2": "256 MiB flush between steps, outside the per-step events; inputs 2.35 GB > L2"}}
     if rank == 0 and world == 1 and not args.no_e2e:
         res["e2e"] = e2e_spmv(args, torch, pb, rowptr, col, val, x)
@@ -408,11 +408,11 @@ def main():
                 "config": dict(res["config"], parallelism=f"row-sharded x{world}" if world > 1 else "single GPU"),
                 "gpu_launches": res["launches"]}
         if world == 1:
-            line["roofline"] = {"bound": "hbm", "kernel": "csr_vec_kernel", "achieved": kernel_gbs,
+            line["roofline"] = {"bound": "hbm", "kernel": "csr_flow_kernel", "achieved": kernel_gbs,
                                 "peak": hbm, "unit": "GB/s", "frac": kernel_gbs / hbm,
                                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
                                 "algorithmic_bytes_per_launch": res["bytes"],
-                                "traffic": ncu_traffic("csr_vec_kernel")}
+                                "traffic": ncu_traffic("csr_flow_kernel")}
         line["clocks"] = clk.summary()
         if "e2e" in res:
             line["e2e"] = res["e2e"]

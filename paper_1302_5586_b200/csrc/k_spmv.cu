@@ -8,7 +8,10 @@
 // (csr_plan_kernel), it gives every warp a contiguous row range holding ~TILE_NNZ
 // non-zeros regardless of the power-law row-length distribution.
 //
-// Executor (csr_stream_kernel): per tile, per batch of 32 rows, the batch's non-zeros
+// Executors (launch_csr_spmv picks one): csr_flow_kernel (default; the tile's non-zeros stream in
+// continuous 16-byte-per-lane windows, batches folded from whichever window holds them),
+// csr_vec_kernel (windows restart at each batch), csr_stream_kernel (scalar loads; any alignment).
+// The structure they share — csr_stream_kernel: per tile, per batch of 32 rows, the batch's non-zeros
 // are streamed with coalesced loads (col, val: evict-first) while x[col] is gathered
 // (evict-last, so the 64 MB vector stays L2-resident), staged in shared memory, then each
 // thread folds its own row in source order: s = s + val[k]*x[col[k]], product and sum each
@@ -195,26 +198,50 @@ __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_v
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
     float* sp = s_prod[warp];
+    // The control path is prefetched one step ahead so its latencies overlap the streaming:
+    // the next tile's ticket and bounds are drawn when a tile starts, and the next 32-row
+    // batch's row starts are loaded when a batch starts (one load per lane: row rb+lane's start;
+    // its end is lane+1's start, rowptr[min(rb + 32, r1)] closes the batch).
+    auto draw = [&](unsigned& t, int& a, int& b) {
+        unsigned v = 0;
+        if (lane == 0) v = atomicAdd(&plan[1], 1u);
+        t = __shfl_sync(0xffffffffu, v, 0);
+        if (t < (unsigned)ntiles) {
+            a = __ldg(tile_row + t);
+            b = __ldg(tile_row + t + 1);
+        }
+    };
+    auto batch_starts = [&](int rb, int r1, int& s_l, int& e_b) {
+        s_l = __ldg(rowptr + min(rb + lane, r1));
+        e_b = __ldg(rowptr + min(rb + 32, r1));
+    };
+    unsigned ticket;
+    int r0 = 0, r1 = 0;
+    draw(ticket, r0, r1);
     for (;;) {
-        unsigned ticket = 0;
-        if (lane == 0) ticket = atomicAdd(&plan[1], 1u);
-        ticket = __shfl_sync(0xffffffffu, ticket, 0);
         if (ticket >= (unsigned)ntiles) {
+            // every warp draws exactly one failing ticket; the last one re-arms the counter
             if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
             return;
         }
-        const int r0 = __ldg(tile_row + ticket), r1 = __ldg(tile_row + ticket + 1);
+        unsigned nticket;
+        int nr0 = 0, nr1 = 0;
+        draw(nticket, nr0, nr1);
+        int cur_s = 0, cur_e = 0;
+        if (r0 < r1) batch_starts(r0, r1, cur_s, cur_e);
         for (int rb = r0; rb < r1; rb += 32) {
+            int nxt_s = 0, nxt_e = 0;
+            if (rb + 32 < r1) batch_starts(rb + 32, r1, nxt_s, nxt_e);
             const int re = min(rb + 32, r1);
             const int row = rb + lane;
             const bool active = row < re;
-            int my_s = 0, my_e = 0;
-            if (active) {
-                my_s = __ldg(rowptr + row);
-                my_e = __ldg(rowptr + row + 1);
-            }
-            const int q_begin = max(__shfl_sync(0xffffffffu, my_s, 0), 0);
-            const int q_end = min(__ldg(rowptr + re), nnz_len);
+            int my_s = cur_s, my_e = __shfl_down_sync(0xffffffffu, cur_s, 1);
+            if (lane == 31) my_e = cur_e;
+            if (!active) my_s = my_e = 0;
+            const int q_begin = max(__shfl_sync(0xffffffffu, cur_s, 0), 0);
+            const int q_end = min(cur_e, nnz_len);
+            cur_s = nxt_s;
+            cur_e = nxt_e;
             float s = 0.f;
             for (int qa = q_begin & ~3; qa < q_end; qa += 128 * VU) {
                 float pr[VU][4];
@@ -256,9 +283,16 @@ __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_v
                             pr[u][k] = __fmul_rn(v[u][k], xv);  // the product rounds on its own
                         }
                     }
+#ifndef SPMV_NOFOLD
                     *reinterpret_cast<float4*>(sp + skew4(128 * u + 4 * lane)) =
                         make_float4(pr[u][0], pr[u][1], pr[u][2], pr[u][3]);
+#else  // timing experiment only (wrong results): no staging, no per-row fold
+                    s += (pr[u][0] + pr[u][1]) + (pr[u][2] + pr[u][3]);
+#endif
                 }
+#ifdef SPMV_NOFOLD
+                if (true) continue;
+#endif
                 __syncwarp();
                 const int lo = max(my_s, qa), hi = min(my_e, qa + 128 * VU);
                 if (ASSOC) {
@@ -280,6 +314,140 @@ __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_v
                 __syncwarp();
             }
             if (active) y[row] = s;
+        }
+        ticket = nticket;
+        r0 = nr0;
+        r1 = nr1;
+    }
+}
+
+// Continuous-stream variant (PENCIL_SPMV_KERNEL=flow): the tile's non-zeros are streamed in
+// full 4-aligned 128-element windows from its first to its last non-zero, independent of the
+// 32-row batches, and every batch overlapping a window is folded from it (a batch that ends
+// inside a window writes y and the next batch — prefetched — continues in the same window).
+// The batch-aligned kernel restarts its windows at every batch, so each 32-row batch (~512
+// non-zeros here) pays a partial first and last window.
+template <bool ASSOC>
+__global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_flow_kernel(
+    int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
+    const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
+    const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
+    unsigned* __restrict__ status) {
+    __shared__ __align__(16) float s_prod[WARPS_PER_CTA][128 + 16];
+    if (plan[0]) {
+        spmv_generic(nrows, ncols, nnz_len, rowptr, col, val, x, y, status);
+        return;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
+    float* sp = s_prod[warp];
+    auto clampp = [&](int v) { return v < 0 ? 0 : (v > nnz_len ? nnz_len : v); };
+    for (;;) {
+        unsigned ticket = 0;
+        if (lane == 0) ticket = atomicAdd(&plan[1], 1u);
+        ticket = __shfl_sync(0xffffffffu, ticket, 0);
+        if (ticket >= (unsigned)ntiles) {
+            if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
+            return;
+        }
+        const int r0 = __ldg(tile_row + ticket), r1 = __ldg(tile_row + ticket + 1);
+        if (r0 >= r1) continue;
+        // batch state: rows [rb, rb + 32), lane = row rb + lane; s_l = start of row rb + lane
+        int rb = r0;
+        int s_l = __ldg(rowptr + min(rb + lane, r1)), e_b = __ldg(rowptr + min(rb + 32, r1));
+        int n_s = 0, n_e = 0;  // the next batch, prefetched
+        if (rb + 32 < r1) {
+            n_s = __ldg(rowptr + min(rb + 32 + lane, r1));
+            n_e = __ldg(rowptr + min(rb + 64, r1));
+        }
+        const int P0 = clampp(__shfl_sync(0xffffffffu, s_l, 0));
+        const int P1 = max(P0, clampp(__ldg(rowptr + r1)));
+        auto bounds = [&](int& my_s, int& my_e) {
+            my_s = clampp(s_l);
+            my_e = __shfl_down_sync(0xffffffffu, s_l, 1);
+            if (lane == 31) my_e = e_b;
+            my_e = max(my_s, clampp(my_e));
+            if (rb + lane >= r1) my_s = my_e = 0;
+        };
+        int my_s, my_e;
+        bounds(my_s, my_e);
+        int bend = clampp(e_b);
+        float s = 0.f;
+        for (int qa = P0 & ~3; qa < P1; qa += 128) {
+            const int p = qa + 4 * lane;
+            float pr[4] = {0.f, 0.f, 0.f, 0.f};
+            if (p + 3 >= P0 && p < P1) {
+                int c[4];
+                float v[4];
+                if (p + 3 < nnz_len) {
+                    const int4 c4 = ld_stream_i4(reinterpret_cast<const int4*>(col + p));
+                    const float4 v4 = ld_stream_f4(reinterpret_cast<const float4*>(val + p));
+                    c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+                    v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        c[k] = p + k < nnz_len ? __ldg(col + p + k) : 0;
+                        v[k] = p + k < nnz_len ? __ldg(val + p + k) : 0.f;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    if (p + k >= P0 && p + k < P1) {
+                        float xv = 0.f;
+                        if ((unsigned)c[k] < (unsigned)ncols) xv = ld_keep_f(x + c[k]);
+                        else raise_fault(status, FAULT_OOB_LOAD);
+                        pr[k] = __fmul_rn(v[k], xv);  // the product rounds on its own
+                    }
+                }
+            }
+            *reinterpret_cast<float4*>(sp + skew4(4 * lane)) = make_float4(pr[0], pr[1], pr[2], pr[3]);
+            __syncwarp();
+            for (;;) {  // fold every batch overlapping this window
+                const int lo = max(my_s, qa), hi = min(my_e, qa + 128);
+                if (ASSOC) {
+                    unsigned big = __ballot_sync(0xffffffffu, hi - lo > 16);
+                    if (hi - lo <= 16)
+                        for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[skew4(t - qa)]);
+                    while (big) {
+                        const int o = __ffs(big) - 1;
+                        big &= big - 1;
+                        const int olo = __shfl_sync(0xffffffffu, lo, o), ohi = __shfl_sync(0xffffffffu, hi, o);
+                        float part = 0.f;
+                        for (int t = olo + lane; t < ohi; t += 32) part += sp[skew4(t - qa)];
+                        part = warp_sum<32>(part);
+                        if (lane == o) s += part;
+                    }
+                } else {
+                    for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[skew4(t - qa)]);
+                }
+                if (bend > qa + 128 || rb >= r1) break;  // the batch continues in the next window
+                if (rb + lane < r1) y[rb + lane] = s;      // batch complete
+                s = 0.f;
+                rb += 32;
+                if (rb >= r1) break;
+                s_l = n_s;
+                e_b = n_e;
+                if (rb + 32 < r1) {
+                    n_s = __ldg(rowptr + min(rb + 32 + lane, r1));
+                    n_e = __ldg(rowptr + min(rb + 64, r1));
+                }
+                bounds(my_s, my_e);
+                bend = clampp(e_b);
+            }
+            __syncwarp();
+        }
+        while (rb < r1) {  // batches past the last non-zero (empty rows)
+            if (rb + lane < r1) y[rb + lane] = s;
+            s = 0.f;
+            rb += 32;
+            if (rb >= r1) break;
+            s_l = n_s;
+            e_b = n_e;
+            if (rb + 32 < r1) {
+                n_s = __ldg(rowptr + min(rb + 32 + lane, r1));
+                n_e = __ldg(rowptr + min(rb + 64, r1));
+            }
         }
     }
 }
@@ -495,13 +663,22 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     // register prefetch of the next chunk's column indices (1.34 ms at 8 CTAs/SM, 1.39 at 7:
     // the ~38% of stall samples on first use of col[] are the request path being full, not
     // latency that more loads in flight could hide).
-    static int use_tma = -1, use_vec = -1;
+    static int use_tma = -1, use_vec = -1, use_flow = -1;
     if (use_tma < 0) {
         const char* e = getenv("PENCIL_SPMV_KERNEL");
         use_tma = (e && !strcmp(e, "tma"));
-        // default: the 128-bit kernel (1.263 ms at 2^24 rows vs 1.288 for the scalar-load one,
-        // PENCIL_SPMV_KERNEL=lsu; PENCIL_SPMV_VU=2, 8 non-zeros per lane: 1.355)
+        // default: the continuous-stream kernel (1.250 ms at 2^24 rows; batch-aligned 128-bit
+        // kernel `vec` 1.265-1.273; scalar-load kernel `lsu` 1.282-1.288; PENCIL_SPMV_VU=2 with vec,
+        // 8 non-zeros per lane: 1.355; a mask-free path for interior windows: 8 B of spills, no gain)
+        use_flow = !(e && (!strcmp(e, "lsu") || !strcmp(e, "tma") || !strcmp(e, "vec")));
         use_vec = !(e && (!strcmp(e, "lsu") || !strcmp(e, "tma")));
+    }
+    if (use_flow && (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
+        if (assoc)
+            return (int)cudaLaunchKernelEx(&cfg, csr_flow_kernel<true>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                           tile_row, ntiles, plan_flags, status);
+        return (int)cudaLaunchKernelEx(&cfg, csr_flow_kernel<false>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                       tile_row, ntiles, plan_flags, status);
     }
     cudaError_t e;
     if (use_vec && (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
