@@ -328,7 +328,10 @@ __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_v
 // The batch-aligned kernel restarts its windows at every batch, so each 32-row batch (~512
 // non-zeros here) pays a partial first and last window.
 template <bool ASSOC>
-__global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_flow_kernel(
+#ifndef FLOW_MINB
+#define FLOW_MINB CTAS_PER_SM
+#endif
+__global__ void __launch_bounds__(SPMV_THREADS, FLOW_MINB) csr_flow_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
     const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
@@ -391,15 +394,19 @@ __global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_flow_kernel(
                         v[k] = p + k < nnz_len ? __ldg(val + p + k) : 0.f;
                     }
                 }
+                // the 4 gathers issue unconditionally (masked / out-of-range entries read x[0]), so
+                // they leave back to back instead of one branch region each
+                bool use[4];
+                float xv[4];
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
-                    if (p + k >= P0 && p + k < P1) {
-                        float xv = 0.f;
-                        if ((unsigned)c[k] < (unsigned)ncols) xv = ld_keep_f(x + c[k]);
-                        else raise_fault(status, FAULT_OOB_LOAD);
-                        pr[k] = __fmul_rn(v[k], xv);  // the product rounds on its own
-                    }
+                    const bool in = p + k >= P0 && p + k < P1, ok = (unsigned)c[k] < (unsigned)ncols;
+                    use[k] = in && ok;
+                    xv[k] = ld_keep_f(x + (use[k] ? c[k] : 0));
+                    if (in && !ok) raise_fault(status, FAULT_OOB_LOAD);
                 }
+#pragma unroll
+                for (int k = 0; k < 4; k++) pr[k] = use[k] ? __fmul_rn(v[k], xv[k]) : 0.f;  // rounds on its own
             }
             *reinterpret_cast<float4*>(sp + skew4(4 * lane)) = make_float4(pr[0], pr[1], pr[2], pr[3]);
             __syncwarp();
