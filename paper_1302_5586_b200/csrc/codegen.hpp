@@ -35,6 +35,37 @@ struct Gen {
     // ret_mode 0: `return` ends the device function; 1: it ends an entry segment (jit.cpp);
     // 2: not allowed (body of a parallel loop)
     int ret_mode = 0;
+    // Warp mode (jit.cpp): a whole warp runs one iteration of a parallel loop.  Array stores
+    // outside the split loops are done by lane 0 only (all lanes hold the same values) and
+    // followed by __syncwarp; the loops in `warp_loops` (reduction loops: op code, variable) are
+    // split across the lanes and their reduction variables combined in a fixed order.
+    bool lane0_stores = false;
+    std::map<const pf::Stmt*, std::vector<std::pair<int, std::string>>> warp_loops;
+
+    static void assigned_scalars(const pf::Stmt& s, std::set<std::string>& out) {
+        switch (s.kind) {
+            case pf::Stmt::Block:
+                for (const auto& c : s.body) assigned_scalars(*c, out);
+                break;
+            case pf::Stmt::Decl:
+                if (s.extents.empty()) out.insert(s.name);
+                break;
+            case pf::Stmt::Assign:
+                if (s.lhs->kind == pf::Expr::Var) out.insert(s.lhs->name);
+                break;
+            case pf::Stmt::For:
+                out.insert(s.name);
+                assigned_scalars(*s.loop_body, out);
+                break;
+            case pf::Stmt::While:
+            case pf::Stmt::Labeled: assigned_scalars(*s.loop_body, out); break;
+            case pf::Stmt::If:
+                assigned_scalars(*s.then_s, out);
+                if (s.else_s) assigned_scalars(*s.else_s, out);
+                break;
+            default: break;
+        }
+    }
     const pf::Unit& u;
     std::ostringstream out;
     int tmp = 0;
@@ -201,6 +232,16 @@ struct Gen {
                 }
                 break;
             case pf::Stmt::Assign: {
+                const bool global_store = s.lhs->kind == pf::Expr::Unary ||
+                                          (s.lhs->kind == pf::Expr::Index && sc.arrays.count(s.lhs->name));
+                if (lane0_stores && global_store) {  // one lane stores, then the warp converges
+                    o << ind << "if ((threadIdx.x & 31) == 0) {\n";
+                    lane0_stores = false;
+                    stmt(s, sc, o, ind + "  ");
+                    lane0_stores = true;
+                    o << ind << "}\n" << ind << "__syncwarp();\n";
+                    break;
+                }
                 std::string rhs0 = ex(*s.rhs, sc, o, ind);
                 std::string rhs = t();
                 o << ind << "V " << rhs << " = " << rhs0 << ";\n";
@@ -228,6 +269,11 @@ struct Gen {
                 break;
             }
             case pf::Stmt::For: {
+                auto wl = warp_loops.find(&s);
+                if (wl != warp_loops.end()) {
+                    warp_split_for(s, wl->second, sc, o, ind);
+                    break;
+                }
                 o << ind << "{\n";
                 std::string in2 = ind + "  ";
                 std::string lo = ex(*s.lo, sc, o, in2);
@@ -284,6 +330,65 @@ struct Gen {
                 break;
             case pf::Stmt::Labeled: stmt(*s.loop_body, sc, o, ind); break;
         }
+    }
+
+    // `for (j = lo; j < hi; j++)` with `reduction (op: r...)`, run by a whole warp: lane l takes
+    // j = lo + l, lo + l + 32, ...; each r starts at the identity (+ 0, * 1, max / min: its value),
+    // the lanes' partials are combined down a fixed tree into lane 0 and broadcast, then
+    // r = r_before (op) total.  Other scalars the body assigns take the values of the lane that
+    // ran the last iteration (the sequential result), the loop variable ends at hi - 1.
+    void warp_split_for(const pf::Stmt& s, const std::vector<std::pair<int, std::string>>& reds, Scope& sc,
+                        std::ostringstream& o, const std::string& ind) {
+        o << ind << "{\n";
+        std::string in2 = ind + "  ";
+        std::string lo = ex(*s.lo, sc, o, in2);
+        std::string lo2 = t();
+        o << in2 << "ll " << lo2 << " = as_i(cx, " << lo << ");\n";
+        std::string hi = ex(*s.hi, sc, o, in2);
+        std::string hi2 = t();
+        o << in2 << "ll " << hi2 << " = as_i(cx, " << hi << ");\n";
+        std::vector<std::string> before;
+        for (const auto& r : reds) {
+            if (!sc.scalars.count(r.second)) unsup(*sc.f, s.line, "reduction variable '" + r.second + "' is not a scalar");
+            std::string b = t();
+            before.push_back(b);
+            o << in2 << "V " << b << " = " << sid(r.second) << ";\n";
+            if (r.first == 0) o << in2 << sid(r.second) << " = VI(0);\n";
+            if (r.first == 1) o << in2 << sid(r.second) << " = VI(1);\n";
+        }
+        const bool saved = lane0_stores;
+        lane0_stores = false;
+        std::string q = t();
+        o << in2 << "for (ll " << q << " = " << lo2 << " + (threadIdx.x & 31); " << q << " < " << hi2 << "; " << q
+          << " += 32) {\n";
+        o << in2 << "  " << sid(s.name) << " = VI(" << q << ");\n";
+        stmt(*s.loop_body, sc, o, in2 + "  ");
+        o << in2 << "}\n";
+        lane0_stores = saved;
+        for (size_t k = 0; k < reds.size(); k++) {
+            const std::string v = sid(reds[k].second);
+            o << in2 << "for (int d = 16; d > 0; d >>= 1) {\n";
+            o << in2 << "  V u; u.i = __shfl_down_sync(0xffffffffu, " << v << ".i, d); u.d = __shfl_down_sync(0xffffffffu, "
+              << v << ".d, d); u.isd = __shfl_down_sync(0xffffffffu, " << v << ".isd, d);\n";
+            o << in2 << "  if ((threadIdx.x & 31) + d < 32) " << v << " = red(" << reds[k].first << ", " << v << ", u);\n";
+            o << in2 << "}\n";
+            o << in2 << v << ".i = __shfl_sync(0xffffffffu, " << v << ".i, 0); " << v << ".d = __shfl_sync(0xffffffffu, " << v
+              << ".d, 0); " << v << ".isd = __shfl_sync(0xffffffffu, " << v << ".isd, 0);\n";
+            o << in2 << v << " = red(" << reds[k].first << ", " << before[k] << ", " << v << ");\n";
+        }
+        std::set<std::string> asg;
+        assigned_scalars(*s.loop_body, asg);
+        asg.insert(s.name);
+        for (const auto& r : reds) asg.erase(r.second);
+        o << in2 << "if (" << hi2 << " > " << lo2 << ") {\n";
+        o << in2 << "  const int src = (int)((" << hi2 << " - 1 - " << lo2 << ") & 31);\n";
+        for (const auto& a : asg) {
+            if (!sc.scalars.count(a)) continue;
+            const std::string v = sid(a);
+            o << in2 << "  " << v << ".i = __shfl_sync(0xffffffffu, " << v << ".i, src); " << v << ".d = __shfl_sync(0xffffffffu, "
+              << v << ".d, src); " << v << ".isd = __shfl_sync(0xffffffffu, " << v << ".isd, src);\n";
+        }
+        o << in2 << "}\n" << ind << "}\n";
     }
 
     std::string signature(const pf::Func& f) {

@@ -59,6 +59,7 @@ struct Red {
 };
 struct Seg {
     bool parallel = false;
+    bool warp = false;  // one warp per iteration, inner reduction loops split across the lanes
     std::vector<const pf::Stmt*> stmts;  // serial: statements in order; parallel: the loop
     std::vector<Red> reds;
     std::set<std::string> private_larrays;  // local arrays declared inside the loop body
@@ -202,6 +203,54 @@ void collect_decls(const pf::Stmt& s, std::set<std::string>& larr) {
     }
 }
 
+// The mapper's rule for an innermost PARALLEL_WITH_REDUCTION loop: a warp per
+// iteration of the parallel loop, the reduction loop split across its lanes.  Taken when the
+// parallel loop's body holds such a loop at its top level and calls no function outside it (a
+// call there would run on every lane).
+bool calls_outside(const pf::Stmt& s, const std::set<const pf::Stmt*>& skip) {
+    if (skip.count(&s)) return false;
+    std::function<bool(const pf::Expr&)> has_call = [&](const pf::Expr& e) {
+        if (e.kind == pf::Expr::Call && e.name != "exp") return true;
+        for (const auto& a : e.args)
+            if (has_call(*a)) return true;
+        return false;
+    };
+    switch (s.kind) {
+        case pf::Stmt::Block:
+            for (const auto& c : s.body)
+                if (calls_outside(*c, skip)) return true;
+            return false;
+        case pf::Stmt::Decl: return (s.rhs && has_call(*s.rhs));
+        case pf::Stmt::Assign: return has_call(*s.rhs) || has_call(*s.lhs);
+        case pf::Stmt::For: return has_call(*s.lo) || has_call(*s.hi) || calls_outside(*s.loop_body, skip);
+        case pf::Stmt::While: return has_call(*s.cond) || calls_outside(*s.loop_body, skip);
+        case pf::Stmt::If:
+            return has_call(*s.cond) || calls_outside(*s.then_s, skip) || (s.else_s && calls_outside(*s.else_s, skip));
+        case pf::Stmt::CallS: return true;
+        case pf::Stmt::Labeled: return calls_outside(*s.loop_body, skip);
+        default: return false;
+    }
+}
+std::vector<std::pair<const pf::Stmt*, std::vector<Red>>> inner_reduction_loops(const pf::Stmt& loop) {
+    std::vector<std::pair<const pf::Stmt*, std::vector<Red>>> out;
+    if (loop.loop_body->kind != pf::Stmt::Block) return out;
+    for (const auto& c : loop.loop_body->body) {
+        if (c->kind != pf::Stmt::For) continue;
+        std::vector<Red> r;
+        bool red = false;
+        for (const auto& p : c->pragmas) red |= parse_reduction(p, r);
+        if (red && !r.empty()) out.push_back({c.get(), r});
+    }
+    return out;
+}
+bool warp_candidate(const pf::Stmt& loop) {
+    auto inner = inner_reduction_loops(loop);
+    if (inner.empty()) return false;
+    std::set<const pf::Stmt*> skip;
+    for (auto& p : inner) skip.insert(p.first);
+    return !calls_outside(*loop.loop_body, skip);
+}
+
 struct Builder {
     const pf::Unit& u;
     pcg::Gen gen;
@@ -280,6 +329,7 @@ struct Builder {
                 collect_decls(*loop->loop_body, g.private_larrays);
                 for (const auto& r : reds)
                     if (!E.slot.count(r.var)) gen.unsup(f, s->line, "reduction variable '" + r.var + "' is not a scalar");
+                g.warp = reds.empty() && warp_candidate(*loop);
                 E.segs.push_back(std::move(g));
             } else {
                 if (E.segs.empty() || E.segs.back().parallel) E.segs.push_back(Seg());
@@ -325,7 +375,36 @@ struct Builder {
         }
         std::set<std::string> redvars;
         for (const auto& r : g.reds) redvars.insert(r.var);
-        {  // body: one iteration per thread, grid-stride
+        if (g.warp) {  // one warp per iteration; the inner reduction loops split across the lanes
+            std::ostringstream o;
+            o << "extern \"C\" __global__ void " << base << "_p(" << params(E)
+              << ", ll lo, ll hi, V* frame_out, V* partials) {\n";
+            o << "  const ll nw = ((ll)gridDim.x * blockDim.x) >> 5, wid = ((ll)blockIdx.x * blockDim.x + threadIdx.x) >> 5;\n";
+            load_frame(E, o);
+            shared_larrays(E, g.private_larrays, o);
+            for (const auto& la : g.private_larrays) {
+                long long n = E.la_n.at(la);
+                if (n > 256) gen.unsup(*E.f, L.line, "local array '" + la + "' inside a parallel loop exceeds 256 elements");
+                o << "  V " << pcg::Gen::lid(la) << "_st[" << std::max(1ll, n) << "]; LArr " << pcg::Gen::lid(la) << " = {"
+                  << pcg::Gen::lid(la) << "_st, " << n << "};\n";
+            }
+            for (auto& p : inner_reduction_loops(L)) {
+                std::vector<std::pair<int, std::string>> rv;
+                for (auto& r : p.second) rv.push_back({r.op, r.var});
+                gen.warp_loops[p.first] = rv;
+            }
+            o << "  for (ll v = lo + wid; v < hi; v += nw) {\n";
+            o << "    " << pcg::Gen::sid(L.name) << " = VI(v);\n";
+            o << "    auto body = [&]() {\n";
+            gen.lane0_stores = true;
+            gen.stmt(*L.loop_body, sc, o, "      ");
+            gen.lane0_stores = false;
+            o << "    };\n    body();\n";
+            o << "    if (v == hi - 1 && (threadIdx.x & 31) == 0) {\n";
+            store_frame(E, o, "frame_out", {}, "      ");
+            o << "    }\n  }\n}\n";
+            k << o.str();
+        } else {  // body: one iteration per thread, grid-stride
             std::ostringstream o;
             o << "extern \"C\" __global__ void " << base << "_p(" << params(E)
               << ", ll lo, ll hi, V* frame_out, V* partials) {\n";
@@ -718,7 +797,7 @@ int pencil_jit_schedule(pencil_jit_t J, const char* fn, char* out, int cap) {
     const auto& segs = J->entries[it->second].segs;
     int n = 0;
     for (const auto& g : segs) {
-        if (n + 1 < cap) out[n] = !g.parallel ? 'S' : (g.reds.empty() ? 'P' : 'R');
+        if (n + 1 < cap) out[n] = !g.parallel ? 'S' : (g.warp ? 'W' : (g.reds.empty() ? 'P' : 'R'));
         n++;
     }
     if (cap > 0) out[std::min(n, cap - 1)] = 0;
@@ -905,6 +984,7 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
         long long nthr = 0;
         if (ran) {
             long long count = hi - lo;
+            if (g.warp) count *= 32;  // a warp per iteration
             long long blocks = std::min<long long>((count + 255) / 256, max_threads / 256);
             nthr = blocks * 256;
             if ((rc = get_kernel(J, base + "_p", &kk))) return release(), rc;
