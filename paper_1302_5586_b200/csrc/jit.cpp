@@ -347,6 +347,7 @@ struct Builder {
         if (!g.parallel) {
             std::ostringstream o;
             o << "extern \"C\" __global__ void " << base << "(" << params(E) << ", int* flags) {\n";
+            o << "  if (flags[0]) return;  // an earlier segment returned\n";
             load_frame(E, o);
             shared_larrays(E, {}, o);
             o << "  V ret_v = VI(0); int ret_f = 0;\n  auto body = [&]() {\n";
@@ -362,7 +363,8 @@ struct Builder {
         gen.ret_mode = 2;
         {  // bounds: one thread evaluates lo and hi (in that order), as the interpreter does
             std::ostringstream o;
-            o << "extern \"C\" __global__ void " << base << "_b(" << params(E) << ", ll* bounds) {\n";
+            o << "extern \"C\" __global__ void " << base << "_b(" << params(E) << ", ll* bounds, int* flags) {\n";
+            o << "  if (flags[0]) { bounds[0] = bounds[1] = 0; return; }\n";
             load_frame(E, o);
             shared_larrays(E, {}, o);
             std::string lo = gen.ex(*L.lo, sc, o, "  ");
@@ -378,7 +380,8 @@ struct Builder {
         if (g.warp) {  // one warp per iteration; the inner reduction loops split across the lanes
             std::ostringstream o;
             o << "extern \"C\" __global__ void " << base << "_p(" << params(E)
-              << ", ll lo, ll hi, V* frame_out, V* partials) {\n";
+              << ", const ll* bounds, V* frame_out, V* partials) {\n";
+            o << "  const ll lo = bounds[0], hi = bounds[1];  // from the bounds kernel: no host round trip\n";
             o << "  const ll nw = ((ll)gridDim.x * blockDim.x) >> 5, wid = ((ll)blockIdx.x * blockDim.x + threadIdx.x) >> 5;\n";
             load_frame(E, o);
             shared_larrays(E, g.private_larrays, o);
@@ -407,7 +410,8 @@ struct Builder {
         } else {  // body: one iteration per thread, grid-stride
             std::ostringstream o;
             o << "extern \"C\" __global__ void " << base << "_p(" << params(E)
-              << ", ll lo, ll hi, V* frame_out, V* partials) {\n";
+              << ", const ll* bounds, V* frame_out, V* partials) {\n";
+            o << "  const ll lo = bounds[0], hi = bounds[1];  // from the bounds kernel: no host round trip\n";
             o << "  const ll nthr = (ll)gridDim.x * blockDim.x, tid = (ll)blockIdx.x * blockDim.x + threadIdx.x;\n";
             load_frame(E, o);
             shared_larrays(E, g.private_larrays, o);
@@ -436,7 +440,9 @@ struct Builder {
         {  // finish: last-iteration scalars into the frame, reductions combined in a fixed order
             std::ostringstream o;
             o << "extern \"C\" __global__ void __launch_bounds__(1024) " << base
-              << "_f(Ctx cx, V* frame, const V* frame_out, const V* partials, ll nthr, int ran) {\n";
+              << "_f(Ctx cx, V* frame, const V* frame_out, const V* partials, ll nthr, const ll* bounds, const int* flags) {\n";
+            o << "  if (flags[0]) return;\n";
+            o << "  const int ran = bounds[1] > bounds[0];\n";
             o << "  __shared__ V sh[1024];\n";
             o << "  if (ran && threadIdx.x == 0) {\n";
             for (size_t i = 0; i < E.scalars.size(); i++)
@@ -696,6 +702,8 @@ struct pencil_jit {
     std::vector<cudaKernel_t> kernels_cache;
     std::map<std::string, cudaKernel_t> kern;
     long long h2d = 0, d2h = 0;  // bytes moved by the last pencil_jit_call_host
+    void* scratch = nullptr;     // per-call frame / local arrays / partials / bounds / flags
+    size_t scratch_bytes = 0;
 };
 
 namespace {
@@ -781,6 +789,7 @@ void pencil_jit_free(pencil_jit_t J) {
     }
     if (J->d_fault) cudaFree(J->d_fault);
     if (J->d_rng) cudaFree(J->d_rng);
+    if (J->scratch) cudaFree(J->scratch);
     if (J->lib) cudaLibraryUnload(J->lib);
     if (J->stream) cudaStreamDestroy(J->stream);
     delete J;
@@ -918,32 +927,27 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
         }
     }
     static_assert(sizeof(HostV) == 24, "V layout");
-    HostV* d_frame = nullptr;
-    HostV* d_out = nullptr;
-    HostV* d_la = nullptr;
-    HostV* d_part = nullptr;
-    long long* d_bounds = nullptr;
-    int* d_flags = nullptr;
-    auto release = [&]() {
-        cudaStreamSynchronize(J->stream);
-        cudaFree(d_frame);
-        cudaFree(d_out);
-        cudaFree(d_la);
-        cudaFree(d_part);
-        cudaFree(d_bounds);
-        cudaFree(d_flags);
-    };
+    // call buffers: one scratch block per unit, grown on demand (cudaMalloc / cudaFree per call
+    // cost more than a small call's kernels)
     const long long max_threads = 148 * 4 * 256;
     size_t max_red = 1;
     for (const auto& g : E.segs) max_red = std::max(max_red, g.reds.size());
-    if (cudaMalloc(&d_frame, (K + 1) * sizeof(HostV)) != cudaSuccess ||
-        cudaMalloc(&d_out, (K + 1) * sizeof(HostV)) != cudaSuccess ||
-        cudaMalloc(&d_la, std::max<long long>(1, E.la_total) * sizeof(HostV)) != cudaSuccess ||
-        cudaMalloc(&d_part, max_threads * max_red * sizeof(HostV)) != cudaSuccess ||
-        cudaMalloc(&d_bounds, 16) != cudaSuccess || cudaMalloc(&d_flags, 16) != cudaSuccess) {
-        release();
-        return fail(PENCIL_E_NOMEM, "E-NOMEM: JIT call buffers");
+    const size_t n_frame = K + 1, n_la = (size_t)std::max<long long>(1, E.la_total), n_part = max_threads * max_red;
+    const size_t need = (2 * n_frame + n_la + n_part) * sizeof(HostV) + 64;
+    if (J->scratch_bytes < need) {
+        if (J->scratch) cudaFree(J->scratch);
+        J->scratch = nullptr;
+        J->scratch_bytes = 0;
+        if (cudaMalloc(&J->scratch, need) != cudaSuccess) return fail(PENCIL_E_NOMEM, "E-NOMEM: JIT call buffers");
+        J->scratch_bytes = need;
     }
+    HostV* d_frame = (HostV*)J->scratch;
+    HostV* d_out = d_frame + n_frame;
+    HostV* d_la = d_out + n_frame;
+    HostV* d_part = d_la + n_la;
+    long long* d_bounds = (long long*)(d_part + n_part);
+    int* d_flags = (int*)(d_bounds + 2);
+    auto release = [&]() { cudaStreamSynchronize(J->stream); };
     JCK(cudaMemcpyAsync(d_frame, frame.data(), (K + 1) * sizeof(HostV), cudaMemcpyHostToDevice, J->stream));
     JCK(cudaMemsetAsync(d_la, 0, std::max<long long>(1, E.la_total) * sizeof(HostV), J->stream));
     JCK(cudaMemsetAsync(d_flags, 0, 16, J->stream));
@@ -964,43 +968,37 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
             std::vector<void*> a = common;
             a.push_back(&d_flags);
             JCK(cudaLaunchKernel((const void*)kk, dim3(1), dim3(1), a.data(), 0, J->stream));
-            int flags = 0;
-            JCK(cudaMemcpyAsync(&flags, d_flags, 4, cudaMemcpyDeviceToHost, J->stream));
-            JCK(cudaStreamSynchronize(J->stream));
-            returned = flags;
             continue;
         }
+        // parallel segment: bounds, body, finish — all stream-ordered (the bounds stay on the
+        // device; the body's grid is fixed and grid-strides over whatever range they hold)
         if ((rc = get_kernel(J, base + "_b", &kk))) return release(), rc;
         {
             std::vector<void*> a = common;
             a.push_back(&d_bounds);
+            a.push_back(&d_flags);
             JCK(cudaLaunchKernel((const void*)kk, dim3(1), dim3(1), a.data(), 0, J->stream));
         }
-        long long b[2] = {0, 0};
-        JCK(cudaMemcpyAsync(b, d_bounds, 16, cudaMemcpyDeviceToHost, J->stream));
-        JCK(cudaStreamSynchronize(J->stream));
-        long long lo = b[0], hi = b[1];
-        int ran = hi > lo;
-        long long nthr = 0;
-        if (ran) {
-            long long count = hi - lo;
-            if (g.warp) count *= 32;  // a warp per iteration
-            long long blocks = std::min<long long>((count + 255) / 256, max_threads / 256);
-            nthr = blocks * 256;
-            if ((rc = get_kernel(J, base + "_p", &kk))) return release(), rc;
+        const long long blocks = max_threads / 256;
+        long long nthr = blocks * 256;
+        if ((rc = get_kernel(J, base + "_p", &kk))) return release(), rc;
+        {
             std::vector<void*> a = common;
-            a.push_back(&lo);
-            a.push_back(&hi);
+            a.push_back(&d_bounds);
             a.push_back(&d_out);
             a.push_back(&d_part);
             JCK(cudaLaunchKernel((const void*)kk, dim3((unsigned)blocks), dim3(256), a.data(), 0, J->stream));
         }
         if ((rc = get_kernel(J, base + "_f", &kk))) return release(), rc;
         {
-            std::vector<void*> a = {&cx, &d_frame, &d_out, &d_part, &nthr, &ran};
+            std::vector<void*> a = {&cx, &d_frame, &d_out, &d_part, &nthr, &d_bounds, &d_flags};
             JCK(cudaLaunchKernel((const void*)kk, dim3(1), dim3(1024), a.data(), 0, J->stream));
         }
     }
+    int flags = 0;
+    JCK(cudaMemcpyAsync(&flags, d_flags, 4, cudaMemcpyDeviceToHost, J->stream));
+    JCK(cudaStreamSynchronize(J->stream));
+    returned = flags;
     HostV rv{0, 0.0, 0};
     if (returned) JCK(cudaMemcpyAsync(&rv, d_frame + K, sizeof(HostV), cudaMemcpyDeviceToHost, J->stream));
     unsigned fw = 0;
