@@ -637,7 +637,9 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     if (persist < 0) {
         const char* e = getenv("PENCIL_SPMV_PERSIST");
         // opt-in: persisting lines outlive the launch and shrink L2 for the caller's next kernels
-        // (measured: later streaming kernels up to 2x slower), for ~4% on the SpMV itself
+        // (measured with the flow kernel: DRAM read 4.30 -> 2.70 GB per SpMV, but no time gain, and
+        // axpy / the stencils 2.2-2.4x slower afterwards — the set-aside L2, not the lines: a
+        // Normal-window re-read of x after the launch does not undo it)
         persist = (e && e[0] == '1');
         int dev = 0, maxp = 0;
         cudaGetDevice(&dev);
