@@ -60,6 +60,7 @@ struct Red {
 struct Seg {
     bool parallel = false;
     bool warp = false;  // one warp per iteration, inner reduction loops split across the lanes
+    const pf::Stmt* inner = nullptr;  // 2-D grid: the nested `independent` loop collapsed with this one
     std::vector<const pf::Stmt*> stmts;  // serial: statements in order; parallel: the loop
     std::vector<Red> reds;
     std::set<std::string> private_larrays;  // local arrays declared inside the loop body
@@ -251,6 +252,27 @@ bool warp_candidate(const pf::Stmt& loop) {
     return !calls_outside(*loop.loop_body, skip);
 }
 
+// The mapper's rule for a nested ASSUMED_PARALLEL loop (second grid dimension):
+// the parallel loop's body is a single `independent` loop whose bounds do not involve the outer
+// variable or any call — the two collapse into one (i, j) iteration space.
+bool mentions(const pf::Expr& e, const std::string& v) {
+    if (e.kind == pf::Expr::Var && e.name == v) return true;
+    if (e.kind == pf::Expr::Call) return true;  // calls are not hoisted
+    for (const auto& a : e.args)
+        if (mentions(*a, v)) return true;
+    return false;
+}
+const pf::Stmt* collapse_candidate(const pf::Stmt& loop) {
+    const pf::Stmt* b = loop.loop_body.get();
+    if (b->kind == pf::Stmt::Block) {
+        if (b->body.size() != 1) return nullptr;
+        b = b->body[0].get();
+    }
+    if (b->kind != pf::Stmt::For || !has_independent(*b) || b->name == loop.name) return nullptr;
+    if (mentions(*b->lo, loop.name) || mentions(*b->hi, loop.name)) return nullptr;
+    return b;
+}
+
 struct Builder {
     const pf::Unit& u;
     pcg::Gen gen;
@@ -330,6 +352,7 @@ struct Builder {
                 for (const auto& r : reds)
                     if (!E.slot.count(r.var)) gen.unsup(f, s->line, "reduction variable '" + r.var + "' is not a scalar");
                 g.warp = reds.empty() && warp_candidate(*loop);
+                if (!g.warp && reds.empty()) g.inner = collapse_candidate(*loop);
                 E.segs.push_back(std::move(g));
             } else {
                 if (E.segs.empty() || E.segs.back().parallel) E.segs.push_back(Seg());
@@ -371,13 +394,49 @@ struct Builder {
             o << "  bounds[0] = as_i(cx, " << lo << ");\n";
             std::string hi = gen.ex(*L.hi, sc, o, "  ");
             o << "  bounds[1] = as_i(cx, " << hi << ");\n";
+            if (g.inner) {  // the inner bounds do not depend on the outer variable: evaluated once
+                std::string lo2 = gen.ex(*g.inner->lo, sc, o, "  ");
+                o << "  bounds[2] = as_i(cx, " << lo2 << ");\n";
+                std::string hi2 = gen.ex(*g.inner->hi, sc, o, "  ");
+                o << "  bounds[3] = as_i(cx, " << hi2 << ");\n";
+            }
             store_frame(E, o, "frame", {}, "  ");
             o << "}\n";
             k << o.str();
         }
         std::set<std::string> redvars;
         for (const auto& r : g.reds) redvars.insert(r.var);
-        if (g.warp) {  // one warp per iteration; the inner reduction loops split across the lanes
+        if (g.inner) {  // 2-D grid over (i, j): one (i, j) iteration per thread
+            const pf::Stmt& J2 = *g.inner;
+            std::ostringstream o;
+            o << "extern \"C\" __global__ void " << base << "_p(" << params(E)
+              << ", const ll* bounds, V* frame_out, V* partials) {\n";
+            o << "  const ll lo = bounds[0], hi = bounds[1], lo2 = bounds[2], hi2 = bounds[3];\n";
+            o << "  const ll n1 = hi > lo ? hi - lo : 0, n2 = hi2 > lo2 ? hi2 - lo2 : 0, total = n1 * n2;\n";
+            o << "  const ll nthr = (ll)gridDim.x * blockDim.x, tid = (ll)blockIdx.x * blockDim.x + threadIdx.x;\n";
+            load_frame(E, o);
+            shared_larrays(E, g.private_larrays, o);
+            for (const auto& la : g.private_larrays) {
+                long long n = E.la_n.at(la);
+                if (n > 256) gen.unsup(*E.f, L.line, "local array '" + la + "' inside a parallel loop exceeds 256 elements");
+                o << "  V " << pcg::Gen::lid(la) << "_st[" << std::max(1ll, n) << "]; LArr " << pcg::Gen::lid(la) << " = {"
+                  << pcg::Gen::lid(la) << "_st, " << n << "};\n";
+            }
+            // outer loop runs but the inner one never does: only the outer variable moves
+            o << "  if (n1 > 0 && n2 == 0 && tid == 0) {\n    " << pcg::Gen::sid(L.name) << " = VI(hi - 1);\n";
+            store_frame(E, o, "frame_out", {}, "    ");
+            o << "  }\n";
+            o << "  for (ll f = tid; f < total; f += nthr) {\n";
+            o << "    " << pcg::Gen::sid(L.name) << " = VI(lo + f / n2);\n";
+            o << "    " << pcg::Gen::sid(J2.name) << " = VI(lo2 + f % n2);\n";
+            o << "    auto body = [&]() {\n";
+            gen.stmt(*J2.loop_body, sc, o, "      ");
+            o << "    };\n    body();\n";
+            o << "    if (f == total - 1) {\n";
+            store_frame(E, o, "frame_out", {}, "      ");
+            o << "    }\n  }\n}\n";
+            k << o.str();
+        } else if (g.warp) {  // one warp per iteration; the inner reduction loops split across the lanes
             std::ostringstream o;
             o << "extern \"C\" __global__ void " << base << "_p(" << params(E)
               << ", const ll* bounds, V* frame_out, V* partials) {\n";
@@ -806,7 +865,7 @@ int pencil_jit_schedule(pencil_jit_t J, const char* fn, char* out, int cap) {
     const auto& segs = J->entries[it->second].segs;
     int n = 0;
     for (const auto& g : segs) {
-        if (n + 1 < cap) out[n] = !g.parallel ? 'S' : (g.warp ? 'W' : (g.reds.empty() ? 'P' : 'R'));
+        if (n + 1 < cap) out[n] = !g.parallel ? 'S' : (g.warp ? 'W' : g.inner ? '2' : (g.reds.empty() ? 'P' : 'R'));
         n++;
     }
     if (cap > 0) out[std::min(n, cap - 1)] = 0;
@@ -946,7 +1005,7 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
     HostV* d_la = d_out + n_frame;
     HostV* d_part = d_la + n_la;
     long long* d_bounds = (long long*)(d_part + n_part);
-    int* d_flags = (int*)(d_bounds + 2);
+    int* d_flags = (int*)(d_bounds + 4);
     auto release = [&]() { cudaStreamSynchronize(J->stream); };
     JCK(cudaMemcpyAsync(d_frame, frame.data(), (K + 1) * sizeof(HostV), cudaMemcpyHostToDevice, J->stream));
     JCK(cudaMemsetAsync(d_la, 0, std::max<long long>(1, E.la_total) * sizeof(HostV), J->stream));

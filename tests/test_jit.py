@@ -32,7 +32,8 @@ def fixture_src(name):
 
 @pytest.mark.parametrize("fixture,fn,sched", [
     ("gemv", "gemv", "W"), ("gemv_t", "gemv_t", "W"), ("dot", "dot", "SRS"), ("axpy", "axpy", "P"),
-    ("spmv", "spmv_vec", "W"), ("spmv", "spmv_inline", "P"), ("spmv", "spmv", "S"), ("gemm", "gemm", "P"),
+    ("spmv", "spmv_vec", "W"), ("spmv", "spmv_inline", "P"), ("spmv", "spmv", "S"), ("gemm", "gemm", "2"),
+    ("conv5x5", "conv5x5_u8", "2"), ("conv5x5", "conv5x5_f32", "2"),
 ])
 def test_schedule_from_directives(fixture, fn, sched):
     assert unit(fixture_src(fixture)).schedule(fn) == sched
@@ -282,3 +283,42 @@ def test_reductions_and_faults(cuda):
     with pytest.raises(pb.PencilError) as e:
         u.call("divz", [4, Arg.array("d")])
     assert e.value.code == "E-INTERP" and "division by zero" in str(e.value)
+
+
+NESTED = r"""
+int grid2(int m, int n, int out[restrict const static m * n])
+{
+  int i;
+  int j;
+  int last;
+  last = -7;
+  #pragma pencil independent
+  for (i = 0; i < m; i++) {
+    #pragma pencil independent
+    for (j = 0; j < n; j++) {
+      out[i * n + j] = i * 1000 + j;
+      last = i + j;
+    }
+  }
+  return i * 100000 + j * 100 + last;
+}
+"""
+
+
+@pytest.mark.gpu
+def test_nested_independent_loops_collapse_to_a_2d_grid(cuda):
+    from paper_1302_5586_b200.interp import Arg
+    u = unit(NESTED)
+    assert u.schedule("grid2") == "S2S"
+    m, n = 37, 53
+    u.set_array("o", np.zeros(m * n, np.int32))
+    ret = u.call("grid2", [m, n, Arg.array("o")])
+    _, ints, _ = u.get_array("o")
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    assert np.array_equal(ints.reshape(m, n), ii * 1000 + jj)
+    # after the loops: i = m-1, j = n-1 (interp.cpp:207-217), last = (m-1)+(n-1)
+    assert ret == (m - 1) * 100000 + (n - 1) * 100 + (m - 1) + (n - 1)
+    # inner range empty: the outer variable still advances, j and last keep their values
+    u.set_array("o0", np.zeros(1, np.int32))
+    ret = u.call("grid2", [5, 0, Arg.array("o0")])
+    assert ret == 4 * 100000 + 0 * 100 - 7
