@@ -235,6 +235,8 @@ int pencil_jit_access(pencil_jit_t j, const char* fn, char* out, int cap);
 int pencil_jit_call_host(pencil_jit_t j, const char* fn, int nargs, const pencil_arg* args, void* const* host,
                          const int* dtypes, const long long* counts, pencil_value* ret);
 int pencil_jit_last_traffic(pencil_jit_t j, long long* h2d, long long* d2h);
+/* Interpreter::set_rand_sequence: rand() returns these first, then the interpreter's LCG */
+int pencil_jit_set_rand_sequence(pencil_jit_t j, const long long* values, long long n);
 /* OptiML construct (docs/op2-input.md; load_optiml_construct + lower_optiml, optiml.hpp:27-41)
  * lowered to a PENCIL unit for pencil_jit_load: returns the text length (cap 0 sizes the buffer)
  * or -1 (E-OPTIML-SHAPE / E-OPTIML-RANGE) */

@@ -11,7 +11,7 @@ typedef long long ll;
 typedef unsigned long long ull;
 struct V { ll i; double d; int isd; };
 struct LArr { V* p; ll n; };
-struct Ctx { unsigned* fault; ull* rng; };
+struct Ctx { unsigned* fault; ull* rng; const ll* rseq; ull* rpos; ll rseq_n; };
 #define F_OOB_LOAD 1u
 #define F_OOB_STORE 2u
 #define F_DIV0 4u
@@ -19,6 +19,8 @@ struct Ctx { unsigned* fault; ull* rng; };
 #define F_NONINT 16u
 #define F_DBLSTORE 32u
 #define F_EMPTY 64u
+#define F_BUDGET 128u
+#define STEP_BUDGET 100000000ll  // the interpreter's step_budget_ (interp.hpp:71), per thread here
 static __device__ __forceinline__ V VI(ll x) { V v; v.i = x; v.d = 0.0; v.isd = 0; return v; }
 static __device__ __forceinline__ V VD(double x) { V v; v.i = 0; v.d = x; v.isd = 1; return v; }
 static __device__ __forceinline__ void fault(const Ctx& c, unsigned b) { atomicOr(c.fault, b); }
@@ -77,6 +79,11 @@ static __device__ __forceinline__ void stl(const Ctx& c, const LArr& a, V idx, i
     a.p[k] = op == 0 ? rhs : apply(c, op, a.p[k], rhs);
 }
 static __device__ __forceinline__ V b_rand(const Ctx& c) {
+    // Interpreter::next_rand (interp.cpp:249-254): the configured sequence first, then the LCG
+    if (c.rpos) {
+        const ull p = *c.rpos;
+        if (p < (ull)c.rseq_n) { *c.rpos = p + 1; return VI(c.rseq[p]); }
+    }
     ull s = *c.rng * 6364136223846793005ull + 1442695040888963407ull;
     *c.rng = s;
     return VI((ll)((s >> 33) & 0x7fffffffull));

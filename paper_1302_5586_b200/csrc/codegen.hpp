@@ -123,6 +123,13 @@ struct Gen {
 
     std::string t() { return "t" + std::to_string(tmp++); }
 
+    // runaway loops: the interpreter stops at its step budget with E-INTERP (interp.cpp:141-144);
+    // here every loop iteration counts against a per-thread budget of the same size
+    std::string budget_check() const {
+        return std::string("if (++steps_ > STEP_BUDGET) { fault(cx, F_BUDGET); ") +
+               (ret_mode ? "return; }" : "return VI(0); }");
+    }
+
     // emits statements computing `e`; returns an expression naming the value (a temp or literal)
     std::string ex(const pf::Expr& e, Scope& sc, std::ostringstream& o, const std::string& ind) {
         char buf[64];
@@ -284,6 +291,7 @@ struct Gen {
                 o << in2 << "ll " << hi2 << " = as_i(cx, " << hi << ");\n";
                 std::string q = t();
                 o << in2 << "for (ll " << q << " = " << lo2 << "; " << q << " < " << hi2 << "; ++" << q << ") {\n";
+                o << in2 << "  " << budget_check() << "\n";
                 o << in2 << "  " << sid(s.name) << " = VI(" << q << ");\n";
                 stmt(*s.loop_body, sc, o, in2 + "  ");
                 o << in2 << "}\n" << ind << "}\n";
@@ -293,6 +301,7 @@ struct Gen {
                 o << ind << "for (;;) {\n";
                 std::string c = ex(*s.cond, sc, o, ind + "  ");
                 o << ind << "  if (!truth(" << c << ")) break;\n";
+                o << ind << "  " << budget_check() << "\n";
                 stmt(*s.loop_body, sc, o, ind + "  ");
                 o << ind << "}\n";
                 break;
@@ -361,6 +370,7 @@ struct Gen {
         std::string q = t();
         o << in2 << "for (ll " << q << " = " << lo2 << " + (threadIdx.x & 31); " << q << " < " << hi2 << "; " << q
           << " += 32) {\n";
+        o << in2 << "  " << budget_check() << "\n";
         o << in2 << "  " << sid(s.name) << " = VI(" << q << ");\n";
         stmt(*s.loop_body, sc, o, in2 + "  ");
         o << in2 << "}\n";
@@ -411,6 +421,7 @@ struct Gen {
         }
         if (f.body) collect(*f.body, sc);
         std::ostringstream body;
+        body << "  ll steps_ = 0;\n";
         for (const auto& s : sc.scalars) {
             bool is_param = false;
             for (const auto& p : f.params)

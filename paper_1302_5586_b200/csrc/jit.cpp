@@ -273,6 +273,39 @@ const pf::Stmt* collapse_candidate(const pf::Stmt& loop) {
     return b;
 }
 
+bool uses_rand(const pf::Unit& u, const pf::Stmt& st) {
+    std::set<std::string> seen;
+    std::function<bool(const pf::Expr&)> ex;
+    std::function<bool(const pf::Stmt&)> sm = [&](const pf::Stmt& s) -> bool {
+        switch (s.kind) {
+            case pf::Stmt::Block:
+                for (const auto& c : s.body)
+                    if (sm(*c)) return true;
+                return false;
+            case pf::Stmt::Decl: return s.rhs && ex(*s.rhs);
+            case pf::Stmt::Assign: return ex(*s.rhs) || ex(*s.lhs);
+            case pf::Stmt::For: return ex(*s.lo) || ex(*s.hi) || sm(*s.loop_body);
+            case pf::Stmt::While: return ex(*s.cond) || sm(*s.loop_body);
+            case pf::Stmt::If: return ex(*s.cond) || sm(*s.then_s) || (s.else_s && sm(*s.else_s));
+            case pf::Stmt::CallS: return ex(*s.call);
+            case pf::Stmt::Return: return s.rhs && ex(*s.rhs);
+            case pf::Stmt::Labeled: return sm(*s.loop_body);
+            default: return false;
+        }
+    };
+    ex = [&](const pf::Expr& e) -> bool {
+        if (e.kind == pf::Expr::Call) {
+            if (e.name == "rand") return true;
+            const pf::Func* f = u.find(e.name);
+            if (f && f->body && seen.insert(e.name).second && sm(*f->body)) return true;
+        }
+        for (const auto& a : e.args)
+            if (ex(*a)) return true;
+        return false;
+    };
+    return sm(st);
+}
+
 struct Builder {
     const pf::Unit& u;
     pcg::Gen gen;
@@ -343,7 +376,8 @@ struct Builder {
                 for (const auto& p : loop->pragmas) red |= parse_reduction(p, reds);
             bool indep = has_independent(*s) || has_independent(*loop) ||
                          (loop->kind == pf::Stmt::For && !red && affine_parallel(*loop));
-            if (loop->kind == pf::Stmt::For && (indep || red)) {
+            // rand() is one sequential stream (Interpreter::next_rand): such loops stay in order
+            if (loop->kind == pf::Stmt::For && (indep || red) && !uses_rand(u, *loop)) {
                 Seg g;
                 g.parallel = true;
                 g.stmts.push_back(loop);
@@ -373,7 +407,7 @@ struct Builder {
             o << "  if (flags[0]) return;  // an earlier segment returned\n";
             load_frame(E, o);
             shared_larrays(E, {}, o);
-            o << "  V ret_v = VI(0); int ret_f = 0;\n  auto body = [&]() {\n";
+            o << "  V ret_v = VI(0); int ret_f = 0; ll steps_ = 0;\n  auto body = [&]() {\n";
             gen.ret_mode = 1;
             for (const pf::Stmt* s : g.stmts) gen.stmt(*s, sc, o, "    ");
             o << "  };\n  body();\n";
@@ -426,6 +460,7 @@ struct Builder {
             o << "  if (n1 > 0 && n2 == 0 && tid == 0) {\n    " << pcg::Gen::sid(L.name) << " = VI(hi - 1);\n";
             store_frame(E, o, "frame_out", {}, "    ");
             o << "  }\n";
+            o << "  ll steps_ = 0;\n";
             o << "  for (ll f = tid; f < total; f += nthr) {\n";
             o << "    " << pcg::Gen::sid(L.name) << " = VI(lo + f / n2);\n";
             o << "    " << pcg::Gen::sid(J2.name) << " = VI(lo2 + f % n2);\n";
@@ -455,6 +490,7 @@ struct Builder {
                 for (auto& r : p.second) rv.push_back({r.op, r.var});
                 gen.warp_loops[p.first] = rv;
             }
+            o << "  ll steps_ = 0;\n";
             o << "  for (ll v = lo + wid; v < hi; v += nw) {\n";
             o << "    " << pcg::Gen::sid(L.name) << " = VI(v);\n";
             o << "    auto body = [&]() {\n";
@@ -483,6 +519,7 @@ struct Builder {
             for (const auto& r : g.reds)
                 o << "  " << pcg::Gen::sid(r.var) << " = " << (r.op == 0 ? "VI(0)" : r.op == 1 ? "VI(1)" : pcg::Gen::sid(r.var))
                   << ";\n";
+            o << "  ll steps_ = 0;\n";
             o << "  for (ll v = lo + tid; v < hi; v += nthr) {\n";
             o << "    " << pcg::Gen::sid(L.name) << " = VI(v);\n";
             o << "    auto body = [&]() {\n";
@@ -763,6 +800,9 @@ struct pencil_jit {
     long long h2d = 0, d2h = 0;  // bytes moved by the last pencil_jit_call_host
     void* scratch = nullptr;     // per-call frame / local arrays / partials / bounds / flags
     size_t scratch_bytes = 0;
+    long long* d_rseq = nullptr;           // Interpreter::set_rand_sequence values
+    unsigned long long* d_rpos = nullptr;  // next position in it
+    long long rseq_n = 0;
 };
 
 namespace {
@@ -849,6 +889,8 @@ void pencil_jit_free(pencil_jit_t J) {
     if (J->d_fault) cudaFree(J->d_fault);
     if (J->d_rng) cudaFree(J->d_rng);
     if (J->scratch) cudaFree(J->scratch);
+    if (J->d_rseq) cudaFree(J->d_rseq);
+    if (J->d_rpos) cudaFree(J->d_rpos);
     if (J->lib) cudaLibraryUnload(J->lib);
     if (J->stream) cudaStreamDestroy(J->stream);
     delete J;
@@ -995,6 +1037,8 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
     const size_t need = (2 * n_frame + n_la + n_part) * sizeof(HostV) + 64;
     if (J->scratch_bytes < need) {
         if (J->scratch) cudaFree(J->scratch);
+    if (J->d_rseq) cudaFree(J->d_rseq);
+    if (J->d_rpos) cudaFree(J->d_rpos);
         J->scratch = nullptr;
         J->scratch_bytes = 0;
         if (cudaMalloc(&J->scratch, need) != cudaSuccess) return fail(PENCIL_E_NOMEM, "E-NOMEM: JIT call buffers");
@@ -1013,7 +1057,10 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
     struct {
         unsigned* fault;
         unsigned long long* rng;
-    } cx{J->d_fault, J->d_rng};
+        const long long* rseq;
+        unsigned long long* rpos;
+        long long rseq_n;
+    } cx{J->d_fault, J->d_rng, J->d_rseq, J->d_rpos, J->rseq_n};
     const int fi = it->second;
     int returned = 0;
     for (size_t si = 0; si < E.segs.size() && !returned; si++) {
@@ -1077,6 +1124,7 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
         if (fw & 8u) m += " modulo by zero;";
         if (fw & 16u) m += " non-integral value where an integer is required;";
         if (fw & 64u) m += " empty pointee;";
+        if (fw & 128u) m += " execution step budget exceeded;";
         return fail(PENCIL_E_INTERP, m);
     }
     return pencil_internal_ok();
@@ -1175,6 +1223,23 @@ int pencil_jit_last_traffic(pencil_jit_t J, long long* h2d, long long* d2h) {
     if (!J) return fail(PENCIL_E_ARG, "E-ARG: null unit");
     if (h2d) *h2d = J->h2d;
     if (d2h) *d2h = J->d2h;
+    return pencil_internal_ok();
+}
+
+// Interpreter::set_rand_sequence (interp.hpp:44): rand() pops these values first, then the LCG
+int pencil_jit_set_rand_sequence(pencil_jit_t J, const long long* values, long long n) {
+    if (!J || n < 0 || (n && !values)) return fail(PENCIL_E_ARG, "E-ARG: bad rand sequence");
+    int rc = setup(J);
+    if (rc) return rc;
+    if (J->d_rseq) cudaFree(J->d_rseq);
+    J->d_rseq = nullptr;
+    if (!J->d_rpos) JCK(cudaMalloc(&J->d_rpos, 8));
+    JCK(cudaMemset(J->d_rpos, 0, 8));
+    if (n) {
+        JCK(cudaMalloc(&J->d_rseq, (size_t)n * 8));
+        JCK(cudaMemcpy(J->d_rseq, values, (size_t)n * 8, cudaMemcpyHostToDevice));
+    }
+    J->rseq_n = n;
     return pencil_internal_ok();
 }
 

@@ -620,7 +620,10 @@ int launch_loop(pencil_op2_model* M, int li) {
     struct Ctx {
         unsigned* fault;
         unsigned long long* rng;
-    } cx{M->d_fault, M->d_rng};
+        const long long* rseq;
+        unsigned long long* rpos;
+        long long rseq_n;
+    } cx{M->d_fault, M->d_rng, nullptr, nullptr, 0};
     const int strat = M->strategy[li];
     std::vector<long long> nn(dats.size());
     std::vector<int> inc(dats.size());
@@ -679,6 +682,7 @@ int collect(pencil_op2_model* M) {
     if (f & 16u) m += " non-integral value where an integer is required;";
     if (f & 32u) m += " non-integer value stored into an integer dat (unsupported);";
     if (f & 64u) m += " empty pointee;";
+    if (f & 128u) m += " execution step budget exceeded;";
     return fail(PENCIL_E_INTERP, m);
 }
 

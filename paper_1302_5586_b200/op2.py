@@ -240,3 +240,13 @@ def _jit_call_host(self, fn, args):
 
 JitUnit.access = _jit_access
 JitUnit.call_host = _jit_call_host
+
+
+def _jit_set_rand_sequence(self, values):
+    """Interpreter::set_rand_sequence (interp.hpp:44): rand() pops these values first."""
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    self._lib.pencil_jit_set_rand_sequence(self._h, v.ctypes.data, v.size)
+    check_status()
+
+
+JitUnit.set_rand_sequence = _jit_set_rand_sequence

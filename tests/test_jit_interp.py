@@ -1,0 +1,89 @@
+"""The reference's own Interpreter tests (tests/test_interp.cpp: arithmetic, arrays shared through
+calls, loops and conditionals, while, rand sequence then LCG, floats, out-of-bounds store,
+unknown function, step budget) replayed through the general mapper on the GPU."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def unit(src):
+    from paper_1302_5586_b200.op2 import JitUnit
+    return JitUnit(src)
+
+
+def test_arithmetic_and_return(cuda):
+    u = unit("int f(int a, int b)\n{\n  int r;\n  r = a * b + a / b - a % b;\n  return r;\n}\n")
+    assert u.call("f", [7, 3]) == 7 * 3 + 7 // 3 - 7 % 3
+
+
+def test_arrays_are_shared_through_calls(cuda):
+    from paper_1302_5586_b200 import Arg
+    u = unit("void set(int n, int A[restrict const static n])\n{\n  A[1] = 42;\n}\n"
+             "void run(int n, int A[restrict const static n])\n{\n  set(n, A);\n  A[0] = A[1];\n}\n")
+    u.set_array("mem", np.zeros(3, np.int32))
+    u.call("run", [3, Arg.array("mem")])
+    assert u.get_array("mem")[1][:2].tolist() == [42, 42]
+
+
+def test_loops_and_conditionals(cuda):
+    u = unit("int tri(int n)\n{\n  int s;\n  int i;\n  s = 0;\n"
+             "  for (i = 1; i <= n; i++) {\n    if (i % 2 == 0) {\n      s += i;\n    }\n  }\n  return s;\n}\n")
+    assert u.call("tri", [6]) == 2 + 4 + 6
+
+
+def test_while_loop(cuda):
+    u = unit("int halve(int n)\n{\n  int c;\n  c = 0;\n  while (n > 1) {\n    n = n / 2;\n    c += 1;\n  }\n"
+             "  return c;\n}\n")
+    assert u.call("halve", [16]) == 4
+
+
+def test_rand_pops_sequence_then_lcg(cuda):
+    from paper_1302_5586_b200 import Arg
+    src = ("void take(int n, int A[restrict const static n])\n{\n  int i;\n"
+           "  for (i = 0; i < n; i++) {\n    A[i] = rand();\n  }\n}\n")
+    outs = []
+    for _ in range(2):
+        u = unit(src)
+        u.set_array("A", np.zeros(5, np.int32))
+        u.set_rand_sequence([9, 8])
+        u.call("take", [5, Arg.array("A")])
+        outs.append(u.get_array("A")[1].tolist())
+    assert outs[0][:2] == [9, 8] and outs[0] == outs[1]
+    # the fallback is the interpreter's LCG from its seed (interp.hpp:67)
+    s, ref = 0x9e3779b97f4a7c15, []
+    for _ in range(3):
+        s = (s * 6364136223846793005 + 1442695040888963407) % (1 << 64)
+        ref.append((s >> 33) & 0x7fffffff)
+    assert outs[0][2:] == ref
+
+
+def test_floating_point_values(cuda):
+    u = unit("float scale(float x)\n{\n  return x * 0.5;\n}\n")
+    assert u.call("scale", [3.0]) == 1.5
+
+
+def test_out_of_bounds_store_faults(cuda):
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200 import Arg
+    u = unit("void f(int n, int A[restrict const static n])\n{\n  A[n] = 1;\n}\n")
+    u.set_array("A", np.zeros(2, np.int32))
+    with pytest.raises(pb.PencilError) as e:
+        u.call("f", [2, Arg.array("A")])
+    assert e.value.code == "E-INTERP"
+
+
+def test_unknown_function_faults(cuda):
+    import paper_1302_5586_b200 as pb
+    u = unit("void f(int n)\n{\n}\n")
+    with pytest.raises(pb.PencilError) as e:
+        u.call("nope", [])
+    assert e.value.code == "E-INTERP"
+
+
+def test_step_budget_stops_runaway_loops(cuda):
+    import paper_1302_5586_b200 as pb
+    u = unit("void spin(int n)\n{\n  while (n < 1) {\n    n = n - 1;\n  }\n}\n")
+    with pytest.raises(pb.PencilError) as e:
+        u.call("spin", [0])
+    assert e.value.code == "E-INTERP" and "budget" in str(e.value)
