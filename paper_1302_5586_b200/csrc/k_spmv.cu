@@ -92,7 +92,36 @@ __device__ void spmv_generic(int nrows, int ncols, int nnz_len, const int* __res
 // Skewed staging index: lane i folds row i, whose slice starts near i*len; without the skew
 // rows of equal length 16 put 16 lanes on one bank (a 16-way conflict on every read).
 __device__ __forceinline__ int skew(int t) { return t + (t >> 5); }
+// the same pad, 4 floats per 32: 16-byte aligned slots for vector stores, conflict-free reads
+__device__ __forceinline__ int skew4(int t) { return t + 4 * (t >> 5); }
 #define WCHUNK_SKEWED (WCHUNK + WCH / 32)
+
+// Fold of one staged window into the lanes' rows: lane r adds the products of its row that lie in
+// [lo, hi) (window positions, `base` = the window's first position).  Source order: each lane
+// adds its slice in order, product-then-sum rounding as the emitted C.  With the reduction
+// licensed (ASSOC), slices longer than 16 are folded by the whole warp instead (strided
+// partials + shuffle tree), one such row at a time.  IDX maps a window offset to its skewed
+// staging slot.
+template <bool ASSOC, int (*IDX)(int)>
+__device__ __forceinline__ float fold_window(float s, int lo, int hi, int base, const float* sp, int lane) {
+    if (ASSOC) {
+        unsigned big = __ballot_sync(0xffffffffu, hi - lo > 16);
+        if (hi - lo <= 16)
+            for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[IDX(t - base)]);
+        while (big) {
+            const int o = __ffs(big) - 1;
+            big &= big - 1;
+            const int olo = __shfl_sync(0xffffffffu, lo, o), ohi = __shfl_sync(0xffffffffu, hi, o);
+            float part = 0.f;
+            for (int t = olo + lane; t < ohi; t += 32) part += sp[IDX(t - base)];
+            part = warp_sum<32>(part);
+            if (lane == o) s += part;
+        }
+    } else {
+        for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[IDX(t - base)]);
+    }
+    return s;
+}
 
 template <bool ASSOC, int WCH>
 __global__ void __launch_bounds__(SPMV_THREADS, (WCH <= 128 ? CTAS_PER_SM : 6)) csr_stream_kernel(
@@ -154,22 +183,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, (WCH <= 128 ? CTAS_PER_SM : 6)) 
                 sp[skew(u * 32 + lane)] = __fmul_rn(v[u], xv[u]);
             __syncwarp();
             const int lo = max(my_s, q), hi = min(my_e, q + cnt);
-            if (ASSOC) {
-                unsigned big = __ballot_sync(0xffffffffu, hi - lo > 16);
-                if (hi - lo <= 16)
-                    for (int p = lo; p < hi; p++) s = __fadd_rn(s, sp[skew(p - q)]);
-                while (big) {
-                    const int o = __ffs(big) - 1;
-                    big &= big - 1;
-                    const int olo = __shfl_sync(0xffffffffu, lo, o), ohi = __shfl_sync(0xffffffffu, hi, o);
-                    float part = 0.f;
-                    for (int p = olo + lane; p < ohi; p += 32) part += sp[skew(p - q)];
-                    part = warp_sum<32>(part);
-                    if (lane == o) s += part;
-                }
-            } else {
-                for (int p = lo; p < hi; p++) s = __fadd_rn(s, sp[skew(p - q)]);
-            }
+            s = fold_window<ASSOC, skew>(s, lo, hi, q, sp, lane);
             __syncwarp();
         }
         if (active) y[row] = s;
@@ -183,7 +197,6 @@ __global__ void __launch_bounds__(SPMV_THREADS, (WCH <= 128 ? CTAS_PER_SM : 6)) 
 // products with one 16-byte shared store: 2 + 1 instructions where the scalar kernel issues
 // 8 + 4.  The staging pad moves to 4 floats per 32 (aligned for the vector store; still
 // conflict-free for rows of equal length).  Needs 16-byte-aligned col / val.
-__device__ __forceinline__ int skew4(int t) { return t + 4 * (t >> 5); }
 template <bool ASSOC, int VU>
 __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_vec_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
@@ -295,22 +308,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_v
 #endif
                 __syncwarp();
                 const int lo = max(my_s, qa), hi = min(my_e, qa + 128 * VU);
-                if (ASSOC) {
-                    unsigned big = __ballot_sync(0xffffffffu, hi - lo > 16);
-                    if (hi - lo <= 16)
-                        for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[skew4(t - qa)]);
-                    while (big) {
-                        const int o = __ffs(big) - 1;
-                        big &= big - 1;
-                        const int olo = __shfl_sync(0xffffffffu, lo, o), ohi = __shfl_sync(0xffffffffu, hi, o);
-                        float part = 0.f;
-                        for (int t = olo + lane; t < ohi; t += 32) part += sp[skew4(t - qa)];
-                        part = warp_sum<32>(part);
-                        if (lane == o) s += part;
-                    }
-                } else {
-                    for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[skew4(t - qa)]);
-                }
+                s = fold_window<ASSOC, skew4>(s, lo, hi, qa, sp, lane);
                 __syncwarp();
             }
             if (active) y[row] = s;
@@ -412,22 +410,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, FLOW_MINB) csr_flow_kernel(
             __syncwarp();
             for (;;) {  // fold every batch overlapping this window
                 const int lo = max(my_s, qa), hi = min(my_e, qa + 128);
-                if (ASSOC) {
-                    unsigned big = __ballot_sync(0xffffffffu, hi - lo > 16);
-                    if (hi - lo <= 16)
-                        for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[skew4(t - qa)]);
-                    while (big) {
-                        const int o = __ffs(big) - 1;
-                        big &= big - 1;
-                        const int olo = __shfl_sync(0xffffffffu, lo, o), ohi = __shfl_sync(0xffffffffu, hi, o);
-                        float part = 0.f;
-                        for (int t = olo + lane; t < ohi; t += 32) part += sp[skew4(t - qa)];
-                        part = warp_sum<32>(part);
-                        if (lane == o) s += part;
-                    }
-                } else {
-                    for (int t = lo; t < hi; t++) s = __fadd_rn(s, sp[skew4(t - qa)]);
-                }
+                s = fold_window<ASSOC, skew4>(s, lo, hi, qa, sp, lane);
                 if (bend > qa + 128 || rb >= r1) break;  // the batch continues in the next window
                 if (rb + lane < r1) y[rb + lane] = s;      // batch complete
                 s = 0.f;
@@ -570,22 +553,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, TMA_CTAS_PER_SM) csr_tma_kernel(
             __syncwarp();
             for (;;) {  // fold every batch overlapping this chunk
                 const int lo = max(my_s, c0), hi = min(my_e, cend);
-                if (ASSOC) {
-                    unsigned big = __ballot_sync(0xffffffffu, hi - lo > 16);
-                    if (hi - lo <= 16)
-                        for (int p = lo; p < hi; p++) s = __fadd_rn(s, B.prod[skew(p - c0)]);
-                    while (big) {
-                        const int o = __ffs(big) - 1;
-                        big &= big - 1;
-                        const int olo = __shfl_sync(0xffffffffu, lo, o), ohi = __shfl_sync(0xffffffffu, hi, o);
-                        float part = 0.f;
-                        for (int p = olo + lane; p < ohi; p += 32) part += B.prod[skew(p - c0)];
-                        part = warp_sum<32>(part);
-                        if (lane == o) s += part;
-                    }
-                } else {
-                    for (int p = lo; p < hi; p++) s = __fadd_rn(s, B.prod[skew(p - c0)]);
-                }
+                s = fold_window<ASSOC, skew>(s, lo, hi, c0, B.prod, lane);
                 if (rb < r1 && bend <= cend) {  // batch complete inside this chunk
                     if (active) y[row] = s;
                     rb += 32;
