@@ -327,7 +327,7 @@ constexpr int P_B_TILE = P_BN_HALF * BK * 4;
 constexpr int P_STAGE_BYTES = 2 * A_TILE + 2 * P_B_TILE;  // per CTA
 constexpr int P_STAGES = 6;
 #ifndef P_GROUP_M_DEF
-#define P_GROUP_M_DEF 2  // swept 2/4/8 at 16384^3: 36.6 / 36.8 / 39.2 ms (tools/gemm_group_probe.sh)
+#define P_GROUP_M_DEF 8  // re-swept 2/4/8/16 at 16384^3 (current kernel): 36.2-36.4 / 36.1 / 34.9-35.8 / 36.2 ms
 #endif
 constexpr int P_GROUP_M = P_GROUP_M_DEF;
 constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
