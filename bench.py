@@ -16,6 +16,7 @@ every step (the data path's real exchange), value = global bytes / max-over-rank
 reference's emit_openmp produced for the same PENCIL fixtures (oracle/_ref), all host cores.
 """
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -205,18 +206,23 @@ def suite(args, torch, pb, hbm):
 
     # gemv 8192^2 (configs[0])
     m = n = 8192
-    A, x, y = dev(synth.f32(m * n)), dev(synth.f32(n, 42, m * n)), torch.zeros(m, device="cuda")
+    hA, hx = synth.f32(m * n), synth.f32(n, 42, m * n)
+    A, x, y = dev(hA), dev(hx), torch.zeros(m, device="cuda")
     ms = statistics.mean(run_steps(torch, lambda: pb.device.gemv(m, n, 1.0, 0.0, A, x, y), k, w, flush))
     b = 4 * (m * n + n + m)
     out["gemv_8192"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm, "bytes": b}
-    del A
+    hy = np.zeros(m, np.float32)
+    cpu_ref(args, out["gemv_8192"], lambda L: L.gemv(m, n, 1.0, 0.0, P(hA), P(hx), P(hy)), b, "full config")
+    del A, hA
 
     # VOBLA chain: gemv_t 16384^2 (lda 16384, incx 2, incy 3) + dot + axpy on 2^28 vectors
     m = n = lda = 16384
-    A = dev(synth.f32(m * lda))
-    xt, yt = dev(synth.f32(m * 2, 42, m * lda)), dev(synth.f32(n * 3, 42, m * lda + 2 * m))
+    hA = synth.f32(m * lda)
+    hxt, hyt = synth.f32(m * 2, 42, m * lda), synth.f32(n * 3, 42, m * lda + 2 * m)
+    A, xt, yt = dev(hA), dev(hxt), dev(hyt)
     nv = 1 << 28
-    xv, yv = dev(synth.f32(nv, 7)), dev(synth.f32(nv, 8))
+    hxv, hyv = synth.f32(nv, 7), synth.f32(nv, 8)
+    xv, yv = dev(hxv), dev(hyv)
     r = torch.zeros(1, device="cuda")
     ms_t = statistics.mean(run_steps(torch, lambda: pb.device.gemv_t(m, n, lda, 2, 3, 1.0, 0.0, A, xt, yt), k, w, flush))
     ms_d = statistics.mean(run_steps(torch, lambda: pb.device.dot(nv, xv, yv, r), k, w, flush))
@@ -234,10 +240,20 @@ def suite(args, torch, pb, hbm):
     out["vobla_chain"] = {"ms": ms_c, "GB/s": (bt + bd + ba) / ms_c / 1e6,
                           "frac_hbm": (bt + bd + ba) / ms_c / 1e6 / hbm, "bytes": bt + bd + ba}
     del A, xv, yv
+    cpu_ref(args, out["gemv_t_16384_strided"],
+            lambda L: L.gemv_t(m, n, lda, 2, 3, 1.0, 0.0, P(hA), P(hxt), P(hyt)), bt, "full config")
+    cpu_ref(args, out["dot_2e28"], lambda L: L.dot(nv, P(hxv), P(hyv)), bd, "full config")
+    cpu_ref(args, out["axpy_2e28"], lambda L: L.axpy(nv, 0.5, P(hxv), P(hyv)), ba, "full config")
+    if "cpu_baseline" in out["gemv_t_16384_strided"]:
+        out["vobla_chain"]["cpu_baseline"] = {
+            "ms": sum(out[q]["cpu_baseline"]["ms"] for q in ("gemv_t_16384_strided", "dot_2e28", "axpy_2e28")),
+            "cores": os.cpu_count(), "kind": "reference", "sample": "sum of the three calls above"}
+    del hA, hxv, hyv
 
     # 5x5 stencils 16384^2
     h = w_ = 16384
-    img_i = dev(synth.u8_i32(h * w_))
+    himg = synth.u8_i32(h * w_)
+    img_i = dev(himg)
     out_i = torch.empty(h * w_, dtype=torch.int32, device="cuda")
     ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8(h, w_, 256, img_i, synth.BINOMIAL, out_i),
                                    k, w, flush))
@@ -245,6 +261,11 @@ def suite(args, torch, pb, hbm):
     out["conv5x5_u8_int32storage_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm}
     img8 = img_i.to(torch.uint8)
     del img_i, out_i
+    hout = np.empty(h * w_, np.int32)
+    kb = np.ascontiguousarray(synth.BINOMIAL, np.int32)
+    cpu_ref(args, out["conv5x5_u8_int32storage_16384"], lambda L: L.conv5x5_u8(h, w_, 256, P(himg), P(kb), P(hout)),
+            b, "full config")
+    del himg, hout
     out8 = torch.empty(h * w_, dtype=torch.uint8, device="cuda")
     ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8_bytes(h, w_, 256, img8, synth.BINOMIAL, out8),
                                    k, w, flush))
@@ -252,13 +273,18 @@ def suite(args, torch, pb, hbm):
     out["conv5x5_u8_bytes_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
                                      "Gpix/s": h * w_ / ms / 1e6}
     del img8, out8
-    imgf = dev(synth.f32(h * w_))
+    himgf = synth.f32(h * w_)
+    imgf = dev(himgf)
     outf = torch.zeros(h * w_, device="cuda")
     kf = (synth.BINOMIAL.astype(np.float32) / 256.0).astype(np.float32)
     ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_f32(h, w_, imgf, kf, outf), k, w, flush))
     b = 8 * h * w_
     out["conv5x5_f32_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm}
     del imgf, outf
+    houtf = np.zeros(h * w_, np.float32)
+    cpu_ref(args, out["conv5x5_f32_16384"], lambda L: L.conv5x5_f32(h, w_, P(himgf), P(kf), P(houtf)), b,
+            "full config")
+    del himgf, houtf
 
     # OP2 mesh loop: the reference's edge->cell increment kernel on a random mesh
     try:
@@ -272,9 +298,44 @@ def suite(args, torch, pb, hbm):
         A, B, C = dev(synth.f32(m * kk)), dev(synth.f32(kk * n, 43)), torch.zeros(m * n, device="cuda")
         ms = statistics.mean(run_steps(torch, lambda: pb.device.gemm(m, n, kk, 1.0, 0.0, A, B, C), 2, 1, flush))
         out["gemm_16384_3xtf32"] = {"ms": ms, "TFLOP/s": 2 * m * n * kk / ms / 1e9}
+        del A, B, C
+        # CPU beside it: the emitted triple loop at 1024^3 (16384^3 would take ~an hour), as a rate
+        q = 1024
+        ha, hb, hc = synth.f32(q * q), synth.f32(q * q, 43), np.zeros(q * q, np.float32)
+        cpu_ref(args, out["gemm_16384_3xtf32"], lambda L: L.gemm(q, q, q, 1.0, 0.0, P(ha), P(hb), P(hc)),
+                None, "1024^3 (rate extrapolated to the config)", reps=1, flops=2 * q ** 3)
     except pb.PencilError as e:
         out["gemm_16384_3xtf32"] = {"unavailable": str(e)}
     return out
+
+
+def P(a):
+    return a.ctypes.data
+
+
+def cpu_ref(args, entry, call, nbytes, sample, reps=2, flops=None):
+    """CPU beside a suite line: the reference's emit_openmp C (outer-loop pragma,
+    oracle/_ref) on the same host inputs, all host threads, best of `reps` after one warm-up."""
+    if args.no_cpu_baseline:
+        return
+    try:
+        import oracle
+        lib = oracle.emitted("outer")
+        call(lib)
+        best = float("inf")
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            call(lib)
+            best = min(best, time.perf_counter() - t0)
+        cb = {"ms": best * 1e3, "cores": os.cpu_count(), "kind": "reference",
+              "sample": sample + ": emit_openmp C (outer pragma), gcc -O3 -fopenmp, best of %d" % reps}
+        if nbytes:
+            cb["GB/s"] = nbytes / best / 1e9
+        if flops:
+            cb["TFLOP/s"] = flops / best / 1e12
+        entry["cpu_baseline"] = cb
+    except Exception as e:  # noqa: BLE001 — a baseline must not take the suite down
+        entry["cpu_baseline"] = {"unavailable": str(e)[:200]}
 
 
 def op2_line(args, torch, pb, k, w):
@@ -426,6 +487,12 @@ def main():
                                         "cores": os.cpu_count(), "kind": "reference",
                                         "sample": "full matrix x3 calls of the emit_openmp C (outer pragma), "
                                                   "gcc -O3 -fopenmp, all host threads"}
+                # and on one thread (OMP_NUM_THREADS = 1 and = all cores)
+                gomp = ctypes.CDLL("libgomp.so.1")
+                gomp.omp_set_num_threads(1)
+                t1 = min(cpu_spmv(1, 0, rowptr, col, val, x))
+                gomp.omp_set_num_threads(os.cpu_count())
+                line["cpu_baseline"]["value_1thread"] = spmv_bytes(1 << 24, 1 << 24, col.size) / t1 / 1e9
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
         if world == 1 and not args.no_suite:
