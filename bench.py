@@ -149,26 +149,48 @@ def bench_spmv(args, torch, pb, rank, world, dist):
         launches = args.steps * 2  # spmv + l2 flush per step
         kernel_ms = statistics.mean(ms)
     else:
-        from paper_1302_5586_b200.dist import RowShardedCsr
+        # one step of a row-sharded iterative SpMV: y = A x for the rank's rows, y gathered on
+        # every rank (the next step's x) — fused into the SpMV kernel (NVLink / NVLS stores) or
+        # SpMV + NCCL all-gather
+        from paper_1302_5586_b200.dist import RowShardedCsr, FusedSpmvAllgather
         sh = RowShardedCsr(rowptr, col, val, rank, world)
         rp, cd, vd = (torch.from_numpy(a).cuda() for a in (sh.rowptr, sh.col, sh.val))
         x_local = sh.pad_local_x(torch.from_numpy(x[sh.r0:sh.r1]).cuda())
-        xg = torch.empty(sh.ncols_padded, device="cuda")
-        y = torch.empty(sh.nrows, device="cuda")
+        xg = sh.allgather_x(x_local)  # the gathered x, resident
+        y_pad = torch.zeros(sh.max_rows, device="cuda")
+        y = y_pad[: sh.nrows]
         plan = pb.device.CsrPlan(sh.nrows, sh.ncols_padded, sh.nnz, rp, mode=1)
+        mode = args.dist_mode if args.dist_backend == "nccl" else "nccl"
+        if mode == "fused":
+            try:
+                fz = FusedSpmvAllgather(sh, torch.device("cuda", torch.cuda.current_device()))
+                exchange = "fused SpMV->all-gather (%s)" % ("NVLS multicast stores" if fz.mc else "NVLink peer stores")
+            except Exception as e:  # noqa: BLE001 — no symmetric memory here: the unfused step
+                mode, why = "nccl", str(e).splitlines()[0][:120]
+        if mode == "fused":
 
-        def step():
-            sh.allgather_x(x_local, xg)
-            plan.spmv(rp, cd, vd, xg, y)
+            def step():
+                fz.step(plan, rp, cd, vd, xg, y)
+        else:
+            yg = torch.empty(sh.ncols_padded, device="cuda")
+            exchange = "SpMV + %s all-gather of y" % args.dist_backend
+            if args.dist_mode == "fused" and args.dist_backend == "nccl":
+                exchange += " (fused path unavailable: %s)" % why
+
+            def step():
+                plan.spmv(rp, cd, vd, xg, y)
+                sh.allgather_x(y_pad, yg)
         ms = run_steps(torch, step, args.steps, args.warmup, flush, dist)
         kernel_ms = statistics.mean(ms)
-        launches = args.steps * 2
+        launches = args.steps * (3 if mode == "fused" else 2)  # + the symmetric-memory barrier
     algo = spmv_bytes(nrows, nrows, nnz)
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
            "config": {"workload": "CSR SpMV fp32 (spmv_vec), power-law rows 2^24 x 2^24, 16 nnz/row",
                       "nrows": nrows, "ncols": nrows, "nnz": nnz, "alpha": 1.5, "xm": round(xm, 4),
                       "maxlen": 4096, "seed": 42, "schedule": "csr_flow_kernel, reassociated (persistent warps, 1024-nnz window tiles, continuous 128-bit col/val streams)",
                       "l2": "256 MiB flush between steps, outside the per-step events; inputs 2.35 GB > L2"}}
+    if world > 1:
+        res["config"]["exchange"] = exchange
     if rank == 0 and world == 1 and not args.no_e2e:
         res["e2e"] = e2e_spmv(args, torch, pb, rowptr, col, val, x)
     return res
@@ -424,6 +446,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--suite-steps", type=int, default=10)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--dist-mode", default="fused", choices=["fused", "nccl"],
+                    help="N>1 SpMV step: fused SpMV->all-gather kernel, or SpMV + NCCL all-gather")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 

@@ -100,6 +100,17 @@ int pencil_csr_plan_info(pencil_csr_plan_t plan, int* ntiles, int* tile_nnz);
 int pencil_spmv_dev(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr, const int* col,
                     const float* val, const float* x, float* y);
 
+/* Fused SpMV -> all-gather of y (one step of a row-sharded iterative SpMV): as
+ * pencil_spmv_dev, and every row result y[i] is also stored to peers[q][i] for q < npeers
+ * (device-visible pointers — NVLink peer mappings of the other ranks' gathered-vector buffers,
+ * each offset to this rank's slot) or, when mc is not NULL, once to the NVLS multicast address
+ * mc + i, which the switch replicates to every rank.  The stores are fenced at system scope
+ * before the launch retires; the caller orders the consumers after it with a cross-rank
+ * barrier on `s`.  npeers <= 8. */
+int pencil_spmv_dev_dist(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr, const int* col,
+                         const float* val, const float* x, float* y, float* const* peers, int npeers,
+                         float* mc);
+
 /* synchronize `s`, return and clear the device fault word (PENCIL_OK or PENCIL_E_INTERP) */
 int pencil_sync_status(pencil_stream_t s);
 

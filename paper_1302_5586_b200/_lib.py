@@ -48,6 +48,7 @@ SIGNATURES = {
     "pencil_csr_plan_destroy": (c_int, [P]),
     "pencil_csr_plan_info": (c_int, [P, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "pencil_spmv_dev": (c_int, [P, P, P, P, P, P, P]),
+    "pencil_spmv_dev_dist": (c_int, [P, P, P, P, P, P, P, ctypes.POINTER(c_void_p), c_int, P]),
     "pencil_sync_status": (c_int, [P]),
     # §4 name dispatch
     "pencil_runtime_create": (c_void_p, [c_int]),

@@ -57,11 +57,29 @@ __global__ void csr_plan_kernel(int nrows, int nnz_len, const int* __restrict__ 
     if (blockIdx.x == 0 && threadIdx.x == 0) tile_row[ntiles] = nrows;
 }
 
+// Row result store.  DIST (fused SpMV -> all-gather, launch_csr_spmv_dist): the value also goes
+// to every peer's copy of the gathered vector — one multimem store when an NVLS multicast
+// address is given (the switch replicates it to all ranks), else one store per peer mapping.
+// Row results of a warp are consecutive, so either form leaves as 128-byte NVLink writes.
+template <bool DIST, bool LOCAL = true>
+__device__ __forceinline__ void put_row(float* __restrict__ y, const PeerSet& ps, long long row, float s) {
+    if (LOCAL) y[row] = s;
+    if (DIST) {
+        if (ps.mc)
+            asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(ps.mc + row), "f"(s) : "memory");
+        else
+#pragma unroll
+            for (int q = 0; q < PENCIL_MAX_PEERS; q++)  // unrolled: no local-memory copy of the params
+                if (q < ps.n) ps.p[q][row] = s;
+    }
+}
+
 // Generic schedule (any rowptr): one thread per row, loads straight from global.
-__device__ void spmv_generic(int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr,
-                             const int* __restrict__ col, const float* __restrict__ val,
-                             const float* __restrict__ x, float* __restrict__ y,
-                             unsigned* __restrict__ status) {
+template <bool DIST>
+__device__ void spmv_generic_t(int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr,
+                               const int* __restrict__ col, const float* __restrict__ val,
+                               const float* __restrict__ x, float* __restrict__ y,
+                               unsigned* __restrict__ status, const PeerSet& ps) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nrows;
          i += (long long)gridDim.x * blockDim.x) {
         int lo = __ldg(rowptr + i), hi = __ldg(rowptr + i + 1);
@@ -74,8 +92,15 @@ __device__ void spmv_generic(int nrows, int ncols, int nnz_len, const int* __res
             else raise_fault(status, FAULT_OOB_LOAD);
             s = __fadd_rn(s, __fmul_rn(__ldg(val + k), xv));
         }
-        y[i] = s;
+        put_row<DIST>(y, ps, i, s);
     }
+}
+
+__device__ void spmv_generic(int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr,
+                             const int* __restrict__ col, const float* __restrict__ val,
+                             const float* __restrict__ x, float* __restrict__ y,
+                             unsigned* __restrict__ status) {
+    spmv_generic_t<false>(nrows, ncols, nnz_len, rowptr, col, val, x, y, status, PeerSet{});
 }
 
 // Persistent warps, no CTA-wide barrier: the kernel is bound by the L1TEX rate of random
@@ -325,7 +350,9 @@ __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_v
 // inside a window writes y and the next batch — prefetched — continues in the same window).
 // The batch-aligned kernel restarts its windows at every batch, so each 32-row batch (~512
 // non-zeros here) pays a partial first and last window.
-template <bool ASSOC>
+// DIST: fused SpMV -> all-gather (put_row); the warp fences its peer stores at system scope
+// before it retires, so the barrier that follows the launch publishes them.
+template <bool ASSOC, bool DIST = false>
 #ifndef FLOW_MINB
 #define FLOW_MINB CTAS_PER_SM
 #endif
@@ -333,10 +360,11 @@ __global__ void __launch_bounds__(SPMV_THREADS, FLOW_MINB) csr_flow_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
     const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
-    unsigned* __restrict__ status) {
+    unsigned* __restrict__ status, const PeerSet ps) {
     __shared__ __align__(16) float s_prod[WARPS_PER_CTA][128 + 16];
     if (plan[0]) {
-        spmv_generic(nrows, ncols, nnz_len, rowptr, col, val, x, y, status);
+        spmv_generic_t<DIST>(nrows, ncols, nnz_len, rowptr, col, val, x, y, status, ps);
+        if (DIST) __threadfence_system();
         return;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -349,6 +377,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, FLOW_MINB) csr_flow_kernel(
         ticket = __shfl_sync(0xffffffffu, ticket, 0);
         if (ticket >= (unsigned)ntiles) {
             if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
+            if (DIST) __threadfence_system();
             return;
         }
         const int r0 = __ldg(tile_row + ticket), r1 = __ldg(tile_row + ticket + 1);
@@ -437,6 +466,18 @@ __global__ void __launch_bounds__(SPMV_THREADS, FLOW_MINB) csr_flow_kernel(
             if (rb + 32 < r1) {
                 n_s = __ldg(rowptr + min(rb + 32 + lane, r1));
                 n_e = __ldg(rowptr + min(rb + 64, r1));
+            }
+        }
+        if (DIST) {
+            // the tile's rows leave together after its fold loop, re-read from y (L2) two rows per
+            // lane at a time.  Measured at 2^24 rows with 1 / 7 local targets: +56 / +178 us over
+            // the plain SpMV; storing from registers at each batch instead costs +170 / +420 us
+            // (the store code in the fold loop costs the gather loop its schedule)
+            __syncwarp();
+            for (int r = r0 + lane; r < r1; r += 64) {
+                const float v0 = y[r], v1 = r + 32 < r1 ? y[r + 32] : 0.f;
+                put_row<true, false>(y, ps, r, v0);
+                if (r + 32 < r1) put_row<true, false>(y, ps, r + 32, v1);
             }
         }
     }
@@ -653,9 +694,9 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     if (use_flow && (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
         if (assoc)
             return (int)cudaLaunchKernelEx(&cfg, csr_flow_kernel<true>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                           tile_row, ntiles, plan_flags, status);
+                                           tile_row, ntiles, plan_flags, status, PeerSet{});
         return (int)cudaLaunchKernelEx(&cfg, csr_flow_kernel<false>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                       tile_row, ntiles, plan_flags, status);
+                                       tile_row, ntiles, plan_flags, status, PeerSet{});
     }
     cudaError_t e;
     if (use_vec && (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
@@ -703,6 +744,47 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
 #undef CSR_LAUNCH
     }
     return (int)e;
+}
+
+// y rows -> peers (the distribution step on its own, for operands the fused kernel cannot take)
+__global__ void dist_rows_kernel(int nrows, const float* __restrict__ y, const PeerSet ps) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nrows;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float v = y[i];
+        if (ps.mc)
+            asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(ps.mc + i), "f"(v) : "memory");
+        else
+#pragma unroll
+            for (int q = 0; q < PENCIL_MAX_PEERS; q++)
+                if (q < ps.n) ps.p[q][i] = v;
+    }
+    __threadfence_system();
+}
+
+int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
+                         const int* rowptr, const int* col, const float* val, const float* x, float* y,
+                         const int* tile_row, int ntiles, unsigned* plan_flags, unsigned* status,
+                         const PeerSet& peers) {
+    if (nrows <= 0) return 0;
+    if ((uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
+        int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+        if (grid > PENCIL_NUM_SMS * CTAS_PER_SM) grid = PENCIL_NUM_SMS * CTAS_PER_SM;
+        if (assoc)
+            csr_flow_kernel<true, true><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                                                       tile_row, ntiles, plan_flags, status, peers);
+        else
+            csr_flow_kernel<false, true><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                                                        tile_row, ntiles, plan_flags, status, peers);
+        return (int)cudaGetLastError();
+    }
+    // unaligned col/val: the regular executor, then the rows leave in a second launch
+    int e = launch_csr_spmv(st, assoc, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles,
+                            plan_flags, status);
+    if (e) return e;
+    long long blocks = ((long long)nrows + 255) / 256;
+    if (blocks > PENCIL_NUM_SMS * 8) blocks = PENCIL_NUM_SMS * 8;
+    dist_rows_kernel<<<(int)blocks, 256, 0, st>>>(nrows, y, peers);
+    return (int)cudaGetLastError();
 }
 
 __global__ void csr_generic_kernel(int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr,

@@ -29,6 +29,19 @@ int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const
                        const int* col, const float* val, const float* x, float* y,
                        unsigned* status);
 int csr_tile_nnz();
+// fused SpMV -> all-gather of y: every row result is also stored to `n` peer buffers (NVLink
+// peer mappings, each already offset to this rank's slot) or, when mc is set, once to an NVLS
+// multicast address that replicates it to every rank
+#define PENCIL_MAX_PEERS 8
+struct PeerSet {
+    float* p[PENCIL_MAX_PEERS];
+    float* mc;
+    int n;
+};
+int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
+                         const int* rowptr, const int* col, const float* val, const float* x, float* y,
+                         const int* tile_row, int ntiles, unsigned* plan_flags, unsigned* status,
+                         const PeerSet& peers);
 
 // k_conv.cu  (taps are host arrays, passed to the kernels by value)
 int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const float* k25,

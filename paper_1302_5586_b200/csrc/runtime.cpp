@@ -731,6 +731,24 @@ int pencil_spmv_dev(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr
                             plan->tile_row, plan->ntiles, plan->flags, c->status));
 }
 
+int pencil_spmv_dev_dist(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr, const int* col,
+                         const float* val, const float* x, float* y, float* const* peers, int npeers,
+                         float* mc) {
+    if (!plan) return fail(PENCIL_E_ARG, "null plan");
+    if (npeers < 0 || npeers > PENCIL_MAX_PEERS || (npeers > 0 && !peers))
+        return fail(PENCIL_E_ARG, "npeers must be 0..%d", PENCIL_MAX_PEERS);
+    PeerSet ps = {};
+    for (int q = 0; q < npeers; q++) {
+        if (!peers[q]) return fail(PENCIL_E_ARG, "null peer pointer %d", q);
+        ps.p[q] = peers[q];
+    }
+    ps.n = npeers;
+    ps.mc = mc;
+    DEV_PROLOGUE;
+    DEV_RET(launch_csr_spmv_dist(st, plan->mode, plan->nrows, plan->ncols, plan->nnz, rowptr, col, val, x, y,
+                                 plan->tile_row, plan->ntiles, plan->flags, c->status, ps));
+}
+
 int pencil_sync_status(pencil_stream_t s) {
     DEV_PROLOGUE;
     return collect_faults(c, st) == PENCIL_OK ? ok() : g_status;

@@ -97,6 +97,15 @@ class CsrPlan:
         _chk(self._lib.pencil_spmv_dev(_stream(stream), self.handle, rowptr.data_ptr(), col.data_ptr(),
                                        val.data_ptr(), x.data_ptr(), y.data_ptr()))
 
+    def spmv_dist(self, rowptr, col, val, x, y, peers=(), mc=0, stream=None):
+        """Fused SpMV -> all-gather (pencil_spmv_dev_dist): y as spmv(), and every row result
+        also stored at peers[q] + 4*i (device addresses, ints) or once at the multicast
+        address mc + 4*i."""
+        arr = (ctypes.c_void_p * max(1, len(peers)))(*[int(p) for p in peers])
+        _chk(self._lib.pencil_spmv_dev_dist(_stream(stream), self.handle, rowptr.data_ptr(), col.data_ptr(),
+                                            val.data_ptr(), x.data_ptr(), y.data_ptr(), arr, len(peers),
+                                            int(mc) or None))
+
     def close(self):
         if self.handle:
             self._lib.pencil_csr_plan_destroy(self.handle)

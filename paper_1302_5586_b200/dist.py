@@ -2,10 +2,11 @@
 (NCCL on B200s, gloo for the CPU tests).  The data path per step:
 
   * CSR SpMV / gemv — row blocks balanced by non-zeros (pencil_shard_rows_by_nnz).  Each rank owns
-    rows [r0, r1) of A and the same slice of x; a step all-gathers x (one NCCL all_gather into a
-    rank-padded buffer) and runs the local SpMV.  Column indices are remapped once, at setup,
-    into the padded layout (col -> owner*max_rows + col - bounds[owner]) so no unpad copy runs
-    per step.
+    rows [r0, r1) of A and the same slice of x; x is gathered into a rank-padded buffer.  Column
+    indices are remapped once, at setup, into the padded layout (col -> owner*max_rows + col -
+    bounds[owner]) so no unpad copy runs per step.  The step of an iterative method (y = A x,
+    y gathered as the next x) runs fused (FusedSpmvAllgather: the SpMV kernel stores its rows
+    into every rank's buffer over NVLink / NVLS multicast) or as SpMV + NCCL all-gather.
   * 5x5 stencils — equal row bands; each rank exchanges 2 halo rows with each neighbour
     (send/recv) and runs the stencil on its band extended by the halos.
   * gemv — row blocks, x replicated (all-gathered from its shards when it starts sharded);
@@ -84,6 +85,48 @@ class RowShardedCsr:
         else:  # gloo (CPU tests): list form
             dist.all_gather(list(out.view(self.world, self.max_rows).unbind(0)), x_local_padded)
         return out
+
+
+def dist_targets(buffer_ptrs, offset, multicast_ptr, rank, max_rows):
+    """Where rank `rank`'s row results go in the fused SpMV -> all-gather step: its slot
+    [rank*max_rows, (rank+1)*max_rows) of every rank's gathered-vector buffer (the padded layout
+    RowShardedCsr remaps columns into, so the result is the next step's x as is).  Returns
+    (peer addresses, multicast address): one multimem store per row when the group has an NVLS
+    multicast mapping, else one store per rank's peer mapping."""
+    slot = 4 * rank * max_rows + offset
+    if multicast_ptr:
+        return [], multicast_ptr + slot
+    return [int(b) + slot for b in buffer_ptrs], 0
+
+
+class FusedSpmvAllgather:
+    """Row-sharded SpMV step whose result reaches every rank inside the SpMV kernel
+    (pencil_spmv_dev_dist): each warp stores its finished rows to the rank's slot of every
+    rank's gathered-vector buffer (torch symmetric memory: NVLink peer mappings, NVLS multicast
+    when the switch offers it) while the rest of the matrix is still being multiplied, so the
+    exchange overlaps the compute row batch by row batch; a symmetric-memory barrier on the
+    stream orders the consumers after it.  The unfused equivalent is SpMV + NCCL all-gather of
+    y (`RowShardedCsr.allgather_x`)."""
+
+    def __init__(self, shard, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.sh = shard
+        self.buf = symm.empty(shard.ncols_padded, dtype=torch.float32, device=device)
+        self.buf.zero_()
+        self.hdl = symm.rendezvous(self.buf, group or dist.group.WORLD)
+        mc = int(self.hdl.multicast_ptr or 0)  # 0: no NVLS multicast mapping for this group
+        base = int(self.hdl.buffer_ptrs[self.hdl.rank])
+        offset = self.buf.data_ptr() - base
+        self.peers, self.mc = dist_targets(self.hdl.buffer_ptrs, offset, mc, shard.rank, shard.max_rows)
+
+    def step(self, plan, rowptr, col, val, x, y):
+        """y = A_local x for this rank's rows; returns the gathered buffer (every rank's rows,
+        padded layout), valid on every rank once this returns (stream order)."""
+        plan.spmv_dist(rowptr, col, val, x, y, self.peers, self.mc)
+        self.hdl.barrier(channel=0)
+        return self.buf
 
 
 class BandShardedImage:

@@ -52,6 +52,65 @@ def _spmv_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _fused_worker(rank, world, port, q, multicast=False):
+    """The fused SpMV -> all-gather step (FusedSpmvAllgather) with its device stores emulated:
+    each rank 'stores' its row results at the addresses dist_targets gives for fake per-rank
+    buffer bases (or a fake multicast base), every rank assembles the writes that land in its
+    own buffer, and three iterations A(A(A x)) over the gathered buffers must equal the
+    single-process result bit for bit."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    from paper_1302_5586_b200 import synth
+    from paper_1302_5586_b200.dist import RowShardedCsr, dist_targets
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rowptr, col, val, x, _ = synth.csr_powerlaw(3000, maxlen=500, seed=11)
+        sh = RowShardedCsr(rowptr, col, val, rank, world)
+        bases = [(r + 1) << 36 for r in range(world)]
+        MC = 7 << 40
+        offset = 256
+        peers, mc = dist_targets(bases, offset, MC if multicast else 0, rank, sh.max_rows)
+        assert (mc != 0) == multicast and (len(peers) == (0 if multicast else world))
+        xg = sh.allgather_x(sh.pad_local_x(torch.from_numpy(x[sh.r0:sh.r1].copy())))
+        buf = xg.numpy().copy()
+        for it in range(2):
+            y = oracle.spmv_f32(sh.nrows, sh.ncols_padded, sh.nnz, sh.rowptr, sh.col, sh.val, buf)
+            # the kernel's stores: y[i] -> address + 4*i, for each target
+            writes = [(t, y) for t in (peers if not mc else [mc])]
+            allw = [None] * world
+            dist.all_gather_object(allw, writes)
+            nxt = np.full(sh.ncols_padded, np.nan, np.float32)
+            for wr in allw:
+                for t, yy in wr:
+                    mine = bases[rank] if not multicast else MC
+                    if not multicast and not (bases[rank] <= t < bases[rank] + (1 << 36)):
+                        continue  # a store into another rank's buffer
+                    start = (t - mine - offset) // 4
+                    assert (t - mine - offset) % 4 == 0 and 0 <= start and start + yy.size <= nxt.size
+                    nxt[start:start + yy.size] = yy
+            # padding slots stay unwritten; everything the remapped columns read must be written
+            used = np.unique(sh.col)
+            assert not np.isnan(nxt[used]).any()
+            buf = np.nan_to_num(nxt)
+        y2 = oracle.spmv_f32(sh.nrows, sh.ncols_padded, sh.nnz, sh.rowptr, sh.col, sh.val, buf)
+        n = rowptr.size - 1
+        ref = oracle.spmv_f32(n, n, col.size, rowptr, col, val,
+                              oracle.spmv_f32(n, n, col.size, rowptr, col, val,
+                                              oracle.spmv_f32(n, n, col.size, rowptr, col, val, x)))
+        ok = torch.tensor([int(np.array_equal(y2.view(np.uint32), ref[sh.r0:sh.r1].view(np.uint32)))])
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            q.put(bool(ok.item()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _fused_worker_mc(rank, world, port, q):
+    _fused_worker(rank, world, port, q, multicast=True)
+
+
 def _conv_worker(rank, world, port, q):
     import sys
     sys.path.insert(0, ROOT)
@@ -159,3 +218,10 @@ def test_dense_shards_gemv_gemvt_dot_axpy_gemm_gloo(world):
     ok, res = _run(_dense_worker, world)
     assert ok, res
     assert res["grid"][0] * res["grid"][1] == world
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("multicast", [False, True])
+def test_fused_spmv_allgather_targets_gloo(world, multicast):
+    """Three iterations (x -> Ax -> A^2x -> A^3x) through the fused step's store targets."""
+    assert _run(_fused_worker_mc if multicast else _fused_worker, world)

@@ -72,3 +72,59 @@ def test_dense_shards_over_nccl(nccl):
     ref = torch.from_numpy(C.copy()).cuda()
     pb.device.gemm(m, nn, k, 1.0, 0.5, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), ref)
     assert torch.equal(out.reshape(-1), ref)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("aligned", [True, False])
+def test_spmv_dist_peer_stores(cuda, mode, aligned):
+    """pencil_spmv_dev_dist with three peer targets (plain device buffers standing in for the
+    NVLink mappings, at different slot offsets): y and every target equal the plain SpMV bit for
+    bit.  Unaligned col/val take the regular executor + the row-distribution launch."""
+    import torch
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200 import synth
+    rowptr, col, val, x, _ = synth.csr_powerlaw(70000, maxlen=3000, seed=9)
+    nrows, nnz = rowptr.size - 1, col.size
+    sh = 0 if aligned else 1
+    rp = torch.from_numpy(rowptr).cuda()
+    cd = torch.zeros(nnz + sh, dtype=torch.int32, device="cuda")[sh:]
+    vd = torch.zeros(nnz + sh, device="cuda")[sh:]
+    cd.copy_(torch.from_numpy(col))
+    vd.copy_(torch.from_numpy(val))
+    xd = torch.from_numpy(x).cuda()
+    plan = pb.device.CsrPlan(nrows, nrows, nnz, rp, mode=mode)
+    ref = torch.empty(nrows, device="cuda")
+    plan.spmv(rp, cd, vd, xd, ref)
+    bufs = [torch.full((nrows + 1000 * q,), float("nan"), device="cuda") for q in range(3)]
+    peers = [b.data_ptr() + 4 * 1000 * q for q, b in enumerate(bufs)]
+    y = torch.empty(nrows, device="cuda")
+    plan.spmv_dist(rp, cd, vd, xd, y, peers)
+    pb.device.sync_status()
+    assert torch.equal(y.view(torch.int32), ref.view(torch.int32))
+    for q, b in enumerate(bufs):
+        assert torch.equal(b[1000 * q:].view(torch.int32), ref.view(torch.int32))
+        assert torch.isnan(b[:1000 * q]).all()  # nothing outside the slot
+
+
+def test_fused_spmv_allgather_world1(nccl):
+    """FusedSpmvAllgather on a real NCCL group + torch symmetric memory (world 1): the gathered
+    buffer holds the rank's rows after the barrier; multicast is used when the group has it."""
+    import torch
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200 import synth
+    from paper_1302_5586_b200.dist import RowShardedCsr, FusedSpmvAllgather
+    rowptr, col, val, x, _ = synth.csr_powerlaw(100000, maxlen=2048, seed=6)
+    sh = RowShardedCsr(rowptr, col, val, 0, 1)
+    rp, cd, vd = (torch.from_numpy(a).cuda() for a in (sh.rowptr, sh.col, sh.val))
+    xg = sh.allgather_x(sh.pad_local_x(torch.from_numpy(x).cuda()))
+    plan = pb.device.CsrPlan(sh.nrows, sh.ncols_padded, sh.nnz, rp, mode=1)
+    fz = FusedSpmvAllgather(sh, torch.device("cuda", torch.cuda.current_device()))
+    y = torch.empty(sh.nrows, device="cuda")
+    out = fz.step(plan, rp, cd, vd, xg, y)
+    ref = torch.empty(sh.nrows, device="cuda")
+    plan.spmv(rp, cd, vd, xg, ref)
+    torch.cuda.synchronize()
+    pb.device.sync_status()
+    assert torch.equal(y.view(torch.int32), ref.view(torch.int32))
+    assert torch.equal(out[: sh.nrows].view(torch.int32), ref.view(torch.int32))
+    print("multicast" if fz.mc else "peer stores", len(fz.peers))
