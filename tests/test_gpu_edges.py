@@ -152,3 +152,38 @@ def test_interpreter_mirror_errors(cuda):
         it.call("dot", [pb.Arg.scalar(7), pb.Arg.array("A"), pb.Arg.array("A")])
     assert e.value.code == "E-INTERP"
     assert it.call("dot", [pb.Arg.scalar(6), pb.Arg.array("A"), pb.Arg.array("A")]) > 0
+
+
+SEPARABLE = [  # integer rank-1 taps k = u (x) v: the SEP kernels (horizontal pass on row entry)
+    (np.outer([1, 4, 6, 4, 1], [1, 4, 6, 4, 1]), 256),
+    (np.outer([1, -2, 1, 0, 0], [-1, 0, 2, 0, -1]), 1),
+    (np.outer([0, 3, 0, -3, 0], [2, 4, 6, 4, 2]), 10),      # v not primitive: factored as 2 * (1,2,3,2,1)
+    (np.outer([5, 5, 5, 5, 5], [5, 5, 5, 5, 5]), 625),      # near the fp32-exact bound
+    (np.outer([0, 0, 1, 0, 0], [0, 0, 1, 0, 0]), 1),        # identity
+    (np.outer([-1, -1, -1, -1, -1], [1, 1, 1, 1, 1]), 3),   # all-negative sums clamp to 0
+]
+
+
+@pytest.mark.parametrize("h,w", [(67, 256), (9, 132), (130, 516), (5, 4)])
+def test_conv_u8_separable_taps_bit_exact(cuda, h, w):
+    """Rank-1 integer taps take the separable kernels (int32 storage and packed bytes): bit-exact
+    against the 25-tap oracle, edges clamped, pow2 and non-pow2 scales."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    img = synth.u8_i32(h * w, seed=h + w)
+    for k, scale in SEPARABLE:
+        k = np.ascontiguousarray(k.reshape(-1), np.int32)
+        ref = oracle.conv5x5_u8(h, w, scale, img, k)
+        out = np.zeros(h * w, np.int32)
+        pb.dropin.conv5x5_u8(h, w, scale, img, k, out)
+        assert np.array_equal(out.astype(np.int64), ref), (k, scale)
+        out8 = torch.empty(h * w, dtype=torch.uint8, device="cuda")
+        pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img.astype(np.uint8)).cuda(), k, out8)
+        assert np.array_equal(out8.cpu().numpy().astype(np.int64), ref), (k, scale)
+    # a non-byte value in int32 storage still diverts to the exact repair pass
+    bad = img.copy()
+    bad[h // 2 * w + 1] = 4000
+    k = np.ascontiguousarray(SEPARABLE[1][0].reshape(-1), np.int32)
+    out = np.zeros(h * w, np.int32)
+    pb.dropin.conv5x5_u8(h, w, 1, bad, k, out)
+    assert np.array_equal(out.astype(np.int64), oracle.conv5x5_u8(h, w, 1, bad, k))
