@@ -85,8 +85,23 @@ struct StencilArgs {
     int exact_only;            // U8: taps too large for the fp32 path
     unsigned* repair_flag;     // U8: set when some window held a value outside [0, 255]
 };
+// The F32 kernel's arguments: StencilArgs without the separable taps.  (ptxas' register
+// allocation follows the parameter layout: F32 measured 0.475 ms with this layout, 0.514 with
+// ku/kv in it; the U8 kernels the other way round, 0.413 vs 0.425 ms.)
+struct StencilArgsF32 {
+    float kf[25];
+    long long ki[25];
+    u64 negz, one;
+    u64 negmag;
+    u64 inv_scale, half_scaled, magic2;
+    int scale, shift;
+    unsigned long long magic;
+    int exact_only;
+    unsigned* repair_flag;
+};
 
-__device__ __forceinline__ unsigned sat_div(long long acc, const StencilArgs& a) {
+template <typename A>
+__device__ __forceinline__ unsigned sat_div(long long acc, const A& a) {
     if (a.scale > 0) {
         const long long nn = acc + (a.scale >> 1);
         if (nn < 0) return 0u;
@@ -106,10 +121,12 @@ __device__ __forceinline__ unsigned sat_div(long long acc, const StencilArgs& a)
 template <bool U8>
 struct Pol {
     typedef float T;
+    typedef StencilArgsF32 A;
 };
 template <>
 struct Pol<true> {
     typedef int T;
+    typedef StencilArgs A;
 };
 
 // Per-lane copy plan, fixed for the whole sweep: lane l copies columns c..c+3 (c = c0 + 4l) of
@@ -146,9 +163,9 @@ __device__ __forceinline__ void ring_issue(const T* src, const RingLane& L, int 
 //   U8:  6 pairs P[m] = (e[m], e[m+2]) for pixel pairs (c, c+2) and (c+1, c+3) (taps P[dj],
 //        P[dj+1]); each pair is converted int -> float by its own LOP3s + one FFMA2, so it lands
 //        in fresh registers too.  `orv` collects every value read (non-byte check).
-template <bool U8>
+template <bool U8, typename A>
 __device__ __forceinline__ void ring_read(const typename Pol<U8>::T* slot, int w, int c0, int lane,
-                                          const StencilArgs& a, u64 (&P)[7], unsigned& orv) {
+                                          const A& a, u64 (&P)[7], unsigned& orv) {
     const int c = c0 + 4 * lane;
     // columns c-2 .. c+5 sit at ring index 4*lane+2 .. 4*lane+9: 8 B + 16 B + 8 B aligned reads
     const typename Pol<U8>::T* p = slot + 4 * lane + 2;
@@ -194,9 +211,9 @@ __device__ __forceinline__ void ring_read(const typename Pol<U8>::T* slot, int w
 // (c, c+2) and (c+1, c+3) of sum_dj kv[dj] * e[m+dj] — so each output row then costs 5
 // vertical FFMA2 per pair instead of 25.  Integer sums regroup exactly (all partial sums stay
 // below 2^22), so the result is the full 25-tap sum bit for bit.
-template <bool SEP>
-__device__ __forceinline__ void enter_row(const u64 (&P)[7], u64 (&Wr)[7], const StencilArgs& a) {
-    if (SEP) {
+template <bool SEP, typename A>
+__device__ __forceinline__ void enter_row(const u64 (&P)[7], u64 (&Wr)[7], const A& a) {
+    if constexpr (SEP) {
         u64 h02 = 0ull, h13 = 0ull;
 #pragma unroll
         for (int dj = 0; dj < 5; dj++) {
@@ -240,7 +257,7 @@ template <bool U8, int S, bool POW2, bool SEP>
 __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int r_end, const RingLane& L,
                                              typename Pol<U8>::T (*ring)[S_ROWE], u64 (&W)[5][7],
                                              Sweep<typename Pol<U8>::T>& sw, unsigned& orv,
-                                             const StencilArgs& a) {
+                                             const typename Pol<U8>::A& a) {
     typedef typename Pol<U8>::T T;
     // the ring holds rows i+2 .. i+2+S_RING-1 in flight; the oldest (row i+2) must have landed
     cp_wait<S_RING - 1>();
@@ -264,7 +281,7 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
 #pragma unroll
     for (int di = 0; di < 5; di++) {
         const int sl = (S + 1 + di) % 5;
-        if (SEP) {  // vertical pass over the horizontally filtered rows
+        if constexpr (SEP) {  // vertical pass over the horizontally filtered rows
             const u64 kk = f2pk(a.ku[di], a.ku[di]);
             a01 = f2fma(kk, W[sl][0], a01);
             a23 = f2fma(kk, W[sl][1], a23);
@@ -328,7 +345,8 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
 #endif
 template <bool U8, bool POW2, bool SEP = false>
 __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? STENCIL_U8_MINB : STENCIL_F32_MINB)) stencil_ring_kernel(
-    int h, int w, const typename Pol<U8>::T* __restrict__ img, typename Pol<U8>::T* __restrict__ out, StencilArgs a) {
+    int h, int w, const typename Pol<U8>::T* __restrict__ img, typename Pol<U8>::T* __restrict__ out,
+    typename Pol<U8>::A a) {
     typedef typename Pol<U8>::T T;
     __shared__ __align__(16) T ring_all[S_WARPS][S_RING][S_ROWE];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -466,7 +484,7 @@ __device__ __forceinline__ void bytes_step(int w, int i, int c, int lane, int r_
 #pragma unroll
     for (int di = 0; di < 5; di++) {
         const int sl = (S + 1 + di) % 5;
-        if (SEP) {
+        if constexpr (SEP) {
             const u64 kk = f2pk(a.ku[di], a.ku[di]);
             a02 = f2fma(kk, W[sl][0], a02);
             a13 = f2fma(kk, W[sl][1], a13);
@@ -620,7 +638,7 @@ int launch_conv5x5_u8_reg(cudaStream_t st, int h, int w, int scale, const int* i
 int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const float* k25, float* out) {
     if (h < 5 || w < 5) return 0;
     if (!ring_ok(h, w, img, out)) return launch_conv5x5_f32_reg(st, h, w, img, k25, out);
-    StencilArgs a = {};
+    StencilArgsF32 a = {};
     for (int t = 0; t < 25; t++) a.kf[t] = k25[t];
     a.negz = pack2(-0.0f);
     a.one = pack2(1.0f);
