@@ -22,12 +22,15 @@ if "f32" in which:
     img = torch.from_numpy(synth.f32(h * w)).cuda(); o = torch.zeros(h * w, device="cuda")
     kf = (synth.BINOMIAL.astype(np.float32) / 256.0).astype(np.float32)
     out["conv_f32_ms"] = t(lambda: pb.device.conv5x5_f32(h, w, img, kf, o)); del img, o
-if "u8" in which:
+# u8 / u8b: binomial (separable kernels) and sharpen (25-tap kernels); u8sharp / u8bsharp: sharpen only
+if "u8" in which or "u8sharp" in which:
     img = torch.from_numpy(synth.u8_i32(h * w)).cuda(); o = torch.empty(h * w, dtype=torch.int32, device="cuda")
-    out["conv_u8_i32_ms"] = t(lambda: pb.device.conv5x5_u8(h, w, 256, img, synth.BINOMIAL, o))
+    if "u8" in which:
+        out["conv_u8_i32_ms"] = t(lambda: pb.device.conv5x5_u8(h, w, 256, img, synth.BINOMIAL, o))
     out["conv_u8_i32_sharpen_ms"] = t(lambda: pb.device.conv5x5_u8(h, w, 1, img, synth.SHARPEN, o)); del img, o
-if "u8b" in which:
+if "u8b" in which or "u8bsharp" in which:
     img = torch.from_numpy(synth.u8(h * w)).cuda(); o = torch.empty(h * w, dtype=torch.uint8, device="cuda")
-    out["conv_u8_bytes_ms"] = t(lambda: pb.device.conv5x5_u8_bytes(h, w, 256, img, synth.BINOMIAL, o))
+    if "u8b" in which:
+        out["conv_u8_bytes_ms"] = t(lambda: pb.device.conv5x5_u8_bytes(h, w, 256, img, synth.BINOMIAL, o))
     out["conv_u8_bytes_sharpen_ms"] = t(lambda: pb.device.conv5x5_u8_bytes(h, w, 1, img, synth.SHARPEN, o))
 print(json.dumps(out))
