@@ -1,0 +1,91 @@
+"""Re-entrancy (SURVEY §8b threading): the drop-in entry points called from several host
+threads at once give the single-threaded results, and the error channel is per thread — a
+thread whose call faults (E-INTERP) does not see, or leak its status into, the others' calls."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1302_5586_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def test_concurrent_dropin_calls_match_sequential(cuda):
+    import paper_1302_5586_b200 as pb
+    rowptr, col, val, x, _ = synth.csr_powerlaw(30000, maxlen=500, seed=21)
+    nrows, nnz = rowptr.size - 1, col.size
+    m, n = 700, 513
+    A, xv = synth.f32(m * n, 4), synth.f32(n, 5)
+    h, w = 90, 132
+    img = synth.u8_i32(h * w, seed=8)
+    ref_spmv = np.zeros(nrows, np.float32)
+    pb.dropin.spmv_inline(nrows, nrows, nnz, rowptr, col, val, x, ref_spmv)
+    ref_conv = oracle.conv5x5_u8(h, w, 256, img, synth.BINOMIAL)
+    ref_gemv = np.zeros(m, np.float32)
+    pb.dropin.gemv(m, n, 1.0, 0.0, A, xv, ref_gemv)
+    errors = []
+
+    def worker(tid):
+        try:
+            for it in range(6):
+                kind = (tid + it) % 3
+                if kind == 0:
+                    y = np.zeros(nrows, np.float32)
+                    pb.dropin.spmv_inline(nrows, nrows, nnz, rowptr, col, val, x, y)
+                    assert np.array_equal(y.view(np.uint32), ref_spmv.view(np.uint32))
+                elif kind == 1:
+                    out = np.zeros(h * w, np.int32)
+                    pb.dropin.conv5x5_u8(h, w, 256, img, synth.BINOMIAL, out)
+                    assert np.array_equal(out.astype(np.int64), ref_conv)
+                else:
+                    y = np.zeros(m, np.float32)
+                    pb.dropin.gemv(m, n, 1.0, 0.0, A, xv, y)
+                    assert np.array_equal(y.view(np.uint32), ref_gemv.view(np.uint32))
+                assert pb.load().pencil_cuda_last_status() == 0
+        except BaseException as e:  # noqa: BLE001
+            errors.append((tid, repr(e)))
+
+    ts = [threading.Thread(target=worker, args=(t,)) for t in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+
+
+def test_fault_status_is_per_thread(cuda):
+    import paper_1302_5586_b200 as pb
+    rowptr = np.array([0, 2, 3], np.int32)
+    bad_col = np.array([0, 99, 1], np.int32)  # column 99 >= ncols: E-INTERP
+    val = np.ones(3, np.float32)
+    x = np.ones(4, np.float32)
+    results = {}
+    go = threading.Barrier(2)
+
+    def faulty():
+        go.wait()
+        try:
+            pb.dropin.spmv_inline(2, 4, 3, rowptr, bad_col, val, x, np.zeros(2, np.float32))
+            results["faulty"] = "no error"
+        except pb.PencilError as e:
+            results["faulty"] = e.code
+        results["faulty_status"] = pb.load().pencil_cuda_last_status()
+
+    def clean():
+        go.wait()
+        y = np.zeros(2, np.float32)
+        for _ in range(20):
+            pb.dropin.spmv_inline(2, 4, 3, rowptr, np.array([0, 1, 1], np.int32), val, x, y)
+        results["clean_status"] = pb.load().pencil_cuda_last_status()
+        results["clean_y"] = y.tolist()
+
+    ts = [threading.Thread(target=faulty), threading.Thread(target=clean)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert results["faulty"] == "E-INTERP"
+    assert results["faulty_status"] != 0
+    assert results["clean_status"] == 0 and results["clean_y"] == [2.0, 1.0]
