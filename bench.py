@@ -148,6 +148,13 @@ def bench_spmv(args, torch, pb, rank, world, dist):
         pb.device.sync_status()
         launches = args.steps * 2  # spmv + l2 flush per step
         kernel_ms = statistics.mean(ms)
+        # the measured ceiling of this matrix: the same col/val stream and x gathers without the
+        # rows (k_micro.cu micro_gather_val), timed the same way, outside the timed SpMV steps
+        lib, st = pb.load(), torch.cuda.current_stream().cuda_stream
+        res_buf = torch.empty(148 * 8 * 256, device="cuda")
+        ceil_ms = statistics.mean(run_steps(
+            torch, lambda: lib.pencil_micro_gather_val(st, nnz, cd.data_ptr(), vd.data_ptr(), xd.data_ptr(),
+                                                       res_buf.data_ptr()), max(3, args.steps // 2), 2, flush))
     else:
         # one step of a row-sharded iterative SpMV: y = A x for the rank's rows, y gathered on
         # every rank (the next step's x) — fused into the SpMV kernel (NVLink / NVLS stores) or
@@ -185,6 +192,7 @@ def bench_spmv(args, torch, pb, rank, world, dist):
         launches = args.steps * (3 if mode == "fused" else 2)  # + the symmetric-memory barrier
     algo = spmv_bytes(nrows, nrows, nnz)
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
+           "ceiling_ms": ceil_ms if world == 1 else None,
            "config": {"workload": "CSR SpMV fp32 (spmv_vec), power-law rows 2^24 x 2^24, 16 nnz/row",
                       "nrows": nrows, "ncols": nrows, "nnz": nnz, "alpha": 1.5, "xm": round(xm, 4),
                       "maxlen": 4096, "seed": 42, "schedule": "csr_flow_kernel, reassociated (persistent warps, 1024-nnz window tiles, continuous 128-bit col/val streams)",
@@ -506,7 +514,11 @@ def main():
                                 "peak": hbm, "unit": "GB/s", "frac": kernel_gbs / hbm,
                                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
                                 "algorithmic_bytes_per_launch": res["bytes"],
-                                "traffic": ncu_traffic("csr_flow_kernel")}
+                                "traffic": ncu_traffic("csr_flow_kernel"),
+                                "measured_ceiling": {
+                                    "kernel": "micro_gather_val: the same col/val stream + x gathers, no rows "
+                                              "(random 4-byte gathers are L1->XBAR request-rate bound, DESIGN.md §3)",
+                                    "ms": res["ceiling_ms"], "frac": res["ceiling_ms"] / res["ms"]}}
         line["clocks"] = clk.summary()
         if "e2e" in res:
             line["e2e"] = res["e2e"]
