@@ -641,22 +641,28 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     // against the 2 GB col/val stream (per-launch access-policy window, PENCIL_SPMV_PERSIST=1;
     // by default the evict-last load policy alone does this).
     cudaLaunchAttribute attr[1];
-    static int persist = -1;
-    static size_t persist_bytes = 0;
-    if (persist < 0) {
+    // opt-in: persisting lines outlive the launch and shrink L2 for the caller's next kernels
+    // (measured with the flow kernel: DRAM read 4.30 -> 2.70 GB per SpMV, but no time gain, and
+    // axpy / the stencils 2.2-2.4x slower afterwards — the set-aside L2, not the lines: a
+    // Normal-window re-read of x after the launch does not undo it)
+    struct PersistCfg {
+        int on;
+        size_t bytes;
+    };
+    static const PersistCfg pcfg = [] {  // read once (thread-safe static initialisation)
         const char* e = getenv("PENCIL_SPMV_PERSIST");
-        // opt-in: persisting lines outlive the launch and shrink L2 for the caller's next kernels
-        // (measured with the flow kernel: DRAM read 4.30 -> 2.70 GB per SpMV, but no time gain, and
-        // axpy / the stencils 2.2-2.4x slower afterwards — the set-aside L2, not the lines: a
-        // Normal-window re-read of x after the launch does not undo it)
-        persist = (e && e[0] == '1');
+        PersistCfg c = {(e && e[0] == '1') ? 1 : 0, 0};
+        if (!c.on) return c;
         int dev = 0, maxp = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        persist_bytes = (size_t)maxp;
-        if (persist && persist_bytes) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist_bytes);
+        c.bytes = (size_t)maxp;
+        if (c.bytes) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c.bytes);
         cudaGetLastError();
-    }
+        return c;
+    }();
+    const int persist = pcfg.on;
+    const size_t persist_bytes = pcfg.bytes;
     size_t xbytes = (size_t)ncols * sizeof(float);
     if (persist && persist_bytes && xbytes) {
         int dev = 0, maxwin = 0;
@@ -686,16 +692,18 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     // chain of dependent smem adds that only many warps interleaved can hide; and an L2
     // prefetch of the col/val windows 1 / 2 / 4 ahead through the TMA engine
     // (cp.async.bulk.prefetch.L2, one lane, no registers): 1.38 / 1.45 / 1.41 ms.
-    static int use_tma = -1, use_vec = -1, use_flow = -1;
-    if (use_tma < 0) {
+    // default: the continuous-stream kernel (1.250 ms at 2^24 rows; batch-aligned 128-bit
+    // kernel `vec` 1.265-1.273; scalar-load kernel `lsu` 1.282-1.288; PENCIL_SPMV_VU=2 with vec,
+    // 8 non-zeros per lane: 1.355; a mask-free path for interior windows: 8 B of spills, no gain)
+    static const int kernel_sel = [] {  // 0 flow, 1 vec, 2 lsu, 3 tma; read once
         const char* e = getenv("PENCIL_SPMV_KERNEL");
-        use_tma = (e && !strcmp(e, "tma"));
-        // default: the continuous-stream kernel (1.250 ms at 2^24 rows; batch-aligned 128-bit
-        // kernel `vec` 1.265-1.273; scalar-load kernel `lsu` 1.282-1.288; PENCIL_SPMV_VU=2 with vec,
-        // 8 non-zeros per lane: 1.355; a mask-free path for interior windows: 8 B of spills, no gain)
-        use_flow = !(e && (!strcmp(e, "lsu") || !strcmp(e, "tma") || !strcmp(e, "vec")));
-        use_vec = !(e && (!strcmp(e, "lsu") || !strcmp(e, "tma")));
-    }
+        if (!e) return 0;
+        if (!strcmp(e, "vec")) return 1;
+        if (!strcmp(e, "lsu")) return 2;
+        if (!strcmp(e, "tma")) return 3;
+        return 0;
+    }();
+    const int use_tma = kernel_sel == 3, use_flow = kernel_sel == 0, use_vec = kernel_sel <= 1;
     if (use_flow && (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
         if (assoc)
             return (int)cudaLaunchKernelEx(&cfg, csr_flow_kernel<true>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
@@ -705,11 +713,10 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     }
     cudaError_t e;
     if (use_vec && (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
-        static int vu = -1;
-        if (vu < 0) {
+        static const int vu = [] {
             const char* w = getenv("PENCIL_SPMV_VU");
-            vu = (w && w[0] == '2') ? 2 : 1;
-        }
+            return (w && w[0] == '2') ? 2 : 1;
+        }();
         if (vu == 2) {
             if ((int)cfg.gridDim.x > PENCIL_NUM_SMS * 6) cfg.gridDim = dim3(PENCIL_NUM_SMS * 6);
             if (assoc)
@@ -735,12 +742,11 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     } else {
         // chunk of non-zeros per warp step (gathers in flight per lane = wch / 32);
         // PENCIL_SPMV_WCHUNK = 64 | 128 | 256 (tuning knob, default 128)
-        static int wch = -1;
-        if (wch < 0) {
+        static const int wch = [] {
             const char* w = getenv("PENCIL_SPMV_WCHUNK");
-            wch = w ? atoi(w) : 128;
-            if (wch != 64 && wch != 256) wch = 128;
-        }
+            const int v = w ? atoi(w) : 128;
+            return (v == 64 || v == 256) ? v : 128;
+        }();
         if (wch == 256 && (int)cfg.gridDim.x > PENCIL_NUM_SMS * 6) cfg.gridDim = dim3(PENCIL_NUM_SMS * 6);
 #define CSR_LAUNCH(A, W) \
     cudaLaunchKernelEx(&cfg, csr_stream_kernel<A, W>, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, status)
@@ -810,11 +816,10 @@ int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const
 }
 
 int csr_tile_nnz() {  // PENCIL_SPMV_TILE overrides the plan window (tuning knob)
-    static int t = -1;
-    if (t < 0) {
+    static const int t = [] {
         const char* e = getenv("PENCIL_SPMV_TILE");
-        t = e ? atoi(e) : SPMV_TILE_NNZ;
-        if (t < 32) t = SPMV_TILE_NNZ;
-    }
+        const int v = e ? atoi(e) : SPMV_TILE_NNZ;
+        return v < 32 ? SPMV_TILE_NNZ : v;
+    }();
     return t;
 }

@@ -25,6 +25,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -617,12 +619,28 @@ bool separable(const int* k, StencilArgs& a) {
 
 // PENCIL_STENCIL_SEP=0 disables the separable kernels (A/B measurement)
 bool sep_enabled() {
-    static int on = -1;
-    if (on < 0) {
+    static const bool on = [] {
         const char* e = getenv("PENCIL_STENCIL_SEP");
-        on = !(e && e[0] == '0');
-    }
+        return !(e && e[0] == '0');
+    }();
     return on;
+}
+
+unsigned* repair_flag_for(cudaStream_t st) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, unsigned*> flags;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    unsigned*& f = flags[{dev, st}];
+    if (!f) {
+        if (cudaMalloc(&f, sizeof(unsigned)) != cudaSuccess) {
+            f = nullptr;
+            return nullptr;
+        }
+        cudaMemset(f, 0, sizeof(unsigned));  // synchronous: before any launch can read it
+    }
+    return f;
 }
 
 bool ring_ok(int h, int w, const void* img, const void* out) {
@@ -673,15 +691,10 @@ int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, 
     } else if (scale >= 2) {
         a.magic = ~0ull / (unsigned long long)scale + 1;
     }
-    // per-device repair flag (zero between launches: the repair pass re-arms it)
-    static unsigned* flags[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!flags[dev & 63]) {
-        if (cudaMalloc(&flags[dev & 63], sizeof(unsigned)) != cudaSuccess) return (int)cudaErrorMemoryAllocation;
-        cudaMemset(flags[dev & 63], 0, sizeof(unsigned));
-    }
-    a.repair_flag = flags[dev & 63];
+    // repair flag per (device, stream): zero between launches (the repair pass re-arms it), and
+    // launches on different streams never see each other's flag
+    a.repair_flag = repair_flag_for(st);
+    if (!a.repair_flag) return (int)cudaErrorMemoryAllocation;
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
     if (!a.exact_only) {
         const bool sep = sep_enabled() && separable(k25, a);

@@ -89,3 +89,29 @@ def test_fault_status_is_per_thread(cuda):
     assert results["faulty"] == "E-INTERP"
     assert results["faulty_status"] != 0
     assert results["clean_status"] == 0 and results["clean_y"] == [2.0, 1.0]
+
+
+def test_conv_u8_repair_flag_is_per_stream(cuda):
+    """Two streams interleave conv5x5_u8 launches, one on an image holding non-byte values
+    (its launches need the exact repair pass), one on a byte image: the repair flag of one
+    stream's launch must never be consumed or re-armed by the other's."""
+    import torch
+    import paper_1302_5586_b200 as pb
+    h, w = 256, 512
+    good = synth.u8_i32(h * w, seed=31)
+    bad = good.copy()
+    bad[::997] = 5000
+    ref_good = oracle.conv5x5_u8(h, w, 256, good, synth.BINOMIAL)
+    ref_bad = oracle.conv5x5_u8(h, w, 256, bad, synth.BINOMIAL)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    dg, db = torch.from_numpy(good).cuda(), torch.from_numpy(bad).cuda()
+    outs_a = [torch.empty(h * w, dtype=torch.int32, device="cuda") for _ in range(8)]
+    outs_b = [torch.empty(h * w, dtype=torch.int32, device="cuda") for _ in range(8)]
+    torch.cuda.synchronize()
+    for i in range(8):
+        pb.device.conv5x5_u8(h, w, 256, db, synth.BINOMIAL, outs_a[i], stream=sa.cuda_stream)
+        pb.device.conv5x5_u8(h, w, 256, dg, synth.BINOMIAL, outs_b[i], stream=sb.cuda_stream)
+    torch.cuda.synchronize()
+    for i in range(8):
+        assert np.array_equal(outs_a[i].cpu().numpy().astype(np.int64), ref_bad), i
+        assert np.array_equal(outs_b[i].cpu().numpy().astype(np.int64), ref_good), i
