@@ -1037,8 +1037,6 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
     const size_t need = (2 * n_frame + n_la + n_part) * sizeof(HostV) + 64;
     if (J->scratch_bytes < need) {
         if (J->scratch) cudaFree(J->scratch);
-    if (J->d_rseq) cudaFree(J->d_rseq);
-    if (J->d_rpos) cudaFree(J->d_rpos);
         J->scratch = nullptr;
         J->scratch_bytes = 0;
         if (cudaMalloc(&J->scratch, need) != cudaSuccess) return fail(PENCIL_E_NOMEM, "E-NOMEM: JIT call buffers");

@@ -87,3 +87,29 @@ def test_step_budget_stops_runaway_loops(cuda):
     with pytest.raises(pb.PencilError) as e:
         u.call("spin", [0])
     assert e.value.code == "E-INTERP" and "budget" in str(e.value)
+
+
+def test_rand_sequence_survives_call_buffer_growth(cuda):
+    """set_rand_sequence, then calls that grow the unit's call buffers (a reduction over many
+    threads) before and between the rand() calls: the sequence must still be read intact, and
+    a second sequence replaces the first (regression: buffer growth used to free it)."""
+    import torch
+    from paper_1302_5586_b200 import Arg
+    src = ("void take(int n, int A[restrict const static n])\n{\n  int i;\n"
+           "  for (i = 0; i < n; i++) {\n    A[i] = rand();\n  }\n}\n"
+           "int big(int n, int B[restrict const static n])\n{\n  int i;\n  int s;\n  s = 0;\n"
+           "  #pragma pencil reduction (+: s)\n  for (i = 0; i < n; i++) {\n    s += B[i];\n  }\n  return s;\n}\n")
+    u = unit(src)
+    seq = list(range(1000, 1300))
+    u.set_rand_sequence(seq)
+    u.set_array("B", np.ones(1 << 20, np.int32))
+    assert u.call("big", [1 << 20, Arg.array("B")]) == 1 << 20
+    junk = torch.full((1 << 22,), -7, dtype=torch.int64, device="cuda")  # reuse freed memory, if any
+    torch.cuda.synchronize()
+    u.set_array("A", np.zeros(300, np.int32))
+    u.call("take", [300, Arg.array("A")])
+    assert u.get_array("A")[1].tolist() == seq
+    u.set_rand_sequence([5, 6, 7])
+    u.call("take", [3, Arg.array("A")])
+    assert u.get_array("A")[1][:3].tolist() == [5, 6, 7]
+    del junk
