@@ -14,7 +14,9 @@
 // 16384^2: int32 storage 0.413 -> 0.374 ms (88% of HBM), packed bytes 0.367 -> 0.258 ms.
 //
 // Measured and dropped: two output rows per step (6-row window, four FFMA2 add chains per warp
-// instead of two): 0.485 ms vs 0.475 — the f32 kernel's `wait` stalls are not chain latency.
+// instead of two): 0.485 ms vs 0.475 — the f32 kernel's `wait` stalls are not chain latency;
+// and a push form (each entering row added into the 5 output rows it feeds, same per-sum
+// order, 80 instead of 104 registers, 6 CTAs/SM): 0.520 ms — 2.4x the MOVs.
 //
 // Policies (same arithmetic as the fallbacks, so the parity claims carry over unchanged):
 //   F32  conv5x5_f32: interior only; acc = acc + k*img per tap in source order with the product
