@@ -17,6 +17,9 @@
 // instead of two): 0.485 ms vs 0.475 — the f32 kernel's `wait` stalls are not chain latency;
 // and a push form (each entering row added into the 5 output rows it feeds, same per-sum
 // order, 80 instead of 104 registers, 6 CTAs/SM): 0.520 ms — 2.4x the MOVs.
+// And a narrow f32 sweep (a lane owns one pixel pair of a 64-column strip: 5x5 window, 76
+// registers, 6 CTAs/SM): 0.542 ms; 7 / 8 CTAs/SM 0.562 / 0.609 ms — more warps do not help,
+// the extra per-pixel ring/loop instructions cost more than the occupancy buys.
 //
 // Policies (same arithmetic as the fallbacks, so the parity claims carry over unchanged):
 //   F32  conv5x5_f32: interior only; acc = acc + k*img per tap in source order with the product
