@@ -1,5 +1,8 @@
 // Measurement probes (not PENCIL kernels): random-gather rate from a table (the x[col[k]]
 // access of SpMV), a float4 copy (HBM roofline check of our own code) and an L2 flush.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -115,10 +118,27 @@ __global__ void micro_fill_kernel(long long n4, float4* __restrict__ d, float v)
         d[i] = make_float4(v, v, v, v);
 }
 
+// Drops the buffer's lines from L2 without writing them back (discard.global.L2, 128 B each).
+__global__ void micro_discard_kernel(long long nlines, char* __restrict__ d) {
+    const long long nthr = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nlines; i += nthr)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(d + i * 128) : "memory");
+}
+
+// L2 flush between timed steps: write the 256 MiB buffer (evicts whatever the last step left),
+// then discard its lines, so the next step starts on an empty, CLEAN L2 (as ncu's cache control
+// does).  Without the discard ~126 MB of the fill's dirty lines are written back while the next
+// step runs (gemv 8192^2: 49.8 us under the fill alone vs 43 us for the kernel itself);
+// PENCIL_L2_FLUSH=dirty keeps the fill-only flush for comparison.
 int launch_micro_l2_flush(cudaStream_t st, long long n, float* buf) {
     static float v = 0.f;
+    static const bool dirty = [] {
+        const char* e = getenv("PENCIL_L2_FLUSH");
+        return e && strcmp(e, "dirty") == 0;
+    }();
     v += 1.f;
     micro_fill_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>(n >> 2, reinterpret_cast<float4*>(buf), v);
+    if (!dirty) micro_discard_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>(n * 4 / 128, reinterpret_cast<char*>(buf));
     return (int)cudaGetLastError();
 }
 
