@@ -369,6 +369,11 @@ __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_v
 // inside a window writes y and the next batch — prefetched — continues in the same window).
 // The batch-aligned kernel restarts its windows at every batch, so each 32-row batch (~512
 // non-zeros here) pays a partial first and last window.
+// Measured and dropped (2^24 rows, A/B on one box): drawing the next tile's ticket one tile ahead
+// (settled after the first window, two extra registers): 1.288 vs 1.239 ms; and, as a bound on
+// the fold's cost, the same kernel with the fold replaced by one shared load per batch (wrong
+// results): 1.292 ms — neither the tile-start round trips nor the fold is what separates this
+// kernel from the 1.01 ms row-free gather stream; both edits cost the gather loop its schedule.
 // DIST: fused SpMV -> all-gather (put_row); the warp fences its peer stores at system scope
 // before it retires, so the barrier that follows the launch publishes them.
 template <bool ASSOC, bool DIST = false>
