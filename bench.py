@@ -191,6 +191,10 @@ def bench_spmv(args, torch, pb, rank, world, dist):
         ms = run_steps(torch, step, args.steps, args.warmup, flush, dist)
         kernel_ms = statistics.mean(ms)
         launches = args.steps * (4 if mode == "fused" else 3)  # + the symmetric-memory barrier
+        e2e = None
+        if not args.no_e2e:
+            sh.total_nnz = nnz
+            e2e = e2e_spmv_dist(args, torch, pb, sh, x, dist)
     algo = spmv_bytes(nrows, nrows, nnz)
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
            "ceiling_ms": ceil_ms if world == 1 else None,
@@ -200,6 +204,8 @@ def bench_spmv(args, torch, pb, rank, world, dist):
                       "l2": "L2 flushed between steps outside the per-step events (256 MiB fill, then its lines discarded: the step starts on a clean, empty L2); inputs 2.35 GB > L2"}}
     if world > 1:
         res["config"]["exchange"] = exchange
+        if e2e:
+            res["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_e2e:
         res["e2e"] = e2e_spmv(args, torch, pb, rowptr, col, val, x)
     return res
@@ -225,6 +231,49 @@ def e2e_spmv(args, torch, pb, rowptr, col, val, x):
     pb.load().pencil_last_transfer_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
     return {"value": algo / t / 1e9, "unit": "GB/s", "ms_per_call": t * 1e3, "h2d_bytes_per_step": h2d.value,
             "d2h_bytes_per_step": d2h.value, "api": "spmv_vec (drop-in C ABI, pinned host arrays)"}
+
+
+def e2e_spmv_dist(args, torch, pb, sh, x, dist):
+    """N>1 end to end: each rank uploads its row block and its slice of x from pinned host memory
+    over its own host link, the x slices are all-gathered (NVLink), the plan is built and the
+    rank's rows multiplied, and its y rows come back to the host — the drop-in call's work,
+    sharded.  Device-timed per rank (events around the whole call), max over ranks."""
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    hrp, hcol, hval, hx = pin(sh.rowptr), pin(sh.col), pin(sh.val), pin(x[sh.r0:sh.r1])
+    hy = torch.empty(sh.nrows, dtype=torch.float32).pin_memory()
+    drp, dcol, dval = (torch.empty(a.numel(), dtype=a.dtype, device="cuda") for a in (hrp, hcol, hval))
+    xpad = torch.zeros(sh.max_rows, device="cuda")
+    xg = torch.empty(sh.ncols_padded, device="cuda")
+    y = torch.empty(sh.nrows, device="cuda")
+    plans = []
+
+    def call():
+        drp.copy_(hrp, non_blocking=True)
+        dcol.copy_(hcol, non_blocking=True)
+        dval.copy_(hval, non_blocking=True)
+        xpad[: sh.nrows].copy_(hx, non_blocking=True)
+        plan = pb.device.CsrPlan(sh.nrows, sh.ncols_padded, sh.nnz, drp, mode=1)  # per call, as the drop-in
+        plans.append(plan)
+        sh.allgather_x(xpad, xg)
+        plan.spmv(drp, dcol, dval, xg, y)
+        hy.copy_(y, non_blocking=True)
+
+    ms = statistics.mean(run_steps(torch, call, max(2, min(args.steps, 5)), 2, lambda: None, dist))
+    torch.cuda.synchronize()
+    for p in plans:
+        p.close()
+    h2d = 4 * ((sh.nrows + 1) + 2 * sh.nnz + sh.nrows)
+    t = torch.tensor([ms, float(h2d), 4.0 * sh.nrows], dtype=torch.float64, device="cuda")
+    tmax = t[:1].clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    ms = float(tmax.item())
+    algo = spmv_bytes(len(x), len(x), int(sh.total_nnz))
+    return {"value": algo / ms / 1e6, "unit": "GB/s", "ms_per_call": ms, "h2d_bytes_per_step": int(t[1].item()),
+            "d2h_bytes_per_step": int(t[2].item()),
+            "api": "row-sharded spmv_vec: per rank pinned-host row block + x slice -> its GPU, %s all-gather "
+                   "of x, plan + SpMV, y rows -> host (device events around the call, max over ranks)"
+                   % dist.get_backend()}
 
 
 def suite(args, torch, pb, hbm):
