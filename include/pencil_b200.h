@@ -86,6 +86,18 @@ int pencil_conv5x5_u8_bytes_dev(pencil_stream_t s, int h, int w, int scale, cons
                                 const int* k_host, uint8_t* out);
 int pencil_conv5x5_f32_dev(pencil_stream_t s, int h, int w, const float* img, const float* k_host,
                            float* out);
+/* Band-sharded 5x5 stencils (multi-GPU row bands; the halo exchange is fused into the sweep):
+ * the band's own h rows at img / out; top[0], top[1] = rows -2, -1 and bot[0], bot[1] = rows h,
+ * h + 1 as device pointers — the neighbour ranks' edge rows through their peer mappings (NVLink),
+ * or the band's own first / last row repeated at the image's top / bottom (clamp-to-edge).  The
+ * f32 form writes band rows [out_lo, out_hi) (the image interior).  Needs w % 4 == 0 and 16-byte
+ * aligned rows (else PENCIL_E_ARG).  Results are the rows of the whole-image call, bit for bit.
+ * Replaces the exchange + compute pair of the row-band path (conv5x5 row). */
+int pencil_conv5x5_u8_band_dev(pencil_stream_t s, int h, int w, int scale, const int* img,
+                               const int* const* top, const int* const* bot, const int* k_host, int* out);
+int pencil_conv5x5_f32_band_dev(pencil_stream_t s, int h, int w, int out_lo, int out_hi, const float* img,
+                                const float* const* top, const float* const* bot, const float* k_host,
+                                float* out);
 int pencil_gemm_dev(pencil_stream_t s, int m, int n, int k, float alpha, float beta, const float* A,
                     const float* B, float* C);
 

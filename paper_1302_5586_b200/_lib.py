@@ -43,6 +43,8 @@ SIGNATURES = {
     "pencil_conv5x5_u8_dev": (c_int, [P, c_int, c_int, c_int, P, P, P]),
     "pencil_conv5x5_u8_bytes_dev": (c_int, [P, c_int, c_int, c_int, P, P, P]),
     "pencil_conv5x5_f32_dev": (c_int, [P, c_int, c_int, P, P, P]),
+    "pencil_conv5x5_u8_band_dev": (c_int, [P, c_int, c_int, c_int, P, P, P, P, P]),
+    "pencil_conv5x5_f32_band_dev": (c_int, [P, c_int, c_int, c_int, c_int, P, P, P, P, P]),
     "pencil_gemm_dev": (c_int, [P, c_int, c_int, c_int, c_float, c_float, P, P, P]),
     "pencil_csr_plan_create": (c_int, [P, c_int, c_int, c_int, P, c_int, ctypes.POINTER(c_void_p)]),
     "pencil_csr_plan_destroy": (c_int, [P]),

@@ -249,6 +249,17 @@ __device__ __forceinline__ unsigned pixel_exact(const int* __restrict__ img, int
     return sat_div(acc, a);
 }
 
+// Row band of a band-sharded image (multi-GPU row bands, halo rows read in place): the two rows
+// above the band and the two below, as row pointers — the neighbour ranks' edge rows through
+// their NVLink peer mappings, or the band's own edge row repeated at the image's top / bottom
+// (clamp-to-edge).  out_lo / out_hi: the band-relative output rows (f32: the image interior).
+template <typename T>
+struct BandSrc {
+    const T* top[2];  // rows -2, -1
+    const T* bot[2];  // rows h, h + 1
+    int out_lo, out_hi;
+};
+
 // Sweep state advanced by one row per step: `src` points at the lane's columns of the next row
 // to enter the ring (rows past the image bottom clamp to `src_last` for U8), `dst` at the
 // lane's columns of the output row.
@@ -260,11 +271,12 @@ struct Sweep {
     long long w;
 };
 
-template <bool U8, int S, bool POW2, bool SEP>
+template <bool U8, int S, bool POW2, bool SEP, bool BAND = false>
 __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int r_end, const RingLane& L,
                                              typename Pol<U8>::T (*ring)[S_ROWE], u64 (&W)[5][7],
                                              Sweep<typename Pol<U8>::T>& sw, unsigned& orv,
-                                             const typename Pol<U8>::A& a) {
+                                             const typename Pol<U8>::A& a,
+                                             const BandSrc<typename Pol<U8>::T>* bs = nullptr, int h = 0) {
     typedef typename Pol<U8>::T T;
     // the ring holds rows i+2 .. i+2+S_RING-1 in flight; the oldest (row i+2) must have landed
     cp_wait<S_RING - 1>();
@@ -278,7 +290,12 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
     __syncwarp();
     if (i + 2 + S_RING < r_end) {
         const T* src = sw.src;
-        if (U8 && src > sw.src_last) src = sw.src_last;  // clamp-to-edge rows below the image
+        if constexpr (BAND) {  // rows h, h + 1: the lower halo
+            const int r = i + 2 + S_RING;
+            if (r >= h) src = (r == h ? bs->bot[0] : bs->bot[1]) + c;
+        } else if (U8 && src > sw.src_last) {
+            src = sw.src_last;  // clamp-to-edge rows below the image
+        }
         ring_issue<T>(src, L, lane, slot);
     }
     cp_commit();
@@ -420,6 +437,88 @@ __global__ void u8_repair_kernel(int h, int w, const int* __restrict__ img, int*
         out[p] = (int)pixel_exact<true>(img, h, w, (int)(p / w), (int)(p % w), a);
 }
 __global__ void u8_rearm_kernel(unsigned* flag) { *flag = 0u; }
+
+// ---------------------------------------------------------------- band-sharded sweep
+// One rank's row band of a band-sharded image with the halo exchange fused away: the rows above
+// and below the band are read where they live (BandSrc: the neighbours' edge rows through NVLink
+// peer mappings, cp.async straight into the ring), so a multi-GPU stencil step is one launch per
+// rank and no halo copy.  Same sweep, arithmetic and policies as stencil_ring_kernel (the output
+// is bit-identical to the single-GPU image's rows); h = the band's own rows.
+template <bool U8, bool POW2, bool SEP = false>
+__global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? STENCIL_U8_MINB : STENCIL_F32_MINB)) stencil_band_kernel(
+    int h, int w, const typename Pol<U8>::T* __restrict__ img, typename Pol<U8>::T* __restrict__ out,
+    typename Pol<U8>::A a, BandSrc<typename Pol<U8>::T> bs) {
+    typedef typename Pol<U8>::T T;
+    __shared__ __align__(16) T ring_all[S_WARPS][S_RING][S_ROWE];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = (blockIdx.x * S_WARPS + warp) * 128;
+    if (c0 >= w) return;
+    const int c = c0 + 4 * lane;
+    const int i0 = bs.out_lo + blockIdx.y * S_BAND;
+    const int i1 = min(bs.out_hi, i0 + S_BAND);
+    if (i0 >= i1) return;
+    const int r_end = i1 + 2;
+    const RingLane L = ring_lane(w, c0, lane);
+    T(*ring)[S_ROWE] = ring_all[warp];
+    auto row_src = [&](int r) {
+        return (r < 0 ? (r == -2 ? bs.top[0] : bs.top[1]) : (r >= h ? (r == h ? bs.bot[0] : bs.bot[1]) : img + (long long)r * w)) + c;
+    };
+#pragma unroll
+    for (int d = 0; d < S_RING; d++) {  // prologue: rows i0-2 .. i0+5 in flight
+        if (i0 - 2 + d < r_end) ring_issue<T>(row_src(i0 - 2 + d), L, lane, ring[(i0 - 2 + d + S_RING) % S_RING]);
+        cp_commit();
+    }
+    u64 W[5][7];
+    unsigned orv = 0;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        cp_wait<S_RING - 1>();
+        __syncwarp();
+        T* slot = ring[(i0 - 2 + d + S_RING) % S_RING];
+        {
+            u64 P[7];
+            ring_read<U8>(slot, w, c0, lane, a, P, orv);
+            enter_row<SEP>(P, W[d], a);
+        }
+        __syncwarp();
+        if (i0 - 2 + d + S_RING < r_end) ring_issue<T>(row_src(i0 - 2 + d + S_RING), L, lane, slot);
+        cp_commit();
+    }
+    Sweep<T> sw;
+    sw.w = w;
+    sw.src_last = nullptr;
+    sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;
+    sw.dst = out + (long long)i0 * w + c;
+    for (int i = i0; i < i1; i += 5) {
+        stencil_step<U8, 4, POW2, SEP, true>(w, i, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 1 < i1) stencil_step<U8, 0, POW2, SEP, true>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 2 < i1) stencil_step<U8, 1, POW2, SEP, true>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 3 < i1) stencil_step<U8, 2, POW2, SEP, true>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 4 < i1) stencil_step<U8, 3, POW2, SEP, true>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+    }
+    cp_wait<0>();
+    if (U8 && __any_sync(0xffffffffu, (orv & ~255u) != 0) && lane == 0) atomicOr(a.repair_flag, 1u);
+}
+
+// the exact int64 repair pass of a band (rows outside it through BandSrc)
+__global__ void u8_band_repair_kernel(int h, int w, const int* __restrict__ img, int* __restrict__ out,
+                                      StencilArgs a, BandSrc<int> bs) {
+    if (!a.exact_only && *(volatile unsigned*)a.repair_flag == 0) return;
+    const long long n = (long long)h * w;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(p / w), j = (int)(p % w);
+        long long acc = 0;
+#pragma unroll 1
+        for (int di = 0; di < 5; di++) {
+            const int r = i + di - 2;
+            const int* row = r < 0 ? (r == -2 ? bs.top[0] : bs.top[1]) : (r >= h ? (r == h ? bs.bot[0] : bs.bot[1]) : img + (long long)r * w);
+#pragma unroll 1
+            for (int dj = 0; dj < 5; dj++) acc += a.ki[di * 5 + dj] * (long long)row[clampi(j + dj - 2, 0, w - 1)];
+        }
+        out[p] = (int)sat_div(acc, a);
+    }
+}
 
 // ---------------------------------------------------------------- packed 8-bit images
 // conv5x5_u8 semantics on 1-byte pixels (pencil_conv5x5_u8_bytes_dev): the same sweep with a
@@ -671,10 +770,9 @@ int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const fl
     return (int)cudaGetLastError();
 }
 
-int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, const int* k25, int* out) {
-    if (h <= 0 || w <= 0) return 0;
-    if (!ring_ok(h, w, img, out)) return launch_conv5x5_u8_reg(st, h, w, scale, img, k25, out);
-    StencilArgs a = {};
+namespace {
+// conv5x5_u8 launch arguments: taps, requantisation constants, the stream's repair flag
+bool u8_args(cudaStream_t st, int scale, const int* k25, StencilArgs& a) {
     bool small = true;
     for (int t = 0; t < 25; t++) {
         a.kf[t] = (float)k25[t];
@@ -699,7 +797,15 @@ int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, 
     // repair flag per (device, stream): zero between launches (the repair pass re-arms it), and
     // launches on different streams never see each other's flag
     a.repair_flag = repair_flag_for(st);
-    if (!a.repair_flag) return (int)cudaErrorMemoryAllocation;
+    return a.repair_flag != nullptr;
+}
+}  // namespace
+
+int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, const int* k25, int* out) {
+    if (h <= 0 || w <= 0) return 0;
+    if (!ring_ok(h, w, img, out)) return launch_conv5x5_u8_reg(st, h, w, scale, img, k25, out);
+    StencilArgs a = {};
+    if (!u8_args(st, scale, k25, a)) return (int)cudaErrorMemoryAllocation;
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
     if (!a.exact_only) {
         const bool sep = sep_enabled() && separable(k25, a);
@@ -711,6 +817,51 @@ int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, 
     const long long n = (long long)h * w, blocks = (n + 255) / 256;
     u8_repair_kernel<<<(int)(blocks < PENCIL_NUM_SMS * 8 ? blocks : PENCIL_NUM_SMS * 8), 256, 0, st>>>(h, w, img, out, a);
     u8_rearm_kernel<<<1, 1, 0, st>>>(a.repair_flag);
+    return (int)cudaGetLastError();
+}
+
+// Band-sharded launches (the fused halo exchange): `top` / `bot` hold the row pointers of rows
+// -2, -1 and h, h + 1 of the band (see BandSrc).  Need w % 4 == 0 and 16-byte aligned rows.
+static bool band_ok(int h, int w, const void* img, const void* out, const void* const* top, const void* const* bot) {
+    bool ok = ring_ok(h, w, img, out);
+    for (int t = 0; t < 2; t++) ok = ok && top[t] && bot[t] && (uintptr_t)top[t] % 16 == 0 && (uintptr_t)bot[t] % 16 == 0;
+    return ok;
+}
+
+int launch_conv5x5_u8_band(cudaStream_t st, int h, int w, int scale, const int* img, const int* const* top,
+                           const int* const* bot, const int* k25, int* out) {
+    if (h <= 0 || w <= 0) return 0;
+    if (!band_ok(h, w, img, out, (const void* const*)top, (const void* const*)bot)) return (int)cudaErrorInvalidValue;
+    StencilArgs a = {};
+    if (!u8_args(st, scale, k25, a)) return (int)cudaErrorMemoryAllocation;
+    const BandSrc<int> bs = {{top[0], top[1]}, {bot[0], bot[1]}, 0, h};
+    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
+    if (!a.exact_only) {
+        const bool sep = sep_enabled() && separable(k25, a);
+        if (sep && a.shift >= 0) stencil_band_kernel<true, true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+        else if (sep) stencil_band_kernel<true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+        else if (a.shift >= 0) stencil_band_kernel<true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+        else stencil_band_kernel<true, false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+    }
+    const long long n = (long long)h * w, blocks = (n + 255) / 256;
+    u8_band_repair_kernel<<<(int)(blocks < PENCIL_NUM_SMS * 8 ? blocks : PENCIL_NUM_SMS * 8), 256, 0, st>>>(h, w, img, out, a, bs);
+    u8_rearm_kernel<<<1, 1, 0, st>>>(a.repair_flag);
+    return (int)cudaGetLastError();
+}
+
+int launch_conv5x5_f32_band(cudaStream_t st, int h, int w, int out_lo, int out_hi, const float* img,
+                            const float* const* top, const float* const* bot, const float* k25, float* out) {
+    if (h <= 0 || w < 5 || out_lo >= out_hi) return 0;
+    if (out_lo < 0 || out_hi > h) return (int)cudaErrorInvalidValue;
+    if (!band_ok(h, w, img, out, (const void* const*)top, (const void* const*)bot)) return (int)cudaErrorInvalidValue;
+    StencilArgsF32 a = {};
+    for (int t = 0; t < 25; t++) a.kf[t] = k25[t];
+    a.negz = pack2(-0.0f);
+    a.one = pack2(1.0f);
+    a.negmag = pack2(-8388608.0f);
+    const BandSrc<float> bs = {{top[0], top[1]}, {bot[0], bot[1]}, out_lo, out_hi};
+    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (out_hi - out_lo + S_BAND - 1) / S_BAND);
+    stencil_band_kernel<false, false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
     return (int)cudaGetLastError();
 }
 

@@ -50,6 +50,11 @@ int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, 
                       int* out);
 int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsigned char* img,
                             const int* k25, unsigned char* out);
+// band-sharded sweeps (k_stencil.cu): rows -2, -1 / h, h + 1 of the band through top / bot
+int launch_conv5x5_u8_band(cudaStream_t st, int h, int w, int scale, const int* img, const int* const* top,
+                           const int* const* bot, const int* k25, int* out);
+int launch_conv5x5_f32_band(cudaStream_t st, int h, int w, int out_lo, int out_hi, const float* img,
+                            const float* const* top, const float* const* bot, const float* k25, float* out);
 
 // k_gemm.cu
 int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, const float* A,

@@ -679,6 +679,29 @@ int pencil_conv5x5_f32_dev(pencil_stream_t s, int h, int w, const float* img, co
     DEV_RET(launch_conv5x5_f32(st, h, w, img, k_host, out));
 }
 
+int pencil_conv5x5_u8_band_dev(pencil_stream_t s, int h, int w, int scale, const int* img, const int* const* top,
+                               const int* const* bot, const int* k_host, int* out) {
+    if (h < 0 || w < 0) return fail(PENCIL_E_ARG, "negative extent");
+    if (!top || !bot || !k_host) return fail(PENCIL_E_ARG, "null argument");
+    if (scale == 0 && h > 0 && w > 0) return fail(PENCIL_E_INTERP, "division by zero");
+    DEV_PROLOGUE;
+    const int e = launch_conv5x5_u8_band(st, h, w, scale, img, top, bot, k_host, out);
+    if (e == (int)cudaErrorInvalidValue)
+        return fail(PENCIL_E_ARG, "band rows must be 16-byte aligned with w %% 4 == 0 (w=%d)", w);
+    DEV_RET(e);
+}
+
+int pencil_conv5x5_f32_band_dev(pencil_stream_t s, int h, int w, int out_lo, int out_hi, const float* img,
+                                const float* const* top, const float* const* bot, const float* k_host, float* out) {
+    if (h < 0 || w < 0) return fail(PENCIL_E_ARG, "negative extent");
+    if (!top || !bot || !k_host) return fail(PENCIL_E_ARG, "null argument");
+    DEV_PROLOGUE;
+    const int e = launch_conv5x5_f32_band(st, h, w, out_lo, out_hi, img, top, bot, k_host, out);
+    if (e == (int)cudaErrorInvalidValue)
+        return fail(PENCIL_E_ARG, "band rows must be 16-byte aligned with w %% 4 == 0 and 0 <= out_lo, out_hi <= h");
+    DEV_RET(e);
+}
+
 int pencil_gemm_dev(pencil_stream_t s, int m, int n, int k, float alpha, float beta, const float* A,
                     const float* B, float* C) {
     if (m < 0 || n < 0 || k < 0) return fail(PENCIL_E_ARG, "negative extent");

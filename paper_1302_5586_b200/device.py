@@ -65,6 +65,26 @@ def conv5x5_u8_bytes(h, w, scale, img, k, out, stream=None):
                                                  kk.ctypes.data, out.data_ptr()))
 
 
+def _ptr2(ptrs):
+    return (ctypes.c_void_p * 2)(*[int(p) for p in ptrs])
+
+
+def conv5x5_u8_band(h, w, scale, img, top, bot, k, out, stream=None):
+    """One rank's row band (h rows at img / out) with its halo rows read in place: top = device
+    addresses of rows -2, -1, bot = of rows h, h + 1 (peer mappings of the neighbours' edge rows,
+    or the band's own edge row at the image's top / bottom) — pencil_conv5x5_u8_band_dev."""
+    kk = _taps(k, np.int32)
+    _chk(_lib.load().pencil_conv5x5_u8_band_dev(_stream(stream), h, w, scale, img.data_ptr(), _ptr2(top),
+                                                _ptr2(bot), kk.ctypes.data, out.data_ptr()))
+
+
+def conv5x5_f32_band(h, w, out_lo, out_hi, img, top, bot, k, out, stream=None):
+    """As conv5x5_u8_band for the fp32 stencil; writes band rows [out_lo, out_hi)."""
+    kk = _taps(k, np.float32)
+    _chk(_lib.load().pencil_conv5x5_f32_band_dev(_stream(stream), h, w, out_lo, out_hi, img.data_ptr(),
+                                                 _ptr2(top), _ptr2(bot), kk.ctypes.data, out.data_ptr()))
+
+
 def conv5x5_f32(h, w, img, k, out, stream=None):
     kk = _taps(k, np.float32)
     _chk(_lib.load().pencil_conv5x5_f32_dev(_stream(stream), h, w, img.data_ptr(), kk.ctypes.data,

@@ -165,6 +165,72 @@ class BandShardedImage:
         return ext
 
 
+def band_halo_rows(band_ptrs, rows, rank, w, esize):
+    """Device addresses of rows -2, -1 (top) and h, h + 1 (bot) of `rank`'s band, h = rows[rank]:
+    band_ptrs[q] is the address of rank q's band (rows[q] rows of w elements of esize bytes).  The
+    neighbours' edge rows, or the band's own first / last row at the image's top / bottom
+    (clamp-to-edge, the conv5x5_u8 edge rule; the fp32 stencil never reads them)."""
+    world = len(rows)
+    if world > 1 and min(rows) < 2:
+        raise ValueError("every band needs >= 2 rows for a 2-row halo")
+    row = lambda q, r: int(band_ptrs[q]) + int(r) * w * esize  # noqa: E731
+    h = int(rows[rank])
+    top = (row(rank - 1, rows[rank - 1] - 2), row(rank - 1, rows[rank - 1] - 1)) if rank > 0 else (row(rank, 0),) * 2
+    bot = (row(rank + 1, 0), row(rank + 1, 1)) if rank < world - 1 else (row(rank, h - 1),) * 2
+    return top, bot
+
+
+def band_interior(h, b0, b1):
+    """Band-relative output rows [lo, hi) of the fp32 stencil (image interior rows 2 .. h-3) for
+    the band of global rows [b0, b1)."""
+    lo = max(0, 2 - b0)
+    return lo, max(lo, min(b1, h - 2) - b0)
+
+
+class FusedBandStencil:
+    """Band-sharded 5x5 stencil step with the halo exchange fused into the sweep: every rank's
+    band lives in torch symmetric memory and the kernel's ring loader reads the two rows above
+    and below the band straight out of the neighbours' buffers over NVLink (cp.async from their
+    peer mappings: pencil_conv5x5_*_band_dev), so a step is one launch per rank with no halo
+    copy.  A symmetric-memory barrier orders it after every rank's band writes, and one after it
+    lets the caller overwrite its band (the next iteration's input).  The unfused equivalent is
+    BandShardedImage.exchange_halos + the stencil on a halo-extended buffer."""
+
+    def __init__(self, h, w, rank, world, dtype, device, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        b = shard_bands(h, world)
+        self.h, self.w, self.rank, self.world = h, w, rank, world
+        self.b0, self.b1 = int(b[rank]), int(b[rank + 1])
+        self.rows = [int(b[q + 1] - b[q]) for q in range(world)]
+        self.nb = self.rows[rank]
+        self.buf = symm.empty(max(self.rows) * w, dtype=dtype, device=device)
+        self.hdl = symm.rendezvous(self.buf, group or dist.group.WORLD)
+        base = int(self.hdl.buffer_ptrs[self.hdl.rank])
+        offset = self.buf.data_ptr() - base
+        ptrs = [int(p) + offset for p in self.hdl.buffer_ptrs]
+        self.top, self.bot = band_halo_rows(ptrs, self.rows, rank, w, self.buf.element_size())
+        self.out_lo, self.out_hi = band_interior(h, self.b0, self.b1)
+
+    def band(self):
+        """This rank's band (nb x w, flattened): write the input rows here."""
+        return self.buf[: self.nb * self.w]
+
+    def step_u8(self, scale, k, out):
+        from . import device
+        self.hdl.barrier(channel=0)
+        device.conv5x5_u8_band(self.nb, self.w, scale, self.buf, self.top, self.bot, k, out)
+        self.hdl.barrier(channel=0)
+        return out
+
+    def step_f32(self, k, out):
+        from . import device
+        self.hdl.barrier(channel=0)
+        device.conv5x5_f32_band(self.nb, self.w, self.out_lo, self.out_hi, self.buf, self.top, self.bot, k, out)
+        self.hdl.barrier(channel=0)
+        return out
+
+
 # ---------------------------------------------------------------- dense BLAS (SURVEY §8e rows)
 def shard_range(n, world, rank, align=4):
     """Contiguous [lo, hi) of n elements for `rank`, interior boundaries multiples of `align`

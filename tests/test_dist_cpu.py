@@ -225,3 +225,48 @@ def test_dense_shards_gemv_gemvt_dot_axpy_gemm_gloo(world):
 def test_fused_spmv_allgather_targets_gloo(world, multicast):
     """Three iterations (x -> Ax -> A^2x -> A^3x) through the fused step's store targets."""
     assert _run(_fused_worker_mc if multicast else _fused_worker, world)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_fused_band_halo_addresses_resolve_to_neighbour_rows(world):
+    """The fused halo exchange (FusedBandStencil): the row addresses band_halo_rows gives each
+    rank for fake per-rank band buffers, resolved back to (rank, row), rebuild the halo-extended
+    band; the oracle stencils on it equal the whole image's rows bit for bit (u8 clamp-to-edge at
+    the image edges through the repeated own rows; f32 interior rows via band_interior)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    from paper_1302_5586_b200 import synth
+    from paper_1302_5586_b200.dist import band_halo_rows, band_interior, shard_bands
+    h, w = 53, 24
+    img = synth.u8_i32(h * w, seed=9).reshape(h, w)
+    imgf = synth.f32(h * w, seed=9).reshape(h, w)
+    b = shard_bands(h, world)
+    rows = [int(b[q + 1] - b[q]) for q in range(world)]
+    esize, bases = 4, [(q + 1) << 32 for q in range(world)]
+
+    def resolve(addr):
+        q = next(q for q in range(world) if bases[q] <= addr < bases[q] + rows[q] * w * esize)
+        off = addr - bases[q]
+        assert off % (w * esize) == 0
+        return q, off // (w * esize)
+
+    ref_u8 = oracle.conv5x5_u8(h, w, 256, img.reshape(-1).copy(), synth.BINOMIAL).reshape(h, w)
+    ref_f = oracle.conv5x5_f32_f32(h, w, imgf.reshape(-1).copy(), (synth.BINOMIAL / 256.0).astype(np.float32),
+                                   np.zeros(h * w, np.float32)).reshape(h, w)
+    for rank in range(world):
+        top, bot = band_halo_rows(bases, rows, rank, w, esize)
+        b0, b1 = int(b[rank]), int(b[rank + 1])
+        pick = lambda a, qr: a[int(b[qr[0]]) + qr[1]]  # noqa: E731
+        for src, ref, f32 in ((img, ref_u8, False), (imgf, ref_f, True)):
+            ext = np.concatenate([np.stack([pick(src, resolve(t)) for t in top]), src[b0:b1],
+                                  np.stack([pick(src, resolve(t)) for t in bot])])
+            n = ext.shape[0]
+            if not f32:
+                out = oracle.conv5x5_u8(n, w, 256, ext.reshape(-1).copy(), synth.BINOMIAL).reshape(n, w)[2:-2]
+                assert np.array_equal(out, ref[b0:b1])
+            else:
+                out = oracle.conv5x5_f32_f32(n, w, ext.reshape(-1).copy(), (synth.BINOMIAL / 256.0).astype(np.float32),
+                                             np.zeros(n * w, np.float32)).reshape(n, w)[2:-2]
+                lo, hi = band_interior(h, b0, b1)
+                assert np.array_equal(out[lo:hi].view(np.uint32), ref[b0 + lo:b0 + hi].view(np.uint32))

@@ -128,3 +128,86 @@ def test_fused_spmv_allgather_world1(nccl):
     assert torch.equal(y.view(torch.int32), ref.view(torch.int32))
     assert torch.equal(out[: sh.nrows].view(torch.int32), ref.view(torch.int32))
     print("multicast" if fz.mc else "peer stores", len(fz.peers))
+
+
+@pytest.mark.parametrize("h,w,world", [(200, 256, 3), (67, 132, 4), (41, 512, 2)])
+@pytest.mark.parametrize("case", ["binomial", "sharpen", "scale3", "nonbyte", "bigtaps", "f32"])
+def test_band_kernels_read_halos_in_place(cuda, h, w, world, case):
+    """The band-sharded sweep (pencil_conv5x5_*_band_dev) on `world` separately allocated bands,
+    each reading its halo rows straight out of its neighbours' buffers (the addresses
+    band_halo_rows gives; peer mappings on a multi-GPU box): the bands' rows equal the
+    whole-image call bit for bit — separable and 25-tap kernels, non-power-of-two scale, the exact
+    repair pass (a non-byte pixel; taps too large for the fp32 path) and the fp32 interior."""
+    import torch
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200 import synth
+    from paper_1302_5586_b200.dist import band_halo_rows, band_interior, shard_bands
+    b = shard_bands(h, world)
+    rows = [int(b[q + 1] - b[q]) for q in range(world)]
+    f32 = case == "f32"
+    if f32:
+        img = torch.from_numpy(synth.f32(h * w, seed=3)).cuda()
+        k = (synth.BINOMIAL / 256.0).astype(np.float32)
+        whole = torch.zeros(h * w, device="cuda")
+        pb.device.conv5x5_f32(h, w, img, k, whole)
+    else:
+        img = torch.from_numpy(synth.u8_i32(h * w, seed=3)).cuda()
+        k, scale = {"binomial": (synth.BINOMIAL, 256), "sharpen": (synth.SHARPEN, 1), "scale3": (synth.SHARPEN, 3),
+                    "nonbyte": (synth.BINOMIAL, 256), "bigtaps": (synth.BINOMIAL * 1000, 256000)}[case]
+        if case == "nonbyte":
+            img[h // 2 * w + 7] = 300
+            img[(rows[0] - 1) * w + 5] = -4  # in a halo row of rank 1
+        whole = torch.empty(h * w, dtype=torch.int32, device="cuda")
+        pb.device.conv5x5_u8(h, w, scale, img, k, whole)
+    bands = [img[int(b[q]) * w:int(b[q + 1]) * w].clone() for q in range(world)]  # separate allocations
+    ptrs = [t.data_ptr() for t in bands]
+    for q in range(world):
+        top, bot = band_halo_rows(ptrs, rows, q, w, 4)
+        b0, b1 = int(b[q]), int(b[q + 1])
+        if f32:
+            out = torch.zeros(rows[q] * w, device="cuda")
+            lo, hi = band_interior(h, b0, b1)
+            pb.device.conv5x5_f32_band(rows[q], w, lo, hi, bands[q], top, bot, k, out)
+            got, ref = out.view(rows[q], w)[lo:hi], whole.view(h, w)[b0 + lo:b0 + hi]
+            assert torch.equal(got.view(torch.int32), ref.contiguous().view(torch.int32))
+        else:
+            out = torch.empty(rows[q] * w, dtype=torch.int32, device="cuda")
+            pb.device.conv5x5_u8_band(rows[q], w, scale, bands[q], top, bot, k, out)
+            assert torch.equal(out, whole[b0 * w:b1 * w])
+
+
+def test_band_kernel_rejects_unaligned_rows(cuda):
+    import torch
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200 import synth
+    img = torch.from_numpy(synth.u8_i32(16 * 64)).cuda()
+    out = torch.empty_like(img)
+    p = img.data_ptr()
+    with pytest.raises(pb.PencilError):
+        pb.device.conv5x5_u8_band(16, 64, 256, img, (p + 4, p), (p, p), synth.BINOMIAL, out)
+
+
+def test_fused_band_stencil_symmetric_memory(nccl):
+    """FusedBandStencil at world 1 on the real stack (symmetric memory rendezvous, barriers,
+    the band launch): the whole image, so both edges clamp through the band's own rows."""
+    import torch
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200 import synth
+    from paper_1302_5586_b200.dist import FusedBandStencil
+    h, w = 96, 256
+    img = torch.from_numpy(synth.u8_i32(h * w, seed=4)).cuda()
+    fb = FusedBandStencil(h, w, 0, 1, torch.int32, torch.device("cuda", torch.cuda.current_device()))
+    fb.band().copy_(img)
+    out = torch.empty(h * w, dtype=torch.int32, device="cuda")
+    fb.step_u8(256, synth.BINOMIAL, out)
+    ref = torch.empty_like(out)
+    pb.device.conv5x5_u8(h, w, 256, img, synth.BINOMIAL, ref)
+    assert torch.equal(out, ref)
+    fbf = FusedBandStencil(h, w, 0, 1, torch.float32, torch.device("cuda", torch.cuda.current_device()))
+    imgf = torch.from_numpy(synth.f32(h * w, seed=4)).cuda()
+    fbf.band().copy_(imgf)
+    k = (synth.BINOMIAL / 256.0).astype(np.float32)
+    outf, reff = torch.zeros(h * w, device="cuda"), torch.zeros(h * w, device="cuda")
+    fbf.step_f32(k, outf)
+    pb.device.conv5x5_f32(h, w, imgf, k, reff)
+    assert torch.equal(outf.view(torch.int32), reff.view(torch.int32))
