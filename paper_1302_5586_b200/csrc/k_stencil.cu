@@ -12,6 +12,9 @@
 // the SEP kernels: rows are filtered horizontally as they enter the window and each output row
 // sums 5 of them vertically — 10 FFMA2 per pixel pair instead of 25, exact in integers.
 // 16384^2: int32 storage 0.413 -> 0.374 ms (88% of HBM), packed bytes 0.367 -> 0.258 ms.
+// Taps supported on the radius-2 diamond (the 12 corner taps zero: sharpen, Laplacian shapes) take
+// the DIA kernels, which drop the zero taps at compile time (13 instead of 25 FFMA2 per pair):
+// the suite's sharpen 0.411 -> 0.364 ms on int32 storage, 0.367 -> 0.283 ms on packed bytes.
 //
 // Measured and dropped: two output rows per step (6-row window, four FFMA2 add chains per warp
 // instead of two): 0.485 ms vs 0.475 — the f32 kernel's `wait` stalls are not chain latency;
@@ -271,7 +274,7 @@ struct Sweep {
     long long w;
 };
 
-template <bool U8, int S, bool POW2, bool SEP, bool BAND = false>
+template <bool U8, int S, bool POW2, bool SEP, bool BAND = false, bool DIA = false>
 __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int r_end, const RingLane& L,
                                              typename Pol<U8>::T (*ring)[S_ROWE], u64 (&W)[5][7],
                                              Sweep<typename Pol<U8>::T>& sw, unsigned& orv,
@@ -313,6 +316,7 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
         }
 #pragma unroll
         for (int dj = 0; dj < 5; dj++) {
+            if (DIA && (di - 2 < 0 ? 2 - di : di - 2) + (dj - 2 < 0 ? 2 - dj : dj - 2) > 2) continue;  // zero tap
             const u64 kk = f2pk(a.kf[di * 5 + dj], a.kf[di * 5 + dj]);
             if (U8) {  // exact integer sums: fused is fine
                 a01 = f2fma(kk, W[sl][dj], a01);      // pixels (c, c+2)
@@ -367,7 +371,7 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
 #ifndef STENCIL_SEP_MINB  // swept 4/5/6/8 at 16384^2: int32 0.374/0.374/0.376/0.378 ms, bytes 0.258/0.258/0.262/0.279
 #define STENCIL_SEP_MINB 4
 #endif
-template <bool U8, bool POW2, bool SEP = false>
+template <bool U8, bool POW2, bool SEP = false, bool DIA = false>
 __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? STENCIL_U8_MINB : STENCIL_F32_MINB)) stencil_ring_kernel(
     int h, int w, const typename Pol<U8>::T* __restrict__ img, typename Pol<U8>::T* __restrict__ out,
     typename Pol<U8>::A a) {
@@ -413,11 +417,11 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
     sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;  // next row to enter the ring: i0 + 2 + S_RING
     sw.dst = out + (long long)i0 * w + c;
     for (int i = i0; i < i1; i += 5) {
-        stencil_step<U8, 4, POW2, SEP>(w, i, c, lane, r_end, L, ring, W, sw, orv, a);
-        if (i + 1 < i1) stencil_step<U8, 0, POW2, SEP>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a);
-        if (i + 2 < i1) stencil_step<U8, 1, POW2, SEP>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a);
-        if (i + 3 < i1) stencil_step<U8, 2, POW2, SEP>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a);
-        if (i + 4 < i1) stencil_step<U8, 3, POW2, SEP>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a);
+        stencil_step<U8, 4, POW2, SEP, false, DIA>(w, i, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 1 < i1) stencil_step<U8, 0, POW2, SEP, false, DIA>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 2 < i1) stencil_step<U8, 1, POW2, SEP, false, DIA>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 3 < i1) stencil_step<U8, 2, POW2, SEP, false, DIA>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 4 < i1) stencil_step<U8, 3, POW2, SEP, false, DIA>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a);
     }
     cp_wait<0>();
     // a non-byte pixel anywhere in the sweep: flag the launch for the exact repair pass
@@ -444,7 +448,7 @@ __global__ void u8_rearm_kernel(unsigned* flag) { *flag = 0u; }
 // peer mappings, cp.async straight into the ring), so a multi-GPU stencil step is one launch per
 // rank and no halo copy.  Same sweep, arithmetic and policies as stencil_ring_kernel (the output
 // is bit-identical to the single-GPU image's rows); h = the band's own rows.
-template <bool U8, bool POW2, bool SEP = false>
+template <bool U8, bool POW2, bool SEP = false, bool DIA = false>
 __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? STENCIL_U8_MINB : STENCIL_F32_MINB)) stencil_band_kernel(
     int h, int w, const typename Pol<U8>::T* __restrict__ img, typename Pol<U8>::T* __restrict__ out,
     typename Pol<U8>::A a, BandSrc<typename Pol<U8>::T> bs) {
@@ -490,11 +494,11 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
     sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;
     sw.dst = out + (long long)i0 * w + c;
     for (int i = i0; i < i1; i += 5) {
-        stencil_step<U8, 4, POW2, SEP, true>(w, i, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
-        if (i + 1 < i1) stencil_step<U8, 0, POW2, SEP, true>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
-        if (i + 2 < i1) stencil_step<U8, 1, POW2, SEP, true>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
-        if (i + 3 < i1) stencil_step<U8, 2, POW2, SEP, true>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
-        if (i + 4 < i1) stencil_step<U8, 3, POW2, SEP, true>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        stencil_step<U8, 4, POW2, SEP, true, DIA>(w, i, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 1 < i1) stencil_step<U8, 0, POW2, SEP, true, DIA>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 2 < i1) stencil_step<U8, 1, POW2, SEP, true, DIA>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 3 < i1) stencil_step<U8, 2, POW2, SEP, true, DIA>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 4 < i1) stencil_step<U8, 3, POW2, SEP, true, DIA>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
     }
     cp_wait<0>();
     if (U8 && __any_sync(0xffffffffu, (orv & ~255u) != 0) && lane == 0) atomicOr(a.repair_flag, 1u);
@@ -565,7 +569,7 @@ __device__ __forceinline__ void bytes_read(const unsigned char* slot, int w, int
     P[5] = byte_pair(W1, 3, W2, 1, a);
 }
 
-template <int S, bool POW2, bool SEP>
+template <int S, bool POW2, bool SEP, bool DIA = false>
 __device__ __forceinline__ void bytes_step(int w, int i, int c, int lane, int r_end, const RingLane& L,
                                            unsigned char (*ring)[SB_ROWE], u64 (&W)[5][7],
                                            Sweep<unsigned char>& sw, const StencilArgs& a) {
@@ -598,6 +602,7 @@ __device__ __forceinline__ void bytes_step(int w, int i, int c, int lane, int r_
         }
 #pragma unroll
         for (int dj = 0; dj < 5; dj++) {
+            if (DIA && (di - 2 < 0 ? 2 - di : di - 2) + (dj - 2 < 0 ? 2 - dj : dj - 2) > 2) continue;  // zero tap
             const u64 kk = f2pk(a.kf[di * 5 + dj], a.kf[di * 5 + dj]);
             a02 = f2fma(kk, W[sl][dj], a02);
             a13 = f2fma(kk, W[sl][dj + 1], a13);
@@ -624,7 +629,7 @@ __device__ __forceinline__ void bytes_step(int w, int i, int c, int lane, int r_
             (unsigned)v[0] | ((unsigned)v[1] << 8) | ((unsigned)v[2] << 16) | ((unsigned)v[3] << 24);
 }
 
-template <bool POW2, bool SEP = false>
+template <bool POW2, bool SEP = false, bool DIA = false>
 __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : STENCIL_U8_MINB) stencil_bytes_kernel(int h, int w,
                                                                                  const unsigned char* __restrict__ img,
                                                                                  unsigned char* __restrict__ out,
@@ -671,11 +676,11 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : STENCIL
     sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;
     sw.dst = out + (long long)i0 * w + c;
     for (int i = i0; i < i1; i += 5) {
-        bytes_step<4, POW2, SEP>(w, i, c, lane, r_end, L, ring, W, sw, a);
-        if (i + 1 < i1) bytes_step<0, POW2, SEP>(w, i + 1, c, lane, r_end, L, ring, W, sw, a);
-        if (i + 2 < i1) bytes_step<1, POW2, SEP>(w, i + 2, c, lane, r_end, L, ring, W, sw, a);
-        if (i + 3 < i1) bytes_step<2, POW2, SEP>(w, i + 3, c, lane, r_end, L, ring, W, sw, a);
-        if (i + 4 < i1) bytes_step<3, POW2, SEP>(w, i + 4, c, lane, r_end, L, ring, W, sw, a);
+        bytes_step<4, POW2, SEP, DIA>(w, i, c, lane, r_end, L, ring, W, sw, a);
+        if (i + 1 < i1) bytes_step<0, POW2, SEP, DIA>(w, i + 1, c, lane, r_end, L, ring, W, sw, a);
+        if (i + 2 < i1) bytes_step<1, POW2, SEP, DIA>(w, i + 2, c, lane, r_end, L, ring, W, sw, a);
+        if (i + 3 < i1) bytes_step<2, POW2, SEP, DIA>(w, i + 3, c, lane, r_end, L, ring, W, sw, a);
+        if (i + 4 < i1) bytes_step<3, POW2, SEP, DIA>(w, i + 4, c, lane, r_end, L, ring, W, sw, a);
     }
     cp_wait<0>();
 }
@@ -728,6 +733,22 @@ bool sep_enabled() {
         return !(e && e[0] == '0');
     }();
     return on;
+}
+
+// Taps supported on the radius-2 diamond (|di-2| + |dj-2| <= 2: the 12 corner taps zero — the
+// isotropic sharpen / Laplacian shapes): the DIA kernels skip the zero taps at compile time
+// (13 FFMA2 per pixel pair instead of 25; exact integer sums, so bit-identical).
+// PENCIL_STENCIL_DIA=0 disables them (A/B measurement).
+bool diamond(const int* k) {
+    static const bool on = [] {
+        const char* e = getenv("PENCIL_STENCIL_DIA");
+        return !(e && e[0] == '0');
+    }();
+    if (!on) return false;
+    for (int di = 0; di < 5; di++)
+        for (int dj = 0; dj < 5; dj++)
+            if (abs(di - 2) + abs(dj - 2) > 2 && k[di * 5 + dj]) return false;
+    return true;
 }
 
 unsigned* repair_flag_for(cudaStream_t st) {
@@ -808,9 +829,11 @@ int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, 
     if (!u8_args(st, scale, k25, a)) return (int)cudaErrorMemoryAllocation;
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
     if (!a.exact_only) {
-        const bool sep = sep_enabled() && separable(k25, a);
+        const bool sep = sep_enabled() && separable(k25, a), dia = !sep && diamond(k25);
         if (sep && a.shift >= 0) stencil_ring_kernel<true, true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
         else if (sep) stencil_ring_kernel<true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+        else if (dia && a.shift >= 0) stencil_ring_kernel<true, true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+        else if (dia) stencil_ring_kernel<true, false, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
         else if (a.shift >= 0) stencil_ring_kernel<true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
         else stencil_ring_kernel<true, false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     }
@@ -837,9 +860,11 @@ int launch_conv5x5_u8_band(cudaStream_t st, int h, int w, int scale, const int* 
     const BandSrc<int> bs = {{top[0], top[1]}, {bot[0], bot[1]}, 0, h};
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
     if (!a.exact_only) {
-        const bool sep = sep_enabled() && separable(k25, a);
+        const bool sep = sep_enabled() && separable(k25, a), dia = !sep && diamond(k25);
         if (sep && a.shift >= 0) stencil_band_kernel<true, true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
         else if (sep) stencil_band_kernel<true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+        else if (dia && a.shift >= 0) stencil_band_kernel<true, true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+        else if (dia) stencil_band_kernel<true, false, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
         else if (a.shift >= 0) stencil_band_kernel<true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
         else stencil_band_kernel<true, false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
     }
@@ -895,9 +920,11 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
         a.magic = ~0ull / (unsigned long long)scale + 1;
     }
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
-    const bool sep = sep_enabled() && separable(k25, a);
+    const bool sep = sep_enabled() && separable(k25, a), dia = !sep && diamond(k25);
     if (sep && a.shift >= 0) stencil_bytes_kernel<true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (sep) stencil_bytes_kernel<false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+    else if (dia && a.shift >= 0) stencil_bytes_kernel<true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+    else if (dia) stencil_bytes_kernel<false, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (a.shift >= 0) stencil_bytes_kernel<true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else stencil_bytes_kernel<false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     return (int)cudaGetLastError();

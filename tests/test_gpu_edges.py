@@ -187,3 +187,39 @@ def test_conv_u8_separable_taps_bit_exact(cuda, h, w):
     out = np.zeros(h * w, np.int32)
     pb.dropin.conv5x5_u8(h, w, 1, bad, k, out)
     assert np.array_equal(out.astype(np.int64), oracle.conv5x5_u8(h, w, 1, bad, k))
+
+
+def _diamond_taps(rng, lim):
+    k = rng.integers(-lim, lim + 1, size=(5, 5)).astype(np.int32)
+    for di in range(5):
+        for dj in range(5):
+            if abs(di - 2) + abs(dj - 2) > 2:
+                k[di, dj] = 0
+    return k.reshape(-1)
+
+
+@pytest.mark.parametrize("h,w", [(67, 256), (9, 132), (130, 516), (5, 4)])
+def test_conv_u8_diamond_taps_bit_exact(cuda, h, w):
+    """Taps supported on the radius-2 diamond (the 12 corner taps zero: the sharpen of the bench
+    suite, Laplacian shapes) take the DIA kernels, which skip the zero taps: bit-exact against
+    the 25-tap oracle on int32 storage and packed bytes, pow2 / non-pow2 / unit scales, signed
+    taps, and the exact repair pass for a non-byte pixel."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    rng = np.random.default_rng(h * 1000 + w)
+    img = synth.u8_i32(h * w, seed=h + 2 * w)
+    cases = [(np.ascontiguousarray(synth.SHARPEN), 1), (np.ascontiguousarray(synth.SHARPEN), 3)]
+    cases += [(_diamond_taps(rng, lim), scale) for lim, scale in ((3, 16), (40, 77), (657, 4096), (1, 1))]
+    for k, scale in cases:
+        ref = oracle.conv5x5_u8(h, w, scale, img, k)
+        out = np.zeros(h * w, np.int32)
+        pb.dropin.conv5x5_u8(h, w, scale, img, k, out)
+        assert np.array_equal(out.astype(np.int64), ref), (k, scale)
+        out8 = torch.empty(h * w, dtype=torch.uint8, device="cuda")
+        pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img.astype(np.uint8)).cuda(), k, out8)
+        assert np.array_equal(out8.cpu().numpy().astype(np.int64), ref), (k, scale)
+    bad = img.copy()
+    bad[h // 2 * w + 3] = -7
+    out = np.zeros(h * w, np.int32)
+    pb.dropin.conv5x5_u8(h, w, 1, bad, synth.SHARPEN, out)
+    assert np.array_equal(out.astype(np.int64), oracle.conv5x5_u8(h, w, 1, bad, synth.SHARPEN))
