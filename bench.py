@@ -343,7 +343,7 @@ def suite(args, torch, pb, hbm):
     ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8(h, w_, 1, img_i, synth.SHARPEN, out_i),
                                    k, w, flush))
     out["conv5x5_u8_int32storage_16384_sharpen"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
-                                                    "taps": "signed sharpen (full 25-tap kernel), scale 1"}
+                                                    "taps": "signed sharpen (diamond support: DIA kernel, 13 of 25 taps nonzero), scale 1"}
     img8 = img_i.to(torch.uint8)
     del img_i, out_i
     hout = np.empty(h * w_, np.int32)
@@ -360,7 +360,7 @@ def suite(args, torch, pb, hbm):
     ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8_bytes(h, w_, 1, img8, synth.SHARPEN, out8),
                                    k, w, flush))
     out["conv5x5_u8_bytes_16384_sharpen"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
-                                             "Gpix/s": h * w_ / ms / 1e6, "taps": "signed sharpen, scale 1"}
+                                             "Gpix/s": h * w_ / ms / 1e6, "taps": "signed sharpen (diamond support: DIA kernel), scale 1"}
     del img8, out8
     himgf = synth.f32(h * w_)
     imgf = dev(himgf)
