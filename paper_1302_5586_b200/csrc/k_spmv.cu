@@ -374,6 +374,11 @@ __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_v
 // the fold's cost, the same kernel with the fold replaced by one shared load per batch (wrong
 // results): 1.292 ms — neither the tile-start round trips nor the fold is what separates this
 // kernel from the 1.01 ms row-free gather stream; both edits cost the gather loop its schedule.
+// Source order (spmv_inline): a long row's serial fold holds its warp's gathers (rows > 32 / 64 /
+// 128 left unfolded, wrong results: 1.21 / 1.25 / 1.30 ms vs 1.52), but deferring them — products
+// parked in a plan scratch (nnz floats) by the flow kernel, folded in order by a second,
+// warp-per-row pass — measured 1.69 / 1.60 ms at thresholds 64 / 128: the scratch stream and the
+// extra code in the window loop cost more than the freed gathers gain.  Dropped.
 // DIST: fused SpMV -> all-gather (put_row); the warp fences its peer stores at system scope
 // before it retires, so the barrier that follows the launch publishes them.
 template <bool ASSOC, bool DIST = false>

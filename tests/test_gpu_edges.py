@@ -223,3 +223,35 @@ def test_conv_u8_diamond_taps_bit_exact(cuda, h, w):
     out = np.zeros(h * w, np.int32)
     pb.dropin.conv5x5_u8(h, w, 1, bad, synth.SHARPEN, out)
     assert np.array_equal(out.astype(np.int64), oracle.conv5x5_u8(h, w, 1, bad, synth.SHARPEN))
+
+
+def test_spmv_source_order_long_rows(cuda):
+    """Source order (spmv_inline / ACCESS spmv) with long rows: lengths around 64, rows spanning
+    many 1024-non-zero tiles, long rows at tile edges, empty rows between long ones, and an
+    out-of-range column inside a long row (fault): bit-identical to the emitted C's fp32 chain,
+    through the device plan and the host-array drop-in."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    rng = np.random.default_rng(17)
+    lens = [63, 64, 65, 66, 0, 1, 3000, 0, 65, 1023, 1024, 1025, 2, 9000] + list(rng.integers(0, 200, 3000))
+    lens += [64, 65] * 200 + list(rng.integers(0, 5, 5000))
+    rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    nrows, nnz, ncols = len(lens), int(rowptr[-1]), 50021
+    col = rng.integers(0, ncols, nnz).astype(np.int32)
+    val, x = synth.f32(nnz, seed=21), synth.f32(ncols, seed=22)
+    exact = oracle.spmv_f32(nrows, ncols, nnz, rowptr, col, val, x)
+    rp = torch.from_numpy(rowptr).cuda()
+    plan = pb.device.CsrPlan(nrows, ncols, nnz, rp, mode=0)
+    y = torch.full((nrows,), 7.0, device="cuda")
+    plan.spmv(rp, torch.from_numpy(col).cuda(), torch.from_numpy(val).cuda(), torch.from_numpy(x).cuda(), y)
+    pb.device.sync_status()
+    assert np.array_equal(y.cpu().numpy().view(np.uint32), exact.view(np.uint32))
+    yh = np.full(nrows, np.nan, np.float32)
+    pb.dropin.spmv_inline(nrows, ncols, nnz, rowptr, col, val, x, yh)
+    assert np.array_equal(yh.view(np.uint32), exact.view(np.uint32))
+    # an out-of-range column inside the 9000-long row: E-INTERP, and the row's other products
+    bad = col.copy()
+    bad[int(rowptr[13]) + 4500] = ncols + 5
+    with pytest.raises(pb.PencilError) as e:
+        pb.dropin.spmv_inline(nrows, ncols, nnz, rowptr, bad, val, x, np.zeros(nrows, np.float32))
+    assert e.value.code == "E-INTERP"
