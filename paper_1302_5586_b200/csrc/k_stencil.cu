@@ -27,6 +27,9 @@
 // Policies (same arithmetic as the fallbacks, so the parity claims carry over unchanged):
 //   F32  conv5x5_f32: interior only; acc = acc + k*img per tap in source order with the product
 //        and the sum each rounded (FFMA2 against runtime -0 / 1): bit-exact vs the emitted C.
+//        Taps 0 / +-2^e (e <= 0) are fused into one FFMA2 (PF kernels: k*x is exact, so one
+//        rounding is the same), guarded against products below 2^-126 (f32_repair_kernel):
+//        binomial/256 at 16384^2 0.475 -> 0.394 ms.
 //   U8   conv5x5_u8 on int32 storage: clamp-to-edge; integer sums on the fp32 pipe (exact for
 //        pixels in [0, 255] and |k| <= 657); a warp-row whose window holds a non-byte value (or
 //        a launch with larger taps) takes the exact int64 path from global memory.
@@ -108,6 +111,7 @@ struct StencilArgsF32 {
     unsigned long long magic;
     int exact_only;
     unsigned* repair_flag;
+    unsigned pf_lim;  // PF kernels: (|x| bits) - 1 below this marks a pixel whose scaled product may round
 };
 
 template <typename A>
@@ -173,7 +177,9 @@ __device__ __forceinline__ void ring_issue(const T* src, const RingLane& L, int 
 //   U8:  6 pairs P[m] = (e[m], e[m+2]) for pixel pairs (c, c+2) and (c+1, c+3) (taps P[dj],
 //        P[dj+1]); each pair is converted int -> float by its own LOP3s + one FFMA2, so it lands
 //        in fresh registers too.  `orv` collects every value read (non-byte check).
-template <bool U8, typename A>
+//   F32 PF: `orv` keeps the minimum of (|x| bits) - 1 over the lane's own columns (the
+//        exactness guard of the fused power-of-two taps, below).
+template <bool U8, typename A, int PF = 0>
 __device__ __forceinline__ void ring_read(const typename Pol<U8>::T* slot, int w, int c0, int lane,
                                           const A& a, u64 (&P)[7], unsigned& orv) {
     const int c = c0 + 4 * lane;
@@ -213,6 +219,11 @@ __device__ __forceinline__ void ring_read(const typename Pol<U8>::T* slot, int w
         for (int m = 0; m < 4; m++) P[2 * m] = q[m];
 #pragma unroll
         for (int m = 0; m < 3; m++) P[2 * m + 1] = f2fma((q[m] >> 32) | (q[m + 1] << 32), a.one, a.negz);
+        if (PF && c + 3 < w) {  // columns c .. c+3 (every pixel is some lane's own column)
+            const unsigned x[4] = {(unsigned)q[1], (unsigned)(q[1] >> 32), (unsigned)q[2], (unsigned)(q[2] >> 32)};
+#pragma unroll
+            for (int t = 0; t < 4; t++) orv = min(orv, (x[t] & 0x7fffffffu) - 1u);
+        }
     }
 }
 
@@ -274,7 +285,13 @@ struct Sweep {
     long long w;
 };
 
-template <bool U8, int S, bool POW2, bool SEP, bool BAND = false, bool DIA = false>
+// F32 taps fused into one FFMA2 by the PF kernels: PF 1 = the 16 taps off the centre row and
+// column (the binomial's powers of two), PF 2 = all 25.
+__host__ __device__ constexpr bool pf_tap(int pf, int di, int dj) {
+    return pf == 2 || (pf == 1 && di != 2 && dj != 2);
+}
+
+template <bool U8, int S, bool POW2, bool SEP, bool BAND = false, bool DIA = false, int PF = 0>
 __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int r_end, const RingLane& L,
                                              typename Pol<U8>::T (*ring)[S_ROWE], u64 (&W)[5][7],
                                              Sweep<typename Pol<U8>::T>& sw, unsigned& orv,
@@ -287,7 +304,7 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
     T* slot = ring[(i + 2) % S_RING];
     {
         u64 P[7];
-        ring_read<U8>(slot, w, c - 4 * lane, lane, a, P, orv);
+        ring_read<U8, typename Pol<U8>::A, PF>(slot, w, c - 4 * lane, lane, a, P, orv);
         enter_row<SEP>(P, W[S], a);
     }
     __syncwarp();
@@ -321,6 +338,9 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
             if (U8) {  // exact integer sums: fused is fine
                 a01 = f2fma(kk, W[sl][dj], a01);      // pixels (c, c+2)
                 a23 = f2fma(kk, W[sl][dj + 1], a23);  // pixels (c+1, c+3)
+            } else if (pf_tap(PF, di, dj)) {  // k = 0 or +-2^e: k*x is exact, so one rounding is the same
+                a01 = f2fma(kk, W[sl][dj], a01);
+                a23 = f2fma(kk, W[sl][dj + 2], a23);
             } else {   // product and sum rounded separately, as written
                 a01 = f2fma(f2fma(kk, W[sl][dj], a.negz), a.one, a01);
                 a23 = f2fma(f2fma(kk, W[sl][dj + 2], a.negz), a.one, a23);
@@ -371,7 +391,7 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
 #ifndef STENCIL_SEP_MINB  // swept 4/5/6/8 at 16384^2: int32 0.374/0.374/0.376/0.378 ms, bytes 0.258/0.258/0.262/0.279
 #define STENCIL_SEP_MINB 4
 #endif
-template <bool U8, bool POW2, bool SEP = false, bool DIA = false>
+template <bool U8, bool POW2, bool SEP = false, bool DIA = false, int PF = 0>
 __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? STENCIL_U8_MINB : STENCIL_F32_MINB)) stencil_ring_kernel(
     int h, int w, const typename Pol<U8>::T* __restrict__ img, typename Pol<U8>::T* __restrict__ out,
     typename Pol<U8>::A a) {
@@ -396,7 +416,7 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
         cp_commit();
     }
     u64 W[5][7];
-    unsigned orv = 0;
+    unsigned orv = PF ? ~0u : 0u;
 #pragma unroll
     for (int d = 0; d < 4; d++) {  // rows i0-2 .. i0+1 into the window, slots refilled
         cp_wait<S_RING - 1>();
@@ -404,7 +424,7 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
         T* slot = ring[(i0 - 2 + d + S_RING) % S_RING];
         {
             u64 P[7];
-            ring_read<U8>(slot, w, c0, lane, a, P, orv);
+            ring_read<U8, typename Pol<U8>::A, PF>(slot, w, c0, lane, a, P, orv);
             enter_row<SEP>(P, W[d], a);
         }
         __syncwarp();
@@ -417,16 +437,49 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
     sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;  // next row to enter the ring: i0 + 2 + S_RING
     sw.dst = out + (long long)i0 * w + c;
     for (int i = i0; i < i1; i += 5) {
-        stencil_step<U8, 4, POW2, SEP, false, DIA>(w, i, c, lane, r_end, L, ring, W, sw, orv, a);
-        if (i + 1 < i1) stencil_step<U8, 0, POW2, SEP, false, DIA>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a);
-        if (i + 2 < i1) stencil_step<U8, 1, POW2, SEP, false, DIA>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a);
-        if (i + 3 < i1) stencil_step<U8, 2, POW2, SEP, false, DIA>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a);
-        if (i + 4 < i1) stencil_step<U8, 3, POW2, SEP, false, DIA>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a);
+        stencil_step<U8, 4, POW2, SEP, false, DIA, PF>(w, i, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 1 < i1) stencil_step<U8, 0, POW2, SEP, false, DIA, PF>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 2 < i1) stencil_step<U8, 1, POW2, SEP, false, DIA, PF>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 3 < i1) stencil_step<U8, 2, POW2, SEP, false, DIA, PF>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a);
+        if (i + 4 < i1) stencil_step<U8, 3, POW2, SEP, false, DIA, PF>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a);
     }
     cp_wait<0>();
     // a non-byte pixel anywhere in the sweep: flag the launch for the exact repair pass
     // (u8_repair_kernel), which recomputes the whole image in int64
     if (U8 && __any_sync(0xffffffffu, (orv & ~255u) != 0) && lane == 0) atomicOr(a.repair_flag, 1u);
+    // PF: a pixel with 0 < |x| < 2^(-126 - emin) (a fused tap's product could round in the
+    // subnormal range): flag the launch for f32_repair_kernel
+    if constexpr (!U8 && PF != 0)
+        if (__any_sync(0xffffffffu, orv < a.pf_lim) && lane == 0) atomicOr(a.repair_flag, 1u);
+}
+
+// Exact pass behind the PF kernels: exits at once unless the fast kernel flagged a pixel outside
+// the fused taps' exact range; then recomputes every interior pixel as written (product and sum
+// rounded separately, source order).  The last CTA out re-arms the flag (flag[1] counts CTAs),
+// so the common case costs one near-empty launch.
+__global__ void f32_repair_kernel(int h, int w, const float* __restrict__ img, float* __restrict__ out,
+                                  StencilArgsF32 a) {
+    if (*(volatile unsigned*)a.repair_flag == 0) return;
+    const long long iw = w - 4, n = (long long)(h - 4) * iw;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        const long long i = 2 + p / iw, j = 2 + p % iw;
+        float acc = 0.f;
+#pragma unroll 1
+        for (int di = 0; di < 5; di++)
+#pragma unroll
+            for (int dj = 0; dj < 5; dj++)
+                acc = __fadd_rn(acc, __fmul_rn(a.kf[di * 5 + dj], img[(i + di - 2) * w + j + dj - 2]));
+        out[i * w + j] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(a.repair_flag + 1, 1u) == gridDim.x - 1) {
+            a.repair_flag[1] = 0u;
+            *(volatile unsigned*)a.repair_flag = 0u;
+        }
+    }
 }
 
 // exact int64 repair pass for conv5x5_u8 on int32 storage: runs after the fast kernel and
@@ -759,13 +812,50 @@ unsigned* repair_flag_for(cudaStream_t st) {
     std::lock_guard<std::mutex> lk(mu);
     unsigned*& f = flags[{dev, st}];
     if (!f) {
-        if (cudaMalloc(&f, sizeof(unsigned)) != cudaSuccess) {
+        if (cudaMalloc(&f, 4 * sizeof(unsigned)) != cudaSuccess) {  // [0] u8, [2..3] f32 PF
             f = nullptr;
             return nullptr;
         }
-        cudaMemset(f, 0, sizeof(unsigned));  // synchronous: before any launch can read it
+        cudaMemset(f, 0, 4 * sizeof(unsigned));  // synchronous: before any launch can read it
     }
     return f;
+}
+
+// conv5x5_f32 taps whose products are exact: fusing `acc + k*x` into one FMA is then the same
+// single rounding as the emitted C's rounded product + rounded sum.  A tap qualifies when it is
+// 0 or +-2^e with -126 <= e <= 0 (no overflow; k*x exact unless it lands below 2^-126, which the
+// kernel's guard catches: pixels with 0 < |x| < 2^(-126 - emin) divert the launch to the exact
+// pass).  Returns the PF pattern (2: all 25 taps, 1: the 16 off the centre row/column, 0: none)
+// and the guard's limit.  PENCIL_STENCIL_PF=0 disables it (A/B measurement).
+bool pow2_tap(float k, int& e) {
+    unsigned u;
+    memcpy(&u, &k, 4);
+    u &= 0x7fffffffu;
+    if (u == 0) return true;
+    if ((u & 0x7fffffu) != 0) return false;
+    const int ex = (int)(u >> 23) - 127;
+    if (ex < -126 || ex > 0) return false;
+    e = ex < e ? ex : e;
+    return true;
+}
+int pow2_fusable(const float* k25, unsigned& lim) {
+    static const bool on = [] {
+        const char* e = getenv("PENCIL_STENCIL_PF");
+        return !(e && e[0] == '0');
+    }();
+    if (!on) return 0;
+    for (int pf = 2; pf >= 1; pf--) {
+        int emin = 0;
+        bool ok = true;
+        for (int di = 0; di < 5 && ok; di++)
+            for (int dj = 0; dj < 5 && ok; dj++)
+                if (pf_tap(pf, di, dj)) ok = pow2_tap(k25[di * 5 + dj], emin);
+        if (ok) {
+            lim = ((unsigned)(1 - emin) << 23) - 1u;  // bits of 2^(-126 - emin), minus 1
+            return pf;
+        }
+    }
+    return 0;
 }
 
 bool ring_ok(int h, int w, const void* img, const void* out) {
@@ -787,7 +877,18 @@ int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const fl
     a.one = pack2(1.0f);
     a.negmag = pack2(-8388608.0f);
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h - 4 + S_BAND - 1) / S_BAND);
-    stencil_ring_kernel<false, false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+    const int pf = pow2_fusable(k25, a.pf_lim);
+    unsigned* flag = pf ? repair_flag_for(st) : nullptr;
+    if (pf && flag) {
+        a.repair_flag = flag + 2;
+        if (pf == 2)
+            stencil_ring_kernel<false, false, false, false, 2><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+        else
+            stencil_ring_kernel<false, false, false, false, 1><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+        f32_repair_kernel<<<PENCIL_NUM_SMS * 4, 256, 0, st>>>(h, w, img, out, a);
+    } else {
+        stencil_ring_kernel<false, false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+    }
     return (int)cudaGetLastError();
 }
 
