@@ -779,6 +779,193 @@ bool separable(const int* k, StencilArgs& a) {
     return true;
 }
 
+
+// ---------------------------------------------------------------- SWAR packed-byte sweep
+// Rank-1 taps k = u (x) v with u, v >= 0, a power-of-two scale and every sum below 2^16
+// (255 * sum u * sum v + scale/2 < 65536, result <= 255 without a clamp: the binomial/256 of the
+// config): the sums run as two 16-bit lanes per 32-bit register (SWAR) on the integer pipes
+// instead of as fp32 pairs.  Unpacking is a funnel shift + one PRMT per byte pair (no int->float),
+// each tap one IMAD on two pixels, requantisation one IADD + one PRMT per 4 pixels (scale 256) —
+// and since a pixel pair costs one register instead of two, a lane owns 8 pixels (256-column
+// strips), halving the per-row ring / sync / pointer overhead per pixel.  Integer sums: exact,
+// bit-identical to the other kernels.
+constexpr int SW_ROWE = 272;  // ring row: columns [c0 - 8, c0 + 264)
+
+struct SwarArgs {
+    unsigned u[5], v[5];  // vertical / horizontal taps (non-negative)
+    unsigned half2;       // (scale / 2) in both 16-bit lanes
+    int shift;            // log2(scale) <= 8
+};
+
+__device__ __forceinline__ void cp8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+
+// Row entering the window, filtered horizontally: H[t] = u16x2 pixel pairs (c, c+2), (c+1, c+3),
+// (c+4, c+6), (c+5, c+7).  Q[m] = (e[c-2+m], e[c+m]), m = 0..9.
+__device__ __forceinline__ void swar_enter(const unsigned char* slot, int w, int c0, int lane, const SwarArgs& a,
+                                           unsigned (&H)[4]) {
+    const unsigned* wp = reinterpret_cast<const unsigned*>(slot) + 2 * lane + 1;  // ring bytes 8l+4 ..
+    unsigned W0 = wp[0], W1 = wp[1], W2 = wp[2], W3 = wp[3];  // columns c-4.. | c.. | c+4.. | c+8..
+    if (c0 == 0 || c0 + 256 >= w) {  // image-edge strips: clamp-to-edge columns
+        const int c = c0 + 8 * lane;
+        unsigned v[12];
+#pragma unroll
+        for (int m = 0; m < 12; m++) v[m] = slot[clampi(c - 2 + m, 0, w - 1) - (c0 - 8)];
+        W0 = (v[0] << 16) | (v[1] << 24);
+        W1 = v[2] | (v[3] << 8) | (v[4] << 16) | (v[5] << 24);
+        W2 = v[6] | (v[7] << 8) | (v[8] << 16) | (v[9] << 24);
+        W3 = v[10] | (v[11] << 8);
+    }
+    const unsigned X[5] = {__funnelshift_r(W0, W1, 16), W1, __funnelshift_r(W1, W2, 16), W2,
+                           __funnelshift_r(W2, W3, 16)};
+    unsigned Q[10];
+#pragma unroll
+    for (int m = 0; m < 5; m++) {
+        Q[2 * m] = __byte_perm(X[m], 0u, 0x4240);      // bytes 0, 2 -> 16-bit lanes
+        Q[2 * m + 1] = __byte_perm(X[m], 0u, 0x4341);  // bytes 1, 3
+    }
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        const int b = (t & 1) + 4 * (t >> 1);
+        unsigned acc = a.v[0] * Q[b];
+#pragma unroll
+        for (int dj = 1; dj < 5; dj++) acc += a.v[dj] * Q[b + dj];
+        H[t] = acc;
+    }
+}
+
+template <int S, bool SH8>
+__device__ __forceinline__ void swar_step(int w, int i, int c, int lane, int r_end, bool body, bool halo,
+                                          unsigned char (*ring)[SW_ROWE], unsigned (&H)[5][4],
+                                          Sweep<unsigned char>& sw, const SwarArgs& a) {
+    cp_wait<S_RING - 1>();
+    __syncwarp();
+    unsigned char* slot = ring[(i + 2) % S_RING];
+    swar_enter(slot, w, c - 8 * lane, lane, a, H[S]);
+    __syncwarp();
+    if (i + 2 + S_RING < r_end) {
+        const unsigned char* src = sw.src > sw.src_last ? sw.src_last : sw.src;
+        unsigned char* dst = slot + 8 + 8 * lane;
+        if (body) cp8(dst, src);
+        if (halo) {
+            if (lane == 0) cp4(dst - 4, src - 4);
+            else cp4(dst + 8, src + 8);
+        }
+    }
+    cp_commit();
+    sw.src += sw.w;
+    unsigned o[4];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        unsigned acc = a.half2;
+#pragma unroll
+        for (int di = 0; di < 5; di++) acc += a.u[di] * H[(S + 1 + di) % 5][t];
+        o[t] = acc;
+    }
+    unsigned char* orow = sw.dst;
+    sw.dst += sw.w;
+    uint2 r;
+    if (SH8) {  // the output bytes are the high bytes of the 16-bit lanes
+        r.x = __byte_perm(o[0], o[1], 0x7351);
+        r.y = __byte_perm(o[2], o[3], 0x7351);
+    } else {
+        r.x = ((o[0] >> a.shift) & 0x00ff00ffu) | (((o[1] >> a.shift) & 0x00ff00ffu) << 8);
+        r.y = ((o[2] >> a.shift) & 0x00ff00ffu) | (((o[3] >> a.shift) & 0x00ff00ffu) << 8);
+    }
+    if (body) *reinterpret_cast<uint2*>(orow) = r;
+}
+
+template <bool SH8>
+__global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int h, int w,
+                                                                           const unsigned char* __restrict__ img,
+                                                                           unsigned char* __restrict__ out,
+                                                                           SwarArgs a) {
+    __shared__ __align__(16) unsigned char ring_all[S_WARPS][S_RING][SW_ROWE];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = (blockIdx.x * S_WARPS + warp) * 256;
+    if (c0 >= w) return;
+    const int c = c0 + 8 * lane;
+    const int i0 = blockIdx.y * S_BAND, i1 = min(h, i0 + S_BAND);
+    if (i0 >= i1) return;
+    const int r_end = i1 + 2;
+    const bool body = c + 7 < w;
+    const bool halo = (lane == 0 && c0 > 0) || (lane == 31 && c0 + 256 < w);
+    unsigned char(*ring)[SW_ROWE] = ring_all[warp];
+    auto issue = [&](int r, unsigned char* slot) {
+        const unsigned char* src = img + (long long)clampi(r, 0, h - 1) * w + c;
+        unsigned char* dst = slot + 8 + 8 * lane;
+        if (body) cp8(dst, src);
+        if (halo) {
+            if (lane == 0) cp4(dst - 4, src - 4);
+            else cp4(dst + 8, src + 8);
+        }
+    };
+#pragma unroll
+    for (int d = 0; d < S_RING; d++) {
+        if (i0 - 2 + d < r_end) issue(i0 - 2 + d, ring[(i0 - 2 + d + S_RING) % S_RING]);
+        cp_commit();
+    }
+    unsigned H[5][4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        cp_wait<S_RING - 1>();
+        __syncwarp();
+        unsigned char* slot = ring[(i0 - 2 + d + S_RING) % S_RING];
+        swar_enter(slot, w, c0, lane, a, H[d]);
+        __syncwarp();
+        if (i0 - 2 + d + S_RING < r_end) issue(i0 - 2 + d + S_RING, slot);
+        cp_commit();
+    }
+    Sweep<unsigned char> sw;
+    sw.w = w;
+    sw.src_last = img + (long long)(h - 1) * w + c;
+    sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;
+    sw.dst = out + (long long)i0 * w + c;
+    for (int i = i0; i < i1; i += 5) {
+        swar_step<4, SH8>(w, i, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 1 < i1) swar_step<0, SH8>(w, i + 1, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 2 < i1) swar_step<1, SH8>(w, i + 2, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 3 < i1) swar_step<2, SH8>(w, i + 3, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 4 < i1) swar_step<3, SH8>(w, i + 4, c, lane, r_end, body, halo, ring, H, sw, a);
+    }
+    cp_wait<0>();
+}
+
+// SwarArgs from the separable factorisation, or false (signs, sums >= 2^16, clamp needed).
+// PENCIL_STENCIL_SWAR=0 disables the SWAR kernel (A/B measurement).
+bool swar_args(const StencilArgs& s, int scale, SwarArgs& a) {
+    static const bool on = [] {
+        const char* e = getenv("PENCIL_STENCIL_SWAR");
+        return !(e && e[0] == '0');
+    }();
+    if (!on || s.shift < 0 || s.shift > 8) return false;
+    long long u[5], v[5], su = 0, sv = 0;
+    bool uneg = true, vneg = true;
+    for (int t = 0; t < 5; t++) {
+        u[t] = (long long)s.ku[t];
+        v[t] = (long long)s.kv[t];
+        uneg &= u[t] <= 0;
+        vneg &= v[t] <= 0;
+    }
+    if (uneg && vneg)
+        for (int t = 0; t < 5; t++) u[t] = -u[t], v[t] = -v[t];
+    for (int t = 0; t < 5; t++) {
+        if (u[t] < 0 || v[t] < 0) return false;
+        su += u[t];
+        sv += v[t];
+    }
+    const long long mx = 255ll * su * sv + (scale >> 1);
+    if (mx > 65535 || (mx >> s.shift) > 255) return false;
+    for (int t = 0; t < 5; t++) {
+        a.u[t] = (unsigned)u[t];
+        a.v[t] = (unsigned)v[t];
+    }
+    a.half2 = (unsigned)(scale >> 1) * 0x00010001u;
+    a.shift = s.shift;
+    return true;
+}
+
 // PENCIL_STENCIL_SEP=0 disables the separable kernels (A/B measurement)
 bool sep_enabled() {
     static const bool on = [] {
@@ -1022,7 +1209,12 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
     }
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
     const bool sep = sep_enabled() && separable(k25, a), dia = !sep && diamond(k25);
-    if (sep && a.shift >= 0) stencil_bytes_kernel<true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+    SwarArgs sa;
+    if (sep && w % 8 == 0 && (uintptr_t)img % 8 == 0 && (uintptr_t)out % 8 == 0 && swar_args(a, scale, sa)) {
+        dim3 g8(((w + 255) / 256 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
+        if (sa.shift == 8) stencil_bytes_swar_kernel<true><<<g8, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+        else stencil_bytes_swar_kernel<false><<<g8, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+    } else if (sep && a.shift >= 0) stencil_bytes_kernel<true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (sep) stencil_bytes_kernel<false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (dia && a.shift >= 0) stencil_bytes_kernel<true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (dia) stencil_bytes_kernel<false, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);

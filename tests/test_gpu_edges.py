@@ -298,3 +298,23 @@ def test_conv_f32_pow2_guard_diverts_tiny_pixels(cuda):
     assert _conv_f32_exact(pb, h, w, tiny, binom)
     assert _conv_f32_exact(pb, h, w, img, binom)  # flag re-armed: the fast path again, still exact
     assert _conv_f32_exact(pb, h, w, tiny, binom)
+
+
+@pytest.mark.parametrize("h,w", [(70, 256), (33, 520), (64, 264), (9, 8), (5, 512), (130, 1024)])
+def test_conv_u8_bytes_swar_bit_exact(cuda, h, w):
+    """Non-negative rank-1 taps with 16-bit sums take the SWAR kernel (two pixels per register,
+    8 pixels per lane; scale 256: byte-select requantisation, other powers of two: shift + mask);
+    strips at both image edges, strips narrower than a warp, and the non-SWAR cases (signed taps,
+    sums >= 2^16, a clamp needed) beside them."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    img = synth.u8_i32(h * w, seed=h * 7 + w)
+    img[: min(h * w, 3 * w)] = 255  # saturated rows: the largest sums
+    box = np.outer([1, 2, 2, 2, 1], [1, 2, 2, 2, 1]).astype(synth.BINOMIAL.dtype).reshape(-1)
+    neg = -synth.BINOMIAL
+    for k, scale in ((synth.BINOMIAL, 256), (box, 64), (box, 32), (neg, 256), (synth.BINOMIAL, 128),
+                     (synth.BINOMIAL * 2, 512), (synth.SHARPEN, 1)):
+        out8 = torch.empty(h * w, dtype=torch.uint8, device="cuda")
+        pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img.astype(np.uint8)).cuda(), k, out8)
+        ref = oracle.conv5x5_u8(h, w, scale, img, k)
+        assert np.array_equal(out8.cpu().numpy().astype(np.int64), ref), (h, w, scale)
