@@ -789,7 +789,12 @@ bool separable(const int* k, StencilArgs& a) {
 // and since a pixel pair costs one register instead of two, a lane owns 8 pixels (256-column
 // strips), halving the per-row ring / sync / pointer overhead per pixel.  Integer sums: exact,
 // bit-identical to the other kernels.
-constexpr int SW_ROWE = 272;  // ring row: columns [c0 - 8, c0 + 264)
+// NP pixels per lane (8 or 16): 32*NP-column strips; ring row = [pad | body | pad], pad = NP bytes
+// (16-byte-aligned bodies for 16-byte cp.async), left halo at pad-4, right halo after the body.
+template <int NP>
+struct SwarGeom {
+    static constexpr int PAD = NP, ROWE = 2 * NP + 32 * NP, NW = NP / 4;
+};
 
 struct SwarArgs {
     unsigned u[5], v[5];  // vertical / horizontal taps (non-negative)
@@ -800,33 +805,42 @@ struct SwarArgs {
 __device__ __forceinline__ void cp8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
+template <int NP>
+__device__ __forceinline__ void cp_body(void* dst, const void* src) {
+    if constexpr (NP == 16) cp16(dst, src);
+    else cp8(dst, src);
+}
 
-// Row entering the window, filtered horizontally: H[t] = u16x2 pixel pairs (c, c+2), (c+1, c+3),
-// (c+4, c+6), (c+5, c+7).  Q[m] = (e[c-2+m], e[c+m]), m = 0..9.
+// Row entering the window, filtered horizontally: H[t] = u16x2 pixel pairs; t = 2g + p holds
+// (c + 4g + p, c + 4g + p + 2).  Q[m] = (e[c-2+m], e[c+m]), m = 0..NP+1.
+template <int NP>
 __device__ __forceinline__ void swar_enter(const unsigned char* slot, int w, int c0, int lane, const SwarArgs& a,
-                                           unsigned (&H)[4]) {
-    const unsigned* wp = reinterpret_cast<const unsigned*>(slot) + 2 * lane + 1;  // ring bytes 8l+4 ..
-    unsigned W0 = wp[0], W1 = wp[1], W2 = wp[2], W3 = wp[3];  // columns c-4.. | c.. | c+4.. | c+8..
-    if (c0 == 0 || c0 + 256 >= w) {  // image-edge strips: clamp-to-edge columns
-        const int c = c0 + 8 * lane;
-        unsigned v[12];
+                                           unsigned (&H)[NP / 2]) {
+    typedef SwarGeom<NP> G;
+    const unsigned* wp = reinterpret_cast<const unsigned*>(slot + G::PAD - 4 + NP * lane);
+    unsigned Wd[G::NW + 2];  // columns c-4.. | c.. | ... | c+NP..
 #pragma unroll
-        for (int m = 0; m < 12; m++) v[m] = slot[clampi(c - 2 + m, 0, w - 1) - (c0 - 8)];
-        W0 = (v[0] << 16) | (v[1] << 24);
-        W1 = v[2] | (v[3] << 8) | (v[4] << 16) | (v[5] << 24);
-        W2 = v[6] | (v[7] << 8) | (v[8] << 16) | (v[9] << 24);
-        W3 = v[10] | (v[11] << 8);
+    for (int k = 0; k < G::NW + 2; k++) Wd[k] = wp[k];
+    if (c0 == 0 || c0 + 32 * NP >= w) {  // image-edge strips: clamp-to-edge columns
+        const int c = c0 + NP * lane;
+        unsigned v[NP + 4];
+#pragma unroll
+        for (int m = 0; m < NP + 4; m++) v[m] = slot[clampi(c - 2 + m, 0, w - 1) - (c0 - G::PAD)];
+        Wd[0] = (v[0] << 16) | (v[1] << 24);
+#pragma unroll
+        for (int k = 0; k < G::NW; k++)
+            Wd[k + 1] = v[4 * k + 2] | (v[4 * k + 3] << 8) | (v[4 * k + 4] << 16) | (v[4 * k + 5] << 24);
+        Wd[G::NW + 1] = v[NP + 2] | (v[NP + 3] << 8);
     }
-    const unsigned X[5] = {__funnelshift_r(W0, W1, 16), W1, __funnelshift_r(W1, W2, 16), W2,
-                           __funnelshift_r(W2, W3, 16)};
-    unsigned Q[10];
+    unsigned Q[NP + 2];
 #pragma unroll
-    for (int m = 0; m < 5; m++) {
-        Q[2 * m] = __byte_perm(X[m], 0u, 0x4240);      // bytes 0, 2 -> 16-bit lanes
-        Q[2 * m + 1] = __byte_perm(X[m], 0u, 0x4341);  // bytes 1, 3
+    for (int k = 0; k <= 2 * G::NW; k++) {
+        const unsigned X = (k & 1) ? Wd[k / 2 + 1] : __funnelshift_r(Wd[k / 2], Wd[k / 2 + 1], 16);
+        Q[2 * k] = __byte_perm(X, 0u, 0x4240);      // bytes 0, 2 -> 16-bit lanes
+        Q[2 * k + 1] = __byte_perm(X, 0u, 0x4341);  // bytes 1, 3
     }
 #pragma unroll
-    for (int t = 0; t < 4; t++) {
+    for (int t = 0; t < NP / 2; t++) {
         const int b = (t & 1) + 4 * (t >> 1);
         unsigned acc = a.v[0] * Q[b];
 #pragma unroll
@@ -835,29 +849,32 @@ __device__ __forceinline__ void swar_enter(const unsigned char* slot, int w, int
     }
 }
 
-template <int S, bool SH8>
+template <int NP>
+__device__ __forceinline__ void swar_issue(const unsigned char* src, unsigned char* slot, int lane, bool body,
+                                           bool halo) {
+    unsigned char* dst = slot + SwarGeom<NP>::PAD + NP * lane;
+    if (body) cp_body<NP>(dst, src);
+    if (halo) {
+        if (lane == 0) cp4(dst - 4, src - 4);
+        else cp4(dst + NP, src + NP);
+    }
+}
+
+template <int NP, int S, bool SH8>
 __device__ __forceinline__ void swar_step(int w, int i, int c, int lane, int r_end, bool body, bool halo,
-                                          unsigned char (*ring)[SW_ROWE], unsigned (&H)[5][4],
+                                          unsigned char (*ring)[SwarGeom<NP>::ROWE], unsigned (&H)[5][NP / 2],
                                           Sweep<unsigned char>& sw, const SwarArgs& a) {
     cp_wait<S_RING - 1>();
     __syncwarp();
     unsigned char* slot = ring[(i + 2) % S_RING];
-    swar_enter(slot, w, c - 8 * lane, lane, a, H[S]);
+    swar_enter<NP>(slot, w, c - NP * lane, lane, a, H[S]);
     __syncwarp();
-    if (i + 2 + S_RING < r_end) {
-        const unsigned char* src = sw.src > sw.src_last ? sw.src_last : sw.src;
-        unsigned char* dst = slot + 8 + 8 * lane;
-        if (body) cp8(dst, src);
-        if (halo) {
-            if (lane == 0) cp4(dst - 4, src - 4);
-            else cp4(dst + 8, src + 8);
-        }
-    }
+    if (i + 2 + S_RING < r_end) swar_issue<NP>(sw.src > sw.src_last ? sw.src_last : sw.src, slot, lane, body, halo);
     cp_commit();
     sw.src += sw.w;
-    unsigned o[4];
+    unsigned o[NP / 2];
 #pragma unroll
-    for (int t = 0; t < 4; t++) {
+    for (int t = 0; t < NP / 2; t++) {
         unsigned acc = a.half2;
 #pragma unroll
         for (int di = 0; di < 5; di++) acc += a.u[di] * H[(S + 1 + di) % 5][t];
@@ -865,56 +882,52 @@ __device__ __forceinline__ void swar_step(int w, int i, int c, int lane, int r_e
     }
     unsigned char* orow = sw.dst;
     sw.dst += sw.w;
-    uint2 r;
-    if (SH8) {  // the output bytes are the high bytes of the 16-bit lanes
-        r.x = __byte_perm(o[0], o[1], 0x7351);
-        r.y = __byte_perm(o[2], o[3], 0x7351);
-    } else {
-        r.x = ((o[0] >> a.shift) & 0x00ff00ffu) | (((o[1] >> a.shift) & 0x00ff00ffu) << 8);
-        r.y = ((o[2] >> a.shift) & 0x00ff00ffu) | (((o[3] >> a.shift) & 0x00ff00ffu) << 8);
+    unsigned r[NP / 4];
+#pragma unroll
+    for (int g = 0; g < NP / 4; g++) {
+        if (SH8)  // the output bytes are the high bytes of the 16-bit lanes
+            r[g] = __byte_perm(o[2 * g], o[2 * g + 1], 0x7351);
+        else
+            r[g] = ((o[2 * g] >> a.shift) & 0x00ff00ffu) | (((o[2 * g + 1] >> a.shift) & 0x00ff00ffu) << 8);
     }
-    if (body) *reinterpret_cast<uint2*>(orow) = r;
+    if (body) {
+        if constexpr (NP == 16) *reinterpret_cast<uint4*>(orow) = make_uint4(r[0], r[1], r[2], r[3]);
+        else *reinterpret_cast<uint2*>(orow) = make_uint2(r[0], r[1]);
+    }
 }
 
-template <bool SH8>
+template <int NP, bool SH8>
 __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int h, int w,
                                                                            const unsigned char* __restrict__ img,
                                                                            unsigned char* __restrict__ out,
                                                                            SwarArgs a) {
-    __shared__ __align__(16) unsigned char ring_all[S_WARPS][S_RING][SW_ROWE];
+    typedef SwarGeom<NP> G;
+    __shared__ __align__(16) unsigned char ring_all[S_WARPS][S_RING][G::ROWE];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int c0 = (blockIdx.x * S_WARPS + warp) * 256;
+    const int c0 = (blockIdx.x * S_WARPS + warp) * 32 * NP;
     if (c0 >= w) return;
-    const int c = c0 + 8 * lane;
+    const int c = c0 + NP * lane;
     const int i0 = blockIdx.y * S_BAND, i1 = min(h, i0 + S_BAND);
     if (i0 >= i1) return;
     const int r_end = i1 + 2;
-    const bool body = c + 7 < w;
-    const bool halo = (lane == 0 && c0 > 0) || (lane == 31 && c0 + 256 < w);
-    unsigned char(*ring)[SW_ROWE] = ring_all[warp];
-    auto issue = [&](int r, unsigned char* slot) {
-        const unsigned char* src = img + (long long)clampi(r, 0, h - 1) * w + c;
-        unsigned char* dst = slot + 8 + 8 * lane;
-        if (body) cp8(dst, src);
-        if (halo) {
-            if (lane == 0) cp4(dst - 4, src - 4);
-            else cp4(dst + 8, src + 8);
-        }
-    };
+    const bool body = c + NP - 1 < w;
+    const bool halo = (lane == 0 && c0 > 0) || (lane == 31 && c0 + 32 * NP < w);
+    unsigned char(*ring)[G::ROWE] = ring_all[warp];
+    auto row = [&](int r) { return img + (long long)clampi(r, 0, h - 1) * w + c; };
 #pragma unroll
     for (int d = 0; d < S_RING; d++) {
-        if (i0 - 2 + d < r_end) issue(i0 - 2 + d, ring[(i0 - 2 + d + S_RING) % S_RING]);
+        if (i0 - 2 + d < r_end) swar_issue<NP>(row(i0 - 2 + d), ring[(i0 - 2 + d + S_RING) % S_RING], lane, body, halo);
         cp_commit();
     }
-    unsigned H[5][4];
+    unsigned H[5][NP / 2];
 #pragma unroll
     for (int d = 0; d < 4; d++) {
         cp_wait<S_RING - 1>();
         __syncwarp();
         unsigned char* slot = ring[(i0 - 2 + d + S_RING) % S_RING];
-        swar_enter(slot, w, c0, lane, a, H[d]);
+        swar_enter<NP>(slot, w, c0, lane, a, H[d]);
         __syncwarp();
-        if (i0 - 2 + d + S_RING < r_end) issue(i0 - 2 + d + S_RING, slot);
+        if (i0 - 2 + d + S_RING < r_end) swar_issue<NP>(row(i0 - 2 + d + S_RING), slot, lane, body, halo);
         cp_commit();
     }
     Sweep<unsigned char> sw;
@@ -923,11 +936,11 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int
     sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;
     sw.dst = out + (long long)i0 * w + c;
     for (int i = i0; i < i1; i += 5) {
-        swar_step<4, SH8>(w, i, c, lane, r_end, body, halo, ring, H, sw, a);
-        if (i + 1 < i1) swar_step<0, SH8>(w, i + 1, c, lane, r_end, body, halo, ring, H, sw, a);
-        if (i + 2 < i1) swar_step<1, SH8>(w, i + 2, c, lane, r_end, body, halo, ring, H, sw, a);
-        if (i + 3 < i1) swar_step<2, SH8>(w, i + 3, c, lane, r_end, body, halo, ring, H, sw, a);
-        if (i + 4 < i1) swar_step<3, SH8>(w, i + 4, c, lane, r_end, body, halo, ring, H, sw, a);
+        swar_step<NP, 4, SH8>(w, i, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 1 < i1) swar_step<NP, 0, SH8>(w, i + 1, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 2 < i1) swar_step<NP, 1, SH8>(w, i + 2, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 3 < i1) swar_step<NP, 2, SH8>(w, i + 3, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 4 < i1) swar_step<NP, 3, SH8>(w, i + 4, c, lane, r_end, body, halo, ring, H, sw, a);
     }
     cp_wait<0>();
 }
@@ -1211,9 +1224,17 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
     const bool sep = sep_enabled() && separable(k25, a), dia = !sep && diamond(k25);
     SwarArgs sa;
     if (sep && w % 8 == 0 && (uintptr_t)img % 8 == 0 && (uintptr_t)out % 8 == 0 && swar_args(a, scale, sa)) {
-        dim3 g8(((w + 255) / 256 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
-        if (sa.shift == 8) stencil_bytes_swar_kernel<true><<<g8, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
-        else stencil_bytes_swar_kernel<false><<<g8, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+        static const int np_max = [] {
+            const char* e = getenv("PENCIL_STENCIL_SWAR_NP");
+            return e && atoi(e) == 8 ? 8 : 16;
+        }();
+        const bool n16 = np_max == 16 && w % 16 == 0 && (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0;
+        const int np = n16 ? 16 : 8;
+        dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
+        if (n16 && sa.shift == 8) stencil_bytes_swar_kernel<16, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+        else if (n16) stencil_bytes_swar_kernel<16, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+        else if (sa.shift == 8) stencil_bytes_swar_kernel<8, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+        else stencil_bytes_swar_kernel<8, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
     } else if (sep && a.shift >= 0) stencil_bytes_kernel<true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (sep) stencil_bytes_kernel<false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (dia && a.shift >= 0) stencil_bytes_kernel<true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);

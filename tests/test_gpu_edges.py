@@ -300,7 +300,7 @@ def test_conv_f32_pow2_guard_diverts_tiny_pixels(cuda):
     assert _conv_f32_exact(pb, h, w, tiny, binom)
 
 
-@pytest.mark.parametrize("h,w", [(70, 256), (33, 520), (64, 264), (9, 8), (5, 512), (130, 1024)])
+@pytest.mark.parametrize("h,w", [(70, 256), (33, 520), (64, 264), (9, 8), (5, 512), (130, 1024), (40, 1040), (12, 16), (21, 1552)])
 def test_conv_u8_bytes_swar_bit_exact(cuda, h, w):
     """Non-negative rank-1 taps with 16-bit sums take the SWAR kernel (two pixels per register,
     8 pixels per lane; scale 256: byte-select requantisation, other powers of two: shift + mask);
