@@ -356,7 +356,8 @@ def suite(args, torch, pb, hbm):
                                    k, w, flush))
     b = 2 * h * w_
     out["conv5x5_u8_bytes_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
-                                     "Gpix/s": h * w_ / ms / 1e6, "taps": "binomial, scale 256"}
+                                     "Gpix/s": h * w_ / ms / 1e6, "taps": "binomial, scale 256",
+                                     "kernel": "stencil_bytes_swar_kernel<16> (16-bit SWAR sums, 16 px per lane)"}
     ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8_bytes(h, w_, 1, img8, synth.SHARPEN, out8),
                                    k, w, flush))
     out["conv5x5_u8_bytes_16384_sharpen"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
@@ -368,7 +369,9 @@ def suite(args, torch, pb, hbm):
     kf = (synth.BINOMIAL.astype(np.float32) / 256.0).astype(np.float32)
     ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_f32(h, w_, imgf, kf, outf), k, w, flush))
     b = 8 * h * w_
-    out["conv5x5_f32_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm}
+    out["conv5x5_f32_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
+                                "taps": "binomial / 256",
+                                "kernel": "stencil_ring_kernel<F32, PF 1> (16 power-of-two taps fused, exact)"}
     del imgf, outf
     houtf = np.zeros(h * w_, np.float32)
     cpu_ref(args, out["conv5x5_f32_16384"], lambda L: L.conv5x5_f32(h, w_, P(himgf), P(kf), P(houtf)), b,

@@ -303,7 +303,7 @@ def test_conv_f32_pow2_guard_diverts_tiny_pixels(cuda):
 @pytest.mark.parametrize("h,w", [(70, 256), (33, 520), (64, 264), (9, 8), (5, 512), (130, 1024), (40, 1040), (12, 16), (21, 1552)])
 def test_conv_u8_bytes_swar_bit_exact(cuda, h, w):
     """Non-negative rank-1 taps with 16-bit sums take the SWAR kernel (two pixels per register,
-    8 pixels per lane; scale 256: byte-select requantisation, other powers of two: shift + mask);
+    16 pixels per lane when w % 16 == 0, else 8; scale 256: byte-select requantisation, other powers of two: shift + mask);
     strips at both image edges, strips narrower than a warp, and the non-SWAR cases (signed taps,
     sums >= 2^16, a clamp needed) beside them."""
     import paper_1302_5586_b200 as pb
