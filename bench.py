@@ -175,22 +175,27 @@ def bench_spmv(args, torch, pb, rank, world, dist):
                 exchange = "fused SpMV->all-gather (%s)" % ("NVLS multicast stores" if fz.mc else "NVLink peer stores")
             except Exception as e:  # noqa: BLE001 — no symmetric memory here: the unfused step
                 mode, why = "nccl", str(e).splitlines()[0][:120]
+        # every step feeds the gathered y back as the next x (the iterative method the step
+        # belongs to): the fused path through its ping-pong halves, the unfused one by swapping
+        # two gathered buffers
         if mode == "fused":
+            fz.load(x_local)
 
             def step():
-                fz.step(plan, rp, cd, vd, xg, y)
+                fz.step(plan, rp, cd, vd, None, y)
         else:
-            yg = torch.empty(sh.ncols_padded, device="cuda")
+            bufs = [xg, torch.empty(sh.ncols_padded, device="cuda")]
             exchange = "SpMV + %s all-gather of y" % args.dist_backend
             if args.dist_mode == "fused" and args.dist_backend == "nccl":
                 exchange += " (fused path unavailable: %s)" % why
 
             def step():
-                plan.spmv(rp, cd, vd, xg, y)
-                sh.allgather_x(y_pad, yg)
+                plan.spmv(rp, cd, vd, bufs[0], y)
+                sh.allgather_x(y_pad, bufs[1])
+                bufs.reverse()
         ms = run_steps(torch, step, args.steps, args.warmup, flush, dist)
         kernel_ms = statistics.mean(ms)
-        launches = args.steps * (4 if mode == "fused" else 3)  # + the symmetric-memory barrier
+        launches = args.steps * (5 if mode == "fused" else 3)  # + the two symmetric-memory barriers
         e2e = None
         if not args.no_e2e:
             sh.total_nnz = nnz

@@ -99,34 +99,80 @@ def dist_targets(buffer_ptrs, offset, multicast_ptr, rank, max_rows):
     return [int(b) + slot for b in buffer_ptrs], 0
 
 
+def pingpong_targets(buffer_ptrs, offset, multicast_ptr, rank, max_rows, n):
+    """dist_targets for both halves of a ping-pong pair of gathered-vector buffers laid out back
+    to back (half h starts 4*h*n bytes after `offset`): [(peers, mc) of half 0, of half 1]."""
+    return [dist_targets(buffer_ptrs, offset + 4 * h * n, multicast_ptr, rank, max_rows) for h in (0, 1)]
+
+
+def step_halves(k):
+    """(half the step reads x from, half it stores the gathered y into) for step k."""
+    return k & 1, (k + 1) & 1
+
+
 class FusedSpmvAllgather:
     """Row-sharded SpMV step whose result reaches every rank inside the SpMV kernel
     (pencil_spmv_dev_dist): each warp stores its finished rows to the rank's slot of every
     rank's gathered-vector buffer (torch symmetric memory: NVLink peer mappings, NVLS multicast
     when the switch offers it) while the rest of the matrix is still being multiplied, so the
-    exchange overlaps the compute row batch by row batch; a symmetric-memory barrier on the
-    stream orders the consumers after it.  The unfused equivalent is SpMV + NCCL all-gather of
-    y (`RowShardedCsr.allgather_x`)."""
+    exchange overlaps the compute row batch by row batch.  The unfused equivalent is SpMV + NCCL
+    all-gather of y (`RowShardedCsr.allgather_x`).
+
+    The gathered vector is double-buffered: step k gathers x from half k & 1 and stores y into
+    half (k + 1) & 1 of every rank, so the next step's x never overwrites entries a warp of this
+    or another rank is still gathering (one buffer would be read and written by the same
+    launch).  Each step is bracketed by symmetric-memory barriers on the stream: the one before
+    orders the stores after every rank's last read of the target half (and after the caller's
+    writes of x), the one after orders the consumers after every rank's stores.
+
+        fz.load(x_local)                      # this rank's slice of x -> the first half
+        for _ in range(iters):
+            x = fz.step(plan, rowptr, col, val, None, y)   # returns the half the next step reads
+    """
 
     def __init__(self, shard, device, group=None):
         import torch
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm
         self.sh = shard
-        self.buf = symm.empty(shard.ncols_padded, dtype=torch.float32, device=device)
-        self.buf.zero_()
-        self.hdl = symm.rendezvous(self.buf, group or dist.group.WORLD)
+        n = shard.ncols_padded
+        self.mem = symm.empty(2 * n, dtype=torch.float32, device=device)
+        self.mem.zero_()
+        self.hdl = symm.rendezvous(self.mem, group or dist.group.WORLD)
+        self.halves = (self.mem[:n], self.mem[n:])
         mc = int(self.hdl.multicast_ptr or 0)  # 0: no NVLS multicast mapping for this group
         base = int(self.hdl.buffer_ptrs[self.hdl.rank])
-        offset = self.buf.data_ptr() - base
-        self.peers, self.mc = dist_targets(self.hdl.buffer_ptrs, offset, mc, shard.rank, shard.max_rows)
+        offset = self.mem.data_ptr() - base
+        self.targets = pingpong_targets(self.hdl.buffer_ptrs, offset, mc, shard.rank, shard.max_rows, n)
+        self.mc = self.targets[0][1]
+        self.peers = self.targets[0][0]
+        self.k = 0
+
+    def current(self):
+        """The gathered x the next step reads (every rank's rows, padded layout)."""
+        return self.halves[step_halves(self.k)[0]]
+
+    def load(self, x_local_padded):
+        """Gather every rank's x slice (max_rows elements, padded) into the half the next step reads."""
+        self.sh.allgather_x(x_local_padded, self.current())
+        return self.current()
 
     def step(self, plan, rowptr, col, val, x, y):
-        """y = A_local x for this rank's rows; returns the gathered buffer (every rank's rows,
-        padded layout), valid on every rank once this returns (stream order)."""
-        plan.spmv_dist(rowptr, col, val, x, y, self.peers, self.mc)
+        """y = A_local x for this rank's rows (x = None: the gathered buffer of the previous step /
+        load()); every rank's y lands in the other half.  Returns that half — the x of the next
+        step — valid on every rank once this returns (stream order)."""
+        src, dst = step_halves(self.k)
+        xin = self.halves[src] if x is None else x
+        d = self.halves[dst]
+        lo, hi = d.data_ptr(), d.data_ptr() + 4 * d.numel()
+        if lo < xin.data_ptr() + 4 * xin.numel() and xin.data_ptr() < hi:
+            raise ValueError("x overlaps the half this step stores into; pass x=None to chain steps")
+        peers, mc = self.targets[dst]
         self.hdl.barrier(channel=0)
-        return self.buf
+        plan.spmv_dist(rowptr, col, val, xin, y, peers, mc)
+        self.hdl.barrier(channel=0)
+        self.k += 1
+        return d
 
 
 class BandShardedImage:

@@ -54,52 +54,57 @@ def _spmv_worker(rank, world, port, q):
 
 def _fused_worker(rank, world, port, q, multicast=False):
     """The fused SpMV -> all-gather step (FusedSpmvAllgather) with its device stores emulated:
-    each rank 'stores' its row results at the addresses dist_targets gives for fake per-rank
-    buffer bases (or a fake multicast base), every rank assembles the writes that land in its
-    own buffer, and three iterations A(A(A x)) over the gathered buffers must equal the
-    single-process result bit for bit."""
+    every rank keeps a persistent two-half gathered-vector buffer at a fake base address; in
+    step k it gathers x from half k & 1 and 'stores' its row results at the addresses
+    pingpong_targets gives for half (k + 1) & 1 (peer bases, or a fake multicast base); every
+    rank applies the writes that land in its own buffer, and no write may touch the half any rank
+    reads in that step.  Three chained iterations A(A(A x)) must equal the single-process result
+    bit for bit."""
     import sys
     sys.path.insert(0, ROOT)
     import oracle
     from paper_1302_5586_b200 import synth
-    from paper_1302_5586_b200.dist import RowShardedCsr, dist_targets
+    from paper_1302_5586_b200.dist import RowShardedCsr, pingpong_targets, step_halves
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         rowptr, col, val, x, _ = synth.csr_powerlaw(3000, maxlen=500, seed=11)
         sh = RowShardedCsr(rowptr, col, val, rank, world)
+        n = sh.ncols_padded
         bases = [(r + 1) << 36 for r in range(world)]
         MC = 7 << 40
         offset = 256
-        peers, mc = dist_targets(bases, offset, MC if multicast else 0, rank, sh.max_rows)
-        assert (mc != 0) == multicast and (len(peers) == (0 if multicast else world))
+        tg = pingpong_targets(bases, offset, MC if multicast else 0, rank, sh.max_rows, n)
+        for peers, mc in tg:
+            assert (mc != 0) == multicast and (len(peers) == (0 if multicast else world))
         xg = sh.allgather_x(sh.pad_local_x(torch.from_numpy(x[sh.r0:sh.r1].copy())))
-        buf = xg.numpy().copy()
-        for it in range(2):
-            y = oracle.spmv_f32(sh.nrows, sh.ncols_padded, sh.nnz, sh.rowptr, sh.col, sh.val, buf)
-            # the kernel's stores: y[i] -> address + 4*i, for each target
-            writes = [(t, y) for t in (peers if not mc else [mc])]
+        mem = np.full(2 * n, np.nan, np.float32)  # this rank's two halves, back to back
+        mem[:n] = xg.numpy()
+        mine = MC if multicast else bases[rank]
+        for k in range(3):
+            src, dst = step_halves(k)
+            y = oracle.spmv_f32(sh.nrows, n, sh.nnz, sh.rowptr, sh.col, sh.val, mem[src * n:(src + 1) * n].copy())
+            peers, mc = tg[dst]
             allw = [None] * world
-            dist.all_gather_object(allw, writes)
-            nxt = np.full(sh.ncols_padded, np.nan, np.float32)
+            dist.all_gather_object(allw, [(t, y) for t in (peers if not mc else [mc])])
             for wr in allw:
                 for t, yy in wr:
-                    mine = bases[rank] if not multicast else MC
                     if not multicast and not (bases[rank] <= t < bases[rank] + (1 << 36)):
                         continue  # a store into another rank's buffer
                     start = (t - mine - offset) // 4
-                    assert (t - mine - offset) % 4 == 0 and 0 <= start and start + yy.size <= nxt.size
-                    nxt[start:start + yy.size] = yy
-            # padding slots stay unwritten; everything the remapped columns read must be written
-            used = np.unique(sh.col)
-            assert not np.isnan(nxt[used]).any()
-            buf = np.nan_to_num(nxt)
-        y2 = oracle.spmv_f32(sh.nrows, sh.ncols_padded, sh.nnz, sh.rowptr, sh.col, sh.val, buf)
-        n = rowptr.size - 1
-        ref = oracle.spmv_f32(n, n, col.size, rowptr, col, val,
-                              oracle.spmv_f32(n, n, col.size, rowptr, col, val,
-                                              oracle.spmv_f32(n, n, col.size, rowptr, col, val, x)))
-        ok = torch.tensor([int(np.array_equal(y2.view(np.uint32), ref[sh.r0:sh.r1].view(np.uint32)))])
+                    assert (t - mine - offset) % 4 == 0
+                    # the race the ping-pong removes: a store into the half being read this step
+                    assert dst * n <= start and start + yy.size <= (dst + 1) * n, "store into the read half"
+                    mem[start:start + yy.size] = yy
+            # everything the remapped columns read next step was written this step
+            assert not np.isnan(mem[dst * n + np.unique(sh.col)]).any()
+            mem[src * n:(src + 1) * n] = np.nan  # the old x is dead: a stale read would show as NaN
+        y3 = mem[step_halves(3)[0] * n:][:n]
+        ref = x
+        for _ in range(3):
+            ref = oracle.spmv_f32(rowptr.size - 1, x.size, col.size, rowptr, col, val, ref)
+        got = y3[sh.rank * sh.max_rows:][: sh.nrows]
+        ok = torch.tensor([int(np.array_equal(got.view(np.uint32), ref[sh.r0:sh.r1].view(np.uint32)))])
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if rank == 0:
             q.put(bool(ok.item()))
@@ -270,3 +275,70 @@ def test_fused_band_halo_addresses_resolve_to_neighbour_rows(world):
                                              np.zeros(n * w, np.float32)).reshape(n, w)[2:-2]
                 lo, hi = band_interior(h, b0, b1)
                 assert np.array_equal(out[lo:hi].view(np.uint32), ref[b0 + lo:b0 + hi].view(np.uint32))
+
+
+def _emulate_fused_concurrent(world, pingpong, multicast=False, steps=3, seed=21):
+    """All ranks of the fused SpMV -> all-gather step in one process, worst-case interleaved: the
+    ranks advance one row at a time, round robin, and every store is visible to every reader at
+    once (the way NVLink stores of one rank land while another rank's warps are still gathering).
+    Rows fold in source order (the emitted C's fp32 rounding).  pingpong=False models the single
+    buffer of round 1 (gather from and store into the same half)."""
+    from paper_1302_5586_b200 import synth
+    from paper_1302_5586_b200.dist import RowShardedCsr, pingpong_targets, step_halves
+    rowptr, col, val, x, _ = synth.csr_powerlaw(600, maxlen=60, seed=seed)
+    shards = [RowShardedCsr(rowptr, col, val, r, world) for r in range(world)]
+    n = shards[0].ncols_padded
+    bases, MC, offset = [(r + 1) << 36 for r in range(world)], 7 << 40, 64
+    span = 8 * n + offset
+    mem = [np.zeros(2 * n, np.float32) for _ in range(world)]
+    for r, sh in enumerate(shards):
+        for q, shq in enumerate(shards):
+            mem[r][q * shq.max_rows:q * shq.max_rows + shq.nrows] = x[shq.r0:shq.r1]
+    tgs = [pingpong_targets(bases, offset, MC if multicast else 0, r, sh.max_rows, n) for r, sh in enumerate(shards)]
+
+    def store(addr, v):
+        if multicast:
+            i = (addr - MC - offset) // 4
+            for m in mem:
+                m[i] = v
+            return
+        r = next(r for r in range(world) if bases[r] <= addr < bases[r] + span)
+        mem[r][(addr - bases[r] - offset) // 4] = v
+
+    for k in range(steps):
+        src, dst = step_halves(k) if pingpong else (0, 0)
+        cursors = [0] * world
+        while any(c < sh.nrows for c, sh in zip(cursors, shards)):
+            for r, sh in enumerate(shards):
+                i = cursors[r]
+                if i >= sh.nrows:
+                    continue
+                xs = mem[r][src * n:(src + 1) * n]
+                s = np.float32(0)
+                for kk in range(sh.rowptr[i], sh.rowptr[i + 1]):
+                    s = np.float32(s + np.float32(sh.val[kk] * xs[sh.col[kk]]))
+                peers, mc = tgs[r][dst]
+                for t in (peers if not mc else [mc]):
+                    store(t + 4 * i, s)
+                cursors[r] += 1
+    last = step_halves(steps)[0] if pingpong else 0
+    got = np.concatenate([mem[0][last * n + q * sh.max_rows:][: sh.nrows] for q, sh in enumerate(shards)])
+    return got, (rowptr, col, val, x)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("multicast", [False, True])
+def test_fused_spmv_pingpong_survives_concurrent_overwrite(world, multicast):
+    """Chained in-place steps under the worst-case interleaving of stores and gathers: with the
+    ping-pong halves the result is A(A(A x)) bit for bit; the single-buffer variant (round 1's
+    FusedSpmvAllgather) is not — the model has teeth."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    got, (rowptr, col, val, x) = _emulate_fused_concurrent(world, True, multicast)
+    ref = x
+    for _ in range(3):
+        ref = oracle.spmv_f32(rowptr.size - 1, x.size, col.size, rowptr, col, val, ref)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    bad, _ = _emulate_fused_concurrent(world, False, multicast)
+    assert not np.array_equal(bad.view(np.uint32), ref.view(np.uint32))

@@ -130,6 +130,47 @@ def test_fused_spmv_allgather_world1(nccl):
     print("multicast" if fz.mc else "peer stores", len(fz.peers))
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fused_spmv_allgather_chained_in_place(nccl, mode):
+    """Iterated in place, as INTEGRATION.md shows it: x = fz.step(..., None, y) four times, each
+    step gathering from the buffer the previous step stored into.  Source order (mode 0) must
+    equal oracle.spmv_f32 applied four times bit for bit; reassociated (mode 1) within 1e-5
+    normwise per step against the oracle applied to the GPU's own previous iterate."""
+    import torch
+    import oracle
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200 import synth
+    from paper_1302_5586_b200.dist import RowShardedCsr, FusedSpmvAllgather
+    from conftest import normwise_err
+    rowptr, col, val, x, _ = synth.csr_powerlaw(60000, maxlen=1500, seed=12)
+    n, nnz = rowptr.size - 1, col.size
+    sh = RowShardedCsr(rowptr, col, val, 0, 1)
+    rp, cd, vd = (torch.from_numpy(a).cuda() for a in (sh.rowptr, sh.col, sh.val))
+    plan = pb.device.CsrPlan(sh.nrows, sh.ncols_padded, sh.nnz, rp, mode=mode)
+    fz = FusedSpmvAllgather(sh, torch.device("cuda", torch.cuda.current_device()))
+    fz.load(sh.pad_local_x(torch.from_numpy(x).cuda()))
+    y = torch.empty(sh.nrows, device="cuda")
+    ref = x.copy()
+    for it in range(4):
+        prev = fz.current()[: n].cpu().numpy()
+        xn = fz.step(plan, rp, cd, vd, None, y)
+        torch.cuda.synchronize()
+        pb.device.sync_status()
+        got = xn[: n].cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), y.cpu().numpy().view(np.uint32))
+        if mode == 0:
+            ref = oracle.spmv_f32(n, n, nnz, rowptr, col, val, ref)
+            assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), f"step {it}"
+        else:
+            r64 = oracle.spmv(n, n, nnz, rowptr, col, val, prev)
+            terms = np.abs(val.astype(np.float64) * prev.astype(np.float64)[col])
+            scale = np.add.reduceat(np.append(terms, 0.0), rowptr[:-1]) * (np.diff(rowptr) > 0)
+            assert normwise_err(got, r64, scale) <= 1e-5, f"step {it}"
+    # an explicit x that aliases the half the step stores into is refused
+    with pytest.raises(ValueError):
+        fz.step(plan, rp, cd, vd, fz.halves[(fz.k + 1) & 1], y)
+
+
 @pytest.mark.parametrize("h,w,world", [(200, 256, 3), (67, 132, 4), (41, 512, 2)])
 @pytest.mark.parametrize("case", ["binomial", "sharpen", "scale3", "nonbyte", "bigtaps", "f32"])
 def test_band_kernels_read_halos_in_place(cuda, h, w, world, case):
