@@ -68,8 +68,11 @@ const char* pencil_status_code(int status); /* "E-INTERP", "E-ARG", ... */
 
 /* ===== 3. Device-resident, stream-ordered API (no host synchronization) ==================
  * `stream` is a cudaStream_t of the current device (0 = the legacy default stream).
- * Device faults (E-INTERP analogues) accumulate in a per-device status word read and
- * cleared by pencil_sync_status(). Return value: pencil_status of the launch itself. */
+ * Device faults (E-INTERP analogues) accumulate in a per-(device, stream) status word read and
+ * cleared by pencil_sync_status(stream). Every device word a launch mutates (fault word, SpMV
+ * tile tickets, gemv_t last-CTA counters) is per (device, stream), so calls on different streams
+ * — one CSR plan included — run concurrently without sharing state.
+ * Return value: pencil_status of the launch itself. */
 typedef void* pencil_stream_t;
 int pencil_gemv_dev(pencil_stream_t s, int m, int n, float alpha, float beta, const float* A,
                     const float* x, float* y);
@@ -158,6 +161,10 @@ int pencil_runtime_call(pencil_runtime_t rt, const char* fn, int nargs, const pe
                         pencil_value* ret);
 /* the fp-reduction-reorders-results flag of the last call (pencilc.cpp:157-161 analogue) */
 int pencil_runtime_fp_reordered(pencil_runtime_t rt);
+/* the kernel variant the mapper chose for the last call (pencil_schedule.kernel): the call
+ * launches that kernel — the CSR fixtures, e.g., fold their rows in source order or
+ * reassociated according to the inner loop's role, not according to the function name */
+const char* pencil_runtime_last_kernel(pencil_runtime_t rt);
 
 /* ===== 5. Mapper: loop verdicts -> grid/block/tile schedule ==============================
  * Verdicts are the reference analyzer's (depanalysis.hpp:14 Verdict, same numbering). */

@@ -62,6 +62,7 @@ SIGNATURES = {
                                           ctypes.POINTER(c_void_p)]),
     "pencil_runtime_call": (c_int, [P, c_char_p, c_int, P, P]),
     "pencil_runtime_fp_reordered": (c_int, [P]),
+    "pencil_runtime_last_kernel": (c_char_p, [P]),
     # §5 mapper
     "pencil_map_nest": (c_int, [c_char_p, P, c_int, P]),
     "pencil_fixture_verdicts": (c_int, [c_char_p, P, c_int]),

@@ -124,6 +124,8 @@ const FnSpec* find_fixture(const char* name) {
 
 }  // namespace
 int pencil_internal_fail(int status, const char* msg);  // runtime.cpp
+int pencil_internal_spmv(int mode, int nrows, int ncols, int nnz, int* rowptr, int* col, float* val, float* x,
+                         float* y);  // runtime.cpp
 namespace {
 
 thread_local char d_msg[512];
@@ -199,6 +201,7 @@ struct pencil_runtime {
     int device = 0;
     std::map<std::string, DArray> arrays;
     int fp_reordered = 0;
+    char last_kernel[48] = "";
 };
 
 extern "C" {
@@ -349,24 +352,30 @@ int pencil_runtime_call(pencil_runtime_t rt, const char* fn, int nargs, const pe
     auto P = [&](int a) { return (float*)ptr[a]; };
     auto Q = [&](int a) { return (int*)ptr[a]; };
     if (ret) { ret->kind = -1; ret->i = 0; ret->f = 0.0; }
-    std::string f = fn;
-    if (f == "gemv") gemv(I(0), I(1), F(2), F(3), P(4), P(5), P(6));
-    else if (f == "gemv_t") gemv_t(I(0), I(1), I(2), I(3), I(4), F(5), F(6), P(7), P(8), P(9));
-    else if (f == "dot") {
+    // launch through the schedule's kernel (the mapper's choice), not through the function name:
+    // the CSR executors take the reduction role of the row loop as their fold mode
+    const std::string k = sch.kernel;
+    snprintf(rt->last_kernel, sizeof rt->last_kernel, "%s", sch.kernel);
+    if (k == "gemv_warp_per_row") gemv(I(0), I(1), F(2), F(3), P(4), P(5), P(6));
+    else if (k == "gemv_t_colblock_splitk") gemv_t(I(0), I(1), I(2), I(3), I(4), F(5), F(6), P(7), P(8), P(9));
+    else if (k == "dot_grid_tree") {
         float r = dot(I(0), P(1), P(2));
         if (ret) { ret->kind = PENCIL_ARG_FLOAT; ret->f = r; }
-    } else if (f == "axpy") axpy(I(0), F(1), P(2), P(3));
-    else if (f == "spmv_vec") spmv_vec(I(0), I(1), I(2), Q(3), Q(4), P(5), P(6), P(7));
-    else if (f == "spmv_inline") spmv_inline(I(0), I(1), I(2), Q(3), Q(4), P(5), P(6), P(7));
-    else if (f == "spmv") spmv(I(0), I(1), I(2), Q(3), Q(4), P(5), P(6), P(7));
-    else if (f == "spmv_row") spmv_row(I(0), I(1), I(2), I(3), Q(4), Q(5), P(6), P(7), P(8));
-    else if (f == "conv5x5_u8") conv5x5_u8(I(0), I(1), I(2), Q(3), Q(4), Q(5));
-    else if (f == "conv5x5_f32") conv5x5_f32(I(0), I(1), P(2), P(3), P(4));
-    else if (f == "gemm") gemm(I(0), I(1), I(2), F(3), F(4), P(5), P(6), P(7));
+    } else if (k == "axpy_stream_f4") axpy(I(0), F(1), P(2), P(3));
+    else if (k == "csr_tiles_reassoc" || k == "csr_tiles_source_order")
+        pencil_internal_spmv(k == "csr_tiles_reassoc" ? 1 : 0, I(0), I(1), I(2), Q(3), Q(4), P(5), P(6), P(7));
+    else if (k == "csr_row_seq") spmv_row(I(0), I(1), I(2), I(3), Q(4), Q(5), P(6), P(7), P(8));
+    else if (k == "conv5x5_u8_sweep") conv5x5_u8(I(0), I(1), I(2), Q(3), Q(4), Q(5));
+    else if (k == "conv5x5_f32_sweep") conv5x5_f32(I(0), I(1), P(2), P(3), P(4));
+    else if (k == "gemm_tcgen05_3xtf32") gemm(I(0), I(1), I(2), F(3), F(4), P(5), P(6), P(7));
+    else return dfail(PENCIL_E_UNSUPPORTED, "E-UNSUPPORTED: no launcher for kernel '%s'", sch.kernel),
+                PENCIL_E_UNSUPPORTED;
     int st = pencil_cuda_last_status();
     if (st) dfail(st, "%s", pencil_cuda_last_error());
     return st;
 }
+
+const char* pencil_runtime_last_kernel(pencil_runtime_t rt) { return rt ? rt->last_kernel : ""; }
 
 // ------------------------------------------------------------------ mapper
 // The verdict switch of emit_openmp (pretty.cpp:479-501) decides one thing per loop:
@@ -412,8 +421,11 @@ int pencil_map_nest(const char* fn, const pencil_loop_verdict* loops, int nloops
     else if (f == "gemv_t" && is({G, R})) k = "gemv_t_colblock_splitk";
     else if (f == "dot" && is({R})) k = "dot_grid_tree";
     else if (f == "axpy" && is({G})) k = "axpy_stream_f4";
-    else if ((f == "spmv_vec") && is({G, R})) k = "csr_stream_assoc";
-    else if ((f == "spmv_inline" || f == "spmv") && is({G, S})) k = "csr_stream_seq";
+    // the CSR nests: the row loop on the grid (persistent warps over nnz-balanced tiles); the
+    // inner loop's role picks the fold — REDUCE (the reduction pragma) reassociates, SEQ (UNKNOWN
+    // or SERIAL: spmv_inline, the ACCESS-summarised spmv driver) keeps the source order
+    else if ((f == "spmv_vec" || f == "spmv_inline" || f == "spmv") && is({G, R})) k = "csr_tiles_reassoc";
+    else if ((f == "spmv_vec" || f == "spmv_inline" || f == "spmv") && is({G, S})) k = "csr_tiles_source_order";
     else if (f == "spmv_row" && is({S})) k = "csr_row_seq";
     else if (f == "conv5x5_u8" && is({G, G, S, S})) k = "conv5x5_u8_sweep";
     else if (f == "conv5x5_f32" && is({G, G, S, S})) k = "conv5x5_f32_sweep";

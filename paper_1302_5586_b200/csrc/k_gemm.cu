@@ -522,11 +522,12 @@ int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, c
         dim3 g((Kp + 31) / 32, (n + 31) / 32);
         split_transpose_kernel<<<g, dim3(32, 8), 0, st>>>(B, k, n, Kp, bhi, blo);
     }
-    // CTA-pair kernel by default (PENCIL_GEMM_2SM=0 selects the single-CTA kernel)
-    static const int two_sm = [] {  // read once (thread-safe static initialisation)
-        const char* e = getenv("PENCIL_GEMM_2SM");
-        return !(e && e[0] == '0') ? 1 : 0;
-    }();
+    // CTA-pair kernel (-DPENCIL_VARIANT_GEMM_1SM builds the single-CTA kernel, tools/variant_build.sh)
+#ifdef PENCIL_VARIANT_GEMM_1SM
+    const int two_sm = 0;
+#else
+    const int two_sm = 1;
+#endif
     CUtensorMap maps[4];
     const int b_box = two_sm ? P_BN_HALF : BN;
     if (!make_map(&maps[0], ahi, m, Kp, BM) || !make_map(&maps[1], alo, m, Kp, BM) ||

@@ -129,13 +129,14 @@ __global__ void micro_discard_kernel(long long nlines, char* __restrict__ d) {
 // then discard its lines, so the next step starts on an empty, CLEAN L2 (as ncu's cache control
 // does).  Without the discard ~126 MB of the fill's dirty lines are written back while the next
 // step runs (gemv 8192^2: 49.8 us under the fill alone vs 43 us for the kernel itself);
-// PENCIL_L2_FLUSH=dirty keeps the fill-only flush for comparison.
+// (-DPENCIL_VARIANT_L2_DIRTY builds the fill-only flush for comparison, tools/variant_build.sh.)
 int launch_micro_l2_flush(cudaStream_t st, long long n, float* buf) {
     static float v = 0.f;
-    static const bool dirty = [] {
-        const char* e = getenv("PENCIL_L2_FLUSH");
-        return e && strcmp(e, "dirty") == 0;
-    }();
+#ifdef PENCIL_VARIANT_L2_DIRTY
+    const bool dirty = true;
+#else
+    const bool dirty = false;
+#endif
     v += 1.f;
     micro_fill_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>(n >> 2, reinterpret_cast<float4*>(buf), v);
     if (!dirty) micro_discard_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>(n * 4 / 128, reinterpret_cast<char*>(buf));

@@ -8,9 +8,9 @@
 // (csr_plan_kernel), it gives every warp a contiguous row range holding ~TILE_NNZ
 // non-zeros regardless of the power-law row-length distribution.
 //
-// Executors (launch_csr_spmv picks one): csr_flow_kernel (default; the tile's non-zeros stream in
-// continuous 16-byte-per-lane windows, batches folded from whichever window holds them),
-// csr_vec_kernel (windows restart at each batch), csr_stream_kernel (scalar loads; any alignment).
+// Executors (launch_csr_spmv picks one): csr_flow_kernel (16-byte-aligned col / val; the tile's
+// non-zeros stream in continuous 16-byte-per-lane windows, batches folded from whichever window
+// holds them) and csr_stream_kernel (scalar loads; any alignment).
 // The structure they share — csr_stream_kernel: per tile, per batch of 32 rows, the batch's non-zeros
 // are streamed with coalesced loads (col, val: evict-first) while x[col] is gathered
 // (evict-last, so the 64 MB vector stays L2-resident), staged in shared memory, then each
@@ -23,9 +23,6 @@
 // Faults (E-INTERP analogues): col outside [0, ncols) or rowptr outside [0, nnz] set a bit
 // in the status word and contribute 0.  A non-monotone rowptr (legal in PENCIL: the row
 // is empty) switches the launch to a generic thread-per-row schedule.
-#include <cstdlib>
-#include <cstring>
-
 #include "common.cuh"
 #include "kernels.h"
 
@@ -119,7 +116,6 @@ __device__ void spmv_generic(int nrows, int ncols, int nnz_len, const int* __res
 __device__ __forceinline__ int skew(int t) { return t + (t >> 5); }
 // the same pad, 4 floats per 32: 16-byte aligned slots for vector stores, conflict-free reads
 __device__ __forceinline__ int skew4(int t) { return t + 4 * (t >> 5); }
-#define WCHUNK_SKEWED (WCHUNK + WCH / 32)
 
 // Fold of one staged window into the lanes' rows: lane r adds the products of its row that lie in
 // [lo, hi) (window positions, `base` = the window's first position).  Source order: each lane
@@ -168,11 +164,11 @@ __device__ __forceinline__ float fold_window(float s, int lo, int hi, int base, 
 }
 
 template <bool ASSOC, int WCH>
-__global__ void __launch_bounds__(SPMV_THREADS, (WCH <= 128 ? CTAS_PER_SM : 6)) csr_stream_kernel(
+__global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_stream_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
-    const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
-    unsigned* __restrict__ status) {
+    const int* __restrict__ tile_row, int ntiles, const unsigned* __restrict__ plan,
+    unsigned* __restrict__ tk, unsigned* __restrict__ status) {
     __shared__ float s_prod[WARPS_PER_CTA][WCH + WCH / 32];
     if (plan[0]) {  // non-monotone rowptr, flagged by the plan kernel earlier on this stream
         spmv_generic(nrows, ncols, nnz_len, rowptr, col, val, x, y, status);
@@ -183,11 +179,11 @@ __global__ void __launch_bounds__(SPMV_THREADS, (WCH <= 128 ? CTAS_PER_SM : 6)) 
     float* sp = s_prod[warp];
     for (;;) {
     unsigned ticket = 0;
-    if (lane == 0) ticket = atomicAdd(&plan[1], 1u);
+    if (lane == 0) ticket = atomicAdd(tk, 1u);
     ticket = __shfl_sync(0xffffffffu, ticket, 0);
     if (ticket >= (unsigned)ntiles) {
         // every warp draws exactly one failing ticket; the last one re-arms the counter
-        if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
+        if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) *tk = 0;
         return;
     }
     const int tile = (int)ticket;
@@ -235,135 +231,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, (WCH <= 128 ? CTAS_PER_SM : 6)) 
     }  // tickets
 }
 
-// 128-bit variant (PENCIL_SPMV_KERNEL=vec): the same tiles, batches and fold, but each lane
-// streams 4 CONSECUTIVE non-zeros with one 16-byte load per array (chunks are 4-aligned windows
-// [qa, qa + 128); lanes whose 4 positions miss the batch's range do not load) and stores its 4
-// products with one 16-byte shared store: 2 + 1 instructions where the scalar kernel issues
-// 8 + 4.  The staging pad moves to 4 floats per 32 (aligned for the vector store; still
-// conflict-free for rows of equal length).  Needs 16-byte-aligned col / val.
-template <bool ASSOC, int VU>
-__global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_vec_kernel(
-    int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
-    const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
-    const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
-    unsigned* __restrict__ status) {
-    __shared__ __align__(16) float s_prod[WARPS_PER_CTA][128 * VU + 16 * VU];
-    if (plan[0]) {
-        spmv_generic(nrows, ncols, nnz_len, rowptr, col, val, x, y, status);
-        return;
-    }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
-    float* sp = s_prod[warp];
-    // The control path is prefetched one step ahead so its latencies overlap the streaming:
-    // the next tile's ticket and bounds are drawn when a tile starts, and the next 32-row
-    // batch's row starts are loaded when a batch starts (one load per lane: row rb+lane's start;
-    // its end is lane+1's start, rowptr[min(rb + 32, r1)] closes the batch).
-    auto draw = [&](unsigned& t, int& a, int& b) {
-        unsigned v = 0;
-        if (lane == 0) v = atomicAdd(&plan[1], 1u);
-        t = __shfl_sync(0xffffffffu, v, 0);
-        if (t < (unsigned)ntiles) {
-            a = __ldg(tile_row + t);
-            b = __ldg(tile_row + t + 1);
-        }
-    };
-    auto batch_starts = [&](int rb, int r1, int& s_l, int& e_b) {
-        s_l = __ldg(rowptr + min(rb + lane, r1));
-        e_b = __ldg(rowptr + min(rb + 32, r1));
-    };
-    unsigned ticket;
-    int r0 = 0, r1 = 0;
-    draw(ticket, r0, r1);
-    for (;;) {
-        if (ticket >= (unsigned)ntiles) {
-            // every warp draws exactly one failing ticket; the last one re-arms the counter
-            if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
-            return;
-        }
-        unsigned nticket;
-        int nr0 = 0, nr1 = 0;
-        draw(nticket, nr0, nr1);
-        int cur_s = 0, cur_e = 0;
-        if (r0 < r1) batch_starts(r0, r1, cur_s, cur_e);
-        for (int rb = r0; rb < r1; rb += 32) {
-            int nxt_s = 0, nxt_e = 0;
-            if (rb + 32 < r1) batch_starts(rb + 32, r1, nxt_s, nxt_e);
-            const int re = min(rb + 32, r1);
-            const int row = rb + lane;
-            const bool active = row < re;
-            int my_s = cur_s, my_e = __shfl_down_sync(0xffffffffu, cur_s, 1);
-            if (lane == 31) my_e = cur_e;
-            if (!active) my_s = my_e = 0;
-            const int q_begin = max(__shfl_sync(0xffffffffu, cur_s, 0), 0);
-            const int q_end = min(cur_e, nnz_len);
-            cur_s = nxt_s;
-            cur_e = nxt_e;
-            float s = 0.f;
-            for (int qa = q_begin & ~3; qa < q_end; qa += 128 * VU) {
-                float pr[VU][4];
-                int c[VU][4];
-                float v[VU][4];
-#pragma unroll
-                for (int u = 0; u < VU; u++) {
-                    const int p = qa + 128 * u + 4 * lane;
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        pr[u][k] = 0.f;
-                        c[u][k] = -1;
-                        v[u][k] = 0.f;
-                    }
-                    if (p + 3 >= q_begin && p < q_end) {
-                        if (p + 3 < nnz_len) {
-                            const int4 c4 = ld_stream_i4(reinterpret_cast<const int4*>(col + p));
-                            const float4 v4 = ld_stream_f4(reinterpret_cast<const float4*>(val + p));
-                            c[u][0] = c4.x; c[u][1] = c4.y; c[u][2] = c4.z; c[u][3] = c4.w;
-                            v[u][0] = v4.x; v[u][1] = v4.y; v[u][2] = v4.z; v[u][3] = v4.w;
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < 4; k++) {
-                                c[u][k] = p + k < nnz_len ? __ldg(col + p + k) : 0;
-                                v[u][k] = p + k < nnz_len ? __ldg(val + p + k) : 0.f;
-                            }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < VU; u++) {
-                    const int p = qa + 128 * u + 4 * lane;
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        if (p + k >= q_begin && p + k < q_end) {
-                            float xv = 0.f;
-                            if ((unsigned)c[u][k] < (unsigned)ncols) xv = ld_keep_f(x + c[u][k]);
-                            else raise_fault(status, FAULT_OOB_LOAD);
-                            pr[u][k] = __fmul_rn(v[u][k], xv);  // the product rounds on its own
-                        }
-                    }
-#ifndef SPMV_NOFOLD
-                    *reinterpret_cast<float4*>(sp + skew4(128 * u + 4 * lane)) =
-                        make_float4(pr[u][0], pr[u][1], pr[u][2], pr[u][3]);
-#else  // timing experiment only (wrong results): no staging, no per-row fold
-                    s += (pr[u][0] + pr[u][1]) + (pr[u][2] + pr[u][3]);
-#endif
-                }
-#ifdef SPMV_NOFOLD
-                if (true) continue;
-#endif
-                __syncwarp();
-                const int lo = max(my_s, qa), hi = min(my_e, qa + 128 * VU);
-                s = fold_window<ASSOC, skew4>(s, lo, hi, qa, sp, lane);
-                __syncwarp();
-            }
-            if (active) y[row] = s;
-        }
-        ticket = nticket;
-        r0 = nr0;
-        r1 = nr1;
-    }
-}
-
-// Continuous-stream variant (PENCIL_SPMV_KERNEL=flow): the tile's non-zeros are streamed in
+// Continuous-stream executor: the tile's non-zeros are streamed in
 // full 4-aligned 128-element windows from its first to its last non-zero, independent of the
 // 32-row batches, and every batch overlapping a window is folded from it (a batch that ends
 // inside a window writes y and the next batch — prefetched — continues in the same window).
@@ -382,14 +250,11 @@ __global__ void __launch_bounds__(SPMV_THREADS, VU == 1 ? CTAS_PER_SM : 6) csr_v
 // DIST: fused SpMV -> all-gather (put_row); the warp fences its peer stores at system scope
 // before it retires, so the barrier that follows the launch publishes them.
 template <bool ASSOC, bool DIST = false>
-#ifndef FLOW_MINB
-#define FLOW_MINB CTAS_PER_SM
-#endif
-__global__ void __launch_bounds__(SPMV_THREADS, FLOW_MINB) csr_flow_kernel(
+__global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_flow_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
-    const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
-    unsigned* __restrict__ status, const PeerSet ps) {
+    const int* __restrict__ tile_row, int ntiles, const unsigned* __restrict__ plan,
+    unsigned* __restrict__ tk, unsigned* __restrict__ status, const PeerSet ps) {
     __shared__ __align__(16) float s_prod[WARPS_PER_CTA][128 + 16];
     if (plan[0]) {
         spmv_generic_t<DIST>(nrows, ncols, nnz_len, rowptr, col, val, x, y, status, ps);
@@ -402,10 +267,10 @@ __global__ void __launch_bounds__(SPMV_THREADS, FLOW_MINB) csr_flow_kernel(
     auto clampp = [&](int v) { return v < 0 ? 0 : (v > nnz_len ? nnz_len : v); };
     for (;;) {
         unsigned ticket = 0;
-        if (lane == 0) ticket = atomicAdd(&plan[1], 1u);
+        if (lane == 0) ticket = atomicAdd(tk, 1u);
         ticket = __shfl_sync(0xffffffffu, ticket, 0);
         if (ticket >= (unsigned)ntiles) {
-            if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
+            if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) *tk = 0;
             if (DIST) __threadfence_system();
             return;
         }
@@ -512,143 +377,9 @@ __global__ void __launch_bounds__(SPMV_THREADS, FLOW_MINB) csr_flow_kernel(
     }
 }
 
-// TMA-fed variant (experimental, PENCIL_SPMV_KERNEL=tma).  The LSU path above spends the SM's
-// L1TEX miss-request bandwidth (the limiter, ~1 request per clock) on both the x gathers AND
-// the col/val stream.  Here the stream comes in through the TMA engine instead: each warp
-// ring-buffers 128-non-zero chunks of col and val with 1-D bulk copies (cp.async.bulk,
-// mbarrier completion), so L1TEX only carries the gathers.  Chunks are cut at 4-aligned
-// absolute positions over the tile's contiguous non-zero range; 32-row batches are merged
-// against the chunk stream.  Measured slower than the LSU path (see TNBUF): per-warp
-// 512-byte bulk copies are too small for the TMA engine.
-#define TCH 128
-#define TNBUF 2  // chunks in flight per warp (measured: 2 -> 1.87 ms, 4 -> 3.78 ms at 2^24 rows)
-#define TMA_CTAS_PER_SM 8
-struct __align__(16) TmaWarpBufs {
-    int col[TNBUF][TCH];
-    float val[TNBUF][TCH];
-    float prod[TCH + TCH / 32];
-    uint64_t bar[TNBUF];
-};
-
-template <bool ASSOC>
-__global__ void __launch_bounds__(SPMV_THREADS, TMA_CTAS_PER_SM) csr_tma_kernel(
-    int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
-    const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
-    const int* __restrict__ tile_row, int ntiles, unsigned* __restrict__ plan,
-    unsigned* __restrict__ status) {
-    __shared__ TmaWarpBufs wb[WARPS_PER_CTA];
-    if (plan[0]) {
-        spmv_generic(nrows, ncols, nnz_len, rowptr, col, val, x, y, status);
-        return;
-    }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
-    TmaWarpBufs& B = wb[warp];
-    if (lane == 0) {
-        for (int b = 0; b < TNBUF; b++) bar_init(&B.bar[b], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    unsigned phases = 0;  // bit b = parity to wait for on buffer b
-    int bi = 0;           // buffer of the next chunk to consume (ring continues across tiles)
-    auto clampp = [&](int v) { return v < 0 ? 0 : (v > nnz_len ? nnz_len : v); };
-    for (;;) {
-        unsigned ticket = 0;
-        if (lane == 0) ticket = atomicAdd(&plan[1], 1u);
-        ticket = __shfl_sync(0xffffffffu, ticket, 0);
-        if (ticket >= (unsigned)ntiles) {
-            if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) plan[1] = 0;
-            return;
-        }
-        const int r0 = __ldg(tile_row + ticket), r1 = __ldg(tile_row + ticket + 1);
-        const int P0 = clampp(__ldg(rowptr + r0)), P1 = max(P0, clampp(__ldg(rowptr + r1)));
-        const int A0 = P0 & ~3;
-        const int nch = P1 > A0 ? (P1 - A0 + TCH - 1) / TCH : 0;
-        // chunk j = [A0 + j*TCH, min(A0 + (j+1)*TCH, P1)); bulk-copied when its 16-byte rounded
-        // extent stays inside the arrays, else read directly (only the array's last chunk)
-        auto chunk_tma_ok = [&](int j) {
-            const int c0 = A0 + j * TCH, cnt = min(TCH, P1 - c0);
-            return c0 + ((cnt + 3) & ~3) <= nnz_len;
-        };
-        auto issue = [&](int j, int b) {
-            const int c0 = A0 + j * TCH, cnt = min(TCH, P1 - c0);
-            const unsigned n4 = (unsigned)((cnt + 3) & ~3);
-            bar_expect_tx(&B.bar[b], n4 * 8u);
-            bulk_g2s(B.col[b], col + c0, n4 * 4u, &B.bar[b]);
-            bulk_g2s(B.val[b], val + c0, n4 * 4u, &B.bar[b]);
-        };
-        if (lane == 0)
-            for (int j = 0; j < TNBUF - 1 && j < nch; j++)
-                if (chunk_tma_ok(j)) issue(j, (bi + j) % TNBUF);
-
-        // 32-row batch state
-        int rb = r0, re = 0, row = 0, my_s = 0, my_e = 0, bend = 0;
-        bool active = false;
-        auto load_batch = [&]() {
-            re = min(rb + 32, r1);
-            row = rb + lane;
-            active = row < re;
-            my_s = active ? clampp(__ldg(rowptr + row)) : 0;
-            my_e = active ? max(my_s, clampp(__ldg(rowptr + row + 1))) : 0;
-            bend = clampp(__ldg(rowptr + re));
-        };
-        if (rb < r1) load_batch();
-        float s = 0.f;
-
-        for (int j = 0; j < nch; j++) {
-            const int c0 = A0 + j * TCH, cend = min(c0 + TCH, P1), cnt = cend - c0;
-            const bool tma = chunk_tma_ok(j);
-            if (j + TNBUF - 1 < nch && lane == 0 && chunk_tma_ok(j + TNBUF - 1))
-                issue(j + TNBUF - 1, (bi + TNBUF - 1) % TNBUF);
-            if (tma) {
-                bar_wait(&B.bar[bi], (phases >> bi) & 1u);
-                phases ^= 1u << bi;
-            }
-            int cc[TCH / 32];
-            float vv[TCH / 32], xv[TCH / 32];
-#pragma unroll
-            for (int u = 0; u < TCH / 32; u++) {
-                const int t = u * 32 + lane;
-                const bool in = t < cnt && c0 + t >= P0;
-                cc[u] = in ? (tma ? B.col[bi][t] : __ldg(col + c0 + t)) : 0;
-                vv[u] = in ? (tma ? B.val[bi][t] : __ldg(val + c0 + t)) : 0.f;
-                xv[u] = 0.f;
-                if (in) {
-                    if ((unsigned)cc[u] < (unsigned)ncols) xv[u] = ld_keep_f(x + cc[u]);
-                    else raise_fault(status, FAULT_OOB_LOAD);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < TCH / 32; u++) B.prod[skew(u * 32 + lane)] = __fmul_rn(vv[u], xv[u]);
-            __syncwarp();
-            for (;;) {  // fold every batch overlapping this chunk
-                const int lo = max(my_s, c0), hi = min(my_e, cend);
-                s = fold_window<ASSOC, skew>(s, lo, hi, c0, B.prod, lane);
-                if (rb < r1 && bend <= cend) {  // batch complete inside this chunk
-                    if (active) y[row] = s;
-                    rb += 32;
-                    s = 0.f;
-                    if (rb >= r1) break;
-                    load_batch();
-                    continue;
-                }
-                break;
-            }
-            __syncwarp();
-            bi = (bi + 1) % TNBUF;
-        }
-        while (rb < r1) {  // batches of empty rows past the last chunk (or tiles without non-zeros)
-            if (active) y[row] = s;
-            s = 0.f;
-            rb += 32;
-            if (rb < r1) load_batch();
-        }
-    }
-}
-
 int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
                     int ntiles, int* tile_row, unsigned* plan_flags, unsigned* status) {
-    cudaMemsetAsync(plan_flags, 0, 64, st);  // [0] non-monotone flag, [1] tile ticket counter
+    cudaMemsetAsync(plan_flags, 0, 64, st);  // [0] non-monotone flag
     long long blocks = ((long long)nrows + 1 + 255) / 256;
     if (blocks > PENCIL_NUM_SMS * 16) blocks = PENCIL_NUM_SMS * 16;
     csr_plan_kernel<<<(int)blocks, 256, 0, st>>>(nrows, nnz_len, rowptr, tile_nnz, ntiles, tile_row,
@@ -656,134 +387,46 @@ int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, 
     return (int)cudaGetLastError();
 }
 
+// Executor choice: the continuous-stream kernel when col / val are 16-byte aligned (1.25 ms at
+// 2^24 rows), else the scalar-load kernel (any alignment; 1.28 ms).  Measured and dropped (numbers
+// at 2^24 rows; the code is in the git history before the round-2 clean-up, commit be69d3c):
+//   * batch-aligned 128-bit kernel (windows restart at each 32-row batch): 1.265-1.273 ms; with 8
+//     non-zeros per lane: 1.355 ms;
+//   * TMA-fed col/val stream (per-warp 512-byte cp.async.bulk ring): 1.87 ms;
+//   * 3-stage software-pipelined LSU variant: 1.41 ms (the chunk/batch merge doubled the
+//     instruction count); cp.async double-buffered col/val prefetch: 2.43 ms (MIO-throttled);
+//   * register prefetch of the next chunk's column indices: 1.34 ms at 8 CTAs/SM, 1.39 at 7;
+//   * warp-specialised split (producer warps stream + gather into an mbarrier-handed smem ring,
+//     one consumer warp per CTA folds): 1.89 ms with 3 producers per consumer, 2.73 with 7;
+//   * cp.async.bulk.prefetch.L2 of the col/val windows 1 / 2 / 4 ahead: 1.38 / 1.45 / 1.41 ms;
+//   * an L2 persisting access-policy window over x: DRAM read 4.30 -> 2.70 GB per SpMV but no
+//     time gain (the request path, not DRAM, is the limit), and the set-aside L2 slowed the
+//     caller's next streaming kernels 2.2-2.4x;
+//   * window tile sizes 256 / 512 / 2048 non-zeros and chunks of 64 / 256: all slower than 1024 x 128.
+// `tk` is the per-(device, stream) ticket word (runtime.cpp): the kernels draw tiles from it and
+// the last warp re-arms it, so launches on one stream never share it with another stream's.
 int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                     const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                    const int* tile_row, int ntiles, unsigned* plan_flags, unsigned* status) {
+                    const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* tk,
+                    unsigned* status) {
     if (nrows <= 0) return 0;
     int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;  // persistent: at most one wave
     if (grid > PENCIL_NUM_SMS * CTAS_PER_SM) grid = PENCIL_NUM_SMS * CTAS_PER_SM;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(SPMV_THREADS);
-    cfg.stream = st;
-    // x is the only re-read operand (each entry ~nnz/ncols times): ask L2 to keep it resident
-    // against the 2 GB col/val stream (per-launch access-policy window, PENCIL_SPMV_PERSIST=1;
-    // by default the evict-last load policy alone does this).
-    cudaLaunchAttribute attr[1];
-    // opt-in: persisting lines outlive the launch and shrink L2 for the caller's next kernels
-    // (measured with the flow kernel: DRAM read 4.30 -> 2.70 GB per SpMV, but no time gain, and
-    // axpy / the stencils 2.2-2.4x slower afterwards — the set-aside L2, not the lines: a
-    // Normal-window re-read of x after the launch does not undo it)
-    struct PersistCfg {
-        int on;
-        size_t bytes;
-    };
-    static const PersistCfg pcfg = [] {  // read once (thread-safe static initialisation)
-        const char* e = getenv("PENCIL_SPMV_PERSIST");
-        PersistCfg c = {(e && e[0] == '1') ? 1 : 0, 0};
-        if (!c.on) return c;
-        int dev = 0, maxp = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        c.bytes = (size_t)maxp;
-        if (c.bytes) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c.bytes);
-        cudaGetLastError();
-        return c;
-    }();
-    const int persist = pcfg.on;
-    const size_t persist_bytes = pcfg.bytes;
-    size_t xbytes = (size_t)ncols * sizeof(float);
-    if (persist && persist_bytes && xbytes) {
-        int dev = 0, maxwin = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-        size_t win = xbytes < (size_t)maxwin ? xbytes : (size_t)maxwin;
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = (void*)x;
-        attr[0].val.accessPolicyWindow.num_bytes = win;
-        attr[0].val.accessPolicyWindow.hitRatio = win <= persist_bytes ? 1.0f : (float)persist_bytes / (float)win;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-    }
-    // executor: all-LSU (default; 1.34 ms at 2^24 rows) or the TMA-fed stream
-    // (PENCIL_SPMV_KERNEL=tma; 1.87 ms — 512-byte bulk copies cost more than they free).
-    // Also measured and dropped: a 3-stage software-pipelined LSU variant (1.41 ms — more
-    // gathers in flight, but the chunk/batch merge doubled the instruction count), and a
-    // cp.async double-buffered col/val prefetch (2.43 ms: MIO-throttled, 16-B LDGSTS per lane
-    // plus the smem re-read of col/val saturate the MIO queue the gathers also need), and a
-    // register prefetch of the next chunk's column indices (1.34 ms at 8 CTAs/SM, 1.39 at 7:
-    // the ~38% of stall samples on first use of col[] are the request path being full, not
-    // latency that more loads in flight could hide), and a warp-specialised split (producer
-    // warps stream + gather into an mbarrier-handed smem ring, one consumer warp per CTA folds
-    // the rows): 1.89 ms with 3 producers per consumer, 2.73 with 7, 4.57 with 1 — a fold is a
-    // chain of dependent smem adds that only many warps interleaved can hide; and an L2
-    // prefetch of the col/val windows 1 / 2 / 4 ahead through the TMA engine
-    // (cp.async.bulk.prefetch.L2, one lane, no registers): 1.38 / 1.45 / 1.41 ms.
-    // default: the continuous-stream kernel (1.250 ms at 2^24 rows; batch-aligned 128-bit
-    // kernel `vec` 1.265-1.273; scalar-load kernel `lsu` 1.282-1.288; PENCIL_SPMV_VU=2 with vec,
-    // 8 non-zeros per lane: 1.355; a mask-free path for interior windows: 8 B of spills, no gain)
-    static const int kernel_sel = [] {  // 0 flow, 1 vec, 2 lsu, 3 tma; read once
-        const char* e = getenv("PENCIL_SPMV_KERNEL");
-        if (!e) return 0;
-        if (!strcmp(e, "vec")) return 1;
-        if (!strcmp(e, "lsu")) return 2;
-        if (!strcmp(e, "tma")) return 3;
-        return 0;
-    }();
-    const int use_tma = kernel_sel == 3, use_flow = kernel_sel == 0, use_vec = kernel_sel <= 1;
-    if (use_flow && (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
+    if ((uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
         if (assoc)
-            return (int)cudaLaunchKernelEx(&cfg, csr_flow_kernel<true>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                           tile_row, ntiles, plan_flags, status, PeerSet{});
-        return (int)cudaLaunchKernelEx(&cfg, csr_flow_kernel<false>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                       tile_row, ntiles, plan_flags, status, PeerSet{});
-    }
-    cudaError_t e;
-    if (use_vec && (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
-        static const int vu = [] {
-            const char* w = getenv("PENCIL_SPMV_VU");
-            return (w && w[0] == '2') ? 2 : 1;
-        }();
-        if (vu == 2) {
-            if ((int)cfg.gridDim.x > PENCIL_NUM_SMS * 6) cfg.gridDim = dim3(PENCIL_NUM_SMS * 6);
-            if (assoc)
-                return (int)cudaLaunchKernelEx(&cfg, csr_vec_kernel<true, 2>, nrows, ncols, nnz_len, rowptr, col, val,
-                                               x, y, tile_row, ntiles, plan_flags, status);
-            return (int)cudaLaunchKernelEx(&cfg, csr_vec_kernel<false, 2>, nrows, ncols, nnz_len, rowptr, col, val, x,
-                                           y, tile_row, ntiles, plan_flags, status);
-        }
-        if (assoc)
-            return (int)cudaLaunchKernelEx(&cfg, csr_vec_kernel<true, 1>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                           tile_row, ntiles, plan_flags, status);
-        return (int)cudaLaunchKernelEx(&cfg, csr_vec_kernel<false, 1>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                       tile_row, ntiles, plan_flags, status);
-    }
-    if (use_tma && grid > PENCIL_NUM_SMS * TMA_CTAS_PER_SM) cfg.gridDim = dim3(PENCIL_NUM_SMS * TMA_CTAS_PER_SM);
-    if (use_tma) {
-        if (assoc)
-            e = cudaLaunchKernelEx(&cfg, csr_tma_kernel<true>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                   tile_row, ntiles, plan_flags, status);
+            csr_flow_kernel<true><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                                                 tile_row, ntiles, plan_flags, tk, status, PeerSet{});
         else
-            e = cudaLaunchKernelEx(&cfg, csr_tma_kernel<false>, nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                   tile_row, ntiles, plan_flags, status);
+            csr_flow_kernel<false><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                                                  tile_row, ntiles, plan_flags, tk, status, PeerSet{});
+    } else if (assoc) {
+        csr_stream_kernel<true, WCHUNK><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                                                       tile_row, ntiles, plan_flags, tk, status);
     } else {
-        // chunk of non-zeros per warp step (gathers in flight per lane = wch / 32);
-        // PENCIL_SPMV_WCHUNK = 64 | 128 | 256 (tuning knob, default 128)
-        static const int wch = [] {
-            const char* w = getenv("PENCIL_SPMV_WCHUNK");
-            const int v = w ? atoi(w) : 128;
-            return (v == 64 || v == 256) ? v : 128;
-        }();
-        if (wch == 256 && (int)cfg.gridDim.x > PENCIL_NUM_SMS * 6) cfg.gridDim = dim3(PENCIL_NUM_SMS * 6);
-#define CSR_LAUNCH(A, W) \
-    cudaLaunchKernelEx(&cfg, csr_stream_kernel<A, W>, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, status)
-        if (assoc) e = wch == 64 ? CSR_LAUNCH(true, 64) : (wch == 256 ? CSR_LAUNCH(true, 256) : CSR_LAUNCH(true, 128));
-        else e = wch == 64 ? CSR_LAUNCH(false, 64) : (wch == 256 ? CSR_LAUNCH(false, 256) : CSR_LAUNCH(false, 128));
-#undef CSR_LAUNCH
+        csr_stream_kernel<false, WCHUNK><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y,
+                                                                        tile_row, ntiles, plan_flags, tk, status);
     }
-    return (int)e;
+    return (int)cudaGetLastError();
 }
 
 // y rows -> peers (the distribution step on its own, for operands the fused kernel cannot take)
@@ -803,23 +446,23 @@ __global__ void dist_rows_kernel(int nrows, const float* __restrict__ y, const P
 
 int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                          const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                         const int* tile_row, int ntiles, unsigned* plan_flags, unsigned* status,
-                         const PeerSet& peers) {
+                         const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* tk,
+                         unsigned* status, const PeerSet& peers) {
     if (nrows <= 0) return 0;
     if ((uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
         int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
         if (grid > PENCIL_NUM_SMS * CTAS_PER_SM) grid = PENCIL_NUM_SMS * CTAS_PER_SM;
         if (assoc)
             csr_flow_kernel<true, true><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                                                       tile_row, ntiles, plan_flags, status, peers);
+                                                                       tile_row, ntiles, plan_flags, tk, status, peers);
         else
             csr_flow_kernel<false, true><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y,
-                                                                        tile_row, ntiles, plan_flags, status, peers);
+                                                                        tile_row, ntiles, plan_flags, tk, status, peers);
         return (int)cudaGetLastError();
     }
     // unaligned col/val: the regular executor, then the rows leave in a second launch
     int e = launch_csr_spmv(st, assoc, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles,
-                            plan_flags, status);
+                            plan_flags, tk, status);
     if (e) return e;
     long long blocks = ((long long)nrows + 255) / 256;
     if (blocks > PENCIL_NUM_SMS * 8) blocks = PENCIL_NUM_SMS * 8;
@@ -844,11 +487,4 @@ int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const
     return (int)cudaGetLastError();
 }
 
-int csr_tile_nnz() {  // PENCIL_SPMV_TILE overrides the plan window (tuning knob)
-    static const int t = [] {
-        const char* e = getenv("PENCIL_SPMV_TILE");
-        const int v = e ? atoi(e) : SPMV_TILE_NNZ;
-        return v < 32 ? SPMV_TILE_NNZ : v;
-    }();
-    return t;
-}
+int csr_tile_nnz() { return SPMV_TILE_NNZ; }

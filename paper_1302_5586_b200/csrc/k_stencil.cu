@@ -947,13 +947,12 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int
 }
 
 // SwarArgs from the separable factorisation, or false (signs, sums >= 2^16, clamp needed).
-// PENCIL_STENCIL_SWAR=0 disables the SWAR kernel (A/B measurement).
+// (A/B builds: tools/variant_build.sh compiles -DPENCIL_VARIANT_NO_SWAR into variants/.)
 bool swar_args(const StencilArgs& s, int scale, SwarArgs& a) {
-    static const bool on = [] {
-        const char* e = getenv("PENCIL_STENCIL_SWAR");
-        return !(e && e[0] == '0');
-    }();
-    if (!on || s.shift < 0 || s.shift > 8) return false;
+#ifdef PENCIL_VARIANT_NO_SWAR
+    return false;
+#endif
+    if (s.shift < 0 || s.shift > 8) return false;
     long long u[5], v[5], su = 0, sv = 0;
     bool uneg = true, vneg = true;
     for (int t = 0; t < 5; t++) {
@@ -980,25 +979,23 @@ bool swar_args(const StencilArgs& s, int scale, SwarArgs& a) {
     return true;
 }
 
-// PENCIL_STENCIL_SEP=0 disables the separable kernels (A/B measurement)
+// (A/B builds: -DPENCIL_VARIANT_NO_SEP disables the separable kernels)
 bool sep_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("PENCIL_STENCIL_SEP");
-        return !(e && e[0] == '0');
-    }();
-    return on;
+#ifdef PENCIL_VARIANT_NO_SEP
+    return false;
+#else
+    return true;
+#endif
 }
 
 // Taps supported on the radius-2 diamond (|di-2| + |dj-2| <= 2: the 12 corner taps zero — the
 // isotropic sharpen / Laplacian shapes): the DIA kernels skip the zero taps at compile time
 // (13 FFMA2 per pixel pair instead of 25; exact integer sums, so bit-identical).
-// PENCIL_STENCIL_DIA=0 disables them (A/B measurement).
+// (A/B builds: -DPENCIL_VARIANT_NO_DIA disables them.)
 bool diamond(const int* k) {
-    static const bool on = [] {
-        const char* e = getenv("PENCIL_STENCIL_DIA");
-        return !(e && e[0] == '0');
-    }();
-    if (!on) return false;
+#ifdef PENCIL_VARIANT_NO_DIA
+    return false;
+#endif
     for (int di = 0; di < 5; di++)
         for (int dj = 0; dj < 5; dj++)
             if (abs(di - 2) + abs(dj - 2) > 2 && k[di * 5 + dj]) return false;
@@ -1027,7 +1024,7 @@ unsigned* repair_flag_for(cudaStream_t st) {
 // 0 or +-2^e with -126 <= e <= 0 (no overflow; k*x exact unless it lands below 2^-126, which the
 // kernel's guard catches: pixels with 0 < |x| < 2^(-126 - emin) divert the launch to the exact
 // pass).  Returns the PF pattern (2: all 25 taps, 1: the 16 off the centre row/column, 0: none)
-// and the guard's limit.  PENCIL_STENCIL_PF=0 disables it (A/B measurement).
+// and the guard's limit.  (A/B builds: -DPENCIL_VARIANT_NO_PF disables it.)
 bool pow2_tap(float k, int& e) {
     unsigned u;
     memcpy(&u, &k, 4);
@@ -1040,11 +1037,9 @@ bool pow2_tap(float k, int& e) {
     return true;
 }
 int pow2_fusable(const float* k25, unsigned& lim) {
-    static const bool on = [] {
-        const char* e = getenv("PENCIL_STENCIL_PF");
-        return !(e && e[0] == '0');
-    }();
-    if (!on) return 0;
+#ifdef PENCIL_VARIANT_NO_PF
+    return 0;
+#endif
     for (int pf = 2; pf >= 1; pf--) {
         int emin = 0;
         bool ok = true;
@@ -1225,10 +1220,11 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
     const bool sep = sep_enabled() && separable(k25, a), dia = !sep && diamond(k25);
     SwarArgs sa;
     if (sep && w % 8 == 0 && (uintptr_t)img % 8 == 0 && (uintptr_t)out % 8 == 0 && swar_args(a, scale, sa)) {
-        static const int np_max = [] {
-            const char* e = getenv("PENCIL_STENCIL_SWAR_NP");
-            return e && atoi(e) == 8 ? 8 : 16;
-        }();
+#ifdef PENCIL_VARIANT_SWAR_NP8
+        const int np_max = 8;
+#else
+        const int np_max = 16;
+#endif
         const bool n16 = np_max == 16 && w % 16 == 0 && (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0;
         const int np = n16 ? 16 : 8;
         dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);

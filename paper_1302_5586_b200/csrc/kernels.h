@@ -22,9 +22,11 @@ int launch_axpy(cudaStream_t st, long long n, float a, const float* a_dev, const
 // k_spmv.cu
 int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
                     int ntiles, int* tile_row, unsigned* plan_flags, unsigned* status);
+// tk: the per-(device, stream) tile-ticket word (zero between launches; the kernels re-arm it)
 int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                     const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                    const int* tile_row, int ntiles, unsigned* plan_flags, unsigned* status);
+                    const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* tk,
+                    unsigned* status);
 int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const int* rowptr,
                        const int* col, const float* val, const float* x, float* y,
                        unsigned* status);
@@ -40,8 +42,8 @@ struct PeerSet {
 };
 int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                          const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                         const int* tile_row, int ntiles, unsigned* plan_flags, unsigned* status,
-                         const PeerSet& peers);
+                         const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* tk,
+                         unsigned* status, const PeerSet& peers);
 
 // k_conv.cu  (taps are host arrays, passed to the kernels by value)
 int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const float* k25,

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -74,20 +75,30 @@ int cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 // ------------------------------------------------------------------ device context
+// Device words a launch mutates are kept per (device, stream), so launches on different streams
+// never share them (re-entrant per (device set, stream)): the fault word the kernels
+// raise E-INTERP bits in, the SpMV tile-ticket word, and the gemv_t last-CTA counters.  Launches
+// on one stream are ordered, so the self-resetting words stay consistent between them.
+struct StreamState {
+    unsigned* words = nullptr;         // device: [0] fault word, [1] SpMV tile ticket
+    unsigned* host = nullptr;          // pinned mirror of the fault word
+    unsigned* gemv_t_counters = nullptr;
+    size_t gemv_t_counter_cap = 0;
+    std::mutex mu;                     // growth of the counters + the launch that uses them
+};
+
 struct DeviceCtx {
     int device = -1;
     cudaStream_t stream = nullptr;
     cudaMemPool_t pool = nullptr;
-    unsigned* status = nullptr;        // fault word (device)
-    unsigned* status_host = nullptr;   // pinned mirror
     float* dot_result = nullptr;
     double* dot_partial = nullptr;
     unsigned* dot_counter = nullptr;
-    unsigned* gemv_t_counters = nullptr;
-    size_t gemv_t_counter_cap = 0;
     float* l2_flush = nullptr;
     long long l2_flush_elems = 0;
     std::mutex mu;                     // serializes drop-in calls on this device
+    std::mutex smu;                    // guards `streams`
+    std::map<cudaStream_t, StreamState*> streams;
 };
 
 std::mutex g_ctx_mu;
@@ -112,9 +123,6 @@ int get_ctx(DeviceCtx** out) {
     CK(cudaMemPoolCreate(&c->pool, &props));
     unsigned long long thresh = ~0ull;  // keep freed blocks cached: the pool is the allocator cache
     CK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
-    CK(cudaMalloc(&c->status, 64));
-    CK(cudaMemset(c->status, 0, 64));
-    CK(cudaMallocHost(&c->status_host, 64));
     CK(cudaMalloc(&c->dot_result, 64));
     CK(cudaMalloc(&c->dot_partial, sizeof(double) * dot_partial_elems()));
     CK(cudaMalloc(&c->dot_counter, 64));
@@ -124,9 +132,35 @@ int get_ctx(DeviceCtx** out) {
     return ok();
 }
 
-// the device API takes the caller's stream literally (0 = the legacy default stream, the CUDA
-// convention, so launches order with the caller's other work); only the drop-in path uses the
-// library's own stream
+// the per-stream words of (c's device, st), created zeroed on first use
+int stream_state(DeviceCtx* c, cudaStream_t st, StreamState** out) {
+    std::lock_guard<std::mutex> lk(c->smu);
+    StreamState*& ss = c->streams[st];
+    if (!ss) {
+        StreamState* n = new StreamState();
+        if (cudaMalloc(&n->words, 64) != cudaSuccess || cudaMemset(n->words, 0, 64) != cudaSuccess ||
+            cudaMallocHost(&n->host, 64) != cudaSuccess) {
+            cudaFree(n->words);
+            delete n;
+            c->streams.erase(st);
+            return cuda_fail(cudaGetLastError(), "per-stream state");
+        }
+        ss = n;
+    }
+    *out = ss;
+    return PENCIL_OK;
+}
+unsigned* fault_word(DeviceCtx* c, cudaStream_t st) {
+    StreamState* ss = nullptr;
+    return stream_state(c, st, &ss) ? nullptr : ss->words;
+}
+unsigned* ticket_word(DeviceCtx* c, cudaStream_t st) {
+    StreamState* ss = nullptr;
+    return stream_state(c, st, &ss) ? nullptr : ss->words + 1;
+}
+
+// the stream's view of the device API (0 = the legacy default stream, the CUDA convention, so
+// launches order with the caller's other work); only the drop-in path uses the library's own stream
 cudaStream_t pick_stream(DeviceCtx*, pencil_stream_t s) { return (cudaStream_t)s; }
 
 int pool_alloc(DeviceCtx* c, cudaStream_t st, size_t bytes, void** p) {
@@ -139,23 +173,30 @@ void pool_free(cudaStream_t st, void* p) {
     if (p) cudaFreeAsync(p, st);
 }
 
-int ensure_gemv_t_counters(DeviceCtx* c, size_t n) {
-    if (c->gemv_t_counter_cap >= n) return PENCIL_OK;
-    if (c->gemv_t_counters) cudaFree(c->gemv_t_counters);
-    c->gemv_t_counters = nullptr;
+// gemv_t's last-CTA counters for stream st (caller holds ss->mu); grown stream-ordered: the new
+// block is zeroed on st and the old one freed on st after every launch that used it
+int ensure_gemv_t_counters(DeviceCtx* c, cudaStream_t st, StreamState* ss, size_t n) {
+    if (ss->gemv_t_counter_cap >= n) return PENCIL_OK;
     size_t cap = n < 1024 ? 1024 : n;
-    CK(cudaMalloc(&c->gemv_t_counters, cap * sizeof(unsigned)));
-    CK(cudaMemset(c->gemv_t_counters, 0, cap * sizeof(unsigned)));
-    c->gemv_t_counter_cap = cap;
+    unsigned* p = nullptr;
+    int r = pool_alloc(c, st, cap * sizeof(unsigned), (void**)&p);
+    if (r) return r;
+    CK(cudaMemsetAsync(p, 0, cap * sizeof(unsigned), st));
+    pool_free(st, ss->gemv_t_counters);
+    ss->gemv_t_counters = p;
+    ss->gemv_t_counter_cap = cap;
     return PENCIL_OK;
 }
 
-// read and clear the fault word (stream must be synchronized by the caller or here)
+// read and clear the fault word of stream st (synchronizes st)
 int collect_faults(DeviceCtx* c, cudaStream_t st) {
-    CK(cudaMemcpyAsync(c->status_host, c->status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemsetAsync(c->status, 0, sizeof(unsigned), st));
+    StreamState* ss = nullptr;
+    int r = stream_state(c, st, &ss);
+    if (r) return r;
+    CK(cudaMemcpyAsync(ss->host, ss->words, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(ss->words, 0, sizeof(unsigned), st));
     CK(cudaStreamSynchronize(st));
-    unsigned f = *c->status_host;
+    unsigned f = *ss->host;
     if (f & 1u) return fail(PENCIL_E_INTERP, "load index out of bounds (device fault word 0x%x)", f);
     if (f & 2u) return fail(PENCIL_E_INTERP, "CSR rowptr entry outside [0, nnz] (device fault word 0x%x)", f);
     if (f & 4u) return fail(PENCIL_E_INTERP, "division by zero");
@@ -249,7 +290,7 @@ struct CsrPlanImpl {
 };
 
 int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int* rowptr, int mode,
-                   CsrPlanImpl* p) {
+                   CsrPlanImpl* p, unsigned* fw = nullptr) {
     p->device = c->device;
     p->nrows = nrows;
     p->nnz = nnz;
@@ -262,8 +303,9 @@ int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int*
     r = pool_alloc(c, st, 64, (void**)&p->flags);
     if (r) return r;
     CK(cudaMemsetAsync(p->tile_row, 0, sizeof(int) * ((size_t)p->ntiles + 1), st));
-    return (int)launch_csr_plan(st, nrows, nnz, rowptr, p->tile_nnz, p->ntiles, p->tile_row, p->flags,
-                                c->status) == 0
+    if (!fw) fw = fault_word(c, st);
+    if (!fw) return g_status;
+    return (int)launch_csr_plan(st, nrows, nnz, rowptr, p->tile_nnz, p->ntiles, p->tile_row, p->flags, fw) == 0
                ? PENCIL_OK
                : fail(PENCIL_E_CUDA, "csr plan launch");
 }
@@ -323,7 +365,17 @@ int spmv_pipelined(int mode, int nrows, int ncols, int nnz, const int* rowptr, c
     int *drp = nullptr, *dcol = nullptr;
     float *dval = nullptr, *dx = nullptr, *dy = nullptr;
     CsrPlanImpl p;
-    auto release = [&]() {
+    // Every exit — the CK / launch-failure returns included — waits for the three streams (the
+    // per-block D2H copies into the caller's y may still be running) and frees the buffers.
+    struct Release {
+        std::function<void()> f;
+        bool done = false;
+        void operator()() {
+            if (!done) f();
+            done = true;
+        }
+        ~Release() { (*this)(); }
+    } release{[&]() {
         cudaStreamSynchronize(s1);
         cudaStreamSynchronize(s2);
         pool_free(s0, drp);
@@ -334,15 +386,15 @@ int spmv_pipelined(int mode, int nrows, int ncols, int nnz, const int* rowptr, c
         pool_free(s0, p.tile_row);
         pool_free(s0, p.flags);
         cudaStreamSynchronize(s0);
-    };
+    }};
+    unsigned *fw0 = fault_word(c, s0), *tk1 = ticket_word(c, s1);  // faults land in the call's word
+    if (!fw0 || !tk1) return g_status;
     if ((r = pool_alloc(c, s0, sizeof(int) * ((size_t)nrows + 1), (void**)&drp)) ||
         (r = pool_alloc(c, s0, sizeof(int) * (size_t)nnz, (void**)&dcol)) ||
         (r = pool_alloc(c, s0, sizeof(float) * (size_t)nnz, (void**)&dval)) ||
         (r = pool_alloc(c, s0, sizeof(float) * nz(ncols), (void**)&dx)) ||
-        (r = pool_alloc(c, s0, sizeof(float) * (size_t)nrows, (void**)&dy))) {
-        release();
+        (r = pool_alloc(c, s0, sizeof(float) * (size_t)nrows, (void**)&dy)))
         return r;
-    }
     // upload: rowptr first (the plan needs it), then x, then the col/val chunks in order
     CK(cudaMemcpyAsync(drp, rowptr, sizeof(int) * ((size_t)nrows + 1), cudaMemcpyHostToDevice, s0));
     CK(cudaEventRecord(pc->ev_rp, s0));
@@ -365,10 +417,7 @@ int spmv_pipelined(int mode, int nrows, int ncols, int nnz, const int* rowptr, c
     }
     // plan on the compute stream as soon as rowptr has landed; fetch the block boundaries
     CK(cudaStreamWaitEvent(s1, pc->ev_rp, 0));
-    if (csr_plan_build(c, s1, nrows, nnz, drp, mode, &p)) {
-        release();
-        return g_status;
-    }
+    if (csr_plan_build(c, s1, nrows, nnz, drp, mode, &p, fw0)) return g_status;
     const int K = p.ntiles < SPMV_PIPE_BLOCKS ? p.ntiles : SPMV_PIPE_BLOCKS;
     int* hb = pc->host_rows;
     CK(cudaMemcpyAsync(hb, p.flags, sizeof(int), cudaMemcpyDeviceToHost, s1));
@@ -380,7 +429,7 @@ int spmv_pipelined(int mode, int nrows, int ncols, int nnz, const int* rowptr, c
     CK(cudaStreamWaitEvent(s1, pc->ev_x, 0));
     auto launch = [&](long long t0, long long t1) {
         return launch_csr_spmv(s1, mode, nrows, ncols, nnz, drp, dcol, dval, dx, dy, p.tile_row + t0,
-                               (int)(t1 - t0), p.flags, c->status);
+                               (int)(t1 - t0), p.flags, tk1, fw0);
     };
     if (hb[0] != 0) {  // non-monotone rowptr: generic schedule after the whole upload
         CK(cudaStreamWaitEvent(s1, pc->ev_chunk[SPMV_PIPE_CHUNKS - 1], 0));
@@ -422,9 +471,11 @@ int spmv_common(int mode, int nrows, int ncols, int nnz, int* rowptr, int* col, 
     return dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
         CsrPlanImpl p;
         if (csr_plan_build(c, s, nrows, nnz, (const int*)st[0].dev, mode, &p)) return (int)cudaErrorUnknown;
+        unsigned *tk = ticket_word(c, s), *fw = fault_word(c, s);
+        if (!tk || !fw) return (int)cudaErrorMemoryAllocation;
         int e = launch_csr_spmv(s, mode, nrows, ncols, nnz, (const int*)st[0].dev, (const int*)st[1].dev,
                                 (const float*)st[2].dev, (const float*)st[3].dev, (float*)st[4].dev,
-                                p.tile_row, p.ntiles, p.flags, c->status);
+                                p.tile_row, p.ntiles, p.flags, tk, fw);
         pool_free(s, p.tile_row);
         pool_free(s, p.flags);
         return e;
@@ -465,12 +516,15 @@ void gemv_t(int m, int n, int lda, int incx, int incy, float alpha, float beta, 
     st[1] = {x, nullptr, sizeof(float) * nz((long long)m * incx), IN};
     st[2] = {y, nullptr, sizeof(float) * nz((long long)n * incy), INOUT};
     dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
-        if (ensure_gemv_t_counters(c, gemv_t_counter_elems(n))) return (int)cudaErrorMemoryAllocation;
+        StreamState* ss = nullptr;
+        if (stream_state(c, s, &ss)) return (int)cudaErrorMemoryAllocation;
+        std::lock_guard<std::mutex> lk(ss->mu);
+        if (ensure_gemv_t_counters(c, s, ss, gemv_t_counter_elems(n))) return (int)cudaErrorMemoryAllocation;
         float* part = nullptr;
         size_t pe = gemv_t_partial_elems(m, n);
         if (pe && pool_alloc(c, s, pe * sizeof(float), (void**)&part)) return (int)cudaErrorMemoryAllocation;
         int e = launch_gemv_t(s, m, n, lda, incx, incy, alpha, beta, (const float*)st[0].dev,
-                              (const float*)st[1].dev, (float*)st[2].dev, part, c->gemv_t_counters);
+                              (const float*)st[1].dev, (float*)st[2].dev, part, ss->gemv_t_counters);
         pool_free(s, part);
         return e;
     });
@@ -523,9 +577,11 @@ void spmv_row(int nrows, int ncols, int nnz, int i, int* rowptr, int* col, float
     st[3] = {x, nullptr, sizeof(float) * nz(ncols), IN};
     st[4] = {y, nullptr, sizeof(float) * nz(nrows), INOUT};
     dropin(st, [&](DeviceCtx* c, cudaStream_t s) {
+        unsigned* fw = fault_word(c, s);
+        if (!fw) return (int)cudaErrorMemoryAllocation;
         return launch_csr_generic(s, 1, ncols, nnz, (const int*)st[0].dev + i, (const int*)st[1].dev,
                                   (const float*)st[2].dev, (const float*)st[3].dev,
-                                  (float*)st[4].dev + i, c->status);
+                                  (float*)st[4].dev + i, fw);
     });
 }
 
@@ -621,11 +677,14 @@ int pencil_gemv_t_dev(pencil_stream_t s, int m, int n, int lda, int incx, int in
                       float beta, const float* A, const float* x, float* y) {
     if (m < 0 || n < 0 || lda < 0 || incx < 1 || incy < 1) return fail(PENCIL_E_ARG, "bad extent/stride");
     DEV_PROLOGUE;
-    if (ensure_gemv_t_counters(c, gemv_t_counter_elems(n))) return g_status;
+    StreamState* ss = nullptr;
+    if (stream_state(c, st, &ss)) return g_status;
+    std::lock_guard<std::mutex> lk(ss->mu);
+    if (ensure_gemv_t_counters(c, st, ss, gemv_t_counter_elems(n))) return g_status;
     float* part = nullptr;
     size_t pe = gemv_t_partial_elems(m, n);
     if (pe && pool_alloc(c, st, pe * sizeof(float), (void**)&part)) return g_status;
-    int e = launch_gemv_t(st, m, n, lda, incx, incy, alpha, beta, A, x, y, part, c->gemv_t_counters);
+    int e = launch_gemv_t(st, m, n, lda, incx, incy, alpha, beta, A, x, y, part, ss->gemv_t_counters);
     pool_free(st, part);
     DEV_RET(e);
 }
@@ -750,8 +809,10 @@ int pencil_spmv_dev(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr
                     const float* val, const float* x, float* y) {
     if (!plan) return fail(PENCIL_E_ARG, "null plan");
     DEV_PROLOGUE;
+    unsigned *tk = ticket_word(c, st), *fw = fault_word(c, st);
+    if (!tk || !fw) return g_status;
     DEV_RET(launch_csr_spmv(st, plan->mode, plan->nrows, plan->ncols, plan->nnz, rowptr, col, val, x, y,
-                            plan->tile_row, plan->ntiles, plan->flags, c->status));
+                            plan->tile_row, plan->ntiles, plan->flags, tk, fw));
 }
 
 int pencil_spmv_dev_dist(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr, const int* col,
@@ -768,8 +829,10 @@ int pencil_spmv_dev_dist(pencil_stream_t s, pencil_csr_plan_t plan, const int* r
     ps.n = npeers;
     ps.mc = mc;
     DEV_PROLOGUE;
+    unsigned *tk = ticket_word(c, st), *fw = fault_word(c, st);
+    if (!tk || !fw) return g_status;
     DEV_RET(launch_csr_spmv_dist(st, plan->mode, plan->nrows, plan->ncols, plan->nnz, rowptr, col, val, x, y,
-                                 plan->tile_row, plan->ntiles, plan->flags, c->status, ps));
+                                 plan->tile_row, plan->ntiles, plan->flags, tk, fw, ps));
 }
 
 int pencil_sync_status(pencil_stream_t s) {
@@ -820,3 +883,9 @@ int pencil_internal_fail(int status, const char* msg) {
     return status;
 }
 int pencil_internal_ok() { return ok(); }
+// the CSR executor with the mapper's reduction choice (dispatch.cpp): mode 1 = row sums
+// reassociated (the inner loop mapped to a REDUCE role), 0 = source order (SEQ role)
+int pencil_internal_spmv(int mode, int nrows, int ncols, int nnz, int* rowptr, int* col, float* val, float* x,
+                         float* y) {
+    return spmv_common(mode, nrows, ncols, nnz, rowptr, col, val, x, y);
+}

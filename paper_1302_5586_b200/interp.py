@@ -135,6 +135,10 @@ class CudaInterpreter:
             return ret.i
         return None
 
+    def last_kernel(self):
+        """The kernel variant the mapper chose for the last call (what was launched)."""
+        return (self._lib.pencil_runtime_last_kernel(self._rt) or b"").decode()
+
     def fp_reordered(self):
         """The `fp-reduction-reorders-results` flag of the last call (pencilc.cpp:157-161)."""
         return bool(self._lib.pencil_runtime_fp_reordered(self._rt))

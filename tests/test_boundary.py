@@ -137,8 +137,8 @@ def map_nest(fn, loops):
 
 
 EXPECTED = {"gemv": ("gemv_warp_per_row", 1), "gemv_t": ("gemv_t_colblock_splitk", 1),
-            "dot": ("dot_grid_tree", 1), "axpy": ("axpy_stream_f4", 0), "spmv_vec": ("csr_stream_assoc", 1),
-            "spmv_inline": ("csr_stream_seq", 0), "spmv": ("csr_stream_seq", 0), "spmv_row": ("csr_row_seq", 0),
+            "dot": ("dot_grid_tree", 1), "axpy": ("axpy_stream_f4", 0), "spmv_vec": ("csr_tiles_reassoc", 1),
+            "spmv_inline": ("csr_tiles_source_order", 0), "spmv": ("csr_tiles_source_order", 0), "spmv_row": ("csr_row_seq", 0),
             "conv5x5_u8": ("conv5x5_u8_sweep", 0), "conv5x5_f32": ("conv5x5_f32_sweep", 0),
             "gemm": ("gemm_tcgen05_3xtf32", 1)}
 
@@ -162,6 +162,12 @@ def test_mapper_rules():
     # a max-reduction is not reassociated by the + tree
     st, s = map_nest("dot", [(0, V["PARALLEL_WITH_REDUCTION"], "max")[:2] + ("M",)])
     assert st == 5 and s.reassociates == 0
+    # the CSR kernel follows the inner loop's role: a licensed + reduction reassociates, UNKNOWN
+    # keeps the source order (pencil_runtime_call launches the schedule's kernel, not the name)
+    st, s = map_nest("spmv_inline", [(0, V["ASSUMED_PARALLEL"], ""), (1, V["PARALLEL_WITH_REDUCTION"], "+")])
+    assert st == 0 and s.kernel.decode() == "csr_tiles_reassoc" and s.reassociates == 1
+    st, s = map_nest("spmv_vec", [(0, V["ASSUMED_PARALLEL"], ""), (1, V["SERIAL"], "")])
+    assert st == 0 and s.kernel.decode() == "csr_tiles_source_order" and s.reassociates == 0
     # third parallel loop becomes an in-thread tile loop
     st, s = map_nest("x", [(0, 0, ""), (1, 4, ""), (2, 0, "")])
     assert list(s.role[:3]) == [0, 0, 1] and s.grid_dims == 2

@@ -1,18 +1,19 @@
 #!/bin/bash
-# Build a tuning variant of the library: one CUDA source recompiled with extra -D flags, linked
-# with the regular objects into variants/<name>/libpencil_b200.so (select it at run time with
-# PENCIL_B200_LIB=...).  Usage: tools/variant_build.sh <name> <k_source.cu> -DMACRO=V ...
+# A/B builds of the product library: the shipped .so carries no run-time selection knobs; each
+# measured alternative is a compile-time variant built here into variants/<name>/ and loaded with
+# PENCIL_B200_LIB=variants/<name>/libpencil_b200.so (tools/ab_spmv.sh, bench.py).
+#   bash tools/variant_build.sh <name> -DPENCIL_VARIANT_...
+# Known variants:
+#   -DPENCIL_VARIANT_NO_SWAR     packed-byte stencil without the 16-bit SWAR kernel
+#   -DPENCIL_VARIANT_SWAR_NP8    SWAR kernel at 8 px per lane only
+#   -DPENCIL_VARIANT_NO_SEP      no separable (rank-1) stencil kernels
+#   -DPENCIL_VARIANT_NO_DIA      no diamond-support stencil kernels
+#   -DPENCIL_VARIANT_NO_PF       no power-of-two fused f32 taps
+#   -DPENCIL_VARIANT_L2_DIRTY    L2 flush without the discard (dirty lines left)
+#   -DPENCIL_VARIANT_GEMM_1SM    single-CTA gemm instead of the CTA pair
 set -e
-name=$1; src=$2; shift 2
+name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
-pkg=$root/paper_1302_5586_b200
-out=$root/variants/$name
-mkdir -p "$out"
-ARCH="-gencode arch=compute_100a,code=sm_100a"
-base=$(basename "$src" .cu)
-/usr/local/cuda/bin/nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr \
-    "$@" -c "$pkg/csrc/$base.cu" -o "$out/$base.o" 2> "$out/$base.ptxas.log"
-objs=$(ls $pkg/build/*.o | grep -v "/$base.o$")
-/usr/local/cuda/bin/nvcc $ARCH -shared -o "$out/libpencil_b200.so" $objs "$out/$base.o" -cudart static \
-    -Xlinker --no-undefined -lpthread -ldl -lrt
-echo "$out/libpencil_b200.so"
+make -s -j8 -C "$root/paper_1302_5586_b200" VARIANT="$*" BUILD="$root/variants/$name/build" \
+     LIBDIR="$root/variants/$name" "$root/variants/$name/libpencil_b200.so"
+echo "variants/$name/libpencil_b200.so ($*)"
