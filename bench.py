@@ -46,11 +46,19 @@ def peaks():
 
 
 def ncu_traffic(kernel):
+    """DRAM read + write bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json, tools/traffic_capture.py); exact name, else the name without
+    its template arguments; None when the kernel was not captured."""
     try:
         with open(NCU_SUMMARY) as f:
-            return json.load(f).get(kernel)
+            t = json.load(f)
     except Exception:
         return None
+    if kernel in t:
+        return t[kernel]
+    base = kernel.split("<")[0]
+    cands = [v for k, v in t.items() if k.split("<")[0] == base]
+    return cands[0] if len(cands) == 1 else None
 
 
 # ------------------------------------------------------------------ clocks sampling
@@ -99,6 +107,12 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ workloads (ours)
+def spmv_config(nrows, nnz, xm):
+    """The headline workload (BASELINE.json configs[1]) — the same dict on both arms."""
+    return {"workload": "CSR SpMV fp32 (spmv_vec), power-law rows 2^24 x 2^24, 16 nnz/row",
+            "nrows": nrows, "ncols": nrows, "nnz": nnz, "alpha": 1.5, "xm": round(xm, 4), "maxlen": 4096, "seed": 42}
+
+
 def spmv_bytes(nrows, ncols, nnz):
     return 8 * nnz + 4 * (nrows + 1) + 4 * nrows + 4 * ncols
 
@@ -203,10 +217,11 @@ def bench_spmv(args, torch, pb, rank, world, dist):
     algo = spmv_bytes(nrows, nrows, nnz)
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
            "ceiling_ms": ceil_ms if world == 1 else None,
-           "config": {"workload": "CSR SpMV fp32 (spmv_vec), power-law rows 2^24 x 2^24, 16 nnz/row",
-                      "nrows": nrows, "ncols": nrows, "nnz": nnz, "alpha": 1.5, "xm": round(xm, 4),
-                      "maxlen": 4096, "seed": 42, "schedule": "csr_flow_kernel, reassociated (persistent warps, 1024-nnz window tiles, continuous 128-bit col/val streams)",
-                      "l2": "L2 flushed between steps outside the per-step events (256 MiB fill, then its lines discarded: the step starts on a clean, empty L2); inputs 2.35 GB > L2"}}
+           "config": dict(spmv_config(nrows, nnz, xm),
+                          schedule="csr_flow_kernel, reassociated (persistent warps, 1024-nnz window tiles, "
+                                   "continuous 128-bit col/val streams)",
+                          l2="L2 flushed between steps outside the per-step events (256 MiB fill, then its lines "
+                             "discarded: the step starts on a clean, empty L2); inputs 2.35 GB > L2")}
     if world > 1:
         res["config"]["exchange"] = exchange
         if e2e:
@@ -217,25 +232,21 @@ def bench_spmv(args, torch, pb, rank, world, dist):
 
 
 def e2e_spmv(args, torch, pb, rowptr, col, val, x):
-    """drop-in C ABI, pinned host buffers, H2D + kernel + D2H per call (synchronous)."""
+    """drop-in C ABI on host buffers, H2D + plan + kernel + D2H per call (synchronous): pinned
+    (the headline `e2e`) and pageable (plain numpy, as a C program relinked from the emitted
+    OpenMP passes its malloc'd arrays) — median over the steps after one warm-up call."""
     nrows, nnz = rowptr.size - 1, col.size
-    pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
-    hrp, hcol, hval, hx = pin(rowptr), pin(col), pin(val), pin(x)
-    hy = torch.empty(nrows, dtype=torch.float32).pin_memory()
-    call = lambda: pb.dropin.spmv_vec(nrows, nrows, nnz, hrp, hcol, hval, hx, hy)  # noqa: E731
-    call()
-    ts = []
-    for _ in range(max(2, min(args.steps, 5))):
-        t0 = time.perf_counter()
-        call()
-        ts.append(time.perf_counter() - t0)
-    t = statistics.median(ts)
     algo = spmv_bytes(nrows, nrows, nnz)
-    import ctypes
-    h2d, d2h = ctypes.c_longlong(), ctypes.c_longlong()  # what the call moved over the link
-    pb.load().pencil_last_transfer_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
-    return {"value": algo / t / 1e9, "unit": "GB/s", "ms_per_call": t * 1e3, "h2d_bytes_per_step": h2d.value,
-            "d2h_bytes_per_step": d2h.value, "api": "spmv_vec (drop-in C ABI, pinned host arrays)"}
+
+    def mk(pinned):
+        hrp, hcol, hval, hx = (host_buf(torch, a, pinned) for a in (rowptr, col, val, x))
+        hy = host_buf(torch, np.zeros(nrows, np.float32), pinned)
+        return lambda: pb.dropin.spmv_vec(nrows, nrows, nnz, hrp, hcol, hval, hx, hy)
+    e = e2e_calls(torch, pb, mk, algo, "GB/s", "spmv_vec (drop-in C ABI on host arrays: pinned = the headline "
+                  "value, pageable beside it)", reps=max(2, min(args.steps, 5)))
+    if "ms_per_call" in e.get("pinned", {}):
+        e["ms_per_call"] = e["pinned"]["ms_per_call"]
+    return e
 
 
 def e2e_spmv_dist(args, torch, pb, sh, x, dist):
@@ -281,13 +292,82 @@ def e2e_spmv_dist(args, torch, pb, sh, x, dist):
                    % dist.get_backend()}
 
 
+# 3xTF32 = three tf32 MMAs per fp32 product; dense tf32 runs at half the bf16 rate, so the
+# measured-scaled 3xTF32 peak is bf16 / 6 (burst: the kernel timed alone; sustained: under the
+# 1 kW power cap in a long loop) — MEASURED_PEAKS.json bf16_tflops / bf16_tflops_sustained
+def tf32x3_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]) / 6.0, float(p.get("bf16_tflops_sustained", p["bf16_tflops"])) / 6.0, "measured"
+    except Exception:
+        return 1590.0 / 6.0, 1400.0 / 6.0, "fallback"
+
+
+def roofline(achieved, peak, unit, kernel, algo, bound="hbm", per="launch", **extra):
+    r = {"bound": bound, "kernel": kernel, "achieved": achieved, "peak": peak, "unit": unit,
+         "frac": achieved / peak if peak else None, "traffic": ncu_traffic(kernel)}
+    r["algorithmic_bytes_per_%s" % per if bound == "hbm" else "algorithmic_flops_per_%s" % per] = algo
+    if bound == "hbm":
+        r["frac_spec"] = achieved / SPEC_HBM_GBS
+    r.update(extra)
+    return r
+
+
+def bw_line(ms, nbytes, hbm, kernel, **extra):
+    gbs = nbytes / ms / 1e6
+    return dict({"ms": ms, "GB/s": gbs, "frac_hbm": gbs / hbm, "bytes": nbytes,
+                 "roofline": roofline(gbs, hbm, "GB/s", kernel, nbytes)}, **extra)
+
+
+def e2e_calls(torch, pb, make_call, metric_amount, unit, api, reps=2):
+    """The line's metric end to end through the library's public call on HOST arrays:
+    make_call(pinned) returns a no-argument call that runs the whole operation on pinned
+    (page-locked) or pageable (plain numpy) host buffers — H2D of the inputs, the kernel(s), D2H
+    of the outputs, synchronous.  Wall time around the call, median of `reps` after a warm-up;
+    the bytes each call moved over the link come from pencil_last_transfer_bytes (or from the
+    call itself when it copies through the device API: it returns (h2d, d2h))."""
+    lib = pb.load()
+    out = {"api": api}
+    for kind in ("pinned", "pageable"):
+        try:
+            call = make_call(kind == "pinned")
+            moved = call()
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                moved = call()
+                ts.append(time.perf_counter() - t0)
+            t = statistics.median(ts)
+            if moved is None:
+                h2d, d2h = ctypes.c_longlong(), ctypes.c_longlong()
+                lib.pencil_last_transfer_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
+                moved = (h2d.value, d2h.value)
+            out[kind] = {"value": metric_amount / t / (1e9 if unit in ("GB/s", "Gpix/s") else 1e12),
+                         "unit": unit, "ms_per_call": t * 1e3, "h2d_bytes_per_step": int(moved[0]),
+                         "d2h_bytes_per_step": int(moved[1])}
+        except Exception as e:  # noqa: BLE001 — one door's failure must not take the suite down
+            out[kind] = {"unavailable": str(e)[:200]}
+    if "value" in out.get("pinned", {}):
+        out.update({k: out["pinned"][k] for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step")})
+    return out
+
+
+def host_buf(torch, a, pinned):
+    """a (numpy) as a host buffer the drop-in call reads: a pinned torch copy, or a itself."""
+    return torch.from_numpy(a).pin_memory() if pinned else a
+
+
 def suite(args, torch, pb, hbm):
-    """Secondary configs of BASELINE.json, one line each (device-resident inputs)."""
+    """Secondary configs of BASELINE.json, one line each: device-resident kernel time (value +
+    roofline object) and the same metric end to end through the C ABI on host buffers (e2e:
+    pinned and pageable), with the reference CPU path beside it."""
     from paper_1302_5586_b200 import synth
     out = {}
     k, w = max(3, args.suite_steps), 3
     flush = lambda: pb.device.l2_flush()  # noqa: E731
     dev = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    no_e2e = args.no_e2e
 
     # gemv 8192^2 (configs[0])
     m = n = 8192
@@ -295,7 +375,12 @@ def suite(args, torch, pb, hbm):
     A, x, y = dev(hA), dev(hx), torch.zeros(m, device="cuda")
     ms = statistics.mean(run_steps(torch, lambda: pb.device.gemv(m, n, 1.0, 0.0, A, x, y), k, w, flush))
     b = 4 * (m * n + n + m)
-    out["gemv_8192"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm, "bytes": b}
+    out["gemv_8192"] = bw_line(ms, b, hbm, "gemv_kernel")
+    if not no_e2e:
+        def mk(pinned):
+            hA_, hx_, hy_ = (host_buf(torch, a, pinned) for a in (hA, hx, np.zeros(m, np.float32)))
+            return lambda: pb.dropin.gemv(m, n, 1.0, 0.0, hA_, hx_, hy_)
+        out["gemv_8192"]["e2e"] = e2e_calls(torch, pb, mk, b, "GB/s", "gemv (drop-in C ABI, host arrays)")
     hy = np.zeros(m, np.float32)
     cpu_ref(args, out["gemv_8192"], lambda L: L.gemv(m, n, 1.0, 0.0, P(hA), P(hx), P(hy)), b, "full config")
     del A, hA
@@ -319,68 +404,148 @@ def suite(args, torch, pb, hbm):
         pb.device.axpy_ptr(nv, r, xv, yv)
     ms_c = statistics.mean(run_steps(torch, chain, k, w, flush))
     bt, bd, ba = 4 * (m * n + m + n), 8 * nv, 12 * nv
-    out["gemv_t_16384_strided"] = {"ms": ms_t, "GB/s": bt / ms_t / 1e6, "frac_hbm": bt / ms_t / 1e6 / hbm}
-    out["dot_2e28"] = {"ms": ms_d, "GB/s": bd / ms_d / 1e6, "frac_hbm": bd / ms_d / 1e6 / hbm}
-    out["axpy_2e28"] = {"ms": ms_a, "GB/s": ba / ms_a / 1e6, "frac_hbm": ba / ms_a / 1e6 / hbm}
-    out["vobla_chain"] = {"ms": ms_c, "GB/s": (bt + bd + ba) / ms_c / 1e6,
-                          "frac_hbm": (bt + bd + ba) / ms_c / 1e6 / hbm, "bytes": bt + bd + ba}
+    out["gemv_t_16384_strided"] = bw_line(ms_t, bt, hbm, "gemv_t_kernel", view="lda 16384, incx 2, incy 3")
+    out["dot_2e28"] = bw_line(ms_d, bd, hbm, "dot_kernel")
+    out["axpy_2e28"] = bw_line(ms_a, ba, hbm, "axpy_kernel", scalar="device (the dot result)")
+    out["vobla_chain"] = bw_line(ms_c, bt + bd + ba, hbm, "gemv_t_kernel + dot_kernel + axpy_kernel",
+                                 chain="gemv_t -> dot -> axpy(dot), scalar stays on the device")
+    out["vobla_chain"]["roofline"]["traffic"] = None
     del A, xv, yv
+    if not no_e2e:
+        def mk_t(pinned):
+            a_, x_, y_ = (host_buf(torch, q, pinned) for q in (hA, hxt, hyt.copy()))
+            return lambda: pb.dropin.gemv_t(m, n, lda, 2, 3, 1.0, 0.0, a_, x_, y_)
+        out["gemv_t_16384_strided"]["e2e"] = e2e_calls(torch, pb, mk_t, bt, "GB/s", "gemv_t (drop-in C ABI)")
+
+        def mk_d(pinned):
+            x_, y_ = host_buf(torch, hxv, pinned), host_buf(torch, hyv, pinned)
+
+            def call():
+                pb.dropin.dot(nv, x_, y_)
+            return call
+        out["dot_2e28"]["e2e"] = e2e_calls(torch, pb, mk_d, bd, "GB/s", "dot (drop-in C ABI, float returned)")
+
+        def mk_a(pinned):
+            x_, y_ = host_buf(torch, hxv, pinned), host_buf(torch, hyv.copy(), pinned)
+            return lambda: pb.dropin.axpy(nv, 0.5, x_, y_)
+        out["axpy_2e28"]["e2e"] = e2e_calls(torch, pb, mk_a, ba, "GB/s", "axpy (drop-in C ABI)")
+
+        def mk_c(pinned):
+            a_, xt_, yt_ = (host_buf(torch, q, pinned) for q in (hA, hxt, hyt.copy()))
+            xv_, yv_ = host_buf(torch, hxv, pinned), host_buf(torch, hyv.copy(), pinned)
+            lib = pb.load()
+
+            def call():
+                moved = [0, 0]
+
+                def acc():
+                    h2d, d2h = ctypes.c_longlong(), ctypes.c_longlong()
+                    lib.pencil_last_transfer_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
+                    moved[0] += h2d.value
+                    moved[1] += d2h.value
+                pb.dropin.gemv_t(m, n, lda, 2, 3, 1.0, 0.0, a_, xt_, yt_)
+                acc()
+                d = pb.dropin.dot(nv, xv_, yv_)
+                acc()
+                pb.dropin.axpy(nv, d, xv_, yv_)
+                acc()
+                return moved
+            return call
+        out["vobla_chain"]["e2e"] = e2e_calls(torch, pb, mk_c, bt + bd + ba, "GB/s",
+                                              "gemv_t, dot, axpy(dot) as three drop-in calls (the scalar returns to the host)")
     cpu_ref(args, out["gemv_t_16384_strided"],
             lambda L: L.gemv_t(m, n, lda, 2, 3, 1.0, 0.0, P(hA), P(hxt), P(hyt)), bt, "full config")
     cpu_ref(args, out["dot_2e28"], lambda L: L.dot(nv, P(hxv), P(hyv)), bd, "full config")
     cpu_ref(args, out["axpy_2e28"], lambda L: L.axpy(nv, 0.5, P(hxv), P(hyv)), ba, "full config")
-    if "cpu_baseline" in out["gemv_t_16384_strided"]:
-        out["vobla_chain"]["cpu_baseline"] = {
+    if "ms" in out["gemv_t_16384_strided"].get("cpu_baseline", {}):
+        out["vobla_chain"]["cpu_baseline"] = dict(out["dot_2e28"]["cpu_baseline"], **{
             "ms": sum(out[q]["cpu_baseline"]["ms"] for q in ("gemv_t_16384_strided", "dot_2e28", "axpy_2e28")),
-            "cores": os.cpu_count(), "kind": "reference", "sample": "sum of the three calls above"}
+            "sample": "sum of the three calls above", "GB/s": None})
+        out["vobla_chain"]["cpu_baseline"]["GB/s"] = (bt + bd + ba) / out["vobla_chain"]["cpu_baseline"]["ms"] / 1e6
     del hA, hxv, hyv
 
     # 5x5 stencils 16384^2
     h = w_ = 16384
-    himg = synth.u8_i32(h * w_)
+    npx = h * w_
+    himg = synth.u8_i32(npx)
     img_i = dev(himg)
-    out_i = torch.empty(h * w_, dtype=torch.int32, device="cuda")
-    ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8(h, w_, 256, img_i, synth.BINOMIAL, out_i),
-                                   k, w, flush))
-    b = 8 * h * w_
-    out["conv5x5_u8_int32storage_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
-                                            "taps": "binomial (rank 1: separable kernel), scale 256"}
-    ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8(h, w_, 1, img_i, synth.SHARPEN, out_i),
-                                   k, w, flush))
-    out["conv5x5_u8_int32storage_16384_sharpen"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
-                                                    "taps": "signed sharpen (diamond support: DIA kernel, 13 of 25 taps nonzero), scale 1"}
+    out_i = torch.empty(npx, dtype=torch.int32, device="cuda")
+    b = 8 * npx
+    for name, taps, scale, kern, desc in (
+            ("conv5x5_u8_int32storage_16384", synth.BINOMIAL, 256, "stencil_ring_kernel<1, 1, 1, 0, 0>",
+             "binomial (rank 1: separable kernel), scale 256"),
+            ("conv5x5_u8_int32storage_16384_sharpen", synth.SHARPEN, 1, "stencil_ring_kernel<1, 1, 0, 1, 0>",
+             "signed sharpen (diamond support: DIA kernel, 13 of 25 taps nonzero), scale 1")):
+        ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8(h, w_, scale, img_i, taps, out_i),
+                                       k, w, flush))
+        out[name] = bw_line(ms, b, hbm, kern, taps=desc)
+        if not no_e2e:
+            def mk_u(pinned, taps=taps, scale=scale):
+                i_, o_ = host_buf(torch, himg, pinned), host_buf(torch, np.empty(npx, np.int32), pinned)
+                return lambda: pb.dropin.conv5x5_u8(h, w_, scale, i_, taps, o_)
+            out[name]["e2e"] = e2e_calls(torch, pb, mk_u, b, "GB/s", "conv5x5_u8 (drop-in C ABI, int32 pixels)")
     img8 = img_i.to(torch.uint8)
     del img_i, out_i
-    hout = np.empty(h * w_, np.int32)
-    kb = np.ascontiguousarray(synth.BINOMIAL, np.int32)
+    hout = np.empty(npx, np.int32)
+    kb, ks = np.ascontiguousarray(synth.BINOMIAL, np.int32), np.ascontiguousarray(synth.SHARPEN, np.int32)
     cpu_ref(args, out["conv5x5_u8_int32storage_16384"], lambda L: L.conv5x5_u8(h, w_, 256, P(himg), P(kb), P(hout)),
             b, "full config")
+    cpu_ref(args, out["conv5x5_u8_int32storage_16384_sharpen"],
+            lambda L: L.conv5x5_u8(h, w_, 1, P(himg), P(ks), P(hout)), b, "full config")
+    himg8 = himg.astype(np.uint8)
     del himg, hout
-    out8 = torch.empty(h * w_, dtype=torch.uint8, device="cuda")
-    ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8_bytes(h, w_, 256, img8, synth.BINOMIAL, out8),
-                                   k, w, flush))
-    b = 2 * h * w_
-    out["conv5x5_u8_bytes_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
-                                     "Gpix/s": h * w_ / ms / 1e6, "taps": "binomial, scale 256",
-                                     "kernel": "stencil_bytes_swar_kernel<16> (16-bit SWAR sums, 16 px per lane)"}
-    ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8_bytes(h, w_, 1, img8, synth.SHARPEN, out8),
-                                   k, w, flush))
-    out["conv5x5_u8_bytes_16384_sharpen"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
-                                             "Gpix/s": h * w_ / ms / 1e6, "taps": "signed sharpen (diamond support: DIA kernel), scale 1"}
-    del img8, out8
-    himgf = synth.f32(h * w_)
+    out8 = torch.empty(npx, dtype=torch.uint8, device="cuda")
+    b = 2 * npx
+    for name, taps, scale, kern, desc in (
+            ("conv5x5_u8_bytes_16384", synth.BINOMIAL, 256, "stencil_bytes_swar_kernel<16, 1>",
+             "binomial, scale 256 (16-bit SWAR sums, 16 px per lane)"),
+            ("conv5x5_u8_bytes_16384_sharpen", synth.SHARPEN, 1, "stencil_bytes_kernel<1, 0, 1>",
+             "signed sharpen (diamond support: DIA kernel), scale 1")):
+        ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8_bytes(h, w_, scale, img8, taps, out8),
+                                       k, w, flush))
+        out[name] = bw_line(ms, b, hbm, kern, taps=desc, **{"Gpix/s": npx / ms / 1e6})
+        if not no_e2e:
+            # packed bytes have no emitted-C door (PENCIL has no uint8): device API + the caller's copies
+            def mk_b(pinned, taps=taps, scale=scale):
+                i_ = host_buf(torch, himg8, pinned) if pinned else torch.from_numpy(himg8)
+                o_ = torch.empty(npx, dtype=torch.uint8).pin_memory() if pinned else torch.empty(npx, dtype=torch.uint8)
+                di, do = torch.empty(npx, dtype=torch.uint8, device="cuda"), torch.empty(npx, dtype=torch.uint8,
+                                                                                        device="cuda")
+
+                def call():
+                    di.copy_(i_, non_blocking=pinned)
+                    pb.device.conv5x5_u8_bytes(h, w_, scale, di, taps, do)
+                    o_.copy_(do, non_blocking=pinned)
+                    torch.cuda.synchronize()
+                    return npx, npx
+                return call
+            out[name]["e2e"] = e2e_calls(torch, pb, mk_b, b, "GB/s",
+                                         "pencil_conv5x5_u8_bytes_dev + the caller's H2D / D2H copies")
+    del img8, out8, himg8
+    himgf = synth.f32(npx)
     imgf = dev(himgf)
-    outf = torch.zeros(h * w_, device="cuda")
+    outf = torch.zeros(npx, device="cuda")
+    b = 8 * npx
     kf = (synth.BINOMIAL.astype(np.float32) / 256.0).astype(np.float32)
-    ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_f32(h, w_, imgf, kf, outf), k, w, flush))
-    b = 8 * h * w_
-    out["conv5x5_f32_16384"] = {"ms": ms, "GB/s": b / ms / 1e6, "frac_hbm": b / ms / 1e6 / hbm,
-                                "taps": "binomial / 256",
-                                "kernel": "stencil_ring_kernel<F32, PF 1> (16 power-of-two taps fused, exact)"}
+    kg = synth.f32(25, 99)  # generic taps (uniform [-0.5, 0.5), not powers of two): as-written rounding
+    for name, taps, kern, desc in (
+            ("conv5x5_f32_16384", kf, "stencil_ring_kernel<0, 0, 0, 0, 1>",
+             "binomial / 256 (16 power-of-two taps fused into one exact FMA each: PF 1)"),
+            ("conv5x5_f32_16384_generic_taps", kg, "stencil_ring_kernel<0, 0, 0, 0, 0>",
+             "25 generic fp32 taps (every product and sum rounds, as the emitted C)")):
+        ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_f32(h, w_, imgf, taps, outf), k, w, flush))
+        out[name] = bw_line(ms, b, hbm, kern, taps=desc)
+        if not no_e2e:
+            def mk_f(pinned, taps=taps):
+                i_, o_ = host_buf(torch, himgf, pinned), host_buf(torch, np.zeros(npx, np.float32), pinned)
+                return lambda: pb.dropin.conv5x5_f32(h, w_, i_, taps, o_)
+            out[name]["e2e"] = e2e_calls(torch, pb, mk_f, b, "GB/s", "conv5x5_f32 (drop-in C ABI)")
     del imgf, outf
-    houtf = np.zeros(h * w_, np.float32)
+    houtf = np.zeros(npx, np.float32)
     cpu_ref(args, out["conv5x5_f32_16384"], lambda L: L.conv5x5_f32(h, w_, P(himgf), P(kf), P(houtf)), b,
             "full config")
+    cpu_ref(args, out["conv5x5_f32_16384_generic_taps"], lambda L: L.conv5x5_f32(h, w_, P(himgf), P(kg), P(houtf)),
+            b, "full config")
     del himgf, houtf
 
     # OP2 mesh loop: the reference's edge->cell increment kernel on a random mesh
@@ -392,10 +557,28 @@ def suite(args, torch, pb, hbm):
     # gemm 16384^3 via 3xTF32
     try:
         m = n = kk = 16384
-        A, B, C = dev(synth.f32(m * kk)), dev(synth.f32(kk * n, 43)), torch.zeros(m * n, device="cuda")
-        ms = statistics.mean(run_steps(torch, lambda: pb.device.gemm(m, n, kk, 1.0, 0.0, A, B, C), 2, 1, flush))
-        out["gemm_16384_3xtf32"] = {"ms": ms, "TFLOP/s": 2 * m * n * kk / ms / 1e9}
+        hA, hB = synth.f32(m * kk), synth.f32(kk * n, 43)
+        A, B, C = dev(hA), dev(hB), torch.zeros(m * n, device="cuda")
+        ms = statistics.mean(run_steps(torch, lambda: pb.device.gemm(m, n, kk, 1.0, 0.0, A, B, C), 5, 3, flush))
+        flops = 2 * m * n * kk
+        tf = flops / ms / 1e9
+        burst, sustained, kind = tf32x3_peaks()
+        out["gemm_16384_3xtf32"] = {
+            "ms": ms, "TFLOP/s": tf,
+            "roofline": roofline(tf, burst, "TFLOP/s", "gemm_3xtf32_2sm_kernel", flops, bound="tensor",
+                                 peak_kind="%s: MEASURED_PEAKS bf16_tflops / 6 (3 tf32 MMAs per fp32 product, "
+                                           "tf32 at half the bf16 rate), burst" % kind,
+                                 frac_sustained=tf / sustained, peak_sustained=sustained,
+                                 frac_spec=tf / 375.0, peak_spec="375 TFLOP/s (1.125 PF dense tf32 / 3)")}
         del A, B, C
+        if not no_e2e:
+            def mk_g(pinned):
+                a_, b_, c_ = host_buf(torch, hA, pinned), host_buf(torch, hB, pinned), \
+                    host_buf(torch, np.zeros(m * n, np.float32), pinned)
+                return lambda: pb.dropin.gemm(m, n, kk, 1.0, 0.0, a_, b_, c_)
+            out["gemm_16384_3xtf32"]["e2e"] = e2e_calls(torch, pb, mk_g, flops, "TFLOP/s", "gemm (drop-in C ABI)",
+                                                        reps=1)
+        del hA, hB
         # CPU beside it: the emitted triple loop at 1024^3 (16384^3 would take ~an hour), as a rate
         q = 1024
         ha, hb, hc = synth.f32(q * q), synth.f32(q * q, 43), np.zeros(q * q, np.float32)
@@ -410,22 +593,54 @@ def P(a):
     return a.ctypes.data
 
 
+def host_cpu():
+    """The host the CPU baselines run on: model name and logical CPUs."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
+_CPU_LIB = {}
+
+
+def cpu_lib():
+    """The reference CPU path for timing: the C the reference's emit_openmp printed for the
+    fixtures (outer-loop pragma), compiled on THIS host with gcc -O3 -march=native -fopenmp
+    (oracle/Makefile `native`; the parity build keeps -march=x86-64-v3 -ffp-contract=off).
+    Falls back to the portable build when the native one cannot be compiled here."""
+    if "lib" not in _CPU_LIB:
+        import oracle
+        try:
+            _CPU_LIB["lib"], _CPU_LIB["build"] = oracle.emitted("native"), "gcc -O3 -march=native -fopenmp"
+        except Exception as e:  # noqa: BLE001
+            _CPU_LIB["lib"] = oracle.emitted("outer")
+            _CPU_LIB["build"] = "gcc -O3 -march=x86-64-v3 -fopenmp -ffp-contract=off (native build failed: %s)" % \
+                str(e)[:80]
+    return _CPU_LIB["lib"], _CPU_LIB["build"]
+
+
 def cpu_ref(args, entry, call, nbytes, sample, reps=2, flops=None):
     """CPU beside a suite line: the reference's emit_openmp C (outer-loop pragma,
     oracle/_ref) on the same host inputs, all host threads, best of `reps` after one warm-up."""
     if args.no_cpu_baseline:
         return
     try:
-        import oracle
-        lib = oracle.emitted("outer")
+        lib, build = cpu_lib()
         call(lib)
         best = float("inf")
         for _ in range(reps):
             t0 = time.perf_counter()
             call(lib)
             best = min(best, time.perf_counter() - t0)
-        cb = {"ms": best * 1e3, "cores": os.cpu_count(), "kind": "reference",
-              "sample": sample + ": emit_openmp C (outer pragma), gcc -O3 -fopenmp, best of %d" % reps}
+        cb = {"ms": best * 1e3, "cores": os.cpu_count(), "kind": "reference", "host": host_cpu()["model"],
+              "sample": sample + ": emit_openmp C (outer pragma), %s, best of %d" % (build, reps)}
         if nbytes:
             cb["GB/s"] = nbytes / best / 1e9
         if flops:
@@ -472,8 +687,7 @@ def op2_line(args, torch, pb, k, w):
 
 # ------------------------------------------------------------------ reference arm (CPU)
 def cpu_spmv(steps, warmup, rowptr, col, val, x):
-    import oracle
-    lib = oracle.emitted("outer")
+    lib, _ = cpu_lib()
     nrows = rowptr.size - 1
     y = np.zeros(nrows, np.float32)
     P = lambda a: a.ctypes.data  # noqa: E731
@@ -491,21 +705,22 @@ def cpu_spmv(steps, warmup, rowptr, col, val, x):
 def reference_arm(args):
     from paper_1302_5586_b200 import synth
     nrows = 1 << 24
-    rowptr, col, val, x, _ = synth.csr_powerlaw(nrows)
+    rowptr, col, val, x, xm = synth.csr_powerlaw(nrows)
     cores = os.cpu_count()
     ts = cpu_spmv(args.steps, min(args.warmup, 3), rowptr, col, val, x)
+    _, build = cpu_lib()
     t = statistics.mean(ts)
     algo = spmv_bytes(nrows, nrows, col.size)
     v = algo / t / 1e9
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "CSR SpMV fp32 (spmv_vec), power-law rows 2^24 x 2^24, 16 nnz/row",
-                       "nrows": nrows, "nnz": int(col.size), "parallelism": f"openmp x{os.environ.get('OMP_NUM_THREADS', cores)}"},
+            "config": dict(spmv_config(nrows, int(col.size), xm),
+                           parallelism=f"openmp x{os.environ.get('OMP_NUM_THREADS', cores)}"),
             "cpu_baseline": {"value": v, "unit": "GB/s", "cores": int(os.environ.get("OMP_NUM_THREADS", cores)),
-                             "kind": "reference",
+                             "kind": "reference", "host": host_cpu(),
                              "sample": "full matrix, one spmv_vec call per step: C emitted by the reference's "
-                                       "emit_openmp (outer-loop pragma), gcc -O3 -fopenmp"},
+                                       "emit_openmp (outer-loop pragma), %s" % build},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -588,9 +803,9 @@ def main():
                 ts = cpu_spmv(3, 1, rowptr, col, val, x)
                 t = statistics.mean(ts)
                 line["cpu_baseline"] = {"value": spmv_bytes(1 << 24, 1 << 24, col.size) / t / 1e9, "unit": "GB/s",
-                                        "cores": os.cpu_count(), "kind": "reference",
+                                        "cores": os.cpu_count(), "kind": "reference", "host": host_cpu(),
                                         "sample": "full matrix x3 calls of the emit_openmp C (outer pragma), "
-                                                  "gcc -O3 -fopenmp, all host threads"}
+                                                  "%s, all host threads" % cpu_lib()[1]}
                 # and on one thread (OMP_NUM_THREADS = 1 and = all cores)
                 gomp = ctypes.CDLL("libgomp.so.1")
                 gomp.omp_set_num_threads(1)

@@ -11,6 +11,7 @@ import this package.  It exposes three reference tiers for the PENCIL kernel fix
                    emit_openmp for the fixtures, compiled -fopenmp (the reference CPU path).
 """
 import ctypes
+import glob
 import os
 import subprocess
 import tempfile
@@ -218,10 +219,28 @@ _EMIT_SIGS = {
 }
 
 
+def build_native():
+    """The emitted outer-pragma C compiled for THIS host's CPU (gcc -O3 -march=native -fopenmp,
+    fp contraction left to gcc) — the timing build of the CPU baseline (bench.py).  Compiled
+    where it runs (the GPU box's host), from the emitted C under _ref/emitted/outer; the parity
+    build (_ref/libpencil_omp_outer.so) keeps -march=x86-64-v3 -ffp-contract=off."""
+    out = os.path.join(REF_DIR, "libpencil_omp_native.so")
+    src = sorted(glob.glob(os.path.join(REF_DIR, "emitted", "outer", "*.c")))
+    if not src:
+        raise FileNotFoundError("no emitted C under oracle/_ref/emitted/outer (build() the oracle first)")
+    defs = ["-DACCESS(x)=", "-DDEF(x)=(void)0", "-DUSE(x)=(void)0", "-DMAY_DEF(x)=(void)0"]
+    subprocess.run(["gcc", "-std=gnu11", "-O3", "-march=native", "-fopenmp", "-fPIC", "-shared"] + defs + src +
+                   ["-o", out], check=True, capture_output=True)
+    return out
+
+
 def emitted(variant="outer"):
     """ctypes handle of the emitted-OpenMP library ('outer': pragmas on outermost loops only —
-    the fast CPU baseline; 'annot': every annotated loop, as the fixtures are written)."""
+    the fast CPU baseline; 'annot': every annotated loop, as the fixtures are written; 'native':
+    'outer' compiled for this host's CPU, timing only, build_native)."""
     if variant not in _emitted:
+        if variant == "native":
+            build_native()
         path = os.path.join(REF_DIR, f"libpencil_omp_{variant}.so")
         lib = ctypes.CDLL(path)
         for name, (res, args) in _EMIT_SIGS.items():
