@@ -12,6 +12,10 @@
 //   lower   FILE                          OpenMP C           (lowering.hpp:29    emit_openmp)
 //   run     FILE FN  < argspec            Interpreter::call  (interp.hpp:49)
 //   signature FILE                        parameter kinds/types/extents (ast.hpp:133-151)
+//   summarize FILE FN [--param n=v] [--array a=v0,v1,..]
+//                                         access triple of a call FN(params...) under the
+//                                         binding (summaries.hpp:42 summarize_call): one JSON
+//                                         line per array parameter: read / must / may index sets
 //
 // `run` reads one argument per line from stdin, in parameter order:
 //   scalar int <v> | scalar float <v> | array <f32|i32> <path>
@@ -19,6 +23,7 @@
 // written back to <path>.out as float64 (f32 arrays) or int64 (i32 arrays) — the
 // interpreter holds every value as int64/fp64 (interp.hpp:12) — and the return
 // value is printed as `ret <int|float> <value>`.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -178,6 +183,61 @@ static int cmd_signature(const char* path) {
     return 0;
 }
 
+// summarize_call (summaries.cpp:635-648) of `fn` called with its own parameter names as the
+// argument expressions, under a concrete binding: per array parameter, the distinct indices read,
+// must-written and may-written, and whether any record had an index not evaluable (unknown).
+static int cmd_summarize(const char* path, const char* fn, int argc, char** argv) {
+    Ast ast = load_unit(path);
+    ParamBinding bind;
+    for (int i = 0; i + 1 < argc; i += 2) {
+        std::string flag = argv[i], kv = argv[i + 1];
+        auto eq = kv.find('=');
+        if (eq == std::string::npos) return 2;
+        std::string k = kv.substr(0, eq), v = kv.substr(eq + 1);
+        if (flag == "--param") {
+            bind.scalars[k] = std::stoll(v);
+        } else if (flag == "--array") {
+            std::vector<long long> vals;
+            std::stringstream ss(v);
+            std::string item;
+            while (std::getline(ss, item, ',')) vals.push_back(std::stoll(item));
+            bind.arrays[k] = vals;
+        } else {
+            return 2;
+        }
+    }
+    const FunctionDef* def = nullptr;
+    for (const auto& f : ast.functions)
+        if (f.name == fn) def = &f;
+    if (!def) return 2;
+    std::vector<ExprPtr> args;
+    for (const auto& p : def->params) args.push_back(make_var(p.name));
+    auto resolved = resolve_access_bindings(ast);
+    AccessResult res = summarize_call(ast, resolved, fn, args, bind);
+    for (const auto& p : def->params) {
+        if (p.kind != ParamKind::Array) continue;
+        auto idx = [&](const std::vector<AccessRecord>& recs, bool& unknown) {
+            std::vector<long long> out;
+            for (const auto& r : recs) {
+                if (r.array != p.name) continue;
+                if (r.unknown_index) unknown = true;
+                else if (!r.index.empty()) out.push_back(r.index[0]);
+            }
+            std::sort(out.begin(), out.end());
+            out.erase(std::unique(out.begin(), out.end()), out.end());
+            std::string js = "[";
+            for (size_t i = 0; i < out.size(); ++i) js += (i ? "," : "") + std::to_string(out[i]);
+            return js + "]";
+        };
+        bool unknown = false;
+        std::string r = idx(res.triple.read, unknown), m = idx(res.triple.must_write, unknown),
+                    y = idx(res.triple.may_write, unknown);
+        std::printf("{\"array\": \"%s\", \"read\": %s, \"must\": %s, \"may\": %s, \"unknown\": %s}\n",
+                    p.name.c_str(), r.c_str(), m.c_str(), y.c_str(), unknown ? "true" : "false");
+    }
+    return 0;
+}
+
 static int cmd_lower(const char* path) {
     Ast ast = load_unit(path);
     auto resolved = resolve_access_bindings(ast);
@@ -267,6 +327,7 @@ int main(int argc, char** argv) {
         if (cmd == "lower") return cmd_lower(argv[2]);
         if (cmd == "signature") return cmd_signature(argv[2]);
         if (cmd == "run" && argc >= 4) return cmd_run(argv[2], argv[3]);
+        if (cmd == "summarize" && argc >= 4) return cmd_summarize(argv[2], argv[3], argc - 4, argv + 4);
     } catch (const PencilError& e) {
         std::fprintf(stderr, "%s\n", e.what());
         return 1;

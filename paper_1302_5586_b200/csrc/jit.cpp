@@ -755,7 +755,37 @@ struct Summarizer {
                     if (p == pos.end() || !f.params[p->second].extent) return;
                     if (expr_str(*f.params[p->second].extent) == expr_str(*L->hi)) acc[p->second].must_all = true;
                 };
+                // the 2-level rectangle: for (i = 0; i < H; i++) for (j = 0; j < W; j++) p[i * W + j] = ...
+                // (unconditional store in the inner body) writes all of p[H * W]: the flattened
+                // row-major image nests (conv5x5_u8); the reference's must-write set is that rectangle
+                auto mark2 = [&](const pf::Stmt& L2, const pf::Expr& idx, const std::string& arr) {
+                    auto p = pos.find(arr);
+                    if (p == pos.end() || !f.params[p->second].extent) return;
+                    const pf::Expr& ext = *f.params[p->second].extent;
+                    if (idx.kind != pf::Expr::Binary || idx.bop != pf::Bin::Add || idx.args.size() != 2) return;
+                    const pf::Expr &rowt = *idx.args[0], &colt = *idx.args[1];
+                    if (colt.kind != pf::Expr::Var || colt.name != L2.name) return;
+                    if (rowt.kind != pf::Expr::Binary || rowt.bop != pf::Bin::Mul || rowt.args[0]->kind != pf::Expr::Var ||
+                        rowt.args[0]->name != L->name || expr_str(*rowt.args[1]) != expr_str(*L2.hi))
+                        return;
+                    if (ext.kind == pf::Expr::Binary && ext.bop == pf::Bin::Mul && ext.args.size() == 2 &&
+                        expr_str(*ext.args[0]) == expr_str(*L->hi) && expr_str(*ext.args[1]) == expr_str(*L2.hi))
+                        acc[p->second].must_all = true;
+                };
                 for (const pf::Stmt* s : body) {
+                    const pf::Stmt* L2 = s;
+                    while (L2->kind == pf::Stmt::Labeled) L2 = L2->loop_body.get();
+                    if (L2->kind == pf::Stmt::For && L2->lo->kind == pf::Expr::IntLit && L2->lo->ival == 0) {
+                        std::vector<const pf::Stmt*> inner;
+                        if (L2->loop_body->kind == pf::Stmt::Block)
+                            for (const auto& c : L2->loop_body->body) inner.push_back(c.get());
+                        else
+                            inner.push_back(L2->loop_body.get());
+                        for (const pf::Stmt* t : inner)
+                            if (t->kind == pf::Stmt::Assign && t->aop == pf::AOp::Set && t->lhs->kind == pf::Expr::Index &&
+                                t->lhs->args.size() == 1)
+                                mark2(*L2, *t->lhs->args[0], t->lhs->name);
+                    }
                     if (s->kind == pf::Stmt::Assign && s->aop == pf::AOp::Set && s->lhs->kind == pf::Expr::Index &&
                         s->lhs->args.size() == 1 && s->lhs->args[0]->kind == pf::Expr::Var &&
                         s->lhs->args[0]->name == L->name)

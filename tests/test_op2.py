@@ -162,6 +162,68 @@ def test_product_lowering_runs_to_the_reference_result():
             assert got.tolist() == CASES["multi_loop_levels"]["result"][d["name"]]
 
 
+# ------------------------------------------- the reference's own OP2 module (oracle/_ref/ref_op2_driver)
+REF_OP2 = os.path.join(os.path.dirname(oracle.REF_DRIVER), "ref_op2_driver")
+
+
+def ref_op2(cmd, doc_or_text):
+    if not os.path.exists(REF_OP2):
+        pytest.skip("oracle/_ref not built")
+    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+        f.write(doc_or_text if isinstance(doc_or_text, str) else json.dumps(doc_or_text))
+    try:
+        return subprocess.run([REF_OP2, cmd, f.name], capture_output=True, text=True)
+    finally:
+        os.unlink(f.name)
+
+
+ALL_DOCS = {**{k: v for k, v in CASES.items()}, **{"random_" + k: v for k, v in
+                                                    json.load(open(os.path.join(HERE, "golden", "op2_random.json"))).items()}}
+
+
+@pytest.mark.parametrize("name", sorted(ALL_DOCS))
+def test_lowering_equals_reference_lower_op2_model(name):
+    """The product's lowered unit (pencil_op2_lowered) is the reference's lower_op2_model
+    (op2.cpp:244-346) statement for statement: both in the reference printer's canonical form
+    (pretty_print of the parsed unit), compiled from the reference sources."""
+    doc = ALL_DOCS[name]["doc"]
+    ref = ref_op2("op2-lower", doc)
+    assert ref.returncode == 0, ref.stdout + ref.stderr
+    ref_unit = "".join(l + "\n" for l in ref.stdout.splitlines() if not l.startswith("driver "))
+    canon = ref_op2("canon", model(doc).lowered)
+    assert canon.returncode == 0
+    assert canon.stdout == ref_unit
+
+
+@pytest.mark.parametrize("name", sorted(ALL_DOCS))
+def test_golden_results_are_the_reference_interpret_op2_reference(name):
+    """The golden dats (and faults) the GPU tests compare against are what the reference's own
+    interpret_op2_reference (op2.cpp:388-429) computes for the model."""
+    case = ALL_DOCS[name]
+    r = ref_op2("op2-run", case["doc"])
+    if "fault" in case:
+        assert r.returncode == 3 and r.stdout.startswith("error E-INTERP"), r.stdout
+        return
+    assert r.returncode == 0, r.stdout + r.stderr
+    got = json.loads(r.stdout)
+    for k, v in case["result"].items():
+        assert got[k] == v, k
+
+
+@pytest.mark.parametrize("mutate,code", [
+    (lambda d: d["maps"][0].__setitem__("table", [0, 1, 1, 5]), "E-OP2-RANGE"),
+    (lambda d: d["dats"][0].__setitem__("data", [1, 2, 3, 4]), "E-OP2-SHAPE"),
+    (lambda d: d["par_loops"][0]["args"][1].__setitem__("offset", 2), "E-OP2-RANGE"),
+])
+def test_validation_codes_equal_reference(mutate, code):
+    """load_op2_model's stable codes (op2.hpp:79-81): the product and the reference agree."""
+    d = copy.deepcopy(CASES["mesh"]["doc"])
+    mutate(d)
+    r = ref_op2("op2-lower", d)
+    assert r.returncode == 3 and r.stdout.split()[1] == code, r.stdout
+    assert err_code(d) == code
+
+
 # ---------------------------------------------------------------- GPU
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", sorted(CASES))
