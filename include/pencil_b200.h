@@ -267,6 +267,20 @@ int pencil_jit_call_host(pencil_jit_t j, const char* fn, int nargs, const pencil
 int pencil_jit_last_traffic(pencil_jit_t j, long long* h2d, long long* d2h);
 /* Interpreter::set_rand_sequence: rand() returns these first, then the interpreter's LCG */
 int pencil_jit_set_rand_sequence(pencil_jit_t j, const long long* values, long long n);
+/* Interpreter::set_array with the interpreter's Value per element (int64 or fp64): element i is
+ * dbls[i] when is_double[i], else ints[i] (arrays may mix both, as the interpreter's do) */
+int pencil_jit_set_array_values(pencil_jit_t j, const char* name, const long long* ints, const double* dbls,
+                                const unsigned char* is_double, long long n);
+/* Interpreter::enable_trace / trace (interp.hpp:45-46, MemTrace interp.hpp:17-21): with the trace
+ * on, calls run every statement on one device thread in the interpreter's order and record each
+ * in-bounds load / store of a named store array (store name, flat index, is_write) — local arrays
+ * and *p dereferences are not recorded, as in the interpreter.  Records accumulate across calls. */
+int pencil_jit_enable_trace(pencil_jit_t j, int on);
+long long pencil_jit_trace_size(pencil_jit_t j);
+/* records [first, first + n): arrays[r] points at the store name (valid while j lives) */
+int pencil_jit_trace_get(pencil_jit_t j, long long first, long long n, const char** arrays, long long* index,
+                         unsigned char* is_write);
+int pencil_jit_trace_clear(pencil_jit_t j);
 /* OptiML construct (docs/op2-input.md; load_optiml_construct + lower_optiml, optiml.hpp:27-41)
  * lowered to a PENCIL unit for pencil_jit_load: returns the text length (cap 0 sizes the buffer)
  * or -1 (E-OPTIML-SHAPE / E-OPTIML-RANGE) */

@@ -106,6 +106,11 @@ SIGNATURES = {
     "pencil_jit_call_host": (c_int, [P, c_char_p, c_int, P, P, P, P, P]),
     "pencil_jit_last_traffic": (c_int, [P, ctypes.POINTER(c_ll), ctypes.POINTER(c_ll)]),
     "pencil_jit_set_rand_sequence": (c_int, [P, P, c_ll]),
+    "pencil_jit_set_array_values": (c_int, [P, c_char_p, P, P, P, c_ll]),
+    "pencil_jit_enable_trace": (c_int, [P, c_int]),
+    "pencil_jit_trace_size": (c_ll, [P]),
+    "pencil_jit_trace_get": (c_int, [P, c_ll, c_ll, P, P, P]),
+    "pencil_jit_trace_clear": (c_int, [P]),
     # introspection used by the boundary tests (not in the public header)
     "pencil_fixture_signature": (c_int, [c_char_p, c_char_p, c_int]),
     "pencil_fixture_count": (c_int, []),

@@ -11,7 +11,9 @@ typedef long long ll;
 typedef unsigned long long ull;
 struct V { ll i; double d; int isd; };
 struct LArr { V* p; ll n; };
-struct Ctx { unsigned* fault; ull* rng; const ll* rseq; ull* rpos; ll rseq_n; };
+struct Ctx { unsigned* fault; ull* rng; const ll* rseq; ull* rpos; ll rseq_n; ull* tr; };
+// tr (JIT trace mode, Interpreter::enable_trace, interp.hpp:45): tr[0] = records, tr[1] = capacity,
+// record r = (array id << 1 | is_write, index) at tr[2 + 2r]; null when tracing is off
 #define F_OOB_LOAD 1u
 #define F_OOB_STORE 2u
 #define F_DIV0 4u
@@ -117,15 +119,24 @@ static __device__ __forceinline__ V deref(const Ctx& c, const Arr& a) {
 )CUDA";
 
 const char* kArrTagged = R"CUDA(
-struct Arr { ll* p; unsigned char* tag; ll n; int inc; };
+struct Arr { ll* p; unsigned char* tag; ll n; int inc; int id; };
+// MemTrace (interp.hpp:17-21): an in-bounds load / store of a store array, in execution order
+// (trace mode runs every statement on one device thread, so the order is the interpreter's)
+static __device__ __forceinline__ void trace(const Ctx& c, int id, ll k, int w) {
+    if (!c.tr) return;
+    const ull r = atomicAdd(c.tr, 1ull);
+    if (r < c.tr[1]) { c.tr[2 + 2 * r] = ((ull)id << 1) | (ull)w; c.tr[3 + 2 * r] = (ull)k; }
+}
 static __device__ __forceinline__ V ld(const Ctx& c, const Arr& a, V idx) {
     ll k = as_i(c, idx);
     if (k < 0 || k >= a.n) { fault(c, F_OOB_LOAD); return VI(0); }
+    trace(c, a.id, k, 0);
     return a.tag[k] ? VD(__longlong_as_double(a.p[k])) : VI(a.p[k]);
 }
 static __device__ __forceinline__ void st(const Ctx& c, const Arr& a, V idx, int op, V rhs) {
     ll k = as_i(c, idx);
     if (k < 0 || k >= a.n) { fault(c, F_OOB_STORE); return; }
+    trace(c, a.id, k, 1);
     V old = a.tag[k] ? VD(__longlong_as_double(a.p[k])) : VI(a.p[k]);
     V v = op == 0 ? rhs : apply(c, op, old, rhs);
     a.p[k] = v.isd ? __double_as_longlong(v.d) : v.i;

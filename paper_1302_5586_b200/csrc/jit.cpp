@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <deque>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -310,7 +311,10 @@ struct Builder {
     const pf::Unit& u;
     pcg::Gen gen;
     std::ostringstream k;  // entry kernels
-    explicit Builder(const pf::Unit& unit) : u(unit), gen(unit) {}
+    // trace mode (Interpreter::enable_trace): every top-level statement a serial segment, so one
+    // device thread executes the call in the interpreter's order and the trace is its MemTrace
+    bool serial_only = false;
+    explicit Builder(const pf::Unit& unit, bool serial = false) : u(unit), gen(unit), serial_only(serial) {}
 
     pcg::Gen::Scope scope(const pf::Func& f) {
         pcg::Gen::Scope sc;
@@ -377,7 +381,7 @@ struct Builder {
             bool indep = has_independent(*s) || has_independent(*loop) ||
                          (loop->kind == pf::Stmt::For && !red && affine_parallel(*loop));
             // rand() is one sequential stream (Interpreter::next_rand): such loops stay in order
-            if (loop->kind == pf::Stmt::For && (indep || red) && !uses_rand(u, *loop)) {
+            if (!serial_only && loop->kind == pf::Stmt::For && (indep || red) && !uses_rand(u, *loop)) {
                 Seg g;
                 g.parallel = true;
                 g.stmts.push_back(loop);
@@ -833,6 +837,23 @@ struct pencil_jit {
     long long* d_rseq = nullptr;           // Interpreter::set_rand_sequence values
     unsigned long long* d_rpos = nullptr;  // next position in it
     long long rseq_n = 0;
+    // trace mode (Interpreter::enable_trace / trace, interp.hpp:45-46): the unit compiled again
+    // with every statement serial (t_*), a device record buffer, and the accumulated trace
+    std::vector<EntryFn> t_entries;
+    std::string t_src;
+    cudaLibrary_t t_lib = nullptr;
+    std::map<std::string, cudaKernel_t> t_kern;
+    bool trace_on = false;
+    unsigned long long* d_trace = nullptr;
+    long long trace_cap = 0;
+    std::deque<std::string> names;   // store name per array id (stable addresses)
+    std::map<std::string, int> name_id;
+    struct TraceRec {
+        int id;
+        long long index;
+        unsigned char write;
+    };
+    std::vector<TraceRec> trace;
 };
 
 namespace {
@@ -859,14 +880,30 @@ int setup(pencil_jit* J) {
     return PENCIL_OK;
 }
 
-int get_kernel(pencil_jit* J, const std::string& name, cudaKernel_t* out) {
-    auto it = J->kern.find(name);
-    if (it != J->kern.end()) {
+int get_kernel(pencil_jit* J, const std::string& name, cudaKernel_t* out, bool traced = false) {
+    auto& cache = traced ? J->t_kern : J->kern;
+    auto it = cache.find(name);
+    if (it != cache.end()) {
         *out = it->second;
         return PENCIL_OK;
     }
-    JCK(cudaLibraryGetKernel(out, J->lib, name.c_str()));
-    J->kern[name] = *out;
+    JCK(cudaLibraryGetKernel(out, traced ? J->t_lib : J->lib, name.c_str()));
+    cache[name] = *out;
+    return PENCIL_OK;
+}
+
+// the serial (trace-mode) build of the unit and its record buffer, compiled on first use
+int setup_trace(pencil_jit* J) {
+    int rc = setup(J);
+    if (rc) return rc;
+    if (J->t_lib) return PENCIL_OK;
+    std::vector<char> cubin;
+    std::string log;
+    rc = pcg::compile_cubin(J->t_src, cubin, log);
+    if (rc) return fail(rc, "E-CUDA: PENCIL unit compilation (trace mode) failed: " + log);
+    JCK(cudaLibraryLoadData(&J->t_lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    J->trace_cap = 1 << 20;  // records per call
+    JCK(cudaMalloc(&J->d_trace, (size_t)(2 + 2 * J->trace_cap) * 8));
     return PENCIL_OK;
 }
 
@@ -900,6 +937,10 @@ pencil_jit_t pencil_jit_load(const char* source) {
             J->entry_index[J->unit.fns[fi].name] = (int)fi;
         }
         J->src = b.gen.out.str() + kJitExtra + b.k.str();
+        Builder t(J->unit, true);
+        t.gen.unit(pcg::kArrTagged);
+        for (size_t fi = 0; fi < J->unit.fns.size(); fi++) J->t_entries.push_back(t.entry(J->unit.fns[fi], (int)fi));
+        J->t_src = t.gen.out.str() + kJitExtra + t.k.str();
     } catch (const pcg::GenError& e) {
         pencil_internal_fail(e.st, e.msg.c_str());
         delete J;
@@ -922,6 +963,8 @@ void pencil_jit_free(pencil_jit_t J) {
     if (J->d_rseq) cudaFree(J->d_rseq);
     if (J->d_rpos) cudaFree(J->d_rpos);
     if (J->lib) cudaLibraryUnload(J->lib);
+    if (J->t_lib) cudaLibraryUnload(J->t_lib);
+    if (J->d_trace) cudaFree(J->d_trace);
     if (J->stream) cudaStreamDestroy(J->stream);
     delete J;
 }
@@ -1021,11 +1064,12 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
     if (!J || !fn || (nargs && !args)) return fail(PENCIL_E_ARG, "E-ARG: null argument");
     auto it = J->entry_index.find(fn);
     if (it == J->entry_index.end()) return fail(PENCIL_E_INTERP, std::string("E-INTERP: no function named '") + fn + "'");
-    const EntryFn& E = J->entries[it->second];
+    const bool traced = J->trace_on;
+    const EntryFn& E = (traced ? J->t_entries : J->entries)[it->second];
     const pf::Func& f = *E.f;
     if ((size_t)nargs != f.params.size())
         return fail(PENCIL_E_INTERP, "E-INTERP: wrong argument count for '" + f.name + "'");
-    int rc = setup(J);
+    int rc = traced ? setup_trace(J) : setup(J);
     if (rc) return rc;
     // frame: scalar parameters from the call, locals 0 (slot K: return value)
     const size_t K = E.scalars.size();
@@ -1035,6 +1079,7 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
         unsigned char* tag;
         long long n;
         int inc;
+        int id;  // the store's name, for the trace (canonical name: arrays keep it through calls)
     };
     std::vector<DevArr> arrs;
     for (int i = 0; i < nargs; i++) {
@@ -1054,7 +1099,12 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
             auto s = J->store.find(args[i].array);
             if (s == J->store.end())
                 return fail(PENCIL_E_INTERP, std::string("E-INTERP: no array storage for '") + args[i].array + "'");
-            arrs.push_back({s->second.bits, s->second.tag, s->second.n, 0});
+            auto nid = J->name_id.find(s->first);
+            if (nid == J->name_id.end()) {
+                nid = J->name_id.emplace(s->first, (int)J->names.size()).first;
+                J->names.push_back(s->first);
+            }
+            arrs.push_back({s->second.bits, s->second.tag, s->second.n, 0, nid->second});
         }
     }
     static_assert(sizeof(HostV) == 24, "V layout");
@@ -1088,7 +1138,12 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
         const long long* rseq;
         unsigned long long* rpos;
         long long rseq_n;
-    } cx{J->d_fault, J->d_rng, J->d_rseq, J->d_rpos, J->rseq_n};
+        unsigned long long* tr;
+    } cx{J->d_fault, J->d_rng, J->d_rseq, J->d_rpos, J->rseq_n, traced ? J->d_trace : nullptr};
+    if (traced) {
+        const unsigned long long head[2] = {0ull, (unsigned long long)J->trace_cap};
+        JCK(cudaMemcpyAsync(J->d_trace, head, 16, cudaMemcpyHostToDevice, J->stream));
+    }
     const int fi = it->second;
     int returned = 0;
     for (size_t si = 0; si < E.segs.size() && !returned; si++) {
@@ -1098,7 +1153,7 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
         for (auto& a : arrs) common.push_back(&a);
         cudaKernel_t kk;
         if (!g.parallel) {
-            if ((rc = get_kernel(J, base, &kk))) return release(), rc;
+            if ((rc = get_kernel(J, base, &kk, traced))) return release(), rc;
             std::vector<void*> a = common;
             a.push_back(&d_flags);
             JCK(cudaLaunchKernel((const void*)kk, dim3(1), dim3(1), a.data(), 0, J->stream));
@@ -1106,7 +1161,7 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
         }
         // parallel segment: bounds, body, finish — all stream-ordered (the bounds stay on the
         // device; the body's grid is fixed and grid-strides over whatever range they hold)
-        if ((rc = get_kernel(J, base + "_b", &kk))) return release(), rc;
+        if ((rc = get_kernel(J, base + "_b", &kk, traced))) return release(), rc;
         {
             std::vector<void*> a = common;
             a.push_back(&d_bounds);
@@ -1115,7 +1170,7 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
         }
         const long long blocks = max_threads / 256;
         long long nthr = blocks * 256;
-        if ((rc = get_kernel(J, base + "_p", &kk))) return release(), rc;
+        if ((rc = get_kernel(J, base + "_p", &kk, traced))) return release(), rc;
         {
             std::vector<void*> a = common;
             a.push_back(&d_bounds);
@@ -1123,7 +1178,7 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
             a.push_back(&d_part);
             JCK(cudaLaunchKernel((const void*)kk, dim3((unsigned)blocks), dim3(256), a.data(), 0, J->stream));
         }
-        if ((rc = get_kernel(J, base + "_f", &kk))) return release(), rc;
+        if ((rc = get_kernel(J, base + "_f", &kk, traced))) return release(), rc;
         {
             std::vector<void*> a = {&cx, &d_frame, &d_out, &d_part, &nthr, &d_bounds, &d_flags};
             JCK(cudaLaunchKernel((const void*)kk, dim3(1), dim3(1024), a.data(), 0, J->stream));
@@ -1139,6 +1194,18 @@ int pencil_jit_call(pencil_jit_t J, const char* fn, int nargs, const pencil_arg*
     JCK(cudaMemcpyAsync(&fw, J->d_fault, 4, cudaMemcpyDeviceToHost, J->stream));
     JCK(cudaMemsetAsync(J->d_fault, 0, 4, J->stream));
     release();
+    if (traced) {  // append this call's records (the interpreter keeps its trace across calls)
+        unsigned long long cnt = 0;
+        JCK(cudaMemcpy(&cnt, J->d_trace, 8, cudaMemcpyDeviceToHost));
+        const unsigned long long keep = std::min<unsigned long long>(cnt, (unsigned long long)J->trace_cap);
+        std::vector<unsigned long long> rec(2 * keep);
+        if (keep) JCK(cudaMemcpy(rec.data(), J->d_trace + 2, 16 * keep, cudaMemcpyDeviceToHost));
+        for (unsigned long long r = 0; r < keep; r++)
+            J->trace.push_back({(int)(rec[2 * r] >> 1), (long long)rec[2 * r + 1], (unsigned char)(rec[2 * r] & 1)});
+        if (cnt > keep && !fw)
+            return fail(PENCIL_E_UNSUPPORTED, "E-UNSUPPORTED: trace of one call longer than " +
+                                                  std::to_string(J->trace_cap) + " records");
+    }
     if (ret) {
         ret->kind = rv.isd ? PENCIL_ARG_FLOAT : PENCIL_ARG_INT;
         ret->i = rv.isd ? 0 : rv.i;
@@ -1251,6 +1318,52 @@ int pencil_jit_last_traffic(pencil_jit_t J, long long* h2d, long long* d2h) {
     if (!J) return fail(PENCIL_E_ARG, "E-ARG: null unit");
     if (h2d) *h2d = J->h2d;
     if (d2h) *d2h = J->d2h;
+    return pencil_internal_ok();
+}
+
+// Interpreter::set_array with the interpreter's Value per element (interp.hpp:12: int64 or fp64):
+// is_double[i] selects dbls[i], else ints[i]
+int pencil_jit_set_array_values(pencil_jit_t J, const char* name, const long long* ints, const double* dbls,
+                                const unsigned char* is_double, long long n) {
+    if (!J || !name || n < 0 || (n && (!ints || !dbls || !is_double)))
+        return fail(PENCIL_E_ARG, "E-ARG: bad set_array_values argument");
+    int rc = pencil_jit_set_array(J, name, PENCIL_FLOAT64, dbls, n);  // allocates; tags below
+    if (rc || !n) return rc;
+    std::vector<long long> bits((size_t)n);
+    std::vector<unsigned char> tag((size_t)n);
+    for (long long i = 0; i < n; i++) {
+        tag[i] = is_double[i] ? 1 : 0;
+        if (tag[i]) memcpy(&bits[i], dbls + i, 8);
+        else bits[i] = ints[i];
+    }
+    StoreArr& a = J->store[name];
+    JCK(cudaMemcpy(a.bits, bits.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
+    JCK(cudaMemcpy(a.tag, tag.data(), (size_t)n, cudaMemcpyHostToDevice));
+    return pencil_internal_ok();
+}
+
+// Interpreter::enable_trace / trace (interp.hpp:45-46, MemTrace :17-21)
+int pencil_jit_enable_trace(pencil_jit_t J, int on) {
+    if (!J) return fail(PENCIL_E_ARG, "E-ARG: null unit");
+    J->trace_on = on != 0;
+    return pencil_internal_ok();
+}
+long long pencil_jit_trace_size(pencil_jit_t J) { return J ? (long long)J->trace.size() : -1; }
+int pencil_jit_trace_get(pencil_jit_t J, long long first, long long n, const char** arrays, long long* index,
+                         unsigned char* is_write) {
+    if (!J || first < 0 || n < 0 || first + n > (long long)J->trace.size())
+        return fail(PENCIL_E_ARG, "E-ARG: trace range out of bounds");
+    for (long long r = 0; r < n; r++) {
+        const auto& t = J->trace[(size_t)(first + r)];
+        if (arrays) arrays[r] = J->names[(size_t)t.id].c_str();
+        if (index) index[r] = t.index;
+        if (is_write) is_write[r] = t.write;
+    }
+    return pencil_internal_ok();
+}
+int pencil_jit_trace_clear(pencil_jit_t J) {
+    if (!J) return fail(PENCIL_E_ARG, "E-ARG: null unit");
+    J->trace.clear();
     return pencil_internal_ok();
 }
 

@@ -623,7 +623,8 @@ int launch_loop(pencil_op2_model* M, int li) {
         const long long* rseq;
         unsigned long long* rpos;
         long long rseq_n;
-    } cx{M->d_fault, M->d_rng, nullptr, nullptr, 0};
+        unsigned long long* tr;  // JIT trace buffer (unused here)
+    } cx{M->d_fault, M->d_rng, nullptr, nullptr, 0, nullptr};
     const int strat = M->strategy[li];
     std::vector<long long> nn(dats.size());
     std::vector<int> inc(dats.size());

@@ -242,6 +242,41 @@ JitUnit.access = _jit_access
 JitUnit.call_host = _jit_call_host
 
 
+def _jit_enable_trace(self, on=True):
+    """Interpreter::enable_trace (interp.hpp:45)."""
+    self._lib.pencil_jit_enable_trace(self._h, int(bool(on)))
+    check_status()
+
+
+def _jit_trace(self):
+    """Interpreter::trace (MemTrace list, interp.hpp:17-21): [(store name, [index], is_write)]."""
+    n = self._lib.pencil_jit_trace_size(self._h)
+    if n <= 0:
+        return []
+    names = (ctypes.c_char_p * n)()
+    idx = np.empty(n, np.int64)
+    w = np.empty(n, np.uint8)
+    self._lib.pencil_jit_trace_get(self._h, 0, n, names, idx.ctypes.data, w.ctypes.data)
+    check_status()
+    return [(names[i].decode(), [int(idx[i])], bool(w[i])) for i in range(n)]
+
+
+def _jit_set_array_values(self, name, values):
+    """Interpreter::set_array with mixed int / float elements (python ints and floats)."""
+    n = len(values)
+    isd = np.array([isinstance(v, float) for v in values], np.uint8)
+    ints = np.array([0 if isinstance(v, float) else int(v) for v in values], np.int64)
+    dbls = np.array([float(v) if isinstance(v, float) else 0.0 for v in values], np.float64)
+    self._lib.pencil_jit_set_array_values(self._h, name.encode(), ints.ctypes.data, dbls.ctypes.data,
+                                          isd.ctypes.data, n)
+    check_status()
+
+
+JitUnit.enable_trace = _jit_enable_trace
+JitUnit.trace = _jit_trace
+JitUnit.set_array_values = _jit_set_array_values
+
+
 def _jit_set_rand_sequence(self, values):
     """Interpreter::set_rand_sequence (interp.hpp:44): rand() pops these values first."""
     v = np.ascontiguousarray(values, dtype=np.int64)

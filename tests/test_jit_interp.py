@@ -113,3 +113,37 @@ def test_rand_sequence_survives_call_buffer_growth(cuda):
     u.call("take", [3, Arg.array("A")])
     assert u.get_array("A")[1][:3].tolist() == [5, 6, 7]
     del junk
+
+
+def test_trace_records_reads_and_writes_in_order(cuda):
+    """test_interp.cpp:64-80 through the Python surface of the JIT (enable_trace / trace)."""
+    from paper_1302_5586_b200 import Arg
+    u = unit("void copy(int n, int A[restrict const static n], int B[restrict const static n])\n"
+             "{\n  A[0] = B[1];\n}\n")
+    u.set_array("A", np.zeros(2, np.int32))
+    u.set_array("B", np.array([5, 6], np.int32))
+    u.enable_trace(True)
+    u.call("copy", [2, Arg.array("A"), Arg.array("B")])
+    assert u.trace() == [("B", [1], False), ("A", [0], True)]
+
+
+def test_trace_of_a_parallel_loop_is_sequential(cuda):
+    """With the trace on, an `independent` loop runs in the interpreter's order (one device thread):
+    records i = 0, 1, 2, ... each a read of x[i] then a write of y[i]; mixed int / float values
+    set with set_array_values keep their types."""
+    from paper_1302_5586_b200 import Arg
+    u = unit("void sc(int n, float x[restrict const static n], float y[restrict const static n])\n{\n"
+             "  #pragma pencil independent\n  for (int i = 0; i < n; i++) {\n    y[i] = x[i] * 2;\n  }\n}\n")
+    u.set_array_values("x", [1, 2.5, -3, 0.25])
+    u.set_array("y", np.zeros(4, np.float32))
+    u.enable_trace(True)
+    u.call("sc", [4, Arg.array("x"), Arg.array("y")])
+    exp = []
+    for i in range(4):
+        exp += [("x", [i], False), ("y", [i], True)]
+    assert u.trace() == exp
+    vals, ints, isd = u.get_array("y")
+    assert vals.tolist() == [2.0, 5.0, -6.0, 0.5] and isd.tolist() == [False, True, False, True]
+    u.enable_trace(False)
+    u.call("sc", [4, Arg.array("x"), Arg.array("y")])
+    assert len(u.trace()) == 8  # off: nothing recorded, earlier records kept
