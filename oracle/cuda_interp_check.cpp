@@ -206,11 +206,19 @@ int main(int argc, char** argv) {
                              Arg::array("A"), Arg::array("x"), Arg::array("y")});
             if (tref.empty()) tref = it.trace();
             else {
-                CHECK(it.trace().size() == tref.size(), "trace length");
+                auto show = [](const MemTrace& t) {
+                    return t.array + "[" + (t.index.empty() ? std::string("?") : std::to_string(t.index[0])) + "]" +
+                           (t.is_write ? "w" : "r");
+                };
+                std::string head;
+                for (size_t r = 0; r < 6 && r < tref.size() && r < it.trace().size(); ++r)
+                    head += " ref " + show(tref[r]) + " / got " + show(it.trace()[r]) + ";";
+                CHECK(it.trace().size() == tref.size(), "trace length " + std::to_string(it.trace().size()) + " vs " +
+                                                           std::to_string(tref.size()) + head);
                 for (size_t r = 0; r < tref.size(); ++r)
                     CHECK(it.trace()[r].array == tref[r].array && it.trace()[r].index == tref[r].index &&
                               it.trace()[r].is_write == tref[r].is_write,
-                          "trace record " + std::to_string(r));
+                          "trace record " + std::to_string(r) + head);
             }
         });
     }

@@ -3,7 +3,7 @@
 // (`V`) that reproduce the reference Interpreter's arithmetic (core/src/interp.cpp:7-83: int64
 // unless a double is involved, C-truncating `/` and `%`, both operands of `&&` / `||` evaluated,
 // faults for division by zero, out-of-bounds and non-integral indices).  Evaluation order is the
-// interpreter's (left operand first; an assignment's right-hand side before its subscript), made
+// reference binary's (right operand first, see Binary; an assignment's right-hand side before its subscript), made
 // explicit with one temporary per node.  Scalars are frame-wide like the interpreter's
 // (Frame::scalars, interp.cpp:86-92).  The array model (`Arr`, `ld`, `st`, `deref`) is supplied by
 // the caller's prelude: int64 storage with atomic OP_INC for OP2, tagged storage for the JIT.
@@ -156,10 +156,15 @@ struct Gen {
                 return r;
             }
             case pf::Expr::Binary: {
-                std::string a = ex(*e.args[0], sc, o, ind);
-                std::string a2 = t();
-                o << ind << "V " << a2 << " = " << a << ";\n";  // both sides always evaluated, left first
-                std::string b = ex(*e.args[1], sc, o, ind);
+                // Both sides always evaluated, the RIGHT one first: the reference evaluates a binary
+                // node as arith(op, eval(lhs), eval(rhs)) (interp.cpp:282), whose argument order C++
+                // leaves unspecified; g++ evaluates it right to left, so that is the reference's order
+                // (observable through rand() draws and the MemTrace of interp.hpp:17-21; checked by
+                // tests/test_jit_interp.py against oracle/_ref/ref_driver).
+                std::string b0 = ex(*e.args[1], sc, o, ind);
+                std::string b = t();
+                o << ind << "V " << b << " = " << b0 << ";\n";
+                std::string a2 = ex(*e.args[0], sc, o, ind);
                 std::string r = t();
                 static const char* fn[] = {"op_add", "op_sub", "op_mul", "op_div", "op_mod", "op_lt", "op_le",
                                            "op_gt",  "op_ge",  "op_eq",  "op_ne",  "op_and", "op_or"};

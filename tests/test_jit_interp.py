@@ -147,3 +147,22 @@ def test_trace_of_a_parallel_loop_is_sequential(cuda):
     u.enable_trace(False)
     u.call("sc", [4, Arg.array("x"), Arg.array("y")])
     assert len(u.trace()) == 8  # off: nothing recorded, earlier records kept
+
+
+def test_binary_operands_in_the_reference_binarys_order(cuda):
+    """The reference evaluates `a - b` as arith(op, eval(a), eval(b)), argument order unspecified in
+    C++; its g++ build evaluates b first.  rand() draws expose the order: the GPU result must equal
+    oracle/_ref/ref_driver's (the reference itself) for the LCG's first two draws."""
+    import os
+    import subprocess
+    import tempfile
+    import oracle
+    if not os.path.exists(oracle.REF_DRIVER):
+        pytest.skip("oracle/_ref not built")
+    src = "int f(void)\n{\n  int r;\n  r = rand() - 2 * rand();\n  return r;\n}\n"
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "u.pencil.c")
+        open(p, "w").write(src)
+        r = subprocess.run([oracle.REF_DRIVER, "run", p, "f"], input="", capture_output=True, text=True)
+    ref = int(r.stdout.split()[-1])
+    assert unit(src).call("f", []) == ref
