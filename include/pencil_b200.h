@@ -286,6 +286,71 @@ int pencil_jit_trace_clear(pencil_jit_t j);
  * or -1 (E-OPTIML-SHAPE / E-OPTIML-RANGE) */
 long long pencil_optiml_lower(const char* json_text, char* out, long long cap);
 
+/* ===== 10. Array and view descriptors ===========================
+ * A view is how a PENCIL nest addresses an array: element (i, j) of the view is
+ * base[offset + i * stride[0] + j * stride[1]] (rank 2) or base[offset + i * stride[0]] (rank 1).
+ * Views come from the symbolic affine forms of a nest's accesses (the reference's affine_form,
+ * depanalysis.cpp:163-193, keeps constant coefficients only; these keep scalar parameters such
+ * as lda / incx / incy and evaluate them under a call's bindings). */
+typedef struct {
+    void* base;            /* device pointer of the array's element 0 */
+    long long offset;      /* first element of the view */
+    int rank;              /* 1 or 2 */
+    int dtype;             /* pencil_dtype */
+    long long extent[2];   /* view shape */
+    long long stride[2];   /* elements between consecutive indices of each dimension */
+} pencil_view;
+/* one array access of a PENCIL function: its enclosing for-loops (outermost first) with their
+ * bounds under the binding, and index = offset + sum_d stride[d] * loop_d when affine */
+typedef struct {
+    char array[32];
+    int is_write;            /* a store (a compound store also yields a load record) */
+    int affine;              /* 0: the index is not affine in the enclosing loop variables */
+    int nloops;
+    char loop[8][16];
+    long long lo[8], hi[8];  /* loop bounds under the binding (hi exclusive) */
+    long long stride[8];     /* index change per unit step of loop d */
+    long long offset;        /* the index with every loop variable 0 */
+    char form[128];          /* symbolic form, e.g. "i*lda + j" */
+} pencil_access_form;
+/* accesses of `fn` in a PENCIL unit under scalar bindings names[k] = values[k]; returns the
+ * number of accesses (out holds the first cap) or -1 (E-ARG / E-SYNTAX) */
+int pencil_affine_accesses(const char* source, const char* fn, int nbind, const char* const* names,
+                           const long long* values, pencil_access_form* out, int cap);
+/* the library's own copy of a fixture unit ("gemv_t", "spmv", ... = pencil/<name>.pencil.c) */
+const char* pencil_fixture_source(const char* fixture);
+/* the sub-view [lo, hi) of dimension dim */
+int pencil_view_slice(const pencil_view* v, int dim, long long lo, long long hi, pencil_view* out);
+/* gemv_t over views (VOBLA: y(j) = alpha * sum_i A(i, j) x(i) + beta * y(j)): A rank 2 with unit
+ * stride along j, x / y rank 1 with positive strides; extents must agree (E-ARG), other
+ * layouts E-UNSUPPORTED.  pencil_gemv_t_dev and the drop-in gemv_t build these views from the
+ * fixture's affine forms (A[i*lda + j], x[i*incx], y[j*incy]) and call this. */
+int pencil_gemv_t_view_dev(pencil_stream_t s, float alpha, float beta, const pencil_view* A, const pencil_view* x,
+                           const pencil_view* y);
+/* the views of the gemv_t fixture's A, x, y for a call's scalars (from its affine forms) */
+int pencil_gemv_t_views(int m, int n, int lda, int incx, int incy, pencil_view views[3]);
+
+/* Array descriptors: element type, extent, a shard spec (ordered element ranges partitioning
+ * [0, n), one per rank / GPU; NULL bounds = one shard = the whole array), the device pointer of
+ * each shard this process can reach (its own memory, or a peer's NVLink mapping) and an optional
+ * host mirror.  The Interpreter mirror's named arrays (§4) and the multi-GPU shard classes keep
+ * their arrays in these. */
+typedef struct pencil_array* pencil_array_t;
+pencil_array_t pencil_array_create(int dtype, long long n, int nshards, const long long* bounds);
+void pencil_array_destroy(pencil_array_t a);
+int pencil_array_attach(pencil_array_t a, int shard, int device, void* ptr);
+int pencil_array_set_mirror(pencil_array_t a, void* host);
+int pencil_array_info(pencil_array_t a, int* dtype, long long* n, int* nshards, void** host);
+int pencil_array_shard(pencil_array_t a, int shard, long long* lo, long long* hi, int* device, void** ptr);
+/* the shard holding element index (-1 if outside) */
+int pencil_array_owner(pencil_array_t a, long long index);
+/* copy a shard's element range host mirror -> device (to_device 1) or back, on stream s */
+int pencil_array_sync(pencil_array_t a, int shard, int to_device, pencil_stream_t s);
+/* rank-1 unit-stride view of a shard's piece */
+int pencil_array_view(pencil_array_t a, int shard, pencil_view* out);
+/* the descriptor of an Interpreter-mirror named array (§4; owned by the runtime, NULL if unknown) */
+pencil_array_t pencil_runtime_array_desc(pencil_runtime_t rt, const char* name);
+
 #ifdef __cplusplus
 }
 #endif

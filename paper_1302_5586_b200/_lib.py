@@ -63,6 +63,22 @@ SIGNATURES = {
     "pencil_runtime_call": (c_int, [P, c_char_p, c_int, P, P]),
     "pencil_runtime_fp_reordered": (c_int, [P]),
     "pencil_runtime_last_kernel": (c_char_p, [P]),
+    "pencil_runtime_array_desc": (c_void_p, [P, c_char_p]),
+    # §10 descriptors
+    "pencil_affine_accesses": (c_int, [c_char_p, c_char_p, c_int, P, P, P, c_int]),
+    "pencil_fixture_source": (c_char_p, [c_char_p]),
+    "pencil_view_slice": (c_int, [P, c_int, c_ll, c_ll, P]),
+    "pencil_gemv_t_view_dev": (c_int, [P, c_float, c_float, P, P, P]),
+    "pencil_gemv_t_views": (c_int, [c_int, c_int, c_int, c_int, c_int, P]),
+    "pencil_array_create": (c_void_p, [c_int, c_ll, c_int, P]),
+    "pencil_array_destroy": (None, [P]),
+    "pencil_array_attach": (c_int, [P, c_int, c_int, P]),
+    "pencil_array_set_mirror": (c_int, [P, P]),
+    "pencil_array_info": (c_int, [P, P, P, P, P]),
+    "pencil_array_shard": (c_int, [P, c_int, P, P, P, P]),
+    "pencil_array_owner": (c_int, [P, c_ll]),
+    "pencil_array_sync": (c_int, [P, c_int, c_int, P]),
+    "pencil_array_view": (c_int, [P, c_int, P]),
     # §5 mapper
     "pencil_map_nest": (c_int, [c_char_p, P, c_int, P]),
     "pencil_fixture_verdicts": (c_int, [c_char_p, P, c_int]),
@@ -128,6 +144,17 @@ class pencil_value(ctypes.Structure):
 
 class pencil_loop_verdict(ctypes.Structure):
     _fields_ = [("loop_id", c_int), ("depth", c_int), ("verdict", c_int), ("reduction_op", ctypes.c_char)]
+
+
+class pencil_view(ctypes.Structure):
+    _fields_ = [("base", c_void_p), ("offset", c_ll), ("rank", c_int), ("dtype", c_int),
+                ("extent", c_ll * 2), ("stride", c_ll * 2)]
+
+
+class pencil_access_form(ctypes.Structure):
+    _fields_ = [("array", ctypes.c_char * 32), ("is_write", c_int), ("affine", c_int), ("nloops", c_int),
+                ("loop", (ctypes.c_char * 16) * 8), ("lo", c_ll * 8), ("hi", c_ll * 8), ("stride", c_ll * 8),
+                ("offset", c_ll), ("form", ctypes.c_char * 128)]
 
 
 class pencil_schedule(ctypes.Structure):

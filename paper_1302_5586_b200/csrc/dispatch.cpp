@@ -191,8 +191,12 @@ size_t dtype_size(int dt) {
 }  // namespace
 
 // ------------------------------------------------------------------ runtime objects
+// Named arrays (Interpreter::set_array / arrays(), interp.hpp:40-43) are array descriptors
+// (descriptors.cpp, include/pencil_b200.h §10): element type, extent, the device shard — one on
+// this runtime's device — and the runtime's ownership of that memory.
 struct pencil_runtime {
     struct DArray {
+        pencil_array_t desc = nullptr;
         int dtype = 0;
         long long n = 0;
         void* dev = nullptr;
@@ -220,8 +224,10 @@ pencil_runtime_t pencil_runtime_create(int device) {
 void pencil_runtime_destroy(pencil_runtime_t rt) {
     if (!rt) return;
     cudaSetDevice(rt->device);
-    for (auto& kv : rt->arrays)
+    for (auto& kv : rt->arrays) {
         if (kv.second.owned) cudaFree(kv.second.dev);
+        pencil_array_destroy(kv.second.desc);
+    }
     delete rt;
 }
 
@@ -229,6 +235,7 @@ static void drop_array(pencil_runtime_t rt, const std::string& name) {
     auto it = rt->arrays.find(name);
     if (it == rt->arrays.end()) return;
     if (it->second.owned) cudaFree(it->second.dev);
+    pencil_array_destroy(it->second.desc);
     rt->arrays.erase(it);
 }
 
@@ -243,8 +250,12 @@ int pencil_runtime_set_array(pencil_runtime_t rt, const char* name, int dtype, c
     size_t bytes = dtype_size(dtype) * (size_t)(n > 0 ? n : 1);
     if (cudaMalloc(&a.dev, bytes) != cudaSuccess) return PENCIL_E_NOMEM;
     a.owned = true;
-    if (n > 0 && host && cudaMemcpy(a.dev, host, dtype_size(dtype) * (size_t)n, cudaMemcpyHostToDevice) != cudaSuccess)
+    if (n > 0 && host && cudaMemcpy(a.dev, host, dtype_size(dtype) * (size_t)n, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(a.dev);
         return PENCIL_E_CUDA;
+    }
+    a.desc = pencil_array_create(dtype, n, 1, nullptr);
+    pencil_array_attach(a.desc, 0, rt->device, a.dev);
     rt->arrays[name] = a;
     return PENCIL_OK;
 }
@@ -257,6 +268,8 @@ int pencil_runtime_bind_array(pencil_runtime_t rt, const char* name, int dtype, 
     a.n = n;
     a.dev = dev;
     a.owned = false;
+    a.desc = pencil_array_create(dtype, n, 1, nullptr);
+    pencil_array_attach(a.desc, 0, rt->device, a.dev);
     rt->arrays[name] = a;
     return PENCIL_OK;
 }
@@ -284,6 +297,12 @@ int pencil_runtime_array_info(pencil_runtime_t rt, const char* name, int* dtype,
 }
 
 int pencil_runtime_fp_reordered(pencil_runtime_t rt) { return rt ? rt->fp_reordered : 0; }
+
+pencil_array_t pencil_runtime_array_desc(pencil_runtime_t rt, const char* name) {
+    if (!rt || !name) return nullptr;
+    auto it = rt->arrays.find(name);
+    return it == rt->arrays.end() ? nullptr : it->second.desc;
+}
 
 const char* pencil_runtime_last_message(void) { return d_msg; }
 

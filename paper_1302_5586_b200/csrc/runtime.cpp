@@ -188,6 +188,33 @@ int ensure_gemv_t_counters(DeviceCtx* c, cudaStream_t st, StreamState* ss, size_
     return PENCIL_OK;
 }
 
+// gemv_t over views: A (rank 2, unit stride along j), x, y (rank 1) -> the strided kernel
+int gemv_t_views_launch(DeviceCtx* c, cudaStream_t st, float alpha, float beta, const pencil_view& A,
+                        const pencil_view& x, const pencil_view& y) {
+    if (A.rank != 2 || x.rank != 1 || y.rank != 1 || A.extent[0] != x.extent[0] || A.extent[1] != y.extent[0] ||
+        A.extent[0] < 0 || A.extent[1] < 0)
+        return fail(PENCIL_E_ARG, "gemv_t views: A must be m x n, x of m, y of n");
+    if (A.stride[1] != 1 || A.stride[0] < 0 || A.stride[0] > 0x7fffffff || x.stride[0] < 1 ||
+        x.stride[0] > 0x7fffffff || y.stride[0] < 1 || y.stride[0] > 0x7fffffff || A.extent[0] > 0x7fffffff ||
+        A.extent[1] > 0x7fffffff)
+        return fail(PENCIL_E_UNSUPPORTED, "gemv_t views: needs unit stride along j and positive 32-bit strides");
+    const int m = (int)A.extent[0], n = (int)A.extent[1];
+    if (n == 0) return PENCIL_OK;
+    StreamState* ss = nullptr;
+    int r = stream_state(c, st, &ss);
+    if (r) return r;
+    std::lock_guard<std::mutex> lk(ss->mu);
+    if ((r = ensure_gemv_t_counters(c, st, ss, gemv_t_counter_elems(n)))) return r;
+    float* part = nullptr;
+    size_t pe = gemv_t_partial_elems(m, n);
+    if (pe && (r = pool_alloc(c, st, pe * sizeof(float), (void**)&part))) return r;
+    const int e = launch_gemv_t(st, m, n, (int)A.stride[0], (int)x.stride[0], (int)y.stride[0], alpha, beta,
+                                (const float*)A.base + A.offset, (const float*)x.base + x.offset,
+                                (float*)y.base + y.offset, part, ss->gemv_t_counters);
+    pool_free(st, part);
+    return e ? cuda_fail((cudaError_t)e, "gemv_t launch") : PENCIL_OK;
+}
+
 // read and clear the fault word of stream st (synchronizes st)
 int collect_faults(DeviceCtx* c, cudaStream_t st) {
     StreamState* ss = nullptr;
@@ -515,18 +542,12 @@ void gemv_t(int m, int n, int lda, int incx, int incy, float alpha, float beta, 
     st[0] = {A, nullptr, sizeof(float) * nz((long long)m * lda), IN};
     st[1] = {x, nullptr, sizeof(float) * nz((long long)m * incx), IN};
     st[2] = {y, nullptr, sizeof(float) * nz((long long)n * incy), INOUT};
+    // the views of the fixture's accesses (A[i*lda + j], x[i*incx], y[j*incy]) for these scalars
+    pencil_view v[3];
+    if (pencil_gemv_t_views(m, n, lda, incx, incy, v)) return;
     dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
-        StreamState* ss = nullptr;
-        if (stream_state(c, s, &ss)) return (int)cudaErrorMemoryAllocation;
-        std::lock_guard<std::mutex> lk(ss->mu);
-        if (ensure_gemv_t_counters(c, s, ss, gemv_t_counter_elems(n))) return (int)cudaErrorMemoryAllocation;
-        float* part = nullptr;
-        size_t pe = gemv_t_partial_elems(m, n);
-        if (pe && pool_alloc(c, s, pe * sizeof(float), (void**)&part)) return (int)cudaErrorMemoryAllocation;
-        int e = launch_gemv_t(s, m, n, lda, incx, incy, alpha, beta, (const float*)st[0].dev,
-                              (const float*)st[1].dev, (float*)st[2].dev, part, ss->gemv_t_counters);
-        pool_free(s, part);
-        return e;
+        for (int q = 0; q < 3; q++) v[q].base = st[q].dev;
+        return gemv_t_views_launch(c, s, alpha, beta, v[0], v[1], v[2]) ? (int)cudaErrorInvalidValue : 0;
     });
 }
 
@@ -677,16 +698,50 @@ int pencil_gemv_t_dev(pencil_stream_t s, int m, int n, int lda, int incx, int in
                       float beta, const float* A, const float* x, float* y) {
     if (m < 0 || n < 0 || lda < 0 || incx < 1 || incy < 1) return fail(PENCIL_E_ARG, "bad extent/stride");
     DEV_PROLOGUE;
-    StreamState* ss = nullptr;
-    if (stream_state(c, st, &ss)) return g_status;
-    std::lock_guard<std::mutex> lk(ss->mu);
-    if (ensure_gemv_t_counters(c, st, ss, gemv_t_counter_elems(n))) return g_status;
-    float* part = nullptr;
-    size_t pe = gemv_t_partial_elems(m, n);
-    if (pe && pool_alloc(c, st, pe * sizeof(float), (void**)&part)) return g_status;
-    int e = launch_gemv_t(st, m, n, lda, incx, incy, alpha, beta, A, x, y, part, ss->gemv_t_counters);
-    pool_free(st, part);
-    DEV_RET(e);
+    pencil_view v[3];
+    if (pencil_gemv_t_views(m, n, lda, incx, incy, v)) return g_status;
+    v[0].base = (void*)A;
+    v[1].base = (void*)x;
+    v[2].base = (void*)y;
+    return gemv_t_views_launch(c, st, alpha, beta, v[0], v[1], v[2]) ? g_status : ok();
+}
+
+int pencil_gemv_t_view_dev(pencil_stream_t s, float alpha, float beta, const pencil_view* A, const pencil_view* x,
+                           const pencil_view* y) {
+    if (!A || !x || !y || !A->base || !x->base || !y->base) return fail(PENCIL_E_ARG, "null view");
+    DEV_PROLOGUE;
+    return gemv_t_views_launch(c, st, alpha, beta, *A, *x, *y) ? g_status : ok();
+}
+
+// The views of gemv_t.pencil.c's accesses for a call's scalars: the symbolic affine forms of
+// A[i * lda + j] (read, nest j, i), x[i * incx] and y[j * incy] (write) evaluated under
+// {m, n, lda, incx, incy} (descriptors.cpp) — the mapper's view descriptors, not hard-coded strides.
+int pencil_gemv_t_views(int m, int n, int lda, int incx, int incy, pencil_view views[3]) {
+    static const char* names[5] = {"m", "n", "lda", "incx", "incy"};
+    const long long vals[5] = {m, n, lda, incx, incy};
+    pencil_access_form f[16];
+    const int k = pencil_affine_accesses(pencil_fixture_source("gemv_t"), "gemv_t", 5, names, vals, f, 16);
+    if (k < 0) return g_status;
+    memset(views, 0, 3 * sizeof(pencil_view));
+    bool have[3] = {false, false, false};
+    for (int a = 0; a < k && a < 16; a++) {
+        const pencil_access_form& r = f[a];
+        if (!r.affine || r.nloops < 1) continue;
+        // loop 0 = j (the output columns), loop 1 = i (the reduction; A and x only)
+        const long long sj = r.stride[0], si = r.nloops > 1 ? r.stride[1] : 0;
+        if (r.nloops == 2 && !strcmp(r.array, "A") && !r.is_write) {
+            views[0] = {nullptr, r.offset, 2, PENCIL_FLOAT32, {r.hi[1] - r.lo[1], r.hi[0] - r.lo[0]}, {si, sj}};
+            have[0] = true;
+        } else if (r.nloops == 2 && !strcmp(r.array, "x")) {
+            views[1] = {nullptr, r.offset, 1, PENCIL_FLOAT32, {r.hi[1] - r.lo[1], 0}, {si, 0}};
+            have[1] = true;
+        } else if (r.nloops == 1 && !strcmp(r.array, "y") && r.is_write) {
+            views[2] = {nullptr, r.offset, 1, PENCIL_FLOAT32, {r.hi[0] - r.lo[0], 0}, {sj, 0}};
+            have[2] = true;
+        }
+    }
+    if (!have[0] || !have[1] || !have[2]) return fail(PENCIL_E_UNSUPPORTED, "gemv_t fixture: views not found");
+    return ok();
 }
 
 int pencil_dot_dev(pencil_stream_t s, long long n, const float* x, const float* y, float* result_dev) {

@@ -308,11 +308,18 @@ def allgather_vector(local, n, world, rank, align=4):
 class RowShardedGemv:
     """gemv (i PARALLEL over rows): rank owns rows [r0, r1) of A and of y; x is replicated (or
     all-gathered from its shards with `allgather_vector`).  No collective on y: each rank's
-    rows are final; `gather_y` assembles them when a caller wants the whole vector."""
+    rows are final; `gather_y` assembles them when a caller wants the whole vector.  The row
+    partition is an array descriptor (include/pencil_b200.h §10): y's shard spec."""
 
     def __init__(self, m, n, rank, world):
+        from .views import ArrayDesc
         self.m, self.n, self.rank, self.world = m, n, rank, world
-        self.r0, self.r1 = shard_range(m, world, rank, align=1)
+        self.y_desc = ArrayDesc(np.float32, m, [shard_range(m, world, r, align=1)[0] for r in range(world)] + [m])
+        self.r0, self.r1 = self.y_desc.shard(rank)[:2]
+
+    def attach(self, device, y_rows):
+        """Record this rank's y rows (device memory) in the descriptor."""
+        self.y_desc.attach(self.rank, device, y_rows)
 
     def step(self, local_gemv, alpha, beta, A_rows, x, y_rows):
         """local_gemv(m, n, alpha, beta, A, x, y): the CUDA kernel (pb.device.gemv) or a checker."""
@@ -324,16 +331,28 @@ class RowShardedGemv:
 
 class ColShardedGemvT:
     """gemv_t (VOBLA transposed view, j PARALLEL over columns): rank owns columns [j0, j1); every
-    rank reads all m rows of its column block (A at offset j0, same lda) and the replicated x,
-    and writes y[j*incy] for its j only.  No collective."""
+    rank reads all m rows of its column block and the replicated x, and writes y[j*incy] for its j
+    only.  No collective.  The rank's work is expressed in view descriptors: the fixture's views
+    (from the affine forms of A[i*lda + j], x[i*incx], y[j*incy], pencil_gemv_t_views) sliced to
+    the column block (pencil_view_slice) — A at offset j0, y at offset j0*incy."""
 
-    def __init__(self, m, n, rank, world):
+    def __init__(self, m, n, rank, world, lda=None, incx=1, incy=1):
+        from . import views as V
         self.m, self.n, self.rank, self.world = m, n, rank, world
         self.j0, self.j1 = shard_range(n, world, rank, align=4)
+        lda = n if lda is None else lda
+        A, x, y = V.gemv_t_views(m, n, lda, incx, incy)
+        self.A, self.x, self.y = A.slice(1, self.j0, self.j1), x, y.slice(0, self.j0, self.j1)
 
-    def views(self, A_flat, y_flat, incy):
-        """(A view, y view) of this rank's column block inside the caller's flat arrays."""
-        return A_flat[self.j0:], y_flat[self.j0 * incy:]
+    def views(self, A_flat, y_flat, incy=None):
+        """(A view, y view) of this rank's column block inside the caller's flat arrays (host
+        arrays: the elements from the views' offsets on)."""
+        return A_flat[self.A.offset:], y_flat[self.y.offset:]
+
+    def step(self, alpha, beta, A, x, y, stream=None):
+        """The rank's columns on the device: A, x, y are the full flat device arrays."""
+        from . import views as V
+        V.gemv_t_view(alpha, beta, self.A.on(A), self.x.on(x), self.y.on(y), stream)
 
 
 def dot_sharded(local_dot, x_local, y_local):

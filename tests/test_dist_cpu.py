@@ -166,8 +166,8 @@ def _dense_worker(rank, world, port, q):
         # gemv_t: column blocks of the strided view, no collective
         m, n, lda, incx, incy = 41, 90, 96, 2, 3
         A, x, y = synth.f32(m * lda, 4), synth.f32(m * incx, 5), synth.f32(n * incy, 6)
-        gt = pd.ColShardedGemvT(m, n, rank, world)
-        Av, yv = gt.views(A, y, incy)
+        gt = pd.ColShardedGemvT(m, n, rank, world, lda=lda, incx=incx, incy=incy)  # views from the affine forms
+        Av, yv = gt.views(A, y)
         mine = oracle.gemv_t(m, gt.j1 - gt.j0, lda, incx, incy, 1.0, 0.25, Av.copy(), x, yv.copy())
         ref = oracle.gemv_t(m, n, lda, incx, incy, 1.0, 0.25, A, x, y)
         js = np.arange(gt.j1 - gt.j0) * incy
