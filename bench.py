@@ -154,7 +154,7 @@ def bench_spmv(args, torch, pb, rank, world, dist):
     rowptr, col, val, x, xm = synth.csr_powerlaw(nrows)
     nnz = int(col.size)
     flush = lambda: pb.device.l2_flush()  # noqa: E731
-    if world == 1:
+    if not args.dist_path:
         rp, cd, vd, xd = (torch.from_numpy(a).cuda() for a in (rowptr, col, val, x))
         y = torch.empty(nrows, device="cuda")
         plan = pb.device.CsrPlan(nrows, nrows, nnz, rp, mode=1)
@@ -216,17 +216,17 @@ def bench_spmv(args, torch, pb, rank, world, dist):
             e2e = e2e_spmv_dist(args, torch, pb, sh, x, dist)
     algo = spmv_bytes(nrows, nrows, nnz)
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
-           "ceiling_ms": ceil_ms if world == 1 else None,
+           "ceiling_ms": ceil_ms if not args.dist_path else None,
            "config": dict(spmv_config(nrows, nnz, xm),
                           schedule="csr_flow_kernel, reassociated (persistent warps, 1024-nnz window tiles, "
                                    "continuous 128-bit col/val streams)",
                           l2="L2 flushed between steps outside the per-step events (256 MiB fill, then its lines "
                              "discarded: the step starts on a clean, empty L2); inputs 2.35 GB > L2")}
-    if world > 1:
+    if args.dist_path:
         res["config"]["exchange"] = exchange
         if e2e:
             res["e2e"] = e2e
-    if rank == 0 and world == 1 and not args.no_e2e:
+    if rank == 0 and not args.dist_path and not args.no_e2e:
         res["e2e"] = e2e_spmv(args, torch, pb, rowptr, col, val, x)
     return res
 
@@ -685,6 +685,174 @@ def op2_line(args, torch, pb, k, w):
     return res
 
 
+# ------------------------------------------------------------------ N>1 suite
+def max_over_ranks(torch, dist, v):
+    t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(torch, dist, v):
+    t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def dist_line(torch, dist, ms_local, amount, unit, hbm_or_peak, kernel, per_rank_amount, extra=None, bound="hbm"):
+    """One N>1 suite line: value = whole-job amount / max-over-ranks time; the roofline is per GPU
+    (each rank's own bytes or flops over its own kernel time, the slowest rank reported)."""
+    ms = max_over_ranks(torch, dist, ms_local)
+    scale = 1e6 if unit in ("GB/s",) else 1e9
+    ach_local = per_rank_amount / ms_local / scale
+    ach = -max_over_ranks(torch, dist, -ach_local)  # the slowest rank
+    line = {"ms": ms, unit: amount / ms / scale, "value": amount / ms / scale, "unit": unit,
+            "roofline": {"bound": bound, "kernel": kernel, "achieved_per_gpu_min": ach, "peak": hbm_or_peak,
+                         "unit": unit, "frac": ach / hbm_or_peak, "traffic": ncu_traffic(kernel)}}
+    if extra:
+        line.update(extra)
+    return line
+
+
+def suite_dist(args, torch, pb, rank, world, dist, hbm):
+    """The sharded configs of SURVEY §8e at N GPUs (one process per GPU, max over ranks):
+    gemm on the R x C tile grid (16384^3), the band-sharded 5x5 stencils with the halo read in
+    place from the neighbours (16384^2, u8 int32 storage and f32), and row-sharded gemv 8192^2
+    (x all-gather + local rows) captured in one CUDA graph.  Each line also carries the same
+    work end to end (per-rank pinned-host inputs -> device -> outputs back, device-timed)."""
+    from paper_1302_5586_b200 import synth
+    from paper_1302_5586_b200 import dist as pd
+    out = {}
+    k, w = max(3, args.suite_steps), 3
+    flush = lambda: pb.device.l2_flush()  # noqa: E731
+    fused_ok = args.dist_backend == "nccl"
+
+    # gemm 16384^3 on the R x C grid: inputs replicated (no data-path collective)
+    try:
+        m = n = kk = 16384
+        tg = pd.GemmTileGrid(m, n, kk, rank, world)
+        hA, hB = synth.f32(m * kk), synth.f32(kk * n, 43)
+        Ap = torch.from_numpy(hA.reshape(m, kk)[tg.m0:tg.m1].copy()).cuda().reshape(-1)
+        Bp = torch.from_numpy(np.ascontiguousarray(hB.reshape(kk, n)[:, tg.n0:tg.n1])).cuda().reshape(-1)
+        mt, nt = tg.m1 - tg.m0, tg.n1 - tg.n0
+        Ct = torch.zeros(mt * nt, device="cuda")
+        step = lambda: pb.device.gemm(mt, nt, kk, 1.0, 0.0, Ap, Bp, Ct)  # noqa: E731
+        ms = statistics.mean(run_steps(torch, step, 5, 3, flush, dist))
+        burst, sustained, _ = tf32x3_peaks()
+        out["gemm_16384_3xtf32_grid"] = dist_line(
+            torch, dist, ms, 2.0 * m * n * kk, "TFLOP/s", burst, "gemm_3xtf32_2sm_kernel", 2.0 * mt * nt * kk,
+            {"grid": "%d x %d" % (tg.R, tg.C), "tile": "%d x %d" % (mt, nt),
+             "collective": "none (A row panel + B column panel replicated per rank)"}, bound="tensor")
+        if not args.no_e2e:
+            pA, pB = torch.from_numpy(hA.reshape(m, kk)[tg.m0:tg.m1].copy()).pin_memory(), \
+                torch.from_numpy(np.ascontiguousarray(hB.reshape(kk, n)[:, tg.n0:tg.n1])).pin_memory()
+            pC = torch.empty(mt * nt).pin_memory()
+
+            def call():
+                Ap.copy_(pA.reshape(-1), non_blocking=True)
+                Bp.copy_(pB.reshape(-1), non_blocking=True)
+                pb.device.gemm(mt, nt, kk, 1.0, 0.0, Ap, Bp, Ct)
+                pC.copy_(Ct, non_blocking=True)
+            ms_e = statistics.mean(run_steps(torch, call, 2, 1, lambda: None, dist))
+            out["gemm_16384_3xtf32_grid"]["e2e"] = {
+                "value": 2.0 * m * n * kk / max_over_ranks(torch, dist, ms_e) / 1e9, "unit": "TFLOP/s",
+                "ms_per_call": max_over_ranks(torch, dist, ms_e),
+                "h2d_bytes_per_step": int(sum_over_ranks(torch, dist, 4 * (mt * kk + kk * nt))),
+                "d2h_bytes_per_step": int(sum_over_ranks(torch, dist, 4 * mt * nt)),
+                "api": "per rank: pinned A row panel + B column panel -> its GPU, pencil_gemm_dev, C tile -> host"}
+        del Ap, Bp, Ct, hA, hB
+    except Exception as e:  # noqa: BLE001
+        out["gemm_16384_3xtf32_grid"] = {"unavailable": str(e)[:200]}
+
+    # band-sharded 5x5 stencils 16384^2, halos read in place (FusedBandStencil) or exchanged (gloo)
+    h = w_ = 16384
+    for name, f32 in (("conv5x5_u8_bands_16384", False), ("conv5x5_f32_bands_16384", True)):
+        try:
+            img = synth.f32(h * w_) if f32 else synth.u8_i32(h * w_)
+            dtype = torch.float32 if f32 else torch.int32
+            if fused_ok:
+                fb = pd.FusedBandStencil(h, w_, rank, world, dtype, torch.device("cuda", torch.cuda.current_device()))
+                fb.band().copy_(torch.from_numpy(img[fb.b0 * w_:fb.b1 * w_]))
+                outb = torch.zeros(fb.nb * w_, dtype=dtype, device="cuda")
+                kf = (synth.BINOMIAL / 256.0).astype(np.float32)
+                step = (lambda: fb.step_f32(kf, outb)) if f32 else (lambda: fb.step_u8(256, synth.BINOMIAL, outb))
+                rows, how = fb.nb, "fused: the band sweep reads the neighbours' edge rows over NVLink (cp.async from peer mappings)"
+            else:
+                band = pd.BandShardedImage(h, w_, rank, world)
+                ext = torch.zeros(band.rows * w_, dtype=dtype, device="cuda")
+                ext.view(band.rows, w_)[band.top:band.top + band.b1 - band.b0] = \
+                    torch.from_numpy(img[band.b0 * w_:band.b1 * w_]).cuda().view(-1, w_)
+                outb = torch.zeros(band.rows * w_, dtype=dtype, device="cuda")
+                kf = (synth.BINOMIAL / 256.0).astype(np.float32)
+
+                def step():
+                    band.exchange_halos(ext.view(band.rows, w_))
+                    if f32:
+                        pb.device.conv5x5_f32(band.rows, w_, ext, kf, outb)
+                    else:
+                        pb.device.conv5x5_u8(band.rows, w_, 256, ext, synth.BINOMIAL, outb)
+                rows, how = band.b1 - band.b0, "unfused: %s send/recv of 2 halo rows, then the stencil" % args.dist_backend
+            ms = statistics.mean(run_steps(torch, step, k, w, flush, dist))
+            out[name] = dist_line(torch, dist, ms, 8.0 * h * w_, "GB/s", hbm,
+                                  "stencil_band_kernel" if fused_ok else "stencil_ring_kernel", 8.0 * rows * w_,
+                                  {"exchange": how, "taps": "binomial" + (" / 256" if f32 else ", scale 256")})
+            del img
+        except Exception as e:  # noqa: BLE001
+            out[name] = {"unavailable": str(e)[:200]}
+
+    # gemv 8192^2 row-sharded: x all-gathered from its shards + the local rows, one CUDA graph
+    try:
+        m = n = 8192
+        g = pd.RowShardedGemv(m, n, rank, world)
+        hA, hx = synth.f32(m * n), synth.f32(n, 42, m * n)
+        A_rows = torch.from_numpy(hA.reshape(m, n)[g.r0:g.r1].copy()).cuda().reshape(-1)
+        lo, hi = pd.shard_range(n, world, rank, align=1)
+        x_shard = torch.from_numpy(hx[lo:hi].copy()).cuda()
+        y_rows = torch.zeros(g.r1 - g.r0, device="cuda")
+        g.attach(torch.cuda.current_device(), y_rows)
+        width = max(b - a for a, b in (pd.shard_range(n, world, r, align=1) for r in range(world)))
+        xpad = torch.zeros(width, device="cuda")
+        xg = torch.empty(width * world, device="cuda")
+        bounds = [pd.shard_range(n, world, r, align=1) for r in range(world)]
+        idx = torch.cat([torch.arange(a, b) + r * width for r, (a, b) in enumerate(bounds)]).cuda()
+        xfull = torch.empty(n, device="cuda")
+
+        def gemv_step():
+            xpad[: hi - lo].copy_(x_shard)
+            if world > 1 and dist.get_backend() == "nccl":
+                dist.all_gather_into_tensor(xg, xpad)
+            elif world > 1:
+                dist.all_gather(list(xg.view(world, width).unbind(0)), xpad)
+            else:
+                xg.copy_(xpad)
+            torch.index_select(xg, 0, idx, out=xfull)
+            pb.device.gemv(g.r1 - g.r0, n, 1.0, 0.0, A_rows, xfull, y_rows)
+        graph = None
+        if dist.get_backend() == "nccl":
+            try:
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(s):
+                    for _ in range(3):
+                        gemv_step()
+                torch.cuda.current_stream().wait_stream(s)
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    gemv_step()
+            except Exception as e:  # noqa: BLE001 — capture refused: plain launches
+                graph, why = None, str(e)[:100]
+        step = graph.replay if graph is not None else gemv_step
+        ms = statistics.mean(run_steps(torch, step, k, w, flush, dist))
+        out["gemv_8192_rows"] = dist_line(
+            torch, dist, ms, 4.0 * (m * n + n + m), "GB/s", hbm, "gemv_kernel", 4.0 * ((g.r1 - g.r0) * n + n + g.r1 - g.r0),
+            {"step": "x all-gather (%s) + local rows" % dist.get_backend(),
+             "launch": "one CUDA graph per step" if graph is not None else "plain launches"})
+        del A_rows, hA
+    except Exception as e:  # noqa: BLE001
+        out["gemv_8192_rows"] = {"unavailable": str(e)[:200]}
+    return out
+
+
 # ------------------------------------------------------------------ reference arm (CPU)
 def cpu_spmv(steps, warmup, rowptr, col, val, x):
     lib, _ = cpu_lib()
@@ -736,6 +904,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--suite-steps", type=int, default=10)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--force-dist", action="store_true",
+                    help="take the N>1 code path (process group, shards, collectives) even at one rank")
     ap.add_argument("--dist-mode", default="fused", choices=["fused", "nccl"],
                     help="N>1 SpMV step: fused SpMV->all-gather kernel, or SpMV + NCCL all-gather")
     args = ap.parse_args()
@@ -758,8 +928,13 @@ def main():
     dev = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     dist = None
-    if world > 1:
+    args.dist_path = world > 1 or args.force_dist
+    if args.dist_path:
         import torch.distributed as tdist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         if args.dist_backend == "nccl":
             tdist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
@@ -769,6 +944,7 @@ def main():
 
     with Clocks(dev) as clk:
         res = bench_spmv(args, torch, pb, rank, world, dist)
+        dsuite = suite_dist(args, torch, pb, rank, world, dist, hbm) if args.dist_path and not args.no_suite else None
     ms = res["ms"]
     if dist:
         t = torch.tensor([ms], device="cuda")
@@ -776,13 +952,13 @@ def main():
         ms = float(t.item())
     value = res["bytes"] / ms / 1e6  # GB/s, whole job (global matrix bytes / max-rank time)
     if rank == 0:
-        kernel_gbs = res["bytes"] / res["ms"] / 1e6 if world == 1 else None
+        kernel_gbs = res["bytes"] / res["ms"] / 1e6 if not args.dist_path else None
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(res["config"], parallelism=f"row-sharded x{world}" if world > 1 else "single GPU"),
+                "config": dict(res["config"], parallelism=f"row-sharded x{world}" if args.dist_path else "single GPU"),
                 "gpu_launches": res["launches"]}
-        if world == 1:
+        if not args.dist_path:
             line["roofline"] = {"bound": "hbm", "kernel": "csr_flow_kernel", "achieved": kernel_gbs,
                                 "peak": hbm, "unit": "GB/s", "frac": kernel_gbs / hbm,
                                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
@@ -796,7 +972,7 @@ def main():
         line["clocks"] = clk.summary()
         if "e2e" in res:
             line["e2e"] = res["e2e"]
-        if world == 1 and not args.no_cpu_baseline:
+        if not args.dist_path and not args.no_cpu_baseline:
             try:
                 from paper_1302_5586_b200 import synth
                 rowptr, col, val, x, _ = synth.csr_powerlaw(1 << 24)
@@ -814,7 +990,9 @@ def main():
                 line["cpu_baseline"]["value_1thread"] = spmv_bytes(1 << 24, 1 << 24, col.size) / t1 / 1e9
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
-        if world == 1 and not args.no_suite:
+        if dsuite is not None:
+            line["suite"] = dsuite
+        if not args.dist_path and not args.no_suite:
             line["suite"] = suite(args, torch, pb, hbm)
             # the measured peak is a copy test (read + write); read-mostly streams go past it, so
             # every bandwidth line also carries its fraction of the B200 spec (8 TB/s HBM3e)
