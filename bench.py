@@ -279,7 +279,7 @@ def e2e_spmv_dist(args, torch, pb, sh, x, dist):
     for p in plans:
         p.close()
     h2d = 4 * ((sh.nrows + 1) + 2 * sh.nnz + sh.nrows)
-    t = torch.tensor([ms, float(h2d), 4.0 * sh.nrows], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms, float(h2d), 4.0 * sh.nrows], dtype=torch.float64, device=coll_dev(dist))
     tmax = t[:1].clone()
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -686,14 +686,19 @@ def op2_line(args, torch, pb, k, w):
 
 
 # ------------------------------------------------------------------ N>1 suite
+def coll_dev(dist):
+    """Where the small timing reductions live: the GPU under NCCL, host memory under gloo."""
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+
 def max_over_ranks(torch, dist, v):
-    t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([float(v)], dtype=torch.float64, device=coll_dev(dist))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
 def sum_over_ranks(torch, dist, v):
-    t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([float(v)], dtype=torch.float64, device=coll_dev(dist))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -821,7 +826,7 @@ def suite_dist(args, torch, pb, rank, world, dist, hbm):
             if world > 1 and dist.get_backend() == "nccl":
                 dist.all_gather_into_tensor(xg, xpad)
             elif world > 1:
-                dist.all_gather(list(xg.view(world, width).unbind(0)), xpad)
+                pd._all_gather_list(list(xg.view(world, width).unbind(0)), xpad)
             else:
                 xg.copy_(xpad)
             torch.index_select(xg, 0, idx, out=xfull)
@@ -947,7 +952,7 @@ def main():
         dsuite = suite_dist(args, torch, pb, rank, world, dist, hbm) if args.dist_path and not args.no_suite else None
     ms = res["ms"]
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=coll_dev(dist))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = res["bytes"] / ms / 1e6  # GB/s, whole job (global matrix bytes / max-rank time)

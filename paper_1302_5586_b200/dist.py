@@ -24,6 +24,24 @@ import numpy as np
 from . import _lib
 
 
+def _gloo():
+    import torch.distributed as dist
+    return dist.get_backend() != "nccl"
+
+
+def _all_gather_list(out_rows, t):
+    """all_gather into the rows of `out_rows` (a list of views).  gloo (CPU tests, one-GPU plumbing
+    runs) moves no CUDA memory: device tensors go through host copies."""
+    import torch.distributed as dist
+    if t.is_cuda and _gloo():
+        host = [r.cpu() for r in out_rows]
+        dist.all_gather(host, t.cpu())
+        for r, h in zip(out_rows, host):
+            r.copy_(h)
+        return
+    dist.all_gather(out_rows, t)
+
+
 def shard_rows_by_nnz(rowptr, nshards):
     lib = _lib.load()
     rowptr = np.ascontiguousarray(rowptr, dtype=np.int32)
@@ -83,7 +101,7 @@ class RowShardedCsr:
         if dist.get_backend() == "nccl":
             dist.all_gather_into_tensor(out, x_local_padded)
         else:  # gloo (CPU tests): list form
-            dist.all_gather(list(out.view(self.world, self.max_rows).unbind(0)), x_local_padded)
+            _all_gather_list(list(out.view(self.world, self.max_rows).unbind(0)), x_local_padded)
         return out
 
 
@@ -194,13 +212,15 @@ class BandShardedImage:
         import torch.distributed as dist
         H, reqs = self.HALO, []
         own0, own1 = self.top, self.top + (self.b1 - self.b0)
+        host = ext.is_cuda and _gloo()  # gloo moves host memory only
+        mv = (lambda t: t.cpu()) if host else (lambda t: t)  # noqa: E731
         if self.rank > 0:
-            reqs.append(dist.isend(ext[own0:own0 + H].contiguous(), self.rank - 1))
-            top = ext[0:H].clone()
+            reqs.append(dist.isend(mv(ext[own0:own0 + H].contiguous()), self.rank - 1))
+            top = mv(ext[0:H].clone())
             reqs.append(dist.irecv(top, self.rank - 1))
         if self.rank < self.world - 1:
-            reqs.append(dist.isend(ext[own1 - H:own1].contiguous(), self.rank + 1))
-            bot = ext[own1:own1 + H].clone()
+            reqs.append(dist.isend(mv(ext[own1 - H:own1].contiguous()), self.rank + 1))
+            bot = mv(ext[own1:own1 + H].clone())
             reqs.append(dist.irecv(bot, self.rank + 1))
         for r in reqs:
             r.wait()
@@ -300,7 +320,7 @@ def allgather_vector(local, n, world, rank, align=4):
     if dist.get_backend() == "nccl":
         dist.all_gather_into_tensor(out, pad)
     else:
-        dist.all_gather(list(out.view(world, width).unbind(0)), pad)
+        _all_gather_list(list(out.view(world, width).unbind(0)), pad)
     parts = out.view(world, width)
     return torch.cat([parts[r, : hi - lo] for r, (lo, hi) in enumerate(bounds)])
 
@@ -360,7 +380,8 @@ def dot_sharded(local_dot, x_local, y_local):
     The partials are summed in fp64 (rank order fixed by the collective) and rounded once."""
     import torch
     import torch.distributed as dist
-    part = torch.tensor([float(local_dot(x_local, y_local))], dtype=torch.float64, device=x_local.device)
+    dev = "cpu" if _gloo() else x_local.device
+    part = torch.tensor([float(local_dot(x_local, y_local))], dtype=torch.float64, device=dev)
     dist.all_reduce(part)
     return float(part.item())
 
@@ -398,7 +419,7 @@ class GemmTileGrid:
         pad = torch.zeros(width, dtype=c_tile.dtype, device=c_tile.device)
         pad[: c_tile.numel()] = c_tile.reshape(-1)
         parts = [torch.empty_like(pad) for _ in range(self.world)]
-        dist.all_gather(parts, pad)
+        _all_gather_list(parts, pad)
         out = torch.empty(self.m, self.n, dtype=c_tile.dtype, device=c_tile.device)
         for r, ((a0, a1), (b0, b1)) in enumerate(tiles):
             out[a0:a1, b0:b1] = parts[r][: (a1 - a0) * (b1 - b0)].view(a1 - a0, b1 - b0)
