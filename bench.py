@@ -818,7 +818,7 @@ def suite_dist(args, torch, pb, rank, world, dist, hbm):
         xpad = torch.zeros(width, device="cuda")
         xg = torch.empty(width * world, device="cuda")
         bounds = [pd.shard_range(n, world, r, align=1) for r in range(world)]
-        idx = torch.cat([torch.arange(a, b) + r * width for r, (a, b) in enumerate(bounds)]).cuda()
+        idx = torch.cat([torch.arange(b - a) + r * width for r, (a, b) in enumerate(bounds)]).cuda()
         xfull = torch.empty(n, device="cuda")
 
         def gemv_step():
