@@ -30,10 +30,15 @@
 // non-zeros per warp tile (plan window); swept over {256..2048} x WCHUNK {64,128,256} at
 // 2^24 rows (tools/spmv_sweep.sh): 1024 x 128 is fastest (1.28 ms; 512: 1.34; 256: 1.59)
 #define SPMV_TILE_NNZ 1024
+#define SEG_CTAS_PER_SM 6
 
+// plan_flags: [0] non-monotone rowptr (generic schedule), [2] some row is empty.  rs_bits (when
+// given): bit k set iff non-zero k is the first of its row — the row-start map of the segmented
+// executor (csr_seg_kernel).
 __global__ void csr_plan_kernel(int nrows, int nnz_len, const int* __restrict__ rowptr,
                                 int tile_nnz, int ntiles, int* __restrict__ tile_row,
-                                unsigned* __restrict__ plan_flags, unsigned* __restrict__ status) {
+                                unsigned* __restrict__ plan_flags, unsigned* __restrict__ rs_bits,
+                                unsigned* __restrict__ status) {
     const int base = __ldg(rowptr);
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= nrows;
          i += (long long)gridDim.x * blockDim.x) {
@@ -42,8 +47,12 @@ __global__ void csr_plan_kernel(int nrows, int nnz_len, const int* __restrict__ 
         const long long cur = (long long)raw - base;
         long long prev = -1;
         if (i > 0) {
-            prev = (long long)__ldg(rowptr + i - 1) - base;
+            const int praw = __ldg(rowptr + i - 1);
+            prev = (long long)praw - base;
             if (cur < prev) atomicOr(plan_flags, 1u);  // non-monotone -> generic schedule
+            if (cur == prev) atomicOr(plan_flags + 2, 1u);  // row i - 1 is empty
+            if (rs_bits && cur > prev && praw >= 0 && praw < nnz_len)
+                atomicOr(rs_bits + (praw >> 5), 1u << (praw & 31));
         }
         if (cur <= prev) continue;
         long long k_lo = prev < 0 ? 0 : prev / tile_nnz + 1;
@@ -377,15 +386,153 @@ __global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_flow_kernel(
     }
 }
 
+// Segmented-reduction executor (reassociation licensed: spmv_vec; rows never empty — the plan's
+// flag — so the k-th row start after a tile's first row is row r0 + k).  The tile's non-zeros
+// stream in 128-element windows exactly as in csr_flow_kernel (16-byte col / val loads, 4 gathers
+// per lane), but instead of staging products and folding each row in its own lane, every lane
+// reduces its 4 products by segments (the row starts come from the plan's bitmap, one 32-bit word
+// per lane), and a warp segmented scan (5 shuffle rounds) carries the open row across lanes and
+// windows; every row is stored once, by the lane where it closes.  Per 128 non-zeros that is ~70
+// warp instructions where the batch-and-fold executor issues ~400 (ncu: 857 M for 2^28
+// non-zeros), so the kernel runs at the rate of its random gathers.  The sum order is fixed
+// (lanes in order, the scan tree, windows in order): deterministic run to run.
+template <bool DIST>
+__global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
+    int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
+    const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
+    const int* __restrict__ tile_row, int ntiles, const unsigned* __restrict__ plan,
+    const unsigned* __restrict__ rs_bits, unsigned* __restrict__ tk, unsigned* __restrict__ status,
+    const PeerSet ps) {
+    if (plan[0]) {
+        spmv_generic_t<DIST>(nrows, ncols, nnz_len, rowptr, col, val, x, y, status, ps);
+        if (DIST) __threadfence_system();
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
+    auto clampp = [&](int v) { return v < 0 ? 0 : (v > nnz_len ? nnz_len : v); };
+    for (;;) {
+        unsigned ticket = 0;
+        if (lane == 0) ticket = atomicAdd(tk, 1u);
+        ticket = __shfl_sync(0xffffffffu, ticket, 0);
+        if (ticket >= (unsigned)ntiles) {
+            if (lane == 0 && ticket == (unsigned)ntiles + total_warps - 1) *tk = 0;
+            if (DIST) __threadfence_system();
+            return;
+        }
+        const int r0 = __ldg(tile_row + ticket), r1 = __ldg(tile_row + ticket + 1);
+        if (r0 >= r1) continue;
+        const int P0 = clampp(__ldg(rowptr + r0));
+        const int P1 = max(P0, clampp(__ldg(rowptr + r1)));
+        int row = r0;       // the row open at the window's first position
+        float carry = 0.f;  // its partial sum from the earlier windows
+        for (int qa = P0 & ~3; qa < P1; qa += 128) {
+            const int p = qa + 4 * lane;
+            float pr[4] = {0.f, 0.f, 0.f, 0.f};
+            unsigned sb = 0;  // bit e: position p + e starts a row (other than the tile's first)
+            if (p + 3 >= P0 && p < P1) {
+                int c[4];
+                float v[4];
+                if (p + 3 < nnz_len) {
+                    const int4 c4 = ld_stream_i4(reinterpret_cast<const int4*>(col + p));
+                    const float4 v4 = ld_stream_f4(reinterpret_cast<const float4*>(val + p));
+                    c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+                    v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        c[k] = p + k < nnz_len ? __ldg(col + p + k) : 0;
+                        v[k] = p + k < nnz_len ? __ldg(val + p + k) : 0.f;
+                    }
+                }
+                const unsigned bits = (__ldg(rs_bits + (p >> 5)) >> (p & 31)) & 0xFu;
+                float xv[4];
+                bool use[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const bool in = p + k >= P0 && p + k < P1, ok = (unsigned)c[k] < (unsigned)ncols;
+                    use[k] = in && ok;
+                    xv[k] = ld_keep_f(x + (use[k] ? c[k] : 0));
+                    if (in && !ok) raise_fault(status, FAULT_OOB_LOAD);
+                    if (in && p + k > P0 && ((bits >> k) & 1u)) sb |= 1u << k;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; k++) pr[k] = use[k] ? v[k] * xv[k] : 0.f;
+            }
+            // the lane's segments: head (before its first start: closes the row open on entry),
+            // complete rows between two starts, tail (from its last start: stays open)
+            const int cnt = __popc(sb);
+            float head = 0.f, acc = 0.f, mid[3] = {0.f, 0.f, 0.f};
+            int nseg = 0;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                if ((sb >> k) & 1u) {
+                    if (nseg == 0) head = acc;
+                    else mid[nseg - 1] = acc;
+                    acc = 0.f;
+                    nseg++;
+                }
+                acc += pr[k];
+            }
+            if (cnt == 0) head = acc;
+            // row index of the row open on entry to this lane: starts in the lanes before
+            int before = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, before, d);
+                if (lane >= d) before += o;
+            }
+            const int win_starts = __shfl_sync(0xffffffffu, before, 31);
+            before -= cnt;
+            // segmented scan of the open row's partial sum across lanes (the window carry enters at lane 0)
+            float sv = cnt ? acc : head + (lane == 0 ? carry : 0.f);
+            bool sf = cnt != 0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const float vo = __shfl_up_sync(0xffffffffu, sv, d);
+                const bool fo = __shfl_up_sync(0xffffffffu, sf, d);
+                if (lane >= d && !sf) {
+                    sv = vo + sv;
+                    sf = fo;
+                }
+            }
+            float excl = __shfl_up_sync(0xffffffffu, sv, 1);
+            if (lane == 0) excl = carry;
+            if (cnt) {
+                const int ro = row + before;
+                y[ro] = excl + head;
+                if (cnt > 1) y[ro + 1] = mid[0];
+                if (cnt > 2) y[ro + 2] = mid[1];
+                if (cnt > 3) y[ro + 3] = mid[2];
+            }
+            carry = __shfl_sync(0xffffffffu, sv, 31);
+            row += win_starts;
+        }
+        if (lane == 0) y[row] = carry;  // the tile's last row (row == r1 - 1)
+        if (DIST) {
+            __syncwarp();
+            __threadfence_block();
+            for (int r = r0 + lane; r < r1; r += 64) {
+                const float v0 = y[r], v1 = r + 32 < r1 ? y[r + 32] : 0.f;
+                put_row<true, false>(y, ps, r, v0);
+                if (r + 32 < r1) put_row<true, false>(y, ps, r + 32, v1);
+            }
+        }
+    }
+}
+
 int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
-                    int ntiles, int* tile_row, unsigned* plan_flags, unsigned* status) {
-    cudaMemsetAsync(plan_flags, 0, 64, st);  // [0] non-monotone flag
+                    int ntiles, int* tile_row, unsigned* plan_flags, unsigned* rs_bits, unsigned* status) {
+    cudaMemsetAsync(plan_flags, 0, 64, st);  // [0] non-monotone flag, [2] empty-row flag
+    if (rs_bits) cudaMemsetAsync(rs_bits, 0, csr_rs_words(nnz_len) * sizeof(unsigned), st);
     long long blocks = ((long long)nrows + 1 + 255) / 256;
     if (blocks > PENCIL_NUM_SMS * 16) blocks = PENCIL_NUM_SMS * 16;
     csr_plan_kernel<<<(int)blocks, 256, 0, st>>>(nrows, nnz_len, rowptr, tile_nnz, ntiles, tile_row,
-                                                 plan_flags, status);
+                                                 plan_flags, rs_bits, status);
     return (int)cudaGetLastError();
 }
+
+size_t csr_rs_words(int nnz_len) { return (size_t)(nnz_len > 0 ? nnz_len : 1) / 32 + 2; }
 
 // Executor choice: the continuous-stream kernel when col / val are 16-byte aligned (1.25 ms at
 // 2^24 rows), else the scalar-load kernel (any alignment; 1.28 ms).  Measured and dropped (numbers
@@ -407,12 +554,22 @@ int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, 
 // the last warp re-arms it, so launches on one stream never share it with another stream's.
 int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                     const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                    const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* tk,
-                    unsigned* status) {
+                    const int* tile_row, int ntiles, const unsigned* plan_flags, const unsigned* rs_bits,
+                    unsigned* tk, unsigned* status) {
     if (nrows <= 0) return 0;
     int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;  // persistent: at most one wave
     if (grid > PENCIL_NUM_SMS * CTAS_PER_SM) grid = PENCIL_NUM_SMS * CTAS_PER_SM;
-    if ((uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
+    const bool aligned = (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0;
+#ifdef PENCIL_VARIANT_NO_SEG
+    rs_bits = nullptr;  // A/B build: the batch-and-fold executor for spmv_vec too
+#endif
+    if (assoc && rs_bits && aligned) {  // reassociation licensed, no empty rows: segmented executor
+        if (grid > PENCIL_NUM_SMS * SEG_CTAS_PER_SM) grid = PENCIL_NUM_SMS * SEG_CTAS_PER_SM;
+        csr_seg_kernel<false><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row,
+                                                            ntiles, plan_flags, rs_bits, tk, status, PeerSet{});
+        return (int)cudaGetLastError();
+    }
+    if (aligned) {
         if (assoc)
             csr_flow_kernel<true><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y,
                                                                  tile_row, ntiles, plan_flags, tk, status, PeerSet{});
@@ -446,10 +603,18 @@ __global__ void dist_rows_kernel(int nrows, const float* __restrict__ y, const P
 
 int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                          const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                         const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* tk,
-                         unsigned* status, const PeerSet& peers) {
+                         const int* tile_row, int ntiles, const unsigned* plan_flags, const unsigned* rs_bits,
+                         unsigned* tk, unsigned* status, const PeerSet& peers) {
     if (nrows <= 0) return 0;
-    if ((uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0) {
+    const bool aligned = (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0;
+    if (assoc && rs_bits && aligned) {
+        int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+        if (grid > PENCIL_NUM_SMS * SEG_CTAS_PER_SM) grid = PENCIL_NUM_SMS * SEG_CTAS_PER_SM;
+        csr_seg_kernel<true><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row,
+                                                           ntiles, plan_flags, rs_bits, tk, status, peers);
+        return (int)cudaGetLastError();
+    }
+    if (aligned) {
         int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
         if (grid > PENCIL_NUM_SMS * CTAS_PER_SM) grid = PENCIL_NUM_SMS * CTAS_PER_SM;
         if (assoc)
@@ -462,7 +627,7 @@ int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int n
     }
     // unaligned col/val: the regular executor, then the rows leave in a second launch
     int e = launch_csr_spmv(st, assoc, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles,
-                            plan_flags, tk, status);
+                            plan_flags, nullptr, tk, status);
     if (e) return e;
     long long blocks = ((long long)nrows + 255) / 256;
     if (blocks > PENCIL_NUM_SMS * 8) blocks = PENCIL_NUM_SMS * 8;

@@ -20,13 +20,17 @@ int launch_axpy(cudaStream_t st, long long n, float a, const float* a_dev, const
                 float* y);
 
 // k_spmv.cu
+// rs_bits (optional, csr_rs_words(nnz) words): the row-start bitmap of the segmented executor
 int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
-                    int ntiles, int* tile_row, unsigned* plan_flags, unsigned* status);
+                    int ntiles, int* tile_row, unsigned* plan_flags, unsigned* rs_bits, unsigned* status);
+size_t csr_rs_words(int nnz_len);
 // tk: the per-(device, stream) tile-ticket word (zero between launches; the kernels re-arm it)
+// rs_bits: the plan's row-start bitmap when the segmented executor may run (reassociation licensed,
+// monotone rowptr, no empty row), else NULL
 int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                     const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                    const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* tk,
-                    unsigned* status);
+                    const int* tile_row, int ntiles, const unsigned* plan_flags, const unsigned* rs_bits,
+                    unsigned* tk, unsigned* status);
 int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const int* rowptr,
                        const int* col, const float* val, const float* x, float* y,
                        unsigned* status);
@@ -42,8 +46,8 @@ struct PeerSet {
 };
 int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                          const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                         const int* tile_row, int ntiles, const unsigned* plan_flags, unsigned* tk,
-                         unsigned* status, const PeerSet& peers);
+                         const int* tile_row, int ntiles, const unsigned* plan_flags, const unsigned* rs_bits,
+                         unsigned* tk, unsigned* status, const PeerSet& peers);
 
 // k_conv.cu  (taps are host arrays, passed to the kernels by value)
 int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const float* k25,

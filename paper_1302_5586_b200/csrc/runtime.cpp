@@ -314,7 +314,24 @@ struct CsrPlanImpl {
     int device, nrows, ncols, nnz, mode, ntiles, tile_nnz;
     int* tile_row = nullptr;
     unsigned* flags = nullptr;
+    unsigned* rs_bits = nullptr;  // row-start bitmap (mode 1)
+    int seg = 0;                  // the segmented executor applies (mode 1, monotone, no empty row)
+    const unsigned* seg_bits() const { return seg ? rs_bits : nullptr; }
 };
+
+// after the plan kernel: which executor the plan takes (reads its two flag words: a sync on st)
+int csr_plan_finalize(cudaStream_t st, CsrPlanImpl* p) {
+    unsigned f[4] = {0, 0, 0, 0};
+    CK(cudaMemcpyAsync(f, p->flags, sizeof f, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    p->seg = p->mode == 1 && p->rs_bits && f[0] == 0 && f[2] == 0;
+    return PENCIL_OK;
+}
+void csr_plan_release(cudaStream_t st, CsrPlanImpl& p) {
+    pool_free(st, p.tile_row);
+    pool_free(st, p.flags);
+    pool_free(st, p.rs_bits);
+}
 
 int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int* rowptr, int mode,
                    CsrPlanImpl* p, unsigned* fw = nullptr) {
@@ -329,10 +346,12 @@ int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int*
     if (r) return r;
     r = pool_alloc(c, st, 64, (void**)&p->flags);
     if (r) return r;
+    if (mode == 1 && (r = pool_alloc(c, st, csr_rs_words(nnz) * sizeof(unsigned), (void**)&p->rs_bits))) return r;
     CK(cudaMemsetAsync(p->tile_row, 0, sizeof(int) * ((size_t)p->ntiles + 1), st));
     if (!fw) fw = fault_word(c, st);
     if (!fw) return g_status;
-    return (int)launch_csr_plan(st, nrows, nnz, rowptr, p->tile_nnz, p->ntiles, p->tile_row, p->flags, fw) == 0
+    return (int)launch_csr_plan(st, nrows, nnz, rowptr, p->tile_nnz, p->ntiles, p->tile_row, p->flags, p->rs_bits,
+                                fw) == 0
                ? PENCIL_OK
                : fail(PENCIL_E_CUDA, "csr plan launch");
 }
@@ -410,8 +429,7 @@ int spmv_pipelined(int mode, int nrows, int ncols, int nnz, const int* rowptr, c
         pool_free(s0, dval);
         pool_free(s0, dx);
         pool_free(s0, dy);
-        pool_free(s0, p.tile_row);
-        pool_free(s0, p.flags);
+        csr_plan_release(s0, p);
         cudaStreamSynchronize(s0);
     }};
     unsigned *fw0 = fault_word(c, s0), *tk1 = ticket_word(c, s1);  // faults land in the call's word
@@ -448,15 +466,17 @@ int spmv_pipelined(int mode, int nrows, int ncols, int nnz, const int* rowptr, c
     const int K = p.ntiles < SPMV_PIPE_BLOCKS ? p.ntiles : SPMV_PIPE_BLOCKS;
     int* hb = pc->host_rows;
     CK(cudaMemcpyAsync(hb, p.flags, sizeof(int), cudaMemcpyDeviceToHost, s1));
+    CK(cudaMemcpyAsync(hb + 40, p.flags + 2, sizeof(int), cudaMemcpyDeviceToHost, s1));
     for (int b = 0; b <= K; b++) {
         const long long t = (long long)b * p.ntiles / K;
         CK(cudaMemcpyAsync(hb + 1 + b, p.tile_row + t, sizeof(int), cudaMemcpyDeviceToHost, s1));
     }
     CK(cudaStreamSynchronize(s1));
+    p.seg = mode == 1 && p.rs_bits && hb[0] == 0 && hb[40] == 0;
     CK(cudaStreamWaitEvent(s1, pc->ev_x, 0));
     auto launch = [&](long long t0, long long t1) {
         return launch_csr_spmv(s1, mode, nrows, ncols, nnz, drp, dcol, dval, dx, dy, p.tile_row + t0,
-                               (int)(t1 - t0), p.flags, tk1, fw0);
+                               (int)(t1 - t0), p.flags, p.seg_bits(), tk1, fw0);
     };
     if (hb[0] != 0) {  // non-monotone rowptr: generic schedule after the whole upload
         CK(cudaStreamWaitEvent(s1, pc->ev_chunk[SPMV_PIPE_CHUNKS - 1], 0));
@@ -497,14 +517,16 @@ int spmv_common(int mode, int nrows, int ncols, int nnz, int* rowptr, int* col, 
     if (nrows == 0) return ok();
     return dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
         CsrPlanImpl p;
-        if (csr_plan_build(c, s, nrows, nnz, (const int*)st[0].dev, mode, &p)) return (int)cudaErrorUnknown;
+        if (csr_plan_build(c, s, nrows, nnz, (const int*)st[0].dev, mode, &p) || csr_plan_finalize(s, &p)) {
+            csr_plan_release(s, p);
+            return (int)cudaErrorUnknown;
+        }
         unsigned *tk = ticket_word(c, s), *fw = fault_word(c, s);
         if (!tk || !fw) return (int)cudaErrorMemoryAllocation;
         int e = launch_csr_spmv(s, mode, nrows, ncols, nnz, (const int*)st[0].dev, (const int*)st[1].dev,
                                 (const float*)st[2].dev, (const float*)st[3].dev, (float*)st[4].dev,
-                                p.tile_row, p.ntiles, p.flags, tk, fw);
-        pool_free(s, p.tile_row);
-        pool_free(s, p.flags);
+                                p.tile_row, p.ntiles, p.flags, p.seg_bits(), tk, fw);
+        csr_plan_release(s, p);
         return e;
     });
 }
@@ -837,7 +859,8 @@ int pencil_csr_plan_create(pencil_stream_t s, int nrows, int ncols, int nnz, con
     DEV_PROLOGUE;
     pencil_csr_plan* p = new pencil_csr_plan();
     p->ncols = ncols;
-    if (csr_plan_build(c, st, nrows, nnz, rowptr_dev, mode ? 1 : 0, p)) {
+    if (csr_plan_build(c, st, nrows, nnz, rowptr_dev, mode ? 1 : 0, p) || csr_plan_finalize(st, p)) {
+        csr_plan_release(st, *p);
         delete p;
         return g_status;
     }
@@ -849,6 +872,7 @@ int pencil_csr_plan_destroy(pencil_csr_plan_t plan) {
     if (!plan) return ok();
     cudaFree(plan->tile_row);  // pool memory: freed through the device's default stream order
     cudaFree(plan->flags);
+    if (plan->rs_bits) cudaFree(plan->rs_bits);
     delete plan;
     return ok();
 }
@@ -867,7 +891,7 @@ int pencil_spmv_dev(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr
     unsigned *tk = ticket_word(c, st), *fw = fault_word(c, st);
     if (!tk || !fw) return g_status;
     DEV_RET(launch_csr_spmv(st, plan->mode, plan->nrows, plan->ncols, plan->nnz, rowptr, col, val, x, y,
-                            plan->tile_row, plan->ntiles, plan->flags, tk, fw));
+                            plan->tile_row, plan->ntiles, plan->flags, plan->seg_bits(), tk, fw));
 }
 
 int pencil_spmv_dev_dist(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr, const int* col,
@@ -887,7 +911,7 @@ int pencil_spmv_dev_dist(pencil_stream_t s, pencil_csr_plan_t plan, const int* r
     unsigned *tk = ticket_word(c, st), *fw = fault_word(c, st);
     if (!tk || !fw) return g_status;
     DEV_RET(launch_csr_spmv_dist(st, plan->mode, plan->nrows, plan->ncols, plan->nnz, rowptr, col, val, x, y,
-                                 plan->tile_row, plan->ntiles, plan->flags, tk, fw, ps));
+                                 plan->tile_row, plan->ntiles, plan->flags, plan->seg_bits(), tk, fw, ps));
 }
 
 int pencil_sync_status(pencil_stream_t s) {
