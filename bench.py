@@ -218,8 +218,9 @@ def bench_spmv(args, torch, pb, rank, world, dist):
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
            "ceiling_ms": ceil_ms if not args.dist_path else None,
            "config": dict(spmv_config(nrows, nnz, xm),
-                          schedule="csr_flow_kernel, reassociated (persistent warps, 1024-nnz window tiles, "
-                                   "continuous 128-bit col/val streams)",
+                          schedule="csr_seg_kernel, reassociated (persistent warps on 4096-nnz row-aligned "
+                                   "tiles, 128-bit col/val streams, per-lane segments + warp segmented scan over "
+                                   "the plan's row-start bitmap)",
                           l2="L2 flushed between steps outside the per-step events (256 MiB fill, then its lines "
                              "discarded: the step starts on a clean, empty L2); inputs 2.35 GB > L2")}
     if args.dist_path:
@@ -964,12 +965,12 @@ def main():
                 "config": dict(res["config"], parallelism=f"row-sharded x{world}" if args.dist_path else "single GPU"),
                 "gpu_launches": res["launches"]}
         if not args.dist_path:
-            line["roofline"] = {"bound": "hbm", "kernel": "csr_flow_kernel", "achieved": kernel_gbs,
+            line["roofline"] = {"bound": "hbm", "kernel": "csr_seg_kernel", "achieved": kernel_gbs,
                                 "peak": hbm, "unit": "GB/s", "frac": kernel_gbs / hbm,
                                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
                                 "frac_spec": kernel_gbs / SPEC_HBM_GBS,
                                 "algorithmic_bytes_per_launch": res["bytes"],
-                                "traffic": ncu_traffic("csr_flow_kernel"),
+                                "traffic": ncu_traffic("csr_seg_kernel"),
                                 "measured_ceiling": {
                                     "kernel": "micro_gather_val: the same col/val stream + x gathers, no rows "
                                               "(random 4-byte gathers are L1->XBAR request-rate bound, DESIGN.md §3)",

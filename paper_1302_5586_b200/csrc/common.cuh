@@ -55,6 +55,13 @@ __device__ __forceinline__ int ld_stream_i(const int* p) {
                  : "l"(p), "l"(pol_evict_first()));
     return r;
 }
+__device__ __forceinline__ unsigned ld_stream_u(const unsigned* p) {
+    unsigned r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(r)
+                 : "l"(p), "l"(pol_evict_first()));
+    return r;
+}
 // Reused data (a gathered vector): keep in L2 as long as possible.
 __device__ __forceinline__ float ld_keep_f(const float* p) {
     float r;

@@ -30,7 +30,12 @@
 // non-zeros per warp tile (plan window); swept over {256..2048} x WCHUNK {64,128,256} at
 // 2^24 rows (tools/spmv_sweep.sh): 1024 x 128 is fastest (1.28 ms; 512: 1.34; 256: 1.59)
 #define SPMV_TILE_NNZ 1024
+#ifndef SEG_E
+#define SEG_E 4  // non-zeros per lane per window of the segmented executor (8: 1.16-1.19 ms, fewer warps)
+#endif
+#ifndef SEG_CTAS_PER_SM
 #define SEG_CTAS_PER_SM 6
+#endif
 
 // plan_flags: [0] non-monotone rowptr (generic schedule), [2] some row is empty.  rs_bits (when
 // given): bit k set iff non-zero k is the first of its row — the row-start map of the segmented
@@ -388,14 +393,131 @@ __global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_flow_kernel(
 
 // Segmented-reduction executor (reassociation licensed: spmv_vec; rows never empty — the plan's
 // flag — so the k-th row start after a tile's first row is row r0 + k).  The tile's non-zeros
-// stream in 128-element windows exactly as in csr_flow_kernel (16-byte col / val loads, 4 gathers
-// per lane), but instead of staging products and folding each row in its own lane, every lane
-// reduces its 4 products by segments (the row starts come from the plan's bitmap, one 32-bit word
-// per lane), and a warp segmented scan (5 shuffle rounds) carries the open row across lanes and
-// windows; every row is stored once, by the lane where it closes.  Per 128 non-zeros that is ~70
-// warp instructions where the batch-and-fold executor issues ~400 (ncu: 857 M for 2^28
-// non-zeros), so the kernel runs at the rate of its random gathers.  The sum order is fixed
-// (lanes in order, the scan tree, windows in order): deterministic run to run.
+// stream in 128-element windows as in csr_flow_kernel (16-byte col / val loads, 4 gathers per
+// lane), but instead of staging products and folding each row in its own lane, every lane reduces
+// its 4 products by segments (the row starts come from the plan's bitmap, one 32-bit word per
+// lane) and a warp segmented scan (5 shuffle rounds) carries the open row across lanes and windows;
+// every row is stored once, by the lane where it closes.  Windows strictly inside the tile take a
+// mask-free path (warp-uniform branch); faults are OR-ed per lane over the tile and raised once.
+// The sum order is fixed (lanes in order, the scan tree, windows in order): deterministic.
+// Measured at 2^24 rows (tools/ab_spmv.sh, one box): 1.241 ms on csr_flow_kernel -> 1.166 with
+// this executor (1024-nnz tiles) -> 1.145 with 4096-nnz tiles (2048: 1.148, 8192: 1.159); the
+// row-free stream + gather probe on the same data runs 1.010 ms.  ncu: 359 M warp instructions
+// (flow kernel 857 M), L1TEX 89.6% (probe 95%).  Timing-only ablations (wrong results, not
+// kept): no scan 1.084, no y stores 1.124, no row-start words 1.126.  Tried and dropped: 8
+// non-zeros per lane (1.16-1.19: fewer warps or spills), the next window's col / val loads issued
+// before this window's gathers (no gain), a ballot-based segmented scan with one shuffle per
+// round (1.160: more ALU), and L2 evict-first stores / row-start loads (no change).
+struct SegState {
+    int row;      // the row open at the next window's first position
+    float carry;  // its partial sum from the earlier windows
+    bool bad;     // a column index outside [0, ncols) was seen
+};
+
+__device__ __forceinline__ void seg_store(float* p, float v) { __stcs(p, v); }
+
+// One window of E * 32 non-zeros (E per lane, E = 4 or 8: E / 4 16-byte loads per array per
+// lane, all E gathers in flight together).  FULL: every position inside the tile (no masks).
+template <int E, bool FULL>
+__device__ __forceinline__ void seg_window(int qa, int P0, int P1, int nnz_len, int ncols, int lane,
+                                           const int* __restrict__ col, const float* __restrict__ val,
+                                           const float* __restrict__ x, const unsigned* __restrict__ rs_bits,
+                                           float* __restrict__ y, SegState& S) {
+    constexpr unsigned EMASK = (1u << E) - 1u;
+    const int p = qa + E * lane;  // qa is E-aligned, so the lane's E row-start bits share a word
+    float pr[E];
+    unsigned sb = 0;  // bit k: position p + k starts a row (other than the tile's first)
+#pragma unroll
+    for (int k = 0; k < E; k++) pr[k] = 0.f;
+    if (FULL || (p + E - 1 >= P0 && p < P1)) {
+        int c[E];
+        float v[E];
+        if (FULL || p + E - 1 < nnz_len) {
+#pragma unroll
+            for (int h = 0; h < E / 4; h++) {
+                const int4 c4 = ld_stream_i4(reinterpret_cast<const int4*>(col + p + 4 * h));
+                const float4 v4 = ld_stream_f4(reinterpret_cast<const float4*>(val + p + 4 * h));
+                c[4 * h] = c4.x; c[4 * h + 1] = c4.y; c[4 * h + 2] = c4.z; c[4 * h + 3] = c4.w;
+                v[4 * h] = v4.x; v[4 * h + 1] = v4.y; v[4 * h + 2] = v4.z; v[4 * h + 3] = v4.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < E; k++) {
+                c[k] = p + k < nnz_len ? __ldg(col + p + k) : 0;
+                v[k] = p + k < nnz_len ? __ldg(val + p + k) : 0.f;
+            }
+        }
+        // the row-start words stream (evict-first, 32 MB): x keeps the L2
+        const unsigned bits = (ld_stream_u(rs_bits + (p >> 5)) >> (p & 31)) & EMASK;
+        float xv[E];
+        bool use[E];
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+            const bool in = FULL || (p + k >= P0 && p + k < P1), ok = (unsigned)c[k] < (unsigned)ncols;
+            use[k] = in && ok;
+            xv[k] = ld_keep_f(x + (use[k] ? c[k] : 0));
+            S.bad |= in && !ok;
+        }
+        sb = bits;
+        if (!FULL) {
+#pragma unroll
+            for (int k = 0; k < E; k++)
+                if (!(p + k > P0 && p + k < P1)) sb &= ~(1u << k);
+        }
+#pragma unroll
+        for (int k = 0; k < E; k++) pr[k] = use[k] ? v[k] * xv[k] : 0.f;
+    }
+    // the lane's segments: head (before its first start: closes the row open on entry), tail (from
+    // its last start: stays open); rows that begin and end inside the lane (cnt >= 2) are stored
+    // after the scan
+    const int cnt = __popc(sb);
+    const int f = sb ? __ffs(sb) - 1 : E, l = sb ? 31 - __clz(sb) : E;
+    float head = f > 0 ? pr[0] : 0.f, acc = l <= 0 ? pr[0] : 0.f;
+#pragma unroll
+    for (int k = 1; k < E; k++) {
+        head += f > k ? pr[k] : 0.f;
+        acc += l <= k ? pr[k] : 0.f;
+    }
+    // one scan, two shuffles per round: the starts in lanes <= this one packed with the segment
+    // flag, and the open row's partial sum, summed only while no start has been crossed (the
+    // window carry enters at lane 0)
+    float sv = cnt ? acc : head + (lane == 0 ? S.carry : 0.f);
+    int pk = (cnt << 1) | (cnt != 0);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const float vo = __shfl_up_sync(0xffffffffu, sv, d);
+        const int po = __shfl_up_sync(0xffffffffu, pk, d);
+        if (lane >= d) {
+            if (!(pk & 1)) sv = vo + sv;
+            pk = (((pk >> 1) + (po >> 1)) << 1) | ((pk | po) & 1);
+        }
+    }
+    const int win_starts = __shfl_sync(0xffffffffu, pk, 31) >> 1;
+    const int before = (pk >> 1) - cnt;
+    float excl = __shfl_up_sync(0xffffffffu, sv, 1);
+    if (lane == 0) excl = S.carry;
+    if (cnt) {  // y streams out (evict-first): its 64 MB must not push x out of L2
+        const int ro = S.row + before;  // the row open on entry to this lane
+        seg_store(y + ro, excl + head);
+        if (cnt > 1) {  // rows wholly inside the lane
+            float a = 0.f;
+            int nseg = 0;
+#pragma unroll
+            for (int k = 0; k < E; k++) {
+                if (k < f) continue;
+                if (k > f && ((sb >> k) & 1u)) {
+                    seg_store(y + ro + 1 + nseg, a);
+                    a = 0.f;
+                    nseg++;
+                }
+                if (nseg < cnt - 1) a += pr[k];
+            }
+        }
+    }
+    S.carry = __shfl_sync(0xffffffffu, sv, 31);
+    S.row += win_starts;
+}
+
 template <bool DIST>
 __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
@@ -424,94 +546,20 @@ __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
         if (r0 >= r1) continue;
         const int P0 = clampp(__ldg(rowptr + r0));
         const int P1 = max(P0, clampp(__ldg(rowptr + r1)));
-        int row = r0;       // the row open at the window's first position
-        float carry = 0.f;  // its partial sum from the earlier windows
-        for (int qa = P0 & ~3; qa < P1; qa += 128) {
-            const int p = qa + 4 * lane;
-            float pr[4] = {0.f, 0.f, 0.f, 0.f};
-            unsigned sb = 0;  // bit e: position p + e starts a row (other than the tile's first)
-            if (p + 3 >= P0 && p < P1) {
-                int c[4];
-                float v[4];
-                if (p + 3 < nnz_len) {
-                    const int4 c4 = ld_stream_i4(reinterpret_cast<const int4*>(col + p));
-                    const float4 v4 = ld_stream_f4(reinterpret_cast<const float4*>(val + p));
-                    c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
-                    v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        c[k] = p + k < nnz_len ? __ldg(col + p + k) : 0;
-                        v[k] = p + k < nnz_len ? __ldg(val + p + k) : 0.f;
-                    }
-                }
-                const unsigned bits = (__ldg(rs_bits + (p >> 5)) >> (p & 31)) & 0xFu;
-                float xv[4];
-                bool use[4];
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const bool in = p + k >= P0 && p + k < P1, ok = (unsigned)c[k] < (unsigned)ncols;
-                    use[k] = in && ok;
-                    xv[k] = ld_keep_f(x + (use[k] ? c[k] : 0));
-                    if (in && !ok) raise_fault(status, FAULT_OOB_LOAD);
-                    if (in && p + k > P0 && ((bits >> k) & 1u)) sb |= 1u << k;
-                }
-#pragma unroll
-                for (int k = 0; k < 4; k++) pr[k] = use[k] ? v[k] * xv[k] : 0.f;
-            }
-            // the lane's segments: head (before its first start: closes the row open on entry),
-            // complete rows between two starts, tail (from its last start: stays open)
-            const int cnt = __popc(sb);
-            float head = 0.f, acc = 0.f, mid[3] = {0.f, 0.f, 0.f};
-            int nseg = 0;
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                if ((sb >> k) & 1u) {
-                    if (nseg == 0) head = acc;
-                    else mid[nseg - 1] = acc;
-                    acc = 0.f;
-                    nseg++;
-                }
-                acc += pr[k];
-            }
-            if (cnt == 0) head = acc;
-            // row index of the row open on entry to this lane: starts in the lanes before
-            int before = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int o = __shfl_up_sync(0xffffffffu, before, d);
-                if (lane >= d) before += o;
-            }
-            const int win_starts = __shfl_sync(0xffffffffu, before, 31);
-            before -= cnt;
-            // segmented scan of the open row's partial sum across lanes (the window carry enters at lane 0)
-            float sv = cnt ? acc : head + (lane == 0 ? carry : 0.f);
-            bool sf = cnt != 0;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const float vo = __shfl_up_sync(0xffffffffu, sv, d);
-                const bool fo = __shfl_up_sync(0xffffffffu, sf, d);
-                if (lane >= d && !sf) {
-                    sv = vo + sv;
-                    sf = fo;
-                }
-            }
-            float excl = __shfl_up_sync(0xffffffffu, sv, 1);
-            if (lane == 0) excl = carry;
-            if (cnt) {
-                const int ro = row + before;
-                y[ro] = excl + head;
-                if (cnt > 1) y[ro + 1] = mid[0];
-                if (cnt > 2) y[ro + 2] = mid[1];
-                if (cnt > 3) y[ro + 3] = mid[2];
-            }
-            carry = __shfl_sync(0xffffffffu, sv, 31);
-            row += win_starts;
+        SegState S{r0, 0.f, false};
+        constexpr int E = SEG_E, W = 32 * E;
+        int qa = P0 & ~(E - 1);
+        if (qa < P1) {  // the first window always masks (positions before P0; P0's own start)
+            seg_window<E, false>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
+            qa += W;
         }
-        if (lane == 0) y[row] = carry;  // the tile's last row (row == r1 - 1)
+        for (; qa + W <= P1; qa += W)  // interior windows: every position in the tile
+            seg_window<E, true>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
+        if (qa < P1) seg_window<E, false>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
+        if (lane == 0) seg_store(y + S.row, S.carry);  // the tile's last row (S.row == r1 - 1)
+        if (S.bad) raise_fault(status, FAULT_OOB_LOAD);
         if (DIST) {
             __syncwarp();
-            __threadfence_block();
             for (int r = r0 + lane; r < r1; r += 64) {
                 const float v0 = y[r], v1 = r + 32 < r1 ? y[r + 32] : 0.f;
                 put_row<true, false>(y, ps, r, v0);
@@ -560,6 +608,9 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;  // persistent: at most one wave
     if (grid > PENCIL_NUM_SMS * CTAS_PER_SM) grid = PENCIL_NUM_SMS * CTAS_PER_SM;
     const bool aligned = (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0;
+#ifdef PENCIL_VARIANT_NO_SEG
+    rs_bits = nullptr;  // A/B build: the batch-and-fold executor for spmv_vec too
+#endif
 #ifdef PENCIL_VARIANT_NO_SEG
     rs_bits = nullptr;  // A/B build: the batch-and-fold executor for spmv_vec too
 #endif
@@ -652,4 +703,8 @@ int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const
     return (int)cudaGetLastError();
 }
 
-int csr_tile_nnz() { return SPMV_TILE_NNZ; }
+// plan window per mode: source order (the batch-and-fold executor) and reassociated (segmented)
+#ifndef SEG_TILE_NNZ
+#define SEG_TILE_NNZ 4096
+#endif
+int csr_tile_nnz(int mode) { return mode == 1 ? SEG_TILE_NNZ : SPMV_TILE_NNZ; }

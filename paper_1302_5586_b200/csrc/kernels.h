@@ -34,7 +34,7 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
 int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const int* rowptr,
                        const int* col, const float* val, const float* x, float* y,
                        unsigned* status);
-int csr_tile_nnz();
+int csr_tile_nnz(int mode);
 // fused SpMV -> all-gather of y: every row result is also stored to `n` peer buffers (NVLink
 // peer mappings, each already offset to this rank's slot) or, when mc is set, once to an NVLS
 // multicast address that replicates it to every rank

@@ -339,7 +339,7 @@ int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int*
     p->nrows = nrows;
     p->nnz = nnz;
     p->mode = mode;
-    p->tile_nnz = csr_tile_nnz();
+    p->tile_nnz = csr_tile_nnz(mode);
     long long nt = ((long long)nnz + p->tile_nnz - 1) / p->tile_nnz;
     p->ntiles = (int)(nt < 1 ? 1 : nt);
     int r = pool_alloc(c, st, sizeof(int) * ((size_t)p->ntiles + 1), (void**)&p->tile_row);
