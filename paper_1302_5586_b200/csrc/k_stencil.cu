@@ -946,6 +946,200 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int
     cp_wait<0>();
 }
 
+// ---------------------------------------------------------------- signed 2-D SWAR packed-byte sweep
+// Taps with a non-negative centre and non-positive off-centre taps (sharpen, Laplacian and
+// unsharp-mask shapes — the signed sharpen of the config), power-of-two scale: every off-centre
+// product k x = |k| (255 - x) - 255 |k| runs on the complemented byte, so the sum
+//   acc' = kc x_c + sum |k| (255 - x) = acc + B,   B = 255 * sum |k_off| >= 0
+// is non-negative and, when 255 * (kc + sum |k_off|) + scale / 2 < 65536, fits a 16-bit SWAR
+// lane: one IMAD per tap per two pixels, no int -> float conversion.  Requantisation per lane:
+// (max(acc' + scale/2, B) - B) >> shift, then min 255 (C truncation and the [0, 255] clamp: a
+// negative numerator gives 0 either way).  Rows are pushed: the row entering the window adds its
+// taps to the five output rows it feeds (5 x NP/2 accumulators), and the output row it completes
+// is requantised and stored.  Integer arithmetic throughout: bit-identical to the other kernels.
+// DIA: the 12 corner taps are zero (skipped at compile time).
+struct Swar2dArgs {
+    unsigned kc;         // centre tap (>= 0)
+    unsigned kn[25];     // |off-centre taps| (kn[12] unused)
+    unsigned bias_half;  // (B + scale / 2) in both 16-bit lanes
+    unsigned bias2;      // B in both lanes
+    int shift;           // log2(scale) <= 8
+};
+
+__device__ __forceinline__ unsigned umax16x2(unsigned a, unsigned b) {
+    unsigned r;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned umin16x2(unsigned a, unsigned b) {
+    unsigned r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+// The row entering the window as byte pairs: Qc[m] = complemented (e[c-2+m], e[c+m]) in 16-bit
+// lanes (m = 0..NP+1), Qp[t] = the plain centre pairs of output pair t (pixels c+4g+p, +2).
+template <int NP>
+__device__ __forceinline__ void swar2d_enter(const unsigned char* slot, int w, int c0, int lane,
+                                             unsigned (&Qc)[NP + 2], unsigned (&Qp)[NP / 2]) {
+    typedef SwarGeom<NP> G;
+    const unsigned* wp = reinterpret_cast<const unsigned*>(slot + G::PAD - 4 + NP * lane);
+    unsigned Wd[G::NW + 2];
+#pragma unroll
+    for (int k = 0; k < G::NW + 2; k++) Wd[k] = wp[k];
+    if (c0 == 0 || c0 + 32 * NP >= w) {  // image-edge strips: clamp-to-edge columns
+        const int c = c0 + NP * lane;
+        unsigned v[NP + 4];
+#pragma unroll
+        for (int m = 0; m < NP + 4; m++) v[m] = slot[clampi(c - 2 + m, 0, w - 1) - (c0 - G::PAD)];
+        Wd[0] = (v[0] << 16) | (v[1] << 24);
+#pragma unroll
+        for (int k = 0; k < G::NW; k++)
+            Wd[k + 1] = v[4 * k + 2] | (v[4 * k + 3] << 8) | (v[4 * k + 4] << 16) | (v[4 * k + 5] << 24);
+        Wd[G::NW + 1] = v[NP + 2] | (v[NP + 3] << 8);
+    }
+#pragma unroll
+    for (int k = 0; k <= 2 * G::NW; k++) {
+        const unsigned X = (k & 1) ? Wd[k / 2 + 1] : __funnelshift_r(Wd[k / 2], Wd[k / 2 + 1], 16);
+        const unsigned lo = __byte_perm(X, 0u, 0x4240), hi = __byte_perm(X, 0u, 0x4341);
+        Qc[2 * k] = lo ^ 0x00ff00ffu;
+        Qc[2 * k + 1] = hi ^ 0x00ff00ffu;
+        // centre pairs: m = b + 2 with b = p + 4g  ->  m = 4g + 2 + p
+        if ((2 * k) % 4 == 2 && (2 * k - 2) / 4 < NP / 4) Qp[2 * ((2 * k - 2) / 4)] = lo;
+        if ((2 * k + 1) % 4 == 3 && (2 * k - 2) / 4 < NP / 4) Qp[2 * ((2 * k - 2) / 4) + 1] = hi;
+    }
+}
+
+template <bool DIA>
+__device__ __forceinline__ constexpr bool tap_on(int di, int dj) {
+    return !DIA || ((di > 2 ? di - 2 : 2 - di) + (dj > 2 ? dj - 2 : 2 - dj) <= 2);
+}
+
+// Row r (slot S = r mod 5 of the rotation) enters: A[(r - di + 2) mod 5] += taps of row di.
+// Then output row r - 2 is complete: requantise, store (when it lies in [i0, i1)), reset.
+template <int NP, int S, bool DIA>
+__device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c, int lane, int r_end, bool body,
+                                            bool halo, unsigned char (*ring)[SwarGeom<NP>::ROWE],
+                                            unsigned (&A)[5][NP / 2], Sweep<unsigned char>& sw,
+                                            const Swar2dArgs& a) {
+    cp_wait<S_RING - 1>();
+    __syncwarp();
+    unsigned char* slot = ring[(r + S_RING) % S_RING];
+    unsigned Qc[NP + 2], Qp[NP / 2];
+    swar2d_enter<NP>(slot, w, c - NP * lane, lane, Qc, Qp);
+    __syncwarp();
+    if (r + S_RING < r_end) swar_issue<NP>(sw.src > sw.src_last ? sw.src_last : sw.src, slot, lane, body, halo);
+    cp_commit();
+    sw.src += sw.w;
+#pragma unroll
+    for (int di = 0; di < 5; di++) {
+        const int o = (S - di + 2 + 5) % 5;  // accumulator slot of output row r - di + 2
+#pragma unroll
+        for (int t = 0; t < NP / 2; t++) {
+            const int b = (t & 1) + 4 * (t >> 1);
+            unsigned acc = A[o][t];
+#pragma unroll
+            for (int dj = 0; dj < 5; dj++) {
+                if (!tap_on<DIA>(di, dj)) continue;
+                if (di == 2 && dj == 2) acc += a.kc * Qp[t];
+                else acc += a.kn[di * 5 + dj] * Qc[b + dj];
+            }
+            A[o][t] = acc;
+        }
+    }
+    // output row r - 2 (slot (S + 3) % 5 = (r - 2) mod 5) is complete
+    constexpr int D = (S + 3) % 5;
+    const int orow = r - 2;
+    if (orow >= i0 && orow < i1 && body) {
+        unsigned q[NP / 2];
+#pragma unroll
+        for (int t = 0; t < NP / 2; t++) {
+            unsigned v = umax16x2(A[D][t], a.bias2) - a.bias2;  // the numerator, clamped at 0
+            v = (v >> a.shift) & ((0xffffu >> a.shift) * 0x00010001u);
+            q[t] = umin16x2(v, 0x00ff00ffu);
+        }
+        unsigned rr[NP / 4];
+#pragma unroll
+        for (int g = 0; g < NP / 4; g++) rr[g] = __byte_perm(q[2 * g], q[2 * g + 1], 0x6240);
+        unsigned char* dst = sw.dst + (long long)(orow - i0) * w;
+        if constexpr (NP == 16) *reinterpret_cast<uint4*>(dst) = make_uint4(rr[0], rr[1], rr[2], rr[3]);
+        else *reinterpret_cast<uint2*>(dst) = make_uint2(rr[0], rr[1]);
+    }
+#pragma unroll
+    for (int t = 0; t < NP / 2; t++) A[D][t] = a.bias_half;
+}
+
+template <int NP, bool DIA>
+__global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_kernel(int h, int w,
+                                                                             const unsigned char* __restrict__ img,
+                                                                             unsigned char* __restrict__ out,
+                                                                             Swar2dArgs a) {
+    typedef SwarGeom<NP> G;
+    __shared__ __align__(16) unsigned char ring_all[S_WARPS][S_RING][G::ROWE];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = (blockIdx.x * S_WARPS + warp) * 32 * NP;
+    if (c0 >= w) return;
+    const int c = c0 + NP * lane;
+    const int i0 = blockIdx.y * S_BAND, i1 = min(h, i0 + S_BAND);
+    if (i0 >= i1) return;
+    const int r_begin = i0 - 2, r_end = i1 + 2;  // input rows of the band (clamped at the image edges)
+    const bool body = c + NP - 1 < w;
+    const bool halo = (lane == 0 && c0 > 0) || (lane == 31 && c0 + 32 * NP < w);
+    unsigned char(*ring)[G::ROWE] = ring_all[warp];
+    auto row = [&](int r) { return img + (long long)clampi(r, 0, h - 1) * w + c; };
+#pragma unroll
+    for (int d = 0; d < S_RING; d++) {
+        if (r_begin + d < r_end) swar_issue<NP>(row(r_begin + d), ring[(r_begin + d + S_RING) % S_RING], lane, body, halo);
+        cp_commit();
+    }
+    unsigned A[5][NP / 2];
+#pragma unroll
+    for (int q = 0; q < 5; q++)
+#pragma unroll
+        for (int t = 0; t < NP / 2; t++) A[q][t] = a.bias_half;
+    Sweep<unsigned char> sw;
+    sw.w = w;
+    sw.src_last = img + (long long)(h - 1) * w + c;
+    sw.src = img + (long long)(r_begin + S_RING) * w + c;
+    sw.dst = out + (long long)i0 * w + c;
+    // the rotation slot of row r is r mod 5; start at a multiple of 5 at or below r_begin so the
+    // slots stay compile-time constants (rows before r_begin are skipped)
+    const int rb5 = r_begin - ((r_begin % 5) + 5) % 5;
+    for (int r = rb5; r < r_end; r += 5) {
+        if (r + 0 >= r_begin) swar2d_step<NP, 0, DIA>(w, r + 0, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        if (r + 1 >= r_begin && r + 1 < r_end) swar2d_step<NP, 1, DIA>(w, r + 1, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        if (r + 2 >= r_begin && r + 2 < r_end) swar2d_step<NP, 2, DIA>(w, r + 2, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        if (r + 3 >= r_begin && r + 3 < r_end) swar2d_step<NP, 3, DIA>(w, r + 3, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        if (r + 4 >= r_begin && r + 4 < r_end) swar2d_step<NP, 4, DIA>(w, r + 4, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+    }
+    cp_wait<0>();
+}
+
+// Swar2dArgs for taps with kc >= 0, every off-centre tap <= 0, a power-of-two scale <= 256 and
+// every biased sum below 2^16; false otherwise.
+bool swar2d_args(const int* k, int scale, Swar2dArgs& a) {
+#ifdef PENCIL_VARIANT_NO_SWAR
+    return false;
+#endif
+    if (scale < 1 || scale > 256 || (scale & (scale - 1))) return false;
+    if (k[12] < 0) return false;
+    long long off = 0;
+    for (int t = 0; t < 25; t++) {
+        if (t == 12) continue;
+        if (k[t] > 0) return false;
+        off += -(long long)k[t];
+    }
+    const long long B = 255 * off;
+    if (255ll * ((long long)k[12] + off) + (scale >> 1) >= 65536) return false;
+    a.kc = (unsigned)k[12];
+    for (int t = 0; t < 25; t++) a.kn[t] = t == 12 ? 0u : (unsigned)(-(long long)k[t]);
+    a.bias_half = (unsigned)(B + (scale >> 1)) * 0x00010001u;
+    a.bias2 = (unsigned)B * 0x00010001u;
+    a.shift = 0;
+    while ((1 << a.shift) != scale) a.shift++;
+    return true;
+}
+
 // SwarArgs from the separable factorisation, or false (signs, sums >= 2^16, clamp needed).
 // (A/B builds: tools/variant_build.sh compiles -DPENCIL_VARIANT_NO_SWAR into variants/.)
 bool swar_args(const StencilArgs& s, int scale, SwarArgs& a) {
@@ -1219,6 +1413,7 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
     const bool sep = sep_enabled() && separable(k25, a), dia = !sep && diamond(k25);
     SwarArgs sa;
+    Swar2dArgs s2;
     if (sep && w % 8 == 0 && (uintptr_t)img % 8 == 0 && (uintptr_t)out % 8 == 0 && swar_args(a, scale, sa)) {
 #ifdef PENCIL_VARIANT_SWAR_NP8
         const int np_max = 8;
@@ -1232,6 +1427,15 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
         else if (n16) stencil_bytes_swar_kernel<16, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
         else if (sa.shift == 8) stencil_bytes_swar_kernel<8, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
         else stencil_bytes_swar_kernel<8, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+    } else if (!sep && w % 8 == 0 && (uintptr_t)img % 8 == 0 && (uintptr_t)out % 8 == 0 &&
+               swar2d_args(k25, scale, s2)) {
+        const bool n16 = w % 16 == 0 && (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0;
+        const int np = n16 ? 16 : 8;
+        dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
+        if (n16 && dia) stencil_bytes_swar2d_kernel<16, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+        else if (n16) stencil_bytes_swar2d_kernel<16, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+        else if (dia) stencil_bytes_swar2d_kernel<8, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+        else stencil_bytes_swar2d_kernel<8, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
     } else if (sep && a.shift >= 0) stencil_bytes_kernel<true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (sep) stencil_bytes_kernel<false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (dia && a.shift >= 0) stencil_bytes_kernel<true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);

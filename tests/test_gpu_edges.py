@@ -318,3 +318,35 @@ def test_conv_u8_bytes_swar_bit_exact(cuda, h, w):
         pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img.astype(np.uint8)).cuda(), k, out8)
         ref = oracle.conv5x5_u8(h, w, scale, img, k)
         assert np.array_equal(out8.cpu().numpy().astype(np.int64), ref), (h, w, scale)
+
+
+LAPLACE25 = np.array([[-1, -1, -1, -1, -1], [-1, -1, -1, -1, -1], [-1, -1, 48, -1, -1],
+                      [-1, -1, -1, -1, -1], [-1, -1, -1, -1, -1]], np.int32).reshape(-1)
+LAPLACE13 = np.array([[0, 0, -1, 0, 0], [0, -1, -2, -1, 0], [-1, -2, 16, -2, -1],
+                      [0, -1, -2, -1, 0], [0, 0, -1, 0, 0]], np.int32).reshape(-1)
+
+
+@pytest.mark.parametrize("h,w", [(70, 256), (33, 520), (64, 264), (9, 8), (5, 512), (130, 1024), (40, 1040),
+                                 (12, 16), (21, 1552), (3, 64), (1, 32), (2, 24)])
+def test_conv_u8_bytes_signed_swar_bit_exact(cuda, h, w):
+    """Centre-positive, off-centre non-positive taps (sharpen, Laplacians) with a power-of-two
+    scale take the signed SWAR kernel (complemented bytes, biased 16-bit sums, per-lane clamp):
+    diamond and full 5x5 supports, scales 1 .. 256, saturated rows, images shorter than the
+    window, strips at both edges and narrower than a warp — bit-exact against the oracle; taps
+    outside that shape (a positive off-centre tap, a negative centre, sums >= 2^16) take the other
+    kernels, also exact."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    img = synth.u8_i32(h * w, seed=h * 11 + w)
+    img[: min(h * w, 2 * w)] = 255
+    img[-min(h * w, w):] = 0
+    mixed = synth.SHARPEN.copy()
+    mixed[0] = 1  # a positive corner tap: not the signed SWAR shape
+    for k, scale in ((synth.SHARPEN, 1), (synth.SHARPEN, 2), (LAPLACE13, 1), (LAPLACE13, 4), (LAPLACE25, 1),
+                     (LAPLACE25, 16), (synth.SHARPEN * 7, 256), (LAPLACE25 * 10, 8), (mixed, 1),
+                     (-synth.SHARPEN, 1), (synth.SHARPEN, 3)):
+        out8 = torch.empty(h * w, dtype=torch.uint8, device="cuda")
+        pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img.astype(np.uint8)).cuda(), k, out8)
+        ref = oracle.conv5x5_u8(h, w, scale, img, k)
+        got = out8.cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, ref), (h, w, scale, int(k[12]), np.flatnonzero(got != ref)[:5])
