@@ -500,8 +500,8 @@ def suite(args, torch, pb, hbm):
     for name, taps, scale, kern, desc in (
             ("conv5x5_u8_bytes_16384", synth.BINOMIAL, 256, "stencil_bytes_swar_kernel<16, 1>",
              "binomial, scale 256 (16-bit SWAR sums, 16 px per lane)"),
-            ("conv5x5_u8_bytes_16384_sharpen", synth.SHARPEN, 1, "stencil_bytes_kernel<1, 0, 1>",
-             "signed sharpen (diamond support: DIA kernel), scale 1")):
+            ("conv5x5_u8_bytes_16384_sharpen", synth.SHARPEN, 1, "stencil_bytes_swar2d_kernel<16, 1>",
+             "signed sharpen (centre-positive, off-centre non-positive diamond taps: signed 2-D SWAR kernel), scale 1")):
         ms = statistics.mean(run_steps(torch, lambda: pb.device.conv5x5_u8_bytes(h, w_, scale, img8, taps, out8),
                                        k, w, flush))
         out[name] = bw_line(ms, b, hbm, kern, taps=desc, **{"Gpix/s": npx / ms / 1e6})
@@ -566,7 +566,7 @@ def suite(args, torch, pb, hbm):
         burst, sustained, kind = tf32x3_peaks()
         out["gemm_16384_3xtf32"] = {
             "ms": ms, "TFLOP/s": tf,
-            "roofline": roofline(tf, burst, "TFLOP/s", "gemm_3xtf32_2sm_kernel", flops, bound="tensor",
+            "roofline": roofline(tf, burst, "TFLOP/s", "gemm_3xtf32_kernel", flops, bound="tensor",
                                  peak_kind="%s: MEASURED_PEAKS bf16_tflops / 6 (3 tf32 MMAs per fp32 product, "
                                            "tf32 at half the bf16 rate), burst" % kind,
                                  frac_sustained=tf / sustained, peak_sustained=sustained,
@@ -745,7 +745,7 @@ def suite_dist(args, torch, pb, rank, world, dist, hbm):
         ms = statistics.mean(run_steps(torch, step, 5, 3, flush, dist))
         burst, sustained, _ = tf32x3_peaks()
         out["gemm_16384_3xtf32_grid"] = dist_line(
-            torch, dist, ms, 2.0 * m * n * kk, "TFLOP/s", burst, "gemm_3xtf32_2sm_kernel", 2.0 * mt * nt * kk,
+            torch, dist, ms, 2.0 * m * n * kk, "TFLOP/s", burst, "gemm_3xtf32_kernel", 2.0 * mt * nt * kk,
             {"grid": "%d x %d" % (tg.R, tg.C), "tile": "%d x %d" % (mt, nt),
              "collective": "none (A row panel + B column panel replicated per rank)"}, bound="tensor")
         if not args.no_e2e:

@@ -1,25 +1,37 @@
 // gemm.pencil.c on the 5th-generation tensor cores: C = alpha * A B + beta * C in fp32 via
 // 3xTF32 (tcgen05.mma kind::tf32, accumulators in TMEM, operands staged by TMA).
 //
-// Schedule (mapper): i, j ASSUMED_PARALLEL -> 2-D grid of 128 x 256 output tiles; p
-// PARALLEL_WITH_REDUCTION(+) -> the K loop is split across tensor-core MMAs (reassociates).
+// Schedule (mapper): i, j ASSUMED_PARALLEL -> 2-D grid of 256 x 256 output tiles, one per CTA
+// pair; p PARALLEL_WITH_REDUCTION(+) -> the K loop is split across tensor-core MMAs (reassociates).
 //
-// Precision: every fp32 operand is split once, by a prologue kernel, into tf32 hi = rna(x)
-// and lo = rna(x - hi); the kernel accumulates hi*hi + hi*lo + lo*hi in fp32 (TMEM) — the
-// dropped lo*lo term and the tf32 rounding of lo are ~2^-22 relative, well inside the 1e-5
-// normwise tolerance of the tests.  The prologue also writes B transposed (N x K, K-major)
-// and pads K to a multiple of BK with zeros, so every operand tile is a K-major 64-byte
-// swizzled TMA box and ragged M/N edges are zero-filled by the TMA unit.
+// Precision: x = hi + lo with hi = x truncated to tf32 (the tensor core reads only the sign,
+// exponent and top 10 mantissa bits of a 32-bit operand, so the raw fp32 tile IS the hi operand)
+// and lo = rna_tf32(x - hi) (x - hi is exact: at most the 13 dropped bits).  The kernel
+// accumulates lo*hi + hi*lo + hi*hi in fp32 (TMEM); the dropped lo*lo term (< 2^-20 |ab|) and the
+// tf32 rounding of lo (< 2^-22 |x|) stay well inside the 1e-5 normwise tolerance of the tests.
 //
-// Kernel anatomy (default: the CTA-pair kernel further down; single-CTA kernel here, 6 warps):
-//   warp 0  TMA producer: per K block of 16, four boxes (A_hi, A_lo 128x16; B_hi, B_lo 256x16)
-//           into a 4-stage smem ring (48 KB/stage), completion on the stage's `full` mbarrier
-//   warp 1  TMEM allocator + MMA issuer (one elected lane): 2 k-steps x 3 products
-//           tcgen05.mma.cta_group::1.kind::tf32 128x256x8 per stage, tcgen05.commit -> `empty`
-//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 (TMEM lane quarter = warp % 4) -> alpha, beta
-//           -> 128-bit global stores
-// Both kernels sustain ~240 TFLOP/s at 16384^3 (85-97% tensor-pipe activity) — the level of
-// the measured sustained bf16 rate / 6, i.e. the 1 kW power cap, not the kernel, is the limit.
+// No prologue, no workspace: A (M x K row-major) is read in place as a K-major operand, B (K x N
+// row-major) in place as an MN-major operand (tcgen05 takes tf32 in either major), both by TMA
+// straight from the caller's arrays; ragged M / N / K edges are zero-filled by the TMA unit.  Only
+// the lo halves are derived, on chip: per stage a converter warpgroup reads the 16 KB hi tile out
+// of shared memory and writes its lo twin next to it (elementwise, so the swizzled layout carries
+// over).  Operands whose row pitch is not a multiple of 16 bytes are first copied to a padded
+// pitch (`pack_rows_kernel`; the only case that needs a workspace).
+//
+// Kernel anatomy (persistent: one CTA pair per two SMs, tiles handed out statically in a grouped
+// raster; 10 warps per CTA):
+//   warp 0    TMA producer (both CTAs): per K block of 16, A box 128x16 (K-major, SW64) and four
+//             B boxes 32x16 (MN-major, SW128 with 32 B atoms) into a 6-stage ring of 32 KB (hi 16 KB + lo 16 KB),
+//             completion on the CTA's own `full` mbarrier
+//   warps 2-5 converters (both CTAs): wait `full`, lo = rna(x - trunc(x)) over the stage's hi
+//             bytes, fence.proxy.async, one arrive per warp on the leader's `conv` barrier
+//   warp 1    (leader CTA) TMEM allocator + MMA issuer (one elected lane): per K block 2 k-steps x
+//             3 products tcgen05.mma.cta_group::2.kind::tf32 256x256x8 into one of two TMEM
+//             accumulators (2 x 256 columns), tcgen05.commit multicast -> both CTAs' `empty`;
+//             after the tile's last block, commit -> `tmem_full`
+//   warps 6-9 epilogue (both CTAs): tcgen05.ld 32x32b.x32 (TMEM lane quarter = warp % 4) ->
+//             alpha, beta -> 128-bit stores, then one arrive per warp on the leader's
+//             `tmem_empty` — so tile t's epilogue overlaps tile t+1's main loop.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -27,20 +39,30 @@
 
 namespace {
 
-// BK fp32 per stage: 16 -> 64-byte operand rows (swizzle-64B), 4 stages of 48 KB in flight;
-// (BK 32 / swizzle-128B fits only 2 stages of 96 KB: measured 83% tensor-pipe activity)
-constexpr int BM = 128, BN = 256, BK = 16;
-constexpr int STAGES = 4;
-constexpr int ROW_BYTES = BK * 4;
-constexpr int ATOM_BYTES = 8 * ROW_BYTES;  // 8-row swizzle atom
-constexpr unsigned long long SW_LAYOUT = ROW_BYTES == 128 ? 2 : (ROW_BYTES == 64 ? 4 : 6);  // UMMA layout type
-constexpr int A_TILE = BM * BK * 4;  // 16 KB
-constexpr int B_TILE = BN * BK * 4;  // 32 KB
-constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
-constexpr int TMEM_COLS = 256;
-constexpr int GEMM_THREADS = 192;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int GROUP_M = 16;  // tile raster: groups of 16 M-tiles share B panels in L2
+constexpr int BK = 16;                   // fp32 per K block: 64-byte A rows (swizzle-64B)
+constexpr int TILE_M = 256, TILE_N = 256;  // per CTA pair
+constexpr int CTA_M = 128, CTA_N = 128;    // A rows / B columns staged by each CTA of the pair
+constexpr int A_BYTES = CTA_M * BK * 4;    // 8 KB
+constexpr int B_CHUNK = 32;                // B columns per 128-byte swizzle row
+constexpr int B_CHUNK_BYTES = B_CHUNK * BK * 4;  // 2 KB (16 K rows x 128 B)
+constexpr int B_BYTES = CTA_N * BK * 4;    // 8 KB = 4 chunks
+constexpr int HI_BYTES = A_BYTES + B_BYTES;
+constexpr int STAGE_BYTES = 2 * HI_BYTES;  // hi | lo
+constexpr int STAGES = 6;
+constexpr int GEMM_THREADS = 320;
+constexpr int CONV_WARP0 = 2, EPI_WARP0 = 6;
+constexpr int TMEM_COLS = 512;  // two 256-column fp32 accumulators
+constexpr int NUM_BARS = 3 * STAGES + 4;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + NUM_BARS * 8 + 16;
+#ifndef GEMM_GROUP_M_DEF
+#define GEMM_GROUP_M_DEF 8  // raster group in 256-row tiles (round 1 sweep 2/4/8/16: 8 best)
+#endif
+constexpr int GROUP_M = GEMM_GROUP_M_DEF;
+
+// idesc: D fp32 (bit 4), A tf32 [7,10), B tf32 [10,13), A K-major (bit 15 = 0), B MN-major
+// (bit 16 = 1), N >> 3 at [17,23), M >> 4 at [24,29)
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(TILE_N >> 3) << 17) |
+                           ((uint32_t)(TILE_M >> 4) << 24);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -61,6 +83,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// arrive on the same barrier in the leader CTA (cluster rank 0) — local for the leader itself.
+// Default (.release.cta) semantics, as the arrive that hands a stage to the MMA: a .cluster
+// release compiles to MEMBAR.ALL.GPU + ERRBAR per arrive and made the converters the bottleneck.
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* b) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(b)));
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
@@ -68,217 +107,268 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
-// K-major, ROW_BYTES-swizzled operand tile: 8-row swizzle atoms stacked every ATOM_BYTES
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+// A: K-major, 64-byte swizzle: 8-row atoms of 8 x 64 B stacked every 512 B (SBO)
+__device__ __forceinline__ uint64_t desc_a(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;                   // leading byte offset (unused for swizzled K-major)
-    d |= (uint64_t)(ATOM_BYTES >> 4) << 32;   // stride byte offset: next 8-row atom
-    d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
-    d |= (uint64_t)SW_LAYOUT << 61;           // SWIZZLE_64B / 128B
+    d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;     // SBO: next 8-row atom
+    d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
+    d |= (uint64_t)4 << 61;              // SWIZZLE_64B
     return d;
 }
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+// B: MN-major.  tf32 MN-major operands take only the 128-byte swizzle with 32-byte atoms
+// (SWIZZLE_128B_BASE32B: 128 B rows of 32 columns, one per k, the four 32 B granules of a row
+// permuted by (row mod 4) — TMA's SWIZZLE_128B_ATOM_32B): 4-k atoms every 512 B (SBO), 32-column
+// chunks every 2 KB (LBO)
+__device__ __forceinline__ uint64_t desc_b(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+#ifndef GEMM_DBG_SWAP_B
+    d |= (uint64_t)(B_CHUNK_BYTES >> 4) << 16;  // LBO: next 32-column chunk
+    d |= (uint64_t)(512 >> 4) << 32;            // SBO: next 4 k
+#else
+    d |= (uint64_t)(512 >> 4) << 16;
+    d |= (uint64_t)(B_CHUNK_BYTES >> 4) << 32;
+#endif
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)1 << 61;                     // SWIZZLE_128B_BASE32B
+    return d;
+}
+__device__ __forceinline__ void mma_tf32_2sm(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(IDESC), "r"(acc));
 }
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
+__device__ __forceinline__ void commit_2sm(uint64_t* bar) {  // arrive on bar in both CTAs
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t lo_tf32(uint32_t x) {
+    const float r = __uint_as_float(x) - __uint_as_float(x & 0xffffe000u);  // exact
+    uint32_t l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+    return l;
 }
 
-// idesc: D fp32, A/B tf32, both K-major, N>>3 at [17,23), M>>4 at [24,29)
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+struct TileRaster {
+    int tiles_m, tiles_n;
+    __device__ void at(int t, int& tm, int& tn) const {
+        const int group = t / (GROUP_M * tiles_n);
+        const int first_m = group * GROUP_M;
+        const int gsize = min(tiles_m - first_m, GROUP_M);
+        tm = first_m + (t % (GROUP_M * tiles_n)) % gsize;
+        tn = (t % (GROUP_M * tiles_n)) / gsize;
+    }
+};
 
-__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_3xtf32_kernel(
-    const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
-    const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo, int M, int N,
-    int Kp, float alpha, float beta, float* __restrict__ C) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, int M,
+                       int N, int K, float alpha, float beta, float* __restrict__ C) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* accum = empty + STAGES;
-    uint32_t* tmem_slot = (uint32_t*)(accum + 1);
+    uint64_t* conv = full + STAGES;
+    uint64_t* empty = conv + STAGES;
+    uint64_t* tmem_full = empty + STAGES;  // [2]
+    uint64_t* tmem_empty = tmem_full + 2;  // [2]
+    uint32_t* tmem_slot = (uint32_t*)(tmem_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // grouped raster over output tiles
-    const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
-    const int tid = blockIdx.x;
-    const int group = tid / (GROUP_M * tiles_n);
-    const int first_m = group * GROUP_M;
-    const int gsize = min(tiles_m - first_m, GROUP_M);
-    const int tm = first_m + (tid % (GROUP_M * tiles_n)) % gsize;
-    const int tn = (tid % (GROUP_M * tiles_n)) / gsize;
-    const int m0 = tm * BM, n0 = tn * BN;
-    const int nk = Kp / BK;
+    const uint32_t rank = cta_rank();
+    const TileRaster ras{(M + TILE_M - 1) / TILE_M, (N + TILE_N - 1) / TILE_N};
+    const int ntiles = ras.tiles_m * ras.tiles_n;
+    const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    const int nk = (K + BK - 1) / BK;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&full[s], 1);
+            mbar_init(&conv[s], 2 * 4);  // 4 converter warps in each CTA
             mbar_init(&empty[s], 1);
         }
-        mbar_init(accum, 1);
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tmem_full[b], 1);
+            mbar_init(&tmem_empty[b], 2 * 4);  // 4 epilogue warps in each CTA
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_ahi) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_alo) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_bhi) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_blo) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_b) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    cluster_sync_all();  // barrier inits and the TMEM allocation visible to the peer CTA
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
-            for (int kb = 0; kb < nk; kb++) {
-                const int s = kb % STAGES;
-                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-                uint8_t* st = smem + s * STAGE_BYTES;
-                mbar_expect_tx(&full[s], STAGE_BYTES);
-                tma_load_2d(st, &tm_ahi, &full[s], kb * BK, m0);
-                tma_load_2d(st + A_TILE, &tm_alo, &full[s], kb * BK, m0);
-                tma_load_2d(st + 2 * A_TILE, &tm_bhi, &full[s], kb * BK, n0);
-                tma_load_2d(st + 2 * A_TILE + B_TILE, &tm_blo, &full[s], kb * BK, n0);
+            int g = 0;
+            for (int t = cluster; t < ntiles; t += nclusters) {
+                int tm, tn;
+                ras.at(t, tm, tn);
+                const int m0 = tm * TILE_M + (int)rank * CTA_M;
+                const int nb = tn * TILE_N + (int)rank * CTA_N;
+                for (int kb = 0; kb < nk; kb++, g++) {
+                    const int s = g % STAGES;
+                    mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+                    uint8_t* st = smem + s * STAGE_BYTES;
+                    mbar_expect_tx(&full[s], HI_BYTES);
+                    tma_load_2d(st, &tm_a, &full[s], kb * BK, m0);
+#pragma unroll
+                    for (int c = 0; c < CTA_N / B_CHUNK; c++)
+                        tma_load_2d(st + A_BYTES + c * B_CHUNK_BYTES, &tm_b, &full[s], nb + c * B_CHUNK, kb * BK);
+                }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer
-            for (int kb = 0; kb < nk; kb++) {
-                const int s = kb % STAGES;
-                mbar_wait(&full[s], (kb / STAGES) & 1);
+        if (rank == 0 && lane == 0) {  // MMA issuer (leader CTA)
+            int g = 0, i = 0;
+            for (int t = cluster; t < ntiles; t += nclusters, i++) {
+                const int b = i & 1;
+                mbar_wait(&tmem_empty[b], ((i >> 1) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
-                const uint64_t ahi = umma_desc_sw128(sa), alo = umma_desc_sw128(sa + A_TILE);
-                const uint64_t bhi = umma_desc_sw128(sa + 2 * A_TILE), blo = umma_desc_sw128(sa + 2 * A_TILE + B_TILE);
+                const uint32_t d = tmem + (uint32_t)(b * TILE_N);
+                for (int kb = 0; kb < nk; kb++, g++) {
+                    const int s = g % STAGES;
+                    mbar_wait(&conv[s], (g / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
+                    const uint64_t ahi = desc_a(sa), bhi = desc_b(sa + A_BYTES);
+                    const uint64_t alo = desc_a(sa + HI_BYTES), blo = desc_b(sa + HI_BYTES + A_BYTES);
 #pragma unroll
-                for (int ks = 0; ks < BK / 8; ks++) {
-                    const uint64_t off = (uint64_t)(ks * 32) >> 4;  // 8 tf32 = 32 B along K inside the atom
-                    const uint32_t first = (kb | ks) != 0;
-                    mma_tf32(tmem, alo + off, bhi + off, IDESC, first);  // small terms first
-                    mma_tf32(tmem, ahi + off, blo + off, IDESC, 1);
-                    mma_tf32(tmem, ahi + off, bhi + off, IDESC, 1);
-                }
-                mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
-            }
-            mma_commit(accum);
-        }
-    } else {
-        // epilogue: warps 2..5, TMEM lane quarter = warp % 4
-        const int q = warp & 3;
-        mbar_wait(accum, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const int row = m0 + q * 32 + lane;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t r[32];
-            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (row < M) {
-                float* crow = C + (long long)row * N + n0 + c0;
-                const int ncols = min(32, N - (n0 + c0));
-                if (ncols == 32 && ((uintptr_t)crow & 15) == 0) {
-#pragma unroll
-                    for (int v = 0; v < 8; v++) {
-                        float4 o;
-                        float4 old = beta != 0.f ? *reinterpret_cast<const float4*>(crow + 4 * v)
-                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-                        o.x = alpha * __uint_as_float(r[4 * v + 0]) + beta * old.x;
-                        o.y = alpha * __uint_as_float(r[4 * v + 1]) + beta * old.y;
-                        o.z = alpha * __uint_as_float(r[4 * v + 2]) + beta * old.z;
-                        o.w = alpha * __uint_as_float(r[4 * v + 3]) + beta * old.w;
-                        *reinterpret_cast<float4*>(crow + 4 * v) = o;
+                    for (int ks = 0; ks < BK / 8; ks++) {
+                        const uint64_t oa = (uint64_t)(ks * 32) >> 4;    // 8 tf32 = 32 B along K in the A atom
+                        const uint64_t ob = (uint64_t)(ks * 1024) >> 4;  // 8 k = two 4-k atoms of B
+                        const uint32_t acc = (kb | ks) != 0;
+#ifndef GEMM_DBG_ONEMMA
+                        mma_tf32_2sm(d, alo + oa, bhi + ob, acc);  // small terms first
+                        mma_tf32_2sm(d, ahi + oa, blo + ob, 1);
+                        mma_tf32_2sm(d, ahi + oa, bhi + ob, 1);
+#else
+                        mma_tf32_2sm(d, ahi + oa, bhi + ob, acc);
+#endif
                     }
-                } else {
-                    for (int v = 0; v < ncols; v++)
-                        crow[v] = alpha * __uint_as_float(r[v]) + (beta != 0.f ? beta * crow[v] : 0.f);
+                    commit_2sm(&empty[s]);  // frees the stage in both CTAs once these MMAs have read it
+                }
+                commit_2sm(&tmem_full[b]);
+            }
+        }
+    } else if (warp < EPI_WARP0) {  // converters
+        const int ct = threadIdx.x - 32 * CONV_WARP0;  // 0..127
+        int g = 0;
+        for (int t = cluster; t < ntiles; t += nclusters) {
+            for (int kb = 0; kb < nk; kb++, g++) {
+                const int s = g % STAGES;
+                mbar_wait(&full[s], (g / STAGES) & 1);
+                const uint32_t src = smem_u32(smem + s * STAGE_BYTES) + 16 * ct;
+#ifndef GEMM_DBG_NOCONV
+                uint4 v[HI_BYTES / 16 / 128];
+#pragma unroll
+                for (int j = 0; j < HI_BYTES / 16 / 128; j++) v[j] = lds128(src + j * 2048);
+#pragma unroll
+                for (int j = 0; j < HI_BYTES / 16 / 128; j++)
+                    sts128(src + HI_BYTES + j * 2048,
+                           make_uint4(lo_tf32(v[j].x), lo_tf32(v[j].y), lo_tf32(v[j].z), lo_tf32(v[j].w)));
+#endif
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+                __syncwarp();
+                if (lane == 0) mbar_arrive_leader(&conv[s]);
+            }
+        }
+    } else {  // epilogue
+        const int q = warp & 3;
+        int i = 0;
+        for (int t = cluster; t < ntiles; t += nclusters, i++) {
+            int tm, tn;
+            ras.at(t, tm, tn);
+            const int b = i & 1;
+            mbar_wait(&tmem_full[b], (i >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int row = tm * TILE_M + (int)rank * CTA_M + q * 32 + lane;
+            const int n0 = tn * TILE_N;
+            for (int c0 = 0; c0 < TILE_N; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TILE_N + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                      "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                      "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+                      "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+                      "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (row < M && n0 + c0 < N) {
+                    float* crow = C + (long long)row * N + n0 + c0;
+                    const int ncols = min(32, N - (n0 + c0));
+                    if (ncols == 32 && ((uintptr_t)crow & 15) == 0) {
+#pragma unroll
+                        for (int v = 0; v < 8; v++) {
+                            float4 o;
+                            const float4 old = beta != 0.f ? *reinterpret_cast<const float4*>(crow + 4 * v)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                            o.x = alpha * __uint_as_float(r[4 * v + 0]) + beta * old.x;
+                            o.y = alpha * __uint_as_float(r[4 * v + 1]) + beta * old.y;
+                            o.z = alpha * __uint_as_float(r[4 * v + 2]) + beta * old.z;
+                            o.w = alpha * __uint_as_float(r[4 * v + 3]) + beta * old.w;
+                            *reinterpret_cast<float4*>(crow + 4 * v) = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < 32; v++)
+                            if (v < ncols)
+                                crow[v] = alpha * __uint_as_float(r[v]) + (beta != 0.f ? beta * crow[v] : 0.f);
+                    }
                 }
             }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_leader(&tmem_empty[b]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    __syncwarp();        // producer / issuer lanes rejoin their warps before the aligned barrier
+    cluster_sync_all();  // both CTAs done with TMEM and with each other's barriers
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }
 }
 
-// ---------------------------------------------------------------- prologue: tf32 split
-__device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-
-// A (rows x K, row-major) -> hi, lo (rows x Kp, zero-padded)
-__global__ void split_rows_kernel(const float* __restrict__ A, int rows, int K, int Kp,
-                                  float* __restrict__ hi, float* __restrict__ lo) {
-    const long long total = (long long)rows * Kp;
-    if (K == Kp && ((uintptr_t)A & 15) == 0) {  // no padding: straight float4 stream
-        const long long t4 = total >> 2;
-        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < t4;
-             i += (long long)gridDim.x * blockDim.x) {
-            const float4 x = ld_stream_f4(reinterpret_cast<const float4*>(A) + i);
-            float4 h, l;
-            h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
-            h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
-            h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
-            h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
-            reinterpret_cast<float4*>(hi)[i] = h;
-            reinterpret_cast<float4*>(lo)[i] = l;
-        }
-        return;
-    }
+// rows x cols (pitch cols) -> dst with pitch dpitch (a multiple of 4 floats); the padding columns
+// are never read (the tensor map's extent is cols)
+__global__ void pack_rows_kernel(const float* __restrict__ src, long long rows, int cols, int dpitch,
+                                 float* __restrict__ dst) {
+    const long long total = rows * cols;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const long long r = i / Kp;
-        const int k = (int)(i - r * Kp);
-        float x = k < K ? A[r * K + k] : 0.f;
-        float h = tf32_rna(x);
-        hi[i] = h;
-        lo[i] = tf32_rna(x - h);
+        const long long r = i / cols;
+        dst[r * dpitch + (i - r * cols)] = src[i];
     }
 }
 
-// B (K x N, row-major) -> Bt hi, lo (N x Kp, K-major), 32x32 smem transpose
-__global__ void split_transpose_kernel(const float* __restrict__ B, int K, int N, int Kp,
-                                       float* __restrict__ hi, float* __restrict__ lo) {
-    __shared__ float t[32][33];
-    const int k0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
-    for (int i = threadIdx.y; i < 32; i += 8) {
-        int k = k0 + i, n = n0 + threadIdx.x;
-        t[i][threadIdx.x] = (k < K && n < N) ? B[(long long)k * N + n] : 0.f;
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 32; i += 8) {
-        int n = n0 + i, k = k0 + threadIdx.x;
-        if (n < N && k < Kp) {
-            float x = t[threadIdx.x][i];
-            float h = tf32_rna(x);
-            hi[(long long)n * Kp + k] = h;
-            lo[(long long)n * Kp + k] = tf32_rna(x - h);
-        }
-    }
+__global__ void scale_c_kernel(long long n, float alpha, float beta, float* __restrict__ C) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        C[i] = alpha * 0.f + (beta != 0.f ? beta * C[i] : 0.f);
 }
 
 // ---------------------------------------------------------------- host side
@@ -298,255 +388,75 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-bool make_map(CUtensorMap* m, const float* base, int rows, int Kp, int box_rows) {
+// 2-D fp32 tensor map: inner extent `inner`, `outer` rows of `pitch` floats, box inner x outer
+bool make_map(CUtensorMap* m, const float* base, int inner, int outer, long long pitch, int box_inner,
+              int box_outer, CUtensorMapSwizzle sw) {
     EncodeTiledFn enc = encode_fn();
     if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)Kp * 4};
-    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
     cuuint32_t estr[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE,
-               ROW_BYTES == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-size_t kpad(int k) { return ((size_t)(k > 0 ? k : 1) + BK - 1) / BK * BK; }
-
-// ---------------------------------------------------------------- 2-SM (CTA pair) variant
-// A cluster of 2 CTAs owns a 256 x 256 output tile; tcgen05.mma.cta_group::2 (M = 256) issued
-// by the leader CTA reads A rows 0-127 / 128-255 and B columns 0-127 / 128-255 from the two
-// CTAs' shared memory at the same offsets, so each SM streams half of B: per MMA 8 KB of smem
-// operand reads per SM instead of 12 KB (the 1-SM kernel's tensor pipe idled ~17% on that).
-// Each CTA TMA-loads its own halves; completion is counted on the leader's `full` barrier (the
-// peer-bit-cleared address); the leader's tcgen05.commit multicasts to both CTAs' `empty` and
-// `accum` barriers.  Each CTA's epilogue drains its own TMEM (its 128 rows x 256 columns).
-constexpr int P_BN_HALF = 128;                        // B rows (N) per CTA
-constexpr int P_B_TILE = P_BN_HALF * BK * 4;
-constexpr int P_STAGE_BYTES = 2 * A_TILE + 2 * P_B_TILE;  // per CTA
-constexpr int P_STAGES = 6;
-#ifndef P_GROUP_M_DEF
-#define P_GROUP_M_DEF 8  // re-swept 2/4/8/16 at 16384^3 (current kernel): 36.2-36.4 / 36.1 / 34.9-35.8 / 36.2 ms
-#endif
-constexpr int P_GROUP_M = P_GROUP_M_DEF;
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
-constexpr uint32_t P_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
-                             ((uint32_t)(256 >> 4) << 24);
-
-__device__ __forceinline__ uint32_t cta_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar_leader, int c0,
-                                                int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-        "%4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1)
-        : "memory");
-}
-__device__ __forceinline__ void mma_tf32_2sm(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
-                                             uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(bar)),
-        "h"((uint16_t)3)
-        : "memory");
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1) gemm_3xtf32_2sm_kernel(
-    const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
-    const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo, int M, int N,
-    int Kp, float alpha, float beta, float* __restrict__ C) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = (uint64_t*)(smem + P_STAGES * P_STAGE_BYTES);
-    uint64_t* empty = full + P_STAGES;
-    uint64_t* accum = empty + P_STAGES;
-    uint32_t* tmem_slot = (uint32_t*)(accum + 1);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cta_rank();
-    const bool leader = rank == 0;
-    const int tiles_m = (M + 255) / 256, tiles_n = (N + BN - 1) / BN;
-    const int tid = blockIdx.x >> 1;  // cluster index
-    constexpr int G = P_GROUP_M;      // raster group in 256-row tiles
-    const int group = tid / (G * tiles_n);
-    const int first_m = group * G;
-    const int gsize = min(tiles_m - first_m, G);
-    const int tm = first_m + (tid % (G * tiles_n)) % gsize;
-    const int tn = (tid % (G * tiles_n)) / gsize;
-    const int m0 = tm * 256 + (int)rank * 128;          // this CTA's A rows / output rows
-    const int nb = tn * BN + (int)rank * P_BN_HALF;     // this CTA's B half
-    const int n0 = tn * BN;
-    const int nk = Kp / BK;
-
-    if (warp == 0 && lane == 0) {
-        for (int s = 0; s < P_STAGES; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        mbar_init(accum, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_ahi) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_alo) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_bhi) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_blo) : "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer CTA
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {  // TMA producer (both CTAs); bytes land on the leader's full barrier
-            for (int kb = 0; kb < nk; kb++) {
-                const int s = kb % P_STAGES;
-                mbar_wait(&empty[s], ((kb / P_STAGES) & 1) ^ 1);
-                uint8_t* st = smem + s * P_STAGE_BYTES;
-                const uint32_t bar = smem_u32(&full[s]) & 0xFEFFFFFFu;
-                if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);
-                tma_load_2d_2sm(st, &tm_ahi, bar, kb * BK, m0);
-                tma_load_2d_2sm(st + A_TILE, &tm_alo, bar, kb * BK, m0);
-                tma_load_2d_2sm(st + 2 * A_TILE, &tm_bhi, bar, kb * BK, nb);
-                tma_load_2d_2sm(st + 2 * A_TILE + P_B_TILE, &tm_blo, bar, kb * BK, nb);
-            }
-        }
-    } else if (warp == 1) {
-        if (leader && lane == 0) {  // MMA issuer (leader only)
-            for (int kb = 0; kb < nk; kb++) {
-                const int s = kb % P_STAGES;
-                mbar_wait(&full[s], (kb / P_STAGES) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t sa = smem_u32(smem + s * P_STAGE_BYTES);
-                const uint64_t ahi = umma_desc_sw128(sa), alo = umma_desc_sw128(sa + A_TILE);
-                const uint64_t bhi = umma_desc_sw128(sa + 2 * A_TILE), blo = umma_desc_sw128(sa + 2 * A_TILE + P_B_TILE);
-#pragma unroll
-                for (int ks = 0; ks < BK / 8; ks++) {
-                    const uint64_t off = (uint64_t)(ks * 32) >> 4;
-                    const uint32_t first = (kb | ks) != 0;
-                    mma_tf32_2sm(tmem, alo + off, bhi + off, P_IDESC, first);
-                    mma_tf32_2sm(tmem, ahi + off, blo + off, P_IDESC, 1);
-                    mma_tf32_2sm(tmem, ahi + off, bhi + off, P_IDESC, 1);
-                }
-                mma_commit_2sm(&empty[s]);  // frees the stage in BOTH CTAs once read
-            }
-            mma_commit_2sm(accum);
-        }
-    } else {
-        const int q = warp & 3;
-        mbar_wait(accum, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const int row = m0 + q * 32 + lane;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t r[32];
-            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (row < M) {
-                float* crow = C + (long long)row * N + n0 + c0;
-                const int ncols = min(32, N - (n0 + c0));
-                if (ncols == 32 && ((uintptr_t)crow & 15) == 0) {
-#pragma unroll
-                    for (int v = 0; v < 8; v++) {
-                        float4 o;
-                        float4 old = beta != 0.f ? *reinterpret_cast<const float4*>(crow + 4 * v)
-                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-                        o.x = alpha * __uint_as_float(r[4 * v + 0]) + beta * old.x;
-                        o.y = alpha * __uint_as_float(r[4 * v + 1]) + beta * old.y;
-                        o.z = alpha * __uint_as_float(r[4 * v + 2]) + beta * old.z;
-                        o.w = alpha * __uint_as_float(r[4 * v + 3]) + beta * old.w;
-                        *reinterpret_cast<float4*>(crow + 4 * v) = o;
-                    }
-                } else {
-                    for (int v = 0; v < ncols; v++)
-                        crow[v] = alpha * __uint_as_float(r[v]) + (beta != 0.f ? beta * crow[v] : 0.f);
-                }
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncwarp();        // producer / issuer lanes rejoin their warps before the aligned barrier
-    cluster_sync_all();  // both CTAs done with TMEM and with each other's barriers
-    if (warp == 1) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
-    }
-}
+// an operand TMA can read in place: 16-byte aligned base and row pitch
+bool in_place(const void* p, int cols) { return ((uintptr_t)p & 15) == 0 && cols % 4 == 0; }
+size_t pad4(int c) { return ((size_t)c + 3) & ~(size_t)3; }
 
 }  // namespace
 
-size_t gemm_workspace_bytes(int m, int n, int k) {
-    return 2 * ((size_t)m + (size_t)n) * kpad(k) * sizeof(float) + 4096;
+size_t gemm_workspace_bytes(int m, int n, int k, const float* A, const float* B) {
+    size_t b = 0;
+    if (!in_place(A, k)) b += (size_t)m * pad4(k) * sizeof(float) + 256;
+    if (!in_place(B, n)) b += (size_t)k * pad4(n) * sizeof(float) + 256;
+    return b;
 }
 
 int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, const float* A,
                 const float* B, float* C, void* workspace, size_t workspace_bytes) {
     if (m <= 0 || n <= 0) return 0;
-    const int Kp = (int)kpad(k);
-    if (workspace_bytes < gemm_workspace_bytes(m, n, k)) return (int)cudaErrorInvalidValue;
-    float* ahi = (float*)(((uintptr_t)workspace + 1023) & ~(uintptr_t)1023);
-    float* alo = ahi + (size_t)m * Kp;
-    float* bhi = alo + (size_t)m * Kp;
-    float* blo = bhi + (size_t)n * Kp;
-    {
-        long long total = (long long)m * Kp;
-        long long blocks = (total + 255) / 256;
-        split_rows_kernel<<<(int)(blocks < PENCIL_NUM_SMS * 16 ? blocks : PENCIL_NUM_SMS * 16), 256, 0, st>>>(
-            A, m, k, Kp, ahi, alo);
-        dim3 g((Kp + 31) / 32, (n + 31) / 32);
-        split_transpose_kernel<<<g, dim3(32, 8), 0, st>>>(B, k, n, Kp, bhi, blo);
-    }
-    // CTA-pair kernel (-DPENCIL_VARIANT_GEMM_1SM builds the single-CTA kernel, tools/variant_build.sh)
-#ifdef PENCIL_VARIANT_GEMM_1SM
-    const int two_sm = 0;
-#else
-    const int two_sm = 1;
-#endif
-    CUtensorMap maps[4];
-    const int b_box = two_sm ? P_BN_HALF : BN;
-    if (!make_map(&maps[0], ahi, m, Kp, BM) || !make_map(&maps[1], alo, m, Kp, BM) ||
-        !make_map(&maps[2], bhi, n, Kp, b_box) || !make_map(&maps[3], blo, n, Kp, b_box))
-        return (int)cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        cudaFuncSetAttribute(gemm_3xtf32_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
-        attr = true;
-    }
-    if (two_sm) {
-        const int clusters = ((m + 255) / 256) * ((n + BN - 1) / BN);
-        gemm_3xtf32_2sm_kernel<<<2 * clusters, GEMM_THREADS, P_SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3],
-                                                                               m, n, Kp, alpha, beta, C);
+    if (workspace_bytes < gemm_workspace_bytes(m, n, k, A, B)) return (int)cudaErrorInvalidValue;
+    if (k == 0) {  // empty sum: C = alpha * 0 + beta * C, as the epilogue would write it
+        scale_c_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>((long long)m * n, alpha, beta, C);
         return (int)cudaGetLastError();
     }
-    const int tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
-    gemm_3xtf32_kernel<<<tiles, GEMM_THREADS, SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], m, n, Kp,
-                                                               alpha, beta, C);
+    long long lda = k, ldb = n;
+    uintptr_t ws = ((uintptr_t)workspace + 255) & ~(uintptr_t)255;
+    const int grid_pack = PENCIL_NUM_SMS * 8;
+    if (!in_place(A, k)) {
+        float* a2 = (float*)ws;
+        lda = (long long)pad4(k);
+        pack_rows_kernel<<<grid_pack, 256, 0, st>>>(A, m, k, (int)lda, a2);
+        A = a2;
+        ws = ((uintptr_t)(a2 + (size_t)m * lda) + 255) & ~(uintptr_t)255;
+    }
+    if (!in_place(B, n)) {
+        float* b2 = (float*)ws;
+        ldb = (long long)pad4(n);
+        pack_rows_kernel<<<grid_pack, 256, 0, st>>>(B, k, n, (int)ldb, b2);
+        B = b2;
+    }
+    CUtensorMap maps[2];
+    if (!make_map(&maps[0], A, k, m, lda, BK, CTA_M, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !make_map(&maps[1], B, n, k, ldb, B_CHUNK, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+        return (int)cudaErrorInvalidValue;
+    static int max_clusters = 0;  // CTA pairs resident at once (one per two SMs)
+    if (!max_clusters) {
+        cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(PENCIL_NUM_SMS);
+        cfg.blockDim = dim3(GEMM_THREADS);
+        cfg.dynamicSmemBytes = SMEM_BYTES;
+        int nc = 0;
+        max_clusters = cudaOccupancyMaxActiveClusters(&nc, gemm_3xtf32_kernel, &cfg) == cudaSuccess && nc > 0
+                           ? nc : PENCIL_NUM_SMS / 2;
+        cudaGetLastError();
+    }
+    const int tiles = ((m + TILE_M - 1) / TILE_M) * ((n + TILE_N - 1) / TILE_N);
+    const int clusters = tiles < max_clusters ? tiles : max_clusters;
+    gemm_3xtf32_kernel<<<2 * clusters, GEMM_THREADS, SMEM_BYTES, st>>>(maps[0], maps[1], m, n, k, alpha, beta, C);
     return (int)cudaGetLastError();
 }

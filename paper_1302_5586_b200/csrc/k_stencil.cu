@@ -961,7 +961,7 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int
 struct Swar2dArgs {
     unsigned kc;         // centre tap (>= 0)
     unsigned kn[25];     // |off-centre taps| (kn[12] unused)
-    unsigned bias_half;  // (B + scale / 2) in both 16-bit lanes
+    unsigned half2;      // scale / 2 in both 16-bit lanes (the accumulators' start: acc' + scale/2)
     unsigned bias2;      // B in both lanes
     int shift;           // log2(scale) <= 8
 };
@@ -1066,7 +1066,7 @@ __device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c,
         else *reinterpret_cast<uint2*>(dst) = make_uint2(rr[0], rr[1]);
     }
 #pragma unroll
-    for (int t = 0; t < NP / 2; t++) A[D][t] = a.bias_half;
+    for (int t = 0; t < NP / 2; t++) A[D][t] = a.half2;
 }
 
 template <int NP, bool DIA>
@@ -1096,7 +1096,7 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_kernel(i
 #pragma unroll
     for (int q = 0; q < 5; q++)
 #pragma unroll
-        for (int t = 0; t < NP / 2; t++) A[q][t] = a.bias_half;
+        for (int t = 0; t < NP / 2; t++) A[q][t] = a.half2;
     Sweep<unsigned char> sw;
     sw.w = w;
     sw.src_last = img + (long long)(h - 1) * w + c;
@@ -1133,7 +1133,7 @@ bool swar2d_args(const int* k, int scale, Swar2dArgs& a) {
     if (255ll * ((long long)k[12] + off) + (scale >> 1) >= 65536) return false;
     a.kc = (unsigned)k[12];
     for (int t = 0; t < 25; t++) a.kn[t] = t == 12 ? 0u : (unsigned)(-(long long)k[t]);
-    a.bias_half = (unsigned)(B + (scale >> 1)) * 0x00010001u;
+    a.half2 = (unsigned)(scale >> 1) * 0x00010001u;
     a.bias2 = (unsigned)B * 0x00010001u;
     a.shift = 0;
     while ((1 << a.shift) != scale) a.shift++;

@@ -65,7 +65,7 @@ int launch_conv5x5_f32_band(cudaStream_t st, int h, int w, int out_lo, int out_h
 // k_gemm.cu
 int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, const float* A,
                 const float* B, float* C, void* workspace, size_t workspace_bytes);
-size_t gemm_workspace_bytes(int m, int n, int k);
+size_t gemm_workspace_bytes(int m, int n, int k, const float* A, const float* B);
 
 // k_micro.cu (measurement probes, not PENCIL kernels)
 int launch_micro_gather(cudaStream_t st, int mode, long long n, const int* idx, const float* table,

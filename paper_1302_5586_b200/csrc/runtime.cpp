@@ -682,7 +682,7 @@ void gemm(int m, int n, int k, float alpha, float beta, float* A, float* B, floa
     st[1] = {B, nullptr, sizeof(float) * nz((long long)k * n), IN};
     st[2] = {C, nullptr, sizeof(float) * nz((long long)m * n), INOUT};
     dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
-        size_t wb = gemm_workspace_bytes(m, n, k);
+        size_t wb = gemm_workspace_bytes(m, n, k, (const float*)st[0].dev, (const float*)st[1].dev);
         void* ws = nullptr;
         if (wb && pool_alloc(c, s, wb, &ws)) return (int)cudaErrorMemoryAllocation;
         int e = launch_gemm(s, m, n, k, alpha, beta, (const float*)st[0].dev, (const float*)st[1].dev,
@@ -842,7 +842,7 @@ int pencil_gemm_dev(pencil_stream_t s, int m, int n, int k, float alpha, float b
                     const float* B, float* C) {
     if (m < 0 || n < 0 || k < 0) return fail(PENCIL_E_ARG, "negative extent");
     DEV_PROLOGUE;
-    size_t wb = gemm_workspace_bytes(m, n, k);
+    size_t wb = gemm_workspace_bytes(m, n, k, A, B);
     void* ws = nullptr;
     if (wb && pool_alloc(c, st, wb, &ws)) return g_status;
     int e = launch_gemm(st, m, n, k, alpha, beta, A, B, C, ws, wb);

@@ -96,27 +96,9 @@ def check(case, got, ret=None):
     assert err <= TOL, (case.name, err)
 
 
-def gemm_supported():
-    import paper_1302_5586_b200 as pb
-    import torch
-    A = torch.zeros(128 * 128, device="cuda")
-    try:
-        pb.device.gemm(128, 128, 128, 1.0, 0.0, A, A, A.clone())
-        torch.cuda.synchronize()
-        return True
-    except pb.PencilError as e:
-        return e.code != "E-UNSUPPORTED"
-
-
-def maybe_skip(case):
-    if case.fn == "gemm" and not gemm_supported():
-        pytest.skip("gemm tcgen05 schedule not built yet")
-
-
 @pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
 def test_golden_via_interpreter_mirror(cuda, case):
     import paper_1302_5586_b200 as pb
-    maybe_skip(case)
     it = pb.CudaInterpreter(0)
     args = []
     for i, a in enumerate(case.args):
@@ -141,7 +123,6 @@ def test_golden_via_interpreter_mirror(cuda, case):
 @pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
 def test_golden_via_dropin_host(cuda, case):
     import paper_1302_5586_b200 as pb
-    maybe_skip(case)
     a = [x.copy() if isinstance(x, np.ndarray) else x for x in case.args]
     fn = getattr(pb.dropin, case.fn)
     if case.fault:
@@ -160,7 +141,6 @@ def test_golden_via_dropin_host(cuda, case):
 def test_golden_via_dropin_device(cuda, case):
     import paper_1302_5586_b200 as pb
     torch = cuda
-    maybe_skip(case)
     a = [torch.from_numpy(x.copy()).cuda() if isinstance(x, np.ndarray) else x for x in case.args]
     fn = getattr(pb.dropin, case.fn)
     if case.fault:

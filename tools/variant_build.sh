@@ -10,7 +10,6 @@
 #   -DPENCIL_VARIANT_NO_DIA      no diamond-support stencil kernels
 #   -DPENCIL_VARIANT_NO_PF       no power-of-two fused f32 taps
 #   -DPENCIL_VARIANT_L2_DIRTY    L2 flush without the discard (dirty lines left)
-#   -DPENCIL_VARIANT_GEMM_1SM    single-CTA gemm instead of the CTA pair
 #   -DPENCIL_VARIANT_NO_SEG      spmv_vec on the batch-and-fold executor (csr_flow_kernel), not csr_seg_kernel
 set -e
 name=$1; shift
