@@ -170,7 +170,15 @@ def bench_spmv(args, torch, pb, rank, world, dist):
         ceil_ms = statistics.mean(run_steps(
             torch, lambda: lib.pencil_micro_gather_val(st, nnz, cd.data_ptr(), vd.data_ptr(), xd.data_ptr(),
                                                        res_buf.data_ptr()), max(3, args.steps // 2), 2, flush))
+        # the same matrix in source order (spmv_inline / the ACCESS-summarised spmv: row sums folded
+        # in order, bit-identical to the emitted C) — a suite line beside the headline
+        plan0 = pb.device.CsrPlan(nrows, nrows, nnz, rp, mode=0)
+        src_ms = statistics.mean(run_steps(torch, lambda: plan0.spmv(rp, cd, vd, xd, y), max(3, args.steps // 2), 2,
+                                           flush))
+        pb.device.sync_status()
+        plan0.close()
     else:
+        src_ms = None
         # one step of a row-sharded iterative SpMV: y = A x for the rank's rows, y gathered on
         # every rank (the next step's x) — fused into the SpMV kernel (NVLink / NVLS stores) or
         # SpMV + NCCL all-gather
@@ -217,6 +225,7 @@ def bench_spmv(args, torch, pb, rank, world, dist):
     algo = spmv_bytes(nrows, nrows, nnz)
     res = {"ms": kernel_ms, "bytes": algo, "launches": launches,
            "ceiling_ms": ceil_ms if not args.dist_path else None,
+           "src_ms": src_ms if not args.dist_path else None,
            "config": dict(spmv_config(nrows, nnz, xm),
                           schedule="csr_seg_kernel, reassociated (persistent warps on 4096-nnz row-aligned "
                                    "tiles, 128-bit col/val streams, per-lane segments + warp segmented scan over "
@@ -965,12 +974,12 @@ def main():
                 "config": dict(res["config"], parallelism=f"row-sharded x{world}" if args.dist_path else "single GPU"),
                 "gpu_launches": res["launches"]}
         if not args.dist_path:
-            line["roofline"] = {"bound": "hbm", "kernel": "csr_seg_kernel", "achieved": kernel_gbs,
+            line["roofline"] = {"bound": "hbm", "kernel": "csr_seg_kernel<0, 0>", "achieved": kernel_gbs,
                                 "peak": hbm, "unit": "GB/s", "frac": kernel_gbs / hbm,
                                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
                                 "frac_spec": kernel_gbs / SPEC_HBM_GBS,
                                 "algorithmic_bytes_per_launch": res["bytes"],
-                                "traffic": ncu_traffic("csr_seg_kernel"),
+                                "traffic": ncu_traffic("csr_seg_kernel<0, 0>"),
                                 "measured_ceiling": {
                                     "kernel": "micro_gather_val: the same col/val stream + x gathers, no rows "
                                               "(random 4-byte gathers are L1->XBAR request-rate bound, DESIGN.md §3)",
@@ -1000,6 +1009,12 @@ def main():
             line["suite"] = dsuite
         if not args.dist_path and not args.no_suite:
             line["suite"] = suite(args, torch, pb, hbm)
+            if res.get("src_ms"):
+                line["suite"] = dict({"spmv_inline_2e24": bw_line(
+                    res["src_ms"], res["bytes"], hbm, "csr_seg_kernel<0, 1>",
+                    order="source order (spmv_inline / ACCESS spmv): each row folded in order, bit-identical to "
+                          "the emitted C; row chains carried lane to lane",
+                    measured_ceiling_ms=res["ceiling_ms"])}, **line["suite"])
             # the measured peak is a copy test (read + write); read-mostly streams go past it, so
             # every bandwidth line also carries its fraction of the B200 spec (8 TB/s HBM3e)
             for v in line["suite"].values():

@@ -8,9 +8,12 @@
 // (csr_plan_kernel), it gives every warp a contiguous row range holding ~TILE_NNZ
 // non-zeros regardless of the power-law row-length distribution.
 //
-// Executors (launch_csr_spmv picks one): csr_flow_kernel (16-byte-aligned col / val; the tile's
-// non-zeros stream in continuous 16-byte-per-lane windows, batches folded from whichever window
-// holds them) and csr_stream_kernel (scalar loads; any alignment).
+// Executors (launch_csr_spmv picks one): csr_seg_kernel (16-byte-aligned col / val, monotone rowptr
+// without empty rows — the plan's flags: per-lane segments over the plan's row-start bitmap, rows
+// scanned across lanes when reassociation is licensed, carried lane to lane in source order
+// otherwise), csr_flow_kernel (aligned, any monotone rowptr: the tile's non-zeros stream in
+// continuous 16-byte-per-lane windows, batches folded from whichever window holds them) and
+// csr_stream_kernel (scalar loads; any alignment).
 // The structure they share — csr_stream_kernel: per tile, per batch of 32 rows, the batch's non-zeros
 // are streamed with coalesced loads (col, val: evict-first) while x[col] is gathered
 // (evict-last, so the 64 MB vector stays L2-resident), staged in shared memory, then each
@@ -416,9 +419,85 @@ struct SegState {
 
 __device__ __forceinline__ void seg_store(float* p, float v) { __stcs(p, v); }
 
+// Source order (spmv_inline, ACCESS spmv: the row loop must fold in order) on the same window: a
+// row's sum is one chain s = (((0 + p_a) + p_b) + ...), each add rounded, so a row spanning several
+// lanes is carried from lane to lane instead of scanned.  A lane holding a row start ("breaker")
+// knows its outgoing carry at once (its tail, folded from 0); a lane without one needs the carry
+// of the lane before it.  R rounds of (shuffle up, refold) settle every chain, R = the longest run
+// of breaker-free lanes (ballot; ~4 for 16-nnz rows, 32 under a long row — the serial chain of
+// the row itself, which source order cannot avoid).  Then each breaker folds its head onto the
+// settled incoming carry and stores the row that closes there; rows wholly inside the lane fold
+// from 0 and are stored in order.  Masked positions carry +0, and s + 0 == s for every s the
+// chain can hold (it starts at +0, so it is never -0): bit-identical to the emitted C.
+template <int E>
+__device__ __forceinline__ void seg_ordered(int lane, unsigned sb, const float (&pr)[E], float* __restrict__ y,
+                                            SegState& S) {
+    const bool brk = sb != 0;
+    const int f = brk ? __ffs(sb) - 1 : E, l = brk ? 31 - __clz(sb) : E;
+    auto fold_all = [&](float c) {
+#pragma unroll
+        for (int k = 0; k < E; k++) c = __fadd_rn(c, pr[k]);
+        return c;
+    };
+    float co;
+    if (brk) {
+        co = 0.f;
+#pragma unroll
+        for (int k = 0; k < E; k++)
+            if (k >= l) co = __fadd_rn(co, pr[k]);
+    } else {
+        co = fold_all(lane == 0 ? S.carry : 0.f);
+    }
+    const unsigned nb = __ballot_sync(0xffffffffu, brk);
+    unsigned run = ~nb;
+    int R = 0;
+    while (run) {  // longest run of breaker-free lanes (warp-uniform)
+        run &= run << 1;
+        R++;
+    }
+    for (int r = 0; r < R; r++) {
+        const float ci = __shfl_up_sync(0xffffffffu, co, 1);
+        if (!brk && lane > 0) co = fold_all(ci);
+    }
+    float ci = __shfl_up_sync(0xffffffffu, co, 1);
+    if (lane == 0) ci = S.carry;
+    // row starts in the lanes before this one
+    const int cnt = __popc(sb);
+    int pre = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, pre, d);
+        if (lane >= d) pre += o;
+    }
+    const int total = __shfl_sync(0xffffffffu, pre, 31);
+    if (brk) {  // rows closing here: the open one (head on the incoming carry), then the inner rows
+        const int ro = S.row + pre - cnt;
+        float h = ci;
+#pragma unroll
+        for (int k = 0; k < E; k++)
+            if (k < f) h = __fadd_rn(h, pr[k]);
+        __stcs(y + ro, h);
+        float a = 0.f;
+        int nseg = 0;
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+            if (k < f || k >= l) continue;
+            if (k > f && ((sb >> k) & 1u)) {
+                __stcs(y + ro + 1 + nseg, a);
+                a = 0.f;
+                nseg++;
+            }
+            a = __fadd_rn(a, pr[k]);
+        }
+        if (l > f) __stcs(y + ro + 1 + nseg, a);  // the row from the last-but-one start closes at l
+    }
+    S.carry = __shfl_sync(0xffffffffu, co, 31);
+    S.row += total;
+}
+
 // One window of E * 32 non-zeros (E per lane, E = 4 or 8: E / 4 16-byte loads per array per
 // lane, all E gathers in flight together).  FULL: every position inside the tile (no masks).
-template <int E, bool FULL>
+template <int E, bool FULL, bool ORDERED>
 __device__ __forceinline__ void seg_window(int qa, int P0, int P1, int nnz_len, int ncols, int lane,
                                            const int* __restrict__ col, const float* __restrict__ val,
                                            const float* __restrict__ x, const unsigned* __restrict__ rs_bits,
@@ -465,7 +544,11 @@ __device__ __forceinline__ void seg_window(int qa, int P0, int P1, int nnz_len, 
                 if (!(p + k > P0 && p + k < P1)) sb &= ~(1u << k);
         }
 #pragma unroll
-        for (int k = 0; k < E; k++) pr[k] = use[k] ? v[k] * xv[k] : 0.f;
+        for (int k = 0; k < E; k++) pr[k] = use[k] ? __fmul_rn(v[k], xv[k]) : 0.f;  // rounds on its own
+    }
+    if (ORDERED) {
+        seg_ordered<E>(lane, sb, pr, y, S);
+        return;
     }
     // the lane's segments: head (before its first start: closes the row open on entry), tail (from
     // its last start: stays open); rows that begin and end inside the lane (cnt >= 2) are stored
@@ -518,7 +601,7 @@ __device__ __forceinline__ void seg_window(int qa, int P0, int P1, int nnz_len, 
     S.row += win_starts;
 }
 
-template <bool DIST>
+template <bool DIST, bool ORDERED>
 __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
@@ -550,12 +633,12 @@ __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
         constexpr int E = SEG_E, W = 32 * E;
         int qa = P0 & ~(E - 1);
         if (qa < P1) {  // the first window always masks (positions before P0; P0's own start)
-            seg_window<E, false>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
+            seg_window<E, false, ORDERED>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
             qa += W;
         }
         for (; qa + W <= P1; qa += W)  // interior windows: every position in the tile
-            seg_window<E, true>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
-        if (qa < P1) seg_window<E, false>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
+            seg_window<E, true, ORDERED>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
+        if (qa < P1) seg_window<E, false, ORDERED>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
         if (lane == 0) seg_store(y + S.row, S.carry);  // the tile's last row (S.row == r1 - 1)
         if (S.bad) raise_fault(status, FAULT_OOB_LOAD);
         if (DIST) {
@@ -609,15 +692,18 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     if (grid > PENCIL_NUM_SMS * CTAS_PER_SM) grid = PENCIL_NUM_SMS * CTAS_PER_SM;
     const bool aligned = (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0;
 #ifdef PENCIL_VARIANT_NO_SEG
-    rs_bits = nullptr;  // A/B build: the batch-and-fold executor for spmv_vec too
+    rs_bits = nullptr;  // A/B build: the batch-and-fold executor for every mode
 #endif
-#ifdef PENCIL_VARIANT_NO_SEG
-    rs_bits = nullptr;  // A/B build: the batch-and-fold executor for spmv_vec too
-#endif
-    if (assoc && rs_bits && aligned) {  // reassociation licensed, no empty rows: segmented executor
+    if (rs_bits && aligned) {  // no empty rows: segmented executor (scan, or carried in source order)
         if (grid > PENCIL_NUM_SMS * SEG_CTAS_PER_SM) grid = PENCIL_NUM_SMS * SEG_CTAS_PER_SM;
-        csr_seg_kernel<false><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row,
-                                                            ntiles, plan_flags, rs_bits, tk, status, PeerSet{});
+        if (assoc)
+            csr_seg_kernel<false, false><<<grid, SPMV_THREADS, 0, st>>>(
+                nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, rs_bits, tk, status,
+                PeerSet{});
+        else
+            csr_seg_kernel<false, true><<<grid, SPMV_THREADS, 0, st>>>(
+                nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, rs_bits, tk, status,
+                PeerSet{});
         return (int)cudaGetLastError();
     }
     if (aligned) {
@@ -658,11 +744,17 @@ int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int n
                          unsigned* tk, unsigned* status, const PeerSet& peers) {
     if (nrows <= 0) return 0;
     const bool aligned = (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0;
-    if (assoc && rs_bits && aligned) {
+    if (rs_bits && aligned) {
         int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
         if (grid > PENCIL_NUM_SMS * SEG_CTAS_PER_SM) grid = PENCIL_NUM_SMS * SEG_CTAS_PER_SM;
-        csr_seg_kernel<true><<<grid, SPMV_THREADS, 0, st>>>(nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row,
-                                                           ntiles, plan_flags, rs_bits, tk, status, peers);
+        if (assoc)
+            csr_seg_kernel<true, false><<<grid, SPMV_THREADS, 0, st>>>(
+                nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, rs_bits, tk, status,
+                peers);
+        else
+            csr_seg_kernel<true, true><<<grid, SPMV_THREADS, 0, st>>>(
+                nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, rs_bits, tk, status,
+                peers);
         return (int)cudaGetLastError();
     }
     if (aligned) {
@@ -707,4 +799,4 @@ int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const
 #ifndef SEG_TILE_NNZ
 #define SEG_TILE_NNZ 4096
 #endif
-int csr_tile_nnz(int mode) { return mode == 1 ? SEG_TILE_NNZ : SPMV_TILE_NNZ; }
+int csr_tile_nnz(int) { return SEG_TILE_NNZ; }

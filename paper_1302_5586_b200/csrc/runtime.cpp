@@ -314,8 +314,8 @@ struct CsrPlanImpl {
     int device, nrows, ncols, nnz, mode, ntiles, tile_nnz;
     int* tile_row = nullptr;
     unsigned* flags = nullptr;
-    unsigned* rs_bits = nullptr;  // row-start bitmap (mode 1)
-    int seg = 0;                  // the segmented executor applies (mode 1, monotone, no empty row)
+    unsigned* rs_bits = nullptr;  // row-start bitmap
+    int seg = 0;                  // the segmented executor applies (monotone rowptr, no empty row)
     const unsigned* seg_bits() const { return seg ? rs_bits : nullptr; }
 };
 
@@ -324,7 +324,7 @@ int csr_plan_finalize(cudaStream_t st, CsrPlanImpl* p) {
     unsigned f[4] = {0, 0, 0, 0};
     CK(cudaMemcpyAsync(f, p->flags, sizeof f, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    p->seg = p->mode == 1 && p->rs_bits && f[0] == 0 && f[2] == 0;
+    p->seg = p->rs_bits && f[0] == 0 && f[2] == 0;
     return PENCIL_OK;
 }
 void csr_plan_release(cudaStream_t st, CsrPlanImpl& p) {
@@ -346,7 +346,7 @@ int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int*
     if (r) return r;
     r = pool_alloc(c, st, 64, (void**)&p->flags);
     if (r) return r;
-    if (mode == 1 && (r = pool_alloc(c, st, csr_rs_words(nnz) * sizeof(unsigned), (void**)&p->rs_bits))) return r;
+    if ((r = pool_alloc(c, st, csr_rs_words(nnz) * sizeof(unsigned), (void**)&p->rs_bits))) return r;
     CK(cudaMemsetAsync(p->tile_row, 0, sizeof(int) * ((size_t)p->ntiles + 1), st));
     if (!fw) fw = fault_word(c, st);
     if (!fw) return g_status;
@@ -472,7 +472,7 @@ int spmv_pipelined(int mode, int nrows, int ncols, int nnz, const int* rowptr, c
         CK(cudaMemcpyAsync(hb + 1 + b, p.tile_row + t, sizeof(int), cudaMemcpyDeviceToHost, s1));
     }
     CK(cudaStreamSynchronize(s1));
-    p.seg = mode == 1 && p.rs_bits && hb[0] == 0 && hb[40] == 0;
+    p.seg = p.rs_bits && hb[0] == 0 && hb[40] == 0;
     CK(cudaStreamWaitEvent(s1, pc->ev_x, 0));
     auto launch = [&](long long t0, long long t1) {
         return launch_csr_spmv(s1, mode, nrows, ncols, nnz, drp, dcol, dval, dx, dy, p.tile_row + t0,
