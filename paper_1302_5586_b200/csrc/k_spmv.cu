@@ -37,7 +37,7 @@
 #define SEG_E 4  // non-zeros per lane per window of the segmented executor (8: 1.16-1.19 ms, fewer warps)
 #endif
 #ifndef SEG_CTAS_PER_SM
-#define SEG_CTAS_PER_SM 6
+#define SEG_CTAS_PER_SM 5  // 48 registers: the one-deep window pipeline (seg_tile)
 #endif
 
 // plan_flags: [0] non-monotone rowptr (generic schedule), [2] some row is empty.  rs_bits (when
@@ -495,57 +495,69 @@ __device__ __forceinline__ void seg_ordered(int lane, unsigned sb, const float (
     S.row += total;
 }
 
-// One window of E * 32 non-zeros (E per lane, E = 4 or 8: E / 4 16-byte loads per array per
-// lane, all E gathers in flight together).  FULL: every position inside the tile (no masks).
-template <int E, bool FULL, bool ORDERED>
-__device__ __forceinline__ void seg_window(int qa, int P0, int P1, int nnz_len, int ncols, int lane,
-                                           const int* __restrict__ col, const float* __restrict__ val,
-                                           const float* __restrict__ x, const unsigned* __restrict__ rs_bits,
-                                           float* __restrict__ y, SegState& S) {
+// One window of E * 32 non-zeros (E per lane: E / 4 16-byte loads per array per lane, all E gathers
+// in flight together), split in two halves so that the tile loop can issue window w+1's loads and
+// gathers before it reduces window w (the reduction's shuffle rounds then overlap gathers in flight
+// instead of leaving the warp without any).  FULL: every position inside the tile (no masks).
+template <int E>
+struct SegWin {
+    float v[E], xv[E];
+    unsigned use;  // bit k: position p + k is in the tile with a valid column
+    unsigned sb;   // bit k: position p + k starts a row (other than the tile's first)
+};
+
+// The window's col / val / row-start loads (streaming) and its x gathers (issued unconditionally:
+// masked / invalid entries read x[0], so the E gathers leave back to back).
+template <int E, bool FULL>
+__device__ __forceinline__ void seg_fetch(int qa, int P0, int P1, int nnz_len, int ncols, int lane,
+                                          const int* __restrict__ col, const float* __restrict__ val,
+                                          const float* __restrict__ x, const unsigned* __restrict__ rs_bits,
+                                          SegWin<E>& w, bool& bad) {
     constexpr unsigned EMASK = (1u << E) - 1u;
     const int p = qa + E * lane;  // qa is E-aligned, so the lane's E row-start bits share a word
-    float pr[E];
-    unsigned sb = 0;  // bit k: position p + k starts a row (other than the tile's first)
+    w.use = 0;
+    w.sb = 0;
 #pragma unroll
-    for (int k = 0; k < E; k++) pr[k] = 0.f;
+    for (int k = 0; k < E; k++) w.v[k] = w.xv[k] = 0.f;
     if (FULL || (p + E - 1 >= P0 && p < P1)) {
         int c[E];
-        float v[E];
         if (FULL || p + E - 1 < nnz_len) {
 #pragma unroll
             for (int h = 0; h < E / 4; h++) {
                 const int4 c4 = ld_stream_i4(reinterpret_cast<const int4*>(col + p + 4 * h));
                 const float4 v4 = ld_stream_f4(reinterpret_cast<const float4*>(val + p + 4 * h));
                 c[4 * h] = c4.x; c[4 * h + 1] = c4.y; c[4 * h + 2] = c4.z; c[4 * h + 3] = c4.w;
-                v[4 * h] = v4.x; v[4 * h + 1] = v4.y; v[4 * h + 2] = v4.z; v[4 * h + 3] = v4.w;
+                w.v[4 * h] = v4.x; w.v[4 * h + 1] = v4.y; w.v[4 * h + 2] = v4.z; w.v[4 * h + 3] = v4.w;
             }
         } else {
 #pragma unroll
             for (int k = 0; k < E; k++) {
                 c[k] = p + k < nnz_len ? __ldg(col + p + k) : 0;
-                v[k] = p + k < nnz_len ? __ldg(val + p + k) : 0.f;
+                w.v[k] = p + k < nnz_len ? __ldg(val + p + k) : 0.f;
             }
         }
         // the row-start words stream (evict-first, 32 MB): x keeps the L2
-        const unsigned bits = (ld_stream_u(rs_bits + (p >> 5)) >> (p & 31)) & EMASK;
-        float xv[E];
-        bool use[E];
+        unsigned sb = (ld_stream_u(rs_bits + (p >> 5)) >> (p & 31)) & EMASK;
+        unsigned use = 0;
 #pragma unroll
         for (int k = 0; k < E; k++) {
             const bool in = FULL || (p + k >= P0 && p + k < P1), ok = (unsigned)c[k] < (unsigned)ncols;
-            use[k] = in && ok;
-            xv[k] = ld_keep_f(x + (use[k] ? c[k] : 0));
-            S.bad |= in && !ok;
+            w.xv[k] = ld_keep_f(x + (in && ok ? c[k] : 0));
+            use |= (unsigned)(in && ok) << k;
+            bad |= in && !ok;
+            if (!FULL && !(p + k > P0 && p + k < P1)) sb &= ~(1u << k);
         }
-        sb = bits;
-        if (!FULL) {
-#pragma unroll
-            for (int k = 0; k < E; k++)
-                if (!(p + k > P0 && p + k < P1)) sb &= ~(1u << k);
-        }
-#pragma unroll
-        for (int k = 0; k < E; k++) pr[k] = use[k] ? __fmul_rn(v[k], xv[k]) : 0.f;  // rounds on its own
+        w.use = use;
+        w.sb = sb;
     }
+}
+
+template <int E, bool ORDERED>
+__device__ __forceinline__ void seg_reduce(int lane, const SegWin<E>& w, float* __restrict__ y, SegState& S) {
+    float pr[E];
+#pragma unroll
+    for (int k = 0; k < E; k++) pr[k] = (w.use >> k) & 1u ? __fmul_rn(w.v[k], w.xv[k]) : 0.f;  // rounds on its own
+    const unsigned sb = w.sb;
     if (ORDERED) {
         seg_ordered<E>(lane, sb, pr, y, S);
         return;
@@ -601,6 +613,36 @@ __device__ __forceinline__ void seg_window(int qa, int P0, int P1, int nnz_len, 
     S.row += win_starts;
 }
 
+// A tile's windows, software-pipelined one deep: window w+1's col / val / row-start loads and its
+// gathers are issued before window w is reduced, so the reduction's shuffle rounds overlap gathers in
+// flight.  Measured at 2^24 rows (tools/ab_spmv_modes.sh): vec / inline 1.145 / 1.306 ms unpipelined
+// at 6 CTAs per SM -> 1.134 / 1.305 pipelined at 5 (at 6 the 40-register cap costs 1.19 / 1.32; at 4,
+// 1.18 / 1.34).  Two deep (w+2's stream loads, w+1's gathers, w's reduction): 1.21 / 1.37 at 4 CTAs
+// per SM and spills at 5 — the registers cost more warps than the deeper pipeline hides.
+template <int E, bool ORDERED>
+__device__ __forceinline__ void seg_tile(int P0, int P1, int nnz_len, int ncols, int lane, const int* __restrict__ col,
+                                         const float* __restrict__ val, const float* __restrict__ x,
+                                         const unsigned* __restrict__ rs_bits, float* __restrict__ y, SegState& S) {
+    constexpr int W = 32 * E;
+    int qa = P0 & ~(E - 1);
+    if (qa >= P1) return;
+    SegWin<E> cur, nxt;
+    // the first window always masks (positions before P0; P0's own start)
+    seg_fetch<E, false>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, cur, S.bad);
+    for (;;) {
+        const int qn = qa + W;
+        const bool more = qn < P1;
+        if (more) {
+            if (qn + W <= P1) seg_fetch<E, true>(qn, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, nxt, S.bad);
+            else seg_fetch<E, false>(qn, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, nxt, S.bad);
+        }
+        seg_reduce<E, ORDERED>(lane, cur, y, S);
+        if (!more) break;
+        cur = nxt;
+        qa = qn;
+    }
+}
+
 template <bool DIST, bool ORDERED>
 __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
@@ -630,15 +672,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
         const int P0 = clampp(__ldg(rowptr + r0));
         const int P1 = max(P0, clampp(__ldg(rowptr + r1)));
         SegState S{r0, 0.f, false};
-        constexpr int E = SEG_E, W = 32 * E;
-        int qa = P0 & ~(E - 1);
-        if (qa < P1) {  // the first window always masks (positions before P0; P0's own start)
-            seg_window<E, false, ORDERED>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
-            qa += W;
-        }
-        for (; qa + W <= P1; qa += W)  // interior windows: every position in the tile
-            seg_window<E, true, ORDERED>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
-        if (qa < P1) seg_window<E, false, ORDERED>(qa, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
+        seg_tile<SEG_E, ORDERED>(P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
         if (lane == 0) seg_store(y + S.row, S.carry);  // the tile's last row (S.row == r1 - 1)
         if (S.bad) raise_fault(status, FAULT_OOB_LOAD);
         if (DIST) {
