@@ -319,6 +319,14 @@ int pencil_affine_accesses(const char* source, const char* fn, int nbind, const 
                            const long long* values, pencil_access_form* out, int cap);
 /* the library's own copy of a fixture unit ("gemv_t", "spmv", ... = pencil/<name>.pencil.c) */
 const char* pencil_fixture_source(const char* fixture);
+/* distribution plan of fn's outermost parallel loop (and the `independent` loop nested in it):
+ * JSON {"function", "dims": [{"var", "kind": "parallel"|"reduction", "reduce": [...],
+ * "arrays": {name: {"mode": r|w|rw, "kind": block|view|via|all, "stride", "halo": [h0, h1],
+ * "inner": [...], "via"}}, "owned", "halo", "replicated", "conflicts"}]} — which arrays a split of
+ * the loop shards (blocks, views, CSR ranges via a row-pointer array), which need a halo, which
+ * must be replicated (all-gathered), which reduction variables need an all-reduce (distplan.cpp).
+ * Returns the length (cap 0 sizes the buffer) or -1 (E-SYNTAX / no such function / no loop). */
+long long pencil_dist_plan(const char* source, const char* fn, char* out, long long cap);
 /* the sub-view [lo, hi) of dimension dim */
 int pencil_view_slice(const pencil_view* v, int dim, long long lo, long long hi, pencil_view* out);
 /* gemv_t over views (VOBLA: y(j) = alpha * sum_i A(i, j) x(i) + beta * y(j)): A rank 2 with unit

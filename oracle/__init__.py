@@ -191,6 +191,41 @@ def ref_run(fixture, fn, args):
         return ret, outs
 
 
+def ref_trace(source, fn, args):
+    """Run `fn` of the unit text `source` in pencil::Interpreter with its MemTrace on
+    (Interpreter::enable_trace / trace, interp.hpp:17-21, 45-46).  args as for ref_run.  Returns
+    [(argument index, flat index, is_write)] for every recorded load / store of an array argument,
+    in the interpreter's order."""
+    if not os.path.exists(REF_DRIVER):
+        raise FileNotFoundError(REF_DRIVER)
+    with tempfile.TemporaryDirectory() as td:
+        src = os.path.join(td, "unit.pencil.c")
+        with open(src, "w") as f:
+            f.write(source)
+        lines = []
+        for idx, a in enumerate(args):
+            if isinstance(a, np.ndarray):
+                path = os.path.join(td, f"a{idx}.bin")
+                lines.append(f"array {'f32' if a.dtype == np.float32 else 'i32'} {path}")
+                a.tofile(path)
+            elif isinstance(a, (int, np.integer)):
+                lines.append(f"scalar int {int(a)}")
+            else:
+                lines.append(f"scalar float {float(a)!r}")
+        tpath = os.path.join(td, "trace.txt")
+        p = subprocess.run([REF_DRIVER, "run", src, fn], input="\n".join(lines) + "\n", capture_output=True,
+                           text=True, env=dict(os.environ, PENCIL_REF_TRACE=tpath))
+        if p.returncode != 0:
+            raise RuntimeError(f"ref_driver failed: {p.stderr}{p.stdout}")
+        out = []
+        with open(tpath) as f:
+            for line in f:
+                parts = line.split()
+                if parts and parts[0].startswith("arg"):
+                    out.append((int(parts[0][3:]), int(parts[1]), parts[-1] == "1"))
+        return out
+
+
 def ref_analyze(fixture, params=None, arrays=None, outer=False):
     import json
     src = os.path.join(FIXTURES, "outer" if outer else "", fixture + ".pencil.c")

@@ -10,7 +10,8 @@
 //   analyze FILE [--param n=v] [--array a=v0,v1,..]
 //                                         loop verdicts      (depanalysis.hpp:79 analyze_unit)
 //   lower   FILE                          OpenMP C           (lowering.hpp:29    emit_openmp)
-//   run     FILE FN  < argspec            Interpreter::call  (interp.hpp:49)
+//   run     FILE FN  < argspec            Interpreter::call  (interp.hpp:49); with PENCIL_REF_TRACE=path
+//                                         the interpreter's MemTrace records go to path
 //   signature FILE                        parameter kinds/types/extents (ast.hpp:133-151)
 //   summarize FILE FN [--param n=v] [--array a=v0,v1,..]
 //                                         access triple of a call FN(params...) under the
@@ -25,6 +26,7 @@
 // value is printed as `ret <int|float> <value>`.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iostream>
@@ -290,11 +292,21 @@ static int cmd_run(const char* path, const char* fn) {
         ++idx;
     }
     Value ret;
+    const char* trace_path = std::getenv("PENCIL_REF_TRACE");  // Interpreter::enable_trace (interp.hpp:45)
+    if (trace_path) interp.enable_trace(true);
     try {
         ret = interp.call(fn, args);
     } catch (const PencilError& e) {
         std::printf("error %s %s\n", e.code().c_str(), e.what());
         return 3;
+    }
+    if (trace_path) {  // one line per recorded access: store name, flat index, 0 = load / 1 = store
+        std::ofstream t(trace_path);
+        for (const auto& r : interp.trace()) {
+            t << r.array;
+            for (long long i : r.index) t << " " << i;
+            t << " " << (r.is_write ? 1 : 0) << "\n";
+        }
     }
     for (const auto& o : outs) {
         const auto& vals = interp.arrays().at(o.name);

@@ -67,6 +67,7 @@ SIGNATURES = {
     # §10 descriptors
     "pencil_affine_accesses": (c_int, [c_char_p, c_char_p, c_int, P, P, P, c_int]),
     "pencil_fixture_source": (c_char_p, [c_char_p]),
+    "pencil_dist_plan": (c_ll, [c_char_p, c_char_p, c_char_p, c_ll]),
     "pencil_view_slice": (c_int, [P, c_int, c_ll, c_ll, P]),
     "pencil_gemv_t_view_dev": (c_int, [P, c_float, c_float, P, P, P]),
     "pencil_gemv_t_views": (c_int, [c_int, c_int, c_int, c_int, c_int, P]),

@@ -341,7 +341,8 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
             } else if (pf_tap(PF, di, dj)) {  // k = 0 or +-2^e: k*x is exact, so one rounding is the same
                 a01 = f2fma(kk, W[sl][dj], a01);
                 a23 = f2fma(kk, W[sl][dj + 2], a23);
-            } else {   // product and sum rounded separately, as written
+            } else {   // product and sum rounded separately, as written (runtime -0 / 1: with
+                       // mul.rn.f32x2 + add.rn.f32x2 ptxas emits one fused FFMA2 — wrong results)
                 a01 = f2fma(f2fma(kk, W[sl][dj], a.negz), a.one, a01);
                 a23 = f2fma(f2fma(kk, W[sl][dj + 2], a.negz), a.one, a23);
             }

@@ -24,6 +24,20 @@ import numpy as np
 from . import _lib
 
 
+_PLANS = {}
+
+
+def fixture_plan(fixture, fn, dim=0):
+    """The distribution plan of a fixture's nest (views.dist_plan: derived from its index
+    expressions and ACCESS summaries, csrc/distplan.cpp) — the shard classes below take their
+    halo widths, replicated (all-gathered) arrays and reductions from it."""
+    key = (fixture, fn, dim)
+    if key not in _PLANS:
+        from .views import dist_plan
+        _PLANS[key] = dist_plan(fixture, fn)["dims"][dim]
+    return _PLANS[key]
+
+
 def _gloo():
     import torch.distributed as dist
     return dist.get_backend() != "nccl"
@@ -69,7 +83,15 @@ def shard_gemm_grid(m, n, nshards):
 
 
 class RowShardedCsr:
-    """Local piece of a row-sharded square CSR matrix plus the x all-gather plumbing."""
+    """Local piece of a row-sharded square CSR matrix plus the x all-gather plumbing.  The plan of
+    spmv_vec: y owned in row blocks, col / val sharded through rowptr (a one-row halo), x
+    replicated — the arrays `gathered()` lists are all-gathered every step."""
+
+    @staticmethod
+    def gathered():
+        p = fixture_plan("spmv", "spmv_vec")
+        assert p["arrays"]["col"]["kind"] == "via" and p["arrays"]["val"]["kind"] == "via" and p["owned"] == ["y"]
+        return p["replicated"]
 
     def __init__(self, rowptr, col, val, rank, world, bounds=None):
         self.rank, self.world = rank, world
@@ -194,11 +216,19 @@ class FusedSpmvAllgather:
 
 
 class BandShardedImage:
-    """Row band of an h x w image with the 2-row halos a 5x5 stencil needs."""
+    """Row band of an h x w image with the halo rows a 5x5 stencil needs (2: the plan of
+    conv5x5_u8 / conv5x5_f32 reads img in rows i - 2 .. i + 2)."""
 
-    HALO = 2
+    @staticmethod
+    def halo_rows():
+        h = 0
+        for fn in ("conv5x5_u8", "conv5x5_f32"):
+            lo, hi = fixture_plan("conv5x5", fn)["arrays"]["img"]["halo"]
+            h = max(h, -lo, hi)
+        return h
 
     def __init__(self, h, w, rank, world):
+        self.HALO = self.halo_rows()
         self.h, self.w, self.rank, self.world = h, w, rank, world
         b = shard_bands(h, world)
         self.b0, self.b1 = int(b[rank]), int(b[rank + 1])
@@ -331,6 +361,10 @@ class RowShardedGemv:
     rows are final; `gather_y` assembles them when a caller wants the whole vector.  The row
     partition is an array descriptor (include/pencil_b200.h §10): y's shard spec."""
 
+    @staticmethod
+    def gathered():
+        return fixture_plan("gemv", "gemv")["replicated"]
+
     def __init__(self, m, n, rank, world):
         from .views import ArrayDesc
         self.m, self.n, self.rank, self.world = m, n, rank, world
@@ -356,6 +390,12 @@ class ColShardedGemvT:
     (from the affine forms of A[i*lda + j], x[i*incx], y[j*incy], pencil_gemv_t_views) sliced to
     the column block (pencil_view_slice) — A at offset j0, y at offset j0*incy."""
 
+    @staticmethod
+    def gathered():
+        p = fixture_plan("gemv_t", "gemv_t")
+        assert p["arrays"]["A"]["kind"] == "view" and p["owned"] == ["y"]  # column blocks of the strided view
+        return p["replicated"]
+
     def __init__(self, m, n, rank, world, lda=None, incx=1, incy=1):
         from . import views as V
         self.m, self.n, self.rank, self.world = m, n, rank, world
@@ -375,6 +415,11 @@ class ColShardedGemvT:
         V.gemv_t_view(alpha, beta, self.A.on(A), self.x.on(x), self.y.on(y), stream)
 
 
+def dot_allreduce_vars():
+    """The reduction variables of dot's loop (its plan): one all-reduce of their partials."""
+    return fixture_plan("dot", "dot")["reduce"]
+
+
 def dot_sharded(local_dot, x_local, y_local):
     """dot (i PARALLEL_WITH_REDUCTION): local partial on this rank's range, then one all-reduce.
     The partials are summed in fp64 (rank order fixed by the collective) and rounded once."""
@@ -391,6 +436,17 @@ class GemmTileGrid:
     pencil_shard_gemm_grid; rank (ri, ci) computes the C tile rows [m0, m1) x cols [n0, n1) from
     A's row panel and B's column panel (inputs replicated: no data-path collective; `gather_c`
     assembles C on every rank when asked)."""
+
+    @staticmethod
+    def panels_needed():
+        """Per operand, the piece a tile needs, from the plans of gemm's i and j dimensions: A is
+        sharded along i (row panel) and replicated along j, B the other way (column panel)."""
+        pi, pj = fixture_plan("gemm", "gemm", 0), fixture_plan("gemm", "gemm", 1)
+        out = {}
+        for a in ("A", "B"):
+            ki, kj = pi["arrays"][a]["kind"], pj["arrays"][a]["kind"]
+            out[a] = "rows" if ki == "block" and kj == "all" else "cols" if ki == "all" and kj == "view" else "all"
+        return out
 
     def __init__(self, m, n, k, rank, world):
         self.m, self.n, self.k, self.rank, self.world = m, n, k, rank, world

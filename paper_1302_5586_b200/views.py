@@ -82,6 +82,24 @@ def fixture_source(name):
     return s.decode()
 
 
+def dist_plan(source, fn):
+    """Distribution plan of fn's parallel loop nest (pencil_dist_plan, csrc/distplan.cpp): per
+    loop dimension, each array's class (block / view / via / all) and the derived sets `owned`,
+    `halo`, `replicated` (all-gathered when produced sharded) and the loop's reduction variables
+    (all-reduced).  `source` is a unit's text or a fixture name ("spmv", "gemm", ...)."""
+    import json
+    lib = _lib.load()
+    if "(" not in source:
+        source = fixture_source(source)
+    n = lib.pencil_dist_plan(source.encode(), fn.encode(), None, 0)
+    if n < 0:
+        check_status()
+        raise KeyError(fn)
+    buf = ctypes.create_string_buffer(n + 1)
+    lib.pencil_dist_plan(source.encode(), fn.encode(), buf, n + 1)
+    return json.loads(buf.value.decode())
+
+
 def gemv_t_views(m, n, lda, incx, incy):
     """(A, x, y) views of the gemv_t fixture for these scalars, from its affine forms."""
     arr = (_lib.pencil_view * 3)()

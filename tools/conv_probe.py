@@ -21,7 +21,9 @@ out = {}
 if "f32" in which:
     img = torch.from_numpy(synth.f32(h * w)).cuda(); o = torch.zeros(h * w, device="cuda")
     kf = (synth.BINOMIAL.astype(np.float32) / 256.0).astype(np.float32)
-    out["conv_f32_ms"] = t(lambda: pb.device.conv5x5_f32(h, w, img, kf, o)); del img, o
+    out["conv_f32_ms"] = t(lambda: pb.device.conv5x5_f32(h, w, img, kf, o))
+    kg = synth.f32(25, 9)  # generic taps (not powers of two): the as-written kernel
+    out["conv_f32_generic_ms"] = t(lambda: pb.device.conv5x5_f32(h, w, img, kg, o)); del img, o
 # u8 / u8b: binomial (separable kernels) and sharpen (25-tap kernels); u8sharp / u8bsharp: sharpen only
 if "u8" in which or "u8sharp" in which:
     img = torch.from_numpy(synth.u8_i32(h * w)).cuda(); o = torch.empty(h * w, dtype=torch.int32, device="cuda")
