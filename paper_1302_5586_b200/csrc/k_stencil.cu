@@ -1018,7 +1018,7 @@ __device__ __forceinline__ constexpr bool tap_on(int di, int dj) {
 
 // Row r (slot S = r mod 5 of the rotation) enters: A[(r - di + 2) mod 5] += taps of row di.
 // Then output row r - 2 is complete: requantise, store (when it lies in [i0, i1)), reset.
-template <int NP, int S, bool DIA>
+template <int NP, int S, bool DIA, bool SH0>
 __device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c, int lane, int r_end, bool body,
                                             bool halo, unsigned char (*ring)[SwarGeom<NP>::ROWE],
                                             unsigned (&A)[5][NP / 2], Sweep<unsigned char>& sw,
@@ -1056,7 +1056,7 @@ __device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c,
 #pragma unroll
         for (int t = 0; t < NP / 2; t++) {
             unsigned v = umax16x2(A[D][t], a.bias2) - a.bias2;  // the numerator, clamped at 0
-            v = (v >> a.shift) & ((0xffffu >> a.shift) * 0x00010001u);
+            if (!SH0) v = (v >> a.shift) & ((0xffffu >> a.shift) * 0x00010001u);  // scale 1: no shift
             q[t] = umin16x2(v, 0x00ff00ffu);
         }
         unsigned rr[NP / 4];
@@ -1070,7 +1070,7 @@ __device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c,
     for (int t = 0; t < NP / 2; t++) A[D][t] = a.half2;
 }
 
-template <int NP, bool DIA>
+template <int NP, bool DIA, bool SH0 = false>
 __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_kernel(int h, int w,
                                                                              const unsigned char* __restrict__ img,
                                                                              unsigned char* __restrict__ out,
@@ -1107,11 +1107,11 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_kernel(i
     // slots stay compile-time constants (rows before r_begin are skipped)
     const int rb5 = r_begin - ((r_begin % 5) + 5) % 5;
     for (int r = rb5; r < r_end; r += 5) {
-        if (r + 0 >= r_begin) swar2d_step<NP, 0, DIA>(w, r + 0, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
-        if (r + 1 >= r_begin && r + 1 < r_end) swar2d_step<NP, 1, DIA>(w, r + 1, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
-        if (r + 2 >= r_begin && r + 2 < r_end) swar2d_step<NP, 2, DIA>(w, r + 2, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
-        if (r + 3 >= r_begin && r + 3 < r_end) swar2d_step<NP, 3, DIA>(w, r + 3, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
-        if (r + 4 >= r_begin && r + 4 < r_end) swar2d_step<NP, 4, DIA>(w, r + 4, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        if (r + 0 >= r_begin) swar2d_step<NP, 0, DIA, SH0>(w, r + 0, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        if (r + 1 >= r_begin && r + 1 < r_end) swar2d_step<NP, 1, DIA, SH0>(w, r + 1, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        if (r + 2 >= r_begin && r + 2 < r_end) swar2d_step<NP, 2, DIA, SH0>(w, r + 2, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        if (r + 3 >= r_begin && r + 3 < r_end) swar2d_step<NP, 3, DIA, SH0>(w, r + 3, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        if (r + 4 >= r_begin && r + 4 < r_end) swar2d_step<NP, 4, DIA, SH0>(w, r + 4, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
     }
     cp_wait<0>();
 }
@@ -1433,7 +1433,9 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
         const bool n16 = w % 16 == 0 && (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0;
         const int np = n16 ? 16 : 8;
         dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
-        if (n16 && dia) stencil_bytes_swar2d_kernel<16, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+        if (n16 && dia && s2.shift == 0)
+            stencil_bytes_swar2d_kernel<16, true, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+        else if (n16 && dia) stencil_bytes_swar2d_kernel<16, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
         else if (n16) stencil_bytes_swar2d_kernel<16, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
         else if (dia) stencil_bytes_swar2d_kernel<8, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
         else stencil_bytes_swar2d_kernel<8, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
