@@ -238,10 +238,16 @@ def bench_spmv(args, torch, pb, rank, world, dist):
             res["e2e"] = e2e
     if rank == 0 and not args.dist_path and not args.no_e2e:
         res["e2e"] = e2e_spmv(args, torch, pb, rowptr, col, val, x)
+        res["src_e2e"] = e2e_spmv(args, torch, pb, rowptr, col, val, x, fn="spmv_inline")
+    if rank == 0 and not args.dist_path:
+        res["src_cpu"] = {}
+        cpu_ref(args, res["src_cpu"], lambda L: L.spmv_inline(nrows, nrows, nnz, P(rowptr), P(col), P(val), P(x),
+                                                               P(np.zeros(nrows, np.float32))),
+                algo, "full matrix, spmv_inline")
     return res
 
 
-def e2e_spmv(args, torch, pb, rowptr, col, val, x):
+def e2e_spmv(args, torch, pb, rowptr, col, val, x, fn="spmv_vec"):
     """drop-in C ABI on host buffers, H2D + plan + kernel + D2H per call (synchronous): pinned
     (the headline `e2e`) and pageable (plain numpy, as a C program relinked from the emitted
     OpenMP passes its malloc'd arrays) — median over the steps after one warm-up call."""
@@ -251,9 +257,9 @@ def e2e_spmv(args, torch, pb, rowptr, col, val, x):
     def mk(pinned):
         hrp, hcol, hval, hx = (host_buf(torch, a, pinned) for a in (rowptr, col, val, x))
         hy = host_buf(torch, np.zeros(nrows, np.float32), pinned)
-        return lambda: pb.dropin.spmv_vec(nrows, nrows, nnz, hrp, hcol, hval, hx, hy)
-    e = e2e_calls(torch, pb, mk, algo, "GB/s", "spmv_vec (drop-in C ABI on host arrays: pinned = the headline "
-                  "value, pageable beside it)", reps=max(2, min(args.steps, 5)))
+        return lambda: getattr(pb.dropin, fn)(nrows, nrows, nnz, hrp, hcol, hval, hx, hy)
+    e = e2e_calls(torch, pb, mk, algo, "GB/s", "%s (drop-in C ABI on host arrays: pinned = the headline "
+                  "value, pageable beside it)" % fn, reps=max(2, min(args.steps, 5)))
     if "ms_per_call" in e.get("pinned", {}):
         e["ms_per_call"] = e["pinned"]["ms_per_call"]
     return e
@@ -1015,6 +1021,10 @@ def main():
                     order="source order (spmv_inline / ACCESS spmv): each row folded in order, bit-identical to "
                           "the emitted C; row chains carried lane to lane",
                     measured_ceiling_ms=res["ceiling_ms"])}, **line["suite"])
+                if res.get("src_e2e"):
+                    line["suite"]["spmv_inline_2e24"]["e2e"] = res["src_e2e"]
+                if res.get("src_cpu", {}).get("cpu_baseline"):
+                    line["suite"]["spmv_inline_2e24"]["cpu_baseline"] = res["src_cpu"]["cpu_baseline"]
             # the measured peak is a copy test (read + write); read-mostly streams go past it, so
             # every bandwidth line also carries its fraction of the B200 spec (8 TB/s HBM3e)
             for v in line["suite"].values():
