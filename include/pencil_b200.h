@@ -103,6 +103,11 @@ int pencil_conv5x5_f32_band_dev(pencil_stream_t s, int h, int w, int out_lo, int
                                 float* out);
 int pencil_gemm_dev(pencil_stream_t s, int m, int n, int k, float alpha, float beta, const float* A,
                     const float* B, float* C);
+/* gemm on strided views: A m x k with row pitch lda, B k x n pitch ldb, C m x n pitch ldc (a tile of a
+ * larger C, a column panel of B — the views of the distribution plan's gemm split, §10); the
+ * operands are read in place by TMA when base and pitch are 16-byte multiples */
+int pencil_gemm_strided_dev(pencil_stream_t s, int m, int n, int k, float alpha, float beta, const float* A,
+                            long long lda, const float* B, long long ldb, float* C, long long ldc);
 
 /* CSR inspector/executor: the plan is built once per sparsity structure (one pass over rowptr)
  * and reused by every SpMV on that structure.  mode: 0 = row sums in source order (spmv_inline,

@@ -46,6 +46,7 @@ SIGNATURES = {
     "pencil_conv5x5_u8_band_dev": (c_int, [P, c_int, c_int, c_int, P, P, P, P, P]),
     "pencil_conv5x5_f32_band_dev": (c_int, [P, c_int, c_int, c_int, c_int, P, P, P, P, P]),
     "pencil_gemm_dev": (c_int, [P, c_int, c_int, c_int, c_float, c_float, P, P, P]),
+    "pencil_gemm_strided_dev": (c_int, [P, c_int, c_int, c_int, c_float, c_float, P, c_ll, P, c_ll, P, c_ll]),
     "pencil_csr_plan_create": (c_int, [P, c_int, c_int, c_int, P, c_int, ctypes.POINTER(c_void_p)]),
     "pencil_csr_plan_destroy": (c_int, [P]),
     "pencil_csr_plan_info": (c_int, [P, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),

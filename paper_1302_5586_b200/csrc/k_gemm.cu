@@ -177,7 +177,7 @@ struct TileRaster {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, int M,
-                       int N, int K, float alpha, float beta, float* __restrict__ C) {
+                       int N, int K, float alpha, float beta, float* __restrict__ C, long long ldc) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -318,7 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (row < M && n0 + c0 < N) {
-                    float* crow = C + (long long)row * N + n0 + c0;
+                    float* crow = C + (long long)row * ldc + n0 + c0;
                     const int ncols = min(32, N - (n0 + c0));
                     if (ncols == 32 && ((uintptr_t)crow & 15) == 0) {
 #pragma unroll
@@ -354,21 +354,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
 }
 
-// rows x cols (pitch cols) -> dst with pitch dpitch (a multiple of 4 floats); the padding columns
+// rows x cols (pitch spitch) -> dst with pitch dpitch (a multiple of 4 floats); the padding columns
 // are never read (the tensor map's extent is cols)
-__global__ void pack_rows_kernel(const float* __restrict__ src, long long rows, int cols, int dpitch,
-                                 float* __restrict__ dst) {
+__global__ void pack_rows_kernel(const float* __restrict__ src, long long spitch, long long rows, int cols,
+                                 int dpitch, float* __restrict__ dst) {
     const long long total = rows * cols;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const long long r = i / cols;
-        dst[r * dpitch + (i - r * cols)] = src[i];
+        const long long r = i / cols, c = i - r * cols;
+        dst[r * dpitch + c] = src[r * spitch + c];
     }
 }
 
-__global__ void scale_c_kernel(long long n, float alpha, float beta, float* __restrict__ C) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        C[i] = alpha * 0.f + (beta != 0.f ? beta * C[i] : 0.f);
+__global__ void scale_c_kernel(long long rows, int cols, long long ldc, float alpha, float beta,
+                               float* __restrict__ C) {
+    const long long n = rows * cols;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / cols;
+        float* c = C + r * ldc + (i - r * cols);
+        *c = alpha * 0.f + (beta != 0.f ? beta * *c : 0.f);
+    }
 }
 
 // ---------------------------------------------------------------- host side
@@ -403,41 +408,46 @@ bool make_map(CUtensorMap* m, const float* base, int inner, int outer, long long
 }
 
 // an operand TMA can read in place: 16-byte aligned base and row pitch
-bool in_place(const void* p, int cols) { return ((uintptr_t)p & 15) == 0 && cols % 4 == 0; }
+bool in_place(const void* p, long long pitch) { return ((uintptr_t)p & 15) == 0 && pitch % 4 == 0; }
 size_t pad4(int c) { return ((size_t)c + 3) & ~(size_t)3; }
 
 }  // namespace
 
-size_t gemm_workspace_bytes(int m, int n, int k, const float* A, const float* B) {
+size_t gemm_workspace_bytes(int m, int n, int k, const float* A, long long lda, const float* B, long long ldb) {
     size_t b = 0;
-    if (!in_place(A, k)) b += (size_t)m * pad4(k) * sizeof(float) + 256;
-    if (!in_place(B, n)) b += (size_t)k * pad4(n) * sizeof(float) + 256;
+    if (!in_place(A, lda)) b += (size_t)m * pad4(k) * sizeof(float) + 256;
+    if (!in_place(B, ldb)) b += (size_t)k * pad4(n) * sizeof(float) + 256;
     return b;
 }
 
-int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, const float* A,
-                const float* B, float* C, void* workspace, size_t workspace_bytes) {
+// C (m x n, row pitch ldc) = alpha A B + beta C with A m x k (pitch lda), B k x n (pitch ldb): the
+// fixture's contiguous call has lda = k, ldb = n, ldc = n; strided views (a tile of a larger C, a
+// column panel of B) pass their parents' pitches.
+int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, const float* A, long long lda,
+                const float* B, long long ldb, float* C, long long ldc, void* workspace, size_t workspace_bytes) {
     if (m <= 0 || n <= 0) return 0;
-    if (workspace_bytes < gemm_workspace_bytes(m, n, k, A, B)) return (int)cudaErrorInvalidValue;
+    if (lda < k || ldb < n || ldc < n) return (int)cudaErrorInvalidValue;
+    if (workspace_bytes < gemm_workspace_bytes(m, n, k, A, lda, B, ldb)) return (int)cudaErrorInvalidValue;
     if (k == 0) {  // empty sum: C = alpha * 0 + beta * C, as the epilogue would write it
-        scale_c_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>((long long)m * n, alpha, beta, C);
+        scale_c_kernel<<<PENCIL_NUM_SMS * 8, 256, 0, st>>>(m, n, ldc, alpha, beta, C);
         return (int)cudaGetLastError();
     }
-    long long lda = k, ldb = n;
     uintptr_t ws = ((uintptr_t)workspace + 255) & ~(uintptr_t)255;
     const int grid_pack = PENCIL_NUM_SMS * 8;
-    if (!in_place(A, k)) {
+    if (!in_place(A, lda)) {
         float* a2 = (float*)ws;
-        lda = (long long)pad4(k);
-        pack_rows_kernel<<<grid_pack, 256, 0, st>>>(A, m, k, (int)lda, a2);
+        const long long p = (long long)pad4(k);
+        pack_rows_kernel<<<grid_pack, 256, 0, st>>>(A, lda, m, k, (int)p, a2);
         A = a2;
-        ws = ((uintptr_t)(a2 + (size_t)m * lda) + 255) & ~(uintptr_t)255;
+        lda = p;
+        ws = ((uintptr_t)(a2 + (size_t)m * p) + 255) & ~(uintptr_t)255;
     }
-    if (!in_place(B, n)) {
+    if (!in_place(B, ldb)) {
         float* b2 = (float*)ws;
-        ldb = (long long)pad4(n);
-        pack_rows_kernel<<<grid_pack, 256, 0, st>>>(B, k, n, (int)ldb, b2);
+        const long long p = (long long)pad4(n);
+        pack_rows_kernel<<<grid_pack, 256, 0, st>>>(B, ldb, k, n, (int)p, b2);
         B = b2;
+        ldb = p;
     }
     CUtensorMap maps[2];
     if (!make_map(&maps[0], A, k, m, lda, BK, CTA_M, CU_TENSOR_MAP_SWIZZLE_64B) ||
@@ -457,6 +467,7 @@ int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, c
     }
     const int tiles = ((m + TILE_M - 1) / TILE_M) * ((n + TILE_N - 1) / TILE_N);
     const int clusters = tiles < max_clusters ? tiles : max_clusters;
-    gemm_3xtf32_kernel<<<2 * clusters, GEMM_THREADS, SMEM_BYTES, st>>>(maps[0], maps[1], m, n, k, alpha, beta, C);
+    gemm_3xtf32_kernel<<<2 * clusters, GEMM_THREADS, SMEM_BYTES, st>>>(maps[0], maps[1], m, n, k, alpha, beta, C,
+                                                                       ldc);
     return (int)cudaGetLastError();
 }

@@ -63,9 +63,9 @@ int launch_conv5x5_f32_band(cudaStream_t st, int h, int w, int out_lo, int out_h
                             const float* const* top, const float* const* bot, const float* k25, float* out);
 
 // k_gemm.cu
-int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, const float* A,
-                const float* B, float* C, void* workspace, size_t workspace_bytes);
-size_t gemm_workspace_bytes(int m, int n, int k, const float* A, const float* B);
+int launch_gemm(cudaStream_t st, int m, int n, int k, float alpha, float beta, const float* A, long long lda,
+                const float* B, long long ldb, float* C, long long ldc, void* workspace, size_t workspace_bytes);
+size_t gemm_workspace_bytes(int m, int n, int k, const float* A, long long lda, const float* B, long long ldb);
 
 // k_micro.cu (measurement probes, not PENCIL kernels)
 int launch_micro_gather(cudaStream_t st, int mode, long long n, const int* idx, const float* table,

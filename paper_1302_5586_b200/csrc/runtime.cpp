@@ -682,11 +682,11 @@ void gemm(int m, int n, int k, float alpha, float beta, float* A, float* B, floa
     st[1] = {B, nullptr, sizeof(float) * nz((long long)k * n), IN};
     st[2] = {C, nullptr, sizeof(float) * nz((long long)m * n), INOUT};
     dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
-        size_t wb = gemm_workspace_bytes(m, n, k, (const float*)st[0].dev, (const float*)st[1].dev);
+        size_t wb = gemm_workspace_bytes(m, n, k, (const float*)st[0].dev, k, (const float*)st[1].dev, n);
         void* ws = nullptr;
         if (wb && pool_alloc(c, s, wb, &ws)) return (int)cudaErrorMemoryAllocation;
-        int e = launch_gemm(s, m, n, k, alpha, beta, (const float*)st[0].dev, (const float*)st[1].dev,
-                            (float*)st[2].dev, ws, wb);
+        int e = launch_gemm(s, m, n, k, alpha, beta, (const float*)st[0].dev, k, (const float*)st[1].dev, n,
+                            (float*)st[2].dev, n, ws, wb);
         pool_free(s, ws);
         return e;
     });
@@ -838,17 +838,23 @@ int pencil_conv5x5_f32_band_dev(pencil_stream_t s, int h, int w, int out_lo, int
     DEV_RET(e);
 }
 
-int pencil_gemm_dev(pencil_stream_t s, int m, int n, int k, float alpha, float beta, const float* A,
-                    const float* B, float* C) {
+int pencil_gemm_strided_dev(pencil_stream_t s, int m, int n, int k, float alpha, float beta, const float* A,
+                            long long lda, const float* B, long long ldb, float* C, long long ldc) {
     if (m < 0 || n < 0 || k < 0) return fail(PENCIL_E_ARG, "negative extent");
+    if (lda < k || ldb < n || ldc < n)
+        return fail(PENCIL_E_ARG, "gemm pitches must cover the rows: lda >= k, ldb >= n, ldc >= n");
     DEV_PROLOGUE;
-    size_t wb = gemm_workspace_bytes(m, n, k, A, B);
+    size_t wb = gemm_workspace_bytes(m, n, k, A, lda, B, ldb);
     void* ws = nullptr;
     if (wb && pool_alloc(c, st, wb, &ws)) return g_status;
-    int e = launch_gemm(st, m, n, k, alpha, beta, A, B, C, ws, wb);
+    int e = launch_gemm(st, m, n, k, alpha, beta, A, lda, B, ldb, C, ldc, ws, wb);
     pool_free(st, ws);
-    if (e == -1) return fail(PENCIL_E_UNSUPPORTED, "gemm shape m=%d n=%d k=%d has no tcgen05 schedule", m, n, k);
     DEV_RET(e);
+}
+
+int pencil_gemm_dev(pencil_stream_t s, int m, int n, int k, float alpha, float beta, const float* A,
+                    const float* B, float* C) {
+    return pencil_gemm_strided_dev(s, m, n, k, alpha, beta, A, k, B, n, C, n);
 }
 
 struct pencil_csr_plan : CsrPlanImpl {};

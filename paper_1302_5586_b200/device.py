@@ -96,6 +96,13 @@ def gemm(m, n, k, alpha, beta, A, B, C, stream=None):
                                      C.data_ptr()))
 
 
+def gemm_strided(m, n, k, alpha, beta, A, lda, B, ldb, C, ldc, stream=None):
+    """gemm on strided views (pencil_gemm_strided_dev): A, B, C are tensors whose first element is
+    the view's (0, 0); rows are lda / ldb / ldc elements apart."""
+    _chk(_lib.load().pencil_gemm_strided_dev(_stream(stream), m, n, k, alpha, beta, A.data_ptr(), lda,
+                                             B.data_ptr(), ldb, C.data_ptr(), ldc))
+
+
 class CsrPlan:
     """Inspector for one CSR sparsity structure (mode 0: row sums in source order — spmv_inline,
     spmv; mode 1: reassociation licensed — spmv_vec)."""

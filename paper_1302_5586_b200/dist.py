@@ -465,6 +465,14 @@ class GemmTileGrid:
     def step(self, local_gemm, alpha, beta, Ap, Bp, C_tile):
         return local_gemm(self.m1 - self.m0, self.n1 - self.n0, self.k, alpha, beta, Ap, Bp, C_tile)
 
+    def step_views(self, gemm_strided, alpha, beta, A, B, C):
+        """The rank's tile on views of the replicated operands (no panel copies): A's row panel
+        (rows m0.., pitch k), B's column panel (columns n0.., pitch n) and C's tile (pitch n) —
+        the plan's split: A a block along i, B a view along j (views.dist_plan("gemm", "gemm"))."""
+        m, n, k = self.m, self.n, self.k
+        return gemm_strided(self.m1 - self.m0, self.n1 - self.n0, k, alpha, beta, A[self.m0 * k:], k,
+                            B[self.n0:], n, C[self.m0 * n + self.n0:], n)
+
     def gather_c(self, c_tile):
         """All-gather every rank's tile (padded to the largest) and assemble the m x n matrix."""
         import torch

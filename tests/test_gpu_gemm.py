@@ -83,3 +83,45 @@ def test_gemm_full_mantissa_wide_exponents(cuda):
     A, B, C = full_mantissa(m * k), full_mantissa(k * n), full_mantissa(m * n)
     err = _check(pb, cuda, m, n, k, 1.0, 1.0, A, B, C)
     assert err <= TOL, err
+
+
+@pytest.mark.parametrize("pitches", [(0, 0, 0), (4, 8, 12), (3, 5, 1)])
+def test_gemm_strided_views(cuda, pitches):
+    """A, B, C as views into wider arrays (row pitches lda > k, ldb > n, ldc > n); odd pitches
+    take the padded copies; the elements between the views' rows are left alone"""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    m, n, k = 300, 260, 72
+    lda, ldb, ldc = k + pitches[0], n + pitches[1], n + pitches[2]
+    rng = np.random.default_rng(11)
+    Aw = rng.random((m, lda), dtype=np.float32) - 0.5
+    Bw = rng.random((k, ldb), dtype=np.float32) - 0.5
+    Cw = rng.random((m, ldc), dtype=np.float32) - 0.5
+    Ad, Bd, Cd = (torch.from_numpy(a.reshape(-1).copy()).cuda() for a in (Aw, Bw, Cw))
+    pb.device.gemm_strided(m, n, k, 1.25, 0.5, Ad, lda, Bd, ldb, Cd, ldc)
+    got = Cd.cpu().numpy().reshape(m, ldc)
+    A2, B2 = Aw[:, :k].astype(np.float64), Bw[:, :n].astype(np.float64)
+    ref = 1.25 * (A2 @ B2) + 0.5 * Cw[:, :n]
+    scale = 1.25 * (np.abs(A2) @ np.abs(B2)) + 0.5 * np.abs(Cw[:, :n])
+    assert normwise_err(got[:, :n], ref, scale) <= TOL
+    assert np.array_equal(got[:, n:], Cw[:, n:])  # the gaps between C's rows are untouched
+
+
+def test_gemm_tile_grid_on_views(cuda):
+    """GemmTileGrid.step_views: every rank's tile from views of the replicated A, B straight into
+    its place in C (no panel copies); the assembled C equals one whole-matrix gemm bit for bit
+    (same tiles, same K order per output)"""
+    import paper_1302_5586_b200 as pb
+    from paper_1302_5586_b200.dist import GemmTileGrid
+    torch = cuda
+    m, n, k, world = 1000, 1200, 256, 8
+    A, B = synth.f32(m * k, 5), synth.f32(k * n, 6)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    C = torch.zeros(m * n, device="cuda")
+    for rank in range(world):
+        GemmTileGrid(m, n, k, rank, world).step_views(pb.device.gemm_strided, 1.0, 0.0, Ad, Bd, C)
+    whole = torch.zeros(m * n, device="cuda")
+    pb.device.gemm(m, n, k, 1.0, 0.0, Ad, Bd, whole)
+    A2, B2 = A.reshape(m, k).astype(np.float64), B.reshape(k, n).astype(np.float64)
+    assert normwise_err(C.cpu().numpy().reshape(m, n), A2 @ B2, np.abs(A2) @ np.abs(B2)) <= TOL
+    assert torch.equal(C, whole)
