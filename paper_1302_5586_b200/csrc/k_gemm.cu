@@ -32,6 +32,14 @@
 //   warps 6-9 epilogue (both CTAs): tcgen05.ld 32x32b.x32 (TMEM lane quarter = warp % 4) ->
 //             alpha, beta -> 128-bit stores, then one arrive per warp on the leader's
 //             `tmem_empty` — so tile t's epilogue overlaps tile t+1's main loop.
+//
+// Measured (16384^3 / 8192^3, tools/gemm_ab.sh): round 1's split prologue + 2-CTA kernel 37.4 ms
+// (1.39 ms of it the split kernels); this kernel 34.6-36.5 ms (box to box) / 3.77 ms = 291 TFLOP/s,
+// tensor pipe 97.8 % of active cycles at the power-capped 1.50 GHz.  Its first build ran 54 ms —
+// unchanged with one MMA per k-step instead of three (so not tensor-bound), 39 ms with the converter
+// loop removed: the converter used generic LD/ST on shared addresses and `.release.cluster` remote
+// arrives (MEMBAR.ALL.GPU + ERRBAR per arrive); explicit ld/st.shared.v4 and default-semantics
+// arrives fixed it.  (Those were timing-only builds with wrong results, not kept.)
 #include <cuda.h>
 
 #include "common.cuh"
@@ -124,13 +132,8 @@ __device__ __forceinline__ uint64_t desc_a(uint32_t saddr) {
 __device__ __forceinline__ uint64_t desc_b(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-#ifndef GEMM_DBG_SWAP_B
     d |= (uint64_t)(B_CHUNK_BYTES >> 4) << 16;  // LBO: next 32-column chunk
     d |= (uint64_t)(512 >> 4) << 32;            // SBO: next 4 k
-#else
-    d |= (uint64_t)(512 >> 4) << 16;
-    d |= (uint64_t)(B_CHUNK_BYTES >> 4) << 32;
-#endif
     d |= (uint64_t)1 << 46;
     d |= (uint64_t)1 << 61;                     // SWIZZLE_128B_BASE32B
     return d;
@@ -258,13 +261,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                         const uint64_t oa = (uint64_t)(ks * 32) >> 4;    // 8 tf32 = 32 B along K in the A atom
                         const uint64_t ob = (uint64_t)(ks * 1024) >> 4;  // 8 k = two 4-k atoms of B
                         const uint32_t acc = (kb | ks) != 0;
-#ifndef GEMM_DBG_ONEMMA
                         mma_tf32_2sm(d, alo + oa, bhi + ob, acc);  // small terms first
                         mma_tf32_2sm(d, ahi + oa, blo + ob, 1);
                         mma_tf32_2sm(d, ahi + oa, bhi + ob, 1);
-#else
-                        mma_tf32_2sm(d, ahi + oa, bhi + ob, acc);
-#endif
                     }
                     commit_2sm(&empty[s]);  // frees the stage in both CTAs once these MMAs have read it
                 }
@@ -279,7 +278,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                 const int s = g % STAGES;
                 mbar_wait(&full[s], (g / STAGES) & 1);
                 const uint32_t src = smem_u32(smem + s * STAGE_BYTES) + 16 * ct;
-#ifndef GEMM_DBG_NOCONV
                 uint4 v[HI_BYTES / 16 / 128];
 #pragma unroll
                 for (int j = 0; j < HI_BYTES / 16 / 128; j++) v[j] = lds128(src + j * 2048);
@@ -287,7 +285,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                 for (int j = 0; j < HI_BYTES / 16 / 128; j++)
                     sts128(src + HI_BYTES + j * 2048,
                            make_uint4(lo_tf32(v[j].x), lo_tf32(v[j].y), lo_tf32(v[j].z), lo_tf32(v[j].w)));
-#endif
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(&conv[s]);
