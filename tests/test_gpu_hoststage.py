@@ -1,0 +1,88 @@
+"""Pageable host arrays through the drop-in ABI (csrc/hoststage.cpp): malloc'd / numpy memory of
+4 MB and more goes through the multi-threaded pinned staging ring instead of the driver's
+single-threaded bounce buffer.  Results must equal the pinned-memory calls bit for bit — whole
+buffers, ragged sizes (not multiples of a chunk or of 64 bytes), the fp32 stencil's interior-only
+copy-back (its border bytes untouched), the pipelined SpMV upload / y download — and concurrent
+calls from several host threads must not mix their chunks."""
+import threading
+
+import numpy as np
+import pytest
+
+from paper_1302_5586_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def pinned(torch, a):
+    return torch.from_numpy(a).pin_memory()
+
+
+def test_gemv_pageable_equals_pinned(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    m, n = 4099, 2053  # 33.7 MB of A: two ring chunks and a ragged tail
+    A, x = synth.f32(m * n, 3), synth.f32(n, 4)
+    y_pg = synth.f32(m, 5)
+    y_pin = pinned(torch, y_pg.copy())
+    pb.dropin.gemv(m, n, 1.5, 0.5, A, x, y_pg)
+    pb.dropin.gemv(m, n, 1.5, 0.5, pinned(torch, A), pinned(torch, x), y_pin)
+    assert np.array_equal(y_pg.view(np.uint32), y_pin.numpy().view(np.uint32))
+
+
+def test_conv_f32_interior_copy_back_pageable(cuda):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    h, w = 2051, 2049
+    img, k = synth.f32(h * w, 6), synth.f32(25, 7)
+    out_pg = np.full(h * w, np.nan, np.float32)
+    out_pin = pinned(torch, out_pg.copy())
+    pb.dropin.conv5x5_f32(h, w, img, k, out_pg)
+    pb.dropin.conv5x5_f32(h, w, pinned(torch, img), k, out_pin)
+    assert np.array_equal(out_pg.view(np.uint32), out_pin.numpy().view(np.uint32))
+    o = out_pg.reshape(h, w)
+    border = np.ones((h, w), bool)
+    border[2:h - 2, 2:w - 2] = False
+    assert np.isnan(o[border]).all() and not np.isnan(o[~border]).any()
+
+
+@pytest.mark.parametrize("fn", ["spmv_vec", "spmv_inline"])
+def test_spmv_pipelined_pageable_equals_pinned(cuda, fn):
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    rowptr, col, val, x, _ = synth.csr_powerlaw(1 << 20, seed=9)  # ~2^24 non-zeros: the pipelined path
+    nrows, nnz = rowptr.size - 1, col.size
+    y_pg = np.zeros(nrows, np.float32)
+    y_pin = pinned(torch, np.zeros(nrows, np.float32))
+    getattr(pb.dropin, fn)(nrows, nrows, nnz, rowptr, col, val, x, y_pg)
+    getattr(pb.dropin, fn)(nrows, nrows, nnz, *(pinned(torch, a) for a in (rowptr, col, val, x)), y_pin)
+    assert np.array_equal(y_pg.view(np.uint32), y_pin.numpy().view(np.uint32))
+
+
+def test_concurrent_pageable_calls(cuda):
+    import paper_1302_5586_b200 as pb
+    m, n = 2048, 2560  # 21 MB of A per call
+    A = [synth.f32(m * n, 10 + t) for t in range(4)]
+    x = synth.f32(n, 20)
+    refs = []
+    for t in range(4):
+        y = np.zeros(m, np.float32)
+        pb.dropin.gemv(m, n, 1.0, 0.0, A[t], x, y)
+        refs.append(y)
+    errors = []
+
+    def worker(t):
+        try:
+            for _ in range(4):
+                y = np.zeros(m, np.float32)
+                pb.dropin.gemv(m, n, 1.0, 0.0, A[t], x, y)
+                assert np.array_equal(y.view(np.uint32), refs[t].view(np.uint32))
+        except BaseException as e:  # noqa: BLE001
+            errors.append((t, repr(e)))
+
+    ts = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
