@@ -431,7 +431,7 @@ __device__ __forceinline__ void seg_store(float* p, float v) { __stcs(p, v); }
 // chain can hold (it starts at +0, so it is never -0): bit-identical to the emitted C.
 template <int E>
 __device__ __forceinline__ void seg_ordered(int lane, unsigned sb, const float (&pr)[E], float* __restrict__ y,
-                                            SegState& S) {
+                                            SegState& S, float* __restrict__ sfold) {
     const bool brk = sb != 0;
     const int f = brk ? __ffs(sb) - 1 : E, l = brk ? 31 - __clz(sb) : E;
     auto fold_all = [&](float c) {
@@ -449,6 +449,24 @@ __device__ __forceinline__ void seg_ordered(int lane, unsigned sb, const float (
         co = fold_all(lane == 0 ? S.carry : 0.f);
     }
     const unsigned nb = __ballot_sync(0xffffffffu, brk);
+    if (E == 4 && nb == 0) {
+        // the whole window continues one row (rows > 128 non-zeros): its chain is 128 adds in a row
+        // whichever way it is split, so lane 0 folds the staged products itself — 32 LDS.128 + 128
+        // FADD instead of 32 shuffle-and-refold rounds
+        reinterpret_cast<float4*>(sfold)[lane] = make_float4(pr[0], pr[E > 1 ? 1 : 0], pr[E > 2 ? 2 : 0], pr[E > 3 ? 3 : 0]);
+        __syncwarp();
+        float c = S.carry;
+        if (lane == 0) {
+#pragma unroll 8
+            for (int q = 0; q < 32; q++) {
+                const float4 v = reinterpret_cast<const float4*>(sfold)[q];
+                c = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(c, v.x), v.y), v.z), v.w);
+            }
+        }
+        S.carry = __shfl_sync(0xffffffffu, c, 0);
+        __syncwarp();  // the slice is free for the next window
+        return;
+    }
     unsigned run = ~nb;
     int R = 0;
     while (run) {  // longest run of breaker-free lanes (warp-uniform)
@@ -553,13 +571,14 @@ __device__ __forceinline__ void seg_fetch(int qa, int P0, int P1, int nnz_len, i
 }
 
 template <int E, bool ORDERED>
-__device__ __forceinline__ void seg_reduce(int lane, const SegWin<E>& w, float* __restrict__ y, SegState& S) {
+__device__ __forceinline__ void seg_reduce(int lane, const SegWin<E>& w, float* __restrict__ y, SegState& S,
+                                           float* __restrict__ sfold) {
     float pr[E];
 #pragma unroll
     for (int k = 0; k < E; k++) pr[k] = (w.use >> k) & 1u ? __fmul_rn(w.v[k], w.xv[k]) : 0.f;  // rounds on its own
     const unsigned sb = w.sb;
     if (ORDERED) {
-        seg_ordered<E>(lane, sb, pr, y, S);
+        seg_ordered<E>(lane, sb, pr, y, S, sfold);
         return;
     }
     // the lane's segments: head (before its first start: closes the row open on entry), tail (from
@@ -622,7 +641,8 @@ __device__ __forceinline__ void seg_reduce(int lane, const SegWin<E>& w, float* 
 template <int E, bool ORDERED>
 __device__ __forceinline__ void seg_tile(int P0, int P1, int nnz_len, int ncols, int lane, const int* __restrict__ col,
                                          const float* __restrict__ val, const float* __restrict__ x,
-                                         const unsigned* __restrict__ rs_bits, float* __restrict__ y, SegState& S) {
+                                         const unsigned* __restrict__ rs_bits, float* __restrict__ y, SegState& S,
+                                         float* __restrict__ sfold) {
     constexpr int W = 32 * E;
     int qa = P0 & ~(E - 1);
     if (qa >= P1) return;
@@ -636,7 +656,7 @@ __device__ __forceinline__ void seg_tile(int P0, int P1, int nnz_len, int ncols,
             if (qn + W <= P1) seg_fetch<E, true>(qn, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, nxt, S.bad);
             else seg_fetch<E, false>(qn, P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, nxt, S.bad);
         }
-        seg_reduce<E, ORDERED>(lane, cur, y, S);
+        seg_reduce<E, ORDERED>(lane, cur, y, S, sfold);
         if (!more) break;
         cur = nxt;
         qa = qn;
@@ -657,6 +677,8 @@ __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
     }
     const int lane = threadIdx.x & 31;
     const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
+    __shared__ __align__(16) float s_fold[ORDERED ? WARPS_PER_CTA : 1][ORDERED ? 4 * 32 : 4];  // one row's window
+    float* sfold = s_fold[ORDERED ? threadIdx.x >> 5 : 0];
     auto clampp = [&](int v) { return v < 0 ? 0 : (v > nnz_len ? nnz_len : v); };
     for (;;) {
         unsigned ticket = 0;
@@ -672,7 +694,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
         const int P0 = clampp(__ldg(rowptr + r0));
         const int P1 = max(P0, clampp(__ldg(rowptr + r1)));
         SegState S{r0, 0.f, false};
-        seg_tile<SEG_E, ORDERED>(P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S);
+        seg_tile<SEG_E, ORDERED>(P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S, sfold);
         if (lane == 0) seg_store(y + S.row, S.carry);  // the tile's last row (S.row == r1 - 1)
         if (S.bad) raise_fault(status, FAULT_OOB_LOAD);
         if (DIST) {
