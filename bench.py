@@ -241,9 +241,9 @@ def bench_spmv(args, torch, pb, rank, world, dist):
         res["src_e2e"] = e2e_spmv(args, torch, pb, rowptr, col, val, x, fn="spmv_inline")
     if rank == 0 and not args.dist_path:
         res["src_cpu"] = {}
+        hy = np.zeros(nrows, np.float32)  # kept alive across the calls (the C writes through its pointer)
         cpu_ref(args, res["src_cpu"], lambda L: L.spmv_inline(nrows, nrows, nnz, P(rowptr), P(col), P(val), P(x),
-                                                               P(np.zeros(nrows, np.float32))),
-                algo, "full matrix, spmv_inline")
+                                                               P(hy)), algo, "full matrix, spmv_inline")
     return res
 
 
