@@ -502,7 +502,7 @@ __global__ void u8_rearm_kernel(unsigned* flag) { *flag = 0u; }
 // peer mappings, cp.async straight into the ring), so a multi-GPU stencil step is one launch per
 // rank and no halo copy.  Same sweep, arithmetic and policies as stencil_ring_kernel (the output
 // is bit-identical to the single-GPU image's rows); h = the band's own rows.
-template <bool U8, bool POW2, bool SEP = false, bool DIA = false>
+template <bool U8, bool POW2, bool SEP = false, bool DIA = false, int PF = 0>
 __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? STENCIL_U8_MINB : STENCIL_F32_MINB)) stencil_band_kernel(
     int h, int w, const typename Pol<U8>::T* __restrict__ img, typename Pol<U8>::T* __restrict__ out,
     typename Pol<U8>::A a, BandSrc<typename Pol<U8>::T> bs) {
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
         cp_commit();
     }
     u64 W[5][7];
-    unsigned orv = 0;
+    unsigned orv = PF ? ~0u : 0u;
 #pragma unroll
     for (int d = 0; d < 4; d++) {
         cp_wait<S_RING - 1>();
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
         T* slot = ring[(i0 - 2 + d + S_RING) % S_RING];
         {
             u64 P[7];
-            ring_read<U8>(slot, w, c0, lane, a, P, orv);
+            ring_read<U8, typename Pol<U8>::A, PF>(slot, w, c0, lane, a, P, orv);
             enter_row<SEP>(P, W[d], a);
         }
         __syncwarp();
@@ -548,14 +548,47 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
     sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;
     sw.dst = out + (long long)i0 * w + c;
     for (int i = i0; i < i1; i += 5) {
-        stencil_step<U8, 4, POW2, SEP, true, DIA>(w, i, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
-        if (i + 1 < i1) stencil_step<U8, 0, POW2, SEP, true, DIA>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
-        if (i + 2 < i1) stencil_step<U8, 1, POW2, SEP, true, DIA>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
-        if (i + 3 < i1) stencil_step<U8, 2, POW2, SEP, true, DIA>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
-        if (i + 4 < i1) stencil_step<U8, 3, POW2, SEP, true, DIA>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        stencil_step<U8, 4, POW2, SEP, true, DIA, PF>(w, i, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 1 < i1) stencil_step<U8, 0, POW2, SEP, true, DIA, PF>(w, i + 1, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 2 < i1) stencil_step<U8, 1, POW2, SEP, true, DIA, PF>(w, i + 2, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 3 < i1) stencil_step<U8, 2, POW2, SEP, true, DIA, PF>(w, i + 3, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
+        if (i + 4 < i1) stencil_step<U8, 3, POW2, SEP, true, DIA, PF>(w, i + 4, c, lane, r_end, L, ring, W, sw, orv, a, &bs, h);
     }
     cp_wait<0>();
     if (U8 && __any_sync(0xffffffffu, (orv & ~255u) != 0) && lane == 0) atomicOr(a.repair_flag, 1u);
+    if constexpr (!U8 && PF != 0)  // as stencil_ring_kernel: a pixel the fused taps cannot take exactly
+        if (__any_sync(0xffffffffu, orv < a.pf_lim) && lane == 0) atomicOr(a.repair_flag, 1u);
+}
+
+// f32_repair_kernel for a band: the band's output rows [out_lo, out_hi) as written, the halo rows
+// read where they live (BandSrc); exits at once unless the PF band sweep flagged a pixel
+__global__ void f32_band_repair_kernel(int h, int w, const float* __restrict__ img, float* __restrict__ out,
+                                       StencilArgsF32 a, BandSrc<float> bs) {
+    if (*(volatile unsigned*)a.repair_flag == 0) return;
+    const long long iw = w - 4, n = (long long)(bs.out_hi - bs.out_lo) * iw;
+    auto row = [&](int r) -> const float* {
+        return r < 0 ? (r == -2 ? bs.top[0] : bs.top[1]) : (r >= h ? (r == h ? bs.bot[0] : bs.bot[1]) : img + (long long)r * w);
+    };
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        const int i = bs.out_lo + (int)(p / iw), j = 2 + (int)(p % iw);
+        float acc = 0.f;
+#pragma unroll 1
+        for (int di = 0; di < 5; di++) {
+            const float* rp = row(i + di - 2);
+#pragma unroll
+            for (int dj = 0; dj < 5; dj++) acc = __fadd_rn(acc, __fmul_rn(a.kf[di * 5 + dj], rp[j + dj - 2]));
+        }
+        out[(long long)i * w + j] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(a.repair_flag + 1, 1u) == gridDim.x - 1) {
+            a.repair_flag[1] = 0u;
+            *(volatile unsigned*)a.repair_flag = 0u;
+        }
+    }
 }
 
 // the exact int64 repair pass of a band (rows outside it through BandSrc)
@@ -1378,7 +1411,19 @@ int launch_conv5x5_f32_band(cudaStream_t st, int h, int w, int out_lo, int out_h
     a.negmag = pack2(-8388608.0f);
     const BandSrc<float> bs = {{top[0], top[1]}, {bot[0], bot[1]}, out_lo, out_hi};
     dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (out_hi - out_lo + S_BAND - 1) / S_BAND);
-    stencil_band_kernel<false, false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+    // power-of-two taps fused as in launch_conv5x5_f32, with the band's own guarded repair pass
+    const int pf = pow2_fusable(k25, a.pf_lim);
+    unsigned* flag = pf ? repair_flag_for(st) : nullptr;
+    if (pf && flag) {
+        a.repair_flag = flag + 2;
+        if (pf == 2)
+            stencil_band_kernel<false, false, false, false, 2><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+        else
+            stencil_band_kernel<false, false, false, false, 1><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+        f32_band_repair_kernel<<<PENCIL_NUM_SMS * 4, 256, 0, st>>>(h, w, img, out, a, bs);
+    } else {
+        stencil_band_kernel<false, false><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
+    }
     return (int)cudaGetLastError();
 }
 

@@ -9,6 +9,8 @@ import socket
 import numpy as np
 import pytest
 
+import oracle
+
 pytestmark = pytest.mark.gpu
 
 
@@ -172,7 +174,7 @@ def test_fused_spmv_allgather_chained_in_place(nccl, mode):
 
 
 @pytest.mark.parametrize("h,w,world", [(200, 256, 3), (67, 132, 4), (41, 512, 2)])
-@pytest.mark.parametrize("case", ["binomial", "sharpen", "scale3", "nonbyte", "bigtaps", "f32"])
+@pytest.mark.parametrize("case", ["binomial", "sharpen", "scale3", "nonbyte", "bigtaps", "f32", "f32tiny", "f32generic"])
 def test_band_kernels_read_halos_in_place(cuda, h, w, world, case):
     """The band-sharded sweep (pencil_conv5x5_*_band_dev) on `world` separately allocated bands,
     each reading its halo rows straight out of its neighbours' buffers (the addresses
@@ -185,12 +187,18 @@ def test_band_kernels_read_halos_in_place(cuda, h, w, world, case):
     from paper_1302_5586_b200.dist import band_halo_rows, band_interior, shard_bands
     b = shard_bands(h, world)
     rows = [int(b[q + 1] - b[q]) for q in range(world)]
-    f32 = case == "f32"
+    f32 = case.startswith("f32")
     if f32:
-        img = torch.from_numpy(synth.f32(h * w, seed=3)).cuda()
-        k = (synth.BINOMIAL / 256.0).astype(np.float32)
+        himg = synth.f32(h * w, seed=3)
+        if case == "f32tiny":  # products of the fused power-of-two taps round: the guarded repair pass
+            himg[h // 2 * w + 9] = np.float32(3e-39)
+            himg[(rows[0] - 1) * w + 11] = np.float32(-2e-38)  # in a halo row of rank 1
+        img = torch.from_numpy(himg).cuda()
+        k = synth.f32(25, 9) if case == "f32generic" else (synth.BINOMIAL / 256.0).astype(np.float32)
         whole = torch.zeros(h * w, device="cuda")
         pb.device.conv5x5_f32(h, w, img, k, whole)
+        ref_c = oracle.conv5x5_f32_f32(h, w, himg, k, np.zeros(h * w, np.float32))  # the emitted C as written
+        assert np.array_equal(whole.cpu().numpy().view(np.uint32), ref_c.view(np.uint32))
     else:
         img = torch.from_numpy(synth.u8_i32(h * w, seed=3)).cuda()
         k, scale = {"binomial": (synth.BINOMIAL, 256), "sharpen": (synth.SHARPEN, 1), "scale3": (synth.SHARPEN, 3),
