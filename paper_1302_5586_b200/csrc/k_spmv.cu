@@ -698,6 +698,9 @@ __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
         if (lane == 0) seg_store(y + S.row, S.carry);  // the tile's last row (S.row == r1 - 1)
         if (S.bad) raise_fault(status, FAULT_OOB_LOAD);
         if (DIST) {
+            // the tile's rows leave together, re-read from y (L2) two per lane, as 128-byte runs.
+            // Storing each row to the peers where it closes instead (one more scattered store per
+            // row and peer) measured 1.427 ms against 1.274 for this at world 1 (one target).
             __syncwarp();
             for (int r = r0 + lane; r < r1; r += 64) {
                 const float v0 = y[r], v1 = r + 32 < r1 ? y[r + 32] : 0.f;
