@@ -257,3 +257,64 @@ def test_shard_classes_follow_plans():
     assert dist.ColShardedGemvT.gathered() == ["x"]
     assert dist.GemmTileGrid.panels_needed() == {"A": "rows", "B": "cols"}
     assert dist.dot_allreduce_vars() == ["s"]
+
+
+# --- random nests against the reference trace ---------------------------------------------------
+def random_unit(rng, idx):
+    """A random 2-deep nest: reads of A in rows i + a (a in [-2, 2]) at columns j + b, of a row
+    vector B[j] (replicated), of a column vector c[i + e]; writes y[i*m + j] or z[i]."""
+    reads, terms = [], []
+    for t in range(int(rng.integers(1, 4))):
+        a, b = int(rng.integers(-2, 3)), int(rng.integers(-1, 2))
+        reads.append(("A", a, b))
+        terms.append(f"A[(i + {a}) * m + j + {b}]")
+    if rng.random() < 0.5:
+        terms.append("B[j]")
+    e = int(rng.integers(-1, 2))
+    terms.append(f"c[i + {e}]")
+    write_row = rng.random() < 0.5
+    body = (f"      y[i * m + j] = {' + '.join(terms)};\n" if write_row else
+            f"      s += {' + '.join(terms)};\n")
+    src = f"""void f{idx}(int n, int m, float A[restrict const static n * m], float B[restrict const static m],
+          float c[restrict const static n], float y[restrict const static n * m], float z[restrict const static n])
+{{
+  #pragma pencil independent
+  for (int i = 2; i < n - 2; i++) {{
+    float s;
+    s = 0.0;
+    for (int j = 1; j < m - 1; j++) {{
+{body}    }}
+    z[i] = s;
+  }}
+}}
+"""
+    a_lo = min(a for _, a, _ in reads)
+    a_hi = max(a for _, a, _ in reads)
+    return src, (a_lo, a_hi), e, "B[j]" in terms, write_row
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_nests_against_reference_trace(seed):
+    rng = np.random.default_rng(100 + seed)
+    src, (a_lo, a_hi), e, has_b, write_row = random_unit(rng, seed)
+    fn = f"f{seed}"
+    p = views.dist_plan(src, fn)["dims"][0]
+    assert cls(p, "A")[:4] == ("r", "block", "m", (a_lo, a_hi))
+    assert cls(p, "c")[:4] == ("r", "block", "1", (e, e))
+    assert ("B" in p["replicated"]) == has_b
+    assert p["owned"] == (["y", "z"] if write_row else ["z"])
+    n, m = 9, 7
+    f32 = lambda k: (rng.random(k, dtype=np.float32) - np.float32(0.5))  # noqa: E731
+    args = [n, m, f32(n * m), f32(m), f32(n), np.zeros(n * m, np.float32), np.zeros(n, np.float32)]
+    names = ["n", "m", "A", "B", "c", "y", "z"]
+    for it in (2, 4, 6):
+        unit = re.sub(r"for \(int i = 2; i < n - 2; i\+\+\)", f"for (int i = {it}; i < {it} + 1; i++)", src)
+        for argi, idx, wr in oracle.ref_trace(unit, fn, args):
+            name = names[argi]
+            c = p["arrays"][name]
+            if c["kind"] == "block":
+                s = {"m": m, "1": 1}[c["stride"]]
+                lo_h, hi_h = c["halo"]
+                assert it + lo_h <= idx // s <= it + hi_h, (name, it, idx, c)
+            if wr:
+                assert name in p["owned"] and c["kind"] == "block" and idx // {"m": m, "1": 1}[c["stride"]] == it
