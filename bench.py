@@ -896,6 +896,9 @@ def reference_arm(args):
     nrows = 1 << 24
     rowptr, col, val, x, xm = synth.csr_powerlaw(nrows)
     cores = os.cpu_count()
+    # all host threads, whatever the launcher set (torchrun exports OMP_NUM_THREADS=1 per rank)
+    cpu_lib()
+    ctypes.CDLL("libgomp.so.1").omp_set_num_threads(cores)
     ts = cpu_spmv(args.steps, min(args.warmup, 3), rowptr, col, val, x)
     _, build = cpu_lib()
     t = statistics.mean(ts)
@@ -905,8 +908,8 @@ def reference_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(spmv_config(nrows, int(col.size), xm),
-                           parallelism=f"openmp x{os.environ.get('OMP_NUM_THREADS', cores)}"),
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": int(os.environ.get("OMP_NUM_THREADS", cores)),
+                           parallelism=f"openmp x{cores}"),
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores,
                              "kind": "reference", "host": host_cpu(),
                              "sample": "full matrix, one spmv_vec call per step: C emitted by the reference's "
                                        "emit_openmp (outer-loop pragma), %s" % build},
