@@ -938,6 +938,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl != "reference":
+        # torchrun exports OMP_NUM_THREADS=1: the synthetic-input generator (OpenMP, outside every
+        # timed region) gets its share of the host instead
+        try:
+            ctypes.CDLL("libgomp.so.1").omp_set_num_threads(max(1, (os.cpu_count() or 1) // world))
+        except OSError:
+            pass
 
     if args.impl == "reference":
         if rank == 0:
