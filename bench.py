@@ -990,12 +990,12 @@ def main():
                 "config": dict(res["config"], parallelism=f"row-sharded x{world}" if args.dist_path else "single GPU"),
                 "gpu_launches": res["launches"]}
         if not args.dist_path:
-            line["roofline"] = {"bound": "hbm", "kernel": "csr_seg_kernel<0, 0>", "achieved": kernel_gbs,
+            line["roofline"] = {"bound": "hbm", "kernel": "csr_seg_kernel<0, 0, 0>", "achieved": kernel_gbs,
                                 "peak": hbm, "unit": "GB/s", "frac": kernel_gbs / hbm,
                                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
                                 "frac_spec": kernel_gbs / SPEC_HBM_GBS,
                                 "algorithmic_bytes_per_launch": res["bytes"],
-                                "traffic": ncu_traffic("csr_seg_kernel<0, 0>"),
+                                "traffic": ncu_traffic("csr_seg_kernel<0, 0, 0>"),
                                 "measured_ceiling": {
                                     "kernel": "micro_gather_val: the same col/val stream + x gathers, no rows "
                                               "(random 4-byte gathers are L1->XBAR request-rate bound, DESIGN.md §3)",
@@ -1027,7 +1027,7 @@ def main():
             line["suite"] = suite(args, torch, pb, hbm)
             if res.get("src_ms"):
                 line["suite"] = dict({"spmv_inline_2e24": bw_line(
-                    res["src_ms"], res["bytes"], hbm, "csr_seg_kernel<0, 1>",
+                    res["src_ms"], res["bytes"], hbm, "csr_seg_kernel<0, 1, 0>",
                     order="source order (spmv_inline / ACCESS spmv): each row folded in order, bit-identical to "
                           "the emitted C; row chains carried lane to lane",
                     measured_ceiling_ms=res["ceiling_ms"])}, **line["suite"])

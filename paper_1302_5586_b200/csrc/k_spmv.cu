@@ -412,12 +412,18 @@ __global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_flow_kernel(
 // before this window's gathers (no gain), a ballot-based segmented scan with one shuffle per
 // round (1.160: more ALU), and L2 evict-first stores / row-start loads (no change).
 struct SegState {
-    int row;      // the row open at the next window's first position
+    int row;      // the row open at the next window's first position (its ordinal among the
+                  // non-empty rows when the matrix has empty rows)
     float carry;  // its partial sum from the earlier windows
     bool bad;     // a column index outside [0, ncols) was seen
+    const int* rowmap;  // plans with empty rows: ordinal -> row (NULL: ordinal == row)
 };
 
 __device__ __forceinline__ void seg_store(float* p, float v) { __stcs(p, v); }
+// y's element of the row with ordinal o
+__device__ __forceinline__ float* seg_addr(float* y, const SegState& S, int o) {
+    return y + (S.rowmap ? __ldg(S.rowmap + o) : o);
+}
 
 // Source order (spmv_inline, ACCESS spmv: the row loop must fold in order) on the same window: a
 // row's sum is one chain s = (((0 + p_a) + p_b) + ...), each add rounded, so a row spanning several
@@ -494,20 +500,20 @@ __device__ __forceinline__ void seg_ordered(int lane, unsigned sb, const float (
 #pragma unroll
         for (int k = 0; k < E; k++)
             if (k < f) h = __fadd_rn(h, pr[k]);
-        __stcs(y + ro, h);
+        __stcs(seg_addr(y, S, ro), h);
         float a = 0.f;
         int nseg = 0;
 #pragma unroll
         for (int k = 0; k < E; k++) {
             if (k < f || k >= l) continue;
             if (k > f && ((sb >> k) & 1u)) {
-                __stcs(y + ro + 1 + nseg, a);
+                __stcs(seg_addr(y, S, ro + 1 + nseg), a);
                 a = 0.f;
                 nseg++;
             }
             a = __fadd_rn(a, pr[k]);
         }
-        if (l > f) __stcs(y + ro + 1 + nseg, a);  // the row from the last-but-one start closes at l
+        if (l > f) __stcs(seg_addr(y, S, ro + 1 + nseg), a);  // the row from the last-but-one start closes at l
     }
     S.carry = __shfl_sync(0xffffffffu, co, 31);
     S.row += total;
@@ -612,7 +618,7 @@ __device__ __forceinline__ void seg_reduce(int lane, const SegWin<E>& w, float* 
     if (lane == 0) excl = S.carry;
     if (cnt) {  // y streams out (evict-first): its 64 MB must not push x out of L2
         const int ro = S.row + before;  // the row open on entry to this lane
-        seg_store(y + ro, excl + head);
+        seg_store(seg_addr(y, S, ro), excl + head);
         if (cnt > 1) {  // rows wholly inside the lane
             float a = 0.f;
             int nseg = 0;
@@ -620,7 +626,7 @@ __device__ __forceinline__ void seg_reduce(int lane, const SegWin<E>& w, float* 
             for (int k = 0; k < E; k++) {
                 if (k < f) continue;
                 if (k > f && ((sb >> k) & 1u)) {
-                    seg_store(y + ro + 1 + nseg, a);
+                    seg_store(seg_addr(y, S, ro + 1 + nseg), a);
                     a = 0.f;
                     nseg++;
                 }
@@ -663,13 +669,13 @@ __device__ __forceinline__ void seg_tile(int P0, int P1, int nnz_len, int ncols,
     }
 }
 
-template <bool DIST, bool ORDERED>
+template <bool DIST, bool ORDERED, bool EMPTY>
 __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
     const int* __restrict__ tile_row, int ntiles, const unsigned* __restrict__ plan,
-    const unsigned* __restrict__ rs_bits, unsigned* __restrict__ tk, unsigned* __restrict__ status,
-    const PeerSet ps) {
+    const unsigned* __restrict__ rs_bits, const int* __restrict__ ord, const int* __restrict__ rowmap,
+    unsigned* __restrict__ tk, unsigned* __restrict__ status, const PeerSet ps) {
     if (plan[0]) {
         spmv_generic_t<DIST>(nrows, ncols, nnz_len, rowptr, col, val, x, y, status, ps);
         if (DIST) __threadfence_system();
@@ -693,10 +699,13 @@ __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
         if (r0 >= r1) continue;
         const int P0 = clampp(__ldg(rowptr + r0));
         const int P1 = max(P0, clampp(__ldg(rowptr + r1)));
-        SegState S{r0, 0.f, false};
-        seg_tile<SEG_E, ORDERED>(P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S, sfold);
-        if (lane == 0) seg_store(y + S.row, S.carry);  // the tile's last row (S.row == r1 - 1)
-        if (S.bad) raise_fault(status, FAULT_OOB_LOAD);
+        if (P1 > P0) {  // (a tile of empty rows only has nothing to fold: their y is zeroed before the launch)
+            // EMPTY is a compile-time flag so that without empty rows the row names fold to ordinals
+            SegState S{EMPTY ? __ldg(ord + r0) : r0, 0.f, false, EMPTY ? rowmap : nullptr};
+            seg_tile<SEG_E, ORDERED>(P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S, sfold);
+            if (lane == 0) seg_store(seg_addr(y, S, S.row), S.carry);  // the tile's last non-empty row
+            if (S.bad) raise_fault(status, FAULT_OOB_LOAD);
+        }
         if (DIST) {
             // the tile's rows leave together, re-read from y (L2) two per lane, as 128-byte runs.
             // Storing each row to the peers where it closes instead (one more scattered store per
@@ -724,6 +733,98 @@ int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, 
 
 size_t csr_rs_words(int nnz_len) { return (size_t)(nnz_len > 0 ? nnz_len : 1) / 32 + 2; }
 
+// Plans with empty rows (monotone rowptr): ord[r] = number of non-empty rows before row r
+// (r = 0..nrows) and rowmap[ord[r]] = r for every non-empty row, so that the segmented executor
+// — which counts row starts, i.e. non-empty rows — can name each row it closes.  Three passes of
+// an exclusive scan over the rows: per-block counts, a one-block scan of those, and the per-block
+// scans that write ord and rowmap.
+constexpr int ORD_BLOCKS = 1024;
+__device__ __forceinline__ int row_nonempty(const int* __restrict__ rowptr, long long r) {
+    return __ldg(rowptr + r + 1) > __ldg(rowptr + r);
+}
+__global__ void csr_ord_count_kernel(int nrows, const int* __restrict__ rowptr, int* __restrict__ bsum) {
+    const long long per = ((long long)nrows + ORD_BLOCKS - 1) / ORD_BLOCKS;
+    const long long lo = blockIdx.x * per, hi = min((long long)nrows, lo + per);
+    int c = 0;
+    for (long long r = lo + threadIdx.x; r < hi; r += blockDim.x) c += row_nonempty(rowptr, r);
+    c = __reduce_add_sync(0xffffffffu, c);
+    __shared__ int ws[32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < (int)blockDim.x / 32; w++) t += ws[w];
+        bsum[blockIdx.x] = t;
+    }
+}
+__global__ void csr_ord_scan_blocks_kernel(int* __restrict__ bsum) {  // one block of ORD_BLOCKS threads
+    __shared__ int s[ORD_BLOCKS];
+    const int t = threadIdx.x;
+    s[t] = bsum[t];
+    __syncthreads();
+    for (int d = 1; d < ORD_BLOCKS; d <<= 1) {  // inclusive Hillis-Steele
+        const int v = t >= d ? s[t - d] : 0;
+        __syncthreads();
+        s[t] += v;
+        __syncthreads();
+    }
+    bsum[t] = t ? s[t - 1] : 0;  // exclusive
+}
+__global__ void csr_ord_write_kernel(int nrows, const int* __restrict__ rowptr, const int* __restrict__ boff,
+                                     int* __restrict__ ord, int* __restrict__ rowmap) {
+    const long long per = ((long long)nrows + ORD_BLOCKS - 1) / ORD_BLOCKS;
+    const long long lo = blockIdx.x * per, hi = min((long long)nrows, lo + per);
+    __shared__ int ws[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int base = boff[blockIdx.x];
+    for (long long r0 = lo; r0 < hi; r0 += blockDim.x) {
+        const long long r = r0 + threadIdx.x;
+        const int f = r < hi ? row_nonempty(rowptr, r) : 0;
+        const unsigned b = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) ws[warp] = __popc(b);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < nw; w++) {
+            before += w < warp ? ws[w] : 0;
+            total += ws[w];
+        }
+        const int o = base + before + __popc(b & ((1u << lane) - 1u));
+        if (r < hi) {
+            ord[r] = o;
+            if (f) rowmap[o] = (int)r;
+        }
+        base += total;
+        __syncthreads();
+    }
+    if (hi == nrows && lo < hi && threadIdx.x == 0) ord[nrows] = base;
+}
+
+int launch_csr_ordinals(cudaStream_t st, int nrows, const int* rowptr, int* ord, int* rowmap, int* bsum) {
+    if (nrows <= 0) return 0;
+    csr_ord_count_kernel<<<ORD_BLOCKS, 256, 0, st>>>(nrows, rowptr, bsum);
+    csr_ord_scan_blocks_kernel<<<1, ORD_BLOCKS, 0, st>>>(bsum);
+    csr_ord_write_kernel<<<ORD_BLOCKS, 256, 0, st>>>(nrows, rowptr, bsum, ord, rowmap);
+    return (int)cudaGetLastError();
+}
+size_t csr_ord_scratch_ints() { return ORD_BLOCKS; }
+
+// the segmented executor's four forms (reassociated / source order, with / without empty rows)
+template <bool DIST>
+void seg_launch(cudaStream_t st, int grid, int assoc, int nrows, int ncols, int nnz_len, const int* rowptr,
+                const int* col, const float* val, const float* x, float* y, const int* tile_row, int ntiles,
+                const unsigned* plan_flags, const SegPlan& seg, unsigned* tk, unsigned* status, const PeerSet& ps) {
+#define SEG_ARGS nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, seg.rs_bits, seg.ord, \
+                 seg.rowmap, tk, status, ps
+    if (seg.ord) {
+        if (assoc) csr_seg_kernel<DIST, false, true><<<grid, SPMV_THREADS, 0, st>>>(SEG_ARGS);
+        else csr_seg_kernel<DIST, true, true><<<grid, SPMV_THREADS, 0, st>>>(SEG_ARGS);
+    } else {
+        if (assoc) csr_seg_kernel<DIST, false, false><<<grid, SPMV_THREADS, 0, st>>>(SEG_ARGS);
+        else csr_seg_kernel<DIST, true, false><<<grid, SPMV_THREADS, 0, st>>>(SEG_ARGS);
+    }
+#undef SEG_ARGS
+}
+
 // Executor choice: the continuous-stream kernel when col / val are 16-byte aligned (1.25 ms at
 // 2^24 rows), else the scalar-load kernel (any alignment; 1.28 ms).  Measured and dropped (numbers
 // at 2^24 rows; the code is in the git history before the round-2 clean-up, commit be69d3c):
@@ -744,8 +845,9 @@ size_t csr_rs_words(int nnz_len) { return (size_t)(nnz_len > 0 ? nnz_len : 1) / 
 // the last warp re-arms it, so launches on one stream never share it with another stream's.
 int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                     const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                    const int* tile_row, int ntiles, const unsigned* plan_flags, const unsigned* rs_bits,
+                    const int* tile_row, int ntiles, const unsigned* plan_flags, const SegPlan& seg,
                     unsigned* tk, unsigned* status) {
+    const unsigned* rs_bits = seg.rs_bits;
     if (nrows <= 0) return 0;
     int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;  // persistent: at most one wave
     if (grid > PENCIL_NUM_SMS * CTAS_PER_SM) grid = PENCIL_NUM_SMS * CTAS_PER_SM;
@@ -753,16 +855,10 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
 #ifdef PENCIL_VARIANT_NO_SEG
     rs_bits = nullptr;  // A/B build: the batch-and-fold executor for every mode
 #endif
-    if (rs_bits && aligned) {  // no empty rows: segmented executor (scan, or carried in source order)
+    if (rs_bits && aligned) {  // segmented executor (scan, or carried in source order)
         if (grid > PENCIL_NUM_SMS * SEG_CTAS_PER_SM) grid = PENCIL_NUM_SMS * SEG_CTAS_PER_SM;
-        if (assoc)
-            csr_seg_kernel<false, false><<<grid, SPMV_THREADS, 0, st>>>(
-                nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, rs_bits, tk, status,
-                PeerSet{});
-        else
-            csr_seg_kernel<false, true><<<grid, SPMV_THREADS, 0, st>>>(
-                nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, rs_bits, tk, status,
-                PeerSet{});
+        seg_launch<false>(st, grid, assoc, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags,
+                          seg, tk, status, PeerSet{});
         return (int)cudaGetLastError();
     }
     if (aligned) {
@@ -799,21 +895,16 @@ __global__ void dist_rows_kernel(int nrows, const float* __restrict__ y, const P
 
 int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                          const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                         const int* tile_row, int ntiles, const unsigned* plan_flags, const unsigned* rs_bits,
+                         const int* tile_row, int ntiles, const unsigned* plan_flags, const SegPlan& seg,
                          unsigned* tk, unsigned* status, const PeerSet& peers) {
+    const unsigned* rs_bits = seg.rs_bits;
     if (nrows <= 0) return 0;
     const bool aligned = (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0;
     if (rs_bits && aligned) {
         int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
         if (grid > PENCIL_NUM_SMS * SEG_CTAS_PER_SM) grid = PENCIL_NUM_SMS * SEG_CTAS_PER_SM;
-        if (assoc)
-            csr_seg_kernel<true, false><<<grid, SPMV_THREADS, 0, st>>>(
-                nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, rs_bits, tk, status,
-                peers);
-        else
-            csr_seg_kernel<true, true><<<grid, SPMV_THREADS, 0, st>>>(
-                nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags, rs_bits, tk, status,
-                peers);
+        seg_launch<true>(st, grid, assoc, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags,
+                         seg, tk, status, peers);
         return (int)cudaGetLastError();
     }
     if (aligned) {
@@ -829,7 +920,7 @@ int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int n
     }
     // unaligned col/val: the regular executor, then the rows leave in a second launch
     int e = launch_csr_spmv(st, assoc, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles,
-                            plan_flags, nullptr, tk, status);
+                            plan_flags, SegPlan{}, tk, status);
     if (e) return e;
     long long blocks = ((long long)nrows + 255) / 256;
     if (blocks > PENCIL_NUM_SMS * 8) blocks = PENCIL_NUM_SMS * 8;

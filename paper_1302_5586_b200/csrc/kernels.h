@@ -24,12 +24,21 @@ int launch_axpy(cudaStream_t st, long long n, float a, const float* a_dev, const
 int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
                     int ntiles, int* tile_row, unsigned* plan_flags, unsigned* rs_bits, unsigned* status);
 size_t csr_rs_words(int nnz_len);
+// plans with empty rows: ord (nrows + 1 ints) / rowmap (one int per non-empty row), bsum scratch
+int launch_csr_ordinals(cudaStream_t st, int nrows, const int* rowptr, int* ord, int* rowmap, int* bsum);
+size_t csr_ord_scratch_ints();
+// The segmented executor's plan data: rs_bits = the row-start bitmap when it may run (monotone
+// rowptr, aligned col / val), else NULL; for plans with empty rows, ord / rowmap (else NULL) — the
+// executor then writes only the non-empty rows: the caller zeroes y first.
+struct SegPlan {
+    const unsigned* rs_bits = nullptr;
+    const int* ord = nullptr;
+    const int* rowmap = nullptr;
+};
 // tk: the per-(device, stream) tile-ticket word (zero between launches; the kernels re-arm it)
-// rs_bits: the plan's row-start bitmap when the segmented executor may run (reassociation licensed,
-// monotone rowptr, no empty row), else NULL
 int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                     const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                    const int* tile_row, int ntiles, const unsigned* plan_flags, const unsigned* rs_bits,
+                    const int* tile_row, int ntiles, const unsigned* plan_flags, const SegPlan& seg,
                     unsigned* tk, unsigned* status);
 int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const int* rowptr,
                        const int* col, const float* val, const float* x, float* y,
@@ -46,7 +55,7 @@ struct PeerSet {
 };
 int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_len,
                          const int* rowptr, const int* col, const float* val, const float* x, float* y,
-                         const int* tile_row, int ntiles, const unsigned* plan_flags, const unsigned* rs_bits,
+                         const int* tile_row, int ntiles, const unsigned* plan_flags, const SegPlan& seg,
                          unsigned* tk, unsigned* status, const PeerSet& peers);
 
 // k_conv.cu  (taps are host arrays, passed to the kernels by value)

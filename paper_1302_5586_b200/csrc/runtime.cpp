@@ -335,27 +335,60 @@ struct CsrPlanImpl {
     int* tile_row = nullptr;
     unsigned* flags = nullptr;
     unsigned* rs_bits = nullptr;  // row-start bitmap
-    int seg = 0;                  // the segmented executor applies (monotone rowptr, no empty row)
-    const unsigned* seg_bits() const { return seg ? rs_bits : nullptr; }
+    int* ord = nullptr;           // plans with empty rows: non-empty ordinal of each row, and its inverse
+    int* rowmap = nullptr;
+    const int* rowptr = nullptr;  // the device rowptr the plan was built from (the ordinals' input)
+    int seg = 0;                  // the segmented executor applies (monotone rowptr)
+    SegPlan seg_plan() const {
+        SegPlan s;
+        if (seg) {
+            s.rs_bits = rs_bits;
+            s.ord = ord;
+            s.rowmap = rowmap;
+        }
+        return s;
+    }
 };
 
 // after the plan kernel: which executor the plan takes (reads its two flag words: a sync on st)
-int csr_plan_finalize(cudaStream_t st, CsrPlanImpl* p) {
+// rows may be empty: the ordinals the segmented executor names its rows by (launch_csr_ordinals)
+int csr_plan_ordinals(DeviceCtx* c, cudaStream_t st, CsrPlanImpl* p) {
+    int* bsum = nullptr;
+    int r;
+    if ((r = pool_alloc(c, st, sizeof(int) * ((size_t)p->nrows + 1), (void**)&p->ord)) ||
+        (r = pool_alloc(c, st, sizeof(int) * ((size_t)p->nrows + 1), (void**)&p->rowmap)) ||
+        (r = pool_alloc(c, st, sizeof(int) * csr_ord_scratch_ints(), (void**)&bsum)))
+        return r;
+    const int e = launch_csr_ordinals(st, p->nrows, p->rowptr, p->ord, p->rowmap, bsum);
+    pool_free(st, bsum);
+    return e ? cuda_fail((cudaError_t)e, "csr ordinals") : PENCIL_OK;
+}
+
+// the empty rows' y before a segmented launch over a plan with empty rows
+cudaError_t zero_empty_rows(const CsrPlanImpl& p, float* y, cudaStream_t st) {
+    return p.seg && p.ord ? cudaMemsetAsync(y, 0, sizeof(float) * (size_t)p.nrows, st) : cudaSuccess;
+}
+
+int csr_plan_finalize(DeviceCtx* c, cudaStream_t st, CsrPlanImpl* p) {
     unsigned f[4] = {0, 0, 0, 0};
     CK(cudaMemcpyAsync(f, p->flags, sizeof f, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    p->seg = p->rs_bits && f[0] == 0 && f[2] == 0;
+    p->seg = p->rs_bits && f[0] == 0;
+    if (p->seg && f[2] != 0) return csr_plan_ordinals(c, st, p);
     return PENCIL_OK;
 }
 void csr_plan_release(cudaStream_t st, CsrPlanImpl& p) {
     pool_free(st, p.tile_row);
     pool_free(st, p.flags);
     pool_free(st, p.rs_bits);
+    pool_free(st, p.ord);
+    pool_free(st, p.rowmap);
 }
 
 int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int* rowptr, int mode,
                    CsrPlanImpl* p, unsigned* fw = nullptr) {
     p->device = c->device;
+    p->rowptr = rowptr;
     p->nrows = nrows;
     p->nnz = nnz;
     p->mode = mode;
@@ -497,11 +530,13 @@ int spmv_pipelined(int mode, int nrows, int ncols, int nnz, const int* rowptr, c
         CK(cudaMemcpyAsync(hb + 1 + b, p.tile_row + t, sizeof(int), cudaMemcpyDeviceToHost, s1));
     }
     CK(cudaStreamSynchronize(s1));
-    p.seg = p.rs_bits && hb[0] == 0 && hb[40] == 0;
+    p.seg = p.rs_bits && hb[0] == 0;
+    if (p.seg && hb[40] != 0 && (r = csr_plan_ordinals(c, s1, &p))) return r;
+    CK(zero_empty_rows(p, dy, s1));
     CK(cudaStreamWaitEvent(s1, pc->ev_x, 0));
     auto launch = [&](long long t0, long long t1) {
         return launch_csr_spmv(s1, mode, nrows, ncols, nnz, drp, dcol, dval, dx, dy, p.tile_row + t0,
-                               (int)(t1 - t0), p.flags, p.seg_bits(), tk1, fw0);
+                               (int)(t1 - t0), p.flags, p.seg_plan(), tk1, fw0);
     };
     const bool y_staged = staged(y, sizeof(float) * (size_t)nrows);  // pageable y: one staged copy at the end
     if (hb[0] != 0) {  // non-monotone rowptr: generic schedule after the whole upload
@@ -548,15 +583,16 @@ int spmv_common(int mode, int nrows, int ncols, int nnz, int* rowptr, int* col, 
     if (nrows == 0) return ok();
     return dropin(st, [&](DeviceCtx* c, cudaStream_t s) -> int {
         CsrPlanImpl p;
-        if (csr_plan_build(c, s, nrows, nnz, (const int*)st[0].dev, mode, &p) || csr_plan_finalize(s, &p)) {
+        if (csr_plan_build(c, s, nrows, nnz, (const int*)st[0].dev, mode, &p) || csr_plan_finalize(c, s, &p)) {
             csr_plan_release(s, p);
             return (int)cudaErrorUnknown;
         }
         unsigned *tk = ticket_word(c, s), *fw = fault_word(c, s);
         if (!tk || !fw) return (int)cudaErrorMemoryAllocation;
+        if (cudaError_t z = zero_empty_rows(p, (float*)st[4].dev, s)) return (int)z;
         int e = launch_csr_spmv(s, mode, nrows, ncols, nnz, (const int*)st[0].dev, (const int*)st[1].dev,
                                 (const float*)st[2].dev, (const float*)st[3].dev, (float*)st[4].dev,
-                                p.tile_row, p.ntiles, p.flags, p.seg_bits(), tk, fw);
+                                p.tile_row, p.ntiles, p.flags, p.seg_plan(), tk, fw);
         csr_plan_release(s, p);
         return e;
     });
@@ -896,7 +932,7 @@ int pencil_csr_plan_create(pencil_stream_t s, int nrows, int ncols, int nnz, con
     DEV_PROLOGUE;
     pencil_csr_plan* p = new pencil_csr_plan();
     p->ncols = ncols;
-    if (csr_plan_build(c, st, nrows, nnz, rowptr_dev, mode ? 1 : 0, p) || csr_plan_finalize(st, p)) {
+    if (csr_plan_build(c, st, nrows, nnz, rowptr_dev, mode ? 1 : 0, p) || csr_plan_finalize(c, st, p)) {
         csr_plan_release(st, *p);
         delete p;
         return g_status;
@@ -910,6 +946,8 @@ int pencil_csr_plan_destroy(pencil_csr_plan_t plan) {
     cudaFree(plan->tile_row);  // pool memory: freed through the device's default stream order
     cudaFree(plan->flags);
     if (plan->rs_bits) cudaFree(plan->rs_bits);
+    if (plan->ord) cudaFree(plan->ord);
+    if (plan->rowmap) cudaFree(plan->rowmap);
     delete plan;
     return ok();
 }
@@ -927,8 +965,9 @@ int pencil_spmv_dev(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr
     DEV_PROLOGUE;
     unsigned *tk = ticket_word(c, st), *fw = fault_word(c, st);
     if (!tk || !fw) return g_status;
+    if (cudaError_t z = zero_empty_rows(*plan, y, st)) return cuda_fail(z, "zero empty rows");
     DEV_RET(launch_csr_spmv(st, plan->mode, plan->nrows, plan->ncols, plan->nnz, rowptr, col, val, x, y,
-                            plan->tile_row, plan->ntiles, plan->flags, plan->seg_bits(), tk, fw));
+                            plan->tile_row, plan->ntiles, plan->flags, plan->seg_plan(), tk, fw));
 }
 
 int pencil_spmv_dev_dist(pencil_stream_t s, pencil_csr_plan_t plan, const int* rowptr, const int* col,
@@ -947,8 +986,9 @@ int pencil_spmv_dev_dist(pencil_stream_t s, pencil_csr_plan_t plan, const int* r
     DEV_PROLOGUE;
     unsigned *tk = ticket_word(c, st), *fw = fault_word(c, st);
     if (!tk || !fw) return g_status;
+    if (cudaError_t z = zero_empty_rows(*plan, y, st)) return cuda_fail(z, "zero empty rows");
     DEV_RET(launch_csr_spmv_dist(st, plan->mode, plan->nrows, plan->ncols, plan->nnz, rowptr, col, val, x, y,
-                                 plan->tile_row, plan->ntiles, plan->flags, plan->seg_bits(), tk, fw, ps));
+                                 plan->tile_row, plan->ntiles, plan->flags, plan->seg_plan(), tk, fw, ps));
 }
 
 int pencil_sync_status(pencil_stream_t s) {

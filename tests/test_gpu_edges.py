@@ -350,3 +350,40 @@ def test_conv_u8_bytes_signed_swar_bit_exact(cuda, h, w):
         ref = oracle.conv5x5_u8(h, w, scale, img, k)
         got = out8.cpu().numpy().astype(np.int64)
         assert np.array_equal(got, ref), (h, w, scale, int(k[12]), np.flatnonzero(got != ref)[:5])
+
+
+@pytest.mark.parametrize("every", [2, 3, 50])
+def test_spmv_empty_rows_take_the_segmented_executor(cuda, every):
+    """A power-law matrix with an empty row inserted after every `every`-th row (runs of empty
+    rows at tile edges included): the segmented executor names rows by their ordinal among the
+    non-empty ones (plan ordinals) and the empty rows' y is zeroed — source order bit-exact against
+    the emitted C semantics, reassociated within the normwise bound, through the device API and the
+    drop-in door on host arrays."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    rowptr, col, val, x, _ = synth.csr_powerlaw(1 << 18, seed=every)
+    n = rowptr.size - 1
+    lens = np.diff(rowptr)
+    nl = np.zeros(n + n // every + 7, np.int64)
+    nl[np.arange(n) + np.arange(n) // every] = lens  # plus 7 trailing empty rows
+    rp2 = np.concatenate([[0], np.cumsum(nl)]).astype(np.int32)
+    n2, nnz = rp2.size - 1, col.size
+    ref = oracle.spmv_f32(n2, x.size, nnz, rp2, col, val, x)
+    rp, cd, vd, xd = (torch.from_numpy(a).cuda() for a in (rp2, col, val, x))
+    for mode in (0, 1):
+        y = torch.full((n2,), float("nan"), device="cuda")
+        plan = pb.device.CsrPlan(n2, x.size, nnz, rp, mode=mode)
+        plan.spmv(rp, cd, vd, xd, y)
+        pb.device.sync_status()
+        got = y.cpu().numpy()
+        if mode == 0:
+            assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+        else:
+            r64 = oracle.spmv(n2, x.size, nnz, rp2, col, val, x)
+            terms = np.abs(val.astype(np.float64) * x.astype(np.float64)[col])
+            scale = np.add.reduceat(np.append(terms, 0.0), rp2[:-1]) * (np.diff(rp2) > 0)
+            assert normwise_err(got, r64, scale) <= 1e-5
+        plan.close()
+    yh = np.full(n2, np.nan, np.float32)
+    pb.dropin.spmv_inline(n2, x.size, nnz, rp2, col, val, x, yh)
+    assert np.array_equal(yh.view(np.uint32), ref.view(np.uint32))
