@@ -8,20 +8,19 @@
 // (csr_plan_kernel), it gives every warp a contiguous row range holding ~TILE_NNZ
 // non-zeros regardless of the power-law row-length distribution.
 //
-// Executors (launch_csr_spmv picks one): csr_seg_kernel (16-byte-aligned col / val, monotone rowptr
-// without empty rows — the plan's flags: per-lane segments over the plan's row-start bitmap, rows
-// scanned across lanes when reassociation is licensed, carried lane to lane in source order
-// otherwise), csr_flow_kernel (aligned, any monotone rowptr: the tile's non-zeros stream in
-// continuous 16-byte-per-lane windows, batches folded from whichever window holds them) and
-// csr_stream_kernel (scalar loads; any alignment).
-// The structure they share — csr_stream_kernel: per tile, per batch of 32 rows, the batch's non-zeros
-// are streamed with coalesced loads (col, val: evict-first) while x[col] is gathered
-// (evict-last, so the 64 MB vector stays L2-resident), staged in shared memory, then each
-// thread folds its own row in source order: s = s + val[k]*x[col[k]], product and sum each
-// rounded to fp32.  That is the reference-emitted C compiled as written, so spmv_inline and
-// spmv (whose row loop is UNKNOWN, i.e. must stay sequential) are bit-identical to it.
-// spmv_vec's reduction pragma (PARALLEL_WITH_REDUCTION) licenses reassociation: rows longer
-// than a warp are then folded by the whole warp (lane partials + shuffle tree).
+// Executors (launch_csr_spmv picks one):
+//   csr_seg_kernel — the default (16-byte-aligned col / val, monotone rowptr): per-lane segments over
+//     the plan's row-start bitmap; rows scanned across lanes when reassociation is licensed
+//     (spmv_vec), carried lane to lane in source order otherwise (spmv_inline, spmv); matrices with
+//     empty rows name their rows through the plan's ordinals (EMPTY form).
+//   csr_flow_kernel — unaligned-safe fallback kept for plans without a row-start bitmap: the tile's
+//     non-zeros stream in continuous 16-byte-per-lane windows and every 32-row batch is folded from
+//     whichever window holds it (each lane its own row, in source order).
+//   csr_stream_kernel — scalar loads, any alignment, same batch-and-fold structure.
+// Every executor keeps the emitted C's rounding where source order is the contract: each product
+// rounds on its own and each row sum is one chain of rounded adds, so spmv_inline and spmv (whose
+// row loop is UNKNOWN, i.e. must stay sequential) are bit-identical to the reference-emitted C;
+// spmv_vec's reduction pragma (PARALLEL_WITH_REDUCTION) licenses reassociation.
 //
 // Faults (E-INTERP analogues): col outside [0, ncols) or rowptr outside [0, nnz] set a bit
 // in the status word and contribute 0.  A non-monotone rowptr (legal in PENCIL: the row
