@@ -13,9 +13,10 @@
 //     the plan's row-start bitmap; rows scanned across lanes when reassociation is licensed
 //     (spmv_vec), carried lane to lane in source order otherwise (spmv_inline, spmv); matrices with
 //     empty rows name their rows through the plan's ordinals (EMPTY form).
-//   csr_flow_kernel — unaligned-safe fallback kept for plans without a row-start bitmap: the tile's
-//     non-zeros stream in continuous 16-byte-per-lane windows and every 32-row batch is folded from
-//     whichever window holds it (each lane its own row, in source order).
+//   csr_flow_kernel — the round-1 executor, now the A/B reference (-DPENCIL_VARIANT_NO_SEG) and the
+//     entry that diverts a non-monotone rowptr to the generic schedule: the tile's non-zeros stream
+//     in continuous 16-byte-per-lane windows and every 32-row batch is folded from whichever window
+//     holds it (each lane its own row, in source order).
 //   csr_stream_kernel — scalar loads, any alignment, same batch-and-fold structure.
 // Every executor keeps the emitted C's rounding where source order is the contract: each product
 // rounds on its own and each row sum is one chain of rounded adds, so spmv_inline and spmv (whose
