@@ -103,7 +103,10 @@ void par_copy(CopyPool& pool, char* dst, size_t dpitch, const char* src, size_t 
     });
 }
 
-constexpr size_t CHUNK = 32u << 20;  // pinned ring: 4 chunks of 32 MB per device
+// pinned ring: 4 chunks of 32 MB per device.  (Pieces of 1/16 of a transfer, 4-32 MB, measured
+// worse: the pipelined SpMV's 70 MB chunks then go as 4 MB pieces and the per-piece dispatch and
+// event waits cost more than the earlier overlap gains — SpMV pageable e2e 45 -> 37 GB/s.)
+constexpr size_t CHUNK = 32u << 20;
 constexpr int RING = 4;
 
 struct Stager {
