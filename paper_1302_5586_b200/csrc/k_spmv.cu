@@ -33,12 +33,25 @@
 // non-zeros per warp tile (plan window); swept over {256..2048} x WCHUNK {64,128,256} at
 // 2^24 rows (tools/spmv_sweep.sh): 1024 x 128 is fastest (1.28 ms; 512: 1.34; 256: 1.59)
 #define SPMV_TILE_NNZ 1024
+// Non-zeros per lane per window and CTAs per SM of the segmented executor, per mode (2^24 rows,
+// tools/ab_spmv_modes.sh): reassociated E 4 at 5 CTAs/SM (48 registers: the one-deep window
+// pipeline) 1.137 ms, E 8 at 4 1.188; source order E 8 at 4 CTAs/SM 1.256 ms, E 4 at 5 1.302
+// (its shuffle rounds are per window: wider windows halve them per non-zero), E 8 at 3 1.323.
 #ifndef SEG_E
-#define SEG_E 4  // non-zeros per lane per window of the segmented executor (8: 1.16-1.19 ms, fewer warps)
+#define SEG_E 4
 #endif
 #ifndef SEG_CTAS_PER_SM
-#define SEG_CTAS_PER_SM 5  // 48 registers: the one-deep window pipeline (seg_tile)
+#define SEG_CTAS_PER_SM 5
 #endif
+#ifndef SEG_E_ORD
+#define SEG_E_ORD 8
+#endif
+#ifndef SEG_CTAS_PER_SM_ORD
+#define SEG_CTAS_PER_SM_ORD 4
+#endif
+#ifndef SEG_LANE0_MAX_E
+#define SEG_LANE0_MAX_E 4  // widest window folded by lane 0 when it lies inside one row: at E 8 the
+#endif                     // 256-add chain in one lane measured 1.310 ms against 1.257 with the rounds
 
 // plan_flags: [0] non-monotone rowptr (generic schedule), [2] some row is empty.  rs_bits (when
 // given): bit k set iff non-zero k is the first of its row — the row-start map of the segmented
@@ -455,17 +468,20 @@ __device__ __forceinline__ void seg_ordered(int lane, unsigned sb, const float (
         co = fold_all(lane == 0 ? S.carry : 0.f);
     }
     const unsigned nb = __ballot_sync(0xffffffffu, brk);
-    if (E == 4 && nb == 0) {
-        // the whole window continues one row (rows > 128 non-zeros): its chain is 128 adds in a row
-        // whichever way it is split, so lane 0 folds the staged products itself — 32 LDS.128 + 128
-        // FADD instead of 32 shuffle-and-refold rounds
-        reinterpret_cast<float4*>(sfold)[lane] = make_float4(pr[0], pr[E > 1 ? 1 : 0], pr[E > 2 ? 2 : 0], pr[E > 3 ? 3 : 0]);
+    if (E % 4 == 0 && E <= SEG_LANE0_MAX_E && nb == 0) {
+        // the whole window continues one row (rows > 32 E non-zeros): its chain is 32 E adds in a
+        // row whichever way it is split, so lane 0 folds the staged products itself — 8 E LDS.128 +
+        // 32 E FADD instead of 32 shuffle-and-refold rounds
+        float4* sf = reinterpret_cast<float4*>(sfold);
+#pragma unroll
+        for (int h = 0; h < E / 4; h++)
+            sf[lane * (E / 4) + h] = make_float4(pr[4 * h], pr[4 * h + 1], pr[4 * h + 2], pr[4 * h + 3]);
         __syncwarp();
         float c = S.carry;
         if (lane == 0) {
 #pragma unroll 8
-            for (int q = 0; q < 32; q++) {
-                const float4 v = reinterpret_cast<const float4*>(sfold)[q];
+            for (int q = 0; q < 8 * E; q++) {
+                const float4 v = sf[q];
                 c = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(c, v.x), v.y), v.z), v.w);
             }
         }
@@ -670,7 +686,7 @@ __device__ __forceinline__ void seg_tile(int P0, int P1, int nnz_len, int ncols,
 }
 
 template <bool DIST, bool ORDERED, bool EMPTY>
-__global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
+__global__ void __launch_bounds__(SPMV_THREADS, ORDERED ? SEG_CTAS_PER_SM_ORD : SEG_CTAS_PER_SM) csr_seg_kernel(
     int nrows, int ncols, int nnz_len, const int* __restrict__ rowptr, const int* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ y,
     const int* __restrict__ tile_row, int ntiles, const unsigned* __restrict__ plan,
@@ -683,7 +699,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
     }
     const int lane = threadIdx.x & 31;
     const unsigned total_warps = gridDim.x * WARPS_PER_CTA;
-    __shared__ __align__(16) float s_fold[ORDERED ? WARPS_PER_CTA : 1][ORDERED ? 4 * 32 : 4];  // one row's window
+    __shared__ __align__(16) float s_fold[ORDERED ? WARPS_PER_CTA : 1][ORDERED ? SEG_E_ORD * 32 : 4];  // a window
     float* sfold = s_fold[ORDERED ? threadIdx.x >> 5 : 0];
     auto clampp = [&](int v) { return v < 0 ? 0 : (v > nnz_len ? nnz_len : v); };
     for (;;) {
@@ -702,7 +718,8 @@ __global__ void __launch_bounds__(SPMV_THREADS, SEG_CTAS_PER_SM) csr_seg_kernel(
         if (P1 > P0) {  // (a tile of empty rows only has nothing to fold: their y is zeroed before the launch)
             // EMPTY is a compile-time flag so that without empty rows the row names fold to ordinals
             SegState S{EMPTY ? __ldg(ord + r0) : r0, 0.f, false, EMPTY ? rowmap : nullptr};
-            seg_tile<SEG_E, ORDERED>(P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S, sfold);
+            seg_tile<ORDERED ? SEG_E_ORD : SEG_E, ORDERED>(P0, P1, nnz_len, ncols, lane, col, val, x, rs_bits, y, S,
+                                                          sfold);
             if (lane == 0) seg_store(seg_addr(y, S, S.row), S.carry);  // the tile's last non-empty row
             if (S.bad) raise_fault(status, FAULT_OOB_LOAD);
         }
@@ -856,7 +873,8 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
     rs_bits = nullptr;  // A/B build: the batch-and-fold executor for every mode
 #endif
     if (rs_bits && aligned) {  // segmented executor (scan, or carried in source order)
-        if (grid > PENCIL_NUM_SMS * SEG_CTAS_PER_SM) grid = PENCIL_NUM_SMS * SEG_CTAS_PER_SM;
+        const int cps = assoc ? SEG_CTAS_PER_SM : SEG_CTAS_PER_SM_ORD;
+        if (grid > PENCIL_NUM_SMS * cps) grid = PENCIL_NUM_SMS * cps;
         seg_launch<false>(st, grid, assoc, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags,
                           seg, tk, status, PeerSet{});
         return (int)cudaGetLastError();
@@ -902,7 +920,8 @@ int launch_csr_spmv_dist(cudaStream_t st, int assoc, int nrows, int ncols, int n
     const bool aligned = (uintptr_t)col % 16 == 0 && (uintptr_t)val % 16 == 0;
     if (rs_bits && aligned) {
         int grid = (ntiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
-        if (grid > PENCIL_NUM_SMS * SEG_CTAS_PER_SM) grid = PENCIL_NUM_SMS * SEG_CTAS_PER_SM;
+        const int cps = assoc ? SEG_CTAS_PER_SM : SEG_CTAS_PER_SM_ORD;
+        if (grid > PENCIL_NUM_SMS * cps) grid = PENCIL_NUM_SMS * cps;
         seg_launch<true>(st, grid, assoc, nrows, ncols, nnz_len, rowptr, col, val, x, y, tile_row, ntiles, plan_flags,
                          seg, tk, status, peers);
         return (int)cudaGetLastError();
