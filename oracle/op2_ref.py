@@ -97,20 +97,42 @@ def mesh_increment_numpy(cells0, edges_val, table):
     return out
 
 
-def compile_lowered_c(doc, outdir):
+def openmp_lowered_c(doc):
+    """The lowered unit with the CPU fix SURVEY §8f.1 names: each driver loop carries
+    `#pragma omp parallel for` with an array-section reduction over the dats it increments
+    (`reduction(+: d[0:n_d])`, OpenMP 4.5) — what emit_openmp's `reduction(+: dcells)` on an array
+    parameter means but cannot express.  Loops that write a dat directly (OP_WRITE / OP_RW through
+    the identity) stay parallel without a reduction; loops with an indirect non-INC write stay serial."""
+    src, arrays, sizes = lower_unit(doc)
+    for li, L in enumerate(doc.get("par_loops", [])):
+        fn = f"{L['kernel']}_loop{li}"
+        inc = _distinct(a["dat"] for a in L["args"] if a.get("access") == "OP_INC")
+        ind_write = any(a.get("map") and a.get("access") in ("OP_WRITE", "OP_RW") for a in L["args"])
+        if ind_write:
+            continue
+        red = (" reduction(+: " + ", ".join(f"{d}[0:n_{d}]" for d in inc) + ")") if inc else ""
+        head = f"void {fn}("
+        i = src.index(head)
+        j = src.index("  for (i = 0; i < n_iter; i++) {", i)
+        src = src[:j] + f"  #pragma omp parallel for{red}\n" + src[j:]
+    return src, arrays, sizes
+
+
+def compile_lowered_c(doc, outdir, openmp=False):
     """The model's lowering (kernels + drivers, as above) compiled as plain C with gcc -O3: the
     reference's CPU path for a mesh model.  emit_openmp would attach `reduction(+: dcells)` to
     the driver loop, which is not valid OpenMP for an array parameter ([P10]), so
     the C runs serially.  C `int` is 32-bit (the interpreter's values are int64): use inputs
     whose sums stay in range.  Returns a ctypes handle exposing `op2_main`."""
     import ctypes
-    src, arrays, sizes = lower_unit(doc)
-    path = os.path.join(outdir, "model.c")
+    src, arrays, sizes = openmp_lowered_c(doc) if openmp else lower_unit(doc)
+    path = os.path.join(outdir, "model_omp.c" if openmp else "model.c")
     with open(path, "w") as f:
         f.write(src)
-    so = os.path.join(outdir, "model.so")
+    so = os.path.join(outdir, "model_omp.so" if openmp else "model.so")
     subprocess.run(["gcc", "-O3", "-march=x86-64-v3", "-std=gnu11", "-fPIC", "-shared", "-DACCESS(x)=",
-                    "-DDEF(x)=(void)0", "-DUSE(x)=(void)0", "-DMAY_DEF(x)=(void)0", "-o", so, path], check=True)
+                    "-DDEF(x)=(void)0", "-DUSE(x)=(void)0", "-DMAY_DEF(x)=(void)0"] + (["-fopenmp"] if openmp else [])
+                   + ["-o", so, path], check=True)
     lib = ctypes.CDLL(so)
     lib.op2_main.restype = None
     return lib, arrays, sizes
