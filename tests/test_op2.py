@@ -293,3 +293,27 @@ def test_random_model_on_gpu(cuda, name):
     m.run()
     for k, v in case["result"].items():
         assert m.dat(k).tolist() == v, k
+
+
+def test_openmp_array_reduction_cpu_form_matches_serial():
+    """The CPU fix SURVEY §8f.1 names (emit_openmp's `reduction(+: dcells)` on an array parameter is
+    not valid OpenMP): each driver loop as `parallel for reduction(+: d[0:n_d])` — bit-identical to
+    the serial lowered C on a random mesh."""
+    import ctypes
+    import sys
+    import tempfile
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import op2_probe
+    from oracle import op2_ref
+    doc = op2_probe.mesh_doc(1 << 12, 1 << 13)
+    src, _, _ = op2_ref.openmp_lowered_c(doc)
+    assert "#pragma omp parallel for reduction(+: dcells[0:n_dcells])" in src
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for omp in (False, True):
+            lib, arrays, sizes = op2_ref.compile_lowered_c(doc, td, openmp=omp)
+            content = {d["name"]: np.asarray(d["data"], np.int32) for d in doc["dats"]}
+            content.update({m["name"]: np.asarray(m["table"], np.int32) for m in doc["maps"]})
+            lib.op2_main(*([ctypes.c_int(n) for n in sizes] + [ctypes.c_void_p(content[a].ctypes.data) for a in arrays]))
+            outs.append(content["dcells"].copy())
+    assert np.array_equal(outs[0], outs[1])
