@@ -681,8 +681,18 @@ def op2_line(args, torch, pb, k, w):
     with torch.cuda.stream(st):
         ms = statistics.mean(run_steps(torch, lambda: m.run_loop_async(0), k, w, lambda: pb.device.l2_flush()))
     m.sync()
-    res = {"ms": ms, "Gedges/s": ne / ms / 1e6, "GB/s": (ne * 32 + nc * 16) / ms / 1e6,
-           "schedule": m.loop_info(0)[0], "data": "random edge->cell map (arity 2), int64 dats"}
+    hbm, _, _ = peaks()
+    # algorithmic bytes: the edge stream (2 map entries + one int64 edge value: 16 B per edge) and
+    # the cell dat read and written once (16 B per cell); the increments themselves are L2 atomics
+    # on the L2-resident 32 MB cell dat, which is what bounds the loop
+    algo = ne * 16 + nc * 16
+    res = {"ms": ms, "Gedges/s": ne / ms / 1e6, "GB/s": algo / ms / 1e6,
+           "schedule": m.loop_info(0)[0], "data": "random edge->cell map (arity 2), int64 dats",
+           "roofline": roofline(algo / ms / 1e6, hbm, "GB/s", "op2_loop_0", algo,
+                                note="bound by L2 atomic throughput (2 x 8-byte atomic adds per edge into "
+                                     "the L2-resident cell dat: %.0f G atomics/s), not by HBM" % (2 * ne / ms / 1e6)),
+           "e2e": {"unavailable": "the OP2 door takes the model as a JSON document (pencil_op2_load): its "
+                                  "parsing, not the transfer, would dominate a host-to-host time"}}
     if not args.no_cpu_baseline:
         # CPU beside it: the model's lowering compiled as C (serial: the emitted reduction on an array
         # parameter is not valid OpenMP), one par_loop over the same mesh
