@@ -125,3 +125,22 @@ def test_gemm_tile_grid_on_views(cuda):
     A2, B2 = A.reshape(m, k).astype(np.float64), B.reshape(k, n).astype(np.float64)
     assert normwise_err(C.cpu().numpy().reshape(m, n), A2 @ B2, np.abs(A2) @ np.abs(B2)) <= TOL
     assert torch.equal(C, whole)
+
+
+def test_gemm_beta_zero_reads_c_as_written(cuda):
+    """the fixture computes alpha * s + beta * C[i*n+j] as written: with beta = 0 a NaN or an
+    infinity in C still gives NaN (0 * NaN, 0 * Inf), finite entries give alpha * s"""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    m, n, k = 300, 260, 40
+    A, B, C = synth.f32(m * k, 1), synth.f32(k * n, 2), synth.f32(m * n, 3)
+    C[[0, 7, 300 * 5 + 3]] = [np.nan, np.inf, -np.inf]
+    Cd = torch.from_numpy(C.copy()).cuda()
+    pb.device.gemm(m, n, k, 1.0, 0.0, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), Cd)
+    got = Cd.cpu().numpy()
+    bad = np.zeros(m * n, bool)
+    bad[[0, 7, 300 * 5 + 3]] = True
+    assert np.isnan(got[bad]).all() and np.isfinite(got[~bad]).all()
+    ref = (A.reshape(m, k).astype(np.float64) @ B.reshape(k, n)).reshape(-1)
+    scale = (np.abs(A.reshape(m, k)).astype(np.float64) @ np.abs(B.reshape(k, n))).reshape(-1)
+    assert np.max(np.abs(got[~bad] - ref[~bad]) / scale[~bad]) <= TOL
