@@ -741,9 +741,84 @@ void conv5x5_f32(int h, int w, float* img, float* k, float* out) {
     });
 }
 
+// Drop-in gemm on host arrays, pipelined by row blocks of A / C: B first (every tile needs all of
+// it), then per block its rows of A and C on the copy stream, the block's gemm (strided views:
+// A + r0*k, C + r0*n) on the compute stream as soon as they have landed, and its C rows back on
+// the D2H stream — so the upload of block b+1 and the download of block b-1 run under block b's
+// tensor work, instead of upload, compute and download one after another.  Pageable arrays go
+// through the staging ring (their C comes back in one staged copy at the end).
+#define GEMM_PIPE_BLOCKS 8
+int gemm_pipelined(int m, int n, int k, float alpha, float beta, const float* A, const float* B, float* C) {
+    DeviceCtx* c = nullptr;
+    int r = get_ctx(&c);
+    if (r) return r;
+    std::lock_guard<std::mutex> lk(c->mu);
+    PipeCtx* pc = nullptr;
+    if ((r = get_pipe(c, &pc))) return r;
+    cudaStream_t s0 = c->stream, s1 = pc->comp, s2 = pc->d2h;
+    float *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    void* ws = nullptr;
+    size_t wb = 0;
+    struct Release {
+        std::function<void()> f;
+        ~Release() { f(); }
+    } release{[&]() {
+        cudaStreamSynchronize(s1);
+        cudaStreamSynchronize(s2);
+        pool_free(s0, dA);
+        pool_free(s0, dB);
+        pool_free(s0, dC);
+        pool_free(s0, ws);
+        cudaStreamSynchronize(s0);
+    }};
+    const size_t na = (size_t)m * k, nb = (size_t)k * n, ncm = (size_t)m * n;
+    if ((r = pool_alloc(c, s0, sizeof(float) * nz(na), (void**)&dA)) ||
+        (r = pool_alloc(c, s0, sizeof(float) * nz(nb), (void**)&dB)) ||
+        (r = pool_alloc(c, s0, sizeof(float) * ncm, (void**)&dC)))
+        return r;
+    auto up = [&](void* d, const void* h, size_t bytes) -> cudaError_t {
+        return staged(h, bytes) ? (cudaError_t)staged_h2d_2d(c->device, d, bytes, h, bytes, bytes, 1, s0)
+                                : cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s0);
+    };
+    g_h2d = (long long)sizeof(float) * (long long)(na + nb + ncm);
+    g_d2h = (long long)sizeof(float) * (long long)ncm;
+    if (nb) CK(up(dB, B, sizeof(float) * nb));
+    const bool c_staged = staged(C, sizeof(float) * ncm);
+    // row blocks of a multiple of 256 rows (one CTA-pair tile)
+    const int rows = ((m + GEMM_PIPE_BLOCKS - 1) / GEMM_PIPE_BLOCKS + 255) / 256 * 256;
+    wb = gemm_workspace_bytes(rows, n, k, dA, k, dB, n);  // 0: the device copies are 16-byte pitched or packed per block
+    if (wb && (r = pool_alloc(c, s1, wb, &ws))) return r;
+    int b = 0;
+    for (int r0 = 0; r0 < m; r0 += rows, b++) {
+        const int mr = std::min(rows, m - r0);
+        if (k) CK(up(dA + (size_t)r0 * k, A + (size_t)r0 * k, sizeof(float) * (size_t)mr * k));
+        CK(up(dC + (size_t)r0 * n, C + (size_t)r0 * n, sizeof(float) * (size_t)mr * n));
+        CK(cudaEventRecord(pc->ev_chunk[b], s0));
+        CK(cudaStreamWaitEvent(s1, pc->ev_chunk[b], 0));
+        const int e = launch_gemm(s1, mr, n, k, alpha, beta, dA + (size_t)r0 * k, k, dB, n, dC + (size_t)r0 * n, n, ws,
+                                  wb);
+        if (e) return cuda_fail((cudaError_t)e, "gemm launch");
+        if (c_staged) continue;
+        CK(cudaEventRecord(pc->ev_blk[b], s1));
+        CK(cudaStreamWaitEvent(s2, pc->ev_blk[b], 0));
+        CK(cudaMemcpyAsync(C + (size_t)r0 * n, dC + (size_t)r0 * n, sizeof(float) * (size_t)mr * n,
+                           cudaMemcpyDeviceToHost, s2));
+    }
+    if (c_staged) CK((cudaError_t)staged_d2h_2d(c->device, C, sizeof(float) * ncm, dC, sizeof(float) * ncm,
+                                                 sizeof(float) * ncm, 1, s1));
+    release.f();
+    release.f = [] {};
+    return collect_faults(c, s0) == PENCIL_OK ? ok() : g_status;
+}
+
 void gemm(int m, int n, int k, float alpha, float beta, float* A, float* B, float* C) {
     if (m < 0 || n < 0 || k < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
     if (m == 0 || n == 0) { ok(); return; }
+    if ((long long)m * n >= (1ll << 22) && m >= 1024 && A && B && C && !is_device_ptr(A) && !is_device_ptr(B) &&
+        !is_device_ptr(C)) {
+        gemm_pipelined(m, n, k, alpha, beta, A, B, C);
+        return;
+    }
     Stage st[3];
     st[0] = {A, nullptr, sizeof(float) * nz((long long)m * k), IN};
     st[1] = {B, nullptr, sizeof(float) * nz((long long)k * n), IN};

@@ -144,3 +144,23 @@ def test_gemm_beta_zero_reads_c_as_written(cuda):
     ref = (A.reshape(m, k).astype(np.float64) @ B.reshape(k, n)).reshape(-1)
     scale = (np.abs(A.reshape(m, k)).astype(np.float64) @ np.abs(B.reshape(k, n))).reshape(-1)
     assert np.max(np.abs(got[~bad] - ref[~bad]) / scale[~bad]) <= TOL
+
+
+@pytest.mark.parametrize("shape", [(2100, 2000, 300), (1500, 2803, 97)])
+def test_gemm_dropin_host_arrays_pipelined(cuda, shape):
+    """the drop-in gemm on host arrays (pipelined by row blocks: B, then each block's A / C rows,
+    its gemm on strided views, its C rows back) equals the device call bit for bit — pageable
+    (numpy) and pinned arrays, pitches that are and are not 16-byte multiples"""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    m, n, k = shape
+    A, B, C = synth.f32(m * k, 21), synth.f32(k * n, 22), synth.f32(m * n, 23)
+    Cd = torch.from_numpy(C.copy()).cuda()
+    pb.device.gemm(m, n, k, 0.75, -0.5, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), Cd)
+    ref = Cd.cpu().numpy()
+    c_pg = C.copy()
+    pb.dropin.gemm(m, n, k, 0.75, -0.5, A, B, c_pg)
+    assert np.array_equal(c_pg.view(np.uint32), ref.view(np.uint32))
+    c_pin = torch.from_numpy(C.copy()).pin_memory()
+    pb.dropin.gemm(m, n, k, 0.75, -0.5, torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory(), c_pin)
+    assert np.array_equal(c_pin.numpy().view(np.uint32), ref.view(np.uint32))
