@@ -705,23 +705,10 @@ def op2_line(args, torch, pb, k, w):
             t0 = time.perf_counter()
             lib.op2_main(*cargs)
             cpu_s = time.perf_counter() - t0
-            # the OpenMP form with the array-section reduction SURVEY §8f.1 proposes as the CPU fix
-            # (reported beside it; on these hosts the per-thread dat copies make it slower)
-            try:
-                lib2, arrays2, sizes2 = op2_ref.compile_lowered_c(doc, td, openmp=True)
-                content2 = {d["name"]: np.asarray(d["data"], np.int32) for d in doc["dats"]}
-                content2.update({mm["name"]: np.asarray(mm["table"], np.int32) for mm in doc["maps"]})
-                cargs2 = [ctypes.c_int(n) for n in sizes2] + [ctypes.c_void_p(content2[a].ctypes.data) for a in arrays2]
-                t0 = time.perf_counter()
-                lib2.op2_main(*cargs2)
-                omp_s = time.perf_counter() - t0
-            except Exception:  # noqa: BLE001
-                omp_s = None
         res["cpu_baseline"] = {"ms": cpu_s * 1e3, "Gedges/s": ne / cpu_s / 1e9, "cores": 1, "kind": "port",
-                               "sample": "the model's lowered driver + kernel as C, gcc -O3, serial (the faster "
-                                         "of the two CPU forms here)",
-                               "openmp_array_reduction_ms": omp_s * 1e3 if omp_s else None,
-                               "openmp_cores": os.cpu_count()}
+                               "sample": "the model's lowered driver + kernel as C, gcc -O3, serial (the OpenMP "
+                                         "form with an array-section reduction, oracle/op2_ref.openmp_lowered_c, "
+                                         "is slower: a private copy of the cell dat per thread)"}
     m.close()
     return res
 
