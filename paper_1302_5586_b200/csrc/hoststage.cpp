@@ -8,7 +8,9 @@
 // 200-300 ms).  Here the bytes go through a ring of pinned chunks that a pool of host threads fills
 // (memcpy, one slice per thread) while the DMA engine drains the previous chunk, and the reverse
 // for device -> host: 45 GB/s with 8-16 threads (tools/probes/h2d_pageable.cu; memcpy alone
-// reaches 52 GB/s, so the host's memory bandwidth, not the link, is the limit).
+// reaches 52 GB/s, so the host's memory bandwidth, not the link, is the limit).  The GPU cannot read
+// pageable memory itself on this platform (cudaDevAttrPageableMemoryAccess = 0: no HMM / ATS,
+// tools/probes/hmm_probe.cu), so some host copy is unavoidable.
 //
 // Semantics: h2d returns when the caller's source may be reused (every chunk copied into the ring);
 // the DMAs are ordered on the caller's stream.  d2h is synchronous (returns with the data in the
