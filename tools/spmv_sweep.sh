@@ -1,6 +1,9 @@
-mkdir -p gpurun_out
-CMD="python bench.py --steps 10 --warmup 3 --no-suite --no-e2e --no-cpu-baseline"
-for W in 64 128 256; do for T in 256 512 1024 2048; do
-  echo "W=$W T=$T $(PENCIL_SPMV_WCHUNK=$W PENCIL_SPMV_TILE=$T $CMD | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"],4), round(d["value"],1))')" >> gpurun_out/sweep.txt
-done; done
-echo done
+# Sweep the segmented executor's compile-time shape (tile non-zeros x non-zeros per lane x CTAs per
+# SM) for both SpMV modes: each point is a variant build (tools/variant_build.sh), timed with
+# tools/ab_spmv_modes.sh on one box.  Round-1 form of this sweep used run-time knobs; the shipped
+# library has none.
+#   bash tools/spmv_sweep.sh          (builds variants/*, then: gpurun -- 'bash tools/ab_spmv_modes.sh base t2048 ...')
+set -e
+for T in 2048 4096 8192; do bash tools/variant_build.sh t$T -DSEG_TILE_NNZ=$T > /dev/null; echo "variants/t$T"; done
+for C in 4 5 6; do bash tools/variant_build.sh c$C -DSEG_CTAS_PER_SM=$C > /dev/null; echo "variants/c$C"; done
+for E in 4 8; do bash tools/variant_build.sh oe$E -DSEG_E_ORD=$E > /dev/null; echo "variants/oe$E"; done
