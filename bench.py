@@ -521,22 +521,12 @@ def suite(args, torch, pb, hbm):
                                        k, w, flush))
         out[name] = bw_line(ms, b, hbm, kern, taps=desc, **{"Gpix/s": npx / ms / 1e6})
         if not no_e2e:
-            # packed bytes have no emitted-C door (PENCIL has no uint8): device API + the caller's copies
+            # packed bytes have no emitted-C door (PENCIL has no uint8): the library's host-array entry
             def mk_b(pinned, taps=taps, scale=scale):
-                i_ = host_buf(torch, himg8, pinned) if pinned else torch.from_numpy(himg8)
-                o_ = torch.empty(npx, dtype=torch.uint8).pin_memory() if pinned else torch.empty(npx, dtype=torch.uint8)
-                di, do = torch.empty(npx, dtype=torch.uint8, device="cuda"), torch.empty(npx, dtype=torch.uint8,
-                                                                                        device="cuda")
-
-                def call():
-                    di.copy_(i_, non_blocking=pinned)
-                    pb.device.conv5x5_u8_bytes(h, w_, scale, di, taps, do)
-                    o_.copy_(do, non_blocking=pinned)
-                    torch.cuda.synchronize()
-                    return npx, npx
-                return call
+                i_, o_ = host_buf(torch, himg8, pinned), host_buf(torch, np.zeros(npx, np.uint8), pinned)
+                return lambda: pb.dropin.conv5x5_u8_bytes(h, w_, scale, i_, taps, o_)
             out[name]["e2e"] = e2e_calls(torch, pb, mk_b, b, "GB/s",
-                                         "pencil_conv5x5_u8_bytes_dev + the caller's H2D / D2H copies")
+                                         "pencil_conv5x5_u8_bytes (host arrays, library staging)")
     del img8, out8, himg8
     himgf = synth.f32(npx)
     imgf = dev(himgf)

@@ -87,6 +87,9 @@ int pencil_conv5x5_u8_dev(pencil_stream_t s, int h, int w, int scale, const int*
 /* packed 8-bit image variant (1 byte per pixel, same arithmetic as conv5x5_u8) */
 int pencil_conv5x5_u8_bytes_dev(pencil_stream_t s, int h, int w, int scale, const uint8_t* img,
                                 const int* k_host, uint8_t* out);
+/* the packed 8-bit stencil on host arrays (copied in / out like the §1 calls; pageable arrays of
+ * 4 MB and more through the library's staging ring) or device arrays (used in place) */
+int pencil_conv5x5_u8_bytes(int h, int w, int scale, const uint8_t* img, const int* k, uint8_t* out);
 int pencil_conv5x5_f32_dev(pencil_stream_t s, int h, int w, const float* img, const float* k_host,
                            float* out);
 /* Band-sharded 5x5 stencils (multi-GPU row bands; the halo exchange is fused into the sweep):

@@ -42,6 +42,7 @@ SIGNATURES = {
     "pencil_axpy_dev_ptr": (c_int, [P, c_ll, P, P, P]),
     "pencil_conv5x5_u8_dev": (c_int, [P, c_int, c_int, c_int, P, P, P]),
     "pencil_conv5x5_u8_bytes_dev": (c_int, [P, c_int, c_int, c_int, P, P, P]),
+    "pencil_conv5x5_u8_bytes": (c_int, [c_int, c_int, c_int, P, P, P]),
     "pencil_conv5x5_f32_dev": (c_int, [P, c_int, c_int, P, P, P]),
     "pencil_conv5x5_u8_band_dev": (c_int, [P, c_int, c_int, c_int, P, P, P, P, P]),
     "pencil_conv5x5_f32_band_dev": (c_int, [P, c_int, c_int, c_int, c_int, P, P, P, P, P]),

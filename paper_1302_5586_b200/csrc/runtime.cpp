@@ -716,6 +716,30 @@ void conv5x5_u8(int h, int w, int scale, int* img, int* k, int* out) {
     });
 }
 
+// packed 8-bit images (an extension: PENCIL has no uint8, so there is no emitted-C door): the same
+// drop-in staging as the int32-storage call — host arrays copied in / out (pageable ones through the
+// staging ring), device arrays used in place
+extern "C" int pencil_conv5x5_u8_bytes(int h, int w, int scale, const uint8_t* img, const int* k, uint8_t* out) {
+    if (h < 0 || w < 0) return fail(PENCIL_E_ARG, "negative extent");
+    if (h == 0 || w == 0) return ok();
+    if (scale == 0) return fail(PENCIL_E_INTERP, "division by zero");
+    if (!k) return fail(PENCIL_E_ARG, "null taps");
+    int taps[25];
+    if (is_device_ptr(k)) {
+        if (cudaMemcpy(taps, k, sizeof taps, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return cuda_fail(cudaGetLastError(), "tap copy");
+    } else {
+        memcpy(taps, k, sizeof taps);
+    }
+    Stage st[2];
+    st[0] = {(void*)img, nullptr, nz((long long)h * w), IN};
+    st[1] = {out, nullptr, nz((long long)h * w), OUT};
+    return dropin(st, [&](DeviceCtx*, cudaStream_t s) {
+        return launch_conv5x5_u8_bytes(s, h, w, scale, (const unsigned char*)st[0].dev, taps,
+                                       (unsigned char*)st[1].dev);
+    });
+}
+
 void conv5x5_f32(int h, int w, float* img, float* k, float* out) {
     if (h < 0 || w < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
     if (h < 5 || w < 5) { ok(); return; }  // no interior pixel: nothing is stored

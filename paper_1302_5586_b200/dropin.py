@@ -68,3 +68,17 @@ def conv5x5_f32(h, w, img, k, out):
 
 def gemm(m, n, k, alpha, beta, A, B, C):
     _call("gemm", m, n, k, alpha, beta, A, B, C)
+
+
+def conv5x5_u8_bytes(h, w, scale, img, k, out):
+    """The packed 8-bit stencil (an extension of the PENCIL ABI: uint8 arrays) on host numpy
+    arrays / torch tensors — pencil_conv5x5_u8_bytes."""
+    if hasattr(k, "data_ptr"):  # a torch tensor (host or device)
+        ok = k.numel() == 25 and str(k.dtype) == "torch.int32" and k.is_contiguous()
+        kk = k
+    else:
+        kk = np.ascontiguousarray(np.asarray(k, dtype=np.int32).reshape(-1))
+        ok = kk.size == 25
+    if not ok:
+        raise ValueError("a 5x5 stencil needs 25 contiguous int32 taps")
+    _call("pencil_conv5x5_u8_bytes", h, w, scale, img, kk, out)

@@ -86,3 +86,47 @@ def test_concurrent_pageable_calls(cuda):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("taps,scale", [("BINOMIAL", 256), ("SHARPEN", 1)])
+def test_conv_u8_bytes_host_entry(cuda, taps, scale):
+    """pencil_conv5x5_u8_bytes on pageable numpy (staging ring: 8.4 MB), pinned and device arrays:
+    bit-identical to the device API and to the oracle"""
+    import oracle
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    k = getattr(synth, taps)
+    h, w = 2051, 4100
+    img = synth.u8_i32(h * w, seed=31)
+    img8 = img.astype(np.uint8)
+    dev_out = torch.empty(h * w, dtype=torch.uint8, device="cuda")
+    pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img8).cuda(), k, dev_out)
+    ref = dev_out.cpu().numpy()
+    out_pg = np.zeros(h * w, np.uint8)
+    pb.dropin.conv5x5_u8_bytes(h, w, scale, img8, k, out_pg)
+    assert np.array_equal(out_pg, ref)
+    out_pin = torch.zeros(h * w, dtype=torch.uint8).pin_memory()
+    pb.dropin.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img8).pin_memory(), k, out_pin)
+    assert np.array_equal(out_pin.numpy(), ref)
+    out_d = torch.zeros(h * w, dtype=torch.uint8, device="cuda")
+    pb.dropin.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img8).cuda(), torch.from_numpy(
+        np.ascontiguousarray(k, np.int32).reshape(-1)).cuda(), out_d)
+    assert np.array_equal(out_d.cpu().numpy(), ref)
+    # small case against the oracle (also below the staging threshold: the driver's copy)
+    hs, ws = 37, 103
+    imgs = synth.u8_i32(hs * ws, seed=5)
+    o = np.zeros(hs * ws, np.uint8)
+    pb.dropin.conv5x5_u8_bytes(hs, ws, scale, imgs.astype(np.uint8), k, o)
+    assert np.array_equal(o.astype(np.int64), oracle.conv5x5_u8(hs, ws, scale, imgs, k))
+
+
+def test_conv_u8_bytes_host_entry_errors(cuda):
+    import paper_1302_5586_b200 as pb
+    img = np.zeros(64, np.uint8)
+    with pytest.raises(pb.PencilError) as e:
+        pb.dropin.conv5x5_u8_bytes(8, 8, 0, img, synth.BINOMIAL, np.zeros(64, np.uint8))
+    assert e.value.code == "E-INTERP"
+    with pytest.raises(pb.PencilError) as e:
+        pb.dropin.conv5x5_u8_bytes(-1, 8, 1, img, synth.BINOMIAL, np.zeros(64, np.uint8))
+    assert e.value.code == "E-ARG"
+    pb.dropin.conv5x5_u8_bytes(0, 8, 0, img, synth.BINOMIAL, np.zeros(64, np.uint8))  # empty: no-op
