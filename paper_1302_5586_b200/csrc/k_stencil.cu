@@ -884,15 +884,32 @@ __device__ __forceinline__ void swar_enter(const unsigned char* slot, int w, int
     }
 }
 
+// predicated cp.async (an @p guard on the instruction itself: no branch, no reconvergence)
+template <int BYTES>
+__device__ __forceinline__ void cp_if(bool p, void* dst, const void* src) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+        "@p cp.async.ca.shared.global [%0], [%1], %3;\n\t}" ::"r"(smem_addr(dst)),
+        "l"(src), "r"((int)p), "n"(BYTES)
+        : "memory");
+}
+template <>
+__device__ __forceinline__ void cp_if<16>(bool p, void* dst, const void* src) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+        "@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(smem_addr(dst)),
+        "l"(src), "r"((int)p)
+        : "memory");
+}
+
+// the lane's NP body bytes, and for lanes 0 / 31 of inner strips the 4 halo bytes beyond them
 template <int NP>
 __device__ __forceinline__ void swar_issue(const unsigned char* src, unsigned char* slot, int lane, bool body,
                                            bool halo) {
     unsigned char* dst = slot + SwarGeom<NP>::PAD + NP * lane;
-    if (body) cp_body<NP>(dst, src);
-    if (halo) {
-        if (lane == 0) cp4(dst - 4, src - 4);
-        else cp4(dst + NP, src + NP);
-    }
+    cp_if<NP>(body, dst, src);
+    const int hd = lane == 0 ? -4 : NP;
+    cp_if<4>(halo, dst + hd, src + hd);
 }
 
 template <int NP, int S, bool SH8>
@@ -982,20 +999,27 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int
 
 // ---------------------------------------------------------------- signed 2-D SWAR packed-byte sweep
 // Taps with a non-negative centre and non-positive off-centre taps (sharpen, Laplacian and
-// unsharp-mask shapes — the signed sharpen of the config), power-of-two scale: every off-centre
-// product k x = |k| (255 - x) - 255 |k| runs on the complemented byte, so the sum
-//   acc' = kc x_c + sum |k| (255 - x) = acc + B,   B = 255 * sum |k_off| >= 0
-// is non-negative and, when 255 * (kc + sum |k_off|) + scale / 2 < 65536, fits a 16-bit SWAR
-// lane: one IMAD per tap per two pixels, no int -> float conversion.  Requantisation per lane:
-// (max(acc' + scale/2, B) - B) >> shift, then min 255 (C truncation and the [0, 255] clamp: a
-// negative numerator gives 0 either way).  Rows are pushed: the row entering the window adds its
-// taps to the five output rows it feeds (5 x NP/2 accumulators), and the output row it completes
-// is requantised and stored.  Integer arithmetic throughout: bit-identical to the other kernels.
+// unsharp-mask shapes — the signed sharpen of the config), power-of-two scale.  With
+// B = 255 * sum |k_off| every 16-bit SWAR lane accumulates
+//   acc = scale/2 + B + kc x_c - sum |k| x
+// starting from scale/2 + B: each off-centre product is SUBTRACTED (an IMAD by the two's-complement
+// tap k = -|k|, exact mod 2^32), and because the partial sums of |k| x never exceed B no lane ever
+// borrows from its neighbour; when 255 * (kc + sum |k_off|) + scale / 2 < 65536 the lane never
+// carries either.  One IMAD per tap per two pixels, no complement, no int -> float conversion.
+// Requantisation per lane: (max(acc, B) - B) >> shift, then min 255 (C truncation and the [0, 255]
+// clamp: a negative numerator gives 0 either way).  Rows are pushed: the row entering the window
+// adds its taps to the five output rows it feeds (5 x NP/2 accumulators), and the output row it
+// completes is requantised and stored.  Integer arithmetic throughout: bit-identical to the other
+// kernels.
 // DIA: the 12 corner taps are zero (skipped at compile time).
+// SYM: taps mirror-symmetric in both axes (k[i][j] = k[4-i][j] = k[i][4-j]: sharpen, Laplacian,
+// Gaussian shapes): per pixel pair the entering row forms the horizontal pair sums S1, S2 once,
+// rows 0 / 4 and 1 / 3 share one partial each, so a diamond costs 6 IMADs + 6 adds per pair
+// instead of 13 IMADs (the IMAD pipe runs at half the issue rate).
 struct Swar2dArgs {
     unsigned kc;         // centre tap (>= 0)
-    unsigned kn[25];     // |off-centre taps| (kn[12] unused)
-    unsigned half2;      // scale / 2 in both 16-bit lanes (the accumulators' start: acc' + scale/2)
+    unsigned kn[25];     // off-centre taps as 32-bit two's complement (-|k|; kn[12] unused)
+    unsigned init2;      // scale / 2 + B in both 16-bit lanes (the accumulators' start)
     unsigned bias2;      // B in both lanes
     int shift;           // log2(scale) <= 8
 };
@@ -1011,17 +1035,26 @@ __device__ __forceinline__ unsigned umin16x2(unsigned a, unsigned b) {
     return r;
 }
 
-// The row entering the window as byte pairs: Qc[m] = complemented (e[c-2+m], e[c+m]) in 16-bit
-// lanes (m = 0..NP+1), Qp[t] = the plain centre pairs of output pair t (pixels c+4g+p, +2).
-template <int NP>
+// The row entering the window as byte pairs: Q[m] = (e[c-2+m], e[c+m]) in 16-bit lanes
+// (m = 0..NP+1); output pair t (pixels c+b, c+b+2 with b = (t & 1) + 4 (t >> 1)) has its centre
+// pair at Q[b + 2].  The lane's 16 body bytes are one 128-bit shared load, its two 4-byte
+// neighbours two 32-bit loads.
+template <int NP, bool EDGE>
 __device__ __forceinline__ void swar2d_enter(const unsigned char* slot, int w, int c0, int lane,
-                                             unsigned (&Qc)[NP + 2], unsigned (&Qp)[NP / 2]) {
+                                             unsigned (&Q)[NP + 2]) {
     typedef SwarGeom<NP> G;
-    const unsigned* wp = reinterpret_cast<const unsigned*>(slot + G::PAD - 4 + NP * lane);
+    const unsigned char* body = slot + G::PAD + NP * lane;
     unsigned Wd[G::NW + 2];
-#pragma unroll
-    for (int k = 0; k < G::NW + 2; k++) Wd[k] = wp[k];
-    if (c0 == 0 || c0 + 32 * NP >= w) {  // image-edge strips: clamp-to-edge columns
+    Wd[0] = *reinterpret_cast<const unsigned*>(body - 4);
+    if constexpr (NP == 16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(body);
+        Wd[1] = v.x, Wd[2] = v.y, Wd[3] = v.z, Wd[4] = v.w;
+    } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(body);
+        Wd[1] = v.x, Wd[2] = v.y;
+    }
+    Wd[G::NW + 1] = *reinterpret_cast<const unsigned*>(body + NP);
+    if (EDGE && (c0 == 0 || c0 + 32 * NP >= w)) {  // image-edge strips: clamp-to-edge columns
         const int c = c0 + NP * lane;
         unsigned v[NP + 4];
 #pragma unroll
@@ -1035,12 +1068,8 @@ __device__ __forceinline__ void swar2d_enter(const unsigned char* slot, int w, i
 #pragma unroll
     for (int k = 0; k <= 2 * G::NW; k++) {
         const unsigned X = (k & 1) ? Wd[k / 2 + 1] : __funnelshift_r(Wd[k / 2], Wd[k / 2 + 1], 16);
-        const unsigned lo = __byte_perm(X, 0u, 0x4240), hi = __byte_perm(X, 0u, 0x4341);
-        Qc[2 * k] = lo ^ 0x00ff00ffu;
-        Qc[2 * k + 1] = hi ^ 0x00ff00ffu;
-        // centre pairs: m = b + 2 with b = p + 4g  ->  m = 4g + 2 + p
-        if ((2 * k) % 4 == 2 && (2 * k - 2) / 4 < NP / 4) Qp[2 * ((2 * k - 2) / 4)] = lo;
-        if ((2 * k + 1) % 4 == 3 && (2 * k - 2) / 4 < NP / 4) Qp[2 * ((2 * k - 2) / 4) + 1] = hi;
+        Q[2 * k] = __byte_perm(X, 0u, 0x4240);
+        Q[2 * k + 1] = __byte_perm(X, 0u, 0x4341);
     }
 }
 
@@ -1051,7 +1080,9 @@ __device__ __forceinline__ constexpr bool tap_on(int di, int dj) {
 
 // Row r (slot S = r mod 5 of the rotation) enters: A[(r - di + 2) mod 5] += taps of row di.
 // Then output row r - 2 is complete: requantise, store (when it lies in [i0, i1)), reset.
-template <int NP, int S, bool DIA, bool SH0>
+// EDGE: the warp may own an image-edge strip (clamped columns); STEADY: row r + S_RING is still
+// an input row of the band and output row r - 2 lies in it (the sweep's middle: no row checks).
+template <int NP, int S, bool DIA, bool SH0, bool SYM, bool EDGE, bool STEADY>
 __device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c, int lane, int r_end, bool body,
                                             bool halo, unsigned char (*ring)[SwarGeom<NP>::ROWE],
                                             unsigned (&A)[5][NP / 2], Sweep<unsigned char>& sw,
@@ -1059,32 +1090,49 @@ __device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c,
     cp_wait<S_RING - 1>();
     __syncwarp();
     unsigned char* slot = ring[(r + S_RING) % S_RING];
-    unsigned Qc[NP + 2], Qp[NP / 2];
-    swar2d_enter<NP>(slot, w, c - NP * lane, lane, Qc, Qp);
+    unsigned Q[NP + 2];
+    swar2d_enter<NP, EDGE>(slot, w, c - NP * lane, lane, Q);
     __syncwarp();
-    if (r + S_RING < r_end) swar_issue<NP>(sw.src > sw.src_last ? sw.src_last : sw.src, slot, lane, body, halo);
+    if (STEADY || r + S_RING < r_end)
+        swar_issue<NP>(sw.src > sw.src_last ? sw.src_last : sw.src, slot, lane, body, halo);
     cp_commit();
     sw.src += sw.w;
-#pragma unroll
-    for (int di = 0; di < 5; di++) {
-        const int o = (S - di + 2 + 5) % 5;  // accumulator slot of output row r - di + 2
+    if constexpr (SYM) {
+        constexpr int o0 = (S + 7) % 5, o1 = (S + 6) % 5, o2 = (S + 5) % 5, o3 = (S + 4) % 5, o4 = (S + 3) % 5;
 #pragma unroll
         for (int t = 0; t < NP / 2; t++) {
             const int b = (t & 1) + 4 * (t >> 1);
-            unsigned acc = A[o][t];
+            const unsigned X = Q[b + 2], S1 = Q[b + 1] + Q[b + 3], S2 = Q[b] + Q[b + 4];
+            unsigned H0 = X * a.kn[2], H1 = S1 * a.kn[6] + X * a.kn[7];
+            if (!DIA) H0 += S2 * a.kn[0] + S1 * a.kn[1], H1 += S2 * a.kn[5];
+            A[o0][t] += H0;
+            A[o4][t] += H0;
+            A[o1][t] += H1;
+            A[o3][t] += H1;
+            A[o2][t] += S2 * a.kn[10] + S1 * a.kn[11] + X * a.kc;
+        }
+    } else {
 #pragma unroll
-            for (int dj = 0; dj < 5; dj++) {
-                if (!tap_on<DIA>(di, dj)) continue;
-                if (di == 2 && dj == 2) acc += a.kc * Qp[t];
-                else acc += a.kn[di * 5 + dj] * Qc[b + dj];
+        for (int di = 0; di < 5; di++) {
+            const int o = (S - di + 2 + 5) % 5;  // accumulator slot of output row r - di + 2
+#pragma unroll
+            for (int t = 0; t < NP / 2; t++) {
+                const int b = (t & 1) + 4 * (t >> 1);
+                unsigned acc = A[o][t];
+#pragma unroll
+                for (int dj = 0; dj < 5; dj++) {
+                    if (!tap_on<DIA>(di, dj)) continue;
+                    acc += (di == 2 && dj == 2 ? a.kc : a.kn[di * 5 + dj]) * Q[b + dj];
+                }
+                A[o][t] = acc;
             }
-            A[o][t] = acc;
         }
     }
     // output row r - 2 (slot (S + 3) % 5 = (r - 2) mod 5) is complete
     constexpr int D = (S + 3) % 5;
+    // (requantised unconditionally, stored under a predicate: no branch around the block)
     const int orow = r - 2;
-    if (orow >= i0 && orow < i1 && body) {
+    {
         unsigned q[NP / 2];
 #pragma unroll
         for (int t = 0; t < NP / 2; t++) {
@@ -1095,15 +1143,46 @@ __device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c,
         unsigned rr[NP / 4];
 #pragma unroll
         for (int g = 0; g < NP / 4; g++) rr[g] = __byte_perm(q[2 * g], q[2 * g + 1], 0x6240);
+        const bool st = (STEADY || (orow >= i0 && orow < i1)) && body;
         unsigned char* dst = sw.dst + (long long)(orow - i0) * w;
-        if constexpr (NP == 16) *reinterpret_cast<uint4*>(dst) = make_uint4(rr[0], rr[1], rr[2], rr[3]);
-        else *reinterpret_cast<uint2*>(dst) = make_uint2(rr[0], rr[1]);
+        if constexpr (NP == 16)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t@p st.global.v4.b32 [%1], {%2, %3, %4, %5};\n\t}"
+                         ::"r"((int)st), "l"(dst), "r"(rr[0]), "r"(rr[1]), "r"(rr[2]), "r"(rr[3]) : "memory");
+        else
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t@p st.global.v2.b32 [%1], {%2, %3};\n\t}"
+                         ::"r"((int)st), "l"(dst), "r"(rr[0]), "r"(rr[1]) : "memory");
     }
 #pragma unroll
-    for (int t = 0; t < NP / 2; t++) A[D][t] = a.half2;
+    for (int t = 0; t < NP / 2; t++) A[D][t] = a.init2;
 }
 
-template <int NP, bool DIA, bool SH0 = false>
+// Rows r0, r0 + 5, ... while r < r_stop (and r < r_end), five steps per iteration; returns the
+// first row not run.  STEADY callers pass r_stop so that every row of their iterations is
+// in the band's middle.
+template <int NP, bool DIA, bool SH0, bool SYM, bool EDGE, bool STEADY>
+__device__ __forceinline__ int swar2d_rows(int r, int r_stop, int w, int i0, int i1, int c, int lane, int r_begin,
+                                           int r_end, bool body, bool halo,
+                                           unsigned char (*ring)[SwarGeom<NP>::ROWE], unsigned (&A)[5][NP / 2],
+                                           Sweep<unsigned char>& sw, const Swar2dArgs& a) {
+    for (; r < r_stop && r < r_end; r += 5) {
+        if (STEADY) {
+            swar2d_step<NP, 0, DIA, SH0, SYM, EDGE, true>(w, r + 0, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+            swar2d_step<NP, 1, DIA, SH0, SYM, EDGE, true>(w, r + 1, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+            swar2d_step<NP, 2, DIA, SH0, SYM, EDGE, true>(w, r + 2, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+            swar2d_step<NP, 3, DIA, SH0, SYM, EDGE, true>(w, r + 3, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+            swar2d_step<NP, 4, DIA, SH0, SYM, EDGE, true>(w, r + 4, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+            continue;
+        }
+#define SWAR2D_STEP(k)                                                                                         \
+    if (r + k >= r_begin && r + k < r_end)                                                                     \
+        swar2d_step<NP, k, DIA, SH0, SYM, EDGE, false>(w, r + k, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
+        SWAR2D_STEP(0) SWAR2D_STEP(1) SWAR2D_STEP(2) SWAR2D_STEP(3) SWAR2D_STEP(4)
+#undef SWAR2D_STEP
+    }
+    return r;
+}
+
+template <int NP, bool DIA, bool SH0 = false, bool SYM = false>
 __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_kernel(int h, int w,
                                                                              const unsigned char* __restrict__ img,
                                                                              unsigned char* __restrict__ out,
@@ -1130,22 +1209,20 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_kernel(i
 #pragma unroll
     for (int q = 0; q < 5; q++)
 #pragma unroll
-        for (int t = 0; t < NP / 2; t++) A[q][t] = a.half2;
+        for (int t = 0; t < NP / 2; t++) A[q][t] = a.init2;
     Sweep<unsigned char> sw;
     sw.w = w;
     sw.src_last = img + (long long)(h - 1) * w + c;
     sw.src = img + (long long)(r_begin + S_RING) * w + c;
     sw.dst = out + (long long)i0 * w + c;
     // the rotation slot of row r is r mod 5; start at a multiple of 5 at or below r_begin so the
-    // slots stay compile-time constants (rows before r_begin are skipped)
+    // slots stay compile-time constants (rows before r_begin are skipped).  (A peeled middle
+    // without row checks, and a separate copy for warps away from the image edges, measured
+    // 0.193 / 0.229 ms against 0.156: three copies of the five-step body thrash the instruction
+    // cache.)
     const int rb5 = r_begin - ((r_begin % 5) + 5) % 5;
-    for (int r = rb5; r < r_end; r += 5) {
-        if (r + 0 >= r_begin) swar2d_step<NP, 0, DIA, SH0>(w, r + 0, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
-        if (r + 1 >= r_begin && r + 1 < r_end) swar2d_step<NP, 1, DIA, SH0>(w, r + 1, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
-        if (r + 2 >= r_begin && r + 2 < r_end) swar2d_step<NP, 2, DIA, SH0>(w, r + 2, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
-        if (r + 3 >= r_begin && r + 3 < r_end) swar2d_step<NP, 3, DIA, SH0>(w, r + 3, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
-        if (r + 4 >= r_begin && r + 4 < r_end) swar2d_step<NP, 4, DIA, SH0>(w, r + 4, i0, i1, c, lane, r_end, body, halo, ring, A, sw, a);
-    }
+    swar2d_rows<NP, DIA, SH0, SYM, true, false>(rb5, r_end, w, i0, i1, c, lane, r_begin, r_end, body, halo, ring, A,
+                                                sw, a);
     cp_wait<0>();
 }
 
@@ -1166,11 +1243,19 @@ bool swar2d_args(const int* k, int scale, Swar2dArgs& a) {
     const long long B = 255 * off;
     if (255ll * ((long long)k[12] + off) + (scale >> 1) >= 65536) return false;
     a.kc = (unsigned)k[12];
-    for (int t = 0; t < 25; t++) a.kn[t] = t == 12 ? 0u : (unsigned)(-(long long)k[t]);
-    a.half2 = (unsigned)(scale >> 1) * 0x00010001u;
+    for (int t = 0; t < 25; t++) a.kn[t] = t == 12 ? 0u : (unsigned)k[t];  // k <= 0: -|k| mod 2^32
+    a.init2 = (unsigned)((scale >> 1) + B) * 0x00010001u;
     a.bias2 = (unsigned)B * 0x00010001u;
     a.shift = 0;
     while ((1 << a.shift) != scale) a.shift++;
+    return true;
+}
+
+// taps mirror-symmetric in both axes
+bool mirror_symmetric(const int* k) {
+    for (int i = 0; i < 5; i++)
+        for (int j = 0; j < 5; j++)
+            if (k[i * 5 + j] != k[(4 - i) * 5 + j] || k[i * 5 + j] != k[i * 5 + 4 - j]) return false;
     return true;
 }
 
@@ -1478,7 +1563,14 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
         const bool n16 = w % 16 == 0 && (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0;
         const int np = n16 ? 16 : 8;
         dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
-        if (n16 && dia && s2.shift == 0)
+        const bool sym = mirror_symmetric(k25);
+        if (n16 && sym && dia && s2.shift == 0)
+            stencil_bytes_swar2d_kernel<16, true, true, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+        else if (n16 && sym && dia)
+            stencil_bytes_swar2d_kernel<16, true, false, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+        else if (n16 && sym)
+            stencil_bytes_swar2d_kernel<16, false, false, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+        else if (n16 && dia && s2.shift == 0)
             stencil_bytes_swar2d_kernel<16, true, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
         else if (n16 && dia) stencil_bytes_swar2d_kernel<16, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
         else if (n16) stencil_bytes_swar2d_kernel<16, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);

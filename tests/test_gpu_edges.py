@@ -324,14 +324,20 @@ LAPLACE25 = np.array([[-1, -1, -1, -1, -1], [-1, -1, -1, -1, -1], [-1, -1, 48, -
                       [-1, -1, -1, -1, -1], [-1, -1, -1, -1, -1]], np.int32).reshape(-1)
 LAPLACE13 = np.array([[0, 0, -1, 0, 0], [0, -1, -2, -1, 0], [-1, -2, 16, -2, -1],
                       [0, -1, -2, -1, 0], [0, 0, -1, 0, 0]], np.int32).reshape(-1)
+SYM25 = np.array([[-1, -2, -3, -2, -1], [-2, -4, -6, -4, -2], [-3, -6, 120, -6, -3],  # mirror-symmetric,
+                  [-2, -4, -6, -4, -2], [-1, -2, -3, -2, -1]], np.int32).reshape(-1)  # all 5 tap values
+ASYM13 = np.array([[0, 0, -1, 0, 0], [0, -2, -1, -3, 0], [-1, -3, 20, -2, 0],      # diamond, no mirror
+                   [0, -1, -2, 0, 0], [0, 0, -4, 0, 0]], np.int32).reshape(-1)
+ASYM25 = np.array([[-1, 0, -2, 0, -3], [0, -1, -1, -5, 0], [-2, -1, 30, -1, -1],   # full support, no mirror
+                   [-1, 0, 0, -2, 0], [0, -1, -1, 0, -4]], np.int32).reshape(-1)
 
 
 @pytest.mark.parametrize("h,w", [(70, 256), (33, 520), (64, 264), (9, 8), (5, 512), (130, 1024), (40, 1040),
                                  (12, 16), (21, 1552), (3, 64), (1, 32), (2, 24)])
 def test_conv_u8_bytes_signed_swar_bit_exact(cuda, h, w):
     """Centre-positive, off-centre non-positive taps (sharpen, Laplacians) with a power-of-two
-    scale take the signed SWAR kernel (complemented bytes, biased 16-bit sums, per-lane clamp):
-    diamond and full 5x5 supports, scales 1 .. 256, saturated rows, images shorter than the
+    scale take the signed SWAR kernel (biased 16-bit sums, per-lane clamp): diamond and full 5x5
+    supports, mirror-symmetric (the shared-partial form) and not, scales 1 .. 256, saturated rows, images shorter than the
     window, strips at both edges and narrower than a warp — bit-exact against the oracle; taps
     outside that shape (a positive off-centre tap, a negative centre, sums >= 2^16) take the other
     kernels, also exact."""
@@ -344,7 +350,8 @@ def test_conv_u8_bytes_signed_swar_bit_exact(cuda, h, w):
     mixed[0] = 1  # a positive corner tap: not the signed SWAR shape
     for k, scale in ((synth.SHARPEN, 1), (synth.SHARPEN, 2), (LAPLACE13, 1), (LAPLACE13, 4), (LAPLACE25, 1),
                      (LAPLACE25, 16), (synth.SHARPEN * 7, 256), (LAPLACE25 * 10, 8), (mixed, 1),
-                     (-synth.SHARPEN, 1), (synth.SHARPEN, 3)):
+                     (-synth.SHARPEN, 1), (synth.SHARPEN, 3), (SYM25, 1), (SYM25, 64), (ASYM13, 1),
+                     (ASYM13, 8), (ASYM25, 2), (ASYM25, 1)):
         out8 = torch.empty(h * w, dtype=torch.uint8, device="cuda")
         pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img.astype(np.uint8)).cuda(), k, out8)
         ref = oracle.conv5x5_u8(h, w, scale, img, k)
