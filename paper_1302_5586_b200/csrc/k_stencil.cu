@@ -846,17 +846,26 @@ __device__ __forceinline__ void cp_body(void* dst, const void* src) {
     else cp8(dst, src);
 }
 
-// Row entering the window, filtered horizontally: H[t] = u16x2 pixel pairs; t = 2g + p holds
-// (c + 4g + p, c + 4g + p + 2).  Q[m] = (e[c-2+m], e[c+m]), m = 0..NP+1.
-template <int NP>
-__device__ __forceinline__ void swar_enter(const unsigned char* slot, int w, int c0, int lane, const SwarArgs& a,
-                                           unsigned (&H)[NP / 2]) {
+// The row entering the window as byte pairs: Q[m] = (e[c-2+m], e[c+m]) in 16-bit lanes
+// (m = 0..NP+1); output pair t (pixels c+b, c+b+2 with b = (t & 1) + 4 (t >> 1)) has its centre
+// pair at Q[b + 2].  The lane's 16 body bytes are one 128-bit shared load, its two 4-byte
+// neighbours two 32-bit loads.
+template <int NP, bool EDGE>
+__device__ __forceinline__ void swar_pairs(const unsigned char* slot, int w, int c0, int lane,
+                                             unsigned (&Q)[NP + 2]) {
     typedef SwarGeom<NP> G;
-    const unsigned* wp = reinterpret_cast<const unsigned*>(slot + G::PAD - 4 + NP * lane);
-    unsigned Wd[G::NW + 2];  // columns c-4.. | c.. | ... | c+NP..
-#pragma unroll
-    for (int k = 0; k < G::NW + 2; k++) Wd[k] = wp[k];
-    if (c0 == 0 || c0 + 32 * NP >= w) {  // image-edge strips: clamp-to-edge columns
+    const unsigned char* body = slot + G::PAD + NP * lane;
+    unsigned Wd[G::NW + 2];
+    Wd[0] = *reinterpret_cast<const unsigned*>(body - 4);
+    if constexpr (NP == 16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(body);
+        Wd[1] = v.x, Wd[2] = v.y, Wd[3] = v.z, Wd[4] = v.w;
+    } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(body);
+        Wd[1] = v.x, Wd[2] = v.y;
+    }
+    Wd[G::NW + 1] = *reinterpret_cast<const unsigned*>(body + NP);
+    if (EDGE && (c0 == 0 || c0 + 32 * NP >= w)) {  // image-edge strips: clamp-to-edge columns
         const int c = c0 + NP * lane;
         unsigned v[NP + 4];
 #pragma unroll
@@ -867,20 +876,45 @@ __device__ __forceinline__ void swar_enter(const unsigned char* slot, int w, int
             Wd[k + 1] = v[4 * k + 2] | (v[4 * k + 3] << 8) | (v[4 * k + 4] << 16) | (v[4 * k + 5] << 24);
         Wd[G::NW + 1] = v[NP + 2] | (v[NP + 3] << 8);
     }
-    unsigned Q[NP + 2];
 #pragma unroll
     for (int k = 0; k <= 2 * G::NW; k++) {
         const unsigned X = (k & 1) ? Wd[k / 2 + 1] : __funnelshift_r(Wd[k / 2], Wd[k / 2 + 1], 16);
-        Q[2 * k] = __byte_perm(X, 0u, 0x4240);      // bytes 0, 2 -> 16-bit lanes
-        Q[2 * k + 1] = __byte_perm(X, 0u, 0x4341);  // bytes 1, 3
+        Q[2 * k] = __byte_perm(X, 0u, 0x4240);
+        Q[2 * k + 1] = __byte_perm(X, 0u, 0x4341);
     }
+}
+
+// predicated 8- / 16-byte row store (no branch around it)
+template <int NP>
+__device__ __forceinline__ void swar_store_if(bool p, unsigned char* dst, const unsigned (&r)[NP / 4]) {
+    if constexpr (NP == 16)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t@p st.global.v4.b32 [%1], {%2, %3, %4, %5};\n\t}"
+                     ::"r"((int)p), "l"(dst), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+    else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t@p st.global.v2.b32 [%1], {%2, %3};\n\t}"
+                     ::"r"((int)p), "l"(dst), "r"(r[0]), "r"(r[1]) : "memory");
+}
+
+// Row entering the window, filtered horizontally: H[t] = u16x2 pixel pairs; t = 2g + p holds
+// (c + 4g + p, c + 4g + p + 2).  SYM (v mirror-symmetric): v0 (Q[b] + Q[b+4]) + v1 (Q[b+1] + Q[b+3])
+// + v2 Q[b+2], 3 IMADs + 2 adds instead of 5 IMADs (exact: the word arithmetic is linear mod 2^32
+// and every final lane lies in [0, 2^16)).
+template <int NP, bool SYM>
+__device__ __forceinline__ void swar_enter(const unsigned char* slot, int w, int c0, int lane, const SwarArgs& a,
+                                           unsigned (&H)[NP / 2]) {
+    unsigned Q[NP + 2];
+    swar_pairs<NP, true>(slot, w, c0, lane, Q);
 #pragma unroll
     for (int t = 0; t < NP / 2; t++) {
         const int b = (t & 1) + 4 * (t >> 1);
-        unsigned acc = a.v[0] * Q[b];
+        if (SYM) {
+            H[t] = a.v[0] * (Q[b] + Q[b + 4]) + a.v[1] * (Q[b + 1] + Q[b + 3]) + a.v[2] * Q[b + 2];
+        } else {
+            unsigned acc = a.v[0] * Q[b];
 #pragma unroll
-        for (int dj = 1; dj < 5; dj++) acc += a.v[dj] * Q[b + dj];
-        H[t] = acc;
+            for (int dj = 1; dj < 5; dj++) acc += a.v[dj] * Q[b + dj];
+            H[t] = acc;
+        }
     }
 }
 
@@ -912,14 +946,14 @@ __device__ __forceinline__ void swar_issue(const unsigned char* src, unsigned ch
     cp_if<4>(halo, dst + hd, src + hd);
 }
 
-template <int NP, int S, bool SH8>
+template <int NP, int S, bool SH8, bool SYM>
 __device__ __forceinline__ void swar_step(int w, int i, int c, int lane, int r_end, bool body, bool halo,
                                           unsigned char (*ring)[SwarGeom<NP>::ROWE], unsigned (&H)[5][NP / 2],
                                           Sweep<unsigned char>& sw, const SwarArgs& a) {
     cp_wait<S_RING - 1>();
     __syncwarp();
     unsigned char* slot = ring[(i + 2) % S_RING];
-    swar_enter<NP>(slot, w, c - NP * lane, lane, a, H[S]);
+    swar_enter<NP, SYM>(slot, w, c - NP * lane, lane, a, H[S]);
     __syncwarp();
     if (i + 2 + S_RING < r_end) swar_issue<NP>(sw.src > sw.src_last ? sw.src_last : sw.src, slot, lane, body, halo);
     cp_commit();
@@ -927,10 +961,15 @@ __device__ __forceinline__ void swar_step(int w, int i, int c, int lane, int r_e
     unsigned o[NP / 2];
 #pragma unroll
     for (int t = 0; t < NP / 2; t++) {
-        unsigned acc = a.half2;
+        if (SYM) {  // u mirror-symmetric: rows i-2 / i+2 and i-1 / i+1 share a tap
+            o[t] = a.half2 + a.u[0] * (H[(S + 1) % 5][t] + H[(S + 5) % 5][t]) +
+                   a.u[1] * (H[(S + 2) % 5][t] + H[(S + 4) % 5][t]) + a.u[2] * H[(S + 3) % 5][t];
+        } else {
+            unsigned acc = a.half2;
 #pragma unroll
-        for (int di = 0; di < 5; di++) acc += a.u[di] * H[(S + 1 + di) % 5][t];
-        o[t] = acc;
+            for (int di = 0; di < 5; di++) acc += a.u[di] * H[(S + 1 + di) % 5][t];
+            o[t] = acc;
+        }
     }
     unsigned char* orow = sw.dst;
     sw.dst += sw.w;
@@ -942,13 +981,10 @@ __device__ __forceinline__ void swar_step(int w, int i, int c, int lane, int r_e
         else
             r[g] = ((o[2 * g] >> a.shift) & 0x00ff00ffu) | (((o[2 * g + 1] >> a.shift) & 0x00ff00ffu) << 8);
     }
-    if (body) {
-        if constexpr (NP == 16) *reinterpret_cast<uint4*>(orow) = make_uint4(r[0], r[1], r[2], r[3]);
-        else *reinterpret_cast<uint2*>(orow) = make_uint2(r[0], r[1]);
-    }
+    swar_store_if<NP>(body, orow, r);
 }
 
-template <int NP, bool SH8>
+template <int NP, bool SH8, bool SYM = false>
 __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int h, int w,
                                                                            const unsigned char* __restrict__ img,
                                                                            unsigned char* __restrict__ out,
@@ -977,7 +1013,7 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int
         cp_wait<S_RING - 1>();
         __syncwarp();
         unsigned char* slot = ring[(i0 - 2 + d + S_RING) % S_RING];
-        swar_enter<NP>(slot, w, c0, lane, a, H[d]);
+        swar_enter<NP, SYM>(slot, w, c0, lane, a, H[d]);
         __syncwarp();
         if (i0 - 2 + d + S_RING < r_end) swar_issue<NP>(row(i0 - 2 + d + S_RING), slot, lane, body, halo);
         cp_commit();
@@ -988,11 +1024,11 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int
     sw.src = img + (long long)(i0 + 2 + S_RING) * w + c;
     sw.dst = out + (long long)i0 * w + c;
     for (int i = i0; i < i1; i += 5) {
-        swar_step<NP, 4, SH8>(w, i, c, lane, r_end, body, halo, ring, H, sw, a);
-        if (i + 1 < i1) swar_step<NP, 0, SH8>(w, i + 1, c, lane, r_end, body, halo, ring, H, sw, a);
-        if (i + 2 < i1) swar_step<NP, 1, SH8>(w, i + 2, c, lane, r_end, body, halo, ring, H, sw, a);
-        if (i + 3 < i1) swar_step<NP, 2, SH8>(w, i + 3, c, lane, r_end, body, halo, ring, H, sw, a);
-        if (i + 4 < i1) swar_step<NP, 3, SH8>(w, i + 4, c, lane, r_end, body, halo, ring, H, sw, a);
+        swar_step<NP, 4, SH8, SYM>(w, i, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 1 < i1) swar_step<NP, 0, SH8, SYM>(w, i + 1, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 2 < i1) swar_step<NP, 1, SH8, SYM>(w, i + 2, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 3 < i1) swar_step<NP, 2, SH8, SYM>(w, i + 3, c, lane, r_end, body, halo, ring, H, sw, a);
+        if (i + 4 < i1) swar_step<NP, 3, SH8, SYM>(w, i + 4, c, lane, r_end, body, halo, ring, H, sw, a);
     }
     cp_wait<0>();
 }
@@ -1035,44 +1071,6 @@ __device__ __forceinline__ unsigned umin16x2(unsigned a, unsigned b) {
     return r;
 }
 
-// The row entering the window as byte pairs: Q[m] = (e[c-2+m], e[c+m]) in 16-bit lanes
-// (m = 0..NP+1); output pair t (pixels c+b, c+b+2 with b = (t & 1) + 4 (t >> 1)) has its centre
-// pair at Q[b + 2].  The lane's 16 body bytes are one 128-bit shared load, its two 4-byte
-// neighbours two 32-bit loads.
-template <int NP, bool EDGE>
-__device__ __forceinline__ void swar2d_enter(const unsigned char* slot, int w, int c0, int lane,
-                                             unsigned (&Q)[NP + 2]) {
-    typedef SwarGeom<NP> G;
-    const unsigned char* body = slot + G::PAD + NP * lane;
-    unsigned Wd[G::NW + 2];
-    Wd[0] = *reinterpret_cast<const unsigned*>(body - 4);
-    if constexpr (NP == 16) {
-        const uint4 v = *reinterpret_cast<const uint4*>(body);
-        Wd[1] = v.x, Wd[2] = v.y, Wd[3] = v.z, Wd[4] = v.w;
-    } else {
-        const uint2 v = *reinterpret_cast<const uint2*>(body);
-        Wd[1] = v.x, Wd[2] = v.y;
-    }
-    Wd[G::NW + 1] = *reinterpret_cast<const unsigned*>(body + NP);
-    if (EDGE && (c0 == 0 || c0 + 32 * NP >= w)) {  // image-edge strips: clamp-to-edge columns
-        const int c = c0 + NP * lane;
-        unsigned v[NP + 4];
-#pragma unroll
-        for (int m = 0; m < NP + 4; m++) v[m] = slot[clampi(c - 2 + m, 0, w - 1) - (c0 - G::PAD)];
-        Wd[0] = (v[0] << 16) | (v[1] << 24);
-#pragma unroll
-        for (int k = 0; k < G::NW; k++)
-            Wd[k + 1] = v[4 * k + 2] | (v[4 * k + 3] << 8) | (v[4 * k + 4] << 16) | (v[4 * k + 5] << 24);
-        Wd[G::NW + 1] = v[NP + 2] | (v[NP + 3] << 8);
-    }
-#pragma unroll
-    for (int k = 0; k <= 2 * G::NW; k++) {
-        const unsigned X = (k & 1) ? Wd[k / 2 + 1] : __funnelshift_r(Wd[k / 2], Wd[k / 2 + 1], 16);
-        Q[2 * k] = __byte_perm(X, 0u, 0x4240);
-        Q[2 * k + 1] = __byte_perm(X, 0u, 0x4341);
-    }
-}
-
 template <bool DIA>
 __device__ __forceinline__ constexpr bool tap_on(int di, int dj) {
     return !DIA || ((di > 2 ? di - 2 : 2 - di) + (dj > 2 ? dj - 2 : 2 - dj) <= 2);
@@ -1091,7 +1089,7 @@ __device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c,
     __syncwarp();
     unsigned char* slot = ring[(r + S_RING) % S_RING];
     unsigned Q[NP + 2];
-    swar2d_enter<NP, EDGE>(slot, w, c - NP * lane, lane, Q);
+    swar_pairs<NP, EDGE>(slot, w, c - NP * lane, lane, Q);
     __syncwarp();
     if (STEADY || r + S_RING < r_end)
         swar_issue<NP>(sw.src > sw.src_last ? sw.src_last : sw.src, slot, lane, body, halo);
@@ -1143,14 +1141,7 @@ __device__ __forceinline__ void swar2d_step(int w, int r, int i0, int i1, int c,
         unsigned rr[NP / 4];
 #pragma unroll
         for (int g = 0; g < NP / 4; g++) rr[g] = __byte_perm(q[2 * g], q[2 * g + 1], 0x6240);
-        const bool st = (STEADY || (orow >= i0 && orow < i1)) && body;
-        unsigned char* dst = sw.dst + (long long)(orow - i0) * w;
-        if constexpr (NP == 16)
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t@p st.global.v4.b32 [%1], {%2, %3, %4, %5};\n\t}"
-                         ::"r"((int)st), "l"(dst), "r"(rr[0]), "r"(rr[1]), "r"(rr[2]), "r"(rr[3]) : "memory");
-        else
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t@p st.global.v2.b32 [%1], {%2, %3};\n\t}"
-                         ::"r"((int)st), "l"(dst), "r"(rr[0]), "r"(rr[1]) : "memory");
+        swar_store_if<NP>((STEADY || (orow >= i0 && orow < i1)) && body, sw.dst + (long long)(orow - i0) * w, rr);
     }
 #pragma unroll
     for (int t = 0; t < NP / 2; t++) A[D][t] = a.init2;
@@ -1554,7 +1545,11 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
         const bool n16 = np_max == 16 && w % 16 == 0 && (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0;
         const int np = n16 ? 16 : 8;
         dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
-        if (n16 && sa.shift == 8) stencil_bytes_swar_kernel<16, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+        const bool sym = sa.u[0] == sa.u[4] && sa.u[1] == sa.u[3] && sa.v[0] == sa.v[4] && sa.v[1] == sa.v[3];
+        if (n16 && sym && sa.shift == 8)
+            stencil_bytes_swar_kernel<16, true, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+        else if (n16 && sym) stencil_bytes_swar_kernel<16, false, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+        else if (n16 && sa.shift == 8) stencil_bytes_swar_kernel<16, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
         else if (n16) stencil_bytes_swar_kernel<16, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
         else if (sa.shift == 8) stencil_bytes_swar_kernel<8, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
         else stencil_bytes_swar_kernel<8, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);

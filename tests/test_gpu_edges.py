@@ -303,7 +303,8 @@ def test_conv_f32_pow2_guard_diverts_tiny_pixels(cuda):
 @pytest.mark.parametrize("h,w", [(70, 256), (33, 520), (64, 264), (9, 8), (5, 512), (130, 1024), (40, 1040), (12, 16), (21, 1552)])
 def test_conv_u8_bytes_swar_bit_exact(cuda, h, w):
     """Non-negative rank-1 taps with 16-bit sums take the SWAR kernel (two pixels per register,
-    16 pixels per lane when w % 16 == 0, else 8; scale 256: byte-select requantisation, other powers of two: shift + mask);
+    16 pixels per lane when w % 16 == 0, else 8; scale 256: byte-select requantisation, other powers of two: shift + mask;
+    mirror-symmetric factors: the shared-pair-sum form, others the general one);
     strips at both image edges, strips narrower than a warp, and the non-SWAR cases (signed taps,
     sums >= 2^16, a clamp needed) beside them."""
     import paper_1302_5586_b200 as pb
@@ -312,8 +313,10 @@ def test_conv_u8_bytes_swar_bit_exact(cuda, h, w):
     img[: min(h * w, 3 * w)] = 255  # saturated rows: the largest sums
     box = np.outer([1, 2, 2, 2, 1], [1, 2, 2, 2, 1]).astype(synth.BINOMIAL.dtype).reshape(-1)
     neg = -synth.BINOMIAL
+    skew = np.outer([1, 3, 5, 2, 0], [2, 1, 4, 6, 3]).astype(synth.BINOMIAL.dtype).reshape(-1)  # not symmetric
+    half = np.outer([1, 4, 6, 4, 1], [0, 1, 5, 3, 1]).astype(synth.BINOMIAL.dtype).reshape(-1)  # one factor symmetric
     for k, scale in ((synth.BINOMIAL, 256), (box, 64), (box, 32), (neg, 256), (synth.BINOMIAL, 128),
-                     (synth.BINOMIAL * 2, 512), (synth.SHARPEN, 1)):
+                     (synth.BINOMIAL * 2, 512), (synth.SHARPEN, 1), (skew, 256), (skew, 64), (half, 128)):
         out8 = torch.empty(h * w, dtype=torch.uint8, device="cuda")
         pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img.astype(np.uint8)).cuda(), k, out8)
         ref = oracle.conv5x5_u8(h, w, scale, img, k)
