@@ -513,7 +513,7 @@ def suite(args, torch, pb, hbm):
     out8 = torch.empty(npx, dtype=torch.uint8, device="cuda")
     b = 2 * npx
     for name, taps, scale, kern, desc in (
-            ("conv5x5_u8_bytes_16384", synth.BINOMIAL, 256, "stencil_bytes_swar_kernel<16, 1>",
+            ("conv5x5_u8_bytes_16384", synth.BINOMIAL, 256, "stencil_bytes_swar_kernel<16, 1, 1>",
              "binomial, scale 256 (16-bit SWAR sums, 16 px per lane)"),
             ("conv5x5_u8_bytes_16384_sharpen", synth.SHARPEN, 1, "stencil_bytes_swar2d_kernel<16, 1, 1, 1>",
              "signed sharpen (centre-positive, off-centre non-positive diamond taps: signed 2-D SWAR kernel), scale 1")):
