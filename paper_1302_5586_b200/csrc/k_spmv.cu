@@ -672,7 +672,10 @@ __device__ __forceinline__ void seg_reduce(int lane, const SegWin<E>& w, float* 
 // flight.  Measured at 2^24 rows (tools/ab_spmv_modes.sh): vec / inline 1.145 / 1.306 ms unpipelined
 // at 6 CTAs per SM -> 1.134 / 1.305 pipelined at 5 (at 6 the 40-register cap costs 1.19 / 1.32; at 4,
 // 1.18 / 1.34).  Two deep (w+2's stream loads, w+1's gathers, w's reduction): 1.21 / 1.37 at 4 CTAs
-// per SM and spills at 5 — the registers cost more warps than the deeper pipeline hides.
+// per SM and spills at 5 — the registers cost more warps than the deeper pipeline hides.  col / val
+// staged through a per-warp shared-memory ring by bulk copies (lane 0, mbarrier completion, 2 / 4 / 5
+// windows ahead) so that the gathers never wait for the column stream: 1.81-2.94 ms (same bits) —
+// the per-warp 1 KB bulk copies are far slower than the LSU streams here.
 template <int E, bool ORDERED>
 __device__ __forceinline__ void seg_tile(int P0, int P1, int nnz_len, int ncols, int lane, const int* __restrict__ col,
                                          const float* __restrict__ val, const float* __restrict__ x,

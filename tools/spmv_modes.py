@@ -35,4 +35,5 @@ out = {}
 for mode, name in ((1, "spmv_vec (reassociated)"), (0, "spmv_inline (source order)")):  # noqa: E501
     plan = pb.device.CsrPlan(n, n, col.size, rp, mode=mode)
     out[name] = t(lambda: plan.spmv(rp, cd, vd, xd, y))
+    out[name + " bits"] = int(y.view(torch.int32).to(torch.int64).sum())  # A/B builds: same bits
 print(json.dumps(out))
