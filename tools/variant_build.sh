@@ -11,6 +11,7 @@
 #   -DPENCIL_VARIANT_NO_PF       no power-of-two fused f32 taps
 #   -DPENCIL_VARIANT_L2_DIRTY    L2 flush without the discard (dirty lines left)
 #   -DPENCIL_VARIANT_NO_SEG      spmv_vec on the batch-and-fold executor (csr_flow_kernel), not csr_seg_kernel
+#   -DGEMM_LO_TRUNC              gemm lo halves truncated by the tensor core instead of rounded (timing only)
 set -e
 name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
