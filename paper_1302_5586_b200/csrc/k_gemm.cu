@@ -42,9 +42,11 @@
 // arrives fixed it.  (Those were timing-only builds with wrong results, not kept.)  A nanosleep
 // back-off in the epilogue's wait for its accumulator (to spend fewer issue slots under the power
 // cap) measured the same: 36.3-36.9 ms either way on one box.  The converters' power matters:
-// leaving lo unrounded for the tensor core to truncate (-DGEMM_LO_TRUNC) runs 2.7 % faster
-// (34.2 -> 33.3 ms, 16384^3, same box) but doubles the per-product error bound (2^-20 -> 2^-19);
-// not shipped.
+// without the cvt.rna.tf32 (lo left for the tensor core to truncate, -DGEMM_LO_TRUNC) the kernel
+// ran 2.7 % faster (34.2 -> 33.3 ms, 16384^3, same box) at twice the error bound; lo_tf32 now gets
+// the same round-to-nearest from one integer add (the tensor core's truncation does the rest):
+// bit-identical C (tools/gemm_bits.py, 1536x1280x2064 and 4096^3) and 1.7 % faster than the CVT
+// (35.0 / 35.6 vs 35.6 / 36.3 ms at 16384^3 on one box, 3.72 vs 3.75 ms at 8192^3).
 #include <cuda.h>
 
 #include "common.cuh"
@@ -165,14 +167,20 @@ __device__ __forceinline__ uint32_t cta_rank() {
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// lo = rna_tf32(x - hi), as the tensor core will read it: it keeps the sign, exponent and top 10
+// mantissa bits of a 32-bit operand (truncation), so adding half a tf32 ulp to the magnitude bits
+// (+0x1000; a carry into the exponent is the correct round-up) makes its truncation round to
+// nearest, ties away — the value cvt.rna.tf32.f32 gives, for one integer add instead of the CVT.
 __device__ __forceinline__ uint32_t lo_tf32(uint32_t x) {
     const float r = __uint_as_float(x) - __uint_as_float(x & 0xffffe000u);  // exact
-#ifdef GEMM_LO_TRUNC  // A/B build: lo left for the tensor core to truncate
+#if defined(GEMM_LO_TRUNC)  // A/B build: lo left for the tensor core to truncate
     return __float_as_uint(r);
-#else
+#elif defined(GEMM_LO_CVT)  // A/B build: the explicit conversion
     uint32_t l;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
     return l;
+#else
+    return __float_as_uint(r) + 0x1000u;
 #endif
 }
 

@@ -12,6 +12,7 @@
 #   -DPENCIL_VARIANT_L2_DIRTY    L2 flush without the discard (dirty lines left)
 #   -DPENCIL_VARIANT_NO_SEG      spmv_vec on the batch-and-fold executor (csr_flow_kernel), not csr_seg_kernel
 #   -DGEMM_LO_TRUNC              gemm lo halves truncated by the tensor core instead of rounded (timing only)
+#   -DGEMM_LO_CVT                gemm lo halves rounded by cvt.rna.tf32 (round 2's first form; same bits)
 set -e
 name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
