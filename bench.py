@@ -201,7 +201,23 @@ def bench_spmv(args, torch, pb, rank, world, dist):
         # belongs to): the fused path through its ping-pong halves, the unfused one by swapping
         # two gathered buffers
         if mode == "fused":
+            # one checked step before the timing: the fused result must equal SpMV + all-gather bit
+            # for bit on every rank, else the bench takes the unfused step (and says why)
             fz.load(x_local)
+            fz.step(plan, rp, cd, vd, None, y)
+            got = fz.current().view(torch.int32).clone()
+            y_ref = torch.zeros(sh.max_rows, device="cuda")
+            plan.spmv(rp, cd, vd, xg, y_ref[: sh.nrows])
+            ref = sh.allgather_x(y_ref).view(torch.int32)
+            bad = torch.tensor([0 if torch.equal(got[: ref.numel()], ref) else 1], device="cuda")
+            dist.all_reduce(bad)
+            if int(bad.item()):
+                mode, why = "nccl", "the fused step differed from SpMV + all-gather on %d rank(s)" % int(bad.item())
+                exchange += " -> failed its check step"
+            else:
+                exchange += ", checked against SpMV + all-gather (bit-identical)"
+                fz.load(x_local)  # restart the chain from x
+        if mode == "fused":
 
             def step():
                 fz.step(plan, rp, cd, vd, None, y)
