@@ -808,20 +808,37 @@ def suite_dist(args, torch, pb, rank, world, dist, hbm):
         try:
             img = synth.f32(h * w_) if f32 else synth.u8_i32(h * w_)
             dtype = torch.float32 if f32 else torch.int32
-            if fused_ok:
+            kf = (synth.BINOMIAL / 256.0).astype(np.float32)
+            fused, check = fused_ok, None
+            if fused:
                 fb = pd.FusedBandStencil(h, w_, rank, world, dtype, torch.device("cuda", torch.cuda.current_device()))
                 fb.band().copy_(torch.from_numpy(img[fb.b0 * w_:fb.b1 * w_]))
                 outb = torch.zeros(fb.nb * w_, dtype=dtype, device="cuda")
-                kf = (synth.BINOMIAL / 256.0).astype(np.float32)
                 step = (lambda: fb.step_f32(kf, outb)) if f32 else (lambda: fb.step_u8(256, synth.BINOMIAL, outb))
                 rows, how = fb.nb, "fused: the band sweep reads the neighbours' edge rows over NVLink (cp.async from peer mappings)"
-            else:
+                # one checked step: the band must equal the same rows of the whole-image stencil
+                step()
+                full_in = torch.from_numpy(img).cuda()
+                full_out = torch.zeros(h * w_, dtype=dtype, device="cuda")
+                if f32:
+                    pb.device.conv5x5_f32(h, w_, full_in, kf, full_out)
+                else:
+                    pb.device.conv5x5_u8(h, w_, 256, full_in, synth.BINOMIAL, full_out)
+                same = torch.equal(outb.view(torch.int32), full_out[fb.b0 * w_:fb.b1 * w_].view(torch.int32))
+                bad = torch.tensor([0 if same else 1], device="cuda")
+                dist.all_reduce(bad)
+                del full_in, full_out
+                if int(bad.item()):
+                    fused, check = False, "the fused band step differed from the whole-image stencil on %d rank(s)" % int(bad.item())
+                    del fb, outb
+                else:
+                    check = "band == the same rows of the whole-image stencil, bit for bit (one step, every rank)"
+            if not fused:
                 band = pd.BandShardedImage(h, w_, rank, world)
                 ext = torch.zeros(band.rows * w_, dtype=dtype, device="cuda")
                 ext.view(band.rows, w_)[band.top:band.top + band.b1 - band.b0] = \
                     torch.from_numpy(img[band.b0 * w_:band.b1 * w_]).cuda().view(-1, w_)
                 outb = torch.zeros(band.rows * w_, dtype=dtype, device="cuda")
-                kf = (synth.BINOMIAL / 256.0).astype(np.float32)
 
                 def step():
                     band.exchange_halos(ext.view(band.rows, w_))
@@ -831,9 +848,11 @@ def suite_dist(args, torch, pb, rank, world, dist, hbm):
                         pb.device.conv5x5_u8(band.rows, w_, 256, ext, synth.BINOMIAL, outb)
                 rows, how = band.b1 - band.b0, "unfused: %s send/recv of 2 halo rows, then the stencil" % args.dist_backend
             ms = statistics.mean(run_steps(torch, step, k, w, flush, dist))
+            extra = {"exchange": how, "taps": "binomial" + (" / 256" if f32 else ", scale 256")}
+            if check:
+                extra["check"] = check
             out[name] = dist_line(torch, dist, ms, 8.0 * h * w_, "GB/s", hbm,
-                                  "stencil_band_kernel" if fused_ok else "stencil_ring_kernel", 8.0 * rows * w_,
-                                  {"exchange": how, "taps": "binomial" + (" / 256" if f32 else ", scale 256")})
+                                  "stencil_band_kernel" if fused else "stencil_ring_kernel", 8.0 * rows * w_, extra)
             del img
         except Exception as e:  # noqa: BLE001
             out[name] = {"unavailable": str(e)[:200]}
