@@ -56,11 +56,19 @@
 // plan_flags: [0] non-monotone rowptr (generic schedule), [2] some row is empty.  rs_bits (when
 // given): bit k set iff non-zero k is the first of its row — the row-start map of the segmented
 // executor (csr_seg_kernel).
-__global__ void csr_plan_kernel(int nrows, int nnz_len, const int* __restrict__ rowptr,
-                                int tile_nnz, int ntiles, int* __restrict__ tile_row,
-                                unsigned* __restrict__ plan_flags, unsigned* __restrict__ rs_bits,
-                                unsigned* __restrict__ status) {
+__global__ void csr_plan_kernel(int nrows, int nnz_len, const int* __restrict__ rowptr, TileSchedule ts,
+                                int* __restrict__ tile_row, unsigned* __restrict__ plan_flags,
+                                unsigned* __restrict__ rs_bits, unsigned* __restrict__ status) {
     const int base = __ldg(rowptr);
+    const long long kA = ts.tail_start / ts.tile_nnz;  // tiles before the tapered tail
+    // window k starts at B(k) = k T (k <= kA), tail_start + (k - kA) T2 after: first k with B(k) > o,
+    // and last k with B(k) <= o
+    auto first_above = [&](long long o) {
+        return o < ts.tail_start ? o / ts.tile_nnz + 1 : kA + (o - ts.tail_start) / ts.tail_nnz + 1;
+    };
+    auto last_at_or_below = [&](long long o) {
+        return o < ts.tail_start ? o / ts.tile_nnz : kA + (o - ts.tail_start) / ts.tail_nnz;
+    };
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= nrows;
          i += (long long)gridDim.x * blockDim.x) {
         const int raw = __ldg(rowptr + i);
@@ -76,12 +84,12 @@ __global__ void csr_plan_kernel(int nrows, int nnz_len, const int* __restrict__ 
                 atomicOr(rs_bits + (praw >> 5), 1u << (praw & 31));
         }
         if (cur <= prev) continue;
-        long long k_lo = prev < 0 ? 0 : prev / tile_nnz + 1;
-        long long k_hi = cur / tile_nnz;
-        if (k_hi > ntiles - 1) k_hi = ntiles - 1;
+        long long k_lo = prev < 0 ? 0 : first_above(prev);
+        long long k_hi = last_at_or_below(cur);
+        if (k_hi > ts.ntiles - 1) k_hi = ts.ntiles - 1;
         for (long long k = k_lo; k <= k_hi; k++) tile_row[k] = (int)i;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) tile_row[ntiles] = nrows;
+    if (blockIdx.x == 0 && threadIdx.x == 0) tile_row[ts.ntiles] = nrows;
 }
 
 // Row result store.  DIST (fused SpMV -> all-gather, launch_csr_spmv_dist): the value also goes
@@ -753,14 +761,14 @@ __global__ void __launch_bounds__(SPMV_THREADS, ORDERED ? SEG_CTAS_PER_SM_ORD : 
     }
 }
 
-int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
-                    int ntiles, int* tile_row, unsigned* plan_flags, unsigned* rs_bits, unsigned* status) {
+int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, const TileSchedule& ts,
+                    int* tile_row, unsigned* plan_flags, unsigned* rs_bits, unsigned* status) {
     cudaMemsetAsync(plan_flags, 0, 64, st);  // [0] non-monotone flag, [2] empty-row flag
     if (rs_bits) cudaMemsetAsync(rs_bits, 0, csr_rs_words(nnz_len) * sizeof(unsigned), st);
     long long blocks = ((long long)nrows + 1 + 255) / 256;
     if (blocks > PENCIL_NUM_SMS * 16) blocks = PENCIL_NUM_SMS * 16;
-    csr_plan_kernel<<<(int)blocks, 256, 0, st>>>(nrows, nnz_len, rowptr, tile_nnz, ntiles, tile_row,
-                                                 plan_flags, rs_bits, status);
+    csr_plan_kernel<<<(int)blocks, 256, 0, st>>>(nrows, nnz_len, rowptr, ts, tile_row, plan_flags, rs_bits,
+                                                 status);
     return (int)cudaGetLastError();
 }
 
@@ -984,4 +992,31 @@ int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const
 #ifndef SEG_TILE_NNZ
 #define SEG_TILE_NNZ 4096
 #endif
-int csr_tile_nnz(int) { return SEG_TILE_NNZ; }
+#ifndef SEG_TAIL_TILE_NNZ
+#define SEG_TAIL_TILE_NNZ 1024  // 0: no tapered tail
+#endif
+#ifndef SEG_TAIL_WAVES
+#define SEG_TAIL_WAVES 0.5  // tail length in full-size tiles per warp of the launch
+#endif
+// Tickets are drawn in matrix order, so the warps that draw the last full-size tiles start them
+// up to one tile time before the end; the tail's smaller tiles (half a wave of the launch's warps
+// of work) keep the other warps busy meanwhile and end within a small tile of each other.
+// Measured at 2^24 rows (tools/ab_spmv_modes.sh, two rounds): vec / inline 1.133 / 1.239 ms
+// without the tail, 1.129 / 1.233 with it (1024-nnz tail tiles, 0.5 wave); 1 wave 1.132 / 1.234,
+// 2 waves 1.139 / 1.238, 512-nnz tail tiles 1.141 / 1.241, 2048 1.132 / 1.234 — small: the
+// request path is shared per SM, so an SM stays busy until its last few warps run dry.
+TileSchedule csr_tile_schedule(int mode, int nnz_len) {
+    TileSchedule ts;
+    const long long nnz = nnz_len > 0 ? nnz_len : 0;
+    ts.tile_nnz = SEG_TILE_NNZ;
+    ts.tail_nnz = SEG_TAIL_TILE_NNZ > 0 ? SEG_TAIL_TILE_NNZ : SEG_TILE_NNZ;
+    const long long warps = (long long)PENCIL_NUM_SMS * (mode ? SEG_CTAS_PER_SM : SEG_CTAS_PER_SM_ORD) * WARPS_PER_CTA;
+    long long tail = SEG_TAIL_TILE_NNZ > 0 ? (long long)(SEG_TAIL_WAVES * (double)warps * SEG_TILE_NNZ) : 0;
+    // the tail starts on a full-size window boundary; small matrices are all tail or all full-size
+    long long start = nnz - tail;
+    start = start > 0 ? start / ts.tile_nnz * ts.tile_nnz : 0;
+    ts.tail_start = start;
+    const long long nt = start / ts.tile_nnz + (nnz - start + ts.tail_nnz - 1) / ts.tail_nnz;
+    ts.ntiles = (int)(nt < 1 ? 1 : nt);
+    return ts;
+}

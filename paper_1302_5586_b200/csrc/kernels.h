@@ -21,8 +21,17 @@ int launch_axpy(cudaStream_t st, long long n, float a, const float* a_dev, const
 
 // k_spmv.cu
 // rs_bits (optional, csr_rs_words(nnz) words): the row-start bitmap of the segmented executor
-int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, int tile_nnz,
-                    int ntiles, int* tile_row, unsigned* plan_flags, unsigned* rs_bits, unsigned* status);
+// The plan's tiles: windows of tile_nnz non-zeros up to tail_start, then of tail_nnz (a tapered
+// tail, so that the warps drawing the last tickets finish together); ntiles in all.
+struct TileSchedule {
+    int tile_nnz = 1;
+    long long tail_start = 0;
+    int tail_nnz = 1;
+    int ntiles = 1;
+};
+TileSchedule csr_tile_schedule(int mode, int nnz_len);
+int launch_csr_plan(cudaStream_t st, int nrows, int nnz_len, const int* rowptr, const TileSchedule& ts,
+                    int* tile_row, unsigned* plan_flags, unsigned* rs_bits, unsigned* status);
 size_t csr_rs_words(int nnz_len);
 // plans with empty rows: ord (nrows + 1 ints) / rowmap (one int per non-empty row), bsum scratch
 int launch_csr_ordinals(cudaStream_t st, int nrows, const int* rowptr, int* ord, int* rowmap, int* bsum);
@@ -43,7 +52,6 @@ int launch_csr_spmv(cudaStream_t st, int assoc, int nrows, int ncols, int nnz_le
 int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const int* rowptr,
                        const int* col, const float* val, const float* x, float* y,
                        unsigned* status);
-int csr_tile_nnz(int mode);
 // fused SpMV -> all-gather of y: every row result is also stored to `n` peer buffers (NVLink
 // peer mappings, each already offset to this rank's slot) or, when mc is set, once to an NVLS
 // multicast address that replicates it to every rank

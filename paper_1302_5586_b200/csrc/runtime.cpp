@@ -392,9 +392,9 @@ int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int*
     p->nrows = nrows;
     p->nnz = nnz;
     p->mode = mode;
-    p->tile_nnz = csr_tile_nnz(mode);
-    long long nt = ((long long)nnz + p->tile_nnz - 1) / p->tile_nnz;
-    p->ntiles = (int)(nt < 1 ? 1 : nt);
+    const TileSchedule ts = csr_tile_schedule(mode, nnz);
+    p->tile_nnz = ts.tile_nnz;
+    p->ntiles = ts.ntiles;
     int r = pool_alloc(c, st, sizeof(int) * ((size_t)p->ntiles + 1), (void**)&p->tile_row);
     if (r) return r;
     r = pool_alloc(c, st, 64, (void**)&p->flags);
@@ -403,8 +403,7 @@ int csr_plan_build(DeviceCtx* c, cudaStream_t st, int nrows, int nnz, const int*
     CK(cudaMemsetAsync(p->tile_row, 0, sizeof(int) * ((size_t)p->ntiles + 1), st));
     if (!fw) fw = fault_word(c, st);
     if (!fw) return g_status;
-    return (int)launch_csr_plan(st, nrows, nnz, rowptr, p->tile_nnz, p->ntiles, p->tile_row, p->flags, p->rs_bits,
-                                fw) == 0
+    return (int)launch_csr_plan(st, nrows, nnz, rowptr, ts, p->tile_row, p->flags, p->rs_bits, fw) == 0
                ? PENCIL_OK
                : fail(PENCIL_E_CUDA, "csr plan launch");
 }
