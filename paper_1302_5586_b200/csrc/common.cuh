@@ -62,6 +62,15 @@ __device__ __forceinline__ unsigned ld_stream_u(const unsigned* p) {
                  : "l"(p), "l"(pol_evict_first()));
     return r;
 }
+// A random gather from a vector that L2 should keep (SpMV's x): not allocated in L1, where the
+// scattered sectors would only evict lines other warps still need.
+__device__ __forceinline__ float ld_gather_f(const float* p) {
+    float r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+                 : "=f"(r)
+                 : "l"(p), "l"(pol_evict_last()));
+    return r;
+}
 // Reused data (a gathered vector): keep in L2 as long as possible.
 __device__ __forceinline__ float ld_keep_f(const float* p) {
     float r;

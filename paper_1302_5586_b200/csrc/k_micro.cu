@@ -17,7 +17,8 @@ __device__ __forceinline__ float gather_ld(const float* p) {
 }
 
 // the SpMV data path without rows: stream idx + val (8 B/nnz, 128-bit loads), gather table[idx]
-// (evict-last), accumulate val * x — the practical ceiling of a CSR SpMV on this matrix
+// (the executor's load: evict-last in L2, not allocated in L1), accumulate val * x — the
+// practical ceiling of a CSR SpMV on this matrix
 __global__ void __launch_bounds__(256) micro_gather_val_kernel(long long n, const int* __restrict__ idx,
                                                                const float* __restrict__ val,
                                                                const float* __restrict__ table,
@@ -29,8 +30,8 @@ __global__ void __launch_bounds__(256) micro_gather_val_kernel(long long n, cons
     for (long long i = tid; i < n4; i += nthr) {
         const int4 a = ld_stream_i4(reinterpret_cast<const int4*>(idx) + i);
         const float4 v = ld_stream_f4(reinterpret_cast<const float4*>(val) + i);
-        acc += v.x * ld_keep_f(table + a.x) + v.y * ld_keep_f(table + a.y) + v.z * ld_keep_f(table + a.z) +
-               v.w * ld_keep_f(table + a.w);
+        acc += v.x * ld_gather_f(table + a.x) + v.y * ld_gather_f(table + a.y) + v.z * ld_gather_f(table + a.z) +
+               v.w * ld_gather_f(table + a.w);
     }
     out[tid] = acc;
 }

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_stream_kernel(
             for (int u = 0; u < WCH / 32; u++) {
                 xv[u] = 0.f;
                 if (u * 32 + lane < cnt) {
-                    if ((unsigned)c[u] < (unsigned)ncols) xv[u] = ld_keep_f(x + c[u]);
+                    if ((unsigned)c[u] < (unsigned)ncols) xv[u] = ld_gather_f(x + c[u]);
                     else raise_fault(status, FAULT_OOB_LOAD);
                 }
             }
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, CTAS_PER_SM) csr_flow_kernel(
                 for (int k = 0; k < 4; k++) {
                     const bool in = p + k >= P0 && p + k < P1, ok = (unsigned)c[k] < (unsigned)ncols;
                     use[k] = in && ok;
-                    xv[k] = ld_keep_f(x + (use[k] ? c[k] : 0));
+                    xv[k] = ld_gather_f(x + (use[k] ? c[k] : 0));
                     if (in && !ok) raise_fault(status, FAULT_OOB_LOAD);
                 }
 #pragma unroll
@@ -600,7 +600,7 @@ __device__ __forceinline__ void seg_fetch(int qa, int P0, int P1, int nnz_len, i
 #pragma unroll
         for (int k = 0; k < E; k++) {
             const bool in = FULL || (p + k >= P0 && p + k < P1), ok = (unsigned)c[k] < (unsigned)ncols;
-            w.xv[k] = ld_keep_f(x + (in && ok ? c[k] : 0));
+            w.xv[k] = ld_gather_f(x + (in && ok ? c[k] : 0));
             use |= (unsigned)(in && ok) << k;
             bad |= in && !ok;
             if (!FULL && !(p + k > P0 && p + k < P1)) sb &= ~(1u << k);
