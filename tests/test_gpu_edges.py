@@ -397,3 +397,43 @@ def test_spmv_empty_rows_take_the_segmented_executor(cuda, every):
     yh = np.full(n2, np.nan, np.float32)
     pb.dropin.spmv_inline(n2, x.size, nnz, rp2, col, val, x, yh)
     assert np.array_equal(yh.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_spmv_tapered_tiles_across_the_tail_start(cuda, mode):
+    """The plan cuts 4096-non-zero tiles, then 1024-non-zero ones for the last half wave of the
+    launch's warps: a 16 M non-zero matrix has both, with long rows (and empty rows) straddling
+    the switch; source order bit-identical to the emitted C's fp32 chain, reassociated within the
+    normwise bound, tile count as the schedule states."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    rng = np.random.default_rng(23)
+    target = 16_000_000
+    lens = list(rng.integers(0, 40, target // 19))
+    rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    # long rows and an empty row wherever the tail may start (either mode's launch width)
+    warps = 148 * (5 if mode else 4) * 8
+    start = (int(rowptr[-1]) - warps * 4096 // 2) // 4096 * 4096
+    r = int(np.searchsorted(rowptr, start))
+    lens[r - 1:r - 1] = [9000, 0, 4097, 1025, 1]
+    rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    nrows, nnz, ncols = len(lens), int(rowptr[-1]), 1 << 20
+    col = rng.integers(0, ncols, nnz).astype(np.int32)
+    val, x = synth.f32(nnz, seed=31), synth.f32(ncols, seed=32)
+    rp = torch.from_numpy(rowptr).cuda()
+    plan = pb.device.CsrPlan(nrows, ncols, nnz, rp, mode=mode)
+    nt, tn = plan.info()
+    tail = warps * 4096 // 2
+    s0 = max(0, nnz - tail) // 4096 * 4096
+    assert tn == 4096 and nt == s0 // 4096 + (nnz - s0 + 1023) // 1024
+    y = torch.full((nrows,), 7.0, device="cuda")
+    plan.spmv(rp, torch.from_numpy(col).cuda(), torch.from_numpy(val).cuda(), torch.from_numpy(x).cuda(), y)
+    pb.device.sync_status()
+    got = y.cpu().numpy()
+    if mode == 0:
+        exact = oracle.spmv_f32(nrows, ncols, nnz, rowptr, col, val, x)
+        assert np.array_equal(got.view(np.uint32), exact.view(np.uint32))
+    else:
+        ref = oracle.spmv(nrows, ncols, nnz, rowptr, col, val, x)
+        scale = oracle.spmv(nrows, ncols, nnz, rowptr, col, np.abs(val), np.abs(x))
+        assert normwise_err(got, ref, scale) < 1e-5
