@@ -48,7 +48,20 @@ constexpr int S_WARPS = 4;
 #ifndef STENCIL_BAND
 #define STENCIL_BAND 64
 #endif
-constexpr int S_BAND = STENCIL_BAND;  // output rows per warp sweep (swept 32/64/128/256: 64 ~ 128 best, within 1%)
+constexpr int S_BAND = STENCIL_BAND;  // output rows per warp sweep of the packed-byte kernels
+// ... and of the ring / band kernels, per storage (16384², tools/conv_probe.py, two rounds on one
+// box): int32-storage u8 32 rows 0.355 / 0.353 ms (binomial / sharpen) against 0.364 at 64 and
+// 0.372 at 128; fp32 128 rows 0.394 / 0.471 ms (PF / generic taps) against 0.396 / 0.475 at 64 and
+// 0.404 / 0.487 at 32 (u8 16 rows: sharpen 0.372; fp32 256: 0.397 / 0.477); the packed-byte SWAR
+// kernels are best at 64 (sharpen 0.139 vs 0.143 / 0.152 at 32 / 128).
+#ifndef STENCIL_BAND_U8
+#define STENCIL_BAND_U8 32
+#endif
+#ifndef STENCIL_BAND_F32
+#define STENCIL_BAND_F32 128
+#endif
+template <bool U8>
+__host__ __device__ constexpr int ring_band() { return U8 ? STENCIL_BAND_U8 : STENCIL_BAND_F32; }
 #ifndef STENCIL_RING
 #define STENCIL_RING 8
 #endif
@@ -422,8 +435,8 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
     if (c0 >= w) return;
     const int c = c0 + 4 * lane;
     // output rows [i0, i1); input rows [i0 - 2, i1 + 2)
-    const int i0 = (U8 ? 0 : 2) + blockIdx.y * S_BAND;
-    const int i1 = min(U8 ? h : h - 2, i0 + S_BAND);
+    const int i0 = (U8 ? 0 : 2) + blockIdx.y * ring_band<U8>();
+    const int i1 = min(U8 ? h : h - 2, i0 + ring_band<U8>());
     if (i0 >= i1) return;
     const int r_end = i1 + 2;
     const RingLane L = ring_lane(w, c0, lane);
@@ -530,8 +543,8 @@ __global__ void __launch_bounds__(32 * S_WARPS, SEP ? STENCIL_SEP_MINB : (U8 ? S
     const int c0 = (blockIdx.x * S_WARPS + warp) * 128;
     if (c0 >= w) return;
     const int c = c0 + 4 * lane;
-    const int i0 = bs.out_lo + blockIdx.y * S_BAND;
-    const int i1 = min(bs.out_hi, i0 + S_BAND);
+    const int i0 = bs.out_lo + blockIdx.y * ring_band<U8>();
+    const int i1 = min(bs.out_hi, i0 + ring_band<U8>());
     if (i0 >= i1) return;
     const int r_end = i1 + 2;
     const RingLane L = ring_lane(w, c0, lane);
@@ -1376,7 +1389,7 @@ int launch_conv5x5_f32(cudaStream_t st, int h, int w, const float* img, const fl
     a.negz = pack2(-0.0f);
     a.one = pack2(1.0f);
     a.negmag = pack2(-8388608.0f);
-    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h - 4 + S_BAND - 1) / S_BAND);
+    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h - 4 + ring_band<false>() - 1) / ring_band<false>());
     const int pf = pow2_fusable(k25, a.pf_lim);
     unsigned* flag = pf ? repair_flag_for(st) : nullptr;
     if (pf && flag) {
@@ -1428,7 +1441,7 @@ int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, 
     if (!ring_ok(h, w, img, out)) return launch_conv5x5_u8_reg(st, h, w, scale, img, k25, out);
     StencilArgs a = {};
     if (!u8_args(st, scale, k25, a)) return (int)cudaErrorMemoryAllocation;
-    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
+    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + ring_band<true>() - 1) / ring_band<true>());
     if (!a.exact_only) {
         const bool sep = sep_enabled() && separable(k25, a), dia = !sep && diamond(k25);
         if (sep && a.shift >= 0) stencil_ring_kernel<true, true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
@@ -1459,7 +1472,7 @@ int launch_conv5x5_u8_band(cudaStream_t st, int h, int w, int scale, const int* 
     StencilArgs a = {};
     if (!u8_args(st, scale, k25, a)) return (int)cudaErrorMemoryAllocation;
     const BandSrc<int> bs = {{top[0], top[1]}, {bot[0], bot[1]}, 0, h};
-    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
+    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (h + ring_band<true>() - 1) / ring_band<true>());
     if (!a.exact_only) {
         const bool sep = sep_enabled() && separable(k25, a), dia = !sep && diamond(k25);
         if (sep && a.shift >= 0) stencil_band_kernel<true, true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, bs);
@@ -1486,7 +1499,7 @@ int launch_conv5x5_f32_band(cudaStream_t st, int h, int w, int out_lo, int out_h
     a.one = pack2(1.0f);
     a.negmag = pack2(-8388608.0f);
     const BandSrc<float> bs = {{top[0], top[1]}, {bot[0], bot[1]}, out_lo, out_hi};
-    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (out_hi - out_lo + S_BAND - 1) / S_BAND);
+    dim3 grid(((w + 127) / 128 + S_WARPS - 1) / S_WARPS, (out_hi - out_lo + ring_band<false>() - 1) / ring_band<false>());
     // power-of-two taps fused as in launch_conv5x5_f32, with the band's own guarded repair pass
     const int pf = pow2_fusable(k25, a.pf_lim);
     unsigned* flag = pf ? repair_flag_for(st) : nullptr;
