@@ -602,6 +602,99 @@ int spmv_common(int mode, int nrows, int ncols, int nnz, int* rowptr, int* col, 
 // =====================================================================================
 // §1 drop-in entry points
 // =====================================================================================
+// Drop-in stencils on host arrays, pipelined by row blocks: block b's input rows upload on the copy
+// stream; its output rows are computed by the band sweep (the rows above / below the block are row
+// pointers into the resident image, clamped at its edges, so the result is the whole-image kernel's
+// bit for bit) once block b+1 has landed (the two rows below); its output rows download on the D2H
+// stream while later blocks upload — the two PCIe directions overlap instead of one after the other.
+// fp32 copies back only the interior rectangle (rows / columns 2 .. n-3), as the whole-image call.
+// Pageable outputs come back through the staging ring after the last block (one pool of host
+// threads serves both directions).  Taken for images of 64 MB and more with w % 4 == 0 on host arrays.
+#define STENCIL_PIPE_BLOCKS 8
+constexpr long long STENCIL_PIPE_MIN = 64ll << 20;
+template <typename T, typename L>
+int stencil_pipelined(int h, int w, bool f32, const T* img, T* out, L launch_block) {
+    DeviceCtx* c = nullptr;
+    int r = get_ctx(&c);
+    if (r) return r;
+    std::lock_guard<std::mutex> lk(c->mu);
+    PipeCtx* pc = nullptr;
+    if ((r = get_pipe(c, &pc))) return r;
+    cudaStream_t s0 = c->stream, s1 = pc->comp, s2 = pc->d2h;
+    T *dIn = nullptr, *dOut = nullptr;
+    struct Release {
+        std::function<void()> f;
+        ~Release() { f(); }
+    } release{[&]() {
+        cudaStreamSynchronize(s1);
+        cudaStreamSynchronize(s2);
+        pool_free(s0, dIn);
+        pool_free(s0, dOut);
+        cudaStreamSynchronize(s0);
+    }};
+    const size_t n = (size_t)h * w, row = sizeof(T) * (size_t)w;
+    if ((r = pool_alloc(c, s0, sizeof(T) * n, (void**)&dIn)) || (r = pool_alloc(c, s0, sizeof(T) * n, (void**)&dOut)))
+        return r;
+    const bool in_staged = staged(img, sizeof(T) * n), out_staged = staged(out, sizeof(T) * n);
+    const int K = STENCIL_PIPE_BLOCKS, rows = (h + K - 1) / K;
+    const int olo = f32 ? 2 : 0, ohi = f32 ? h - 2 : h;  // output rows the call stores
+    const size_t col0 = f32 ? 2 : 0, ncol = f32 ? (size_t)w - 4 : (size_t)w;
+    g_h2d = (long long)(sizeof(T) * n);
+    g_d2h = (long long)(sizeof(T) * ncol * (size_t)(ohi - olo));
+    auto rowp = [&](T* base, int i) { return base + (size_t)(i < 0 ? 0 : (i > h - 1 ? h - 1 : i)) * w; };
+    int nb = 0;
+    for (int r0 = 0; r0 < h; r0 += rows) nb++;
+    for (int b = 0; b < nb; b++) {  // uploads, in order on the copy stream
+        const int r0 = b * rows, r1 = std::min(h, r0 + rows);
+        const size_t bytes = row * (size_t)(r1 - r0);
+        if (in_staged) CK((cudaError_t)staged_h2d_2d(c->device, dIn + (size_t)r0 * w, bytes, img + (size_t)r0 * w,
+                                                     bytes, bytes, 1, s0));
+        else CK(cudaMemcpyAsync(dIn + (size_t)r0 * w, img + (size_t)r0 * w, bytes, cudaMemcpyHostToDevice, s0));
+        CK(cudaEventRecord(pc->ev_blk[b], s0));
+        if (b == 0) continue;
+        // block b-1 can run: its rows and the two below it have landed
+        const int q0 = (b - 1) * rows, q1 = std::min(h, q0 + rows);
+        CK(cudaStreamWaitEvent(s1, pc->ev_blk[b], 0));
+        const T* top[2] = {rowp(dIn, q0 - 2), rowp(dIn, q0 - 1)};
+        const T* bot[2] = {rowp(dIn, q1), rowp(dIn, q1 + 1)};
+        int e = launch_block(s1, q0, q1, dIn + (size_t)q0 * w, top, bot, dOut + (size_t)q0 * w);
+        if (e) return cuda_fail((cudaError_t)e, "stencil launch");
+        if (out_staged) continue;
+        const int o0 = std::max(q0, olo), o1 = std::min(q1, ohi);
+        if (o1 <= o0) continue;
+        CK(cudaEventRecord(pc->ev_chunk[b - 1], s1));
+        CK(cudaStreamWaitEvent(s2, pc->ev_chunk[b - 1], 0));
+        CK(cudaMemcpy2DAsync(out + (size_t)o0 * w + col0, row, dOut + (size_t)o0 * w + col0, row, sizeof(T) * ncol,
+                             (size_t)(o1 - o0), cudaMemcpyDeviceToHost, s2));
+    }
+    {  // the last block
+        const int q0 = (nb - 1) * rows, q1 = h;
+        CK(cudaStreamWaitEvent(s1, pc->ev_blk[nb - 1], 0));
+        const T* top[2] = {rowp(dIn, q0 - 2), rowp(dIn, q0 - 1)};
+        const T* bot[2] = {rowp(dIn, q1), rowp(dIn, q1 + 1)};
+        int e = launch_block(s1, q0, q1, dIn + (size_t)q0 * w, top, bot, dOut + (size_t)q0 * w);
+        if (e) return cuda_fail((cudaError_t)e, "stencil launch");
+        const int o0 = std::max(q0, olo), o1 = std::min(q1, ohi);
+        if (!out_staged && o1 > o0) {
+            CK(cudaEventRecord(pc->ev_chunk[nb - 1], s1));
+            CK(cudaStreamWaitEvent(s2, pc->ev_chunk[nb - 1], 0));
+            CK(cudaMemcpy2DAsync(out + (size_t)o0 * w + col0, row, dOut + (size_t)o0 * w + col0, row,
+                                 sizeof(T) * ncol, (size_t)(o1 - o0), cudaMemcpyDeviceToHost, s2));
+        }
+    }
+    if (out_staged && ohi > olo)
+        CK((cudaError_t)staged_d2h_2d(c->device, out + (size_t)olo * w + col0, row, dOut + (size_t)olo * w + col0,
+                                      row, sizeof(T) * ncol, (size_t)(ohi - olo), s1));
+    release.f();
+    release.f = [] {};
+    return collect_faults(c, s0) == PENCIL_OK ? ok() : g_status;
+}
+
+bool stencil_pipe_ok(int h, int w, size_t elem, const void* img, const void* out) {
+    return (long long)h * w * (long long)elem >= STENCIL_PIPE_MIN && h >= 64 && w % 4 == 0 && img && out &&
+           (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0 && !is_device_ptr(img) && !is_device_ptr(out);
+}
+
 extern "C" {
 
 void gemv(int m, int n, float alpha, float beta, float* A, float* x, float* y) {
@@ -707,6 +800,14 @@ void conv5x5_u8(int h, int w, int scale, int* img, int* k, int* out) {
     } else {
         memcpy(taps, k, sizeof taps);
     }
+    if (stencil_pipe_ok(h, w, sizeof(int), img, out)) {
+        stencil_pipelined<int>(h, w, false, img, out,
+                               [&](cudaStream_t s, int q0, int q1, const int* bi, const int* const* top,
+                                   const int* const* bot, int* bo) {
+                                   return launch_conv5x5_u8_band(s, q1 - q0, w, scale, bi, top, bot, taps, bo);
+                               });
+        return;
+    }
     Stage st[2];
     st[0] = {img, nullptr, sizeof(int) * nz((long long)h * w), IN};
     st[1] = {out, nullptr, sizeof(int) * nz((long long)h * w), OUT};
@@ -750,6 +851,16 @@ void conv5x5_f32(int h, int w, float* img, float* k, float* out) {
         }
     } else {
         memcpy(taps, k, sizeof taps);
+    }
+    if (stencil_pipe_ok(h, w, sizeof(float), img, out)) {
+        stencil_pipelined<float>(h, w, true, img, out,
+                                 [&](cudaStream_t s, int q0, int q1, const float* bi, const float* const* top,
+                                     const float* const* bot, float* bo) {
+                                     const int lo = std::max(q0, 2) - q0, hi = std::min(q1, h - 2) - q0;
+                                     if (hi <= lo) return 0;
+                                     return launch_conv5x5_f32_band(s, q1 - q0, w, lo, hi, bi, top, bot, taps, bo);
+                                 });
+        return;
     }
     Stage st[2];
     st[0] = {img, nullptr, sizeof(float) * nz((long long)h * w), IN};

@@ -130,3 +130,36 @@ def test_conv_u8_bytes_host_entry_errors(cuda):
         pb.dropin.conv5x5_u8_bytes(-1, 8, 1, img, synth.BINOMIAL, np.zeros(64, np.uint8))
     assert e.value.code == "E-ARG"
     pb.dropin.conv5x5_u8_bytes(0, 8, 0, img, synth.BINOMIAL, np.zeros(64, np.uint8))  # empty: no-op
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_stencil_dropins_pipelined_equal_device_api(cuda, pinned):
+    """conv5x5_u8 / conv5x5_f32 on host arrays of 64 MB and more run pipelined by row blocks (band
+    sweeps over the resident image, uploads and downloads overlapping): bit-identical to the device
+    API on the whole image — ragged last block, separable / diamond / generic taps, a non-byte pixel
+    (the exact repair pass), fp32 power-of-two and generic taps with the border left untouched."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    h, w = 4099, 4100  # 67 MB of int32 / fp32: ragged blocks of 513 rows
+    host = (lambda a: torch.from_numpy(a).pin_memory()) if pinned else (lambda a: a)
+    img = synth.u8_i32(h * w, seed=41)
+    odd = img.copy()
+    odd[h // 2 * w + 7] = 300  # not a byte: the exact repair pass
+    for im, k, scale in ((img, synth.BINOMIAL, 256), (img, synth.SHARPEN, 1), (odd, synth.BINOMIAL, 256),
+                         (img, synth.BINOMIAL * 3, 7)):
+        dev = torch.empty(h * w, dtype=torch.int32, device="cuda")
+        pb.device.conv5x5_u8(h, w, scale, torch.from_numpy(im).cuda(), k, dev)
+        out = host(np.full(h * w, -1, np.int32))
+        pb.dropin.conv5x5_u8(h, w, scale, host(im), k, out)
+        got = out.numpy() if pinned else out
+        assert np.array_equal(got, dev.cpu().numpy()), (scale, int(k[12]))
+    f = synth.f32(h * w, 43)
+    for k in ((synth.BINOMIAL / 256.0).astype(np.float32), synth.f32(25, 44)):
+        dev = torch.full((h * w,), np.nan, device="cuda")
+        pb.device.conv5x5_f32(h, w, torch.from_numpy(f).cuda(), k, dev)
+        out = host(np.full(h * w, np.nan, np.float32))
+        pb.dropin.conv5x5_f32(h, w, host(f), k, out)
+        got = out.numpy() if pinned else out
+        assert np.array_equal(got.view(np.uint32), dev.cpu().numpy().view(np.uint32))
+        o = got.reshape(h, w)
+        assert np.isnan(o[:2]).all() and np.isnan(o[-2:]).all() and np.isnan(o[:, :2]).all() and np.isnan(o[:, -2:]).all()
