@@ -997,18 +997,17 @@ __device__ __forceinline__ void swar_step(int w, int i, int c, int lane, int r_e
     swar_store_if<NP>(body, orow, r);
 }
 
-template <int NP, bool SH8, bool SYM = false>
-__global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int h, int w,
-                                                                           const unsigned char* __restrict__ img,
-                                                                           unsigned char* __restrict__ out,
-                                                                           SwarArgs a) {
+// lo / hi: the output rows computed (the whole image: 0 / h; the pipelined drop-in: a row block)
+template <int NP, bool SH8, bool SYM>
+__device__ __forceinline__ void swar_sweep(int h, int w, const unsigned char* __restrict__ img,
+                                           unsigned char* __restrict__ out, const SwarArgs& a, int lo, int hi) {
     typedef SwarGeom<NP> G;
     __shared__ __align__(16) unsigned char ring_all[S_WARPS][S_RING][G::ROWE];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c0 = (blockIdx.x * S_WARPS + warp) * 32 * NP;
     if (c0 >= w) return;
     const int c = c0 + NP * lane;
-    const int i0 = blockIdx.y * S_BAND, i1 = min(h, i0 + S_BAND);
+    const int i0 = lo + blockIdx.y * S_BAND, i1 = min(hi, i0 + S_BAND);
     if (i0 >= i1) return;
     const int r_end = i1 + 2;
     const bool body = c + NP - 1 < w;
@@ -1044,6 +1043,22 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int
         if (i + 4 < i1) swar_step<NP, 3, SH8, SYM>(w, i + 4, c, lane, r_end, body, halo, ring, H, sw, a);
     }
     cp_wait<0>();
+}
+// the whole image (its own kernel: the row-block form's two extra parameters cost the sweep ~2 %)
+template <int NP, bool SH8, bool SYM = false>
+__global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_kernel(int h, int w,
+                                                                           const unsigned char* __restrict__ img,
+                                                                           unsigned char* __restrict__ out,
+                                                                           SwarArgs a) {
+    swar_sweep<NP, SH8, SYM>(h, w, img, out, a, 0, h);
+}
+// output rows [lo, hi) (the pipelined drop-in's row blocks)
+template <int NP, bool SH8, bool SYM = false>
+__global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar_rows_kernel(int h, int w,
+                                                                                const unsigned char* __restrict__ img,
+                                                                                unsigned char* __restrict__ out,
+                                                                                SwarArgs a, int lo, int hi) {
+    swar_sweep<NP, SH8, SYM>(h, w, img, out, a, lo, hi);
 }
 
 // ---------------------------------------------------------------- signed 2-D SWAR packed-byte sweep
@@ -1186,18 +1201,16 @@ __device__ __forceinline__ int swar2d_rows(int r, int r_stop, int w, int i0, int
     return r;
 }
 
-template <int NP, bool DIA, bool SH0 = false, bool SYM = false>
-__global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_kernel(int h, int w,
-                                                                             const unsigned char* __restrict__ img,
-                                                                             unsigned char* __restrict__ out,
-                                                                             Swar2dArgs a) {
+template <int NP, bool DIA, bool SH0, bool SYM>
+__device__ __forceinline__ void swar2d_sweep(int h, int w, const unsigned char* __restrict__ img,
+                                             unsigned char* __restrict__ out, const Swar2dArgs& a, int lo, int hi) {
     typedef SwarGeom<NP> G;
     __shared__ __align__(16) unsigned char ring_all[S_WARPS][S_RING][G::ROWE];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c0 = (blockIdx.x * S_WARPS + warp) * 32 * NP;
     if (c0 >= w) return;
     const int c = c0 + NP * lane;
-    const int i0 = blockIdx.y * S_BAND, i1 = min(h, i0 + S_BAND);
+    const int i0 = lo + blockIdx.y * S_BAND, i1 = min(hi, i0 + S_BAND);
     if (i0 >= i1) return;
     const int r_begin = i0 - 2, r_end = i1 + 2;  // input rows of the band (clamped at the image edges)
     const bool body = c + NP - 1 < w;
@@ -1228,6 +1241,20 @@ __global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_kernel(i
     swar2d_rows<NP, DIA, SH0, SYM, true, false>(rb5, r_end, w, i0, i1, c, lane, r_begin, r_end, body, halo, ring, A,
                                                 sw, a);
     cp_wait<0>();
+}
+template <int NP, bool DIA, bool SH0 = false, bool SYM = false>
+__global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_kernel(int h, int w,
+                                                                             const unsigned char* __restrict__ img,
+                                                                             unsigned char* __restrict__ out,
+                                                                             Swar2dArgs a) {
+    swar2d_sweep<NP, DIA, SH0, SYM>(h, w, img, out, a, 0, h);
+}
+template <int NP, bool DIA, bool SH0 = false, bool SYM = false>
+__global__ void __launch_bounds__(32 * S_WARPS, 4) stencil_bytes_swar2d_rows_kernel(int h, int w,
+                                                                                  const unsigned char* __restrict__ img,
+                                                                                  unsigned char* __restrict__ out,
+                                                                                  Swar2dArgs a, int lo, int hi) {
+    swar2d_sweep<NP, DIA, SH0, SYM>(h, w, img, out, a, lo, hi);
 }
 
 // Swar2dArgs for taps with kc >= 0, every off-centre tap <= 0, a power-of-two scale <= 256 and
@@ -1519,13 +1546,39 @@ int launch_conv5x5_f32_band(cudaStream_t st, int h, int w, int out_lo, int out_h
 int launch_conv5x5_u8_bytes_dp4a(cudaStream_t st, int h, int w, int scale, const unsigned char* img,
                                  const int* k25, unsigned char* out);
 
+// the whole-image kernel, or its row-block twin
+template <typename Arg>
+static void swar_go(void (*kw)(int, int, const unsigned char*, unsigned char*, Arg),
+                    void (*kr)(int, int, const unsigned char*, unsigned char*, Arg, int, int), dim3 g,
+                    cudaStream_t st, bool rows, int h, int w, const unsigned char* img, unsigned char* out,
+                    const Arg& a, int lo, int hi) {
+    if (rows) kr<<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, a, lo, hi);
+    else kw<<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
+}
+// Output rows [lo, hi) of the h-row image (rows_only: only when a SWAR kernel applies — the row-block
+// form of the pipelined drop-in; returns cudaErrorNotSupported otherwise, launching nothing).
+// probe: report whether the row-block form applies (16-byte aligned buffers assumed), launch nothing.
+static int conv_u8_bytes_rows(cudaStream_t st, int h, int w, int scale, const unsigned char* img, const int* k25,
+                              unsigned char* out, int lo, int hi, bool rows_only, bool probe = false);
 int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsigned char* img, const int* k25,
                             unsigned char* out) {
-    if (h <= 0 || w <= 0) return 0;
+    return conv_u8_bytes_rows(st, h, w, scale, img, k25, out, 0, h, false);
+}
+int launch_conv5x5_u8_bytes_rows(cudaStream_t st, int h, int w, int scale, const unsigned char* img, const int* k25,
+                                 unsigned char* out, int lo, int hi) {
+    if (lo < 0 || hi > h || lo > hi) return (int)cudaErrorInvalidValue;
+    return conv_u8_bytes_rows(st, h, w, scale, img, k25, out, lo, hi, true);
+}
+bool conv5x5_u8_bytes_rows_ok(int h, int w, int scale, const int* k25) {
+    return h > 0 && conv_u8_bytes_rows(nullptr, h, w, scale, nullptr, k25, nullptr, 0, h, true, true) == 0;
+}
+static int conv_u8_bytes_rows(cudaStream_t st, int h, int w, int scale, const unsigned char* img, const int* k25,
+                              unsigned char* out, int lo, int hi, bool rows_only, bool probe) {
+    if (h <= 0 || w <= 0 || hi <= lo) return probe ? (int)cudaErrorNotSupported : 0;
     bool small = true;
     for (int t = 0; t < 25; t++) small &= (k25[t] >= -657 && k25[t] <= 657);
     if (!small || w % 4 != 0 || (uintptr_t)img % 4 != 0 || (uintptr_t)out % 4 != 0)
-        return launch_conv5x5_u8_bytes_dp4a(st, h, w, scale, img, k25, out);
+        return rows_only ? (int)cudaErrorNotSupported : launch_conv5x5_u8_bytes_dp4a(st, h, w, scale, img, k25, out);
     StencilArgs a = {};
     for (int t = 0; t < 25; t++) {
         a.kf[t] = (float)k25[t];
@@ -1557,33 +1610,37 @@ int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsi
 #endif
         const bool n16 = np_max == 16 && w % 16 == 0 && (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0;
         const int np = n16 ? 16 : 8;
-        dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
+        dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (hi - lo + S_BAND - 1) / S_BAND);
         const bool sym = sa.u[0] == sa.u[4] && sa.u[1] == sa.u[3] && sa.v[0] == sa.v[4] && sa.v[1] == sa.v[3];
+        if (probe) return 0;
         if (n16 && sym && sa.shift == 8)
-            stencil_bytes_swar_kernel<16, true, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
-        else if (n16 && sym) stencil_bytes_swar_kernel<16, false, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
-        else if (n16 && sa.shift == 8) stencil_bytes_swar_kernel<16, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
-        else if (n16) stencil_bytes_swar_kernel<16, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
-        else if (sa.shift == 8) stencil_bytes_swar_kernel<8, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
-        else stencil_bytes_swar_kernel<8, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, sa);
+            swar_go<SwarArgs>(stencil_bytes_swar_kernel<16, true, true>, stencil_bytes_swar_rows_kernel<16, true, true>, g, st, rows_only, h, w, img, out, sa, lo, hi);
+        else if (n16 && sym) swar_go<SwarArgs>(stencil_bytes_swar_kernel<16, false, true>, stencil_bytes_swar_rows_kernel<16, false, true>, g, st, rows_only, h, w, img, out, sa, lo, hi);
+        else if (n16 && sa.shift == 8) swar_go<SwarArgs>(stencil_bytes_swar_kernel<16, true>, stencil_bytes_swar_rows_kernel<16, true>, g, st, rows_only, h, w, img, out, sa, lo, hi);
+        else if (n16) swar_go<SwarArgs>(stencil_bytes_swar_kernel<16, false>, stencil_bytes_swar_rows_kernel<16, false>, g, st, rows_only, h, w, img, out, sa, lo, hi);
+        else if (sa.shift == 8) swar_go<SwarArgs>(stencil_bytes_swar_kernel<8, true>, stencil_bytes_swar_rows_kernel<8, true>, g, st, rows_only, h, w, img, out, sa, lo, hi);
+        else swar_go<SwarArgs>(stencil_bytes_swar_kernel<8, false>, stencil_bytes_swar_rows_kernel<8, false>, g, st, rows_only, h, w, img, out, sa, lo, hi);
     } else if (!sep && w % 8 == 0 && (uintptr_t)img % 8 == 0 && (uintptr_t)out % 8 == 0 &&
                swar2d_args(k25, scale, s2)) {
         const bool n16 = w % 16 == 0 && (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0;
         const int np = n16 ? 16 : 8;
-        dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (h + S_BAND - 1) / S_BAND);
+        dim3 g(((w + 32 * np - 1) / (32 * np) + S_WARPS - 1) / S_WARPS, (hi - lo + S_BAND - 1) / S_BAND);
+        if (probe) return 0;
         const bool sym = mirror_symmetric(k25);
         if (n16 && sym && dia && s2.shift == 0)
-            stencil_bytes_swar2d_kernel<16, true, true, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+            swar_go<Swar2dArgs>(stencil_bytes_swar2d_kernel<16, true, true, true>, stencil_bytes_swar2d_rows_kernel<16, true, true, true>, g, st, rows_only, h, w, img, out, s2, lo, hi);
         else if (n16 && sym && dia)
-            stencil_bytes_swar2d_kernel<16, true, false, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+            swar_go<Swar2dArgs>(stencil_bytes_swar2d_kernel<16, true, false, true>, stencil_bytes_swar2d_rows_kernel<16, true, false, true>, g, st, rows_only, h, w, img, out, s2, lo, hi);
         else if (n16 && sym)
-            stencil_bytes_swar2d_kernel<16, false, false, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+            swar_go<Swar2dArgs>(stencil_bytes_swar2d_kernel<16, false, false, true>, stencil_bytes_swar2d_rows_kernel<16, false, false, true>, g, st, rows_only, h, w, img, out, s2, lo, hi);
         else if (n16 && dia && s2.shift == 0)
-            stencil_bytes_swar2d_kernel<16, true, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
-        else if (n16 && dia) stencil_bytes_swar2d_kernel<16, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
-        else if (n16) stencil_bytes_swar2d_kernel<16, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
-        else if (dia) stencil_bytes_swar2d_kernel<8, true><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
-        else stencil_bytes_swar2d_kernel<8, false><<<g, 32 * S_WARPS, 0, st>>>(h, w, img, out, s2);
+            swar_go<Swar2dArgs>(stencil_bytes_swar2d_kernel<16, true, true>, stencil_bytes_swar2d_rows_kernel<16, true, true>, g, st, rows_only, h, w, img, out, s2, lo, hi);
+        else if (n16 && dia) swar_go<Swar2dArgs>(stencil_bytes_swar2d_kernel<16, true>, stencil_bytes_swar2d_rows_kernel<16, true>, g, st, rows_only, h, w, img, out, s2, lo, hi);
+        else if (n16) swar_go<Swar2dArgs>(stencil_bytes_swar2d_kernel<16, false>, stencil_bytes_swar2d_rows_kernel<16, false>, g, st, rows_only, h, w, img, out, s2, lo, hi);
+        else if (dia) swar_go<Swar2dArgs>(stencil_bytes_swar2d_kernel<8, true>, stencil_bytes_swar2d_rows_kernel<8, true>, g, st, rows_only, h, w, img, out, s2, lo, hi);
+        else swar_go<Swar2dArgs>(stencil_bytes_swar2d_kernel<8, false>, stencil_bytes_swar2d_rows_kernel<8, false>, g, st, rows_only, h, w, img, out, s2, lo, hi);
+    } else if (rows_only) {
+        return (int)cudaErrorNotSupported;
     } else if (sep && a.shift >= 0) stencil_bytes_kernel<true, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (sep) stencil_bytes_kernel<false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);
     else if (dia && a.shift >= 0) stencil_bytes_kernel<true, false, true><<<grid, 32 * S_WARPS, 0, st>>>(h, w, img, out, a);

@@ -73,6 +73,10 @@ int launch_conv5x5_u8(cudaStream_t st, int h, int w, int scale, const int* img, 
                       int* out);
 int launch_conv5x5_u8_bytes(cudaStream_t st, int h, int w, int scale, const unsigned char* img,
                             const int* k25, unsigned char* out);
+// output rows [lo, hi) of the h-row image, when a SWAR kernel applies (cudaErrorNotSupported otherwise)
+int launch_conv5x5_u8_bytes_rows(cudaStream_t st, int h, int w, int scale, const unsigned char* img, const int* k25,
+                                 unsigned char* out, int lo, int hi);
+bool conv5x5_u8_bytes_rows_ok(int h, int w, int scale, const int* k25);
 // band-sharded sweeps (k_stencil.cu): rows -2, -1 / h, h + 1 of the band through top / bot
 int launch_conv5x5_u8_band(cudaStream_t st, int h, int w, int scale, const int* img, const int* const* top,
                            const int* const* bot, const int* k25, int* out);

@@ -609,7 +609,9 @@ int spmv_common(int mode, int nrows, int ncols, int nnz, int* rowptr, int* col, 
 // stream while later blocks upload — the two PCIe directions overlap instead of one after the other.
 // fp32 copies back only the interior rectangle (rows / columns 2 .. n-3), as the whole-image call.
 // Pageable outputs come back through the staging ring after the last block (one pool of host
-// threads serves both directions).  Taken for images of 64 MB and more with w % 4 == 0 on host arrays.
+// threads serves both directions).  Taken for images of 64 MB and more with w % 4 == 0 on host arrays
+// (packed bytes: when a SWAR kernel applies — its row-block form reads the rows around the block
+// from the resident image as the whole-image sweep does).
 #define STENCIL_PIPE_BLOCKS 8
 constexpr long long STENCIL_PIPE_MIN = 64ll << 20;
 template <typename T, typename L>
@@ -641,7 +643,6 @@ int stencil_pipelined(int h, int w, bool f32, const T* img, T* out, L launch_blo
     const size_t col0 = f32 ? 2 : 0, ncol = f32 ? (size_t)w - 4 : (size_t)w;
     g_h2d = (long long)(sizeof(T) * n);
     g_d2h = (long long)(sizeof(T) * ncol * (size_t)(ohi - olo));
-    auto rowp = [&](T* base, int i) { return base + (size_t)(i < 0 ? 0 : (i > h - 1 ? h - 1 : i)) * w; };
     int nb = 0;
     for (int r0 = 0; r0 < h; r0 += rows) nb++;
     for (int b = 0; b < nb; b++) {  // uploads, in order on the copy stream
@@ -655,9 +656,7 @@ int stencil_pipelined(int h, int w, bool f32, const T* img, T* out, L launch_blo
         // block b-1 can run: its rows and the two below it have landed
         const int q0 = (b - 1) * rows, q1 = std::min(h, q0 + rows);
         CK(cudaStreamWaitEvent(s1, pc->ev_blk[b], 0));
-        const T* top[2] = {rowp(dIn, q0 - 2), rowp(dIn, q0 - 1)};
-        const T* bot[2] = {rowp(dIn, q1), rowp(dIn, q1 + 1)};
-        int e = launch_block(s1, q0, q1, dIn + (size_t)q0 * w, top, bot, dOut + (size_t)q0 * w);
+        int e = launch_block(s1, q0, q1, (const T*)dIn, dOut);
         if (e) return cuda_fail((cudaError_t)e, "stencil launch");
         if (out_staged) continue;
         const int o0 = std::max(q0, olo), o1 = std::min(q1, ohi);
@@ -670,9 +669,7 @@ int stencil_pipelined(int h, int w, bool f32, const T* img, T* out, L launch_blo
     {  // the last block
         const int q0 = (nb - 1) * rows, q1 = h;
         CK(cudaStreamWaitEvent(s1, pc->ev_blk[nb - 1], 0));
-        const T* top[2] = {rowp(dIn, q0 - 2), rowp(dIn, q0 - 1)};
-        const T* bot[2] = {rowp(dIn, q1), rowp(dIn, q1 + 1)};
-        int e = launch_block(s1, q0, q1, dIn + (size_t)q0 * w, top, bot, dOut + (size_t)q0 * w);
+        int e = launch_block(s1, q0, q1, (const T*)dIn, dOut);
         if (e) return cuda_fail((cudaError_t)e, "stencil launch");
         const int o0 = std::max(q0, olo), o1 = std::min(q1, ohi);
         if (!out_staged && o1 > o0) {
@@ -688,6 +685,13 @@ int stencil_pipelined(int h, int w, bool f32, const T* img, T* out, L launch_blo
     release.f();
     release.f = [] {};
     return collect_faults(c, s0) == PENCIL_OK ? ok() : g_status;
+}
+
+// the band sweep's row pointers for rows [q0, q1) of a resident h-row image (clamped at its edges)
+template <typename T>
+void band_rows(const T* img, int h, int w, int q0, int q1, const T* (&top)[2], const T* (&bot)[2]) {
+    auto rowp = [&](int i) { return img + (size_t)(i < 0 ? 0 : (i > h - 1 ? h - 1 : i)) * w; };
+    top[0] = rowp(q0 - 2), top[1] = rowp(q0 - 1), bot[0] = rowp(q1), bot[1] = rowp(q1 + 1);
 }
 
 bool stencil_pipe_ok(int h, int w, size_t elem, const void* img, const void* out) {
@@ -801,11 +805,12 @@ void conv5x5_u8(int h, int w, int scale, int* img, int* k, int* out) {
         memcpy(taps, k, sizeof taps);
     }
     if (stencil_pipe_ok(h, w, sizeof(int), img, out)) {
-        stencil_pipelined<int>(h, w, false, img, out,
-                               [&](cudaStream_t s, int q0, int q1, const int* bi, const int* const* top,
-                                   const int* const* bot, int* bo) {
-                                   return launch_conv5x5_u8_band(s, q1 - q0, w, scale, bi, top, bot, taps, bo);
-                               });
+        stencil_pipelined<int>(h, w, false, img, out, [&](cudaStream_t s, int q0, int q1, const int* di, int* dout) {
+            const int *top[2], *bot[2];
+            band_rows(di, h, w, q0, q1, top, bot);
+            return launch_conv5x5_u8_band(s, q1 - q0, w, scale, di + (size_t)q0 * w, top, bot, taps,
+                                          dout + (size_t)q0 * w);
+        });
         return;
     }
     Stage st[2];
@@ -831,6 +836,11 @@ extern "C" int pencil_conv5x5_u8_bytes(int h, int w, int scale, const uint8_t* i
     } else {
         memcpy(taps, k, sizeof taps);
     }
+    if (stencil_pipe_ok(h, w, 1, img, out) && conv5x5_u8_bytes_rows_ok(h, w, scale, taps))  // row blocks
+        return stencil_pipelined<uint8_t>(h, w, false, img, out, [&](cudaStream_t s, int q0, int q1,
+                                                                     const uint8_t* di, uint8_t* dout) {
+            return launch_conv5x5_u8_bytes_rows(s, h, w, scale, di, taps, dout, q0, q1);
+        });
     Stage st[2];
     st[0] = {(void*)img, nullptr, nz((long long)h * w), IN};
     st[1] = {out, nullptr, nz((long long)h * w), OUT};
@@ -853,13 +863,15 @@ void conv5x5_f32(int h, int w, float* img, float* k, float* out) {
         memcpy(taps, k, sizeof taps);
     }
     if (stencil_pipe_ok(h, w, sizeof(float), img, out)) {
-        stencil_pipelined<float>(h, w, true, img, out,
-                                 [&](cudaStream_t s, int q0, int q1, const float* bi, const float* const* top,
-                                     const float* const* bot, float* bo) {
-                                     const int lo = std::max(q0, 2) - q0, hi = std::min(q1, h - 2) - q0;
-                                     if (hi <= lo) return 0;
-                                     return launch_conv5x5_f32_band(s, q1 - q0, w, lo, hi, bi, top, bot, taps, bo);
-                                 });
+        stencil_pipelined<float>(h, w, true, img, out, [&](cudaStream_t s, int q0, int q1, const float* di,
+                                                           float* dout) {
+            const int lo = std::max(q0, 2) - q0, hi = std::min(q1, h - 2) - q0;
+            if (hi <= lo) return 0;
+            const float *top[2], *bot[2];
+            band_rows(di, h, w, q0, q1, top, bot);
+            return launch_conv5x5_f32_band(s, q1 - q0, w, lo, hi, di + (size_t)q0 * w, top, bot, taps,
+                                           dout + (size_t)q0 * w);
+        });
         return;
     }
     Stage st[2];

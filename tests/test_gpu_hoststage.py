@@ -163,3 +163,26 @@ def test_stencil_dropins_pipelined_equal_device_api(cuda, pinned):
         assert np.array_equal(got.view(np.uint32), dev.cpu().numpy().view(np.uint32))
         o = got.reshape(h, w)
         assert np.isnan(o[:2]).all() and np.isnan(o[-2:]).all() and np.isnan(o[:, :2]).all() and np.isnan(o[:, -2:]).all()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_bytes_stencil_pipelined_equals_device_api(cuda, pinned):
+    """pencil_conv5x5_u8_bytes on host arrays of 64 MB and more runs the SWAR kernels by row blocks
+    (output rows [q0, q1) of the resident image): bit-identical to the whole-image device call —
+    separable and signed / symmetric and skewed taps, 16- and 8-pixel lanes (w % 16 != 0), a ragged
+    last block; taps without a SWAR form take the whole-image path."""
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    host = (lambda a: torch.from_numpy(a).pin_memory()) if pinned else (lambda a: a)
+    skew = np.outer([1, 3, 5, 2, 0], [2, 1, 4, 6, 3]).astype(np.int32).reshape(-1)
+    asym = np.array([[0, 0, -1, 0, 0], [0, -2, -1, -3, 0], [-1, -3, 20, -2, 0],
+                     [0, -1, -2, 0, 0], [0, 0, -4, 0, 0]], np.int32).reshape(-1)
+    for h, w in ((8195, 8192), (8193, 8200)):
+        img8 = synth.u8_i32(h * w, seed=h + w).astype(np.uint8)
+        for k, scale in ((synth.BINOMIAL, 256), (synth.SHARPEN, 1), (skew, 256), (asym, 2), (synth.BINOMIAL * 40, 9)):
+            dev = torch.empty(h * w, dtype=torch.uint8, device="cuda")
+            pb.device.conv5x5_u8_bytes(h, w, scale, torch.from_numpy(img8).cuda(), k, dev)
+            out = host(np.zeros(h * w, np.uint8))
+            pb.dropin.conv5x5_u8_bytes(h, w, scale, host(img8), k, out)
+            got = out.numpy() if pinned else out
+            assert np.array_equal(got, dev.cpu().numpy()), (h, w, scale, int(k[12]))
