@@ -694,6 +694,60 @@ void band_rows(const T* img, int h, int w, int q0, int q1, const T* (&top)[2], c
     top[0] = rowp(q0 - 2), top[1] = rowp(q0 - 1), bot[0] = rowp(q1), bot[1] = rowp(q1 + 1);
 }
 
+// Drop-in axpy on host arrays of 64 MB and more, pipelined by chunks: chunk b of x and y uploads on the
+// copy stream, its axpy runs on the compute stream, its y downloads on the D2H stream under the next
+// chunks' uploads (pageable y: one staged download at the end).
+int axpy_pipelined(long long n, float a, const float* x, float* y) {
+    DeviceCtx* c = nullptr;
+    int r = get_ctx(&c);
+    if (r) return r;
+    std::lock_guard<std::mutex> lk(c->mu);
+    PipeCtx* pc = nullptr;
+    if ((r = get_pipe(c, &pc))) return r;
+    cudaStream_t s0 = c->stream, s1 = pc->comp, s2 = pc->d2h;
+    float *dx = nullptr, *dy = nullptr;
+    struct Release {
+        std::function<void()> f;
+        ~Release() { f(); }
+    } release{[&]() {
+        cudaStreamSynchronize(s1);
+        cudaStreamSynchronize(s2);
+        pool_free(s0, dx);
+        pool_free(s0, dy);
+        cudaStreamSynchronize(s0);
+    }};
+    if ((r = pool_alloc(c, s0, sizeof(float) * n, (void**)&dx)) || (r = pool_alloc(c, s0, sizeof(float) * n, (void**)&dy)))
+        return r;
+    const bool y_staged = staged(y, sizeof(float) * n);
+    auto up = [&](float* d, const float* hp, size_t bytes) -> cudaError_t {
+        return staged(hp, bytes) ? (cudaError_t)staged_h2d_2d(c->device, d, bytes, hp, bytes, bytes, 1, s0)
+                                 : cudaMemcpyAsync(d, hp, bytes, cudaMemcpyHostToDevice, s0);
+    };
+    g_h2d = (long long)(2 * sizeof(float) * n);
+    g_d2h = (long long)(sizeof(float) * n);
+    const int K = STENCIL_PIPE_BLOCKS;
+    const long long chunk = ((n + K - 1) / K + 3) / 4 * 4;  // float4-aligned chunk starts
+    int b = 0;
+    for (long long o = 0; o < n; o += chunk, b++) {
+        const long long len = std::min(chunk, n - o);
+        CK(up(dx + o, x + o, sizeof(float) * len));
+        CK(up(dy + o, y + o, sizeof(float) * len));
+        CK(cudaEventRecord(pc->ev_blk[b], s0));
+        CK(cudaStreamWaitEvent(s1, pc->ev_blk[b], 0));
+        const int e = launch_axpy(s1, len, a, nullptr, dx + o, dy + o);
+        if (e) return cuda_fail((cudaError_t)e, "axpy launch");
+        if (y_staged) continue;
+        CK(cudaEventRecord(pc->ev_chunk[b], s1));
+        CK(cudaStreamWaitEvent(s2, pc->ev_chunk[b], 0));
+        CK(cudaMemcpyAsync(y + o, dy + o, sizeof(float) * len, cudaMemcpyDeviceToHost, s2));
+    }
+    if (y_staged)
+        CK((cudaError_t)staged_d2h_2d(c->device, y, sizeof(float) * n, dy, sizeof(float) * n, sizeof(float) * n, 1, s1));
+    release.f();
+    release.f = [] {};
+    return collect_faults(c, s0) == PENCIL_OK ? ok() : g_status;
+}
+
 bool stencil_pipe_ok(int h, int w, size_t elem, const void* img, const void* out) {
     return (long long)h * w * (long long)elem >= STENCIL_PIPE_MIN && h >= 64 && w % 4 == 0 && img && out &&
            (uintptr_t)img % 16 == 0 && (uintptr_t)out % 16 == 0 && !is_device_ptr(img) && !is_device_ptr(out);
@@ -755,6 +809,10 @@ float dot(int n, float* x, float* y) {
 void axpy(int n, float a, float* x, float* y) {
     if (n < 0) { fail(PENCIL_E_ARG, "negative extent"); return; }
     if (n == 0) { ok(); return; }
+    if ((long long)n * 4 >= STENCIL_PIPE_MIN && x && y && !is_device_ptr(x) && !is_device_ptr(y)) {
+        axpy_pipelined(n, a, x, y);
+        return;
+    }
     Stage st[2];
     st[0] = {x, nullptr, sizeof(float) * nz(n), IN};
     st[1] = {y, nullptr, sizeof(float) * nz(n), INOUT};

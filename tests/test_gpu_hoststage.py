@@ -186,3 +186,20 @@ def test_bytes_stencil_pipelined_equals_device_api(cuda, pinned):
             pb.dropin.conv5x5_u8_bytes(h, w, scale, host(img8), k, out)
             got = out.numpy() if pinned else out
             assert np.array_equal(got, dev.cpu().numpy()), (h, w, scale, int(k[12]))
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_axpy_pipelined_equals_emitted_c(cuda, pinned):
+    """axpy on host arrays of 64 MB and more runs in chunks (upload / axpy / download overlapping):
+    y bit-identical to the emitted C's a * x + y, ragged last chunk (n not a multiple of 4)."""
+    import oracle
+    import paper_1302_5586_b200 as pb
+    torch = cuda
+    n = (1 << 24) + 3
+    x, y0 = synth.f32(n, 51), synth.f32(n, 52)
+    ref = oracle.axpy_f32(n, np.float32(1.7), x, y0)
+    host = (lambda a: torch.from_numpy(a).pin_memory()) if pinned else (lambda a: a)
+    y = host(y0.copy())
+    pb.dropin.axpy(n, 1.7, host(x), y)
+    got = y.numpy() if pinned else y
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
