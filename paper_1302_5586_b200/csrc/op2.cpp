@@ -41,6 +41,15 @@
 #include "mini_json.hpp"
 #include "pencil_front.hpp"
 
+// hoststage.cpp: pageable host arrays of OP2_STAGE_MIN bytes and more go through the library's
+// multi-threaded pinned staging ring (as the drop-in calls' do)
+bool host_is_pageable(const void* p);
+int staged_h2d_2d(int device, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                  cudaStream_t st);
+int staged_d2h_2d(int device, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                  cudaStream_t st);
+constexpr size_t OP2_STAGE_MIN = 4u << 20;
+
 int pencil_internal_fail(int status, const char* msg);  // runtime.cpp
 int pencil_internal_ok();                                // runtime.cpp
 
@@ -808,7 +817,13 @@ int pencil_op2_get_dat(pencil_op2_t M, const char* dat, long long* out, long lon
     if (n != (long long)d.size()) return fail(PENCIL_E_ARG, "E-ARG: dat size mismatch");
     if (M->stream) {
         OCK(cudaStreamSynchronize(M->stream));
-        if (n) OCK(cudaMemcpy(out, M->d_dat[di], (size_t)n * 8, cudaMemcpyDeviceToHost));
+        const size_t bytes = (size_t)n * 8;
+        if (n && bytes >= OP2_STAGE_MIN && host_is_pageable(out)) {  // the multi-threaded staging ring
+            OCK((cudaError_t)staged_d2h_2d(M->device, out, bytes, M->d_dat[di], bytes, bytes, 1, M->stream));
+            OCK(cudaStreamSynchronize(M->stream));
+        } else if (n) {
+            OCK(cudaMemcpy(out, M->d_dat[di], bytes, cudaMemcpyDeviceToHost));
+        }
     } else if (n) {
         memcpy(out, d.data(), (size_t)n * 8);
     }
@@ -821,11 +836,19 @@ int pencil_op2_set_dat(pencil_op2_t M, const char* dat, const long long* in, lon
     if (di < 0) return fail(PENCIL_E_ARG, std::string("E-ARG: no dat named '") + dat + "'");
     auto& d = M->m.dats[di].data;
     if (n != (long long)d.size()) return fail(PENCIL_E_ARG, "E-ARG: dat size mismatch");
-    if (n) memcpy(d.data(), in, (size_t)n * 8);
-    if (M->stream) {
-        OCK(cudaStreamSynchronize(M->stream));
-        if (n) OCK(cudaMemcpy(M->d_dat[di], in, (size_t)n * 8, cudaMemcpyHostToDevice));
+    if (!M->stream) {  // before prepare: the host copy is what the device setup uploads
+        if (n) memcpy(d.data(), in, (size_t)n * 8);
+        return pencil_internal_ok();
     }
+    // on the device the device copy is the dat (the host copy is stale from the first run on)
+    M->host_stale = true;
+    OCK(cudaStreamSynchronize(M->stream));
+    const size_t bytes = (size_t)n * 8;
+    if (n && bytes >= OP2_STAGE_MIN && host_is_pageable(in))  // the multi-threaded staging ring
+        OCK((cudaError_t)staged_h2d_2d(M->device, M->d_dat[di], bytes, in, bytes, bytes, 1, M->stream));
+    else if (n)
+        OCK(cudaMemcpyAsync(M->d_dat[di], in, bytes, cudaMemcpyHostToDevice, M->stream));
+    OCK(cudaStreamSynchronize(M->stream));
     return pencil_internal_ok();
 }
 

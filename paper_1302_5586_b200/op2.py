@@ -70,11 +70,15 @@ class Op2Model:
         return self._lib.pencil_op2_stream(self._h)
 
     # -- data --------------------------------------------------------------------------------
-    def dat(self, name):
+    def dat(self, name, out=None):
+        """The dat's values (int64); `out`: an int64 array of the dat's size to fill instead of a new one."""
         n = self._lib.pencil_op2_dat_size(self._h, name.encode())
         if n < 0:
             raise KeyError(name)
-        out = np.empty(n, np.int64)
+        if out is None:
+            out = np.empty(n, np.int64)
+        elif out.dtype != np.int64 or out.size != n or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError("out must be a contiguous int64 array of the dat's size")
         self._lib.pencil_op2_get_dat(self._h, name.encode(), out.ctypes.data, n)
         check_status()
         return out

@@ -269,6 +269,16 @@ def test_full_size_mesh_increments_vs_numpy(cuda):
     m.run()
     ref = op2_ref.mesh_increment_numpy(cells, dedges, table)
     assert np.array_equal(m.dat("dcells"), ref)
+    # dats of 4 MB and more set / read through the staging ring on the device side, into a reused array
+    d2 = dedges[::-1].copy()
+    m.set_dat("dcells", cells)
+    m.set_dat("dedges", d2)
+    m.run()
+    out = np.full(nc, 7, np.int64)
+    assert m.dat("dcells", out=out) is out
+    assert np.array_equal(out, op2_ref.mesh_increment_numpy(cells, d2, table))
+    with pytest.raises(ValueError):
+        m.dat("dcells", out=np.empty(nc, np.int32))
 
 
 RANDOM = json.load(open(os.path.join(HERE, "golden", "op2_random.json")))
