@@ -352,7 +352,7 @@ def bw_line(ms, nbytes, hbm, kernel, **extra):
                  "roofline": roofline(gbs, hbm, "GB/s", kernel, nbytes)}, **extra)
 
 
-def e2e_calls(torch, pb, make_call, metric_amount, unit, api, reps=2):
+def e2e_calls(torch, pb, make_call, metric_amount, unit, api, reps=3):
     """The line's metric end to end through the library's public call on HOST arrays:
     make_call(pinned) returns a no-argument call that runs the whole operation on pinned
     (page-locked) or pageable (plain numpy) host buffers — H2D of the inputs, the kernel(s), D2H
