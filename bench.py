@@ -376,8 +376,8 @@ def e2e_calls(torch, pb, make_call, metric_amount, unit, api, reps=3):
                 lib.pencil_last_transfer_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
                 moved = (h2d.value, d2h.value)
             out[kind] = {"value": metric_amount / t / (1e9 if unit in ("GB/s", "Gpix/s") else 1e12),
-                         "unit": unit, "ms_per_call": t * 1e3, "h2d_bytes_per_step": int(moved[0]),
-                         "d2h_bytes_per_step": int(moved[1])}
+                         "unit": unit, "ms_per_call": t * 1e3, "ms_calls": [round(v * 1e3, 2) for v in ts],
+                         "h2d_bytes_per_step": int(moved[0]), "d2h_bytes_per_step": int(moved[1])}
         except Exception as e:  # noqa: BLE001 — one door's failure must not take the suite down
             out[kind] = {"unavailable": str(e)[:200]}
     if "value" in out.get("pinned", {}):
