@@ -30,9 +30,9 @@
 #include "kernels.h"
 
 #define SPMV_THREADS 256
-// non-zeros per warp tile (plan window); swept over {256..2048} x WCHUNK {64,128,256} at
-// 2^24 rows (tools/spmv_sweep.sh): 1024 x 128 is fastest (1.28 ms; 512: 1.34; 256: 1.59)
-#define SPMV_TILE_NNZ 1024
+// Plan windows: csr_tile_schedule (end of file).  Round 1's batch-and-fold executor swept
+// {256..2048} x WCHUNK {64,128,256} at 2^24 rows (tools/spmv_sweep.sh): 1024 x 128 was its best
+// (1.28 ms; 512: 1.34; 256: 1.59); the segmented executor runs 4096-non-zero windows.
 // Non-zeros per lane per window and CTAs per SM of the segmented executor, per mode (2^24 rows,
 // tools/ab_spmv_modes.sh): reassociated E 4 at 5 CTAs/SM (48 registers: the one-deep window
 // pipeline) 1.137 ms, E 8 at 4 1.188; source order E 8 at 4 CTAs/SM 1.256 ms, E 4 at 5 1.302
