@@ -1,3 +1,6 @@
+"""End-to-end timing of the pipelined host-array stencil drop-ins (conv5x5_u8 int32 / conv5x5_f32 at
+16384^2, pinned and after pageable staged calls) with the bytes each call moved — the check behind
+the bench lines' e2e numbers.  usage: python tools/e2e_stencil_probe.py"""
 import sys, os, time, ctypes
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
