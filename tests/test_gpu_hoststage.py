@@ -203,3 +203,21 @@ def test_axpy_pipelined_equals_emitted_c(cuda, pinned):
     pb.dropin.axpy(n, 1.7, host(x), y)
     got = y.numpy() if pinned else y
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+def test_f32_stencil_pipelined_tiny_pixels_across_block_edges(cuda):
+    """The pipelined fp32 stencil (row blocks of 513 rows at h = 4099) with pixels whose fused
+    power-of-two products would round (below 2^-126) straddling a block edge: each block's guard /
+    repair pass keeps the result as written — bit-identical to the emitted C, border untouched."""
+    import oracle
+    import paper_1302_5586_b200 as pb
+    h, w = 4099, 4100
+    binom = (synth.BINOMIAL.astype(np.float32) / 256.0).astype(np.float32)
+    img = synth.f32(h * w, seed=61).reshape(h, w)
+    img[505:522, 90:150] = (img[505:522, 90:150] * np.float32(2.0 ** -118)).astype(np.float32)  # rows 513 +- 8
+    img = img.reshape(-1)
+    o0 = synth.f32(h * w, seed=62)
+    out = o0.copy()
+    pb.dropin.conv5x5_f32(h, w, img, binom, out)
+    exact = oracle.conv5x5_f32_f32(h, w, img, binom, o0)
+    assert np.array_equal(out.view(np.uint32), exact.view(np.uint32))
