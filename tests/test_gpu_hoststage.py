@@ -145,6 +145,7 @@ def test_stencil_dropins_pipelined_equal_device_api(cuda, pinned):
     img = synth.u8_i32(h * w, seed=41)
     odd = img.copy()
     odd[h // 2 * w + 7] = 300  # not a byte: the exact repair pass
+    odd[2051 * w + 100] = -5   # ... and one in the rows both blocks around row 2052 read
     for im, k, scale in ((img, synth.BINOMIAL, 256), (img, synth.SHARPEN, 1), (odd, synth.BINOMIAL, 256),
                          (img, synth.BINOMIAL * 3, 7)):
         dev = torch.empty(h * w, dtype=torch.int32, device="cuda")
