@@ -879,6 +879,44 @@ def suite_dist(args, torch, pb, rank, world, dist, hbm):
         except Exception as e:  # noqa: BLE001
             out[name] = {"unavailable": str(e)[:200]}
 
+    # VOBLA chain sharded (SURVEY §8e gemv_t / dot / axpy rows): gemv_t over this rank's column block
+    # of the strided view (no collective), dot over its range of the 2^28 vectors + one all-reduce
+    # of the partial (NCCL on the device scalar), axpy over the range with that scalar
+    try:
+        m = n = lda = 16384
+        nv = 1 << 28
+        g = pd.ColShardedGemvT(m, n, rank, world, lda=lda, incx=2, incy=3)
+        A = torch.from_numpy(synth.f32(m * lda)).cuda()
+        xt = torch.from_numpy(synth.f32(m * 2, 42, m * lda)).cuda()
+        yt = torch.from_numpy(synth.f32(n * 3, 42, m * lda + 2 * m)).cuda()
+        Av, yv_t = g.views(A, yt)
+        lo, hi = pd.shard_range(nv, world, rank, align=4)
+        xv = torch.from_numpy(synth.f32(hi - lo, 7, lo)).cuda()  # elements lo .. hi of the same streams
+        yv = torch.from_numpy(synth.f32(hi - lo, 8, lo)).cuda()
+        r = torch.zeros(1, device="cuda")
+        nb = g.j1 - g.j0
+
+        def chain():
+            pb.device.gemv_t(m, nb, lda, 2, 3, 1.0, 0.0, Av, xt, yv_t)
+            pb.device.dot(hi - lo, xv, yv, r)
+            if world > 1 and dist.get_backend() == "nccl":
+                dist.all_reduce(r)
+            elif world > 1:
+                rc = r.cpu()
+                dist.all_reduce(rc)
+                r.copy_(rc)
+            pb.device.axpy_ptr(hi - lo, r, xv, yv)
+        ms = statistics.mean(run_steps(torch, chain, k, w, flush, dist))
+        bt, bd, ba = 4 * (m * n + m + n), 8 * nv, 12 * nv
+        mine = 4 * (m * nb + m + nb) + 20 * (hi - lo)
+        out["vobla_chain_ranks"] = dist_line(
+            torch, dist, ms, bt + bd + ba, "GB/s", hbm, "gemv_t_kernel + dot_kernel + axpy_kernel", mine,
+            {"split": "gemv_t column blocks of the strided view (%d columns here), dot / axpy ranges (%d elements), "
+                      "one all-reduce of the dot partial (%s)" % (nb, hi - lo, dist.get_backend())})
+        del A, xv, yv
+    except Exception as e:  # noqa: BLE001
+        out["vobla_chain_ranks"] = {"unavailable": str(e)[:200]}
+
     # gemv 8192^2 row-sharded: x all-gathered from its shards + the local rows, one CUDA graph
     try:
         m = n = 8192
