@@ -105,6 +105,9 @@ void par_copy(CopyPool& pool, char* dst, size_t dpitch, const char* src, size_t 
     });
 }
 
+// (Non-temporal stores for these copies — no read-for-ownership of the destination — measured the
+// same: spmv_vec / axpy / conv5x5_u8 pageable 47.6-47.9 / 49.3 / 48.6-49.4 GB/s either way,
+// tools/pageable_probe.py.)
 // pinned ring: 4 chunks of 32 MB per device.  (Pieces of 1/16 of a transfer, 4-32 MB, measured
 // worse: the pipelined SpMV's 70 MB chunks then go as 4 MB pieces and the per-piece dispatch and
 // event waits cost more than the earlier overlap gains — SpMV pageable e2e 45 -> 37 GB/s.)
