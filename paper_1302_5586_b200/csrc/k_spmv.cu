@@ -990,21 +990,25 @@ int launch_csr_generic(cudaStream_t st, int nrows, int ncols, int nnz_len, const
 
 // plan window per mode: source order (the batch-and-fold executor) and reassociated (segmented)
 #ifndef SEG_TILE_NNZ
-#define SEG_TILE_NNZ 4096
+#define SEG_TILE_NNZ 8192
 #endif
 #ifndef SEG_TAIL_TILE_NNZ
 #define SEG_TAIL_TILE_NNZ 1024  // 0: no tapered tail
 #endif
 #ifndef SEG_TAIL_WAVES
-#define SEG_TAIL_WAVES 0.5  // tail length in full-size tiles per warp of the launch
+#define SEG_TAIL_WAVES 0.25  // tail length in full-size tiles per warp of the launch
 #endif
 // Tickets are drawn in matrix order, so the warps that draw the last full-size tiles start them
-// up to one tile time before the end; the tail's smaller tiles (half a wave of the launch's warps
-// of work) keep the other warps busy meanwhile and end within a small tile of each other.
+// up to one tile time before the end; the tail's smaller tiles (a quarter of a wave of the launch's
+// warps of full-size tiles) keep the other warps busy meanwhile and end within a small tile of
+// each other.
 // Measured at 2^24 rows (tools/ab_spmv_modes.sh, two rounds): vec / inline 1.133 / 1.239 ms
 // without the tail, 1.129 / 1.233 with it (1024-nnz tail tiles, 0.5 wave); 1 wave 1.132 / 1.234,
 // 2 waves 1.139 / 1.238, 512-nnz tail tiles 1.141 / 1.241, 2048 1.132 / 1.234 — small: the
 // request path is shared per SM, so an SM stays busy until its last few warps run dry.
+// With the tail, larger full-size tiles pay (fewer tickets and window-pipeline restarts): 8192-nnz
+// tiles with a quarter wave of 1024-nnz tail tiles (the same tail length) 1.110 / 1.215 ms against
+// 1.116 / 1.224 for 4096 (16384: 1.112 / 1.219; 2048: 1.129 / 1.240; 2048-nnz tail tiles 1.113 / 1.218).
 TileSchedule csr_tile_schedule(int mode, int nnz_len) {
     TileSchedule ts;
     const long long nnz = nnz_len > 0 ? nnz_len : 0;

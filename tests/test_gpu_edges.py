@@ -401,10 +401,11 @@ def test_spmv_empty_rows_take_the_segmented_executor(cuda, every):
 
 @pytest.mark.parametrize("mode", [0, 1])
 def test_spmv_tapered_tiles_across_the_tail_start(cuda, mode):
-    """The plan cuts 4096-non-zero tiles, then 1024-non-zero ones for the last half wave of the
-    launch's warps: a 16 M non-zero matrix has both, with long rows (and empty rows) straddling
-    the switch; source order bit-identical to the emitted C's fp32 chain, reassociated within the
-    normwise bound, tile count as the schedule states."""
+    """The plan cuts full-size tiles (TILE non-zeros), then 1024-non-zero ones for the last quarter
+    wave of the launch's warps (k_spmv.cu csr_tile_schedule): a 16 M non-zero matrix has both, with
+    long rows (and empty rows) straddling the switch; source order bit-identical to the emitted C's
+    fp32 chain, reassociated within the normwise bound, tile count as the schedule states."""
+    TILE, WAVES = 8192, 0.25
     import paper_1302_5586_b200 as pb
     torch = cuda
     rng = np.random.default_rng(23)
@@ -413,7 +414,8 @@ def test_spmv_tapered_tiles_across_the_tail_start(cuda, mode):
     rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     # long rows and an empty row wherever the tail may start (either mode's launch width)
     warps = 148 * (5 if mode else 4) * 8
-    start = (int(rowptr[-1]) - warps * 4096 // 2) // 4096 * 4096
+    tail = int(WAVES * warps * TILE)
+    start = (int(rowptr[-1]) - tail) // TILE * TILE
     r = int(np.searchsorted(rowptr, start))
     lens[r - 1:r - 1] = [9000, 0, 4097, 1025, 1]
     rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
@@ -423,9 +425,8 @@ def test_spmv_tapered_tiles_across_the_tail_start(cuda, mode):
     rp = torch.from_numpy(rowptr).cuda()
     plan = pb.device.CsrPlan(nrows, ncols, nnz, rp, mode=mode)
     nt, tn = plan.info()
-    tail = warps * 4096 // 2
-    s0 = max(0, nnz - tail) // 4096 * 4096
-    assert tn == 4096 and nt == s0 // 4096 + (nnz - s0 + 1023) // 1024
+    s0 = max(0, nnz - tail) // TILE * TILE
+    assert tn == TILE and nt == s0 // TILE + (nnz - s0 + 1023) // 1024
     y = torch.full((nrows,), 7.0, device="cuda")
     plan.spmv(rp, torch.from_numpy(col).cuda(), torch.from_numpy(val).cuda(), torch.from_numpy(x).cuda(), y)
     pb.device.sync_status()
