@@ -420,7 +420,8 @@ __device__ __forceinline__ void stencil_step(int w, int i, int c, int lane, int 
 #ifndef STENCIL_U8_MINB
 #define STENCIL_U8_MINB 4
 #endif
-#ifndef STENCIL_SEP_MINB  // swept 4/5/6/8 at 16384^2: int32 0.374/0.374/0.376/0.378 ms, bytes 0.258/0.258/0.262/0.279
+#ifndef STENCIL_SEP_MINB  // swept 4/5/6/8 at 16384^2: int32 0.374/0.374/0.376/0.378 ms, bytes 0.258/0.258/0.262/0.279;
+                          // again at 32-row bands (round 2): 4/5/6 0.355/0.355/0.361 ms
 #define STENCIL_SEP_MINB 4
 #endif
 template <bool U8, bool POW2, bool SEP = false, bool DIA = false, int PF = 0>
