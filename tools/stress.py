@@ -2,7 +2,9 @@
 long rows, ragged sizes) through both SpMV modes and the drop-in, random stencil shapes / taps
 through every kernel family (int32 storage, packed bytes, fp32), random gemm shapes — each against
 the oracle (bit-exact where the contract is, normwise 1e-5 otherwise) until the time budget runs out.
-usage: python tools/stress.py [seconds]"""
+--large: host-array sizes that take the pipelined drop-ins (SpMV >= 4 M non-zeros, stencils and
+axpy >= 64 MB), fewer cases.
+usage: python tools/stress.py [seconds] [--large]"""
 import os
 import sys
 import time
@@ -17,7 +19,8 @@ import paper_1302_5586_b200 as pb  # noqa: E402
 from conftest import normwise_err  # noqa: E402
 from paper_1302_5586_b200 import synth  # noqa: E402
 
-budget = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
+budget = float(sys.argv[1]) if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else 240.0
+LARGE = "--large" in sys.argv
 t_end = time.time() + budget
 rng = np.random.default_rng(int(time.time()) & 0xffff)
 counts = {"spmv": 0, "conv_u8": 0, "conv_bytes": 0, "conv_f32": 0, "gemm": 0}
@@ -25,8 +28,8 @@ fails = []
 
 
 def spmv_case():
-    nrows = int(rng.integers(1, 300_000))
-    ncols = int(rng.integers(1, 200_000))
+    nrows = int(rng.integers(300_000, 2_000_000)) if LARGE else int(rng.integers(1, 300_000))
+    ncols = int(rng.integers(1, 2_000_000 if LARGE else 200_000))
     lens = rng.integers(0, 40, nrows)
     if rng.random() < 0.5:
         lens[rng.integers(0, nrows, 3)] = rng.integers(0, 20_000, 3)  # long rows
@@ -73,9 +76,14 @@ def taps_case():
 
 
 def conv_case():
-    h, w = int(rng.integers(1, 700)), int(rng.integers(1, 1500))
-    if rng.random() < 0.5:
-        w = (w // 16 + 1) * 16
+    if LARGE:  # >= 64 MB of int32 / fp32 (and of bytes for the larger ones): the pipelined drop-ins
+        h, w = int(rng.integers(4100, 9000)), int(rng.integers(4100, 9000)) // 4 * 4
+        if rng.random() < 0.5:
+            w = w // 16 * 16
+    else:
+        h, w = int(rng.integers(1, 700)), int(rng.integers(1, 1500))
+        if rng.random() < 0.5:
+            w = (w // 16 + 1) * 16
     img = synth.u8_i32(h * w, int(rng.integers(1, 1 << 30)))
     k = taps_case()
     scale = int(rng.choice([1, 2, 4, 16, 256, 3, 7, 1000]))
@@ -102,6 +110,18 @@ def conv_case():
         counts["conv_f32"] += 1
 
 
+def axpy_case():
+    n = int(rng.integers(1 << 24, 1 << 26))
+    x, y = synth.f32(n, int(rng.integers(1, 1 << 30))), synth.f32(n, int(rng.integers(1, 1 << 30)))
+    a = np.float32(rng.normal())
+    ref = oracle.axpy_f32(n, a, x, y)
+    yy = y.copy()
+    pb.dropin.axpy(n, float(a), x, yy)
+    if not np.array_equal(yy.view(np.uint32), ref.view(np.uint32)):
+        fails.append(("axpy", n))
+    counts["axpy"] = counts.get("axpy", 0) + 1
+
+
 def gemm_case():
     m, n, k = (int(v) for v in rng.integers(1, 700, 3))
     A, B, C = synth.f32(m * k, 1), synth.f32(k * n, 2), synth.f32(m * n, 3)
@@ -118,6 +138,9 @@ def gemm_case():
 while time.time() < t_end and not fails:
     spmv_case()
     conv_case()
-    gemm_case()
+    if LARGE:
+        axpy_case()
+    else:
+        gemm_case()
 print("cases", counts, "fails", fails[:5], flush=True)
 sys.exit(1 if fails else 0)
