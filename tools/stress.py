@@ -122,6 +122,34 @@ def axpy_case():
     counts["axpy"] = counts.get("axpy", 0) + 1
 
 
+def blas_case():
+    m, n = int(rng.integers(1, 3000)), int(rng.integers(1, 3000))
+    lda = n + int(rng.integers(0, 9))
+    incx, incy = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+    A = synth.f32(m * lda, int(rng.integers(1, 1 << 30)))
+    alpha, beta = float(rng.choice([1.0, -0.5, 2.0])), float(rng.choice([0.0, 1.0, 0.5]))
+    x, y = synth.f32(n, 3), synth.f32(m, 4)
+    ref = oracle.gemv(m, n, alpha, beta, A[: m * n], x, y)
+    scale = oracle.gemv(m, n, abs(alpha), abs(beta), np.abs(A[: m * n]), np.abs(x), np.abs(y))
+    yy = y.copy()
+    pb.dropin.gemv(m, n, alpha, beta, A[: m * n].copy(), x, yy)
+    if not normwise_err(yy, ref, scale) <= 1e-5:
+        fails.append(("gemv", m, n))
+    xt, yt = synth.f32(m * incx, 5), synth.f32(n * incy, 6)
+    ref = oracle.gemv_t(m, n, lda, incx, incy, alpha, beta, A, xt, yt)
+    scale = oracle.gemv_t(m, n, lda, incx, incy, abs(alpha), abs(beta), np.abs(A), np.abs(xt), np.abs(yt))
+    yy = yt.copy()
+    pb.dropin.gemv_t(m, n, lda, incx, incy, alpha, beta, A, xt, yy)
+    if not normwise_err(yy, ref, scale) <= 1e-5:
+        fails.append(("gemv_t", m, n, lda, incx, incy))
+    nd = int(rng.integers(1, 5_000_000))
+    xd, yd = synth.f32(nd, 7), synth.f32(nd, 8)
+    got, ref, sc = pb.dropin.dot(nd, xd, yd), oracle.dot(nd, xd, yd), oracle.dot(nd, np.abs(xd), np.abs(yd))
+    if not abs(got - ref) <= 1e-5 * sc:
+        fails.append(("dot", nd))
+    counts["blas"] = counts.get("blas", 0) + 1
+
+
 def gemm_case():
     m, n, k = (int(v) for v in rng.integers(1, 700, 3))
     A, B, C = synth.f32(m * k, 1), synth.f32(k * n, 2), synth.f32(m * n, 3)
@@ -142,5 +170,6 @@ while time.time() < t_end and not fails:
         axpy_case()
     else:
         gemm_case()
+        blas_case()
 print("cases", counts, "fails", fails[:5], flush=True)
 sys.exit(1 if fails else 0)
