@@ -70,7 +70,8 @@ constexpr int TMEM_COLS = 512;  // two 256-column fp32 accumulators
 constexpr int NUM_BARS = 3 * STAGES + 4;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + NUM_BARS * 8 + 16;
 #ifndef GEMM_GROUP_M_DEF
-#define GEMM_GROUP_M_DEF 8  // raster group in 256-row tiles (round 1 sweep 2/4/8/16: 8 best)
+#define GEMM_GROUP_M_DEF 8  // raster group in 256-row tiles (round 1 sweep 2/4/8/16: 8 best; round 2 re-check
+                            // on the fused kernel: 4 / 8 / 16 -> 33.7-34.4 / 33.2-33.4 / 33.4-33.5 ms at 16384^3)
 #endif
 constexpr int GROUP_M = GEMM_GROUP_M_DEF;
 
